@@ -1,0 +1,161 @@
+/*
+ * he_sm100.h -- C-ABI of the B200 (sm_100a) RNS-CKKS engine, libhe_sm100.so.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `hebatch` (/root/reference/pkg/src/hebatch).  The reference's boundary is
+ * the Python `VectorEngine` protocol (engine.py:164-177) whose only backend,
+ * `SimulatorEngine` (engine.py:229-420), does float64 slot arithmetic with
+ * numpy.  Each entry point below is what that protocol's operations bind to
+ * in the B200 build; the Python host layer (paper_2604_16834_b200/engine.py,
+ * `GpuEngine`) calls them through ctypes.  The reference interface each one
+ * replaces is cited beside it.
+ *
+ * Conventions
+ *   - Every function returns 0 on success or a negative HE_E* code; the
+ *     message for the last failure on the calling thread is he_last_error().
+ *     Validation happens before any device work is enqueued (the reference
+ *     raises before touching counters: engine.py:280-283, :300-303).
+ *   - A ciphertext is ONE device allocation laid out uint64 [n_comp][ell][N]
+ *     (n_comp = 2, or 3 after a tensor product), NTT domain, bit-reversed
+ *     evaluation order, every residue canonical in [0, q_i).  Limb i < ell
+ *     is modulo Q-prime i.
+ *   - Batched calls take HOST arrays of `count` device pointers (plain
+ *     uint64_t addresses); work is enqueued on `stream` (a cudaStream_t, NULL
+ *     = legacy default stream) and is asynchronous unless stated.
+ *   - No torch types cross this boundary.
+ */
+#ifndef HE_SM100_H
+#define HE_SM100_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HE_ABI_VERSION 1
+
+enum {
+    HE_OK = 0,
+    HE_EINVAL = -1,         /* bad argument (ShapeMismatch / ValueError)       */
+    HE_ECUDA = -2,          /* CUDA runtime failure                            */
+    HE_ENOKEY = -3,         /* MissingRotationKey (errors.py:12-17)            */
+    HE_ELEVEL = -4,         /* LevelExhausted (errors.py:24-25)                */
+    HE_ENOMEM = -5,         /* device allocation failed                        */
+    HE_ECONTEXT = -6,       /* ContextMismatch (errors.py:20-21)               */
+    HE_ELENGTH = -7,        /* LengthExceedsSlots (errors.py:8-9)              */
+};
+
+/* Parameter set.  Replaces EngineContext (engine.py:36-63): the reference's
+ * inert first_modulus_bits / rescale_bits / key_switch_digits become the
+ * live q_bits[0] / q_bits[1..] / alpha.  Same layout as oracle/ckks_oracle.h. */
+typedef struct {
+    int32_t log_n;
+    int32_t n_q;          /* L  = max_level + 1 Q-primes                  */
+    int32_t n_p;          /* K  special primes                             */
+    int32_t alpha;        /* limbs per key-switch digit, dnum=ceil(L/alpha) */
+    int32_t q_bits[48];
+    int32_t p_bits[16];
+    uint64_t seed;        /* Philox4x32-10 key for every random stream     */
+    double scale;         /* default encoding scale Delta                  */
+} he_params;
+
+typedef struct he_ctx he_ctx;
+
+const char *he_last_error(void);
+int he_abi_version(void);
+
+/* context: moduli, twiddle tables, BConv tables; secret key sampled from
+ * params.seed and kept on the device.  Replaces SimulatorEngine.__init__
+ * (engine.py:237-243). */
+int he_ctx_create(const he_params *p, int device, he_ctx **out);
+int he_ctx_destroy(he_ctx *ctx);
+int he_ctx_moduli(const he_ctx *ctx, uint64_t *moduli /* L+K */, uint64_t *psi /* L+K */);
+
+/* keys.  galois_elt 0 = relinearisation key (s^2); otherwise the key for
+ * X -> X^galois_elt.  Replaces register_rotation_keys / unload_rotation_keys
+ * (engine.py:343-354; RotationKeySet engine.py:93-136). */
+int he_gen_switch_key(he_ctx *ctx, uint32_t galois_elt, void *stream);
+int he_drop_switch_key(he_ctx *ctx, uint32_t galois_elt);
+int he_has_switch_key(const he_ctx *ctx, uint32_t galois_elt);
+/* copies (canonical form) for parity tests: sk [L+K][N]; key [dnum][2][L+K][N] */
+int he_export_secret_key(he_ctx *ctx, uint64_t *dev_out, void *stream);
+int he_export_switch_key(he_ctx *ctx, uint32_t galois_elt, uint64_t *dev_out, void *stream);
+
+/* batched NTT / INTT over data [batch][ell][N]; limb i uses Q-prime i. */
+int he_ntt(he_ctx *ctx, uint64_t *data, int batch, int ell, int inverse, void *stream);
+
+/* encode + encrypt.  vals: device float64 [count][nvals] (zero-padded to
+ * n = N/2 slots); ct k gets randomness index ct_index0 + k.  Output cts are
+ * at the top level (ell = L).  Replaces encrypt (engine.py:257-264) and the
+ * per-channel loop of pack_inputs (packing.py:119-123). */
+int he_encrypt(he_ctx *ctx, const double *vals, int count, int nvals, double scale,
+               uint32_t ct_index0, uint64_t *const *out, void *stream);
+/* decrypt + decode to device float64 [count][N/2].  scales: host [count].
+ * Replaces decrypt (engine.py:266-268) / unpack_outputs (packing.py:126-135). */
+int he_decrypt(he_ctx *ctx, const uint64_t *const *cts, int count, int ell, const double *scales,
+               double *slots_out, void *stream);
+/* decrypt to integer coefficients (as float64 [count][N]) -- parity tests */
+int he_decrypt_coeffs(he_ctx *ctx, const uint64_t *const *cts, int count, int ell, double *out,
+                      void *stream);
+/* encode a full-width plaintext at `scale` into NTT residues pt [ell][N]
+ * (PlainVec encoding inside mult_plain / add_plain, engine.py:291-304). */
+int he_encode_plain(he_ctx *ctx, const double *vals, int nvals, double scale, int ell,
+                    uint64_t *pt_out, void *stream);
+
+/* element-wise.  add/sub: engine.py:285-289.  add_const: add_plain with a
+ * constant over the occupied span (engine.py:291-295, conv.py:160-166);
+ * residues host [count][ell].  mul_const: scalar plaintext product
+ * (mult_plain before its rescale, engine.py:297-304); residues [count][ell]. */
+int he_add(he_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out,
+           int count, int ell, int n_comp, void *stream);
+int he_sub(he_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out,
+           int count, int ell, int n_comp, void *stream);
+int he_add_const(he_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int ell,
+                 const uint64_t *residues, void *stream);
+int he_mul_const(he_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int ell,
+                 int n_comp, const uint64_t *residues, void *stream);
+int he_mul_plain(he_ctx *ctx, const uint64_t *const *in, const uint64_t *pt, uint64_t *const *out,
+                 int count, int ell, int n_comp, void *stream);
+/* keep the first ell_out limbs of each component (level drop, no rescale) */
+int he_drop_limbs(he_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int ell_in,
+                  int ell_out, int n_comp, void *stream);
+
+/* ct x ct pieces.  tensor: (a0b0, a0b1+a1b0, a1b1) -> out [3][ell][N].
+ * relin: [3][ell][N] -> [2][ell][N] with the galois_elt-0 key.
+ * keyswitch: d [ell][N] -> (o0, o1) with key galois_elt (parity tests).
+ * rescale: [n_comp][ell][N] -> [n_comp][ell-1][N], divide-and-round by q_{ell-1}.
+ * mult_ct = tensor + relin + rescale (mult_ct, engine.py:306-313). */
+int he_tensor(he_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out,
+              int count, int ell, void *stream);
+int he_relin(he_ctx *ctx, const uint64_t *const *d3, uint64_t *const *out, int count, int ell,
+             void *stream);
+int he_keyswitch(he_ctx *ctx, uint32_t galois_elt, const uint64_t *const *d, uint64_t *const *out0,
+                 uint64_t *const *out1, int count, int ell, void *stream);
+int he_rescale(he_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int ell,
+               int n_comp, void *stream);
+int he_mult_ct(he_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out,
+               int count, int ell, void *stream);
+
+/* rotation: X -> X^galois_elt on both components, then key switch of the
+ * permuted c1 (rotate, engine.py:276-283; galois_elt = 5^k mod 2N). */
+int he_automorphism(he_ctx *ctx, uint32_t galois_elt, const uint64_t *const *in, uint64_t *const *out,
+                    int count, int ell, int n_comp, void *stream);
+int he_rotate(he_ctx *ctx, uint32_t galois_elt, const uint64_t *const *in, uint64_t *const *out,
+              int count, int ell, void *stream);
+
+/* feature-major linear layer (the batched form of conv_forward's k=1 path,
+ * conv.py:109-173, and of feature-major conv / pool):
+ *   out[o] = sum_{t in [row_ptr[o], row_ptr[o+1])} w[t] * in[col[t]]   mod q_i
+ * w: signed int64 (|w| < 2^62) shared by every limb; row_ptr/col/w are host
+ * arrays.  Output is NOT rescaled (call he_rescale; bias via he_add_const). */
+int he_lincomb(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
+               const int32_t *row_ptr, const int32_t *col, const int64_t *w, int ell, int n_comp,
+               void *stream);
+
+/* block until all work on `stream` is done; returns HE_ECUDA on async error */
+int he_sync(void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

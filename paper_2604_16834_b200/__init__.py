@@ -1,0 +1,22 @@
+"""B200-native batched RNS-CKKS engine for encrypted inference (arXiv 2604.16834).
+
+Drop-in for the hot path of the reference package ``hebatch``: the same
+``EngineContext`` / ``VectorEngine`` / ``pack_inputs`` / ``conv_forward`` /
+``unpack_outputs`` API, backed by hand-written sm_100a CUDA kernels in
+``libhe_sm100.so`` (C-ABI: include/he_sm100.h) instead of float64 slot
+simulation.  See DESIGN.md.
+"""
+
+from .errors import HebatchError  # noqa: F401
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # lazy: importing the package must not require torch / a GPU (CPU tests)
+    if name in ("EngineContext", "GpuEngine", "CipherVec", "PlainVec", "OpCounters", "RotationKeySet",
+                "VectorEngine"):
+        from . import engine
+
+        return getattr(engine, name)
+    raise AttributeError(name)

@@ -1,0 +1,185 @@
+// common.cuh -- shared host/device definitions for libhe_sm100.so.
+//
+// Modular arithmetic on 64-bit residues (q < 2^62):
+//   * Shoup products for constant multipliers (twiddles, q_l^-1, P^-1):
+//     one 64x64 high product + two low products, result in [0, 2q) (lazy).
+//   * Montgomery REDC for sums of products against stored constants whose
+//     table entries are pre-multiplied by R = 2^64 (BConv tables, key-switch
+//     keys, lincomb weights): accumulate exact 128-bit sums, reduce once.
+// Every kernel boundary leaves residues canonical in [0, q): that is the
+// bit-exact contract with oracle/ckks_oracle.c.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/he_sm100.h"
+
+#define HE_MAXM 64
+
+struct ModConst {
+    uint64_t q;
+    uint64_t qinv;      // q^-1 mod 2^64 (Montgomery)
+    uint64_t r2;        // 2^128 mod q  (redc(x * r2) = x * 2^64 mod q)
+    uint64_t ninv;      // N^-1 mod q
+    uint64_t ninv_sh;   // Shoup(ninv)
+    uint64_t pad[3];
+};
+
+// Per-(level, digit) ModUp table and per-level ModDown table, device resident.
+struct BconvTable {
+    int n_src, n_dst;
+    uint64_t *d;        // [n_src] qhat_inv, [n_src] Shoup(qhat_inv), [n_src][n_dst] qhat mod dst (Montgomery form)
+    int32_t *d_src_mod; // [n_src] modulus index of each source
+    int32_t *d_dst_mod; // [n_dst] modulus index of each target
+};
+
+struct he_ctx {
+    he_params prm;
+    int N, logN, L, K, alpha, dnum, nslots, device;
+    std::vector<uint64_t> mod, psi;
+    ModConst *d_mc = nullptr;        // [L+K]
+    uint64_t *d_tw = nullptr;        // [L+K][4][N]  psi_brv, shoup, ipsi_brv, shoup
+    uint64_t *d_sk = nullptr;        // [L+K][N]     canonical, NTT domain
+    double *d_fftw = nullptr;        // [nslots][2]  omega^k
+    double *d_twist = nullptr;       // [nslots][2]  zeta^j
+    int32_t *d_slot_brv = nullptr;   // [nslots]     brv(pos[i]): slot i <-> FFT input index
+    uint8_t *d_ident = nullptr;      // [HE_MAXM]    identity modulus map
+    std::map<uint32_t, uint64_t *> keys;            // [dnum][2][L+K][N] Montgomery form
+    std::map<uint64_t, BconvTable> modup_tab;       // key = ell*64 + digit
+    std::map<int, BconvTable> moddown_tab;          // key = ell
+    std::vector<uint64_t> h_pmodq, h_pinv;          // P mod q_i, P^-1 mod q_i (i < L)
+    uint64_t *d_pinv = nullptr;                     // [L] P^-1 mod q_i and Shoup  ([L][2])
+    uint64_t *d_qlinv = nullptr;                    // [L][L][2] q_l^-1 mod q_i, Shoup
+    std::mutex mu;
+};
+
+// ---------------------------------------------------------------- errors
+
+void he_set_error(const char *fmt, ...);
+#define HE_CHECK_CUDA(call)                                                            \
+    do {                                                                               \
+        cudaError_t _e = (call);                                                       \
+        if (_e != cudaSuccess) {                                                       \
+            he_set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e)); \
+            return HE_ECUDA;                                                           \
+        }                                                                              \
+    } while (0)
+#define HE_CHECK_LAUNCH() HE_CHECK_CUDA(cudaGetLastError())
+#define HE_TRY(x)                     \
+    do {                              \
+        int _r = (x);                 \
+        if (_r != HE_OK) return _r;   \
+    } while (0)
+
+// ---------------------------------------------------------------- device math
+
+__device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+// Shoup: w * a mod q with wp = floor(w 2^64 / q); lazy result in [0, 2q)
+__device__ __forceinline__ uint64_t shoup_lazy(uint64_t a, uint64_t w, uint64_t wp, uint64_t q) {
+    return a * w - mulhi(a, wp) * q;
+}
+__device__ __forceinline__ uint64_t shoup(uint64_t a, uint64_t w, uint64_t wp, uint64_t q) {
+    uint64_t r = shoup_lazy(a, w, wp, q);
+    return r >= q ? r - q : r;
+}
+__device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) {
+    uint64_t s = a + b;
+    return s >= q ? s - q : s;
+}
+__device__ __forceinline__ uint64_t sub_mod(uint64_t a, uint64_t b, uint64_t q) {
+    return a >= b ? a - b : a + q - b;
+}
+
+struct u128 {
+    uint64_t lo, hi;
+};
+// acc += a * b  (exact 128-bit)
+__device__ __forceinline__ void mac128(u128 &acc, uint64_t a, uint64_t b) {
+    asm("mad.lo.cc.u64 %0, %2, %3, %0;\n\t"
+        "madc.hi.u64 %1, %2, %3, %1;"
+        : "+l"(acc.lo), "+l"(acc.hi)
+        : "l"(a), "l"(b));
+}
+// Montgomery reduction of T = hi 2^64 + lo < q 2^64: returns T 2^-64 mod q in [0, q)
+__device__ __forceinline__ uint64_t redc(uint64_t hi, uint64_t lo, uint64_t q, uint64_t qinv) {
+    uint64_t m = lo * qinv;
+    uint64_t mh = mulhi(m, q);
+    uint64_t t = hi - mh;
+    return hi < mh ? t + q : t;
+}
+// exact a * b mod q for canonical a, b: two Montgomery reductions
+__device__ __forceinline__ uint64_t mul_mod(uint64_t a, uint64_t b, const ModConst &mc) {
+    uint64_t t = redc(mulhi(a, b), a * b, mc.q, mc.qinv);  // a b R^-1
+    return redc(mulhi(t, mc.r2), t * mc.r2, mc.q, mc.qinv);  // (a b R^-1)(R^2) R^-1
+}
+// signed int64 -> canonical residue
+__device__ __forceinline__ uint64_t smod64(int64_t v, uint64_t q) {
+    if (v >= 0) return (uint64_t)v % q;
+    uint64_t r = ((uint64_t)(-(v + 1))) % q;
+    return q - 1 - r;
+}
+
+// ---------------------------------------------------------------- philox
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+        uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = lo1;
+        c[2] = n2;
+        c[3] = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+enum { DOM_SK = 1, DOM_ENC_A = 2, DOM_ENC_E = 3, DOM_KSK_A = 4, DOM_KSK_E = 5 };
+__device__ __forceinline__ void rnd4(uint64_t seed, uint32_t dom, uint32_t obj, uint32_t limb, uint32_t idx,
+                                     uint32_t o[4]) {
+    o[0] = idx;
+    o[1] = limb;
+    o[2] = obj;
+    o[3] = dom;
+    philox4x32_10(o, (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+__device__ __forceinline__ int64_t sample_cbd(uint64_t seed, uint32_t dom, uint32_t obj, uint32_t j) {
+    uint32_t r[4];
+    rnd4(seed, dom, obj, 0, j, r);
+    return (int64_t)__popc(r[0] & 0x1FFFFFu) - (int64_t)__popc(r[1] & 0x1FFFFFu);
+}
+__device__ __forceinline__ uint64_t sample_uniform(uint64_t seed, uint32_t dom, uint32_t obj, uint32_t limb,
+                                                   uint32_t j, uint64_t q) {
+    uint32_t r[4];
+    rnd4(seed, dom, obj, limb, j, r);
+    uint64_t lo = (uint64_t)r[0] | ((uint64_t)r[1] << 32);
+    uint64_t hi = (uint64_t)r[2] | ((uint64_t)r[3] << 32);
+    uint64_t ph_lo = hi * q, ph_hi = mulhi(hi, q);
+    uint64_t pl_hi = mulhi(lo, q);
+    uint64_t mid = ph_lo + pl_hi;
+    return ph_hi + (mid < ph_lo ? 1 : 0);
+}
+
+// ---------------------------------------------------------------- host helpers (defined in context.cu)
+int he_upload_ptrs(const void *const *host_ptrs, int count, void ***dev_out, cudaStream_t s);
+int he_scratch_alloc(void **p, size_t bytes, cudaStream_t s);
+void he_scratch_free(void *p, cudaStream_t s);
+int he_get_modup_table(he_ctx *ctx, int ell, int digit, const BconvTable **out);
+int he_get_moddown_table(he_ctx *ctx, int ell, const BconvTable **out);
+const uint64_t *he_get_key(he_ctx *ctx, uint32_t galois_elt);
+
+// NTT launchers (ntt.cu).  Polys: data + p*N for p in [0, n_polys); the
+// modulus of poly p is mod_map[p % per] (0xFF: skip the poly).
+int he_ntt_fwd(he_ctx *ctx, uint64_t *data, int n_polys, const uint8_t *mod_map, int per, cudaStream_t s);
+int he_ntt_inv(he_ctx *ctx, uint64_t *data, int n_polys, const uint8_t *mod_map, int per, cudaStream_t s);
+// pointer-array form: poly p = ptrs[p / per] + (p % per) * N (ptrs in device memory)
+int he_ntt_fwd_ptrs(he_ctx *ctx, uint64_t *const *ptrs, int count, int per, const uint8_t *mod_map, cudaStream_t s);
+int he_ntt_inv_ptrs(he_ctx *ctx, uint64_t *const *ptrs, int count, int per, const uint8_t *mod_map, cudaStream_t s);
+
+static inline unsigned ceil_div(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }

@@ -1,0 +1,366 @@
+// ntt.cu -- batched negacyclic NTT / INTT for sm_100a.
+//
+// Contract: forward is Cooley-Tukey, natural order in,
+// bit-reversed order out, out[k] = a(psi^(2 brv(k) + 1)); inverse is
+// Gentleman-Sande, bit-reversed in, natural out, scaled by N^-1.  Outputs are
+// canonical, so the result is the unique NTT and bit-exact with any other
+// correct implementation (oracle/ckks_oracle.c oc_ntt / oc_intt).
+//
+// Structure: every thread keeps 16 residues in registers and runs radix-16
+// "phases" of 4 butterfly stages; phases exchange data through shared memory.
+//   N = 2^16: two kernels (two HBM round trips), 4096 residues per CTA:
+//     pass "cols": stages 0..7 on 16 columns x 256 rows (stride-256 column
+//     sub-transforms), pass "rows": stages 8..15 on 16 contiguous rows of 256.
+//   N = 2^12: one kernel, one CTA per limb-polynomial, three phases.
+// Butterflies use Harvey's lazy reduction (values in [0, 4q) forward,
+// [0, 2q) inverse) with Shoup twiddles read through the read-only cache.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int TPB = 256;  // threads per CTA, 16 residues each = 4096 per CTA
+
+__device__ __forceinline__ uint64_t reduce4q(uint64_t x, uint64_t q) {
+    uint64_t q2 = 2 * q;
+    x = x >= q2 ? x - q2 : x;
+    return x >= q ? x - q : x;
+}
+
+// Four CT stages lm = LM0..LM0+3 on x[j] with global index e0 + j*estride.
+template <int LOGN, int LM0>
+__device__ __forceinline__ void phase_ct(uint64_t (&x)[16], uint32_t e0, uint32_t estride, const uint64_t *__restrict__ W,
+                                         const uint64_t *__restrict__ Wp, uint64_t q) {
+    const uint64_t q2 = 2 * q;
+#pragma unroll
+    for (int s = 0; s < 4; s++) {
+        const int lm = LM0 + s;
+        const int d = 8 >> s;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            if (j & d) continue;
+            uint32_t e = e0 + (uint32_t)j * estride;
+            uint32_t idx = (1u << lm) + (e >> (LOGN - lm));
+            uint64_t w = __ldg(W + idx), wp = __ldg(Wp + idx);
+            uint64_t u = x[j];
+            u = u >= q2 ? u - q2 : u;
+            uint64_t v = shoup_lazy(x[j + d], w, wp, q);
+            x[j] = u + v;
+            x[j + d] = u - v + q2;
+        }
+    }
+}
+
+// Four GS stages lt = LT0..LT0+3 (element distance 2^lt).
+template <int LOGN, int LT0>
+__device__ __forceinline__ void phase_gs(uint64_t (&x)[16], uint32_t e0, uint32_t estride, const uint64_t *__restrict__ W,
+                                         const uint64_t *__restrict__ Wp, uint64_t q) {
+    const uint64_t q2 = 2 * q;
+#pragma unroll
+    for (int s = 0; s < 4; s++) {
+        const int lt = LT0 + s;
+        const int d = 1 << s;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            if (j & d) continue;
+            uint32_t e = e0 + (uint32_t)j * estride;
+            uint32_t idx = (1u << (LOGN - 1 - lt)) + (e >> (lt + 1));
+            uint64_t w = __ldg(W + idx), wp = __ldg(Wp + idx);
+            uint64_t u = x[j], v = x[j + d];
+            uint64_t sm = u + v;
+            sm = sm >= q2 ? sm - q2 : sm;
+            x[j] = sm;
+            x[j + d] = shoup_lazy(u - v + q2, w, wp, q);
+        }
+    }
+}
+
+__device__ __forceinline__ int pad16(int e) { return e + (e >> 4); }
+
+struct PolyInfo {
+    uint64_t *p;
+    const uint64_t *W, *Wp;
+    uint64_t q;
+    const ModConst *mc;
+};
+
+// Polys live either contiguously (data + poly*N) or, when ptrs != nullptr, in
+// per-ciphertext allocations: poly p = ptrs[p / per] + (p % per) * N.
+struct PolySrc {
+    uint64_t *data;
+    uint64_t *const *ptrs;
+};
+
+__device__ __forceinline__ bool poly_info(PolyInfo &pi, PolySrc src, size_t poly, const uint8_t *mod_map, int per,
+                                          const uint64_t *tw, const ModConst *mc, int logN, bool inverse) {
+    int m = mod_map[poly % per];
+    if (m == 0xFF) return false;
+    size_t N = (size_t)1 << logN;
+    pi.p = src.ptrs ? src.ptrs[poly / per] + (poly % per) * N : src.data + poly * N;
+    pi.W = tw + (size_t)m * 4 * N + (inverse ? 2 * N : 0);
+    pi.Wp = pi.W + N;
+    pi.q = mc[m].q;
+    pi.mc = mc + m;
+    return true;
+}
+
+// ---------------------------------------------------------------- N = 2^16
+// pass 1 forward: 16 columns x 256 rows, stages 0..7
+__global__ void __launch_bounds__(TPB) k_fwd16_cols(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw,
+                                                    const ModConst *mc) {
+    __shared__ uint64_t sm[256 * 16];
+    PolyInfo pi;
+    if (!poly_info(pi, data, blockIdx.x >> 4, mod_map, per, tw, mc, 16, false)) return;
+    const int tid = threadIdx.x, lc = tid & 15, g = tid >> 4;
+    const uint32_t col = (blockIdx.x & 15) * 16 + lc;
+    uint64_t x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = pi.p[(g + 16 * j) * 256 + col];
+    phase_ct<16, 0>(x, col + 256 * g, 4096, pi.W, pi.Wp, pi.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[(g + 16 * j) * 16 + lc] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[(16 * g + j) * 16 + lc];
+    phase_ct<16, 4>(x, col + 4096 * g, 256, pi.W, pi.Wp, pi.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) pi.p[(16 * g + j) * 256 + col] = x[j];  // lazy [0,4q) between passes
+}
+
+// pass 2 forward: 16 rows of 256, stages 8..15, canonical output
+__global__ void __launch_bounds__(TPB) k_fwd16_rows(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw,
+                                                    const ModConst *mc) {
+    __shared__ uint64_t sm[16 * 272];
+    PolyInfo pi;
+    if (!poly_info(pi, data, blockIdx.x >> 4, mod_map, per, tw, mc, 16, false)) return;
+    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+    const uint32_t r = (blockIdx.x & 15) * 16 + rl;
+    uint64_t *row = pi.p + r * 256;
+    uint64_t x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
+    phase_ct<16, 8>(x, r * 256 + g, 16, pi.W, pi.Wp, pi.q);
+    uint64_t *s = sm + rl * 272;
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
+    phase_ct<16, 12>(x, r * 256 + 16 * g, 1, pi.W, pi.Wp, pi.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], pi.q);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) row[g + 16 * j] = s[pad16(g + 16 * j)];
+}
+
+// pass 1 inverse: 16 rows of 256, GS stages 0..7
+__global__ void __launch_bounds__(TPB) k_inv16_rows(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw,
+                                                    const ModConst *mc) {
+    __shared__ uint64_t sm[16 * 272];
+    PolyInfo pi;
+    if (!poly_info(pi, data, blockIdx.x >> 4, mod_map, per, tw, mc, 16, true)) return;
+    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+    const uint32_t r = (blockIdx.x & 15) * 16 + rl;
+    uint64_t *row = pi.p + r * 256;
+    uint64_t *s = sm + rl * 272;
+    uint64_t x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = row[g + 16 * j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
+    phase_gs<16, 0>(x, r * 256 + 16 * g, 1, pi.W, pi.Wp, pi.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
+    phase_gs<16, 4>(x, r * 256 + g, 16, pi.W, pi.Wp, pi.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) row[g + 16 * j] = x[j];  // lazy [0,2q)
+}
+
+// pass 2 inverse: 16 columns x 256 rows, GS stages 8..15, times N^-1, canonical
+__global__ void __launch_bounds__(TPB) k_inv16_cols(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw,
+                                                    const ModConst *mc) {
+    __shared__ uint64_t sm[256 * 16];
+    PolyInfo pi;
+    if (!poly_info(pi, data, blockIdx.x >> 4, mod_map, per, tw, mc, 16, true)) return;
+    const int tid = threadIdx.x, lc = tid & 15, g = tid >> 4;
+    const uint32_t col = (blockIdx.x & 15) * 16 + lc;
+    uint64_t x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = pi.p[(16 * g + j) * 256 + col];
+    phase_gs<16, 8>(x, col + 4096 * g, 256, pi.W, pi.Wp, pi.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[(16 * g + j) * 16 + lc] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[(g + 16 * j) * 16 + lc];
+    phase_gs<16, 12>(x, col + 256 * g, 4096, pi.W, pi.Wp, pi.q);
+    const uint64_t ni = pi.mc->ninv, nip = pi.mc->ninv_sh;
+#pragma unroll
+    for (int j = 0; j < 16; j++) pi.p[(g + 16 * j) * 256 + col] = shoup(x[j], ni, nip, pi.q);
+}
+
+// ---------------------------------------------------------------- N = 2^12, one CTA per poly
+__global__ void __launch_bounds__(TPB) k_fwd12(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw,
+                                               const ModConst *mc) {
+    __shared__ uint64_t sm[4096 + 256];
+    PolyInfo pi;
+    if (!poly_info(pi, data, blockIdx.x, mod_map, per, tw, mc, 12, false)) return;
+    const int g = threadIdx.x;
+    uint64_t x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = pi.p[g + 256 * j];
+    phase_ct<12, 0>(x, g, 256, pi.W, pi.Wp, pi.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[pad16(g + 256 * j)] = x[j];
+    __syncthreads();
+    const uint32_t e1 = (g & 15) + 256 * (g >> 4);
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[pad16(e1 + 16 * j)];
+    phase_ct<12, 4>(x, e1, 16, pi.W, pi.Wp, pi.q);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[pad16(e1 + 16 * j)] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[pad16(16 * g + j)];
+    phase_ct<12, 8>(x, 16 * g, 1, pi.W, pi.Wp, pi.q);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[pad16(16 * g + j)] = reduce4q(x[j], pi.q);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) pi.p[g + 256 * j] = sm[pad16(g + 256 * j)];
+}
+
+__global__ void __launch_bounds__(TPB) k_inv12(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw,
+                                               const ModConst *mc) {
+    __shared__ uint64_t sm[4096 + 256];
+    PolyInfo pi;
+    if (!poly_info(pi, data, blockIdx.x, mod_map, per, tw, mc, 12, true)) return;
+    const int g = threadIdx.x;
+    uint64_t x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[pad16(g + 256 * j)] = pi.p[g + 256 * j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[pad16(16 * g + j)];
+    phase_gs<12, 0>(x, 16 * g, 1, pi.W, pi.Wp, pi.q);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[pad16(16 * g + j)] = x[j];
+    __syncthreads();
+    const uint32_t e1 = (g & 15) + 256 * (g >> 4);
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[pad16(e1 + 16 * j)];
+    phase_gs<12, 4>(x, e1, 16, pi.W, pi.Wp, pi.q);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[pad16(e1 + 16 * j)] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[pad16(g + 256 * j)];
+    phase_gs<12, 8>(x, g, 256, pi.W, pi.Wp, pi.q);
+    const uint64_t ni = pi.mc->ninv, nip = pi.mc->ninv_sh;
+#pragma unroll
+    for (int j = 0; j < 16; j++) pi.p[g + 256 * j] = shoup(x[j], ni, nip, pi.q);
+}
+
+// ---------------------------------------------------------------- generic N <= 2^14
+// One CTA per polynomial, radix-2 stages in shared memory.  Used for the small
+// rings of the API-level tests (SPEC.md examples at n = 4 ... 8192 slots).
+__global__ void k_ntt_generic(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw, const ModConst *mc,
+                              int logN, int inverse) {
+    extern __shared__ uint64_t sg[];
+    PolyInfo pi;
+    if (!poly_info(pi, data, blockIdx.x, mod_map, per, tw, mc, logN, inverse)) return;
+    const int N = 1 << logN, half = N >> 1;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sg[i] = pi.p[i];
+    __syncthreads();
+    const uint64_t q = pi.q;
+    if (!inverse) {
+        for (int lm = 0; lm < logN; lm++) {
+            int t = half >> lm;
+            for (int b = threadIdx.x; b < half; b += blockDim.x) {
+                int i = b / t, j = 2 * i * t + (b % t);
+                uint64_t w = pi.W[(1 << lm) + i], wp = pi.Wp[(1 << lm) + i];
+                uint64_t u = sg[j], v = shoup(sg[j + t], w, wp, q);
+                sg[j] = add_mod(u, v, q);
+                sg[j + t] = sub_mod(u, v, q);
+            }
+            __syncthreads();
+        }
+    } else {
+        for (int lt = 0; lt < logN; lt++) {
+            int t = 1 << lt;
+            for (int b = threadIdx.x; b < half; b += blockDim.x) {
+                int i = b / t, j = 2 * i * t + (b % t);
+                int idx = (N >> (lt + 1)) + i;
+                uint64_t u = sg[j], v = sg[j + t];
+                sg[j] = add_mod(u, v, q);
+                sg[j + t] = shoup(sub_mod(u, v, q), pi.W[idx], pi.Wp[idx], q);
+            }
+            __syncthreads();
+        }
+        for (int i = threadIdx.x; i < N; i += blockDim.x) sg[i] = shoup(sg[i], pi.mc->ninv, pi.mc->ninv_sh, q);
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) pi.p[i] = sg[i];
+}
+
+}  // namespace
+
+static int ntt_launch(he_ctx *c, PolySrc src, int n_polys, const uint8_t *mod_map, int per, bool inv, cudaStream_t s) {
+    if (n_polys <= 0) return HE_OK;
+    if (c->logN == 16) {
+        unsigned g = (unsigned)n_polys * 16;
+        if (!inv) {
+            k_fwd16_cols<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
+            k_fwd16_rows<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
+        } else {
+            k_inv16_rows<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
+            k_inv16_cols<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
+        }
+    } else if (c->logN == 12) {
+        if (!inv)
+            k_fwd12<<<(unsigned)n_polys, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
+        else
+            k_inv12<<<(unsigned)n_polys, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
+    } else {
+        int N = c->N, threads = std::min(std::max(N / 2, 32), 512);
+        size_t smem = (size_t)N * 8;
+        if (smem > 48 * 1024)
+            HE_CHECK_CUDA(cudaFuncSetAttribute(k_ntt_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_ntt_generic<<<(unsigned)n_polys, threads, smem, s>>>(src, mod_map, per, c->d_tw, c->d_mc, c->logN, inv);
+    }
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+int he_ntt_fwd(he_ctx *c, uint64_t *data, int n_polys, const uint8_t *mod_map, int per, cudaStream_t s) {
+    return ntt_launch(c, PolySrc{data, nullptr}, n_polys, mod_map, per, false, s);
+}
+int he_ntt_inv(he_ctx *c, uint64_t *data, int n_polys, const uint8_t *mod_map, int per, cudaStream_t s) {
+    return ntt_launch(c, PolySrc{data, nullptr}, n_polys, mod_map, per, true, s);
+}
+int he_ntt_fwd_ptrs(he_ctx *c, uint64_t *const *ptrs, int count, int per, const uint8_t *mod_map, cudaStream_t s) {
+    return ntt_launch(c, PolySrc{nullptr, ptrs}, count * per, mod_map, per, false, s);
+}
+int he_ntt_inv_ptrs(he_ctx *c, uint64_t *const *ptrs, int count, int per, const uint8_t *mod_map, cudaStream_t s) {
+    return ntt_launch(c, PolySrc{nullptr, ptrs}, count * per, mod_map, per, true, s);
+}
+
+extern "C" int he_ntt(he_ctx *c, uint64_t *data, int batch, int ell, int inverse, void *stream) {
+    if (!c || !data || batch < 0 || ell < 1 || ell > c->L) {
+        he_set_error("he_ntt: bad arguments (batch=%d ell=%d)", batch, ell);
+        return HE_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    return inverse ? he_ntt_inv(c, data, batch * ell, c->d_ident, ell, s)
+                   : he_ntt_fwd(c, data, batch * ell, c->d_ident, ell, s);
+}

@@ -1,0 +1,803 @@
+"""B200 RNS-CKKS engine behind the reference's VectorEngine protocol.
+
+Drop-in for ``hebatch.engine`` (reference /root/reference/pkg/src/hebatch/
+engine.py).  ``EngineContext``, ``CipherVec``, ``PlainVec``,
+``RotationKeySet``, ``OpCounters`` and the ``VectorEngine`` protocol keep the
+reference's names, fields and semantics; ``GpuEngine`` replaces
+``SimulatorEngine`` (engine.py:229-420): the float64 slot arithmetic becomes
+real RNS-CKKS executed by the sm_100a kernels of libhe_sm100.so.
+
+Semantics preserved from the reference (and tested):
+  * rotate(ct, k): output slot i holds input slot i+k (engine.py:13-15);
+    k = 0 mod n returns the same handle uncounted (engine.py:278-279); a
+    missing key raises MissingRotationKey(k) before anything is counted.
+  * every mult_plain / mult_ct costs ``mult_level_cost`` levels and raises
+    LevelExhausted when the level would go negative (engine.py:297-313);
+    add/mult_ct results sit at the lower operand level (engine.py:289).
+  * counters, live-handle tracking, window peaks and double-release errors
+    behave as in _Accounting (engine.py:180-227).
+A ciphertext at ``level`` has ``level + 1`` Q-limbs; a fresh one is at
+``max_level``.  There is no CPU fallback: without the CUDA library or a GPU
+the engine raises.
+"""
+
+from __future__ import annotations
+
+import itertools
+import math
+import threading
+from dataclasses import dataclass, field
+from typing import Iterable, Protocol, Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import (
+    ContextMismatch,
+    HebatchError,
+    LengthExceedsSlots,
+    LevelExhausted,
+    MissingRotationKey,
+    ScaleMismatch,
+)
+
+# relative scale difference tolerated by add() (error contribution <= 2^-20 * |x|)
+SCALE_RTOL = 2.0 ** -20
+
+
+@dataclass(frozen=True)
+class EngineContext:
+    """CKKS parameter set (reference EngineContext, engine.py:36-63).
+
+    The reference carries ``first_modulus_bits``, ``rescale_bits`` and
+    ``key_switch_digits`` "for configuration fidelity only"; here they are
+    live: q_0 has ``first_modulus_bits`` bits, q_1..q_max_level have
+    ``rescale_bits`` bits, and key switching uses ``key_switch_digits`` digits
+    (alpha = ceil((max_level+1)/digits) limbs each).  Additions:
+    ``special_prime_bits`` (default: alpha primes of first_modulus_bits bits),
+    ``scale_bits`` (encoding scale, default rescale_bits), ``q_bits`` (explicit
+    Q chain override) and ``device``.  ``noise_sigma`` is the simulator's
+    slot perturbation and has no meaning for real encryption (ignored).
+    """
+
+    n: int
+    max_level: int = 25
+    mult_level_cost: int = 1
+    noise_sigma: float = 0.0
+    bootstrap_reserve: int = 10
+    first_modulus_bits: int = 50
+    rescale_bits: int = 46
+    key_switch_digits: int = 4
+    noise_seed: int = 0
+    special_prime_bits: tuple = ()
+    scale_bits: int | None = None
+    q_bits: tuple | None = None
+    device: int = 0
+
+    def __post_init__(self) -> None:
+        if self.n < 1 or (self.n & (self.n - 1)) != 0:
+            raise ValueError(f"slot count must be a power of two, got {self.n}")
+        if not (0 < self.bootstrap_reserve < self.max_level):
+            raise ValueError("bootstrap_reserve must lie in (0, max_level)")
+        if self.mult_level_cost < 1:
+            raise ValueError("mult_level_cost must be >= 1")
+        if self.noise_sigma < 0:
+            raise ValueError("noise_sigma must be nonnegative")
+        if self.key_switch_digits < 1:
+            raise ValueError("key_switch_digits must be >= 1")
+        if self.q_bits is not None and len(self.q_bits) != self.max_level + 1:
+            raise ValueError("q_bits must list max_level + 1 prime sizes")
+
+    # -- derived RNS parameters
+    @property
+    def ring_degree(self) -> int:
+        return 2 * self.n
+
+    @property
+    def log_n(self) -> int:
+        return int(math.log2(self.ring_degree))
+
+    @property
+    def n_q(self) -> int:
+        return self.max_level + 1
+
+    @property
+    def alpha(self) -> int:
+        return -(-self.n_q // self.key_switch_digits)
+
+    @property
+    def q_chain_bits(self) -> tuple:
+        if self.q_bits is not None:
+            return tuple(self.q_bits)
+        return (self.first_modulus_bits,) + (self.rescale_bits,) * self.max_level
+
+    @property
+    def p_chain_bits(self) -> tuple:
+        if self.special_prime_bits:
+            return tuple(self.special_prime_bits)
+        return (self.first_modulus_bits,) * self.alpha
+
+    @property
+    def scale(self) -> float:
+        return 2.0 ** (self.scale_bits if self.scale_bits is not None else self.rescale_bits)
+
+    def he_params(self) -> "_lib.HeParams":
+        p = _lib.HeParams()
+        p.log_n = self.log_n
+        qb, pb = self.q_chain_bits, self.p_chain_bits
+        p.n_q, p.n_p, p.alpha = len(qb), len(pb), self.alpha
+        for i, b in enumerate(qb):
+            p.q_bits[i] = b
+        for i, b in enumerate(pb):
+            p.p_bits[i] = b
+        p.seed = self.noise_seed & 0xFFFFFFFFFFFFFFFF
+        p.scale = self.scale
+        return p
+
+
+@dataclass(frozen=True, eq=False)
+class CipherVec:
+    """Handle to one device-resident RNS-CKKS ciphertext.
+
+    ``data`` is a torch int64 tensor [n_comp][level+1][N] (NTT domain, the
+    uint64 residues reinterpreted); ``scale`` is the exact CKKS scale;
+    ``scale_bits`` its rounded log2 (reference field, engine.py:66-80).
+    Immutable: every engine operation returns a fresh handle.
+    """
+
+    data: object
+    level: int
+    scale_bits: int
+    id: int
+    scale: float = 1.0
+    n_slots: int = 0
+    owner: int = 0
+
+    def __len__(self) -> int:
+        return self.n_slots
+
+    @property
+    def limbs(self) -> int:
+        return self.level + 1
+
+    @property
+    def ptr(self) -> int:
+        if self.data is None:
+            raise HebatchError(f"ciphertext {self.id} was released")
+        return self.data.data_ptr()
+
+
+@dataclass(frozen=True)
+class PlainVec:
+    """A plaintext slot vector, full slot width (engine.py:83-90).
+
+    Host data: encoding happens inside mult_plain / add_plain, at the scale
+    the operation needs.  A vector whose slots are all equal takes the scalar
+    fast path (a constant polynomial: the same residue at every NTT point).
+    """
+
+    slots: np.ndarray
+
+    def __len__(self) -> int:
+        return self.slots.shape[0]
+
+
+class RotationKeySet:
+    """Resident rotation offsets, canonical mod n (engine.py:93-136).
+
+    Offset 0 is never stored; ``generation_count`` counts every key ever
+    registered.  The key material itself lives on the device (he_ctx).
+    """
+
+    def __init__(self, n: int):
+        self._n = n
+        self._offsets: set[int] = set()
+        self.generation_count = 0
+
+    def canonical(self, offset: int) -> int:
+        return offset % self._n
+
+    def register(self, offsets: Iterable[int]) -> list[int]:
+        """Add keys; returns the newly resident canonical offsets."""
+        new = []
+        for off in offsets:
+            c = self.canonical(off)
+            if c and c not in self._offsets:
+                self._offsets.add(c)
+                new.append(c)
+        self.generation_count += len(new)
+        return new
+
+    def unload(self, offsets: Iterable[int]) -> list[int]:
+        gone = []
+        for off in offsets:
+            c = self.canonical(off)
+            if c in self._offsets:
+                self._offsets.discard(c)
+                gone.append(c)
+        return gone
+
+    def unload_all(self) -> list[int]:
+        gone = sorted(self._offsets)
+        self._offsets.clear()
+        return gone
+
+    def holds(self, offset: int) -> bool:
+        return self.canonical(offset) in self._offsets
+
+    @property
+    def resident(self) -> frozenset:
+        return frozenset(self._offsets)
+
+    def __len__(self) -> int:
+        return len(self._offsets)
+
+
+@dataclass(frozen=True)
+class OpCounters:
+    """Cumulative operation counts plus the live-ciphertext peak."""
+
+    rotations: int = 0
+    plain_mults: int = 0
+    ct_mults: int = 0
+    adds: int = 0
+    bootstraps: int = 0
+    key_loads: int = 0
+    peak_live_ciphertexts: int = 0
+
+    def delta(self, earlier: "OpCounters") -> "OpCounters":
+        """Difference since ``earlier``; the peak is reported as-is."""
+        return OpCounters(
+            rotations=self.rotations - earlier.rotations,
+            plain_mults=self.plain_mults - earlier.plain_mults,
+            ct_mults=self.ct_mults - earlier.ct_mults,
+            adds=self.adds - earlier.adds,
+            bootstraps=self.bootstraps - earlier.bootstraps,
+            key_loads=self.key_loads - earlier.key_loads,
+            peak_live_ciphertexts=self.peak_live_ciphertexts,
+        )
+
+
+class VectorEngine(Protocol):
+    """Operation surface every backend provides (engine.py:164-177)."""
+
+    context: EngineContext
+
+    def encrypt(self, values) -> CipherVec: ...
+    def decrypt(self, ct: CipherVec) -> np.ndarray: ...
+    def rotate(self, ct: CipherVec, k: int) -> CipherVec: ...
+    def add(self, a: CipherVec, b: CipherVec) -> CipherVec: ...
+    def add_plain(self, a: CipherVec, p: PlainVec) -> CipherVec: ...
+    def mult_plain(self, ct: CipherVec, p: PlainVec) -> CipherVec: ...
+    def mult_ct(self, a: CipherVec, b: CipherVec) -> CipherVec: ...
+    def bootstrap(self, ct: CipherVec) -> CipherVec: ...
+    def release(self, *cts: CipherVec) -> None: ...
+
+
+class _Ledger:
+    """Lock-protected counters and live-handle set (engine.py:180-227)."""
+
+    _FIELDS = ("rotations", "plain_mults", "ct_mults", "adds", "bootstraps", "key_loads")
+
+    def __init__(self) -> None:
+        self.lock = threading.Lock()
+        self.counts = dict.fromkeys(self._FIELDS, 0)
+        self.live: set[int] = set()
+        self.peak = 0
+        self.window_peak = 0
+
+    def bump(self, name: str, by: int = 1) -> None:
+        with self.lock:
+            self.counts[name] += by
+
+    def track(self, ids: Sequence[int]) -> None:
+        with self.lock:
+            self.live.update(ids)
+            k = len(self.live)
+            self.peak = max(self.peak, k)
+            self.window_peak = max(self.window_peak, k)
+
+    def drop(self, handle: int) -> None:
+        with self.lock:
+            if handle not in self.live:
+                raise HebatchError(f"release of unknown or already-released handle {handle}")
+            self.live.discard(handle)
+
+    def snapshot(self) -> OpCounters:
+        with self.lock:
+            return OpCounters(peak_live_ciphertexts=self.peak, **self.counts)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class GpuEngine:
+    """RNS-CKKS on one B200: the sm_100a replacement of SimulatorEngine.
+
+    Per-ciphertext protocol methods (encrypt, add, mult_plain, ...) each launch
+    a handful of kernels; the ``*_batch`` methods and ``lincomb`` are the
+    batched hot path used by the layer calls (conv_forward, fm_* in
+    featuremajor.py): one launch sequence for a whole layer.
+    """
+
+    def __init__(self, context: EngineContext):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise HebatchError("GpuEngine needs a CUDA device (sm_100a); there is no CPU fallback")
+        if context.mult_level_cost != 1:
+            raise HebatchError("GpuEngine implements mult_level_cost == 1 (one rescale per multiplication)")
+        self.context = context
+        self.device = torch.device("cuda", context.device)
+        self._L = _lib.load()
+        import ctypes as C
+
+        self._params = context.he_params()
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self._L.he_ctx_create(C.byref(self._params), context.device, C.byref(h)), "he_ctx_create")
+        self._h = h
+        M = context.n_q + len(context.p_chain_bits)
+        mods = np.zeros(M, np.uint64)
+        psi = np.zeros(M, np.uint64)
+        _lib.check(self._L.he_ctx_moduli(self._h, _lib.addr(mods), _lib.addr(psi)))
+        self.moduli = [int(x) for x in mods]
+        self.psi = [int(x) for x in psi]
+        self.N = context.ring_degree
+        self.keys = RotationKeySet(context.n)
+        self._acct = _Ledger()
+        self._ids = itertools.count(1)
+        self._enc_counter = 0
+        self._enc_lock = threading.Lock()
+        self.registration_log: list[frozenset] = []
+        self._relin = False
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and getattr(self, "_L", None) is not None:
+            try:
+                self._L.he_ctx_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ------------------------------------------------------------ plumbing
+    @property
+    def stream(self) -> int:
+        return _torch().cuda.current_stream(self.device).cuda_stream
+
+    def _alloc(self, count: int, n_comp: int, limbs: int):
+        torch = _torch()
+        return torch.empty((count, n_comp, limbs, self.N), dtype=torch.int64, device=self.device)
+
+    def _wrap(self, tensors, level: int, scales) -> list[CipherVec]:
+        ids = [next(self._ids) for _ in range(len(tensors))]
+        out = []
+        for t, i, s in zip(tensors, ids, scales):
+            out.append(CipherVec(data=t, level=level, scale_bits=int(round(math.log2(s))), id=i, scale=float(s),
+                                 n_slots=self.context.n, owner=id(self)))
+        self._acct.track(ids)
+        return out
+
+    def _wrap_batch(self, batch, level: int, scales) -> list[CipherVec]:
+        return self._wrap([batch[i] for i in range(batch.shape[0])], level, scales)
+
+    @staticmethod
+    def _ptrs(cts: Sequence[CipherVec]) -> np.ndarray:
+        return _lib.ptr_array([c.ptr for c in cts])
+
+    @staticmethod
+    def _tptrs(batch) -> np.ndarray:
+        base, stride = batch.data_ptr(), batch.stride(0) * 8
+        return _lib.ptr_array([base + i * stride for i in range(batch.shape[0])])
+
+    def _check(self, ct: CipherVec) -> None:
+        if not isinstance(ct, CipherVec) or ct.n_slots != self.context.n or ct.owner != id(self):
+            width = getattr(ct, "n_slots", None)
+            raise ContextMismatch(f"ciphertext (width {width}) does not belong to this context (slots {self.context.n})")
+        if ct.data is None:
+            raise HebatchError(f"ciphertext {ct.id} was released")
+
+    def _check_plain(self, p: PlainVec) -> np.ndarray:
+        v = np.asarray(p.slots, dtype=np.float64)
+        if v.shape != (self.context.n,):
+            raise ContextMismatch(f"plaintext width {v.shape[0] if v.ndim else 0} != context slots {self.context.n}")
+        return v
+
+    def _res(self, value_int: int, limbs: int) -> list[int]:
+        return [value_int % q for q in self.moduli[:limbs]]
+
+    def _at_level(self, cts: Sequence[CipherVec], level: int) -> list:
+        """Tensors of `cts` truncated to level (+1 limbs); copies only if needed."""
+        out = []
+        for c in cts:
+            if c.level == level:
+                out.append(c.data)
+            else:
+                out.append(c.data[:, : level + 1].contiguous())
+        return out
+
+    # ------------------------------------------------------------ encryption
+    def _next_enc(self, count: int) -> int:
+        with self._enc_lock:
+            base = self._enc_counter
+            self._enc_counter += count
+        return base
+
+    def encrypt(self, values) -> CipherVec:
+        return self.encrypt_batch(np.asarray(values, dtype=np.float64).ravel()[None, :])[0]
+
+    def encrypt_batch(self, values) -> list[CipherVec]:
+        """Encode + encrypt each row of a [count, <=n] array (one launch sequence)."""
+        torch = _torch()
+        if isinstance(values, torch.Tensor):
+            v = values.to(device=self.device, dtype=torch.float64)
+        else:
+            v = torch.as_tensor(np.asarray(values, dtype=np.float64), device=self.device)
+        if v.dim() != 2:
+            raise HebatchError("encrypt_batch expects a 2-D [count, values] array")
+        count, nvals = v.shape
+        if nvals > self.context.n:
+            raise LengthExceedsSlots(f"{nvals} values > {self.context.n} slots")
+        v = v.contiguous()
+        L = self.context.n_q
+        out = self._alloc(count, 2, L)
+        ptrs = self._tptrs(out)
+        base = self._next_enc(count)
+        _lib.check(self._L.he_encrypt(self._h, v.data_ptr(), count, nvals, self.context.scale, base,
+                                      _lib.addr(ptrs), self.stream), "encrypt")
+        return self._wrap_batch(out, L - 1, [self.context.scale] * count)
+
+    def decrypt(self, ct: CipherVec) -> np.ndarray:
+        return self.decrypt_batch([ct])[0]
+
+    def decrypt_batch(self, cts: Sequence[CipherVec], as_tensor: bool = False):
+        """Decrypt + decode to float64 slots; levels may differ."""
+        torch = _torch()
+        for c in cts:
+            self._check(c)
+        out = torch.empty((len(cts), self.context.n), dtype=torch.float64, device=self.device)
+        by_level: dict[int, list[int]] = {}
+        for i, c in enumerate(cts):
+            by_level.setdefault(c.level, []).append(i)
+        for level, idx in by_level.items():
+            sub = [cts[i] for i in idx]
+            tmp = out if len(idx) == len(cts) else torch.empty((len(idx), self.context.n), dtype=torch.float64,
+                                                              device=self.device)
+            ptrs = self._ptrs(sub)
+            scales = np.array([c.scale for c in sub], np.float64)
+            _lib.check(self._L.he_decrypt(self._h, _lib.addr(ptrs), len(sub), level + 1, _lib.addr(scales),
+                                          tmp.data_ptr(), self.stream), "decrypt")
+            if tmp is not out:
+                out[torch.as_tensor(idx, device=self.device)] = tmp
+        if as_tensor:
+            return out
+        return out.cpu().numpy()
+
+    def decrypt_coeffs(self, ct: CipherVec) -> np.ndarray:
+        torch = _torch()
+        self._check(ct)
+        out = torch.empty((1, self.N), dtype=torch.float64, device=self.device)
+        ptrs = self._ptrs([ct])
+        _lib.check(self._L.he_decrypt_coeffs(self._h, _lib.addr(ptrs), 1, ct.level + 1, out.data_ptr(), self.stream))
+        return out.cpu().numpy()[0]
+
+    def release(self, *cts: CipherVec) -> None:
+        for ct in cts:
+            self._acct.drop(ct.id)
+            object.__setattr__(ct, "data", None)
+
+    # ------------------------------------------------------------ arithmetic
+    def rotate(self, ct: CipherVec, k: int) -> CipherVec:
+        self._check(ct)
+        if k % self.context.n == 0:
+            return ct
+        if not self.keys.holds(k):
+            raise MissingRotationKey(k)
+        self._acct.bump("rotations")
+        return self._rotate_batch([ct], k)[0]
+
+    def _rotate_batch(self, cts: Sequence[CipherVec], k: int) -> list[CipherVec]:
+        level = cts[0].level
+        g = pow(5, k % self.context.n, 2 * self.N)
+        out = self._alloc(len(cts), 2, level + 1)
+        src = self._ptrs(cts)
+        dst = self._tptrs(out)
+        _lib.check(self._L.he_rotate(self._h, g, _lib.addr(src), _lib.addr(dst), len(cts), level + 1, self.stream),
+                   "rotate")
+        return self._wrap_batch(out, level, [c.scale for c in cts])
+
+    def add(self, a: CipherVec, b: CipherVec) -> CipherVec:
+        self._check(a)
+        self._check(b)
+        self._acct.bump("adds")
+        return self._add_batch([a], [b])[0]
+
+    def _add_batch(self, A: Sequence[CipherVec], B: Sequence[CipherVec], sub: bool = False) -> list[CipherVec]:
+        level = min(min(c.level for c in A), min(c.level for c in B))
+        for a, b in zip(A, B):
+            if abs(a.scale / b.scale - 1.0) > SCALE_RTOL:
+                raise ScaleMismatch(f"scales {a.scale:.6g} and {b.scale:.6g} differ")
+        ta, tb = self._at_level(A, level), self._at_level(B, level)
+        out = self._alloc(len(A), 2, level + 1)
+        pa = _lib.ptr_array([t.data_ptr() for t in ta])
+        pb = _lib.ptr_array([t.data_ptr() for t in tb])
+        po = self._tptrs(out)
+        fn = self._L.he_sub if sub else self._L.he_add
+        _lib.check(fn(self._h, _lib.addr(pa), _lib.addr(pb), _lib.addr(po), len(A), level + 1, 2, self.stream), "add")
+        return self._wrap_batch(out, level, [a.scale for a in A])
+
+    def add_batch(self, A: Sequence[CipherVec], B: Sequence[CipherVec]) -> list[CipherVec]:
+        for c in list(A) + list(B):
+            self._check(c)
+        self._acct.bump("adds", len(A))
+        return self._add_batch(A, B)
+
+    def add_plain(self, a: CipherVec, p: PlainVec) -> CipherVec:
+        self._check(a)
+        v = self._check_plain(p)
+        self._acct.bump("adds")
+        if np.all(v == v[0]):
+            return self.add_const_batch([a], [float(v[0])], count=False)[0]
+        torch = _torch()
+        limbs = a.level + 1
+        pt = torch.empty((limbs, self.N), dtype=torch.int64, device=self.device)
+        vv = torch.as_tensor(v, device=self.device)
+        _lib.check(self._L.he_encode_plain(self._h, vv.data_ptr(), self.context.n, a.scale, limbs, pt.data_ptr(),
+                                           self.stream), "encode_plain")
+        out = self._alloc(1, 2, limbs)
+        out[0, 1].copy_(a.data[1])
+        pa = _lib.ptr_array([a.ptr])
+        pp = _lib.ptr_array([pt.data_ptr()])
+        po = self._tptrs(out)
+        _lib.check(self._L.he_add(self._h, _lib.addr(pa), _lib.addr(pp), _lib.addr(po), 1, limbs, 1, self.stream))
+        return self._wrap_batch(out, a.level, [a.scale])[0]
+
+    def add_const_batch(self, cts: Sequence[CipherVec], values: Sequence[float], count: bool = True) -> list[CipherVec]:
+        """ct_i + values[i] in every slot (no level consumed)."""
+        for c in cts:
+            self._check(c)
+        if count:
+            self._acct.bump("adds", len(cts))
+        level = cts[0].level
+        if any(c.level != level for c in cts):
+            raise HebatchError("add_const_batch needs equal levels")
+        limbs = level + 1
+        res = np.array([self._res(int(np.rint(v * c.scale)), limbs) for v, c in zip(values, cts)], np.uint64)
+        out = self._alloc(len(cts), 2, limbs)
+        pi, po = self._ptrs(cts), self._tptrs(out)
+        _lib.check(self._L.he_add_const(self._h, _lib.addr(pi), _lib.addr(po), len(cts), limbs, _lib.addr(res),
+                                        self.stream), "add_const")
+        return self._wrap_batch(out, level, [c.scale for c in cts])
+
+    def mult_plain(self, ct: CipherVec, p: PlainVec) -> CipherVec:
+        self._check(ct)
+        v = self._check_plain(p)
+        cost = self.context.mult_level_cost
+        if ct.level < cost:
+            raise LevelExhausted(f"level {ct.level} < multiplication cost {cost}")
+        self._acct.bump("plain_mults")
+        if np.all(v == v[0]):
+            return self.mul_const_batch([ct], [float(v[0])], count=False)[0]
+        torch = _torch()
+        limbs = ct.level + 1
+        ql = self.moduli[limbs - 1]
+        pt = torch.empty((limbs, self.N), dtype=torch.int64, device=self.device)
+        vv = torch.as_tensor(v, device=self.device)
+        _lib.check(self._L.he_encode_plain(self._h, vv.data_ptr(), self.context.n, float(ql), limbs, pt.data_ptr(),
+                                           self.stream), "encode_plain")
+        tmp = self._alloc(1, 2, limbs)
+        pi, pt_, pm = self._ptrs([ct]), pt.data_ptr(), self._tptrs(tmp)
+        _lib.check(self._L.he_mul_plain(self._h, _lib.addr(pi), pt_, _lib.addr(pm), 1, limbs, 2, self.stream))
+        return self._rescale_tensor(tmp, limbs, [ct.scale])
+
+    def mul_const_batch(self, cts: Sequence[CipherVec], values: Sequence[float], count: bool = True,
+                        out_scales: Sequence[float] | None = None) -> list[CipherVec]:
+        """ct_i * values[i] then rescale (one level).  The constant is encoded at
+        q_last * out_scale / in_scale so the result lands exactly on out_scale
+        (default: the input scale)."""
+        for c in cts:
+            self._check(c)
+        level = cts[0].level
+        if any(c.level != level for c in cts):
+            raise HebatchError("mul_const_batch needs equal levels")
+        if level < self.context.mult_level_cost:
+            raise LevelExhausted(f"level {level} < multiplication cost {self.context.mult_level_cost}")
+        if count:
+            self._acct.bump("plain_mults", len(cts))
+        limbs = level + 1
+        ql = self.moduli[limbs - 1]
+        outs = list(out_scales) if out_scales is not None else [c.scale for c in cts]
+        res = np.array([self._res(int(np.rint(v * ql * (o / c.scale))), limbs) for v, c, o in zip(values, cts, outs)],
+                       np.uint64)
+        tmp = self._alloc(len(cts), 2, limbs)
+        pi, pm = self._ptrs(cts), self._tptrs(tmp)
+        _lib.check(self._L.he_mul_const(self._h, _lib.addr(pi), _lib.addr(pm), len(cts), limbs, 2, _lib.addr(res),
+                                        self.stream), "mul_const")
+        return self._rescale_tensor(tmp, limbs, outs)
+
+    def _rescale_tensor(self, t, limbs: int, scales) -> list[CipherVec]:
+        out = self._alloc(t.shape[0], 2, limbs - 1)
+        pi, po = self._tptrs(t), self._tptrs(out)
+        _lib.check(self._L.he_rescale(self._h, _lib.addr(pi), _lib.addr(po), t.shape[0], limbs, 2, self.stream),
+                   "rescale")
+        return self._wrap_batch(out, limbs - 2, scales)
+
+    def mult_ct(self, a: CipherVec, b: CipherVec) -> CipherVec:
+        self._check(a)
+        self._check(b)
+        cost = self.context.mult_level_cost
+        if a.level < cost or b.level < cost:
+            raise LevelExhausted(f"levels ({a.level}, {b.level}) < multiplication cost {cost}")
+        self._acct.bump("ct_mults")
+        return self._mult_ct_batch([a], [b])[0]
+
+    def mult_ct_batch(self, A: Sequence[CipherVec], B: Sequence[CipherVec]) -> list[CipherVec]:
+        for c in list(A) + list(B):
+            self._check(c)
+        if any(c.level < self.context.mult_level_cost for c in list(A) + list(B)):
+            raise LevelExhausted("operand level below multiplication cost")
+        self._acct.bump("ct_mults", len(A))
+        return self._mult_ct_batch(A, B)
+
+    def _ensure_relin(self) -> None:
+        if not self._relin:
+            _lib.check(self._L.he_gen_switch_key(self._h, 0, self.stream), "relin keygen")
+            self._relin = True
+
+    def _mult_ct_batch(self, A, B) -> list[CipherVec]:
+        self._ensure_relin()
+        level = min(min(c.level for c in A), min(c.level for c in B))
+        limbs = level + 1
+        ta, tb = self._at_level(A, level), self._at_level(B, level)
+        out = self._alloc(len(A), 2, limbs - 1)
+        pa = _lib.ptr_array([t.data_ptr() for t in ta])
+        pb = _lib.ptr_array([t.data_ptr() for t in tb])
+        po = self._tptrs(out)
+        _lib.check(self._L.he_mult_ct(self._h, _lib.addr(pa), _lib.addr(pb), _lib.addr(po), len(A), limbs, self.stream),
+                   "mult_ct")
+        ql = self.moduli[limbs - 1]
+        return self._wrap_batch(out, level - 1, [a.scale * b.scale / ql for a, b in zip(A, B)])
+
+    def drop_level_batch(self, cts: Sequence[CipherVec], level: int) -> list[CipherVec]:
+        """Discard limbs down to ``level`` (no rescale, scale unchanged)."""
+        for c in cts:
+            self._check(c)
+            if c.level < level:
+                raise LevelExhausted(f"cannot raise level {c.level} to {level}")
+        out = self._alloc(len(cts), 2, level + 1)
+        for i, c in enumerate(cts):
+            out[i].copy_(c.data[:, : level + 1])
+        return self._wrap_batch(out, level, [c.scale for c in cts])
+
+    def bootstrap(self, ct: CipherVec) -> CipherVec:
+        self._check(ct)
+        raise HebatchError("bootstrapping is not part of the B200 engine (no BASELINE configuration bootstraps)")
+
+    def ensure_level(self, ct: CipherVec, needed: int) -> CipherVec:
+        if ct.level >= needed:
+            return ct
+        fresh = self.bootstrap(ct)
+        self.release(ct)
+        return fresh
+
+    # ------------------------------------------------------------ feature-major linear layer
+    def lincomb(self, inputs: Sequence[CipherVec], row_ptr, col, weights, bias=None,
+                out_scale: float | None = None, count_as_conv: bool = True) -> list[CipherVec]:
+        """out[o] = sum_t weights[t] * inputs[col[t]] (+ bias[o]), then rescale.
+
+        The batched form of conv_forward's k=1 fold loop (conv.py:137-166) and
+        of feature-major conv / pool / dense.  Each real weight is encoded as
+        the integer round(w * q_last * out_scale / scale(input)), so the output
+        scale after the rescale is exactly ``out_scale`` (default: the scale of
+        inputs[0]) even when the inputs' scales differ.  Counters advance as
+        the reference loop would: one plain_mult and one add per term.
+        """
+        for c in inputs:
+            self._check(c)
+        level = min(c.level for c in inputs)
+        if level < self.context.mult_level_cost:
+            raise LevelExhausted(f"level {level} < multiplication cost {self.context.mult_level_cost}")
+        limbs = level + 1
+        row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+        col = np.ascontiguousarray(col, np.int32)
+        w = np.asarray(weights, np.float64)
+        n_out = len(row_ptr) - 1
+        ql = self.moduli[limbs - 1]
+        s_out = float(out_scale) if out_scale is not None else inputs[0].scale
+        in_scale = np.array([c.scale for c in inputs], np.float64)
+        wf = w * (ql * s_out) / in_scale[col]
+        if np.any(np.abs(wf) >= 2.0 ** 62):
+            raise HebatchError("lincomb weight too large for the int64 encoding (|w * q| >= 2^62)")
+        wi = np.rint(wf).astype(np.int64)
+        tins = self._at_level(inputs, level)
+        pin = _lib.ptr_array([t.data_ptr() for t in tins])
+        acc = self._alloc(n_out, 2, limbs)
+        pacc = self._tptrs(acc)
+        _lib.check(self._L.he_lincomb(self._h, _lib.addr(pin), len(inputs), _lib.addr(pacc), n_out,
+                                      _lib.addr(row_ptr), _lib.addr(col), _lib.addr(wi), limbs, 2, self.stream),
+                   "lincomb")
+        out = self._alloc(n_out, 2, limbs - 1)
+        pout = self._tptrs(out)
+        _lib.check(self._L.he_rescale(self._h, _lib.addr(pacc), _lib.addr(pout), n_out, limbs, 2, self.stream),
+                   "rescale")
+        del acc
+        if bias is not None:
+            b = np.asarray(bias, np.float64)
+            res = np.array([self._res(int(np.rint(bv * s_out)), limbs - 1) for bv in b], np.uint64)
+            _lib.check(self._L.he_add_const(self._h, _lib.addr(pout), _lib.addr(pout), n_out, limbs - 1,
+                                            _lib.addr(res), self.stream), "bias")
+        if count_as_conv:
+            self._acct.bump("plain_mults", int(len(col)))
+            self._acct.bump("adds", int(len(col)))
+        return self._wrap_batch(out, level - 1, [s_out] * n_out)
+
+    # ------------------------------------------------------------ keys
+    def register_rotation_keys(self, offsets: Iterable[int]) -> None:
+        offsets = list(offsets)
+        new = self.keys.register(offsets)
+        for c in new:
+            _lib.check(self._L.he_gen_switch_key(self._h, pow(5, c, 2 * self.N), self.stream), "galois keygen")
+        if new:
+            self._acct.bump("key_loads", len(new))
+        self.registration_log.append(
+            frozenset(self.keys.canonical(o) for o in offsets if self.keys.canonical(o) != 0))
+
+    def unload_rotation_keys(self, offsets: Iterable[int]) -> None:
+        for c in self.keys.unload(offsets):
+            self._L.he_drop_switch_key(self._h, pow(5, c, 2 * self.N))
+
+    def unload_all_rotation_keys(self) -> None:
+        for c in self.keys.unload_all():
+            self._L.he_drop_switch_key(self._h, pow(5, c, 2 * self.N))
+
+    @property
+    def resident_key_count(self) -> int:
+        return len(self.keys)
+
+    # ------------------------------------------------------------ accounting
+    def snapshot_counters(self) -> OpCounters:
+        return self._acct.snapshot()
+
+    @property
+    def live_ciphertexts(self) -> int:
+        with self._acct.lock:
+            return len(self._acct.live)
+
+    def begin_live_window(self) -> None:
+        with self._acct.lock:
+            self._acct.window_peak = len(self._acct.live)
+
+    @property
+    def window_peak_live(self) -> int:
+        with self._acct.lock:
+            return self._acct.window_peak
+
+    def synchronize(self) -> None:
+        _lib.check(self._L.he_sync(self.stream))
+
+    # ------------------------------------------------------------ plaintext helpers
+    def plain(self, values) -> PlainVec:
+        values = np.asarray(values, dtype=np.float64).ravel()
+        n = self.context.n
+        if values.shape[0] > n:
+            raise LengthExceedsSlots(f"{values.shape[0]} values > {n} slots")
+        slots = np.zeros(n, dtype=np.float64)
+        slots[: values.shape[0]] = values
+        return PlainVec(slots=slots)
+
+    def constant(self, value: float) -> PlainVec:
+        return PlainVec(slots=np.full(self.context.n, float(value)))
+
+
+__all__ = [
+    "CipherVec",
+    "EngineContext",
+    "GpuEngine",
+    "OpCounters",
+    "PlainVec",
+    "RotationKeySet",
+    "VectorEngine",
+]

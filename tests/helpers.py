@@ -1,0 +1,50 @@
+"""Shared test helpers: parameter sets and GPU<->oracle plumbing."""
+
+from __future__ import annotations
+
+import numpy as np
+
+# name -> (log_n, q_bits, p_bits, alpha, scale_bits)
+PARAMS = {
+    "tiny": (5, (60, 40, 40, 40), (60, 60), 2, 40),
+    "cfg1": (12, (60, 40, 40, 40, 40), (60,), 1, 40),
+    "cfg2": (16, (50,) * 24, (50,) * 4, 4, 50),
+    "cfg3": (16, (60,) + (40,) * 13, (60,) * 3, 3, 40),
+    "cfg4": (16, (50,) * 24, (50,) * 4, 4, 50),
+}
+
+
+def engine_context(name, seed=1):
+    from paper_2604_16834_b200.engine import EngineContext
+
+    log_n, qb, pb, alpha, sb = PARAMS[name]
+    L = len(qb)
+    return EngineContext(n=1 << (log_n - 1), max_level=L - 1, bootstrap_reserve=1, first_modulus_bits=qb[0],
+                         rescale_bits=qb[-1] if L > 1 else qb[0], key_switch_digits=-(-L // alpha),
+                         noise_seed=seed, special_prime_bits=tuple(pb), scale_bits=sb, q_bits=tuple(qb))
+
+
+def oracle_for(name, seed=1):
+    import oracle as O
+
+    log_n, qb, pb, alpha, sb = PARAMS[name]
+    return O.Oracle(log_n, list(qb), list(pb), alpha, seed=seed, scale=2.0 ** sb)
+
+
+def to_np(t):
+    """torch int64 cuda tensor -> numpy uint64 (same bits)."""
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+def from_np(a, device):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(device)
+
+
+def rand_residues(rng, moduli, shape_prefix, N):
+    """uniform residues: array [*shape_prefix, len(moduli), N]"""
+    out = np.empty(tuple(shape_prefix) + (len(moduli), N), np.uint64)
+    for i, q in enumerate(moduli):
+        out[..., i, :] = rng.integers(0, q, size=tuple(shape_prefix) + (N,), dtype=np.uint64)
+    return out
