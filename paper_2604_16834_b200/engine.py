@@ -353,6 +353,37 @@ class GpuEngine:
         self._enc_lock = threading.Lock()
         self.registration_log: list[frozenset] = []
         self._relin = False
+        self._timing = None  # {category: [(start_event, end_event, units)]} when enabled
+
+    # ------------------------------------------------------------ timing hooks (bench.py)
+    def enable_timing(self, on: bool = True) -> None:
+        """Record CUDA events around every C-ABI call, on the launching stream."""
+        self._timing = {} if on else None
+
+    def timing_summary(self) -> dict:
+        """{category: (calls, total_ms, units)} for the recorded calls (synchronises)."""
+        torch = _torch()
+        torch.cuda.synchronize(self.device)
+        out = {}
+        for cat, evs in (self._timing or {}).items():
+            ms = sum(s.elapsed_time(e) for s, e, _ in evs)
+            units = np.sum(np.array([u for _, _, u in evs], dtype=np.float64), axis=0)
+            out[cat] = (len(evs), ms, units)
+        return out
+
+    def _call(self, cat: str, fn, *args, units=(0.0, 0.0)):
+        """Run one C-ABI call; with timing on, bracket it with CUDA events.
+        ``units`` = (algorithmic HBM bytes, algorithmic modular MACs)."""
+        if self._timing is None:
+            return fn(*args)
+        torch = _torch()
+        st = torch.cuda.current_stream(self.device)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(st)
+        rc = fn(*args)
+        e.record(st)
+        self._timing.setdefault(cat, []).append((s, e, units))
+        return rc
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -446,8 +477,9 @@ class GpuEngine:
         out = self._alloc(count, 2, L)
         ptrs = self._tptrs(out)
         base = self._next_enc(count)
-        _lib.check(self._L.he_encrypt(self._h, v.data_ptr(), count, nvals, self.context.scale, base,
-                                      _lib.addr(ptrs), self.stream), "encrypt")
+        _lib.check(self._call("encrypt", self._L.he_encrypt, self._h, v.data_ptr(), count, nvals, self.context.scale,
+                              base, _lib.addr(ptrs), self.stream,
+                              units=(count * (2.0 * L * self.N + nvals) * 8, 0.0)), "encrypt")
         return self._wrap_batch(out, L - 1, [self.context.scale] * count)
 
     def decrypt(self, ct: CipherVec) -> np.ndarray:
@@ -468,8 +500,9 @@ class GpuEngine:
                                                               device=self.device)
             ptrs = self._ptrs(sub)
             scales = np.array([c.scale for c in sub], np.float64)
-            _lib.check(self._L.he_decrypt(self._h, _lib.addr(ptrs), len(sub), level + 1, _lib.addr(scales),
-                                          tmp.data_ptr(), self.stream), "decrypt")
+            _lib.check(self._call("decrypt", self._L.he_decrypt, self._h, _lib.addr(ptrs), len(sub), level + 1,
+                                  _lib.addr(scales), tmp.data_ptr(), self.stream,
+                                  units=(len(sub) * 4.0 * self.N * 8, 0.0)), "decrypt")
             if tmp is not out:
                 out[torch.as_tensor(idx, device=self.device)] = tmp
         if as_tensor:
@@ -568,8 +601,9 @@ class GpuEngine:
         res = np.array([self._res(int(np.rint(v * c.scale)), limbs) for v, c in zip(values, cts)], np.uint64)
         out = self._alloc(len(cts), 2, limbs)
         pi, po = self._ptrs(cts), self._tptrs(out)
-        _lib.check(self._L.he_add_const(self._h, _lib.addr(pi), _lib.addr(po), len(cts), limbs, _lib.addr(res),
-                                        self.stream), "add_const")
+        _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pi), _lib.addr(po), len(cts),
+                              limbs, _lib.addr(res), self.stream, units=(len(cts) * 4.0 * limbs * self.N * 8, 0.0)),
+                   "add_const")
         return self._wrap_batch(out, level, [c.scale for c in cts])
 
     def mult_plain(self, ct: CipherVec, p: PlainVec) -> CipherVec:
@@ -656,8 +690,8 @@ class GpuEngine:
         pa = _lib.ptr_array([t.data_ptr() for t in ta])
         pb = _lib.ptr_array([t.data_ptr() for t in tb])
         po = self._tptrs(out)
-        _lib.check(self._L.he_mult_ct(self._h, _lib.addr(pa), _lib.addr(pb), _lib.addr(po), len(A), limbs, self.stream),
-                   "mult_ct")
+        _lib.check(self._call("mult_ct", self._L.he_mult_ct, self._h, _lib.addr(pa), _lib.addr(pb), _lib.addr(po),
+                              len(A), limbs, self.stream, units=(len(A) * 6.0 * limbs * self.N * 8, 0.0)), "mult_ct")
         ql = self.moduli[limbs - 1]
         return self._wrap_batch(out, level - 1, [a.scale * b.scale / ql for a, b in zip(A, B)])
 
@@ -716,23 +750,56 @@ class GpuEngine:
         pin = _lib.ptr_array([t.data_ptr() for t in tins])
         acc = self._alloc(n_out, 2, limbs)
         pacc = self._tptrs(acc)
-        _lib.check(self._L.he_lincomb(self._h, _lib.addr(pin), len(inputs), _lib.addr(pacc), n_out,
-                                      _lib.addr(row_ptr), _lib.addr(col), _lib.addr(wi), limbs, 2, self.stream),
-                   "lincomb")
+        n_used = len(np.unique(col))
+        poly = 2 * limbs * self.N
+        _lib.check(self._call("lincomb", self._L.he_lincomb, self._h, _lib.addr(pin), len(inputs), _lib.addr(pacc),
+                              n_out, _lib.addr(row_ptr), _lib.addr(col), _lib.addr(wi), limbs, 2, self.stream,
+                              units=((n_used + n_out) * poly * 8.0, float(len(col)) * poly)), "lincomb")
         out = self._alloc(n_out, 2, limbs - 1)
         pout = self._tptrs(out)
-        _lib.check(self._L.he_rescale(self._h, _lib.addr(pacc), _lib.addr(pout), n_out, limbs, 2, self.stream),
-                   "rescale")
+        _lib.check(self._call("rescale", self._L.he_rescale, self._h, _lib.addr(pacc), _lib.addr(pout), n_out, limbs,
+                              2, self.stream, units=(n_out * (2 * limbs - 1) * 2 * self.N * 8.0, 0.0)), "rescale")
         del acc
         if bias is not None:
             b = np.asarray(bias, np.float64)
             res = np.array([self._res(int(np.rint(bv * s_out)), limbs - 1) for bv in b], np.uint64)
-            _lib.check(self._L.he_add_const(self._h, _lib.addr(pout), _lib.addr(pout), n_out, limbs - 1,
-                                            _lib.addr(res), self.stream), "bias")
+            _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pout), _lib.addr(pout), n_out,
+                                  limbs - 1, _lib.addr(res), self.stream,
+                                  units=(n_out * 2.0 * (limbs - 1) * self.N * 8, 0.0)), "bias")
         if count_as_conv:
             self._acct.bump("plain_mults", int(len(col)))
             self._acct.bump("adds", int(len(col)))
         return self._wrap_batch(out, level - 1, [s_out] * n_out)
+
+    def lincomb_int(self, inputs: Sequence[CipherVec], row_ptr, col, int_weights, out_scale: float,
+                    count_adds: bool = True) -> list[CipherVec]:
+        """out[o] = sum_t int_weights[t] * inputs[col[t]] with NO rescale (level kept).
+
+        Used for average pooling / global average pooling: with unit weights
+        the sum of k ciphertexts at scale s encodes the mean at scale k*s,
+        so the 1/k factor costs no level (it is folded into the next layer's
+        weight encoding).  ``out_scale`` is the scale the caller declares.
+        """
+        for c in inputs:
+            self._check(c)
+        level = min(c.level for c in inputs)
+        limbs = level + 1
+        row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+        col = np.ascontiguousarray(col, np.int32)
+        wi = np.ascontiguousarray(int_weights, np.int64)
+        n_out = len(row_ptr) - 1
+        tins = self._at_level(inputs, level)
+        pin = _lib.ptr_array([t.data_ptr() for t in tins])
+        out = self._alloc(n_out, 2, limbs)
+        pout = self._tptrs(out)
+        poly = 2 * limbs * self.N
+        _lib.check(self._call("lincomb_int", self._L.he_lincomb, self._h, _lib.addr(pin), len(inputs),
+                              _lib.addr(pout), n_out, _lib.addr(row_ptr), _lib.addr(col), _lib.addr(wi), limbs, 2,
+                              self.stream, units=((len(np.unique(col)) + n_out) * poly * 8.0, float(len(col)) * poly)),
+                   "lincomb_int")
+        if count_adds:
+            self._acct.bump("adds", max(0, int(len(col)) - n_out))
+        return self._wrap_batch(out, level, [float(out_scale)] * n_out)
 
     # ------------------------------------------------------------ keys
     def register_rotation_keys(self, offsets: Iterable[int]) -> None:

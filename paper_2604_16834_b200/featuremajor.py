@@ -1,0 +1,323 @@
+"""Feature-major batched layers and the BASELINE networks (configs 1, 3, 4, 5).
+
+Feature-major packing puts ONE feature (pixel of one channel) of n samples in
+each ciphertext, so every linear layer is a plaintext-weighted linear
+combination of whole ciphertexts and needs no rotation:
+
+  conv3x3 (pad 1): out[o,y,x] = sum_{i,dy,dx valid} W[o,i,dy,dx] in[i,y+dy,x+dx]
+  2x2 avg pool   : out[c,y,x] = 1/4 sum_{a,b} in[c,2y+a,2x+b]
+  GAP            : out[c]     = 1/HW sum_p in[c,p]
+  dense          : out[o]     = sum_c W[o,c] in[c] + b[o]
+
+The reference expresses the k=1 case through conv_forward (conv.py:109-173,
+PackingLayout(H=1, W=1, b=n, p=features)); it has no feature-major spatial
+conv, but one is exactly reproduced with its own constant / mult_plain / add
+primitives.  Here each layer is one he_lincomb launch.
+
+Level plan (frozen; the CPU oracle follows the same one):
+  * conv / dense: one rescale; weights encoded at q_last * s_out / s_in so the
+    output scale is exactly the context scale.
+  * degree-2 activation c2 x^2 + c1 x + c0 = (a x + b)^2 + c with
+    a = sqrt(c2), b = c1 / (2 sqrt(c2)), c = c0 - c1^2 / (4 c2): (a, b) are
+    folded into the preceding layer's weights / bias, leaving one ct x ct
+    multiply (relinearise + rescale) and one constant add -> 1 level.
+  * degree-3 activation c3 x^3 + c1 x + c0 with y = a x, a = cbrt(c3):
+    y (y^2 + c1/a) + c0 -> 2 levels, 2 relinearisations.
+  * average pools: unit-weight sums without rescale, the 1/k factor is moved
+    into the ciphertext scale (k * s) and cancelled by the next layer's
+    weight encoding -> 0 levels.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import ShapeMismatch
+
+
+# ---------------------------------------------------------------- term builders (CSR)
+def conv3x3_csr(p: int, out_channels, H: int, W: int):
+    """CSR of a pad-1 3x3 conv for the listed output channels.
+
+    Inputs are indexed i*H*W + y*W + x; outputs (o in out_channels, y, x) in
+    that order.  Returns (row_ptr, col, widx) with widx indexing
+    weights.reshape(-1) of a (q, p, 3, 3) tensor.
+    """
+    oc = np.asarray(list(out_channels), dtype=np.int64)
+    q = len(oc)
+    y = np.arange(H)[:, None, None, None]
+    x = np.arange(W)[None, :, None, None]
+    dy = (np.arange(9) // 3 - 1)[None, None, None, :]
+    dx = (np.arange(9) % 3 - 1)[None, None, None, :]
+    i = np.arange(p)[None, None, :, None]
+    yy, xx = y + dy, x + dx
+    valid = (yy >= 0) & (yy < H) & (xx >= 0) & (xx < W)                      # [H, W, 1, 9]
+    valid = np.broadcast_to(valid, (H, W, p, 9))
+    col = (i * H * W + yy * W + xx)                                          # [H, W, p, 9]
+    col = np.broadcast_to(col, (H, W, p, 9))
+    tap = np.broadcast_to(i * 9 + np.arange(9)[None, None, None, :], (H, W, p, 9))
+    counts = valid.reshape(H * W, -1).sum(axis=1)                            # terms per pixel
+    cols_px = col[valid]                                                     # pixel-major order
+    taps_px = tap[valid]
+    row_ptr = np.zeros(q * H * W + 1, np.int64)
+    row_ptr[1:] = np.cumsum(np.tile(counts, q))
+    cols = np.tile(cols_px, q)
+    widx = (oc[:, None] * (p * 9) + taps_px[None, :]).reshape(-1)
+    return row_ptr.astype(np.int32), cols.astype(np.int32), widx
+
+
+def pool2x2_csr(C: int, H: int, W: int):
+    """CSR of a 2x2 / stride-2 sum pool: out (c, y, x) at H/2 x W/2."""
+    if H % 2 or W % 2:
+        raise ShapeMismatch(f"{H}x{W} not divisible by 2")
+    Hp, Wp = H // 2, W // 2
+    c = np.arange(C)[:, None, None, None]
+    y = np.arange(Hp)[None, :, None, None]
+    x = np.arange(Wp)[None, None, :, None]
+    a = np.array([0, 0, 1, 1])[None, None, None, :]
+    b = np.array([0, 1, 0, 1])[None, None, None, :]
+    cols = (c * H * W + (2 * y + a) * W + (2 * x + b)).reshape(-1)
+    row_ptr = np.arange(C * Hp * Wp + 1) * 4
+    return row_ptr.astype(np.int32), cols.astype(np.int32)
+
+
+def gap_csr(C: int, HW: int, channel_offset: int = 0):
+    """CSR of per-channel sums over HW positions (inputs c*HW + p)."""
+    row_ptr = np.arange(C + 1) * HW
+    cols = (np.arange(C)[:, None] * HW + np.arange(HW)[None, :]).reshape(-1) + channel_offset
+    return row_ptr.astype(np.int32), cols.astype(np.int32)
+
+
+def dense_csr(n_out: int, n_in: int):
+    row_ptr = np.arange(n_out + 1) * n_in
+    cols = np.tile(np.arange(n_in), n_out)
+    return row_ptr.astype(np.int32), cols.astype(np.int32)
+
+
+# ---------------------------------------------------------------- activations
+@dataclass(frozen=True)
+class Activation:
+    """Polynomial activation sum_k coeffs[k] x^k (degree 2, or 3 with no x^2 term)."""
+
+    coeffs: tuple
+
+    @property
+    def degree(self) -> int:
+        return len(self.coeffs) - 1
+
+    @property
+    def depth(self) -> int:
+        return 1 if self.degree == 2 else 2
+
+    def fold(self):
+        """(a, b): the affine map folded into the preceding linear layer."""
+        if self.degree == 2:
+            c0, c1, c2 = self.coeffs
+            if c2 <= 0:
+                raise ValueError("degree-2 activation needs a positive x^2 coefficient")
+            a = math.sqrt(c2)
+            return a, c1 / (2 * a)
+        c0, c1, c2, c3 = self.coeffs
+        if c2 != 0 or c3 == 0:
+            raise ValueError("degree-3 activation must have c2 = 0 and c3 != 0")
+        return float(np.cbrt(c3)), 0.0
+
+    def __call__(self, x):
+        return sum(c * x ** k for k, c in enumerate(self.coeffs))
+
+
+def apply_activation(engine, cts, act: Activation):
+    """Evaluate ``act`` on ciphertexts that already carry the folded affine map."""
+    if act.degree == 2:
+        c0, c1, c2 = act.coeffs
+        a = math.sqrt(c2)
+        c = c0 - c1 * c1 / (4 * c2)
+        sq = engine.mult_ct_batch(cts, cts)
+        if c == 0:
+            return sq
+        out = engine.add_const_batch(sq, [c] * len(sq))
+        engine.release(*sq)
+        return out
+    c0, c1, c2, c3 = act.coeffs
+    a = float(np.cbrt(c3))
+    d = c1 / a
+    sq = engine.mult_ct_batch(cts, cts)                  # y^2
+    sqd = engine.add_const_batch(sq, [d] * len(sq)) if d else sq
+    if sqd is not sq:
+        engine.release(*sq)
+    cub = engine.mult_ct_batch(cts, sqd)                  # y (y^2 + d)
+    engine.release(*sqd)
+    if c0 == 0:
+        return cub
+    out = engine.add_const_batch(cub, [c0] * len(cub))
+    engine.release(*cub)
+    return out
+
+
+# ---------------------------------------------------------------- layer calls
+def fm_conv3x3(engine, inputs, weights, bias, H, W, out_channels=None, fold=(1.0, 0.0), out_scale=None):
+    """Feature-major 3x3 / pad-1 convolution (+ folded affine), one launch.
+
+    inputs: p*H*W ciphertexts indexed i*H*W + y*W + x.  Returns the outputs
+    for ``out_channels`` (default all), indexed (o, y, x)."""
+    w = np.asarray(weights, np.float64)
+    q, p = w.shape[:2]
+    if len(inputs) != p * H * W:
+        raise ShapeMismatch(f"{len(inputs)} inputs for {p}x{H}x{W}")
+    oc = list(range(q)) if out_channels is None else list(out_channels)
+    rp, cols, widx = conv3x3_csr(p, oc, H, W)
+    a, b = fold
+    wt = a * w.reshape(-1)[widx]
+    bias_out = np.repeat(a * np.asarray(bias, np.float64)[oc] + b, H * W)
+    return engine.lincomb(inputs, rp, cols, wt, bias=bias_out, out_scale=out_scale or engine.context.scale)
+
+
+def fm_avgpool2x2(engine, inputs, C, H, W):
+    """2x2 average pool as unit-weight sums (no level): scale x4."""
+    rp, cols = pool2x2_csr(C, H, W)
+    s = inputs[0].scale
+    return engine.lincomb_int(inputs, rp, cols, np.ones(len(cols), np.int64), out_scale=4.0 * s)
+
+
+def fm_gap(engine, inputs, C, HW):
+    rp, cols = gap_csr(C, HW)
+    s = inputs[0].scale
+    return engine.lincomb_int(inputs, rp, cols, np.ones(len(cols), np.int64), out_scale=HW * s)
+
+
+def fm_dense(engine, inputs, weights, bias, fold=(1.0, 0.0), out_scale=None):
+    w = np.asarray(weights, np.float64)
+    rp, cols = dense_csr(w.shape[0], w.shape[1])
+    a, b = fold
+    return engine.lincomb(inputs, rp, cols, a * w.reshape(-1), bias=a * np.asarray(bias, np.float64) + b,
+                          out_scale=out_scale or engine.context.scale)
+
+
+# ---------------------------------------------------------------- networks
+@dataclass
+class CnnWeights:
+    convs: list            # [(W (q,p,3,3), b (q,))]
+    dense: tuple           # (W (10, C), b (10,))
+
+
+@dataclass(frozen=True)
+class CnnSpec:
+    """A feature-major CNN: conv blocks, pools after listed blocks, GAP, dense."""
+
+    channels: tuple        # (3, 16, 32) -> convs 3->16, 16->32
+    H: int
+    W: int
+    act: Activation
+    pool_after: tuple      # block indices followed by a 2x2 avg pool
+    n_classes: int = 10
+
+    def make_weights(self, seed: int) -> CnnWeights:
+        """N(0, 1/fan_in) weights, zero biases (BASELINE.json configs 3-4)."""
+        rng = np.random.default_rng(seed)
+        convs = []
+        for p, q in zip(self.channels[:-1], self.channels[1:]):
+            convs.append((rng.normal(0.0, math.sqrt(1.0 / (9 * p)), (q, p, 3, 3)), np.zeros(q)))
+        C = self.channels[-1]
+        dense = (rng.normal(0.0, math.sqrt(1.0 / C), (self.n_classes, C)), np.zeros(self.n_classes))
+        return CnnWeights(convs, dense)
+
+    def levels_needed(self) -> int:
+        return len(self.channels[:-1]) * (1 + self.act.depth) + 1
+
+    def forward_plain(self, wts: CnnWeights, images: np.ndarray) -> np.ndarray:
+        """float64 reference forward pass. images [samples, C, H, W] -> [samples, classes]."""
+        x = np.asarray(images, np.float64)
+        H, W = self.H, self.W
+        for blk, (w, b) in enumerate(wts.convs):
+            xp = np.pad(x, ((0, 0), (0, 0), (1, 1), (1, 1)))
+            out = np.zeros((x.shape[0], w.shape[0], H, W))
+            for dy in range(3):
+                for dx in range(3):
+                    out += np.einsum("oi,sihw->sohw", w[:, :, dy, dx], xp[:, :, dy:dy + H, dx:dx + W])
+            x = self.act(out + b[None, :, None, None])
+            if blk in self.pool_after:
+                x = x.reshape(x.shape[0], x.shape[1], H // 2, 2, W // 2, 2).mean(axis=(3, 5))
+                H, W = H // 2, W // 2
+        g = x.mean(axis=(2, 3))
+        return g @ wts.dense[0].T + wts.dense[1]
+
+
+def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, release_inputs: bool = True):
+    """Encrypted forward pass of ``spec`` over feature-major input ciphertexts.
+
+    x_cts: C0*H*W ciphertexts (channel-major).  The conv of each block is
+    evaluated per output channel and immediately activated / pooled, so the
+    full pre-pool activation map of a layer is never resident (config 3's
+    conv1 output alone would be 223 GB).  Releases its inputs unless
+    ``release_inputs`` is False.  Returns the n_classes output ciphertexts.
+    """
+    H, W = spec.H, spec.W
+    cur = list(x_cts)
+    nblk = len(wts.convs)
+    a, b = spec.act.fold()
+    for blk, (w, bias) in enumerate(wts.convs):
+        q = w.shape[0]
+        pool = blk in spec.pool_after
+        last = blk == nblk - 1
+        nxt = []
+        groups = [[o] for o in range(q)] if stream else [list(range(q))]
+        for oc in groups:
+            y = fm_conv3x3(engine, cur, w, bias, H, W, out_channels=oc, fold=(a, b))
+            z = apply_activation(engine, y, spec.act)
+            engine.release(*y)
+            if pool:
+                zp = fm_avgpool2x2(engine, z, len(oc), H, W)
+                engine.release(*z)
+                z = zp
+            if last:
+                hw = (H // 2) * (W // 2) if pool else H * W
+                g = fm_gap(engine, z, len(oc), hw)
+                engine.release(*z)
+                z = g
+            nxt.extend(z)
+        if blk > 0 or release_inputs:
+            engine.release(*cur)
+        cur = nxt
+        if pool:
+            H, W = H // 2, W // 2
+    out = fm_dense(engine, cur, wts.dense[0], wts.dense[1])
+    engine.release(*cur)
+    return out
+
+
+# ---------------------------------------------------------------- config 1: MLP
+@dataclass(frozen=True)
+class MlpSpec:
+    sizes: tuple = (64, 32, 10)
+    act: Activation = Activation((0.0, 0.0, 1.0))
+
+    def make_weights(self, seed: int):
+        rng = np.random.default_rng(seed)
+        return [(rng.normal(0.0, math.sqrt(1.0 / p), (q, p)), np.zeros(q))
+                for p, q in zip(self.sizes[:-1], self.sizes[1:])]
+
+    def forward_plain(self, wts, x):
+        h = np.asarray(x, np.float64)
+        for k, (w, b) in enumerate(wts):
+            h = h @ w.T + b
+            if k < len(wts) - 1:
+                h = self.act(h)
+        return h
+
+
+def run_mlp(engine, x_cts, spec: MlpSpec, wts):
+    cur = list(x_cts)
+    a, bb = spec.act.fold()
+    for k, (w, b) in enumerate(wts):
+        last = k == len(wts) - 1
+        y = fm_dense(engine, cur, w, b, fold=(1.0, 0.0) if last else (a, bb))
+        engine.release(*cur)
+        if not last:
+            z = apply_activation(engine, y, spec.act)
+            engine.release(*y)
+            y = z
+        cur = y
+    return cur

@@ -1,0 +1,134 @@
+"""End-to-end encrypted networks on the B200 vs the float64 reference forward
+pass (decrypt-level, 1e-3 max-abs as BASELINE.json requires) and vs the CPU
+oracle (bit-exact, layerwise sampled: the oracle recomputes chosen output
+ciphertexts from the GPU's own layer inputs)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import oracle_for, to_np
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+def _cfg1_data(seed=0):
+    from paper_2604_16834_b200 import configs
+
+    rng = np.random.default_rng(seed)
+    images = rng.uniform(0.0, 1.0, size=(2048, 8, 8))
+    wts = configs.MLP1.make_weights(seed + 1)
+    return images, wts
+
+
+def test_cfg1_through_reference_api_matches_plaintext_and_counters():
+    """pack_inputs -> conv_forward(k=1) -> mult_ct (x^2) -> conv_forward -> decrypt,
+    the reference call sequence of SURVEY.md 3.A, on the GPU engine."""
+    from paper_2604_16834_b200 import configs
+    from paper_2604_16834_b200.conv import ConvSpec, conv_forward
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.packing import PackingLayout, pack_inputs
+
+    images, ((W1, b1), (W2, b2)) = _cfg1_data()
+    eng = GpuEngine(configs.context(1, seed=3))
+    lay1 = PackingLayout(n=2048, H=1, W=1, b=2048, p=64)
+    cts = pack_inputs(eng, [im.reshape(64, 1, 1) for im in images], lay1)
+    h = conv_forward(eng, cts, ConvSpec(W1[:, :, None, None], b1, lay1))
+    h2 = [eng.mult_ct(x, x) for x in h]
+    out = conv_forward(eng, h2, ConvSpec(W2[:, :, None, None], b2, lay1.with_channels(32)))
+    got = np.stack([eng.decrypt(c) for c in out], axis=1)             # [samples, 10]
+    ref = configs.MLP1.forward_plain([(W1, b1), (W2, b2)], images.reshape(2048, 64))
+    assert np.max(np.abs(got - ref)) < TOL
+    c = eng.snapshot_counters()
+    assert (c.plain_mults, c.adds, c.ct_mults, c.rotations) == (2368, 2368, 32, 0)
+    assert out[0].level == 1
+
+
+def test_cfg1_fm_runner_bit_exact_vs_oracle():
+    from paper_2604_16834_b200 import configs
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.featuremajor import run_mlp
+    from paper_2604_16834_b200.packing import pack_features
+
+    images, wts = _cfg1_data(1)
+    eng = GpuEngine(configs.context(1, seed=5))
+    x = pack_features(eng, images.reshape(2048, 64))
+    x_np = [to_np(c.data) for c in x]
+    out = run_mlp(eng, x, configs.MLP1, wts)
+    got = eng.decrypt_batch(out).T
+    ref = configs.MLP1.forward_plain(wts, images.reshape(2048, 64))
+    assert np.max(np.abs(got - ref)) < TOL
+    # oracle replays the whole MLP with the same integer encodings
+    orc = oracle_for("cfg1", seed=5)
+    rk = orc.switch_key(0)
+    moduli = orc.moduli
+    cur, scales = x_np, [eng.context.scale] * 64
+    (W1, b1), (W2, b2) = wts
+    a, b = configs.MLP1.act.fold()
+    for k, (w, bias, fold) in enumerate([(W1, b1, (a, b)), (W2, b2, (1.0, 0.0))]):
+        ell = cur[0].shape[1]
+        ql = moduli[ell - 1]
+        q, p = w.shape
+        rows = np.arange(q + 1) * p
+        cols = np.tile(np.arange(p), q)
+        s_out = eng.context.scale
+        wf = (fold[0] * w.reshape(-1)) * (ql * s_out) / np.asarray(scales)[cols]
+        acc = orc.lincomb(cur, rows, cols, np.rint(wf).astype(np.int64))
+        nxt = []
+        for o in range(q):
+            r = orc.rescale(acc[o])
+            bv = fold[0] * bias[o] + fold[1]
+            r = orc.add_const(r, [int(np.rint(bv * s_out)) % m for m in moduli[: ell - 1]])
+            nxt.append(r)
+        cur, scales = nxt, [s_out] * q
+        if k == 0:
+            ql2 = moduli[ell - 2]
+            cur = [orc.mult_ct(c, c, rk) for c in cur]
+            scales = [s * s / ql2 for s in scales]
+    for o in range(10):
+        assert np.array_equal(to_np(out[o].data), cur[o]), o
+
+
+@pytest.mark.slow
+def test_cfg3_network_decrypt_and_sampled_bit_exact():
+    from paper_2604_16834_b200 import configs
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.featuremajor import fm_conv3x3, run_cnn
+    from paper_2604_16834_b200.packing import pack_features
+
+    rng = np.random.default_rng(7)
+    spec = configs.CNN3
+    images = rng.uniform(0.0, 1.0, size=(32768, 3, 32, 32)).astype(np.float64)
+    wts = spec.make_weights(11)
+    eng = GpuEngine(configs.context(3, seed=9))
+    x = pack_features(eng, images.reshape(32768, -1))
+    # sampled bit-exact check of conv1 + activation on a few outputs
+    orc = oracle_for("cfg3", seed=9)
+    a, b = spec.act.fold()
+    w1, b1 = wts.convs[0]
+    y = fm_conv3x3(eng, x, w1, b1, 32, 32, out_channels=[5], fold=(a, b))
+    for (yy, xx) in [(0, 0), (13, 31), (31, 7)]:
+        o = yy * 32 + xx
+        terms = [(i, yy + dy, xx + dx, dy, dx) for i in range(3) for dy in (-1, 0, 1) for dx in (-1, 0, 1)
+                 if 0 <= yy + dy < 32 and 0 <= xx + dx < 32]
+        ins = [to_np(x[i * 1024 + py * 32 + px].data) for (i, py, px, _, _) in terms]
+        ell = 14
+        ql = eng.moduli[ell - 1]
+        s = eng.context.scale
+        wv = np.array([a * w1[5, i, dy + 1, dx + 1] for (i, _, _, dy, dx) in terms])
+        wi = np.rint(wv * (ql * s) / s).astype(np.int64)
+        acc = orc.lincomb(ins, [0, len(terms)], list(range(len(terms))), wi)[0]
+        r = orc.rescale(acc)
+        r = orc.add_const(r, [int(np.rint((a * b1[5] + b) * s)) % m for m in eng.moduli[:13]])
+        assert np.array_equal(to_np(y[o].data), r), (yy, xx)
+    sq = eng.mult_ct_batch([y[0]], [y[0]])
+    assert np.array_equal(to_np(sq[0].data), orc.mult_ct(to_np(y[0].data), to_np(y[0].data), orc.switch_key(0)))
+    eng.release(*y, *sq)
+    # full network, decrypt-level
+    out = run_cnn(eng, x, spec, wts)
+    got = eng.decrypt_batch(out).T
+    ref = spec.forward_plain(wts, images[:256])
+    assert np.max(np.abs(got[:256] - ref)) < TOL
