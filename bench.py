@@ -1,0 +1,289 @@
+"""Benchmark: amortised encrypted samples/s of the feature-major CIFAR CNN.
+
+Workload (BASELINE.json configs 3 and 5): the 14-limb CNN (conv3x3 3->16,
+act, 2x2 avgpool, conv3x3 16->32, act, GAP, dense 32->10) on one
+32768-sample ciphertext group (3072 input ciphertexts, N = 2^16) per GPU per
+step.  With --gpus 8 the 8 groups of config 5 run one per GPU (weak scaling,
+no data-path collective: groups are independent).
+
+  value : samples/s with the encrypted inputs resident in HBM (network only)
+  e2e   : samples/s through the public API with HOST buffers: pinned images
+          -> H2D -> pack_features (encode + encrypt) -> network -> decrypt ->
+          D2H logits, all inside the timed region
+  --impl reference : the CPU oracle port on the host cores (rank 0 only)
+
+Prints ONE JSON line (rank 0).  Inputs (45 GB of ciphertexts per group) are
+far larger than the 126 MB L2, so no explicit flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "amortised encrypted samples/sec"
+SAMPLES_PER_GROUP = 32768
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=None, help="(ncu) run exactly this many network passes")
+    return ap.parse_args()
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def _config(world):
+    return {"workload": "cfg3/cfg5 CIFAR-shaped CNN, one 32768-sample ciphertext group per GPU per step",
+            "ring_degree": 65536, "q_limbs": 14, "special_primes": 3, "scale_bits": 40,
+            "input_ciphertexts_per_group": 3072, "groups_per_step": world,
+            "samples_per_step": SAMPLES_PER_GROUP * world, "parallelism": f"groups{world}",
+            "l2_flush": "inputs (45 GB per group) >> 126 MB L2"}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        import statistics
+
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import cpu_baseline
+
+    t = time.perf_counter()
+    # each "step" = one bounded oracle sample, extrapolated to one group
+    vals = []
+    for _ in range(max(1, args.steps)):
+        r = cpu_baseline.measure()
+        vals.append(r["samples_per_s"])
+    v = float(sorted(vals)[len(vals) // 2])
+    line = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * SAMPLES_PER_GROUP / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic",
+            "config": _config(1), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": r["threads"], "kind": "port",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = _args()
+    rank, world, local = _dist()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2604_16834_b200 import _lib, configs
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.featuremajor import run_cnn
+    from paper_2604_16834_b200.packing import pack_features
+
+    spec = configs.CNN3
+    wts = spec.make_weights(1234)                       # same model on every rank
+    group = rank                                         # config 5: group g seeded g
+    eng = GpuEngine(configs.context(3, seed=42, device=local))
+    rng = np.random.default_rng(group)
+    images = rng.uniform(0.0, 1.0, size=(SAMPLES_PER_GROUP, 3 * 32 * 32))
+    feat_host = torch.from_numpy(np.ascontiguousarray(images.T)).pin_memory()   # [3072, 32768] f64
+    x = pack_features(eng, images)                        # resident encrypted inputs
+    eng._ensure_relin()
+    del images
+
+    def step():
+        out = run_cnn(eng, x, spec, wts, release_inputs=False)
+        eng.release(*out)
+
+    if args.profile_steps is not None:                   # ncu mode: no timing, no baseline
+        for _ in range(args.profile_steps):
+            step()
+        torch.cuda.synchronize()
+        return
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # ---- device-resident timed region
+    eng.enable_timing(True)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.load().he_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier()
+    launches = _lib.load().he_launch_count() - launches0
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    summ = eng.timing_summary()
+    eng.enable_timing(False)
+    value = world * SAMPLES_PER_GROUP * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API with host buffers
+    eng.release(*x)                                      # free the resident inputs (45 GB)
+    del x
+    torch.cuda.empty_cache()
+    e2e_steps = args.e2e_steps or args.steps
+    out_host = torch.empty((10, SAMPLES_PER_GROUP), dtype=torch.float64).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        dev = feat_host.to("cuda", non_blocking=True)
+        cts = eng.encrypt_batch(dev)
+        del dev
+        out = run_cnn(eng, cts, spec, wts, release_inputs=True)
+        logits = eng.decrypt_batch(out, as_tensor=True)
+        eng.release(*out)
+        out_host.copy_(logits, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e = world * SAMPLES_PER_GROUP * e2e_steps / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (CUDA events over the timed region)
+    dom = max(summ.items(), key=lambda kv: kv[1][1])
+    calls, dom_ms, units = dom
+    peak, peak_kind = _peaks()
+    ach = units[0] / (dom_ms / 1e3) / 1e9
+    traffic = _traffic().get(dom[0])
+    breakdown = {k: {"calls": v[0], "ms": round(v[1], 2), "alg_GBps": round(v[2][0] / max(v[1], 1e-9) / 1e6, 1),
+                     "GMACps": round(v[2][1] / max(v[1], 1e-9) / 1e6, 1)} for k, v in summ.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import cpu_baseline
+
+        r = cpu_baseline.measure()
+        cpu = {"value": r["samples_per_s"], "unit": "samples/s", "cores": r["threads"], "kind": "port",
+               "sample": r["sample"]}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64 (RNS residues mod 40/60-bit primes)",
+            "data": "synthetic (seeded U[0,1] CIFAR-shaped images, N(0,1/fan_in) weights)",
+            "config": _config(world),
+            "e2e": {"value": e2e, "unit": "samples/s", "steps": e2e_steps,
+                    "h2d_bytes_per_step": int(feat_host.numel() * 8),
+                    "d2h_bytes_per_step": int(out_host.numel() * 8)},
+            "roofline": {"kernel": dom[0], "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "calls": calls, "avg_ms": dom_ms / calls,
+                         "int_GMACps": units[1] / (dom_ms / 1e3) / 1e9},
+            "breakdown": breakdown,
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -152,8 +152,21 @@ int he_lincomb(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *const
                const int32_t *row_ptr, const int32_t *col, const int64_t *w, int ell, int n_comp,
                void *stream);
 
+/* grouped form of he_lincomb for feature-major convolutions: every group g
+ * (an output pixel) shares one input gather and feeds M outputs:
+ *   out[out_base[g] + m*out_stride] = sum_{t in group g} weights[m*T + tap[t]] * in[col[t]]
+ * for m < M (M <= 32), mod q_i.  term_ptr [n_groups+1], col/tap [nnz],
+ * out_base [n_groups], weights [M][T] signed int64; all host arrays.
+ * Not rescaled.  Same semantics as expanding the groups into he_lincomb. */
+int he_lincomb_grouped(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
+                       int n_groups, const int32_t *term_ptr, const int32_t *term_col, const int32_t *term_tap,
+                       const int32_t *out_base, int out_stride, int M, int T, const int64_t *weights, int ell,
+                       int n_comp, void *stream);
+
 /* block until all work on `stream` is done; returns HE_ECUDA on async error */
 int he_sync(void *stream);
+/* number of kernels this library has launched in the process (bench evidence) */
+unsigned long long he_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,101 @@
+"""CPU baseline: the C oracle (ckks_oracle.c, OpenMP + one ciphertext per host
+thread) timed on a bounded sample of the config-3 network and extrapolated
+with that network's exact operation counts.
+
+TEST / MEASUREMENT INFRASTRUCTURE ONLY: used by bench.py's cpu_baseline leg
+and ``bench.py --impl reference``.  The reference package has no compiled
+CPU implementation of this path (hebatch is a float64 simulator without
+cryptography), so the oracle port stands in for it ("kind": "port").
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import oracle as O  # noqa: E402
+
+
+def cfg3_op_counts():
+    """Exact per-group op counts of the frozen config-3 plan (featuremajor.run_cnn)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_2604_16834_b200.featuremajor import conv3x3_csr
+
+    N = 1 << 16
+    nnz1 = len(conv3x3_csr(3, range(16), 32, 32)[1])
+    nnz2 = len(conv3x3_csr(16, range(32), 16, 16)[1])
+    return {
+        # (count, limbs): modular MACs over 2 components
+        "lincomb_macs": nnz1 * 2 * 14 * N + nnz2 * 2 * 12 * N + 320 * 2 * 10 * N,
+        "intsum_macs": 16384 * 2 * 12 * N + 8192 * 2 * 10 * N,
+        "rescale": [(16384, 14), (8192, 12), (10, 10)],
+        "mult_ct": [(16384, 13), (8192, 11)],
+    }
+
+
+def measure(seconds_budget: float = 20.0, threads: int | None = None, seed: int = 0) -> dict:
+    """Time the oracle on a bounded sample; returns samples/s for one 32768-sample group."""
+    threads = threads or len(os.sched_getaffinity(0))
+    orc = O.Oracle(16, [60] + [40] * 13, [60] * 3, 3, seed=seed, scale=2.0 ** 40)
+    rng = np.random.default_rng(seed)
+    N = orc.N
+    mods = orc.moduli
+
+    def rand_ct(ell, nc=2):
+        out = np.empty((nc, ell, N), np.uint64)
+        for i in range(ell):
+            out[:, i] = rng.integers(0, mods[i], (nc, N), dtype=np.uint64)
+        return out
+
+    ops = cfg3_op_counts()
+    res = {"threads": threads}
+    # 1. linear combination throughput (OpenMP over outputs)
+    n_out, k = 2 * threads, 27
+    ins = [rand_ct(14) for _ in range(k)]
+    rows = np.arange(n_out + 1) * k
+    cols = np.tile(np.arange(k), n_out)
+    w = rng.integers(-(2 ** 41), 2 ** 41, len(cols))
+    t = time.perf_counter()
+    orc.lincomb(ins, rows, cols, w, n_threads=threads)
+    dt = time.perf_counter() - t
+    res["lincomb_mac_per_s"] = len(cols) * 2 * 14 * N / dt
+    # 2. ct x ct (tensor + relin + rescale), one ciphertext per host thread
+    rk = orc.switch_key(0)
+    per_relin = {}
+    for ell in (13, 11):
+        a = [rand_ct(ell) for _ in range(threads)]
+        t = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda c: orc.mult_ct(c, c, rk), a))
+        per_relin[ell] = (time.perf_counter() - t) / threads
+    res["mult_ct_s"] = per_relin
+    # 3. rescale
+    per_rs = {}
+    for ell in (14, 12):
+        a = [rand_ct(ell) for _ in range(threads)]
+        t = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(orc.rescale, a))
+        per_rs[ell] = (time.perf_counter() - t) / threads
+    res["rescale_s"] = per_rs
+    total = ops["lincomb_macs"] / res["lincomb_mac_per_s"] + ops["intsum_macs"] / res["lincomb_mac_per_s"]
+    total += sum(cnt * per_relin[ell] for cnt, ell in ops["mult_ct"])
+    total += sum(cnt * per_rs.get(ell, per_rs[12] * ell / 12) for cnt, ell in ops["rescale"])
+    res["group_seconds_extrapolated"] = total
+    res["samples_per_s"] = 32768.0 / total
+    res["sample"] = (f"oracle on {threads} host threads: {n_out}x{k}-term lincomb at 14 limbs, {threads} mult_ct "
+                     f"at 13 and 11 limbs, {threads} rescales at 14 and 12 limbs; extrapolated with the exact "
+                     f"config-3 op counts of one 32768-sample group")
+    return res
+
+
+if __name__ == "__main__":
+    import json
+
+    print(json.dumps(measure(), default=str))

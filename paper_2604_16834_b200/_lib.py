@@ -32,7 +32,7 @@ EXPORTS = [
     "he_export_switch_key", "he_ntt", "he_encrypt", "he_decrypt", "he_decrypt_coeffs",
     "he_encode_plain", "he_add", "he_sub", "he_add_const", "he_mul_const", "he_mul_plain",
     "he_drop_limbs", "he_tensor", "he_relin", "he_keyswitch", "he_rescale", "he_mult_ct",
-    "he_automorphism", "he_rotate", "he_lincomb", "he_sync",
+    "he_automorphism", "he_rotate", "he_lincomb", "he_sync", "he_launch_count", "he_lincomb_grouped",
 ]
 
 
@@ -100,6 +100,8 @@ def load():
         "he_rotate": (i, [vp, u32, pp, pp, i, i, vp]),
         "he_lincomb": (i, [vp, pp, i, pp, i, vp, vp, vp, i, i, vp]),
         "he_sync": (i, [vp]),
+        "he_launch_count": (C.c_ulonglong, []),
+        "he_lincomb_grouped": (i, [vp, pp, i, pp, i, i, vp, vp, vp, vp, i, i, i, vp, i, i, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

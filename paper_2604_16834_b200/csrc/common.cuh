@@ -27,8 +27,15 @@ struct ModConst {
     uint64_t r2;        // 2^128 mod q  (redc(x * r2) = x * 2^64 mod q)
     uint64_t ninv;      // N^-1 mod q
     uint64_t ninv_sh;   // Shoup(ninv)
-    uint64_t pad[3];
+    uint64_t ratio;     // floor((2^64 - 1) / q): reduce64
+    uint64_t pad[2];
 };
+
+// x mod q for any 64-bit x (one high product + one conditional subtract)
+__device__ __forceinline__ uint64_t reduce64(uint64_t x, const ModConst &mc) {
+    uint64_t r = x - __umul64hi(x, mc.ratio) * mc.q;
+    return r >= mc.q ? r - mc.q : r;
+}
 
 // Per-(level, digit) ModUp table and per-level ModDown table, device resident.
 struct BconvTable {
@@ -61,6 +68,7 @@ struct he_ctx {
 // ---------------------------------------------------------------- errors
 
 void he_set_error(const char *fmt, ...);
+void he_count_launch(int n);  // process-wide kernel launch counter (he_launch_count)
 #define HE_CHECK_CUDA(call)                                                            \
     do {                                                                               \
         cudaError_t _e = (call);                                                       \
@@ -69,7 +77,11 @@ void he_set_error(const char *fmt, ...);
             return HE_ECUDA;                                                           \
         }                                                                              \
     } while (0)
-#define HE_CHECK_LAUNCH() HE_CHECK_CUDA(cudaGetLastError())
+#define HE_CHECK_LAUNCH()         \
+    do {                          \
+        he_count_launch(1);       \
+        HE_CHECK_CUDA(cudaGetLastError()); \
+    } while (0)
 #define HE_TRY(x)                     \
     do {                              \
         int _r = (x);                 \

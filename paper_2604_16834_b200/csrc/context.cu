@@ -22,6 +22,11 @@ void he_set_error(const char *fmt, ...) {
     va_end(ap);
 }
 extern "C" const char *he_last_error(void) { return g_err; }
+
+#include <atomic>
+static std::atomic<unsigned long long> g_launches{0};
+void he_count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+extern "C" unsigned long long he_launch_count(void) { return g_launches.load(); }
 extern "C" int he_abi_version(void) { return HE_ABI_VERSION; }
 
 // ---------------------------------------------------------------- host modular helpers
@@ -216,6 +221,7 @@ static int build_tables(he_ctx *c) {
         k.r2 = (uint64_t)(((hu128)h_mont(1, q) << 64) % q);  // R^2 mod q
         k.ninv = h_inv((uint64_t)N % q, q);
         k.ninv_sh = h_shoup(k.ninv, q);
+        k.ratio = UINT64_MAX / q;
     }
     HE_CHECK_CUDA(cudaMalloc(&c->d_tw, tw.size() * 8));
     HE_CHECK_CUDA(cudaMemcpy(c->d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));

@@ -322,9 +322,11 @@ static int ntt_launch(he_ctx *c, PolySrc src, int n_polys, const uint8_t *mod_ma
         if (!inv) {
             k_fwd16_cols<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
             k_fwd16_rows<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
+            he_count_launch(1);
         } else {
             k_inv16_rows<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
             k_inv16_cols<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
+            he_count_launch(1);
         }
     } else if (c->logN == 12) {
         if (!inv)

@@ -152,8 +152,9 @@ __global__ void k_expand_centered(uint64_t *t, const uint64_t *r, size_t npc, in
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
         size_t pc = i / ((size_t)lm1 * N);
         int l = (int)((i >> logN) % lm1);
-        uint64_t v = r[pc * N + (i & (N - 1))], q = mc[l].q;
-        t[i] = v > half ? sub_mod(0, (ql - v) % q, q) : v % q;
+        uint64_t v = r[pc * N + (i & (N - 1))];
+        const ModConst m = mc[l];
+        t[i] = v > half ? sub_mod(0, reduce64(ql - v, m), m.q) : reduce64(v, m);
     }
 }
 // out[i] = (x_i - t_i) * ql^-1 mod q_i

@@ -771,6 +771,61 @@ class GpuEngine:
             self._acct.bump("adds", int(len(col)))
         return self._wrap_batch(out, level - 1, [s_out] * n_out)
 
+    def lincomb_grouped(self, inputs: Sequence[CipherVec], term_ptr, term_col, term_tap, out_base, out_stride: int,
+                        weights, n_out: int, bias=None, out_scale: float | None = None) -> list[CipherVec]:
+        """Grouped linear combination (he_lincomb_grouped) + rescale + bias.
+
+        Group g (an output pixel) gathers inputs col[t] (t in its term range)
+        and produces M = weights.shape[0] outputs
+        out[out_base[g] + m * out_stride] = sum_t weights[m, tap[t]] * in[col[t]].
+        All inputs must share one scale; weights are encoded like lincomb().
+        """
+        for c in inputs:
+            self._check(c)
+        s_in = inputs[0].scale
+        if any(abs(c.scale / s_in - 1.0) > 0 for c in inputs):
+            raise ScaleMismatch("lincomb_grouped needs inputs at one scale")
+        level = min(c.level for c in inputs)
+        if level < self.context.mult_level_cost:
+            raise LevelExhausted(f"level {level} < multiplication cost {self.context.mult_level_cost}")
+        limbs = level + 1
+        w = np.asarray(weights, np.float64)
+        M, T = w.shape
+        ql = self.moduli[limbs - 1]
+        s_out = float(out_scale) if out_scale is not None else s_in
+        wf = w * (ql * s_out) / s_in
+        if np.any(np.abs(wf) >= 2.0 ** 62):
+            raise HebatchError("lincomb weight too large for the int64 encoding (|w * q| >= 2^62)")
+        wi = np.ascontiguousarray(np.rint(wf).astype(np.int64))
+        tp = np.ascontiguousarray(term_ptr, np.int32)
+        tc = np.ascontiguousarray(term_col, np.int32)
+        tt = np.ascontiguousarray(term_tap, np.int32)
+        ob = np.ascontiguousarray(out_base, np.int32)
+        tins = self._at_level(inputs, level)
+        pin = _lib.ptr_array([t.data_ptr() for t in tins])
+        acc = self._alloc(n_out, 2, limbs)
+        pacc = self._tptrs(acc)
+        poly = 2 * limbs * self.N
+        n_used = len(np.unique(tc))
+        _lib.check(self._call("lincomb", self._L.he_lincomb_grouped, self._h, _lib.addr(pin), len(inputs),
+                              _lib.addr(pacc), n_out, len(ob), _lib.addr(tp), _lib.addr(tc), _lib.addr(tt),
+                              _lib.addr(ob), int(out_stride), M, T, _lib.addr(wi), limbs, 2, self.stream,
+                              units=((n_used + n_out) * poly * 8.0, float(len(tc)) * M * poly)), "lincomb_grouped")
+        out = self._alloc(n_out, 2, limbs - 1)
+        pout = self._tptrs(out)
+        _lib.check(self._call("rescale", self._L.he_rescale, self._h, _lib.addr(pacc), _lib.addr(pout), n_out, limbs,
+                              2, self.stream, units=(n_out * (2 * limbs - 1) * 2 * self.N * 8.0, 0.0)), "rescale")
+        del acc
+        if bias is not None:
+            b = np.asarray(bias, np.float64)
+            res = np.array([self._res(int(np.rint(bv * s_out)), limbs - 1) for bv in b], np.uint64)
+            _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pout), _lib.addr(pout), n_out,
+                                  limbs - 1, _lib.addr(res), self.stream,
+                                  units=(n_out * 2.0 * (limbs - 1) * self.N * 8, 0.0)), "bias")
+        self._acct.bump("plain_mults", int(len(tc)) * M)
+        self._acct.bump("adds", int(len(tc)) * M)
+        return self._wrap_batch(out, level - 1, [s_out] * n_out)
+
     def lincomb_int(self, inputs: Sequence[CipherVec], row_ptr, col, int_weights, out_scale: float,
                     count_adds: bool = True) -> list[CipherVec]:
         """out[o] = sum_t int_weights[t] * inputs[col[t]] with NO rescale (level kept).

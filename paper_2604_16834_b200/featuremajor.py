@@ -69,6 +69,30 @@ def conv3x3_csr(p: int, out_channels, H: int, W: int):
     return row_ptr.astype(np.int32), cols.astype(np.int32), widx
 
 
+def conv3x3_groups(p: int, H: int, W: int, rows=None):
+    """Pixel groups of a pad-1 3x3 conv restricted to output ``rows``.
+
+    Group g = pixel (y, x) in row-major order over the selected rows; its terms
+    are the valid taps (i, dy, dx) with input col = i*H*W + (y+dy)*W + (x+dx)
+    and tap index i*9 + (dy+1)*3 + (dx+1) into a (q, p, 3, 3) weight tensor.
+    Returns (term_ptr, col, tap, n_pixels)."""
+    rows = np.arange(H) if rows is None else np.asarray(list(rows))
+    y = rows[:, None, None, None]
+    x = np.arange(W)[None, :, None, None]
+    k = np.arange(9)[None, None, None, :]
+    dy, dx = k // 3 - 1, k % 3 - 1
+    i = np.arange(p)[None, None, :, None]
+    yy, xx = y + dy, x + dx
+    shape = (len(rows), W, p, 9)
+    valid = np.broadcast_to((yy >= 0) & (yy < H) & (xx >= 0) & (xx < W), shape)
+    col = np.broadcast_to(i * H * W + yy * W + xx, shape)[valid]
+    tap = np.broadcast_to(i * 9 + k, shape)[valid]
+    counts = valid.reshape(len(rows) * W, -1).sum(axis=1)
+    term_ptr = np.zeros(len(counts) + 1, np.int64)
+    term_ptr[1:] = np.cumsum(counts)
+    return term_ptr.astype(np.int32), col.astype(np.int32), tap.astype(np.int32), len(counts)
+
+
 def pool2x2_csr(C: int, H: int, W: int):
     """CSR of a 2x2 / stride-2 sum pool: out (c, y, x) at H/2 x W/2."""
     if H % 2 or W % 2:
@@ -158,21 +182,30 @@ def apply_activation(engine, cts, act: Activation):
 
 
 # ---------------------------------------------------------------- layer calls
-def fm_conv3x3(engine, inputs, weights, bias, H, W, out_channels=None, fold=(1.0, 0.0), out_scale=None):
-    """Feature-major 3x3 / pad-1 convolution (+ folded affine), one launch.
+def fm_conv3x3(engine, inputs, weights, bias, H, W, out_channels=None, fold=(1.0, 0.0), out_scale=None,
+               rows=None):
+    """Feature-major 3x3 / pad-1 convolution (+ folded affine).
 
     inputs: p*H*W ciphertexts indexed i*H*W + y*W + x.  Returns the outputs
-    for ``out_channels`` (default all), indexed (o, y, x)."""
+    for ``out_channels`` (default all; at most 32 per launch) and output
+    ``rows`` (default all), indexed (o, y, x) over the selection.  Each
+    launch is one he_lincomb_grouped: a pixel's taps are gathered once and
+    multiplied into every selected channel."""
     w = np.asarray(weights, np.float64)
     q, p = w.shape[:2]
     if len(inputs) != p * H * W:
         raise ShapeMismatch(f"{len(inputs)} inputs for {p}x{H}x{W}")
     oc = list(range(q)) if out_channels is None else list(out_channels)
-    rp, cols, widx = conv3x3_csr(p, oc, H, W)
     a, b = fold
-    wt = a * w.reshape(-1)[widx]
-    bias_out = np.repeat(a * np.asarray(bias, np.float64)[oc] + b, H * W)
-    return engine.lincomb(inputs, rp, cols, wt, bias=bias_out, out_scale=out_scale or engine.context.scale)
+    tp, col, tap, npix = conv3x3_groups(p, H, W, rows)
+    out = []
+    for c0 in range(0, len(oc), 32):
+        ch = oc[c0:c0 + 32]
+        wm = a * w[ch].reshape(len(ch), p * 9)
+        bias_out = np.repeat(a * np.asarray(bias, np.float64)[ch] + b, npix)
+        out.extend(engine.lincomb_grouped(inputs, tp, col, tap, np.arange(npix), npix, wm, len(ch) * npix,
+                                          bias=bias_out, out_scale=out_scale or engine.context.scale))
+    return out
 
 
 def fm_avgpool2x2(engine, inputs, C, H, W):
@@ -245,14 +278,18 @@ class CnnSpec:
         return g @ wts.dense[0].T + wts.dense[1]
 
 
-def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, release_inputs: bool = True):
+def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, release_inputs: bool = True,
+            tile_outputs: int = 1024):
     """Encrypted forward pass of ``spec`` over feature-major input ciphertexts.
 
-    x_cts: C0*H*W ciphertexts (channel-major).  The conv of each block is
-    evaluated per output channel and immediately activated / pooled, so the
-    full pre-pool activation map of a layer is never resident (config 3's
-    conv1 output alone would be 223 GB).  Releases its inputs unless
-    ``release_inputs`` is False.  Returns the n_classes output ciphertexts.
+    x_cts: C0*H*W ciphertexts (channel-major).  Each block is streamed over
+    tiles of output rows: one grouped conv launch per tile covers every output
+    channel (<= 32 per launch), then the tile is activated and pooled (or
+    GAP-summed) before the next tile starts, so the full pre-pool activation
+    map is never resident (config 3's conv1 output alone would be 223 GB).
+    ``tile_outputs`` bounds ciphertexts per launch.  Releases its inputs
+    unless ``release_inputs`` is False.  Returns the n_classes output
+    ciphertexts.
     """
     H, W = spec.H, spec.W
     cur = list(x_cts)
@@ -262,27 +299,42 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
         q = w.shape[0]
         pool = blk in spec.pool_after
         last = blk == nblk - 1
-        nxt = []
-        groups = [[o] for o in range(q)] if stream else [list(range(q))]
-        for oc in groups:
-            y = fm_conv3x3(engine, cur, w, bias, H, W, out_channels=oc, fold=(a, b))
+        R = max(2 if pool else 1, (tile_outputs // (q * W)) // 2 * 2 if pool else tile_outputs // (q * W))
+        R = min(R, H) if stream else H
+        Ho, Wo = (H // 2, W // 2) if pool else (H, W)
+        nxt = [None] * (q * Ho * Wo) if not last else None
+        gap = None
+        for r0 in range(0, H, R):
+            rows = list(range(r0, min(H, r0 + R)))
+            nr = len(rows)
+            y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows)   # [o][r][x]
             z = apply_activation(engine, y, spec.act)
             engine.release(*y)
             if pool:
-                zp = fm_avgpool2x2(engine, z, len(oc), H, W)
+                zp = fm_avgpool2x2(engine, z, q, nr, W)                         # [o][r/2][x/2]
                 engine.release(*z)
                 z = zp
+                nr //= 2
             if last:
-                hw = (H // 2) * (W // 2) if pool else H * W
-                g = fm_gap(engine, z, len(oc), hw)
+                rp, cols = gap_csr(q, nr * Wo)
+                part = engine.lincomb_int(z, rp, cols, np.ones(len(cols), np.int64), out_scale=Ho * Wo * z[0].scale)
                 engine.release(*z)
-                z = g
-            nxt.extend(z)
+                if gap is None:
+                    gap = part
+                else:
+                    nsum = engine.add_batch(gap, part)
+                    engine.release(*gap, *part)
+                    gap = nsum
+                continue
+            y0 = rows[0] // 2 if pool else rows[0]
+            for o in range(q):
+                for r in range(nr):
+                    for x in range(Wo):
+                        nxt[o * Ho * Wo + (y0 + r) * Wo + x] = z[(o * nr + r) * Wo + x]
         if blk > 0 or release_inputs:
             engine.release(*cur)
-        cur = nxt
-        if pool:
-            H, W = H // 2, W // 2
+        cur = gap if last else nxt
+        H, W = Ho, Wo
     out = fm_dense(engine, cur, wts.dense[0], wts.dense[1])
     engine.release(*cur)
     return out

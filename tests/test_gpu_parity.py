@@ -162,6 +162,38 @@ def test_mult_ct_and_rotate_bit_exact(pair):
         assert np.max(np.abs(eng.decrypt(r) - np.roll(a_v, -k))) < 1e-5
 
 
+def test_lincomb_grouped_conv_bit_exact(pair):
+    """he_lincomb_grouped (3x3 conv pixel groups, all channels) vs the oracle's
+    CSR linear combination on the expanded terms."""
+    from paper_2604_16834_b200.featuremajor import conv3x3_groups
+
+    name, eng, orc = pair
+    if eng.N < 128:
+        pytest.skip("grouped kernel needs N >= 128")
+    rng = np.random.default_rng(21)
+    p, q, H, W = 2, 3, 4, 4
+    vals = rng.uniform(-1, 1, (p * H * W, eng.context.n))
+    cts = eng.encrypt_batch(vals)
+    w = rng.normal(0, 0.3, (q, p, 3, 3))
+    tp, col, tap, npix = conv3x3_groups(p, H, W, rows=[1, 2, 3])
+    outs = eng.lincomb_grouped(cts, tp, col, tap, np.arange(npix), npix, w.reshape(q, -1), q * npix)
+    ell = cts[0].level + 1
+    ql = eng.moduli[ell - 1]
+    s = cts[0].scale
+    wi = np.rint(w.reshape(q, -1) * (ql * s) / s).astype(np.int64)
+    rows, cols, ws = [0], [], []
+    for m in range(q):
+        for g in range(npix):
+            for t in range(tp[g], tp[g + 1]):
+                cols.append(col[t])
+                ws.append(wi[m, tap[t]])
+            rows.append(len(cols))
+    ins = [to_np(c.data) for c in cts]
+    acc = orc.lincomb(ins, rows, cols, ws)
+    for o in range(q * npix):
+        assert np.array_equal(to_np(outs[o].data), orc.rescale(acc[o])), o
+
+
 def test_lincomb_bit_exact(pair):
     name, eng, orc = pair
     rng = np.random.default_rng(9)
