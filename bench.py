@@ -245,11 +245,10 @@ def main():
     e2e = world * SAMPLES_PER_GROUP * e2e_steps / (e2e_ms / 1e3)
 
     # ---- roofline of the dominant kernel (CUDA events over the timed region)
-    dom = max(summ.items(), key=lambda kv: kv[1][1])
-    calls, dom_ms, units = dom
+    dom_name, (calls, dom_ms, units) = max(summ.items(), key=lambda kv: kv[1][1])
     peak, peak_kind = _peaks()
     ach = units[0] / (dom_ms / 1e3) / 1e9
-    traffic = _traffic().get(dom[0])
+    traffic = _traffic().get(dom_name)
     breakdown = {k: {"calls": v[0], "ms": round(v[1], 2), "alg_GBps": round(v[2][0] / max(v[1], 1e-9) / 1e6, 1),
                      "GMACps": round(v[2][1] / max(v[1], 1e-9) / 1e6, 1)} for k, v in summ.items()}
 
@@ -271,7 +270,7 @@ def main():
             "e2e": {"value": e2e, "unit": "samples/s", "steps": e2e_steps,
                     "h2d_bytes_per_step": int(feat_host.numel() * 8),
                     "d2h_bytes_per_step": int(out_host.numel() * 8)},
-            "roofline": {"kernel": dom[0], "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+            "roofline": {"kernel": dom_name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
                          "calls": calls, "avg_ms": dom_ms / calls,
                          "int_GMACps": units[1] / (dom_ms / 1e3) / 1e9},

@@ -167,6 +167,9 @@ int he_lincomb_grouped(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_
 int he_sync(void *stream);
 /* number of kernels this library has launched in the process (bench evidence) */
 unsigned long long he_launch_count(void);
+/* integer-pipe peak on `device`: ops_per_s[0] = 32-bit IMAD/s,
+ * ops_per_s[1] = 64x64->128 multiply-accumulates/s (roofline denominators) */
+int he_microbench_intpipe(int device, double *ops_per_s);
 
 #ifdef __cplusplus
 }

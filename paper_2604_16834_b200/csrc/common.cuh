@@ -118,6 +118,40 @@ __device__ __forceinline__ void mac128(u128 &acc, uint64_t a, uint64_t b) {
         : "+l"(acc.lo), "+l"(acc.hi)
         : "l"(a), "l"(b));
 }
+// Split accumulator for moduli q < 2^52 (operands < 2^52): x*w is accumulated
+// as L (64-bit, carries counted in C) + M 2^32 + H 2^64 from four 32x32->64
+// products -- 7 instructions per MAC instead of a full 128-bit product chain.
+// Valid while the exact sum stays < 2^116 (terms * q^2), which callers ensure.
+struct acc52 {
+    uint64_t L, M, H;
+    uint32_t C;
+};
+__device__ __forceinline__ void acc52_zero(acc52 &a) {
+    a.L = 0;
+    a.M = 0;
+    a.H = 0;
+    a.C = 0;
+}
+__device__ __forceinline__ void mac52(acc52 &a, uint64_t x, uint64_t w) {
+    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32), wl = (uint32_t)w, wh = (uint32_t)(w >> 32);
+    uint64_t p = (uint64_t)xl * wl;
+    asm("add.cc.u64 %0, %0, %2;\n\t"
+        "addc.u32 %1, %1, 0;"
+        : "+l"(a.L), "+r"(a.C)
+        : "l"(p));
+    a.M += (uint64_t)xh * wl;
+    a.M += (uint64_t)xl * wh;
+    a.H += (uint64_t)xh * wh;
+}
+// collapse to a 128-bit (hi, lo)
+__device__ __forceinline__ u128 acc52_sum(const acc52 &a) {
+    u128 r;
+    uint64_t ml = a.M << 32, mh = a.M >> 32;
+    r.lo = a.L + ml;
+    r.hi = a.H + mh + (uint64_t)a.C + (r.lo < ml ? 1 : 0);
+    return r;
+}
+
 // Montgomery reduction of T = hi 2^64 + lo < q 2^64: returns T 2^-64 mod q in [0, q)
 __device__ __forceinline__ uint64_t redc(uint64_t hi, uint64_t lo, uint64_t q, uint64_t qinv) {
     uint64_t m = lo * qinv;

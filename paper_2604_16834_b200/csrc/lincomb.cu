@@ -4,11 +4,16 @@
 // input gather (the <= 9p valid taps of the window) against every output
 // channel's weights.  Grouping outputs by pixel turns the layer into a series
 // of tiny dense GEMMs  out[m] = sum_k W[m][tap_k] * in[col_k]  (m < M):
-// each thread loads an input residue once and feeds M 128-bit accumulators,
-// so the load count per modular MAC drops by M and the kernel becomes
-// integer-pipe bound.  Weights (signed integers, shared by all limbs) are
-// converted per limb to Montgomery form and staged in shared memory as
-// [tap][m] so a thread reads two weights per 128-bit LDS.
+// each thread loads an input residue once and feeds M accumulators, so the
+// load count per modular MAC drops by M.  Weights (signed integers, shared by
+// all limbs) are converted per limb to Montgomery form and staged in shared
+// memory as [tap][m] so a thread reads two weights per 128-bit LDS.  Terms
+// carry the input's device address directly (no pointer-table indirection)
+// and the gather is software-pipelined four terms deep.
+//
+// Two accumulator variants: for limbs with q < 2^52 (and a bounded term
+// count) the split 32-bit accumulator mac52 (~7 instructions per MAC);
+// otherwise exact 128-bit mad.lo.cc/madc.hi with a per-term fold.
 //
 // Replaces the fold loop of the reference's conv_forward (conv.py:137-156,
 // one mult_plain + add per (output, input, tap)) with one launch per layer
@@ -20,6 +25,13 @@
 namespace {
 
 constexpr int LB = 128;  // threads (coefficients) per CTA
+constexpr int PF = 4;    // gather prefetch depth (terms)
+
+struct __align__(16) Term {
+    const uint64_t *p;  // input ciphertext base address
+    int32_t tap;
+    int32_t pad;
+};
 
 __global__ void k_group_weights(uint64_t *wM, const int64_t *w, int M, int MM, int T, int ell, const ModConst *mc) {
     // wM [ell][T][MM] Montgomery; padded m >= M are zero
@@ -38,67 +50,129 @@ __global__ void k_group_weights(uint64_t *wM, const int64_t *w, int M, int MM, i
     }
 }
 
-template <int MM>
-__global__ void __launch_bounds__(LB) k_lincomb_grouped(uint64_t *const *__restrict__ out,
-                                                        const uint64_t *const *__restrict__ in,
-                                                        const int32_t *__restrict__ term_ptr,
-                                                        const int2 *__restrict__ terms,
-                                                        const int32_t *__restrict__ out_base, int out_stride, int M,
-                                                        int T, const uint64_t *__restrict__ wM, int n_groups, int gpb,
-                                                        int ell, int logN, int kmax, const ModConst *mc) {
-    extern __shared__ uint64_t wsm[];  // [T][MM]
-    const int N = 1 << logN;
+struct GroupArgs {
+    uint64_t *const *out;
+    const int32_t *term_ptr;
+    const Term *terms;
+    const int32_t *out_base;
+    const uint64_t *wM;  // [ell][T][WS] Montgomery weights
+    const ModConst *mc;
+    int out_stride, M, T, WS, n_groups, gpb, ell, logN, kmax;
+    int l_lo, nl;        // this launch covers limbs [l_lo, l_lo + nl) of every component
+    int m_off;           // first output channel handled by this launch
+};
+
+template <bool FAST>
+struct Acc;
+template <>
+struct Acc<true> {
+    acc52 a;
+    __device__ __forceinline__ void zero() { acc52_zero(a); }
+    __device__ __forceinline__ void mac(uint64_t x, uint64_t w) { mac52(a, x, w); }
+    __device__ __forceinline__ void fold(uint64_t) {}
+    __device__ __forceinline__ u128 sum() const { return acc52_sum(a); }
+};
+template <>
+struct Acc<false> {
+    u128 a;
+    __device__ __forceinline__ void zero() { a = {0, 0}; }
+    __device__ __forceinline__ void mac(uint64_t x, uint64_t w) { mac128(a, x, w); }
+    __device__ __forceinline__ void fold(uint64_t q) {
+        if (a.hi >= q) a.hi -= q;
+    }
+    __device__ __forceinline__ u128 sum() const { return a; }
+};
+
+// FAST: every limb of the launch has q < 2^52 and kmax * q < 2^64, so the
+// split 32-bit accumulator applies and no per-term fold is needed.
+template <int MM, bool FAST>
+__global__ void __launch_bounds__(LB) k_lincomb_grouped(const GroupArgs a) {
+    extern __shared__ uint64_t wsm[];  // [T][WS]
+    const int N = 1 << a.logN;
     const int cpp = N / LB;
-    const int pl = blockIdx.y / cpp;  // comp * ell + limb
-    const int l = pl % ell;
-    const size_t off = (size_t)pl * N + (size_t)(blockIdx.y % cpp) * LB + threadIdx.x;
-    const ModConst c = mc[l];
-    const uint64_t *src = wM + (size_t)l * T * MM;
-    for (int i = threadIdx.x; i < T * MM; i += LB) wsm[i] = src[i];
+    const int pl = blockIdx.y / cpp;  // comp * nl + (limb - l_lo)
+    const int l = a.l_lo + pl % a.nl;
+    const int comp = pl / a.nl;
+    const size_t off = ((size_t)comp * a.ell + l) * N + (size_t)(blockIdx.y % cpp) * LB + threadIdx.x;
+    const ModConst c = a.mc[l];
+    const uint64_t *src = a.wM + (size_t)l * a.T * a.WS;
+    for (int i = threadIdx.x; i < a.T * a.WS; i += LB) wsm[i] = src[i];
     __syncthreads();
     // sums of kmax products < q^2 need a fold to keep hi < q when kmax * q >= 2^64
-    const bool fold = (double)kmax * (double)c.q >= 1.8e19;
-    const int g0 = blockIdx.x * gpb, g1 = min(g0 + gpb, n_groups);
+    const bool fold = !FAST && (double)a.kmax * (double)c.q >= 1.8e19;
+    const int g0 = blockIdx.x * a.gpb, g1 = min(g0 + a.gpb, a.n_groups);
     for (int g = g0; g < g1; g++) {
-        u128 acc[MM];
+        const int t0 = a.term_ptr[g], t1 = a.term_ptr[g + 1];
+        const int ob = a.out_base[g] + a.m_off * a.out_stride;
+        Acc<FAST> acc[MM];
 #pragma unroll
-        for (int m = 0; m < MM; m++) acc[m] = {0, 0};
-        const int t1 = term_ptr[g + 1];
-        for (int t = term_ptr[g]; t < t1; t++) {
-            const int2 ct = terms[t];
-            const uint64_t x = __ldg(in[ct.x] + off);
-            const uint64_t *wr = wsm + ct.y * MM;
+        for (int m = 0; m < MM; m++) acc[m].zero();
+        for (int t = t0; t < t1; t += PF) {
+            uint64_t xs[PF];
+            int taps[PF];
 #pragma unroll
-            for (int m = 0; m < MM; m += 2) {
-                const ulonglong2 w2 = *(const ulonglong2 *)(wr + m);
-                mac128(acc[m], x, w2.x);
-                mac128(acc[m + 1], x, w2.y);
+            for (int u = 0; u < PF; u++) {  // issue all gathers first
+                if (t + u < t1) {
+                    const Term tm = a.terms[t + u];
+                    xs[u] = __ldg(tm.p + off);
+                    taps[u] = tm.tap;
+                } else {
+                    xs[u] = 0;
+                    taps[u] = 0;
+                }
             }
-            if (fold) {
 #pragma unroll
-                for (int m = 0; m < MM; m++)
-                    if (acc[m].hi >= c.q) acc[m].hi -= c.q;
+            for (int u = 0; u < PF; u++) {
+                const uint64_t *wr = wsm + taps[u] * a.WS + a.m_off;
+#pragma unroll
+                for (int m = 0; m < MM; m += 2) {
+                    const ulonglong2 w2 = *(const ulonglong2 *)(wr + m);
+                    acc[m].mac(xs[u], w2.x);
+                    acc[m + 1].mac(xs[u], w2.y);
+                }
+                if (fold) {
+#pragma unroll
+                    for (int m = 0; m < MM; m++) acc[m].fold(c.q);
+                }
             }
         }
-        const int ob = out_base[g];
 #pragma unroll
         for (int m = 0; m < MM; m++) {
             // hi < q: either folded per term, or kmax * q < 2^64 bounds the sum
-            if (m < M) out[ob + m * out_stride][off] = redc(acc[m].hi, acc[m].lo, c.q, c.qinv);
+            if (a.m_off + m < a.M) {
+                const u128 sm = acc[m].sum();
+                a.out[ob + m * a.out_stride][off] = redc(sm.hi, sm.lo, c.q, c.qinv);
+            }
         }
     }
 }
 
-template <int MM>
-int launch_grouped(dim3 grid, size_t smem, cudaStream_t s, uint64_t *const *out, const uint64_t *const *in,
-                   const int32_t *tp, const int2 *terms, const int32_t *ob, int out_stride, int M, int T,
-                   const uint64_t *wM, int G, int gpb, int ell, int logN, int kmax, const ModConst *mc) {
+template <int MM, bool FAST>
+int launch_grouped(dim3 grid, size_t smem, cudaStream_t s, const GroupArgs &a) {
     if (smem > 48 * 1024)
-        HE_CHECK_CUDA(cudaFuncSetAttribute(k_lincomb_grouped<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_lincomb_grouped<MM><<<grid, LB, smem, s>>>(out, in, tp, terms, ob, out_stride, M, T, wM, G, gpb, ell, logN, kmax,
-                                                 mc);
+        HE_CHECK_CUDA(cudaFuncSetAttribute(k_lincomb_grouped<MM, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+    k_lincomb_grouped<MM, FAST><<<grid, LB, smem, s>>>(a);
     HE_CHECK_LAUNCH();
     return HE_OK;
+}
+
+int dispatch_grouped(int MM, bool fast, dim3 grid, size_t smem, cudaStream_t s, const GroupArgs &a) {
+    if (fast) {
+        switch (MM) {
+            case 2: return launch_grouped<2, true>(grid, smem, s, a);
+            case 4: return launch_grouped<4, true>(grid, smem, s, a);
+            case 8: return launch_grouped<8, true>(grid, smem, s, a);
+            default: return launch_grouped<16, true>(grid, smem, s, a);
+        }
+    }
+    switch (MM) {
+        case 2: return launch_grouped<2, false>(grid, smem, s, a);
+        case 4: return launch_grouped<4, false>(grid, smem, s, a);
+        case 8: return launch_grouped<8, false>(grid, smem, s, a);
+        case 16: return launch_grouped<16, false>(grid, smem, s, a);
+        default: return launch_grouped<32, false>(grid, smem, s, a);
+    }
 }
 
 }  // namespace
@@ -134,29 +208,31 @@ extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in
             return HE_EINVAL;
         }
     }
-    for (int t = 0; t < nnz; t++)
+    std::vector<Term> terms(std::max(nnz, 1));
+    for (int t = 0; t < nnz; t++) {
         if (term_col[t] < 0 || term_col[t] >= n_in || term_tap[t] < 0 || term_tap[t] >= T) {
             he_set_error("he_lincomb_grouped: term %d (col %d tap %d) out of range", t, term_col[t], term_tap[t]);
             return HE_EINVAL;
         }
+        terms[t].p = in[term_col[t]];
+        terms[t].tap = term_tap[t];
+        terms[t].pad = 0;
+    }
     for (int i = 0; i < M * T; i++)
         if (weights[i] >= ((int64_t)1 << 62) || weights[i] <= -((int64_t)1 << 62)) {
             he_set_error("he_lincomb_grouped: |w| >= 2^62");
             return HE_EINVAL;
         }
-    int MM = M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : M <= 16 ? 16 : 32;
+    const int MM = M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : M <= 16 ? 16 : 32;
     cudaStream_t s = (cudaStream_t)stream;
-    void **din = nullptr, **dout = nullptr;
-    HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
+    void **dout = nullptr;
     HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
-    std::vector<int2> terms(std::max(nnz, 1));
-    for (int t = 0; t < nnz; t++) terms[t] = make_int2(term_col[t], term_tap[t]);
-    size_t b_tp = (size_t)(n_groups + 1) * 4, b_terms = (size_t)terms.size() * 8, b_ob = (size_t)n_groups * 4,
+    size_t b_tp = (size_t)(n_groups + 1) * 4, b_terms = terms.size() * sizeof(Term), b_ob = (size_t)n_groups * 4,
            b_w = (size_t)M * T * 8, b_wM = (size_t)ell * T * MM * 8;
     char *meta = nullptr;
     HE_TRY(he_scratch_alloc((void **)&meta, b_wM + b_terms + b_w + b_tp + b_ob + 64, s));
     uint64_t *wM = (uint64_t *)meta;
-    int2 *dterms = (int2 *)(meta + b_wM);
+    Term *dterms = (Term *)(meta + b_wM);
     int64_t *dw = (int64_t *)(meta + b_wM + b_terms);
     int32_t *dtp = (int32_t *)(meta + b_wM + b_terms + b_w);
     int32_t *dob = (int32_t *)(meta + b_wM + b_terms + b_w + b_tp);
@@ -166,28 +242,49 @@ extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in
     HE_CHECK_CUDA(cudaMemcpyAsync(dob, out_base, b_ob, cudaMemcpyHostToDevice, s));
     k_group_weights<<<ceil_div((size_t)ell * T * MM, 256), 256, 0, s>>>(wM, dw, M, MM, T, ell, c->d_mc);
     HE_CHECK_LAUNCH();
-    int gpb = std::max(1, std::min(8, n_groups / 148));
-    int cpp = c->N / LB;
-    size_t smem = (size_t)T * MM * 8;
+    const int gpb = std::max(1, std::min(8, n_groups / 148));
+    const int cpp = c->N / LB;
+    const size_t smem = (size_t)T * MM * 8;
     int rc = HE_OK;
     if ((size_t)nc * ell * cpp > 65535) {
         he_set_error("he_lincomb_grouped: grid too large");
         rc = HE_EINVAL;
     }
-    if (rc == HE_OK) {
-        dim3 grid(ceil_div(n_groups, gpb), (unsigned)(nc * ell * cpp));
-        auto O = (uint64_t *const *)dout;
-        auto I = (const uint64_t *const *)din;
-        switch (MM) {
-            case 2: rc = launch_grouped<2>(grid, smem, s, O, I, dtp, dterms, dob, out_stride, M, T, wM, n_groups, gpb, ell, c->logN, kmax, c->d_mc); break;
-            case 4: rc = launch_grouped<4>(grid, smem, s, O, I, dtp, dterms, dob, out_stride, M, T, wM, n_groups, gpb, ell, c->logN, kmax, c->d_mc); break;
-            case 8: rc = launch_grouped<8>(grid, smem, s, O, I, dtp, dterms, dob, out_stride, M, T, wM, n_groups, gpb, ell, c->logN, kmax, c->d_mc); break;
-            case 16: rc = launch_grouped<16>(grid, smem, s, O, I, dtp, dterms, dob, out_stride, M, T, wM, n_groups, gpb, ell, c->logN, kmax, c->d_mc); break;
-            default: rc = launch_grouped<32>(grid, smem, s, O, I, dtp, dterms, dob, out_stride, M, T, wM, n_groups, gpb, ell, c->logN, kmax, c->d_mc); break;
+    GroupArgs a;
+    a.out = (uint64_t *const *)dout;
+    a.term_ptr = dtp;
+    a.terms = dterms;
+    a.out_base = dob;
+    a.wM = wM;
+    a.mc = c->d_mc;
+    a.out_stride = out_stride;
+    a.M = M;
+    a.T = T;
+    a.WS = MM;
+    a.n_groups = n_groups;
+    a.gpb = gpb;
+    a.ell = ell;
+    a.logN = c->logN;
+    a.kmax = kmax;
+    // runs of consecutive limbs that share the accumulator variant
+    auto fast_ok = [&](int l) {
+        return c->mod[l] < (1ull << 52) && (double)kmax * (double)c->mod[l] < 1.8e19 && kmax <= 2048;
+    };
+    for (int l0 = 0; l0 < ell && rc == HE_OK;) {
+        const bool fast = fast_ok(l0);
+        int l1 = l0 + 1;
+        while (l1 < ell && fast_ok(l1) == fast) l1++;
+        a.l_lo = l0;
+        a.nl = l1 - l0;
+        dim3 grid(ceil_div(n_groups, gpb), (unsigned)(nc * a.nl * cpp));
+        const int mm = fast ? std::min(MM, 16) : MM;
+        for (int m0 = 0; m0 < M && rc == HE_OK; m0 += mm) {
+            a.m_off = m0;
+            rc = dispatch_grouped(mm, fast, grid, smem, s, a);
         }
+        l0 = l1;
     }
     he_scratch_free(meta, s);
-    he_scratch_free(din, s);
     he_scratch_free(dout, s);
     return rc;
 }

@@ -1,0 +1,74 @@
+// microbench.cu -- integer-pipe peak measurement for the roofline denominators.
+//
+// MEASURED_PEAKS.json carries only HBM and bf16 tensor peaks; the NTT, key
+// switching and CUDA-core linear combination are integer-pipe bound, so the
+// engine measures the pipe it runs on: independent 32-bit IMAD chains
+// (8 per thread, full grid) and the 64x64->128 multiply-accumulate the
+// kernels use (mad.lo.cc.u64 + madc.hi.u64).
+#include "common.cuh"
+
+namespace {
+
+__global__ void k_imad32(uint32_t *sink, int iters, uint32_t seed) {
+    uint32_t a[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = seed + threadIdx.x * 8 + k;
+    const uint32_t m = seed | 1u;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) a[k] = a[k] * m + (uint32_t)k;
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) s ^= a[k];
+    if (s == 0x12345678u) sink[0] = s;
+}
+
+__global__ void k_mac128(uint64_t *sink, int iters, uint64_t seed) {
+    u128 acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    uint64_t x = seed + threadIdx.x, w = seed * 3 + 1;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) mac128(acc[k], x + k, w);
+        x += acc[0].lo & 1;
+    }
+    uint64_t s = acc[0].hi ^ acc[1].hi ^ acc[2].hi ^ acc[3].lo;
+    if (s == 0x123456789ull) sink[0] = s;
+}
+
+}  // namespace
+
+// ops_per_s[0] = 32-bit IMAD/s, ops_per_s[1] = 64x64->128 MAC/s (blocking)
+extern "C" int he_microbench_intpipe(int device, double *ops_per_s) {
+    HE_CHECK_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    HE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    void *sink;
+    HE_CHECK_CUDA(cudaMalloc(&sink, 64));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    float ms = 0;
+    for (int rep = 0; rep < 2; rep++) {  // first run warms clocks
+        cudaEventRecord(e0);
+        k_imad32<<<blocks, threads>>>((uint32_t *)sink, iters, 12345u);
+        cudaEventRecord(e1);
+        HE_CHECK_CUDA(cudaEventSynchronize(e1));
+    }
+    cudaEventElapsedTime(&ms, e0, e1);
+    ops_per_s[0] = (double)blocks * threads * iters * 8 / (ms * 1e-3);
+    for (int rep = 0; rep < 2; rep++) {
+        cudaEventRecord(e0);
+        k_mac128<<<blocks, threads>>>((uint64_t *)sink, iters, 12345u);
+        cudaEventRecord(e1);
+        HE_CHECK_CUDA(cudaEventSynchronize(e1));
+    }
+    cudaEventElapsedTime(&ms, e0, e1);
+    ops_per_s[1] = (double)blocks * threads * iters * 4 / (ms * 1e-3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
