@@ -50,7 +50,7 @@ struct he_ctx {
     int N, logN, L, K, alpha, dnum, nslots, device;
     std::vector<uint64_t> mod, psi;
     ModConst *d_mc = nullptr;        // [L+K]
-    uint64_t *d_tw = nullptr;        // [L+K][4][N]  psi_brv, shoup, ipsi_brv, shoup
+    uint64_t *d_tw = nullptr;        // [L+K][fwd|inv][N][2]  (psi^brv(i), Shoup) pairs
     uint64_t *d_sk = nullptr;        // [L+K][N]     canonical, NTT domain
     double *d_fftw = nullptr;        // [nslots][2]  omega^k
     double *d_twist = nullptr;       // [nslots][2]  zeta^j

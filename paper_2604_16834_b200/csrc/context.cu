@@ -194,7 +194,7 @@ static int build_tables(he_ctx *c) {
             }
         }
     }
-    // twiddles
+    // twiddles: per modulus [fwd|inv][N] pairs (psi^brv(i), Shoup) -- one 16-byte load each
     std::vector<uint64_t> tw((size_t)M * 4 * N);
     std::vector<ModConst> mc(M);
     for (int m = 0; m < M; m++) {
@@ -203,14 +203,12 @@ static int build_tables(he_ctx *c) {
         uint64_t pw = 1, ipw = 1;
         for (int i = 0; i < N; i++) {
             uint32_t r = h_brv((uint32_t)i, c->logN);
-            T[r] = pw;
-            T[2 * N + r] = ipw;
+            T[2 * r] = pw;
+            T[2 * r + 1] = h_shoup(pw, q);
+            T[2 * N + 2 * r] = ipw;
+            T[2 * N + 2 * r + 1] = h_shoup(ipw, q);
             pw = h_mulmod(pw, psi, q);
             ipw = h_mulmod(ipw, ipsi, q);
-        }
-        for (int i = 0; i < N; i++) {
-            T[N + i] = h_shoup(T[i], q);
-            T[3 * N + i] = h_shoup(T[2 * N + i], q);
         }
         ModConst &k = mc[m];
         memset(&k, 0, sizeof k);

@@ -29,58 +29,66 @@ __device__ __forceinline__ uint64_t reduce4q(uint64_t x, uint64_t q) {
 }
 
 // Four CT stages lm = LM0..LM0+3 on x[j] with global index e0 + j*estride.
-template <int LOGN, int LM0>
-__device__ __forceinline__ void phase_ct(uint64_t (&x)[16], uint32_t e0, uint32_t estride, const uint64_t *__restrict__ W,
-                                         const uint64_t *__restrict__ Wp, uint64_t q) {
+// In stage s (j-distance d = 8>>s) the butterflies of each run of 2d
+// consecutive j share one twiddle, index (1<<lm) + (e0 >> (LOGN-lm)) + run:
+// every call site keeps e0 mod 2t below the element stride, so a phase needs
+// 1+2+4+8 = 15 twiddle pairs, each one 16-byte load.
+template <int LOGN, int LM, int D>
+__device__ __forceinline__ void stage_ct(uint64_t (&x)[16], uint32_t e0, const ulonglong2 *__restrict__ W2, uint64_t q) {
     const uint64_t q2 = 2 * q;
+    const uint32_t base = (1u << LM) + (e0 >> (LOGN - LM));
 #pragma unroll
-    for (int s = 0; s < 4; s++) {
-        const int lm = LM0 + s;
-        const int d = 8 >> s;
+    for (int k = 0; k < 8 / D; k++) {
+        const ulonglong2 tw = __ldg(W2 + base + k);
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-            if (j & d) continue;
-            uint32_t e = e0 + (uint32_t)j * estride;
-            uint32_t idx = (1u << lm) + (e >> (LOGN - lm));
-            uint64_t w = __ldg(W + idx), wp = __ldg(Wp + idx);
-            uint64_t u = x[j];
+        for (int jj = 0; jj < D; jj++) {
+            uint64_t u = x[2 * D * k + jj];
             u = u >= q2 ? u - q2 : u;
-            uint64_t v = shoup_lazy(x[j + d], w, wp, q);
-            x[j] = u + v;
-            x[j + d] = u - v + q2;
+            const uint64_t v = shoup_lazy(x[2 * D * k + jj + D], tw.x, tw.y, q);
+            x[2 * D * k + jj] = u + v;
+            x[2 * D * k + jj + D] = u - v + q2;
         }
     }
 }
+template <int LOGN, int LM0>
+__device__ __forceinline__ void phase_ct(uint64_t (&x)[16], uint32_t e0, const ulonglong2 *__restrict__ W2, uint64_t q) {
+    stage_ct<LOGN, LM0, 8>(x, e0, W2, q);
+    stage_ct<LOGN, LM0 + 1, 4>(x, e0, W2, q);
+    stage_ct<LOGN, LM0 + 2, 2>(x, e0, W2, q);
+    stage_ct<LOGN, LM0 + 3, 1>(x, e0, W2, q);
+}
 
-// Four GS stages lt = LT0..LT0+3 (element distance 2^lt).
-template <int LOGN, int LT0>
-__device__ __forceinline__ void phase_gs(uint64_t (&x)[16], uint32_t e0, uint32_t estride, const uint64_t *__restrict__ W,
-                                         const uint64_t *__restrict__ Wp, uint64_t q) {
+// Four GS stages lt = LT0..LT0+3 (element distance 2^lt), same twiddle sharing.
+template <int LOGN, int LT, int D>
+__device__ __forceinline__ void stage_gs(uint64_t (&x)[16], uint32_t e0, const ulonglong2 *__restrict__ W2, uint64_t q) {
     const uint64_t q2 = 2 * q;
+    const uint32_t base = (1u << (LOGN - 1 - LT)) + (e0 >> (LT + 1));
 #pragma unroll
-    for (int s = 0; s < 4; s++) {
-        const int lt = LT0 + s;
-        const int d = 1 << s;
+    for (int k = 0; k < 8 / D; k++) {
+        const ulonglong2 tw = __ldg(W2 + base + k);
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-            if (j & d) continue;
-            uint32_t e = e0 + (uint32_t)j * estride;
-            uint32_t idx = (1u << (LOGN - 1 - lt)) + (e >> (lt + 1));
-            uint64_t w = __ldg(W + idx), wp = __ldg(Wp + idx);
-            uint64_t u = x[j], v = x[j + d];
+        for (int jj = 0; jj < D; jj++) {
+            const uint64_t u = x[2 * D * k + jj], v = x[2 * D * k + jj + D];
             uint64_t sm = u + v;
             sm = sm >= q2 ? sm - q2 : sm;
-            x[j] = sm;
-            x[j + d] = shoup_lazy(u - v + q2, w, wp, q);
+            x[2 * D * k + jj] = sm;
+            x[2 * D * k + jj + D] = shoup_lazy(u - v + q2, tw.x, tw.y, q);
         }
     }
+}
+template <int LOGN, int LT0>
+__device__ __forceinline__ void phase_gs(uint64_t (&x)[16], uint32_t e0, const ulonglong2 *__restrict__ W2, uint64_t q) {
+    stage_gs<LOGN, LT0, 1>(x, e0, W2, q);
+    stage_gs<LOGN, LT0 + 1, 2>(x, e0, W2, q);
+    stage_gs<LOGN, LT0 + 2, 4>(x, e0, W2, q);
+    stage_gs<LOGN, LT0 + 3, 8>(x, e0, W2, q);
 }
 
 __device__ __forceinline__ int pad16(int e) { return e + (e >> 4); }
 
 struct PolyInfo {
     uint64_t *p;
-    const uint64_t *W, *Wp;
+    const ulonglong2 *W2;  // (twiddle, Shoup) pairs
     uint64_t q;
     const ModConst *mc;
 };
@@ -98,8 +106,7 @@ __device__ __forceinline__ bool poly_info(PolyInfo &pi, PolySrc src, size_t poly
     if (m == 0xFF) return false;
     size_t N = (size_t)1 << logN;
     pi.p = src.ptrs ? src.ptrs[poly / per] + (poly % per) * N : src.data + poly * N;
-    pi.W = tw + (size_t)m * 4 * N + (inverse ? 2 * N : 0);
-    pi.Wp = pi.W + N;
+    pi.W2 = (const ulonglong2 *)(tw + (size_t)m * 4 * N + (inverse ? 2 * N : 0));
     pi.q = mc[m].q;
     pi.mc = mc + m;
     return true;
@@ -117,13 +124,13 @@ __global__ void __launch_bounds__(TPB) k_fwd16_cols(PolySrc data, const uint8_t 
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = pi.p[(g + 16 * j) * 256 + col];
-    phase_ct<16, 0>(x, col + 256 * g, 4096, pi.W, pi.Wp, pi.q);
+    phase_ct<16, 0>(x, col + 256 * g, pi.W2, pi.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) sm[(g + 16 * j) * 16 + lc] = x[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = sm[(16 * g + j) * 16 + lc];
-    phase_ct<16, 4>(x, col + 4096 * g, 256, pi.W, pi.Wp, pi.q);
+    phase_ct<16, 4>(x, col + 4096 * g, pi.W2, pi.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) pi.p[(16 * g + j) * 256 + col] = x[j];  // lazy [0,4q) between passes
 }
@@ -140,14 +147,14 @@ __global__ void __launch_bounds__(TPB) k_fwd16_rows(PolySrc data, const uint8_t 
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
-    phase_ct<16, 8>(x, r * 256 + g, 16, pi.W, pi.Wp, pi.q);
+    phase_ct<16, 8>(x, r * 256 + g, pi.W2, pi.q);
     uint64_t *s = sm + rl * 272;
 #pragma unroll
     for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = x[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
-    phase_ct<16, 12>(x, r * 256 + 16 * g, 1, pi.W, pi.Wp, pi.q);
+    phase_ct<16, 12>(x, r * 256 + 16 * g, pi.W2, pi.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], pi.q);
     __syncthreads();
@@ -171,13 +178,13 @@ __global__ void __launch_bounds__(TPB) k_inv16_rows(PolySrc data, const uint8_t 
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
-    phase_gs<16, 0>(x, r * 256 + 16 * g, 1, pi.W, pi.Wp, pi.q);
+    phase_gs<16, 0>(x, r * 256 + 16 * g, pi.W2, pi.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = x[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
-    phase_gs<16, 4>(x, r * 256 + g, 16, pi.W, pi.Wp, pi.q);
+    phase_gs<16, 4>(x, r * 256 + g, pi.W2, pi.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) row[g + 16 * j] = x[j];  // lazy [0,2q)
 }
@@ -193,13 +200,13 @@ __global__ void __launch_bounds__(TPB) k_inv16_cols(PolySrc data, const uint8_t 
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = pi.p[(16 * g + j) * 256 + col];
-    phase_gs<16, 8>(x, col + 4096 * g, 256, pi.W, pi.Wp, pi.q);
+    phase_gs<16, 8>(x, col + 4096 * g, pi.W2, pi.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) sm[(16 * g + j) * 16 + lc] = x[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = sm[(g + 16 * j) * 16 + lc];
-    phase_gs<16, 12>(x, col + 256 * g, 4096, pi.W, pi.Wp, pi.q);
+    phase_gs<16, 12>(x, col + 256 * g, pi.W2, pi.q);
     const uint64_t ni = pi.mc->ninv, nip = pi.mc->ninv_sh;
 #pragma unroll
     for (int j = 0; j < 16; j++) pi.p[(g + 16 * j) * 256 + col] = shoup(x[j], ni, nip, pi.q);
@@ -215,21 +222,21 @@ __global__ void __launch_bounds__(TPB) k_fwd12(PolySrc data, const uint8_t *mod_
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = pi.p[g + 256 * j];
-    phase_ct<12, 0>(x, g, 256, pi.W, pi.Wp, pi.q);
+    phase_ct<12, 0>(x, g, pi.W2, pi.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) sm[pad16(g + 256 * j)] = x[j];
     __syncthreads();
     const uint32_t e1 = (g & 15) + 256 * (g >> 4);
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = sm[pad16(e1 + 16 * j)];
-    phase_ct<12, 4>(x, e1, 16, pi.W, pi.Wp, pi.q);
+    phase_ct<12, 4>(x, e1, pi.W2, pi.q);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) sm[pad16(e1 + 16 * j)] = x[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = sm[pad16(16 * g + j)];
-    phase_ct<12, 8>(x, 16 * g, 1, pi.W, pi.Wp, pi.q);
+    phase_ct<12, 8>(x, 16 * g, pi.W2, pi.q);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) sm[pad16(16 * g + j)] = reduce4q(x[j], pi.q);
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(TPB) k_inv12(PolySrc data, const uint8_t *mod_
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = sm[pad16(16 * g + j)];
-    phase_gs<12, 0>(x, 16 * g, 1, pi.W, pi.Wp, pi.q);
+    phase_gs<12, 0>(x, 16 * g, pi.W2, pi.q);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) sm[pad16(16 * g + j)] = x[j];
@@ -258,14 +265,14 @@ __global__ void __launch_bounds__(TPB) k_inv12(PolySrc data, const uint8_t *mod_
     const uint32_t e1 = (g & 15) + 256 * (g >> 4);
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = sm[pad16(e1 + 16 * j)];
-    phase_gs<12, 4>(x, e1, 16, pi.W, pi.Wp, pi.q);
+    phase_gs<12, 4>(x, e1, pi.W2, pi.q);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) sm[pad16(e1 + 16 * j)] = x[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = sm[pad16(g + 256 * j)];
-    phase_gs<12, 8>(x, g, 256, pi.W, pi.Wp, pi.q);
+    phase_gs<12, 8>(x, g, pi.W2, pi.q);
     const uint64_t ni = pi.mc->ninv, nip = pi.mc->ninv_sh;
 #pragma unroll
     for (int j = 0; j < 16; j++) pi.p[g + 256 * j] = shoup(x[j], ni, nip, pi.q);
@@ -288,8 +295,8 @@ __global__ void k_ntt_generic(PolySrc data, const uint8_t *mod_map, int per, con
             int t = half >> lm;
             for (int b = threadIdx.x; b < half; b += blockDim.x) {
                 int i = b / t, j = 2 * i * t + (b % t);
-                uint64_t w = pi.W[(1 << lm) + i], wp = pi.Wp[(1 << lm) + i];
-                uint64_t u = sg[j], v = shoup(sg[j + t], w, wp, q);
+                const ulonglong2 tw = pi.W2[(1 << lm) + i];
+                uint64_t u = sg[j], v = shoup(sg[j + t], tw.x, tw.y, q);
                 sg[j] = add_mod(u, v, q);
                 sg[j + t] = sub_mod(u, v, q);
             }
@@ -303,7 +310,7 @@ __global__ void k_ntt_generic(PolySrc data, const uint8_t *mod_map, int per, con
                 int idx = (N >> (lt + 1)) + i;
                 uint64_t u = sg[j], v = sg[j + t];
                 sg[j] = add_mod(u, v, q);
-                sg[j + t] = shoup(sub_mod(u, v, q), pi.W[idx], pi.Wp[idx], q);
+                sg[j + t] = shoup(sub_mod(u, v, q), pi.W2[idx].x, pi.W2[idx].y, q);
             }
             __syncthreads();
         }
