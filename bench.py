@@ -28,6 +28,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# torch and libhe_sm100.so share one stream-ordered pool (see package __init__)
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "backend:cudaMallocAsync")
 
 METRIC = "amortised encrypted samples/sec"
 SAMPLES_PER_GROUP = 32768

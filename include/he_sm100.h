@@ -111,7 +111,7 @@ int he_add(he_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint
 int he_sub(he_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out,
            int count, int ell, int n_comp, void *stream);
 int he_add_const(he_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int ell,
-                 const uint64_t *residues, void *stream);
+                 int n_comp, const uint64_t *residues, void *stream);
 int he_mul_const(he_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int ell,
                  int n_comp, const uint64_t *residues, void *stream);
 int he_mul_plain(he_ctx *ctx, const uint64_t *const *in, const uint64_t *pt, uint64_t *const *out,

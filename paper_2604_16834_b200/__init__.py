@@ -7,7 +7,18 @@ Drop-in for the hot path of the reference package ``hebatch``: the same
 simulation.  See DESIGN.md.
 """
 
-from .errors import HebatchError  # noqa: F401
+import os as _os
+import sys as _sys
+
+# Ciphertext tensors come from torch; kernel scratch comes from cudaMallocAsync
+# inside libhe_sm100.so.  Both must draw on the SAME stream-ordered pool, or
+# memory freed by one is invisible to the other (config 3 peaks at ~135 GB).
+# torch fixes its allocator backend when it is imported, so this only takes
+# effect if the package is imported first (bench.py / conftest set it too).
+if "torch" not in _sys.modules:
+    _os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "backend:cudaMallocAsync")
+
+from .errors import HebatchError  # noqa: E402,F401
 
 __version__ = "0.1.0"
 

@@ -88,7 +88,7 @@ def load():
         "he_encode_plain": (i, [vp, vp, i, dbl, i, vp, vp]),
         "he_add": (i, [vp, pp, pp, pp, i, i, i, vp]),
         "he_sub": (i, [vp, pp, pp, pp, i, i, i, vp]),
-        "he_add_const": (i, [vp, pp, pp, i, i, vp, vp]),
+        "he_add_const": (i, [vp, pp, pp, i, i, i, vp, vp]),
         "he_mul_const": (i, [vp, pp, pp, i, i, i, vp, vp]),
         "he_mul_plain": (i, [vp, pp, vp, pp, i, i, i, vp]),
         "he_drop_limbs": (i, [vp, pp, pp, i, i, i, i, vp]),

@@ -40,6 +40,8 @@ __device__ __forceinline__ uint64_t reduce64(uint64_t x, const ModConst &mc) {
 // Per-(level, digit) ModUp table and per-level ModDown table, device resident.
 struct BconvTable {
     int n_src, n_dst;
+    std::vector<uint64_t> h_qhinv;  // host copy: qhat_s^-1 mod q_s
+    std::vector<int> h_dst_mod;     // host copy: target modulus indices
     uint64_t *d;        // [n_src] qhat_inv, [n_src] Shoup(qhat_inv), [n_src][n_dst] qhat mod dst (Montgomery form)
     int32_t *d_src_mod; // [n_src] modulus index of each source
     int32_t *d_dst_mod; // [n_dst] modulus index of each target
@@ -62,8 +64,20 @@ struct he_ctx {
     std::vector<uint64_t> h_pmodq, h_pinv;          // P mod q_i, P^-1 mod q_i (i < L)
     uint64_t *d_pinv = nullptr;                     // [L] P^-1 mod q_i and Shoup  ([L][2])
     uint64_t *d_qlinv = nullptr;                    // [L][L][2] q_l^-1 mod q_i, Shoup
+    std::vector<uint64_t> h_qlinv;                  // host copy of d_qlinv
+    std::vector<uint64_t> h_ninv;                   // N^-1 mod every modulus
     std::mutex mu;
 };
+
+// host-side modular helpers (context.cu)
+uint64_t he_h_mulmod(uint64_t a, uint64_t b, uint64_t q);
+uint64_t he_h_shoup(uint64_t w, uint64_t q);
+// fused N = 2^16 key switching / rescale (fused.cu); pointer lists are HOST arrays
+int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d, const uint64_t *const *d_dev, int B,
+                       int ell, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *const *add0,
+                       const uint64_t *const *add1, cudaStream_t s);
+int he_rescale_fused(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, int B, int ell, int nc,
+                     cudaStream_t s);
 
 // ---------------------------------------------------------------- errors
 

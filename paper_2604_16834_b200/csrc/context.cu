@@ -43,6 +43,8 @@ static uint64_t h_pow(uint64_t a, uint64_t e, uint64_t q) {
 }
 static uint64_t h_inv(uint64_t a, uint64_t q) { return h_pow(a % q, q - 2, q); }
 static uint64_t h_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((hu128)w << 64) / q); }
+uint64_t he_h_mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)((hu128)a * b % q); }
+uint64_t he_h_shoup(uint64_t w, uint64_t q) { return h_shoup(w, q); }
 static uint64_t h_mont(uint64_t w, uint64_t q) { return (uint64_t)(((hu128)(w % q) << 64) % q); }
 static bool h_is_prime(uint64_t n) {
     static const uint64_t B[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
@@ -218,6 +220,7 @@ static int build_tables(he_ctx *c) {
         k.qinv = inv;
         k.r2 = (uint64_t)(((hu128)h_mont(1, q) << 64) % q);  // R^2 mod q
         k.ninv = h_inv((uint64_t)N % q, q);
+        c->h_ninv.push_back(k.ninv);
         k.ninv_sh = h_shoup(k.ninv, q);
         k.ratio = UINT64_MAX / q;
     }
@@ -233,6 +236,7 @@ static int build_tables(he_ctx *c) {
             qlinv[((size_t)l * c->L + i) * 2] = v;
             qlinv[((size_t)l * c->L + i) * 2 + 1] = h_shoup(v, c->mod[i]);
         }
+    c->h_qlinv = qlinv;
     HE_CHECK_CUDA(cudaMalloc(&c->d_qlinv, qlinv.size() * 8));
     HE_CHECK_CUDA(cudaMemcpy(c->d_qlinv, qlinv.data(), qlinv.size() * 8, cudaMemcpyHostToDevice));
     c->h_pmodq.assign(c->L, 0);
@@ -392,6 +396,8 @@ static int make_table(he_ctx *c, const std::vector<int> &src, const std::vector<
     }
     t.n_src = ns;
     t.n_dst = nd;
+    t.h_qhinv.assign(h.begin(), h.begin() + ns);
+    t.h_dst_mod = dst;
     HE_CHECK_CUDA(cudaMalloc(&t.d, h.size() * 8));
     HE_CHECK_CUDA(cudaMemcpy(t.d, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
     HE_CHECK_CUDA(cudaMalloc(&t.d_src_mod, 4 * ns));

@@ -1,0 +1,477 @@
+// fused.cu -- key switching and rescale with their conversions fused into the
+// NTT passes (N = 2^16).
+//
+// Unfused, one hybrid key switch at level l streams every intermediate
+// through HBM: INTT(d) -> BConv -> NTT -> inner product -> INTT(P) -> BConv ->
+// NTT -> subtract/scale.  Here each NTT pass is driven by a per-polynomial job
+// descriptor whose loader/epilogue absorbs the neighbouring element-wise step:
+//
+//   INTT of d       pass 2 multiplies by N^-1 * qhat_s^-1   (ModUp's Shoup step)
+//   ModUp NTT       pass 1 loads sum_s v_s * qhat_s (BConv, Montgomery REDC)
+//   ModUp NTT pass 2 + key inner product: one kernel per (ct, target limb)
+//                   runs pass 2 of every digit and accumulates e_j * key_j
+//                   in registers -- the extended digits never return to HBM
+//   INTT of P limbs pass 2 multiplies by N^-1 * phat_k^-1
+//   ModDown NTT     pass 1 loads the P->Q BConv, pass 2 writes
+//                   (acc - conv) * P^-1 (+ d0/d1 for relinearisation)
+//   rescale         INTT(last limb); pass 1 loads the centred lift into each
+//                   q_i; pass 2 writes (x_i - t_i) * q_l^-1
+//
+// Every stage computes exactly the values of the unfused definition
+// (oracle/ckks_oracle.c), so results stay bit-exact.
+#include <algorithm>
+#include <vector>
+
+#include "ntt_core.cuh"
+
+namespace {
+
+constexpr int LOGN = 16;
+constexpr size_t NN = (size_t)1 << LOGN;
+
+struct Job {
+    const uint64_t *src;  // pass-1 input: direct poly / first BConv source limb / centred source
+    uint64_t *dst;        // pass-1 output (and pass-2 in-place buffer)
+    uint64_t *out;        // pass-2 epilogue destination
+    const uint64_t *aux;  // epilogue operand (acc limb / rescale input limb)
+    const uint64_t *add;  // epilogue addend (relin d0/d1 limb) or nullptr
+    const uint64_t *tab;  // BConv Montgomery constants [ns]
+    uint64_t cw, cwp;     // Shoup constant: inverse final scale / epilogue scale
+    uint64_t ql;          // centred-lift source modulus
+    int32_t mod;          // modulus index of this polynomial
+    int32_t ns;           // BConv source count
+};
+
+enum { L_DIRECT = 0, L_BCONV = 1, L_CENTER = 2 };
+enum { E_STORE = 0, E_SUBSCALE = 1 };
+
+// ---------------------------------------------------------------- forward pass 1 (columns)
+template <int LD>
+__global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs, const uint64_t *tw,
+                                                  const ModConst *mc) {
+    __shared__ uint64_t sm[256 * 16];
+    const Job jb = jobs[blockIdx.x >> 4];
+    const ModConst c = mc[jb.mod];
+    const ulonglong2 *W2 = tw_fwd(tw, jb.mod, LOGN);
+    const int tid = threadIdx.x, lc = tid & 15, g = tid >> 4;
+    const uint32_t col = (blockIdx.x & 15) * 16 + lc;
+    uint64_t x[16];
+    if (LD == L_DIRECT) {
+#pragma unroll
+        for (int j = 0; j < 16; j++) x[j] = jb.src[(g + 16 * j) * 256 + col];
+    } else if (LD == L_BCONV) {
+        uint64_t t[8];
+#pragma unroll
+        for (int s = 0; s < 8; s++) t[s] = s < jb.ns ? jb.tab[s] : 0;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const size_t idx = (g + 16 * j) * 256 + col;
+            u128 acc = {0, 0};
+#pragma unroll
+            for (int s = 0; s < 8; s++) {
+                if (s < jb.ns) {
+                    mac128(acc, jb.src[(size_t)s * NN + idx], t[s]);  // v_s < 2^61, t < q: hi < q kept by fold
+                    if (acc.hi >= c.q) acc.hi -= c.q;
+                }
+            }
+            x[j] = redc(acc.hi, acc.lo, c.q, c.qinv);
+        }
+    } else {
+        const uint64_t half = (jb.ql - 1) >> 1;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const uint64_t v = jb.src[(g + 16 * j) * 256 + col];
+            x[j] = v > half ? sub_mod(0, reduce64(jb.ql - v, c), c.q) : reduce64(v, c);
+        }
+    }
+    phase_ct<16, 0>(x, col + 256 * g, W2, c.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[(g + 16 * j) * 16 + lc] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[(16 * g + j) * 16 + lc];
+    phase_ct<16, 4>(x, col + 4096 * g, W2, c.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) jb.dst[(16 * g + j) * 256 + col] = x[j];  // lazy [0, 4q)
+}
+
+// ---------------------------------------------------------------- forward pass 2 (rows)
+template <int EP>
+__global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs, const uint64_t *tw,
+                                                  const ModConst *mc) {
+    __shared__ uint64_t sm[16 * 272];
+    const Job jb = jobs[blockIdx.x >> 4];
+    const ModConst c = mc[jb.mod];
+    const ulonglong2 *W2 = tw_fwd(tw, jb.mod, LOGN);
+    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+    const uint32_t r = (blockIdx.x & 15) * 16 + rl;
+    uint64_t *row = jb.dst + r * 256;
+    uint64_t x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
+    phase_ct<16, 8>(x, r * 256 + g, W2, c.q);
+    uint64_t *s = sm + rl * 272;
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = x[j];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
+    phase_ct<16, 12>(x, r * 256 + 16 * g, W2, c.q);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], c.q);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        const int cc = g + 16 * j;
+        const uint64_t v = s[pad16(cc)];
+        if (EP == E_STORE) {
+            row[cc] = v;
+        } else {
+            const size_t idx = r * 256 + cc;
+            uint64_t y = shoup(sub_mod(jb.aux[idx], v, c.q), jb.cw, jb.cwp, c.q);
+            if (jb.add) y = add_mod(y, jb.add[idx], c.q);
+            jb.out[idx] = y;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- inverse passes
+// pass 1 (rows): reads src, writes dst (may alias), GS stages 0..7, lazy [0, 2q)
+__global__ void __launch_bounds__(NTT_TPB) ki_rows(const Job *__restrict__ jobs, const uint64_t *tw,
+                                                  const ModConst *mc) {
+    __shared__ uint64_t sm[16 * 272];
+    const Job jb = jobs[blockIdx.x >> 4];
+    const ModConst c = mc[jb.mod];
+    const ulonglong2 *W2 = tw_inv(tw, jb.mod, LOGN);
+    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+    const uint32_t r = (blockIdx.x & 15) * 16 + rl;
+    const uint64_t *in = jb.src + r * 256;
+    uint64_t *s = sm + rl * 272;
+    uint64_t x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = in[g + 16 * j];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
+    phase_gs<16, 0>(x, r * 256 + 16 * g, W2, c.q);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = x[j];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
+    phase_gs<16, 4>(x, r * 256 + g, W2, c.q);
+    uint64_t *out = jb.dst + r * 256;
+#pragma unroll
+    for (int j = 0; j < 16; j++) out[g + 16 * j] = x[j];
+}
+
+// pass 2 (columns): in place on dst, GS stages 8..15, times (cw, cwp) = N^-1 * extra
+__global__ void __launch_bounds__(NTT_TPB) ki_cols(const Job *__restrict__ jobs, const uint64_t *tw,
+                                                  const ModConst *mc) {
+    __shared__ uint64_t sm[256 * 16];
+    const Job jb = jobs[blockIdx.x >> 4];
+    const ModConst c = mc[jb.mod];
+    const ulonglong2 *W2 = tw_inv(tw, jb.mod, LOGN);
+    const int tid = threadIdx.x, lc = tid & 15, g = tid >> 4;
+    const uint32_t col = (blockIdx.x & 15) * 16 + lc;
+    uint64_t x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = jb.dst[(16 * g + j) * 256 + col];
+    phase_gs<16, 8>(x, col + 4096 * g, W2, c.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[(16 * g + j) * 16 + lc] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[(g + 16 * j) * 16 + lc];
+    phase_gs<16, 12>(x, col + 256 * g, W2, c.q);
+#pragma unroll
+    for (int j = 0; j < 16; j++) jb.dst[(g + 16 * j) * 256 + col] = shoup(x[j], jb.cw, jb.cwp, c.q);
+}
+
+// ---------------------------------------------------------------- ModUp pass 2 + inner product
+struct IpArgs {
+    const uint64_t *ext;  // [B][beta][ext_n][N] ModUp pass-1 outputs (lazy)
+    const uint64_t *const *d;  // [B] device pointers to d (NTT domain, [ell][N])
+    const uint64_t *key;  // [dnum][2][M][N] Montgomery form
+    uint64_t *acc;        // [B][2][ext_n][N]
+    const uint64_t *tw;
+    const ModConst *mc;
+    int ell, ext_n, beta, alpha, L, M;
+};
+
+__global__ void __launch_bounds__(NTT_TPB) k_modup_ip(const IpArgs a) {
+    __shared__ uint64_t sm[16 * 272];
+    const int rt = blockIdx.x & 15, bt = blockIdx.x >> 4;
+    const int t = bt % a.ext_n, b = bt / a.ext_n;
+    const int m = t < a.ell ? t : a.L + (t - a.ell);
+    const ModConst c = a.mc[m];
+    const ulonglong2 *W2 = tw_fwd(a.tw, m, LOGN);
+    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+    const uint32_t r = rt * 16 + rl;
+    const int jt = t < a.ell ? t / a.alpha : -1;
+    uint64_t *s = sm + rl * 272;
+    uint64_t acc0[16], acc1[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) acc0[j] = acc1[j] = 0;
+    for (int dj = 0; dj < a.beta; dj++) {
+        uint64_t x[16];
+        if (dj == jt) {
+            const uint64_t *dp = a.d[b] + (size_t)t * NN + r * 256;
+#pragma unroll
+            for (int j = 0; j < 16; j++) x[j] = dp[g + 16 * j];
+        } else {
+            const uint64_t *row = a.ext + ((((size_t)b * a.beta + dj) * a.ext_n + t) << LOGN) + r * 256;
+#pragma unroll
+            for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
+            phase_ct<16, 8>(x, r * 256 + g, W2, c.q);
+#pragma unroll
+            for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = x[j];
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
+            phase_ct<16, 12>(x, r * 256 + 16 * g, W2, c.q);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], c.q);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
+            __syncwarp();
+        }
+        const uint64_t *k0 = a.key + (((size_t)dj * 2 * a.M + m) << LOGN) + r * 256;
+        const uint64_t *k1 = k0 + ((size_t)a.M << LOGN);
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const int cc = g + 16 * j;
+            const uint64_t w0 = __ldg(k0 + cc), w1 = __ldg(k1 + cc);
+            acc0[j] = add_mod(acc0[j], redc(mulhi(x[j], w0), x[j] * w0, c.q, c.qinv), c.q);
+            acc1[j] = add_mod(acc1[j], redc(mulhi(x[j], w1), x[j] * w1, c.q, c.qinv), c.q);
+        }
+    }
+    uint64_t *o0 = a.acc + ((((size_t)b * 2) * a.ext_n + t) << LOGN) + r * 256;
+    uint64_t *o1 = o0 + ((size_t)a.ext_n << LOGN);
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        o0[g + 16 * j] = acc0[j];
+        o1[g + 16 * j] = acc1[j];
+    }
+}
+
+// ---------------------------------------------------------------- host plumbing
+struct JobBuf {
+    Job *d = nullptr;
+    cudaStream_t s;
+    explicit JobBuf(cudaStream_t st) : s(st) {}
+    ~JobBuf() { he_scratch_free(d, s); }
+    int up(const std::vector<Job> &v) {
+        HE_TRY(he_scratch_alloc((void **)&d, v.size() * sizeof(Job), s));
+        HE_CHECK_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(Job), cudaMemcpyHostToDevice, s));
+        return HE_OK;
+    }
+};
+
+int run_inverse(he_ctx *c, const std::vector<Job> &jobs, cudaStream_t s) {
+    if (jobs.empty()) return HE_OK;
+    JobBuf jb(s);
+    HE_TRY(jb.up(jobs));
+    unsigned g = (unsigned)jobs.size() * 16;
+    ki_rows<<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+    HE_CHECK_LAUNCH();
+    ki_cols<<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+template <int LD, int EP>
+int run_forward(he_ctx *c, const std::vector<Job> &jobs, cudaStream_t s) {
+    if (jobs.empty()) return HE_OK;
+    JobBuf jb(s);
+    HE_TRY(jb.up(jobs));
+    unsigned g = (unsigned)jobs.size() * 16;
+    kf_cols<LD><<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+    HE_CHECK_LAUNCH();
+    kf_rows<EP><<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+Job blank() {
+    Job j;
+    memset(&j, 0, sizeof j);
+    return j;
+}
+
+}  // namespace
+
+// Fused hybrid key switch for B ciphertexts (N = 2^16).  Pointer arguments are
+// HOST arrays of device addresses; d_dev is the same list of d pointers in
+// device memory (read by the inner-product kernel).
+int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d, const uint64_t *const *d_dev, int B,
+                       int ell, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *const *add0,
+                       const uint64_t *const *add1, cudaStream_t s) {
+    const int L = c->L, K = c->K, alpha = c->alpha, M = L + K;
+    const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
+    const size_t w_dc = (size_t)B * ell * NN, w_ext = (size_t)B * beta * ext_n * NN, w_acc = (size_t)B * 2 * ext_n * NN,
+                 w_md = (size_t)B * 2 * ell * NN;
+    void *scr = nullptr;
+    HE_TRY(he_scratch_alloc(&scr, (w_dc + w_ext + w_acc + w_md) * 8, s));
+    uint64_t *dcv = (uint64_t *)scr, *ext = dcv + w_dc, *acc = ext + w_ext, *md = acc + w_acc;
+    int rc = HE_OK;
+    std::vector<const BconvTable *> up(beta);
+    for (int j = 0; j < beta && rc == HE_OK; j++) rc = he_get_modup_table(c, ell, j, &up[j]);
+    const BconvTable *dn = nullptr;
+    if (rc == HE_OK) rc = he_get_moddown_table(c, ell, &dn);
+    // 1. v = INTT(d) * qhat_s^-1 (ModUp's per-source Shoup step folded into INTT's N^-1)
+    if (rc == HE_OK) {
+        std::vector<Job> jobs;
+        for (int b = 0; b < B; b++)
+            for (int i = 0; i < ell; i++) {
+                Job j = blank();
+                j.src = d[b] + (size_t)i * NN;
+                j.dst = dcv + ((size_t)b * ell + i) * NN;
+                j.mod = i;
+                const int dj = i / alpha, si = i - dj * alpha;
+                j.cw = he_h_mulmod(c->h_ninv[i], up[dj]->h_qhinv[si], c->mod[i]);
+                j.cwp = he_h_shoup(j.cw, c->mod[i]);
+                jobs.push_back(j);
+            }
+        rc = run_inverse(c, jobs, s);
+    }
+    // 2. ModUp pass 1: BConv loaded straight into the NTT of every target limb
+    if (rc == HE_OK) {
+        std::vector<Job> jobs;
+        for (int b = 0; b < B; b++)
+            for (int dj = 0; dj < beta; dj++) {
+                const BconvTable *tb = up[dj];
+                const int s0 = dj * alpha, ns = tb->n_src;
+                for (int dst = 0; dst < tb->n_dst; dst++) {
+                    const int m = tb->h_dst_mod[dst];
+                    const int t = m < L ? m : ell + (m - L);
+                    Job j = blank();
+                    j.src = dcv + ((size_t)b * ell + s0) * NN;
+                    j.ns = ns;
+                    j.tab = tb->d + 2 * ns + (size_t)dst * ns;
+                    j.mod = m;
+                    j.dst = ext + (((size_t)b * beta + dj) * ext_n + t) * NN;
+                    jobs.push_back(j);
+                }
+            }
+        if (!jobs.empty()) {
+            JobBuf jb(s);
+            rc = jb.up(jobs);
+            if (rc == HE_OK) {
+                kf_cols<L_BCONV><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+                he_count_launch(1);
+                if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+            }
+        }
+    }
+    // 3. ModUp pass 2 fused with the key inner product
+    if (rc == HE_OK) {
+        IpArgs a;
+        a.ext = ext;
+        a.d = d_dev;
+        a.key = key;
+        a.acc = acc;
+        a.tw = c->d_tw;
+        a.mc = c->d_mc;
+        a.ell = ell;
+        a.ext_n = ext_n;
+        a.beta = beta;
+        a.alpha = alpha;
+        a.L = L;
+        a.M = M;
+        k_modup_ip<<<(unsigned)(B * ext_n * 16), NTT_TPB, 0, s>>>(a);
+        he_count_launch(1);
+        if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+    }
+    // 4. ModDown: INTT of the P limbs (times N^-1 * phat_k^-1), then the P->Q
+    //    BConv NTT whose epilogue writes (acc - conv) * P^-1 (+ d0 / d1)
+    if (rc == HE_OK) {
+        std::vector<Job> jobs;
+        for (int b = 0; b < B; b++)
+            for (int cc = 0; cc < 2; cc++)
+                for (int k = 0; k < K; k++) {
+                    Job j = blank();
+                    j.src = j.dst = acc + (((size_t)b * 2 + cc) * ext_n + ell + k) * NN;
+                    j.mod = L + k;
+                    j.cw = he_h_mulmod(c->h_ninv[L + k], dn->h_qhinv[k], c->mod[L + k]);
+                    j.cwp = he_h_shoup(j.cw, c->mod[L + k]);
+                    jobs.push_back(j);
+                }
+        rc = run_inverse(c, jobs, s);
+    }
+    if (rc == HE_OK) {
+        std::vector<Job> jobs;
+        for (int b = 0; b < B; b++)
+            for (int cc = 0; cc < 2; cc++) {
+                const uint64_t *const *addv = cc == 0 ? add0 : add1;
+                uint64_t *const *outv = cc == 0 ? out0 : out1;
+                for (int i = 0; i < ell; i++) {
+                    Job j = blank();
+                    j.src = acc + (((size_t)b * 2 + cc) * ext_n + ell) * NN;
+                    j.ns = K;
+                    j.tab = dn->d + 2 * K + (size_t)i * K;
+                    j.mod = i;
+                    j.dst = md + (((size_t)b * 2 + cc) * ell + i) * NN;
+                    j.aux = acc + (((size_t)b * 2 + cc) * ext_n + i) * NN;
+                    j.add = addv ? addv[b] + (size_t)i * NN : nullptr;
+                    j.out = outv[b] + (size_t)i * NN;
+                    j.cw = c->h_pinv[2 * i];
+                    j.cwp = c->h_pinv[2 * i + 1];
+                    jobs.push_back(j);
+                }
+            }
+        rc = run_forward<L_BCONV, E_SUBSCALE>(c, jobs, s);
+    }
+    he_scratch_free(scr, s);
+    return rc;
+}
+
+// Fused rescale for B ciphertexts of nc components at ell limbs (N = 2^16).
+// in / out: HOST arrays of device addresses ([nc][ell][N] -> [nc][ell-1][N]).
+int he_rescale_fused(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, int B, int ell, int nc,
+                     cudaStream_t s) {
+    const int lm1 = ell - 1;
+    const size_t npc = (size_t)B * nc;
+    void *scr = nullptr;
+    HE_TRY(he_scratch_alloc(&scr, (npc + npc * lm1) * NN * 8, s));
+    uint64_t *r = (uint64_t *)scr, *tmp = r + npc * NN;
+    int rc = HE_OK;
+    {
+        std::vector<Job> jobs;
+        for (int b = 0; b < B; b++)
+            for (int cc = 0; cc < nc; cc++) {
+                Job j = blank();
+                j.src = in[b] + ((size_t)cc * ell + lm1) * NN;
+                j.dst = r + ((size_t)b * nc + cc) * NN;
+                j.mod = lm1;
+                j.cw = c->h_ninv[lm1];
+                j.cwp = he_h_shoup(j.cw, c->mod[lm1]);
+                jobs.push_back(j);
+            }
+        rc = run_inverse(c, jobs, s);
+    }
+    if (rc == HE_OK) {
+        std::vector<Job> jobs;
+        for (int b = 0; b < B; b++)
+            for (int cc = 0; cc < nc; cc++)
+                for (int i = 0; i < lm1; i++) {
+                    Job j = blank();
+                    j.src = r + ((size_t)b * nc + cc) * NN;
+                    j.ql = c->mod[lm1];
+                    j.mod = i;
+                    j.dst = tmp + (((size_t)b * nc + cc) * lm1 + i) * NN;
+                    j.aux = in[b] + ((size_t)cc * ell + i) * NN;
+                    j.out = out[b] + ((size_t)cc * lm1 + i) * NN;
+                    j.cw = c->h_qlinv[((size_t)lm1 * c->L + i) * 2];
+                    j.cwp = c->h_qlinv[((size_t)lm1 * c->L + i) * 2 + 1];
+                    jobs.push_back(j);
+                }
+        rc = run_forward<L_CENTER, E_SUBSCALE>(c, jobs, s);
+    }
+    he_scratch_free(scr, s);
+    return rc;
+}

@@ -16,75 +16,11 @@
 // [0, 2q) inverse) with Shoup twiddles read through the read-only cache.
 #include <algorithm>
 
-#include "common.cuh"
+#include "ntt_core.cuh"
 
 namespace {
 
-constexpr int TPB = 256;  // threads per CTA, 16 residues each = 4096 per CTA
-
-__device__ __forceinline__ uint64_t reduce4q(uint64_t x, uint64_t q) {
-    uint64_t q2 = 2 * q;
-    x = x >= q2 ? x - q2 : x;
-    return x >= q ? x - q : x;
-}
-
-// Four CT stages lm = LM0..LM0+3 on x[j] with global index e0 + j*estride.
-// In stage s (j-distance d = 8>>s) the butterflies of each run of 2d
-// consecutive j share one twiddle, index (1<<lm) + (e0 >> (LOGN-lm)) + run:
-// every call site keeps e0 mod 2t below the element stride, so a phase needs
-// 1+2+4+8 = 15 twiddle pairs, each one 16-byte load.
-template <int LOGN, int LM, int D>
-__device__ __forceinline__ void stage_ct(uint64_t (&x)[16], uint32_t e0, const ulonglong2 *__restrict__ W2, uint64_t q) {
-    const uint64_t q2 = 2 * q;
-    const uint32_t base = (1u << LM) + (e0 >> (LOGN - LM));
-#pragma unroll
-    for (int k = 0; k < 8 / D; k++) {
-        const ulonglong2 tw = __ldg(W2 + base + k);
-#pragma unroll
-        for (int jj = 0; jj < D; jj++) {
-            uint64_t u = x[2 * D * k + jj];
-            u = u >= q2 ? u - q2 : u;
-            const uint64_t v = shoup_lazy(x[2 * D * k + jj + D], tw.x, tw.y, q);
-            x[2 * D * k + jj] = u + v;
-            x[2 * D * k + jj + D] = u - v + q2;
-        }
-    }
-}
-template <int LOGN, int LM0>
-__device__ __forceinline__ void phase_ct(uint64_t (&x)[16], uint32_t e0, const ulonglong2 *__restrict__ W2, uint64_t q) {
-    stage_ct<LOGN, LM0, 8>(x, e0, W2, q);
-    stage_ct<LOGN, LM0 + 1, 4>(x, e0, W2, q);
-    stage_ct<LOGN, LM0 + 2, 2>(x, e0, W2, q);
-    stage_ct<LOGN, LM0 + 3, 1>(x, e0, W2, q);
-}
-
-// Four GS stages lt = LT0..LT0+3 (element distance 2^lt), same twiddle sharing.
-template <int LOGN, int LT, int D>
-__device__ __forceinline__ void stage_gs(uint64_t (&x)[16], uint32_t e0, const ulonglong2 *__restrict__ W2, uint64_t q) {
-    const uint64_t q2 = 2 * q;
-    const uint32_t base = (1u << (LOGN - 1 - LT)) + (e0 >> (LT + 1));
-#pragma unroll
-    for (int k = 0; k < 8 / D; k++) {
-        const ulonglong2 tw = __ldg(W2 + base + k);
-#pragma unroll
-        for (int jj = 0; jj < D; jj++) {
-            const uint64_t u = x[2 * D * k + jj], v = x[2 * D * k + jj + D];
-            uint64_t sm = u + v;
-            sm = sm >= q2 ? sm - q2 : sm;
-            x[2 * D * k + jj] = sm;
-            x[2 * D * k + jj + D] = shoup_lazy(u - v + q2, tw.x, tw.y, q);
-        }
-    }
-}
-template <int LOGN, int LT0>
-__device__ __forceinline__ void phase_gs(uint64_t (&x)[16], uint32_t e0, const ulonglong2 *__restrict__ W2, uint64_t q) {
-    stage_gs<LOGN, LT0, 1>(x, e0, W2, q);
-    stage_gs<LOGN, LT0 + 1, 2>(x, e0, W2, q);
-    stage_gs<LOGN, LT0 + 2, 4>(x, e0, W2, q);
-    stage_gs<LOGN, LT0 + 3, 8>(x, e0, W2, q);
-}
-
-__device__ __forceinline__ int pad16(int e) { return e + (e >> 4); }
+constexpr int TPB = NTT_TPB;
 
 struct PolyInfo {
     uint64_t *p;

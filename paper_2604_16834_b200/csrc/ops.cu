@@ -524,9 +524,9 @@ static int const_op(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, 
     return HE_OK;
 }
 
-extern "C" int he_add_const(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, int count, int ell,
+extern "C" int he_add_const(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, int count, int ell, int nc,
                             const uint64_t *res, void *stream) {
-    return const_op(c, in, out, count, ell, 2, res, stream, 0, "he_add_const");
+    return const_op(c, in, out, count, ell, nc, res, stream, 0, "he_add_const");
 }
 
 extern "C" int he_mul_const(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, int count, int ell, int nc,
@@ -598,8 +598,12 @@ extern "C" int he_keyswitch(he_ctx *c, uint32_t g, const uint64_t *const *d, uin
     int ch = chunk_of(ks_bytes_per_ct(c, ell), count);
     for (int b0 = 0; b0 < count; b0 += ch) {
         int B = std::min(ch, count - b0);
-        HE_TRY(keyswitch_chunk(c, key, D.as<uint64_t>() + b0, B, ell, O0.as<uint64_t>() + b0, O1.as<uint64_t>() + b0,
-                               nullptr, nullptr, s));
+        if (c->logN == 16)
+            HE_TRY(he_keyswitch_fused(c, key, d + b0, D.as<const uint64_t>() + b0, B, ell, out0 + b0, out1 + b0,
+                                      nullptr, nullptr, s));
+        else
+            HE_TRY(keyswitch_chunk(c, key, D.as<uint64_t>() + b0, B, ell, O0.as<uint64_t>() + b0,
+                                   O1.as<uint64_t>() + b0, nullptr, nullptr, s));
     }
     return HE_OK;
 }
@@ -632,8 +636,13 @@ extern "C" int he_relin(he_ctx *c, const uint64_t *const *d3, uint64_t *const *o
     int ch = chunk_of(ks_bytes_per_ct(c, ell), count);
     for (int b0 = 0; b0 < count; b0 += ch) {
         int B = std::min(ch, count - b0);
-        HE_TRY(keyswitch_chunk(c, key, D2.as<uint64_t>() + b0, B, ell, O0.as<uint64_t>() + b0, O1.as<uint64_t>() + b0,
-                               D0.as<const uint64_t>() + b0, D1.as<const uint64_t>() + b0, s));
+        if (c->logN == 16)
+            HE_TRY(he_keyswitch_fused(c, key, p2.data() + b0, D2.as<const uint64_t>() + b0, B, ell, q0.data() + b0,
+                                      q1.data() + b0, p0.data() + b0, p1.data() + b0, s));
+        else
+            HE_TRY(keyswitch_chunk(c, key, D2.as<uint64_t>() + b0, B, ell, O0.as<uint64_t>() + b0,
+                                   O1.as<uint64_t>() + b0, D0.as<const uint64_t>() + b0, D1.as<const uint64_t>() + b0,
+                                   s));
     }
     return HE_OK;
 }
@@ -653,7 +662,10 @@ extern "C" int he_rescale(he_ctx *c, const uint64_t *const *in, uint64_t *const 
     int ch = chunk_of((size_t)nc * ell * c->N * 8, count);
     for (int b0 = 0; b0 < count; b0 += ch) {
         int B = std::min(ch, count - b0);
-        HE_TRY(rescale_chunk(c, I.as<const uint64_t>() + b0, O.as<uint64_t>() + b0, B, ell, nc, s));
+        if (c->logN == 16)
+            HE_TRY(he_rescale_fused(c, in + b0, out + b0, B, ell, nc, s));
+        else
+            HE_TRY(rescale_chunk(c, I.as<const uint64_t>() + b0, O.as<uint64_t>() + b0, B, ell, nc, s));
     }
     return HE_OK;
 }
@@ -705,9 +717,15 @@ extern "C" int he_mult_ct(he_ctx *c, const uint64_t *const *a, const uint64_t *c
         k_tensor<<<grid_ew(P, Bn), EW, 0, s>>>(D3.as<uint64_t>(), A.as<const uint64_t>() + b0,
                                                B.as<const uint64_t>() + b0, Bn, ell, c->logN, c->d_mc);
         HE_CHECK_LAUNCH();
-        HE_TRY(keyswitch_chunk(c, key, D2.as<uint64_t>(), Bn, ell, R0.as<uint64_t>(), R1.as<uint64_t>(),
-                               D0.as<const uint64_t>(), D1.as<const uint64_t>(), s));
-        HE_TRY(rescale_chunk(c, RL.as<const uint64_t>(), O.as<uint64_t>() + b0, Bn, ell, 2, s));
+        if (c->logN == 16) {
+            HE_TRY(he_keyswitch_fused(c, key, pd2.data(), D2.as<const uint64_t>(), Bn, ell, pr0.data(), pr1.data(),
+                                      pd0.data(), pd1.data(), s));
+            HE_TRY(he_rescale_fused(c, prl.data(), out + b0, Bn, ell, 2, s));
+        } else {
+            HE_TRY(keyswitch_chunk(c, key, D2.as<uint64_t>(), Bn, ell, R0.as<uint64_t>(), R1.as<uint64_t>(),
+                                   D0.as<const uint64_t>(), D1.as<const uint64_t>(), s));
+            HE_TRY(rescale_chunk(c, RL.as<const uint64_t>(), O.as<uint64_t>() + b0, Bn, ell, 2, s));
+        }
     }
     return HE_OK;
 }
@@ -765,8 +783,12 @@ extern "C" int he_rotate(he_ctx *c, uint32_t g, const uint64_t *const *in, uint6
         k_automorph_ptrs<<<grid_ew(2 * P, Bn), EW, 0, s>>>(T.as<uint64_t>(), I.as<const uint64_t>() + b0, Bn, 2 * ell,
                                                             c->logN, g);
         HE_CHECK_LAUNCH();
-        HE_TRY(keyswitch_chunk(c, key, T1.as<uint64_t>(), Bn, ell, O0.as<uint64_t>(), O1.as<uint64_t>(),
-                               T0.as<const uint64_t>(), nullptr, s));
+        if (c->logN == 16)
+            HE_TRY(he_keyswitch_fused(c, key, p1.data(), T1.as<const uint64_t>(), Bn, ell, o0.data(), o1.data(),
+                                      p0.data(), nullptr, s));
+        else
+            HE_TRY(keyswitch_chunk(c, key, T1.as<uint64_t>(), Bn, ell, O0.as<uint64_t>(), O1.as<uint64_t>(),
+                                   T0.as<const uint64_t>(), nullptr, s));
     }
     return HE_OK;
 }

@@ -553,13 +553,14 @@ class GpuEngine:
         for a, b in zip(A, B):
             if abs(a.scale / b.scale - 1.0) > SCALE_RTOL:
                 raise ScaleMismatch(f"scales {a.scale:.6g} and {b.scale:.6g} differ")
+        nc = self._ncomp(list(A) + list(B))
         ta, tb = self._at_level(A, level), self._at_level(B, level)
-        out = self._alloc(len(A), 2, level + 1)
+        out = self._alloc(len(A), nc, level + 1)
         pa = _lib.ptr_array([t.data_ptr() for t in ta])
         pb = _lib.ptr_array([t.data_ptr() for t in tb])
         po = self._tptrs(out)
         fn = self._L.he_sub if sub else self._L.he_add
-        _lib.check(fn(self._h, _lib.addr(pa), _lib.addr(pb), _lib.addr(po), len(A), level + 1, 2, self.stream), "add")
+        _lib.check(fn(self._h, _lib.addr(pa), _lib.addr(pb), _lib.addr(po), len(A), level + 1, nc, self.stream), "add")
         return self._wrap_batch(out, level, [a.scale for a in A])
 
     def add_batch(self, A: Sequence[CipherVec], B: Sequence[CipherVec]) -> list[CipherVec]:
@@ -598,13 +599,63 @@ class GpuEngine:
         if any(c.level != level for c in cts):
             raise HebatchError("add_const_batch needs equal levels")
         limbs = level + 1
+        nc = self._ncomp(cts)
         res = np.array([self._res(int(np.rint(v * c.scale)), limbs) for v, c in zip(values, cts)], np.uint64)
-        out = self._alloc(len(cts), 2, limbs)
+        out = self._alloc(len(cts), nc, limbs)
         pi, po = self._ptrs(cts), self._tptrs(out)
         _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pi), _lib.addr(po), len(cts),
-                              limbs, _lib.addr(res), self.stream, units=(len(cts) * 4.0 * limbs * self.N * 8, 0.0)),
-                   "add_const")
+                              limbs, nc, _lib.addr(res), self.stream,
+                              units=(len(cts) * 2.0 * nc * limbs * self.N * 8, 0.0)), "add_const")
         return self._wrap_batch(out, level, [c.scale for c in cts])
+
+    @staticmethod
+    def _ncomp(cts: Sequence[CipherVec]) -> int:
+        nc = cts[0].data.shape[0]
+        if any(c.data.shape[0] != nc for c in cts):
+            raise HebatchError("mixed 2- and 3-component ciphertexts in one batch")
+        return nc
+
+    def tensor_batch(self, A: Sequence[CipherVec], B: Sequence[CipherVec]) -> list[CipherVec]:
+        """ct x ct WITHOUT relinearisation or rescale: 3-component results at the
+        common level, scale s_a * s_b (lazy relinearisation / rescaling: sums of
+        such products -- pooling, GAP -- are relinearised and rescaled once)."""
+        for c in list(A) + list(B):
+            self._check(c)
+        if any(c.level < self.context.mult_level_cost for c in list(A) + list(B)):
+            raise LevelExhausted("operand level below multiplication cost")
+        self._acct.bump("ct_mults", len(A))
+        level = min(min(c.level for c in A), min(c.level for c in B))
+        limbs = level + 1
+        ta, tb = self._at_level(A, level), self._at_level(B, level)
+        out = self._alloc(len(A), 3, limbs)
+        pa = _lib.ptr_array([t.data_ptr() for t in ta])
+        pb = _lib.ptr_array([t.data_ptr() for t in tb])
+        po = self._tptrs(out)
+        _lib.check(self._call("tensor", self._L.he_tensor, self._h, _lib.addr(pa), _lib.addr(pb), _lib.addr(po),
+                              len(A), limbs, self.stream, units=(len(A) * 7.0 * limbs * self.N * 8, 0.0)), "tensor")
+        return self._wrap_batch(out, level, [a.scale * b.scale for a, b in zip(A, B)])
+
+    def relin_rescale_batch(self, cts: Sequence[CipherVec]) -> list[CipherVec]:
+        """3-component ciphertexts -> relinearise (key switch of c2) -> rescale."""
+        for c in cts:
+            self._check(c)
+        if self._ncomp(cts) != 3:
+            raise HebatchError("relin_rescale_batch expects 3-component ciphertexts")
+        self._ensure_relin()
+        level = cts[0].level
+        if any(c.level != level for c in cts) or level < 1:
+            raise LevelExhausted("relin_rescale_batch needs equal levels >= 1")
+        limbs = level + 1
+        mid = self._alloc(len(cts), 2, limbs)
+        pi, pm = self._ptrs(cts), self._tptrs(mid)
+        _lib.check(self._call("relin", self._L.he_relin, self._h, _lib.addr(pi), _lib.addr(pm), len(cts), limbs,
+                              self.stream, units=(len(cts) * 5.0 * limbs * self.N * 8, 0.0)), "relin")
+        ql = self.moduli[limbs - 1]
+        out = self._alloc(len(cts), 2, limbs - 1)
+        po = self._tptrs(out)
+        _lib.check(self._call("rescale", self._L.he_rescale, self._h, _lib.addr(pm), _lib.addr(po), len(cts), limbs,
+                              2, self.stream, units=(len(cts) * (2 * limbs - 1) * 2 * self.N * 8.0, 0.0)), "rescale")
+        return self._wrap_batch(out, level - 1, [c.scale / ql for c in cts])
 
     def mult_plain(self, ct: CipherVec, p: PlainVec) -> CipherVec:
         self._check(ct)
@@ -764,7 +815,7 @@ class GpuEngine:
             b = np.asarray(bias, np.float64)
             res = np.array([self._res(int(np.rint(bv * s_out)), limbs - 1) for bv in b], np.uint64)
             _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pout), _lib.addr(pout), n_out,
-                                  limbs - 1, _lib.addr(res), self.stream,
+                                  limbs - 1, 2, _lib.addr(res), self.stream,
                                   units=(n_out * 2.0 * (limbs - 1) * self.N * 8, 0.0)), "bias")
         if count_as_conv:
             self._acct.bump("plain_mults", int(len(col)))
@@ -820,7 +871,7 @@ class GpuEngine:
             b = np.asarray(bias, np.float64)
             res = np.array([self._res(int(np.rint(bv * s_out)), limbs - 1) for bv in b], np.uint64)
             _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pout), _lib.addr(pout), n_out,
-                                  limbs - 1, _lib.addr(res), self.stream,
+                                  limbs - 1, 2, _lib.addr(res), self.stream,
                                   units=(n_out * 2.0 * (limbs - 1) * self.N * 8, 0.0)), "bias")
         self._acct.bump("plain_mults", int(len(tc)) * M)
         self._acct.bump("adds", int(len(tc)) * M)
@@ -843,13 +894,14 @@ class GpuEngine:
         col = np.ascontiguousarray(col, np.int32)
         wi = np.ascontiguousarray(int_weights, np.int64)
         n_out = len(row_ptr) - 1
+        nc = self._ncomp(inputs)
         tins = self._at_level(inputs, level)
         pin = _lib.ptr_array([t.data_ptr() for t in tins])
-        out = self._alloc(n_out, 2, limbs)
+        out = self._alloc(n_out, nc, limbs)
         pout = self._tptrs(out)
-        poly = 2 * limbs * self.N
+        poly = nc * limbs * self.N
         _lib.check(self._call("lincomb_int", self._L.he_lincomb, self._h, _lib.addr(pin), len(inputs),
-                              _lib.addr(pout), n_out, _lib.addr(row_ptr), _lib.addr(col), _lib.addr(wi), limbs, 2,
+                              _lib.addr(pout), n_out, _lib.addr(row_ptr), _lib.addr(col), _lib.addr(wi), limbs, nc,
                               self.stream, units=((len(np.unique(col)) + n_out) * poly * 8.0, float(len(col)) * poly)),
                    "lincomb_int")
         if count_adds:

@@ -153,13 +153,19 @@ class Activation:
         return sum(c * x ** k for k, c in enumerate(self.coeffs))
 
 
-def apply_activation(engine, cts, act: Activation):
-    """Evaluate ``act`` on ciphertexts that already carry the folded affine map."""
+def apply_activation(engine, cts, act: Activation, lazy: bool = False):
+    """Evaluate ``act`` on ciphertexts that already carry the folded affine map.
+
+    lazy=True leaves the LAST ciphertext product unrelinearised and unrescaled
+    (3 components at scale s^2): the caller sums such outputs (pool / GAP)
+    and relinearises + rescales only the sums (engine.relin_rescale_batch).
+    Relinearisation and rescale are linear up to their rounding, so this is
+    the standard lazy-relinearisation / lazy-rescale rewrite; the CPU oracle
+    replays exactly the same sequence."""
     if act.degree == 2:
         c0, c1, c2 = act.coeffs
-        a = math.sqrt(c2)
         c = c0 - c1 * c1 / (4 * c2)
-        sq = engine.mult_ct_batch(cts, cts)
+        sq = engine.tensor_batch(cts, cts) if lazy else engine.mult_ct_batch(cts, cts)
         if c == 0:
             return sq
         out = engine.add_const_batch(sq, [c] * len(sq))
@@ -172,7 +178,7 @@ def apply_activation(engine, cts, act: Activation):
     sqd = engine.add_const_batch(sq, [d] * len(sq)) if d else sq
     if sqd is not sq:
         engine.release(*sq)
-    cub = engine.mult_ct_batch(cts, sqd)                  # y (y^2 + d)
+    cub = engine.tensor_batch(cts, sqd) if lazy else engine.mult_ct_batch(cts, sqd)   # y (y^2 + d)
     engine.release(*sqd)
     if c0 == 0:
         return cub
@@ -279,7 +285,7 @@ class CnnSpec:
 
 
 def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, release_inputs: bool = True,
-            tile_outputs: int = 1024):
+            tile_outputs: int = 1024, lazy_relin: bool = True):
     """Encrypted forward pass of ``spec`` over feature-major input ciphertexts.
 
     x_cts: C0*H*W ciphertexts (channel-major).  Each block is streamed over
@@ -308,16 +314,14 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
             rows = list(range(r0, min(H, r0 + R)))
             nr = len(rows)
             y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows)   # [o][r][x]
-            z = apply_activation(engine, y, spec.act)
+            lazy = lazy_relin and (pool or last)
+            z = apply_activation(engine, y, spec.act, lazy=lazy)
             engine.release(*y)
-            if pool:
-                zp = fm_avgpool2x2(engine, z, q, nr, W)                         # [o][r/2][x/2]
-                engine.release(*z)
-                z = zp
-                nr //= 2
             if last:
-                rp, cols = gap_csr(q, nr * Wo)
-                part = engine.lincomb_int(z, rp, cols, np.ones(len(cols), np.int64), out_scale=Ho * Wo * z[0].scale)
+                # GAP of the (pooled) map = mean over every pixel of the block
+                hw = H * W
+                rp, cols = gap_csr(q, nr * W)
+                part = engine.lincomb_int(z, rp, cols, np.ones(len(cols), np.int64), out_scale=hw * z[0].scale)
                 engine.release(*z)
                 if gap is None:
                     gap = part
@@ -326,6 +330,15 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
                     engine.release(*gap, *part)
                     gap = nsum
                 continue
+            if pool:
+                zp = fm_avgpool2x2(engine, z, q, nr, W)                         # [o][r/2][x/2]
+                engine.release(*z)
+                z = zp
+                nr //= 2
+            if lazy:
+                zr = engine.relin_rescale_batch(z)
+                engine.release(*z)
+                z = zr
             y0 = rows[0] // 2 if pool else rows[0]
             for o in range(q):
                 for r in range(nr):
@@ -333,6 +346,10 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
                         nxt[o * Ho * Wo + (y0 + r) * Wo + x] = z[(o * nr + r) * Wo + x]
         if blk > 0 or release_inputs:
             engine.release(*cur)
+        if last and lazy_relin:
+            g2 = engine.relin_rescale_batch(gap)
+            engine.release(*gap)
+            gap = g2
         cur = gap if last else nxt
         H, W = Ho, Wo
     out = fm_dense(engine, cur, wts.dense[0], wts.dense[1])

@@ -7,10 +7,10 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2604_16834_b200 import configs  # first: selects torch's allocator backend
 import numpy as np
 import torch
 
-from paper_2604_16834_b200 import configs
 from paper_2604_16834_b200.engine import GpuEngine
 from paper_2604_16834_b200.featuremajor import run_cnn, run_mlp
 from paper_2604_16834_b200.packing import pack_features

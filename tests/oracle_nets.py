@@ -63,7 +63,33 @@ def mult_ct(orc, rk, a, b):
 
 
 def add_const(orc, a, v):
-    return OracleCts(orc.add_const(a.data, residues(np.rint(v * a.scale), orc.moduli, a.ell)), a.scale)
+    """constant added to component 0 (works for 2- and 3-component ciphertexts)."""
+    res = residues(np.rint(v * a.scale), orc.moduli, a.ell)
+    out = a.data.copy()
+    c0 = orc.add_const(np.ascontiguousarray(a.data[:2]), res)[0]
+    out[0] = c0
+    return OracleCts(out, a.scale)
+
+
+def tensor(orc, a, b):
+    """engine.tensor_batch: 3-component product, no relin / rescale, scale s_a s_b."""
+    ell = min(a.ell, b.ell)
+    return OracleCts(orc.tensor(np.ascontiguousarray(a.data[:, :ell]), np.ascontiguousarray(b.data[:, :ell])),
+                     a.scale * b.scale)
+
+
+def relin_rescale(orc, rk, a):
+    """engine.relin_rescale_batch: relinearise the 3-component ct, then rescale."""
+    r = orc.relin(np.ascontiguousarray(a.data), rk)
+    return OracleCts(orc.rescale(r), a.scale / orc.moduli[a.ell - 1])
+
+
+def activation_lazy(orc, cts, coeffs):
+    """apply_activation(lazy=True) for degree 2: tensor + constant (3 components)."""
+    c0, c1, c2 = coeffs
+    c = c0 - c1 * c1 / (4 * c2)
+    out = [tensor(orc, x, x) for x in cts]
+    return [add_const(orc, y, c) for y in out] if c != 0 else out
 
 
 def activation(orc, rk, cts, coeffs):

@@ -92,14 +92,24 @@ def test_small_cnn_oracle_ckks_decrypts_to_reference():
     s = orc.scale
     w1 = wts.convs[0][0]
     y = ON.conv3x3(orc, x, w1, np.zeros(3), 4, 4, ON.fold(spec.act.coeffs), s)
-    z = ON.activation(orc, rk, y, spec.act.coeffs)
-    rp, cols = pool2x2_csr(3, 4, 4)
-    pz = ON.lincomb_int(orc, z, rp, cols, 4 * z[0].scale)
-    rp, cols = gap_csr(3, 4)
-    gz = ON.lincomb_int(orc, pz, rp, cols, 4 * pz[0].scale)
     rows = np.arange(6) * 3
     cols = np.tile(np.arange(3), 5)
+    # eager plan: relinearise + rescale every activation, then pool and GAP
+    z = ON.activation(orc, rk, y, spec.act.coeffs)
+    rp, cols_p = pool2x2_csr(3, 4, 4)
+    pz = ON.lincomb_int(orc, z, rp, cols_p, 4 * z[0].scale)
+    rp, cols_g = gap_csr(3, 4)
+    gz = ON.lincomb_int(orc, pz, rp, cols_g, 4 * pz[0].scale)
     out = ON.lincomb(orc, gz, rows, cols, wts.dense[0].reshape(-1), bias=np.zeros(5), out_scale=s)
+    got = np.stack([orc.decrypt(o.data, o.scale) for o in out], axis=1)
+    assert np.max(np.abs(got - g["logits"])) < 1e-3
+    # lazy plan (run_cnn's last block): unrelinearised squares summed by the
+    # GAP over all 16 pixels, ONE relin + rescale per channel, then dense
+    zl = ON.activation_lazy(orc, y, spec.act.coeffs)
+    rp, cols_g = gap_csr(3, 16)
+    gl = ON.lincomb_int(orc, zl, rp, cols_g, 16 * zl[0].scale)
+    gl = [ON.relin_rescale(orc, rk, c) for c in gl]
+    out = ON.lincomb(orc, gl, rows, cols, wts.dense[0].reshape(-1), bias=np.zeros(5), out_scale=s)
     got = np.stack([orc.decrypt(o.data, o.scale) for o in out], axis=1)
     assert np.max(np.abs(got - g["logits"])) < 1e-3
 

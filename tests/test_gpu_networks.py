@@ -124,8 +124,22 @@ def test_cfg3_network_decrypt_and_sampled_bit_exact():
         r = orc.rescale(acc)
         r = orc.add_const(r, [int(np.rint((a * b1[5] + b) * s)) % m for m in eng.moduli[:13]])
         assert np.array_equal(to_np(y[o].data), r), (yy, xx)
+    rk = orc.switch_key(0)
     sq = eng.mult_ct_batch([y[0]], [y[0]])
-    assert np.array_equal(to_np(sq[0].data), orc.mult_ct(to_np(y[0].data), to_np(y[0].data), orc.switch_key(0)))
+    assert np.array_equal(to_np(sq[0].data), orc.mult_ct(to_np(y[0].data), to_np(y[0].data), rk))
+    # lazy activation + pool window (0, 0): tensor, +c, sum of 4, relin, rescale
+    import oracle_nets as ON
+
+    win = [y[0], y[1], y[32], y[33]]
+    c = 0.25 - 0.5 ** 2 / (4 * 0.125)
+    t = eng.add_const_batch(eng.tensor_batch(win, win), [c] * 4)
+    p = eng.lincomb_int(t, [0, 4], [0, 1, 2, 3], np.ones(4, np.int64), out_scale=4 * t[0].scale)
+    r = eng.relin_rescale_batch(p)[0]
+    oc = [ON.OracleCts(to_np(v.data), v.scale) for v in win]
+    ot = [ON.add_const(orc, ON.tensor(orc, v, v), c) for v in oc]
+    op = ON.lincomb_int(orc, ot, [0, 4], [0, 1, 2, 3], 4 * ot[0].scale)[0]
+    orr = ON.relin_rescale(orc, rk, op)
+    assert np.array_equal(to_np(r.data), orr.data) and r.scale == orr.scale
     eng.release(*y, *sq)
     # full network, decrypt-level
     out = run_cnn(eng, x, spec, wts)
