@@ -132,37 +132,48 @@ __device__ __forceinline__ void mac128(u128 &acc, uint64_t a, uint64_t b) {
         : "+l"(acc.lo), "+l"(acc.hi)
         : "l"(a), "l"(b));
 }
-// Split accumulator for moduli q < 2^52 (operands < 2^52): x*w is accumulated
-// as L (64-bit, carries counted in C) + M 2^32 + H 2^64 from four 32x32->64
-// products -- 7 instructions per MAC instead of a full 128-bit product chain.
-// Valid while the exact sum stays < 2^116 (terms * q^2), which callers ensure.
-struct acc52 {
-    uint64_t L, M, H;
-    uint32_t C;
+// Carry-free split accumulator for moduli q < 2^52 (operands < 2^52) and at
+// most 1024 terms: with x = xh 2^32 + xl1 2^16 + xl0 and w = wh 2^32 + wl,
+//   x w = xl0 wl + 2^16 xl1 wl + 2^32 (xh wl + xl wh) + 2^64 xh wh,
+// and every column sum fits its 64-bit accumulator (xl0 wl, xl1 wl < 2^48;
+// xh wl, xl wh < 2^52; xh wh < 2^40), so one MAC is five IMAD.WIDE.U32 with
+// 64-bit accumulate and no carry propagation.  The x split (xl0, xl1, xh) is
+// done once per input and shared by every output of the group.
+struct xsplit {
+    uint32_t l0, l1, l, h;
 };
-__device__ __forceinline__ void acc52_zero(acc52 &a) {
-    a.L = 0;
-    a.M = 0;
-    a.H = 0;
-    a.C = 0;
+__device__ __forceinline__ xsplit split52(uint64_t x) {
+    xsplit s;
+    s.l = (uint32_t)x;
+    s.h = (uint32_t)(x >> 32);
+    s.l0 = s.l & 0xFFFFu;
+    s.l1 = s.l >> 16;
+    return s;
 }
-__device__ __forceinline__ void mac52(acc52 &a, uint64_t x, uint64_t w) {
-    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32), wl = (uint32_t)w, wh = (uint32_t)(w >> 32);
-    uint64_t p = (uint64_t)xl * wl;
-    asm("add.cc.u64 %0, %0, %2;\n\t"
-        "addc.u32 %1, %1, 0;"
-        : "+l"(a.L), "+r"(a.C)
-        : "l"(p));
-    a.M += (uint64_t)xh * wl;
-    a.M += (uint64_t)xl * wh;
-    a.H += (uint64_t)xh * wh;
+struct acc52 {
+    uint64_t L0, L1, M, H;
+};
+__device__ __forceinline__ void acc52_zero(acc52 &a) { a.L0 = a.L1 = a.M = a.H = 0; }
+__device__ __forceinline__ void mac52(acc52 &a, const xsplit &x, uint64_t w) {
+    const uint32_t wl = (uint32_t)w, wh = (uint32_t)(w >> 32);
+    // mad.wide.u32 = one IMAD.WIDE.U32 with 64-bit accumulate (ptxas does not
+    // always form it from the C expression)
+    asm("mad.wide.u32 %0, %4, %6, %0;\n\t"
+        "mad.wide.u32 %1, %5, %6, %1;\n\t"
+        "mad.wide.u32 %2, %7, %6, %2;\n\t"
+        "mad.wide.u32 %2, %8, %9, %2;\n\t"
+        "mad.wide.u32 %3, %7, %9, %3;"
+        : "+l"(a.L0), "+l"(a.L1), "+l"(a.M), "+l"(a.H)
+        : "r"(x.l0), "r"(x.l1), "r"(wl), "r"(x.h), "r"(x.l), "r"(wh));
 }
 // collapse to a 128-bit (hi, lo)
 __device__ __forceinline__ u128 acc52_sum(const acc52 &a) {
     u128 r;
-    uint64_t ml = a.M << 32, mh = a.M >> 32;
-    r.lo = a.L + ml;
-    r.hi = a.H + mh + (uint64_t)a.C + (r.lo < ml ? 1 : 0);
+    const uint64_t l1s = a.L1 << 16, ms = a.M << 32;
+    uint64_t lo = a.L0 + l1s;
+    uint64_t hi = a.H + (a.L1 >> 48) + (a.M >> 32) + (lo < l1s ? 1 : 0);
+    r.lo = lo + ms;
+    r.hi = hi + (r.lo < ms ? 1 : 0);
     return r;
 }
 

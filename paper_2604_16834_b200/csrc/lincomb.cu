@@ -67,27 +67,33 @@ struct Acc;
 template <>
 struct Acc<true> {
     acc52 a;
+    using X = xsplit;
+    __device__ __forceinline__ static X prep(uint64_t x) { return split52(x); }
     __device__ __forceinline__ void zero() { acc52_zero(a); }
-    __device__ __forceinline__ void mac(uint64_t x, uint64_t w) { mac52(a, x, w); }
+    __device__ __forceinline__ void mac(const X &x, uint64_t w) { mac52(a, x, w); }
     __device__ __forceinline__ void fold(uint64_t) {}
     __device__ __forceinline__ u128 sum() const { return acc52_sum(a); }
 };
 template <>
 struct Acc<false> {
     u128 a;
+    using X = uint64_t;
+    __device__ __forceinline__ static X prep(uint64_t x) { return x; }
     __device__ __forceinline__ void zero() { a = {0, 0}; }
-    __device__ __forceinline__ void mac(uint64_t x, uint64_t w) { mac128(a, x, w); }
+    __device__ __forceinline__ void mac(const X &x, uint64_t w) { mac128(a, x, w); }
     __device__ __forceinline__ void fold(uint64_t q) {
         if (a.hi >= q) a.hi -= q;
     }
     __device__ __forceinline__ u128 sum() const { return a; }
 };
 
-// FAST: every limb of the launch has q < 2^52 and kmax * q < 2^64, so the
-// split 32-bit accumulator applies and no per-term fold is needed.
+// FAST: every limb of the launch has q < 2^52 and kmax * q < 2^64 (and
+// kmax <= 1024), so the carry-free split accumulator applies and no per-term
+// fold is needed.  Dynamic shared memory: weights [T][WS], then the block's
+// terms (pointer, tap) so the gather addresses never wait on global loads.
 template <int MM, bool FAST>
 __global__ void __launch_bounds__(LB) k_lincomb_grouped(const GroupArgs a) {
-    extern __shared__ uint64_t wsm[];  // [T][WS]
+    extern __shared__ uint64_t wsm[];  // [T][WS] then Term[block terms]
     const int N = 1 << a.logN;
     const int cpp = N / LB;
     const int pl = blockIdx.y / cpp;  // comp * nl + (limb - l_lo)
@@ -97,12 +103,15 @@ __global__ void __launch_bounds__(LB) k_lincomb_grouped(const GroupArgs a) {
     const ModConst c = a.mc[l];
     const uint64_t *src = a.wM + (size_t)l * a.T * a.WS;
     for (int i = threadIdx.x; i < a.T * a.WS; i += LB) wsm[i] = src[i];
+    const int g0 = blockIdx.x * a.gpb, g1 = min(g0 + a.gpb, a.n_groups);
+    const int tb0 = a.term_ptr[g0], tb1 = a.term_ptr[g1];
+    Term *tsm = (Term *)(wsm + a.T * a.WS);
+    for (int i = threadIdx.x; i < tb1 - tb0; i += LB) tsm[i] = a.terms[tb0 + i];
     __syncthreads();
     // sums of kmax products < q^2 need a fold to keep hi < q when kmax * q >= 2^64
     const bool fold = !FAST && (double)a.kmax * (double)c.q >= 1.8e19;
-    const int g0 = blockIdx.x * a.gpb, g1 = min(g0 + a.gpb, a.n_groups);
     for (int g = g0; g < g1; g++) {
-        const int t0 = a.term_ptr[g], t1 = a.term_ptr[g + 1];
+        const int t0 = a.term_ptr[g] - tb0, t1 = a.term_ptr[g + 1] - tb0;
         const int ob = a.out_base[g] + a.m_off * a.out_stride;
         Acc<FAST> acc[MM];
 #pragma unroll
@@ -113,7 +122,7 @@ __global__ void __launch_bounds__(LB) k_lincomb_grouped(const GroupArgs a) {
 #pragma unroll
             for (int u = 0; u < PF; u++) {  // issue all gathers first
                 if (t + u < t1) {
-                    const Term tm = a.terms[t + u];
+                    const Term tm = tsm[t + u];
                     xs[u] = __ldg(tm.p + off);
                     taps[u] = tm.tap;
                 } else {
@@ -124,11 +133,12 @@ __global__ void __launch_bounds__(LB) k_lincomb_grouped(const GroupArgs a) {
 #pragma unroll
             for (int u = 0; u < PF; u++) {
                 const uint64_t *wr = wsm + taps[u] * a.WS + a.m_off;
+                const typename Acc<FAST>::X xv = Acc<FAST>::prep(xs[u]);
 #pragma unroll
                 for (int m = 0; m < MM; m += 2) {
                     const ulonglong2 w2 = *(const ulonglong2 *)(wr + m);
-                    acc[m].mac(xs[u], w2.x);
-                    acc[m + 1].mac(xs[u], w2.y);
+                    acc[m].mac(xv, w2.x);
+                    acc[m + 1].mac(xv, w2.y);
                 }
                 if (fold) {
 #pragma unroll
@@ -162,8 +172,7 @@ int dispatch_grouped(int MM, bool fast, dim3 grid, size_t smem, cudaStream_t s, 
         switch (MM) {
             case 2: return launch_grouped<2, true>(grid, smem, s, a);
             case 4: return launch_grouped<4, true>(grid, smem, s, a);
-            case 8: return launch_grouped<8, true>(grid, smem, s, a);
-            default: return launch_grouped<16, true>(grid, smem, s, a);
+            default: return launch_grouped<8, true>(grid, smem, s, a);
         }
     }
     switch (MM) {
@@ -244,7 +253,16 @@ extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in
     HE_CHECK_LAUNCH();
     const int gpb = std::max(1, std::min(8, n_groups / 148));
     const int cpp = c->N / LB;
-    const size_t smem = (size_t)T * MM * 8;
+    int max_block_terms = 0;
+    for (int g0 = 0; g0 < n_groups; g0 += gpb)
+        max_block_terms = std::max(max_block_terms, term_ptr[std::min(g0 + gpb, n_groups)] - term_ptr[g0]);
+    const size_t smem = (size_t)T * MM * 8 + (size_t)max_block_terms * sizeof(Term);
+    if (smem > 200 * 1024) {
+        he_set_error("he_lincomb_grouped: %zu bytes of shared memory needed (T=%d, M=%d)", smem, T, M);
+        he_scratch_free(meta, s);
+        he_scratch_free(dout, s);
+        return HE_EINVAL;
+    }
     int rc = HE_OK;
     if ((size_t)nc * ell * cpp > 65535) {
         he_set_error("he_lincomb_grouped: grid too large");
@@ -268,7 +286,7 @@ extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in
     a.kmax = kmax;
     // runs of consecutive limbs that share the accumulator variant
     auto fast_ok = [&](int l) {
-        return c->mod[l] < (1ull << 52) && (double)kmax * (double)c->mod[l] < 1.8e19 && kmax <= 2048;
+        return c->mod[l] < (1ull << 52) && (double)kmax * (double)c->mod[l] < 1.8e19 && kmax <= 1024;
     };
     for (int l0 = 0; l0 < ell && rc == HE_OK;) {
         const bool fast = fast_ok(l0);
@@ -277,7 +295,7 @@ extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in
         a.l_lo = l0;
         a.nl = l1 - l0;
         dim3 grid(ceil_div(n_groups, gpb), (unsigned)(nc * a.nl * cpp));
-        const int mm = fast ? std::min(MM, 16) : MM;
+        const int mm = fast ? std::min(MM, 8) : MM;
         for (int m0 = 0; m0 < M && rc == HE_OK; m0 += mm) {
             a.m_off = m0;
             rc = dispatch_grouped(mm, fast, grid, smem, s, a);
