@@ -635,27 +635,33 @@ class GpuEngine:
                               len(A), limbs, self.stream, units=(len(A) * 7.0 * limbs * self.N * 8, 0.0)), "tensor")
         return self._wrap_batch(out, level, [a.scale * b.scale for a, b in zip(A, B)])
 
-    def relin_rescale_batch(self, cts: Sequence[CipherVec]) -> list[CipherVec]:
-        """3-component ciphertexts -> relinearise (key switch of c2) -> rescale."""
+    def relin_rescale_batch(self, cts: Sequence[CipherVec], drops: int = 1) -> list[CipherVec]:
+        """3-component ciphertexts -> relinearise (key switch of c2) -> rescale
+        ``drops`` times (2 after a deferred-rescale linear layer)."""
         for c in cts:
             self._check(c)
         if self._ncomp(cts) != 3:
             raise HebatchError("relin_rescale_batch expects 3-component ciphertexts")
         self._ensure_relin()
         level = cts[0].level
-        if any(c.level != level for c in cts) or level < 1:
-            raise LevelExhausted("relin_rescale_batch needs equal levels >= 1")
+        if any(c.level != level for c in cts) or level < drops:
+            raise LevelExhausted(f"relin_rescale_batch needs equal levels >= {drops}")
         limbs = level + 1
-        mid = self._alloc(len(cts), 2, limbs)
-        pi, pm = self._ptrs(cts), self._tptrs(mid)
+        cur = self._alloc(len(cts), 2, limbs)
+        pi, pm = self._ptrs(cts), self._tptrs(cur)
         _lib.check(self._call("relin", self._L.he_relin, self._h, _lib.addr(pi), _lib.addr(pm), len(cts), limbs,
                               self.stream, units=(len(cts) * 5.0 * limbs * self.N * 8, 0.0)), "relin")
-        ql = self.moduli[limbs - 1]
-        out = self._alloc(len(cts), 2, limbs - 1)
-        po = self._tptrs(out)
-        _lib.check(self._call("rescale", self._L.he_rescale, self._h, _lib.addr(pm), _lib.addr(po), len(cts), limbs,
-                              2, self.stream, units=(len(cts) * (2 * limbs - 1) * 2 * self.N * 8.0, 0.0)), "rescale")
-        return self._wrap_batch(out, level - 1, [c.scale / ql for c in cts])
+        scales = [c.scale for c in cts]
+        for _ in range(drops):
+            ql = self.moduli[limbs - 1]
+            out = self._alloc(len(cts), 2, limbs - 1)
+            po = self._tptrs(out)
+            _lib.check(self._call("rescale", self._L.he_rescale, self._h, _lib.addr(pm), _lib.addr(po), len(cts),
+                                  limbs, 2, self.stream, units=(len(cts) * (2 * limbs - 1) * 2 * self.N * 8.0, 0.0)),
+                       "rescale")
+            cur, pm, limbs = out, po, limbs - 1
+            scales = [s / ql for s in scales]
+        return self._wrap_batch(cur, level - drops, scales)
 
     def mult_plain(self, ct: CipherVec, p: PlainVec) -> CipherVec:
         self._check(ct)
@@ -823,13 +829,19 @@ class GpuEngine:
         return self._wrap_batch(out, level - 1, [s_out] * n_out)
 
     def lincomb_grouped(self, inputs: Sequence[CipherVec], term_ptr, term_col, term_tap, out_base, out_stride: int,
-                        weights, n_out: int, bias=None, out_scale: float | None = None) -> list[CipherVec]:
+                        weights, n_out: int, bias=None, out_scale: float | None = None,
+                        weight_scale: float | None = None) -> list[CipherVec]:
         """Grouped linear combination (he_lincomb_grouped) + rescale + bias.
 
         Group g (an output pixel) gathers inputs col[t] (t in its term range)
         and produces M = weights.shape[0] outputs
         out[out_base[g] + m * out_stride] = sum_t weights[m, tap[t]] * in[col[t]].
         All inputs must share one scale; weights are encoded like lincomb().
+
+        With ``weight_scale`` the rescale is DEFERRED: weights are encoded as
+        round(w * weight_scale), nothing is rescaled, and the outputs keep the
+        input level at scale s_in * weight_scale (the caller drops the extra
+        prime later -- run_cnn does it after the activation's relinearisation).
         """
         for c in inputs:
             self._check(c)
@@ -843,8 +855,13 @@ class GpuEngine:
         w = np.asarray(weights, np.float64)
         M, T = w.shape
         ql = self.moduli[limbs - 1]
-        s_out = float(out_scale) if out_scale is not None else s_in
-        wf = w * (ql * s_out) / s_in
+        deferred = weight_scale is not None
+        if deferred:
+            s_out = s_in * float(weight_scale)
+            wf = w * float(weight_scale)
+        else:
+            s_out = float(out_scale) if out_scale is not None else s_in
+            wf = w * (ql * s_out) / s_in
         if np.any(np.abs(wf) >= 2.0 ** 62):
             raise HebatchError("lincomb weight too large for the int64 encoding (|w * q| >= 2^62)")
         wi = np.ascontiguousarray(np.rint(wf).astype(np.int64))
@@ -862,20 +879,25 @@ class GpuEngine:
                               _lib.addr(pacc), n_out, len(ob), _lib.addr(tp), _lib.addr(tc), _lib.addr(tt),
                               _lib.addr(ob), int(out_stride), M, T, _lib.addr(wi), limbs, 2, self.stream,
                               units=((n_used + n_out) * poly * 8.0, float(len(tc)) * M * poly)), "lincomb_grouped")
-        out = self._alloc(n_out, 2, limbs - 1)
-        pout = self._tptrs(out)
-        _lib.check(self._call("rescale", self._L.he_rescale, self._h, _lib.addr(pacc), _lib.addr(pout), n_out, limbs,
-                              2, self.stream, units=(n_out * (2 * limbs - 1) * 2 * self.N * 8.0, 0.0)), "rescale")
-        del acc
+        if deferred:
+            out, pout, out_limbs = acc, pacc, limbs
+        else:
+            out = self._alloc(n_out, 2, limbs - 1)
+            pout = self._tptrs(out)
+            _lib.check(self._call("rescale", self._L.he_rescale, self._h, _lib.addr(pacc), _lib.addr(pout), n_out,
+                                  limbs, 2, self.stream, units=(n_out * (2 * limbs - 1) * 2 * self.N * 8.0, 0.0)),
+                       "rescale")
+            del acc
+            out_limbs = limbs - 1
         if bias is not None:
             b = np.asarray(bias, np.float64)
-            res = np.array([self._res(int(np.rint(bv * s_out)), limbs - 1) for bv in b], np.uint64)
+            res = np.array([self._res(int(np.rint(bv * s_out)), out_limbs) for bv in b], np.uint64)
             _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pout), _lib.addr(pout), n_out,
-                                  limbs - 1, 2, _lib.addr(res), self.stream,
-                                  units=(n_out * 2.0 * (limbs - 1) * self.N * 8, 0.0)), "bias")
+                                  out_limbs, 2, _lib.addr(res), self.stream,
+                                  units=(n_out * 2.0 * out_limbs * self.N * 8, 0.0)), "bias")
         self._acct.bump("plain_mults", int(len(tc)) * M)
         self._acct.bump("adds", int(len(tc)) * M)
-        return self._wrap_batch(out, level - 1, [s_out] * n_out)
+        return self._wrap_batch(out, out_limbs - 1, [s_out] * n_out)
 
     def lincomb_int(self, inputs: Sequence[CipherVec], row_ptr, col, int_weights, out_scale: float,
                     count_adds: bool = True) -> list[CipherVec]:

@@ -189,7 +189,7 @@ def apply_activation(engine, cts, act: Activation, lazy: bool = False):
 
 # ---------------------------------------------------------------- layer calls
 def fm_conv3x3(engine, inputs, weights, bias, H, W, out_channels=None, fold=(1.0, 0.0), out_scale=None,
-               rows=None):
+               rows=None, weight_scale=None):
     """Feature-major 3x3 / pad-1 convolution (+ folded affine).
 
     inputs: p*H*W ciphertexts indexed i*H*W + y*W + x.  Returns the outputs
@@ -210,8 +210,18 @@ def fm_conv3x3(engine, inputs, weights, bias, H, W, out_channels=None, fold=(1.0
         wm = a * w[ch].reshape(len(ch), p * 9)
         bias_out = np.repeat(a * np.asarray(bias, np.float64)[ch] + b, npix)
         out.extend(engine.lincomb_grouped(inputs, tp, col, tap, np.arange(npix), npix, wm, len(ch) * npix,
-                                          bias=bias_out, out_scale=out_scale or engine.context.scale))
+                                          bias=bias_out, out_scale=out_scale or engine.context.scale,
+                                          weight_scale=weight_scale))
     return out
+
+
+def deferred_weight_scale(engine, cts) -> float:
+    """Weight scale for a deferred-rescale conv feeding a degree-2 activation:
+    (s_in * dw)^2 / (q_{l-1} q_{l-2}) = Delta, so after the activation's
+    relinearisation two dropped primes bring the scale back to Delta."""
+    limbs = cts[0].level + 1
+    q1, q2 = engine.moduli[limbs - 1], engine.moduli[limbs - 2]
+    return math.sqrt(engine.context.scale * q1 * q2) / cts[0].scale
 
 
 def fm_avgpool2x2(engine, inputs, C, H, W):
@@ -310,11 +320,15 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
         Ho, Wo = (H // 2, W // 2) if pool else (H, W)
         nxt = [None] * (q * Ho * Wo) if not last else None
         gap = None
+        lazy = lazy_relin and (pool or last)
+        # deferred rescale: the conv output keeps its level (weights at ~2^20),
+        # the activation's summed products drop two primes after relinearising
+        defer = lazy and spec.act.degree == 2
+        dw = deferred_weight_scale(engine, cur) if defer else None
         for r0 in range(0, H, R):
             rows = list(range(r0, min(H, r0 + R)))
             nr = len(rows)
-            y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows)   # [o][r][x]
-            lazy = lazy_relin and (pool or last)
+            y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw)   # [o][r][x]
             z = apply_activation(engine, y, spec.act, lazy=lazy)
             engine.release(*y)
             if last:
@@ -336,7 +350,7 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
                 z = zp
                 nr //= 2
             if lazy:
-                zr = engine.relin_rescale_batch(z)
+                zr = engine.relin_rescale_batch(z, drops=2 if defer else 1)
                 engine.release(*z)
                 z = zr
             y0 = rows[0] // 2 if pool else rows[0]
@@ -347,7 +361,7 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
         if blk > 0 or release_inputs:
             engine.release(*cur)
         if last and lazy_relin:
-            g2 = engine.relin_rescale_batch(gap)
+            g2 = engine.relin_rescale_batch(gap, drops=2 if defer else 1)
             engine.release(*gap)
             gap = g2
         cur = gap if last else nxt

@@ -136,6 +136,38 @@ def conv3x3(orc, ins, w, bias, H, W, fold_ab, out_scale):
     return lincomb(orc, ins, rows, cols, ws, bias=bias_out, out_scale=out_scale)
 
 
+def conv3x3_deferred(orc, ins, w, bias, H, W, fold_ab, target_scale):
+    """fm_conv3x3(weight_scale=deferred_weight_scale(...)) restated: integer
+    weights round(a w dw), NO rescale, bias at s_in dw."""
+    from paper_2604_16834_b200.featuremajor import conv3x3_groups
+
+    q, p = w.shape[:2]
+    a, b = fold_ab
+    ell = ins[0].ell
+    s_in = ins[0].scale
+    dw = math.sqrt(target_scale * orc.moduli[ell - 1] * orc.moduli[ell - 2]) / s_in
+    tp, col, tap, npix = conv3x3_groups(p, H, W)
+    wi = np.rint((a * w.reshape(q, p * 9)) * dw).astype(np.int64)
+    rows, cols, ws = [0], [], []
+    for m in range(q):
+        for g in range(npix):
+            for t in range(tp[g], tp[g + 1]):
+                cols.append(col[t])
+                ws.append(wi[m, tap[t]])
+            rows.append(len(cols))
+    acc = orc.lincomb([np.ascontiguousarray(c.data) for c in ins], rows, cols, ws)
+    s_out = s_in * dw
+    bias_out = np.repeat(a * np.asarray(bias, np.float64) + b, npix)
+    return [OracleCts(orc.add_const(x, residues(np.rint(bias_out[o] * s_out), orc.moduli, ell)), s_out)
+            for o, x in enumerate(acc)]
+
+
+def relin_rescale2(orc, rk, a):
+    r = orc.rescale(orc.relin(np.ascontiguousarray(a.data), rk))
+    s = a.scale / orc.moduli[a.ell - 1]
+    return OracleCts(orc.rescale(r), s / orc.moduli[a.ell - 2])
+
+
 def encrypt_features(orc, feats, base_index=0):
     """feature-major packing: column f of feats -> ciphertext f."""
     return [OracleCts(orc.encrypt(feats[:, f], base_index + f), orc.scale) for f in range(feats.shape[1])]

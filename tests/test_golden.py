@@ -112,6 +112,17 @@ def test_small_cnn_oracle_ckks_decrypts_to_reference():
     out = ON.lincomb(orc, gl, rows, cols, wts.dense[0].reshape(-1), bias=np.zeros(5), out_scale=s)
     got = np.stack([orc.decrypt(o.data, o.scale) for o in out], axis=1)
     assert np.max(np.abs(got - g["logits"])) < 1e-3
+    # deferred-rescale plan (run_cnn default): conv at weight scale ~2^20, no
+    # rescale; lazy square; GAP; relin; drop two primes; dense
+    yd = ON.conv3x3_deferred(orc, x, w1, np.zeros(3), 4, 4, ON.fold(spec.act.coeffs), s)
+    assert yd[0].ell == 4
+    zd = ON.activation_lazy(orc, yd, spec.act.coeffs)
+    gd = ON.lincomb_int(orc, zd, rp, cols_g, 16 * zd[0].scale)
+    gd = [ON.relin_rescale2(orc, rk, c) for c in gd]
+    out = ON.lincomb(orc, gd, rows, cols, wts.dense[0].reshape(-1), bias=np.zeros(5), out_scale=s)
+    got = np.stack([orc.decrypt(o.data, o.scale) for o in out], axis=1)
+    assert out[0].ell == 1
+    assert np.max(np.abs(got - g["logits"])) < 1e-3
 
 
 def test_spec_examples_fixture_is_the_reference_behaviour():

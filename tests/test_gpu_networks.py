@@ -141,6 +141,22 @@ def test_cfg3_network_decrypt_and_sampled_bit_exact():
     orr = ON.relin_rescale(orc, rk, op)
     assert np.array_equal(to_np(r.data), orr.data) and r.scale == orr.scale
     eng.release(*y, *sq)
+    # deferred-rescale conv (run_cnn's default for layers feeding pool / GAP)
+    from paper_2604_16834_b200.featuremajor import deferred_weight_scale
+
+    dw = deferred_weight_scale(eng, x)
+    yd = fm_conv3x3(eng, x, w1, b1, 32, 32, out_channels=[5], fold=(a, b), weight_scale=dw)
+    yy, xx = 13, 31
+    terms = [(i, yy + dy, xx + dx, dy, dx) for i in range(3) for dy in (-1, 0, 1) for dx in (-1, 0, 1)
+             if 0 <= yy + dy < 32 and 0 <= xx + dx < 32]
+    ins = [to_np(x[i * 1024 + py * 32 + px].data) for (i, py, px, _, _) in terms]
+    wi = np.rint(np.array([a * w1[5, i, dy + 1, dx + 1] for (i, _, _, dy, dx) in terms]) * dw).astype(np.int64)
+    acc = orc.lincomb(ins, [0, len(terms)], list(range(len(terms))), wi)[0]
+    so = x[0].scale * dw
+    acc = orc.add_const(acc, [int(np.rint((a * b1[5] + b) * so)) % m for m in eng.moduli[:14]])
+    assert yd[yy * 32 + xx].level == 13 and yd[0].scale == so
+    assert np.array_equal(to_np(yd[yy * 32 + xx].data), acc)
+    eng.release(*yd)
     # full network, decrypt-level
     out = run_cnn(eng, x, spec, wts)
     got = eng.decrypt_batch(out).T
