@@ -163,6 +163,14 @@ int he_lincomb_grouped(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_
                        const int32_t *out_base, int out_stride, int M, int T, const int64_t *weights, int ell,
                        int n_comp, void *stream);
 
+/* lazy degree-2 activation fused with a pooling / GAP sum (feature-major):
+ *   out[o] = sum_{t in [row_ptr[o], row_ptr[o+1])} in[col[t]] (x) in[col[t]]  (+ residues[o] on c0)
+ * (x) = tensor product without relinearisation: inputs [2][ell][N], outputs
+ * [3][ell][N], no rescale.  residues: host [n_out][ell] or NULL.  Identical to
+ * he_tensor + he_add_const per input followed by a unit-weight he_lincomb. */
+int he_square_sum(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
+                  const int32_t *row_ptr, const int32_t *col, const uint64_t *residues, int ell, void *stream);
+
 /* block until all work on `stream` is done; returns HE_ECUDA on async error */
 int he_sync(void *stream);
 /* number of kernels this library has launched in the process (bench evidence) */

@@ -184,7 +184,108 @@ int dispatch_grouped(int MM, bool fast, dim3 grid, size_t smem, cudaStream_t s, 
     }
 }
 
+// Sum of squares over groups (lazy degree-2 activation fused with the pool /
+// GAP sum):  out[o] = sum_{t in row o} in[col_t] (x) in[col_t]  + cres[o],
+// where (x) is the tensor product (d0, d1, d2) = (x0^2, 2 x0 x1, x1^2) and
+// cres is added to d0.  Bit-identical to he_tensor + he_add_const per input
+// followed by the unit-weight he_lincomb (all steps are exact mod q).
+// One thread = one (limb, coefficient) of one output; inputs [2][ell][N],
+// outputs [3][ell][N].
+__global__ void __launch_bounds__(LB) k_square_sum(uint64_t *const *out, const uint64_t *const *in,
+                                                   const int32_t *row_ptr, const int32_t *col, const uint64_t *cres,
+                                                   int n_out, int ell, int logN, int kmax, const ModConst *mc) {
+    const size_t N = (size_t)1 << logN;
+    const int cpp = (int)(N / LB);
+    const int l = blockIdx.y / cpp;
+    const size_t k = (size_t)(blockIdx.y % cpp) * LB + threadIdx.x;
+    const size_t o0 = (size_t)l * N + k, o1 = ((size_t)ell + l) * N + k;
+    const ModConst c = mc[l];
+    const bool fold = (double)(2 * kmax) * (double)c.q >= 1.8e19;
+    const int o = blockIdx.x;
+    u128 a0 = {0, 0}, a1 = {0, 0}, a2 = {0, 0};
+    for (int t = row_ptr[o]; t < row_ptr[o + 1]; t++) {
+        const uint64_t *x = in[col[t]];
+        const uint64_t x0 = __ldg(x + o0), x1 = __ldg(x + o1);
+        mac128(a0, x0, x0);
+        mac128(a1, x0, x1);
+        mac128(a1, x0, x1);
+        mac128(a2, x1, x1);
+        if (fold) {
+            if (a0.hi >= c.q) a0.hi -= c.q;
+            if (a1.hi >= c.q) a1.hi -= c.q;
+            if (a1.hi >= c.q) a1.hi -= c.q;
+            if (a2.hi >= c.q) a2.hi -= c.q;
+        }
+    }
+    // redc gives sum * 2^-64; one more Montgomery product with R^2 restores it
+    uint64_t d[3] = {redc(a0.hi, a0.lo, c.q, c.qinv), redc(a1.hi, a1.lo, c.q, c.qinv),
+                     redc(a2.hi, a2.lo, c.q, c.qinv)};
+    uint64_t *O = out[o];
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        uint64_t v = redc(mulhi(d[j], c.r2), d[j] * c.r2, c.q, c.qinv);
+        if (j == 0 && cres) v = add_mod(v, cres[(size_t)o * ell + l], c.q);
+        O[((size_t)j * ell + l) * N + k] = v;
+    }
+}
+
 }  // namespace
+
+extern "C" int he_square_sum(he_ctx *c, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
+                             const int32_t *row_ptr, const int32_t *col, const uint64_t *residues, int ell,
+                             void *stream) {
+    if (!c || n_in < 1 || n_out < 0 || ell < 1 || ell > c->L || !row_ptr || !col || c->N < LB) {
+        he_set_error("he_square_sum: bad arguments");
+        return HE_EINVAL;
+    }
+    if (!n_out) return HE_OK;
+    const int nnz = row_ptr[n_out];
+    int kmax = 0;
+    for (int o = 0; o < n_out; o++) {
+        if (row_ptr[o + 1] < row_ptr[o]) {
+            he_set_error("he_square_sum: row_ptr not monotone");
+            return HE_EINVAL;
+        }
+        kmax = std::max(kmax, row_ptr[o + 1] - row_ptr[o]);
+    }
+    for (int t = 0; t < nnz; t++)
+        if (col[t] < 0 || col[t] >= n_in) {
+            he_set_error("he_square_sum: col[%d] out of range", t);
+            return HE_EINVAL;
+        }
+    if (residues)
+        for (int i = 0; i < n_out * ell; i++)
+            if (residues[i] >= c->mod[i % ell]) {
+                he_set_error("he_square_sum: residue %d not canonical", i);
+                return HE_EINVAL;
+            }
+    cudaStream_t s = (cudaStream_t)stream;
+    void **din = nullptr, **dout = nullptr;
+    HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
+    HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
+    char *meta = nullptr;
+    size_t b_rp = (size_t)(n_out + 1) * 4, b_col = (size_t)std::max(nnz, 1) * 4, b_res = (size_t)n_out * ell * 8;
+    HE_TRY(he_scratch_alloc((void **)&meta, b_res + b_rp + b_col + 64, s));
+    uint64_t *dres = residues ? (uint64_t *)meta : nullptr;
+    int32_t *drp = (int32_t *)(meta + b_res), *dcol = (int32_t *)(meta + b_res + b_rp);
+    if (residues) HE_CHECK_CUDA(cudaMemcpyAsync(dres, residues, b_res, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(cudaMemcpyAsync(drp, row_ptr, b_rp, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(cudaMemcpyAsync(dcol, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s));
+    int rc = HE_OK;
+    const int cpp = c->N / LB;
+    for (int o0 = 0; o0 < n_out && rc == HE_OK; o0 += 65535) {
+        const int cnt = std::min(65535, n_out - o0);
+        dim3 grid((unsigned)cnt, (unsigned)(ell * cpp));
+        k_square_sum<<<grid, LB, 0, s>>>((uint64_t *const *)dout + o0, (const uint64_t *const *)din, drp + o0, dcol,
+                                         dres ? dres + (size_t)o0 * ell : nullptr, cnt, ell, c->logN, kmax, c->d_mc);
+        he_count_launch(1);
+        if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+    }
+    he_scratch_free(meta, s);
+    he_scratch_free(din, s);
+    he_scratch_free(dout, s);
+    return rc;
+}
 
 extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
                                   int n_groups, const int32_t *term_ptr, const int32_t *term_col,

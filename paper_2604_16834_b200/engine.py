@@ -635,6 +635,37 @@ class GpuEngine:
                               len(A), limbs, self.stream, units=(len(A) * 7.0 * limbs * self.N * 8, 0.0)), "tensor")
         return self._wrap_batch(out, level, [a.scale * b.scale for a, b in zip(A, B)])
 
+    def square_sum_batch(self, inputs: Sequence[CipherVec], row_ptr, col, const: float,
+                         scale_mult: float) -> list[CipherVec]:
+        """out[o] = sum_{t in row o} (in[col_t]^2 + const), unrelinearised (3
+        components), not rescaled; declared scale s_in^2 * scale_mult (pool: 4,
+        GAP: pixel count).  Equals tensor_batch + add_const_batch + lincomb_int."""
+        for c in inputs:
+            self._check(c)
+        s = inputs[0].scale
+        if any(c.scale != s for c in inputs):
+            raise ScaleMismatch("square_sum_batch needs inputs at one scale")
+        level = min(c.level for c in inputs)
+        limbs = level + 1
+        rp = np.ascontiguousarray(row_ptr, np.int32)
+        cl = np.ascontiguousarray(col, np.int32)
+        n_out = len(rp) - 1
+        cnt = np.diff(rp)
+        C = int(np.rint(const * (s * s)))                 # add_const_batch's residue per square
+        res = np.array([self._res(int(k) * C, limbs) for k in cnt], np.uint64) if const else None
+        tins = self._at_level(inputs, level)
+        pin = _lib.ptr_array([t.data_ptr() for t in tins])
+        out = self._alloc(n_out, 3, limbs)
+        pout = self._tptrs(out)
+        _lib.check(self._call("square_sum", self._L.he_square_sum, self._h, _lib.addr(pin), len(inputs),
+                              _lib.addr(pout), n_out, _lib.addr(rp), _lib.addr(cl),
+                              _lib.addr(res) if res is not None else None, limbs, self.stream,
+                              units=((len(np.unique(cl)) * 2 + n_out * 3) * limbs * self.N * 8.0,
+                                     4.0 * len(cl) * limbs * self.N)), "square_sum")
+        self._acct.bump("ct_mults", int(len(cl)))
+        self._acct.bump("adds", int(len(cl)) + max(0, int(len(cl)) - n_out))
+        return self._wrap_batch(out, level, [s * s * scale_mult] * n_out)
+
     def relin_rescale_batch(self, cts: Sequence[CipherVec], drops: int = 1) -> list[CipherVec]:
         """3-component ciphertexts -> relinearise (key switch of c2) -> rescale
         ``drops`` times (2 after a deferred-rescale linear layer)."""
@@ -817,7 +848,7 @@ class GpuEngine:
         _lib.check(self._call("rescale", self._L.he_rescale, self._h, _lib.addr(pacc), _lib.addr(pout), n_out, limbs,
                               2, self.stream, units=(n_out * (2 * limbs - 1) * 2 * self.N * 8.0, 0.0)), "rescale")
         del acc
-        if bias is not None:
+        if bias is not None and np.any(np.asarray(bias) != 0):  # adding zero residues is a no-op
             b = np.asarray(bias, np.float64)
             res = np.array([self._res(int(np.rint(bv * s_out)), limbs - 1) for bv in b], np.uint64)
             _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pout), _lib.addr(pout), n_out,
@@ -889,7 +920,7 @@ class GpuEngine:
                        "rescale")
             del acc
             out_limbs = limbs - 1
-        if bias is not None:
+        if bias is not None and np.any(np.asarray(bias) != 0):  # adding zero residues is a no-op
             b = np.asarray(bias, np.float64)
             res = np.array([self._res(int(np.rint(bv * s_out)), out_limbs) for bv in b], np.uint64)
             _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pout), _lib.addr(pout), n_out,

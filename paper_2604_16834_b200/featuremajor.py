@@ -329,6 +329,34 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
             rows = list(range(r0, min(H, r0 + R)))
             nr = len(rows)
             y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw)   # [o][r][x]
+            if lazy and spec.act.degree == 2:
+                # fused: square (no relin) + constant + pool / GAP sum, one pass
+                c0, c1, c2 = spec.act.coeffs
+                cst = c0 - c1 * c1 / (4 * c2)
+                if last:
+                    rp, cols = gap_csr(q, nr * W)
+                    part = engine.square_sum_batch(y, rp, cols, cst, H * W)
+                else:
+                    rp, cols = pool2x2_csr(q, nr, W)
+                    part = engine.square_sum_batch(y, rp, cols, cst, 4.0)
+                engine.release(*y)
+                if last:
+                    if gap is None:
+                        gap = part
+                    else:
+                        nsum = engine.add_batch(gap, part)
+                        engine.release(*gap, *part)
+                        gap = nsum
+                    continue
+                z = engine.relin_rescale_batch(part, drops=2 if defer else 1)
+                engine.release(*part)
+                nr //= 2
+                y0 = rows[0] // 2
+                for o in range(q):
+                    for r in range(nr):
+                        for x in range(Wo):
+                            nxt[o * Ho * Wo + (y0 + r) * Wo + x] = z[(o * nr + r) * Wo + x]
+                continue
             z = apply_activation(engine, y, spec.act, lazy=lazy)
             engine.release(*y)
             if last:
