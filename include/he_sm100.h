@@ -157,11 +157,13 @@ int he_lincomb(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *const
  *   out[out_base[g] + m*out_stride] = sum_{t in group g} weights[m*T + tap[t]] * in[col[t]]
  * for m < M (M <= 32), mod q_i.  term_ptr [n_groups+1], col/tap [nnz],
  * out_base [n_groups], weights [M][T] signed int64; all host arrays.
- * Not rescaled.  Same semantics as expanding the groups into he_lincomb. */
+ * residues: [M][ell] constant added to component 0 of channel m, or NULL.
+ * Not rescaled.  Same semantics as expanding the groups into he_lincomb
+ * (+ he_add_const). */
 int he_lincomb_grouped(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
                        int n_groups, const int32_t *term_ptr, const int32_t *term_col, const int32_t *term_tap,
-                       const int32_t *out_base, int out_stride, int M, int T, const int64_t *weights, int ell,
-                       int n_comp, void *stream);
+                       const int32_t *out_base, int out_stride, int M, int T, const int64_t *weights,
+                       const uint64_t *residues, int ell, int n_comp, void *stream);
 
 /* lazy degree-2 activation fused with a pooling / GAP sum (feature-major):
  *   out[o] = sum_{t in [row_ptr[o], row_ptr[o+1])} in[col[t]] (x) in[col[t]]  (+ residues[o] on c0)

@@ -102,7 +102,7 @@ def load():
         "he_lincomb": (i, [vp, pp, i, pp, i, vp, vp, vp, i, i, vp]),
         "he_sync": (i, [vp]),
         "he_launch_count": (C.c_ulonglong, []),
-        "he_lincomb_grouped": (i, [vp, pp, i, pp, i, i, vp, vp, vp, vp, i, i, i, vp, i, i, vp]),
+        "he_lincomb_grouped": (i, [vp, pp, i, pp, i, i, vp, vp, vp, vp, i, i, i, vp, vp, i, i, vp]),
         "he_microbench_intpipe": (i, [i, vp]),
         "he_square_sum": (i, [vp, pp, i, pp, i, vp, vp, vp, i, vp]),
     }

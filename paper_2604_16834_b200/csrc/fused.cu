@@ -201,7 +201,7 @@ struct IpArgs {
     int ell, ext_n, beta, alpha, L, M;
 };
 
-__global__ void __launch_bounds__(NTT_TPB) k_modup_ip(const IpArgs a) {
+__global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
     __shared__ uint64_t sm[16 * 272];
     const int rt = blockIdx.x & 15, bt = blockIdx.x >> 4;
     const int t = bt % a.ext_n, b = bt / a.ext_n;

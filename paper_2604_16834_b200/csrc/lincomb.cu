@@ -55,6 +55,7 @@ struct GroupArgs {
     const int32_t *term_ptr;
     const Term *terms;
     const int32_t *out_base;
+    const uint64_t *cres;  // [M][ell] constant added to component 0 of output channel m, or nullptr
     const uint64_t *wM;  // [ell][T][WS] Montgomery weights
     const ModConst *mc;
     int out_stride, M, T, WS, n_groups, gpb, ell, logN, kmax;
@@ -151,7 +152,9 @@ __global__ void __launch_bounds__(LB) k_lincomb_grouped(const GroupArgs a) {
             // hi < q: either folded per term, or kmax * q < 2^64 bounds the sum
             if (a.m_off + m < a.M) {
                 const u128 sm = acc[m].sum();
-                a.out[ob + m * a.out_stride][off] = redc(sm.hi, sm.lo, c.q, c.qinv);
+                uint64_t v = redc(sm.hi, sm.lo, c.q, c.qinv);
+                if (a.cres && comp == 0) v = add_mod(v, a.cres[(size_t)(a.m_off + m) * a.ell + l], c.q);
+                a.out[ob + m * a.out_stride][off] = v;
             }
         }
     }
@@ -290,7 +293,8 @@ extern "C" int he_square_sum(he_ctx *c, const uint64_t *const *in, int n_in, uin
 extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
                                   int n_groups, const int32_t *term_ptr, const int32_t *term_col,
                                   const int32_t *term_tap, const int32_t *out_base, int out_stride, int M, int T,
-                                  const int64_t *weights, int ell, int nc, void *stream) {
+                                  const int64_t *weights, const uint64_t *residues, int ell, int nc,
+                                  void *stream) {
     if (!c || n_in < 1 || n_out < 0 || n_groups < 0 || M < 1 || M > 32 || T < 1 || ell < 1 || ell > c->L ||
         nc < 1 || nc > 3 || !term_ptr || !term_col || !term_tap || !out_base || !weights) {
         he_set_error("he_lincomb_grouped: bad arguments (M=%d T=%d ell=%d)", M, T, ell);
@@ -337,10 +341,19 @@ extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in
     cudaStream_t s = (cudaStream_t)stream;
     void **dout = nullptr;
     HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
+    if (residues)
+        for (int i = 0; i < M * ell; i++)
+            if (residues[i] >= c->mod[i % ell]) {
+                he_set_error("he_lincomb_grouped: residue %d not canonical", i);
+                return HE_EINVAL;
+            }
     size_t b_tp = (size_t)(n_groups + 1) * 4, b_terms = terms.size() * sizeof(Term), b_ob = (size_t)n_groups * 4,
-           b_w = (size_t)M * T * 8, b_wM = (size_t)ell * T * MM * 8;
+           b_w = (size_t)M * T * 8, b_wM = (size_t)ell * T * MM * 8, b_res = (size_t)M * ell * 8;
     char *meta = nullptr;
-    HE_TRY(he_scratch_alloc((void **)&meta, b_wM + b_terms + b_w + b_tp + b_ob + 64, s));
+    HE_TRY(he_scratch_alloc((void **)&meta, b_wM + b_terms + b_w + b_tp + b_ob + b_res + 64, s));
+    uint64_t *dres =
+        residues ? (uint64_t *)(meta + ((b_wM + b_terms + b_w + b_tp + b_ob + 7) & ~(size_t)7)) : nullptr;
+    if (residues) HE_CHECK_CUDA(cudaMemcpyAsync(dres, residues, b_res, cudaMemcpyHostToDevice, s));
     uint64_t *wM = (uint64_t *)meta;
     Term *dterms = (Term *)(meta + b_wM);
     int64_t *dw = (int64_t *)(meta + b_wM + b_terms);
@@ -376,6 +389,7 @@ extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in
     a.out_base = dob;
     a.wM = wM;
     a.mc = c->d_mc;
+    a.cres = dres;
     a.out_stride = out_stride;
     a.M = M;
     a.T = T;

@@ -906,12 +906,20 @@ class GpuEngine:
         pacc = self._tptrs(acc)
         poly = 2 * limbs * self.N
         n_used = len(np.unique(tc))
+        # bias: one value per output channel m; zero residues are a no-op
+        b = None if bias is None else np.asarray(bias, np.float64).reshape(M)
+        has_bias = b is not None and bool(np.any(b != 0))
+        out_limbs = limbs if deferred else limbs - 1
+        ch_res = (np.array([self._res(int(np.rint(bv * s_out)), out_limbs) for bv in b], np.uint64)
+                  if has_bias else None)
+        fused_res = ch_res if (deferred and has_bias) else None     # added inside the lincomb store
         _lib.check(self._call("lincomb", self._L.he_lincomb_grouped, self._h, _lib.addr(pin), len(inputs),
                               _lib.addr(pacc), n_out, len(ob), _lib.addr(tp), _lib.addr(tc), _lib.addr(tt),
-                              _lib.addr(ob), int(out_stride), M, T, _lib.addr(wi), limbs, 2, self.stream,
+                              _lib.addr(ob), int(out_stride), M, T, _lib.addr(wi),
+                              _lib.addr(fused_res) if fused_res is not None else None, limbs, 2, self.stream,
                               units=((n_used + n_out) * poly * 8.0, float(len(tc)) * M * poly)), "lincomb_grouped")
         if deferred:
-            out, pout, out_limbs = acc, pacc, limbs
+            out, pout = acc, pacc
         else:
             out = self._alloc(n_out, 2, limbs - 1)
             pout = self._tptrs(out)
@@ -919,13 +927,13 @@ class GpuEngine:
                                   limbs, 2, self.stream, units=(n_out * (2 * limbs - 1) * 2 * self.N * 8.0, 0.0)),
                        "rescale")
             del acc
-            out_limbs = limbs - 1
-        if bias is not None and np.any(np.asarray(bias) != 0):  # adding zero residues is a no-op
-            b = np.asarray(bias, np.float64)
-            res = np.array([self._res(int(np.rint(bv * s_out)), out_limbs) for bv in b], np.uint64)
-            _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pout), _lib.addr(pout), n_out,
-                                  out_limbs, 2, _lib.addr(res), self.stream,
-                                  units=(n_out * 2.0 * out_limbs * self.N * 8, 0.0)), "bias")
+            if has_bias:  # after the rescale, at the output scale
+                res = np.zeros((n_out, out_limbs), np.uint64)
+                for m in range(M):
+                    res[ob + m * int(out_stride)] = ch_res[m]
+                _lib.check(self._call("add_const", self._L.he_add_const, self._h, _lib.addr(pout), _lib.addr(pout),
+                                      n_out, out_limbs, 2, _lib.addr(res), self.stream,
+                                      units=(n_out * 2.0 * out_limbs * self.N * 8, 0.0)), "bias")
         self._acct.bump("plain_mults", int(len(tc)) * M)
         self._acct.bump("adds", int(len(tc)) * M)
         return self._wrap_batch(out, out_limbs - 1, [s_out] * n_out)

@@ -208,9 +208,9 @@ def fm_conv3x3(engine, inputs, weights, bias, H, W, out_channels=None, fold=(1.0
     for c0 in range(0, len(oc), 32):
         ch = oc[c0:c0 + 32]
         wm = a * w[ch].reshape(len(ch), p * 9)
-        bias_out = np.repeat(a * np.asarray(bias, np.float64)[ch] + b, npix)
+        bias_ch = a * np.asarray(bias, np.float64)[ch] + b             # one value per output channel
         out.extend(engine.lincomb_grouped(inputs, tp, col, tap, np.arange(npix), npix, wm, len(ch) * npix,
-                                          bias=bias_out, out_scale=out_scale or engine.context.scale,
+                                          bias=bias_ch, out_scale=out_scale or engine.context.scale,
                                           weight_scale=weight_scale))
     return out
 
