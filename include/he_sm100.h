@@ -165,6 +165,16 @@ int he_lincomb_grouped(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_
                        const int32_t *out_base, int out_stride, int M, int T, const int64_t *weights,
                        const uint64_t *residues, int ell, int n_comp, void *stream);
 
+/* tensor-core form of he_lincomb_grouped for convolutions: every group has
+ * exactly T tap slots, gcol [n_groups][T] = input index or -1 (zero tap):
+ *   out[out_base[g] + m*out_stride] = sum_t weights[m][t] * in[gcol[g][t]] mod q_i
+ * (+ residues[m][i] on component 0).  Exact int8 digit decomposition on
+ * mma.sync u8 x s8 -> s32; needs |weights| < 2^31 and ceil(M*E/8) <= 12
+ * (E = signed byte digits of the largest weight), else HE_EINVAL. */
+int he_conv_mma(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out, int n_groups,
+                const int32_t *gcol, const int32_t *out_base, int out_stride, int M, int T, const int64_t *weights,
+                const uint64_t *residues, int ell, int n_comp, void *stream);
+
 /* lazy degree-2 activation fused with a pooling / GAP sum (feature-major):
  *   out[o] = sum_{t in [row_ptr[o], row_ptr[o+1])} in[col[t]] (x) in[col[t]]  (+ residues[o] on c0)
  * (x) = tensor product without relinearisation: inputs [2][ell][N], outputs

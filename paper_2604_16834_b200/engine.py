@@ -354,6 +354,8 @@ class GpuEngine:
         self.registration_log: list[frozenset] = []
         self._relin = False
         self._timing = None  # {category: [(start_event, end_event, units)]} when enabled
+        # exact int8-digit tensor-core convolutions (he_conv_mma); False = CUDA-core kernel
+        self.use_tensor_cores = True
 
     # ------------------------------------------------------------ timing hooks (bench.py)
     def enable_timing(self, on: bool = True) -> None:
@@ -937,6 +939,51 @@ class GpuEngine:
         self._acct.bump("plain_mults", int(len(tc)) * M)
         self._acct.bump("adds", int(len(tc)) * M)
         return self._wrap_batch(out, out_limbs - 1, [s_out] * n_out)
+
+    def conv_mma(self, inputs: Sequence[CipherVec], gcol, out_base, out_stride: int, weights, n_out: int,
+                 weight_scale: float, bias=None) -> list[CipherVec] | None:
+        """Tensor-core (int8-digit, mma.sync) form of a deferred-rescale
+        lincomb_grouped with full tap slots: gcol [G][T] input index or -1.
+        Weights are encoded as round(w * weight_scale) exactly as in
+        lincomb_grouped(weight_scale=...), so the results are bit-identical.
+        Returns None when the tensor-core bounds do not hold (caller falls
+        back to the CUDA-core kernel)."""
+        for c in inputs:
+            self._check(c)
+        s_in = inputs[0].scale
+        if any(c.scale != s_in for c in inputs):
+            raise ScaleMismatch("conv_mma needs inputs at one scale")
+        level = min(c.level for c in inputs)
+        if level < self.context.mult_level_cost:
+            raise LevelExhausted(f"level {level} < multiplication cost {self.context.mult_level_cost}")
+        limbs = level + 1
+        w = np.asarray(weights, np.float64)
+        M, T = w.shape
+        wi = np.ascontiguousarray(np.rint(w * float(weight_scale)).astype(np.int64))
+        if np.abs(wi).max(initial=0) >= 2 ** 31:
+            return None
+        s_out = s_in * float(weight_scale)
+        gc = np.ascontiguousarray(gcol, np.int32)
+        ob = np.ascontiguousarray(out_base, np.int32)
+        b = None if bias is None else np.asarray(bias, np.float64).reshape(M)
+        res = (np.array([self._res(int(np.rint(bv * s_out)), limbs) for bv in b], np.uint64)
+               if b is not None and np.any(b != 0) else None)
+        tins = self._at_level(inputs, level)
+        pin = _lib.ptr_array([t.data_ptr() for t in tins])
+        out = self._alloc(n_out, 2, limbs)
+        pout = self._tptrs(out)
+        poly = 2 * limbs * self.N
+        nnz = int((gc >= 0).sum())
+        rc = self._call("lincomb", self._L.he_conv_mma, self._h, _lib.addr(pin), len(inputs), _lib.addr(pout), n_out,
+                        gc.shape[0], _lib.addr(gc), _lib.addr(ob), int(out_stride), M, T, _lib.addr(wi),
+                        _lib.addr(res) if res is not None else None, limbs, 2, self.stream,
+                        units=((len(np.unique(gc[gc >= 0])) + n_out) * poly * 8.0, float(nnz) * M * poly))
+        if rc == _lib.HE_EINVAL:
+            return None
+        _lib.check(rc, "conv_mma")
+        self._acct.bump("plain_mults", nnz * M)
+        self._acct.bump("adds", nnz * M)
+        return self._wrap_batch(out, level, [s_out] * n_out)
 
     def lincomb_int(self, inputs: Sequence[CipherVec], row_ptr, col, int_weights, out_scale: float,
                     count_adds: bool = True) -> list[CipherVec]:

@@ -204,15 +204,37 @@ def fm_conv3x3(engine, inputs, weights, bias, H, W, out_channels=None, fold=(1.0
     oc = list(range(q)) if out_channels is None else list(out_channels)
     a, b = fold
     tp, col, tap, npix = conv3x3_groups(p, H, W, rows)
+    use_tc = weight_scale is not None and getattr(engine, "use_tensor_cores", False) and engine.N % 128 == 0
+    gcol = conv3x3_fulltaps(p, H, W, rows) if use_tc else None
     out = []
     for c0 in range(0, len(oc), 32):
         ch = oc[c0:c0 + 32]
         wm = a * w[ch].reshape(len(ch), p * 9)
         bias_ch = a * np.asarray(bias, np.float64)[ch] + b             # one value per output channel
-        out.extend(engine.lincomb_grouped(inputs, tp, col, tap, np.arange(npix), npix, wm, len(ch) * npix,
-                                          bias=bias_ch, out_scale=out_scale or engine.context.scale,
-                                          weight_scale=weight_scale))
+        res = None
+        if use_tc:   # exact int8-digit tensor-core path (bit-identical results)
+            res = engine.conv_mma(inputs, gcol, np.arange(npix), npix, wm, len(ch) * npix, weight_scale,
+                                  bias=bias_ch)
+        if res is None:
+            res = engine.lincomb_grouped(inputs, tp, col, tap, np.arange(npix), npix, wm, len(ch) * npix,
+                                         bias=bias_ch, out_scale=out_scale or engine.context.scale,
+                                         weight_scale=weight_scale)
+        out.extend(res)
     return out
+
+
+def conv3x3_fulltaps(p: int, H: int, W: int, rows=None) -> np.ndarray:
+    """[pixels][9p] input index of every tap slot (-1 where the window leaves
+    the image), tap order i*9 + (dy+1)*3 + (dx+1), pixels row-major over rows."""
+    rows = np.arange(H) if rows is None else np.asarray(list(rows))
+    y = rows[:, None, None, None]
+    x = np.arange(W)[None, :, None, None]
+    k = np.arange(9)[None, None, None, :]
+    yy, xx = y + k // 3 - 1, x + k % 3 - 1
+    i = np.arange(p)[None, None, :, None]
+    valid = (yy >= 0) & (yy < H) & (xx >= 0) & (xx < W)
+    col = np.where(valid, i * H * W + yy * W + xx, -1)
+    return np.ascontiguousarray(col.reshape(len(rows) * W, p * 9).astype(np.int32))
 
 
 def deferred_weight_scale(engine, cts) -> float:

@@ -194,6 +194,46 @@ def test_lincomb_grouped_conv_bit_exact(pair):
         assert np.array_equal(to_np(outs[o].data), orc.rescale(acc[o])), o
 
 
+@pytest.mark.parametrize("p,q", [(3, 4), (16, 32)])
+def test_conv_mma_tensor_cores_bit_exact(pair, p, q):
+    """he_conv_mma (int8-digit mma.sync) == CUDA-core he_lincomb_grouped == oracle,
+    deferred-rescale weights, border taps, every limb (incl. 50/60-bit)."""
+    from paper_2604_16834_b200.featuremajor import conv3x3_fulltaps, conv3x3_groups
+
+    name, eng, orc = pair
+    if eng.N < 128 or (name == "cfg2" and p == 16):
+        pytest.skip("tensor-core path needs N >= 128; cfg2 x large case covered by cfg3")
+    rng = np.random.default_rng(31 + p)
+    H = W = 4
+    vals = rng.uniform(-1, 1, (p * H * W, eng.context.n))
+    cts = eng.encrypt_batch(vals)
+    w = rng.normal(0, 1.0 / np.sqrt(9 * p), (q, p, 3, 3))
+    ws = 2.0 ** 20
+    bias = rng.normal(0, 0.3, q)
+    rows = [0, 2, 3]
+    gcol = conv3x3_fulltaps(p, H, W, rows)
+    npix = gcol.shape[0]
+    tc = eng.conv_mma(cts, gcol, np.arange(npix), npix, w.reshape(q, -1), q * npix, ws, bias=bias)
+    assert tc is not None
+    tp, col, tap, _ = conv3x3_groups(p, H, W, rows)
+    cu = eng.lincomb_grouped(cts, tp, col, tap, np.arange(npix), npix, w.reshape(q, -1), q * npix, bias=bias,
+                             weight_scale=ws)
+    for o in range(q * npix):
+        assert np.array_equal(to_np(tc[o].data), to_np(cu[o].data)), o
+        assert tc[o].scale == cu[o].scale and tc[o].level == cu[o].level
+    # oracle on two outputs: integer weights, no rescale, bias at s_in * ws
+    wi = np.rint(w.reshape(q, -1) * ws).astype(np.int64)
+    ins = [to_np(c.data) for c in cts]
+    ell = cts[0].level + 1
+    for o in (0, q * npix - 1):
+        m, g = divmod(o, npix)
+        taps = [t for t in range(p * 9) if gcol[g, t] >= 0]
+        acc = orc.lincomb(ins, [0, len(taps)], [int(gcol[g, t]) for t in taps], [wi[m, t] for t in taps])[0]
+        so = cts[0].scale * ws
+        acc = orc.add_const(acc, [int(np.rint(bias[m] * so)) % mm for mm in eng.moduli[:ell]])
+        assert np.array_equal(to_np(tc[o].data), acc), o
+
+
 def test_lincomb_bit_exact(pair):
     name, eng, orc = pair
     rng = np.random.default_rng(9)

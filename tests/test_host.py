@@ -178,6 +178,12 @@ def test_conv_csr_builders_equal_direct_convolution():
         for gi, (y, xx) in enumerate([(r, c) for r in (2, 3, 5) for c in range(W)]):
             v = sum(wm[m, tap[t]] * feats[col[t]] for t in range(tp[gi], tp[gi + 1]))
             assert np.allclose(v, ref[m * H * W + y * W + xx])
+    from paper_2604_16834_b200.featuremajor import conv3x3_fulltaps
+
+    full = conv3x3_fulltaps(p, H, W, rows=[2, 3, 5])
+    for gi in range(full.shape[0]):
+        valid = [(t, int(full[gi, t])) for t in range(p * 9) if full[gi, t] >= 0]
+        assert valid == [(int(tap[t]), int(col[t])) for t in range(tp[gi], tp[gi + 1])]
     rp, cols = pool2x2_csr(2, 4, 4)
     assert list(cols[:4]) == [0, 1, 4, 5] and len(rp) == 2 * 4 + 1
     rp, cols = gap_csr(2, 9, channel_offset=0)
