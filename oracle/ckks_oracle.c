@@ -753,11 +753,24 @@ void oc_lincomb(const oc_ctx *c, const uint64_t *const *in, uint64_t *const *out
             for (int i = 0; i < ell; i++) {
                 uint64_t q = c->mod[i];
                 uint64_t *y = out[o] + ((size_t)p * ell + i) * N;
-                for (int k = 0; k < N; k++) y[k] = 0;
-                for (int t = row_ptr[o]; t < row_ptr[o + 1]; t++) {
-                    uint64_t wq = smod(w[t], q);
-                    const uint64_t *x = in[col[t]] + ((size_t)p * ell + i) * N;
-                    for (int k = 0; k < N; k++) y[k] = addmod(y[k], mulmod(x[k], wq, q), q);
+                /* exact 128-bit sums of (x * (w mod q)), reduced every 32 terms (x, w < 2^61:
+                 * 32 products < 2^127) -- the same residue as adding mulmod() terms one by one */
+                const int CH = N < 256 ? N : 256;
+                for (int k0 = 0; k0 < N; k0 += CH) {
+                    u128 acc[256];
+                    uint64_t part[256];
+                    for (int k = 0; k < CH; k++) { acc[k] = 0; part[k] = 0; }
+                    int cnt = 0;
+                    for (int t = row_ptr[o]; t < row_ptr[o + 1]; t++) {
+                        uint64_t wq = smod(w[t], q);
+                        const uint64_t *x = in[col[t]] + ((size_t)p * ell + i) * N + k0;
+                        for (int k = 0; k < CH; k++) acc[k] += (u128)x[k] * wq;
+                        if (++cnt == 32) {
+                            for (int k = 0; k < CH; k++) { part[k] = addmod(part[k], (uint64_t)(acc[k] % q), q); acc[k] = 0; }
+                            cnt = 0;
+                        }
+                    }
+                    for (int k = 0; k < CH; k++) y[k0 + k] = addmod(part[k], (uint64_t)(acc[k] % q), q);
                 }
             }
     }

@@ -22,7 +22,10 @@ import oracle as O  # noqa: E402
 
 
 def cfg3_op_counts():
-    """Exact per-group op counts of the frozen config-3 plan (featuremajor.run_cnn)."""
+    """Exact per-group op counts of the frozen config-3 plan (featuremajor.run_cnn):
+    conv1 at 14 limbs (deferred rescale) -> square+pool sums -> relin at 14 ->
+    2 rescales -> conv2 at 12 -> square+GAP sums -> relin at 12 -> 2 rescales
+    -> dense at 10 limbs -> rescale."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
     from paper_2604_16834_b200.featuremajor import conv3x3_csr
@@ -31,11 +34,12 @@ def cfg3_op_counts():
     nnz1 = len(conv3x3_csr(3, range(16), 32, 32)[1])
     nnz2 = len(conv3x3_csr(16, range(32), 16, 16)[1])
     return {
-        # (count, limbs): modular MACs over 2 components
+        # modular MACs over 2 components (conv1, conv2, dense)
         "lincomb_macs": nnz1 * 2 * 14 * N + nnz2 * 2 * 12 * N + 320 * 2 * 10 * N,
-        "intsum_macs": 16384 * 2 * 12 * N + 8192 * 2 * 10 * N,
-        "rescale": [(16384, 14), (8192, 12), (10, 10)],
-        "mult_ct": [(16384, 13), (8192, 11)],
+        # squares summed into pools / GAP: 4 modular products per coefficient
+        "square_macs": 16384 * 4 * 14 * N + 8192 * 4 * 12 * N,
+        "relin": [(4096, 14), (32, 12)],
+        "rescale": [(4096, 14), (4096, 13), (32, 12), (32, 11), (10, 10)],
     }
 
 
@@ -56,7 +60,7 @@ def measure(seconds_budget: float = 20.0, threads: int | None = None, seed: int 
     ops = cfg3_op_counts()
     res = {"threads": threads}
     # 1. linear combination throughput (OpenMP over outputs)
-    n_out, k = 2 * threads, 27
+    n_out, k = 8 * threads, 27
     ins = [rand_ct(14) for _ in range(k)]
     rows = np.arange(n_out + 1) * k
     cols = np.tile(np.arange(k), n_out)
@@ -65,16 +69,16 @@ def measure(seconds_budget: float = 20.0, threads: int | None = None, seed: int 
     orc.lincomb(ins, rows, cols, w, n_threads=threads)
     dt = time.perf_counter() - t
     res["lincomb_mac_per_s"] = len(cols) * 2 * 14 * N / dt
-    # 2. ct x ct (tensor + relin + rescale), one ciphertext per host thread
+    # 2. relinearisation of 3-component ciphertexts, one per host thread
     rk = orc.switch_key(0)
     per_relin = {}
-    for ell in (13, 11):
-        a = [rand_ct(ell) for _ in range(threads)]
+    for ell in (14, 12):
+        a = [rand_ct(ell, 3) for _ in range(threads)]
         t = time.perf_counter()
         with ThreadPoolExecutor(threads) as ex:
-            list(ex.map(lambda c: orc.mult_ct(c, c, rk), a))
+            list(ex.map(lambda c: orc.relin(c, rk), a))
         per_relin[ell] = (time.perf_counter() - t) / threads
-    res["mult_ct_s"] = per_relin
+    res["relin_s"] = per_relin
     # 3. rescale
     per_rs = {}
     for ell in (14, 12):
@@ -84,14 +88,21 @@ def measure(seconds_budget: float = 20.0, threads: int | None = None, seed: int 
             list(ex.map(orc.rescale, a))
         per_rs[ell] = (time.perf_counter() - t) / threads
     res["rescale_s"] = per_rs
-    total = ops["lincomb_macs"] / res["lincomb_mac_per_s"] + ops["intsum_macs"] / res["lincomb_mac_per_s"]
-    total += sum(cnt * per_relin[ell] for cnt, ell in ops["mult_ct"])
-    total += sum(cnt * per_rs.get(ell, per_rs[12] * ell / 12) for cnt, ell in ops["rescale"])
+    # 4. tensor products (the squares summed into pools)
+    a = [rand_ct(14) for _ in range(threads)]
+    t = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda c: orc.tensor(c, c), a))
+    res["square_mac_per_s"] = threads * 4 * 14 * N / (time.perf_counter() - t)
+    total = ops["lincomb_macs"] / res["lincomb_mac_per_s"] + ops["square_macs"] / res["square_mac_per_s"]
+    total += sum(cnt * per_relin[14 if ell > 12 else 12] * ell / (14 if ell > 12 else 12) for cnt, ell in ops["relin"])
+    total += sum(cnt * per_rs[14 if ell > 12 else 12] * ell / (14 if ell > 12 else 12) for cnt, ell in ops["rescale"])
     res["group_seconds_extrapolated"] = total
     res["samples_per_s"] = 32768.0 / total
-    res["sample"] = (f"oracle on {threads} host threads: {n_out}x{k}-term lincomb at 14 limbs, {threads} mult_ct "
-                     f"at 13 and 11 limbs, {threads} rescales at 14 and 12 limbs; extrapolated with the exact "
-                     f"config-3 op counts of one 32768-sample group")
+    res["sample"] = (f"oracle on {threads} host threads running the same plan as the GPU: {n_out}x{k}-term lincomb "
+                     f"at 14 limbs, {threads} relinearisations at 14 and 12 limbs, {threads} rescales at 14 and 12 "
+                     f"limbs, {threads} tensor products; extrapolated with the exact config-3 op counts of one "
+                     f"32768-sample group")
     return res
 
 
