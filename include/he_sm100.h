@@ -129,6 +129,12 @@ int he_tensor(he_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, u
               int count, int ell, void *stream);
 int he_relin(he_ctx *ctx, const uint64_t *const *d3, uint64_t *const *out, int count, int ell,
              void *stream);
+/* relin + `extra` rescales as ONE ModDown over P u {q_{ell-extra}..q_{ell-1}}:
+ * [3][ell][N] -> [2][ell-extra][N], result ~= relin(d3) / prod dropped q (fast BConv)
+ * (the activation's mult_ct + the deferred conv rescale, engine.py:306-313;
+ * N = 2^16 only, HE_EINVAL otherwise; extra in [0, min(ell-1, 8)]). */
+int he_relin_rescale(he_ctx *ctx, const uint64_t *const *d3, uint64_t *const *out, int count, int ell,
+                     int extra, void *stream);
 int he_keyswitch(he_ctx *ctx, uint32_t galois_elt, const uint64_t *const *d, uint64_t *const *out0,
                  uint64_t *const *out1, int count, int ell, void *stream);
 int he_rescale(he_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int ell,

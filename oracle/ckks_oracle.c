@@ -613,6 +613,96 @@ static void bconv(const oc_ctx *c, const uint64_t *const *src, const int *sidx, 
     }
 }
 
+/* ModUp of d + inner product with the key: acc [2][ell+K][N] (NTT domain,
+ * limbs Q_0..Q_{ell-1} then P_0..P_{K-1}); caller frees */
+static uint64_t *ks_inner(const oc_ctx *c, const uint64_t *d, const uint64_t *key, int ell) {
+    int N = c->N, L = c->L, K = c->K, total = L + K;
+    size_t comp = (size_t)total * N;
+    int ext = ell + K;
+    int midx[MAXM];
+    for (int t = 0; t < ell; t++) midx[t] = t;
+    for (int k = 0; k < K; k++) midx[ell + k] = L + k;
+    uint64_t *dc = (uint64_t *)malloc(8 * (size_t)ell * N);
+    memcpy(dc, d, 8 * (size_t)ell * N);
+    for (int i = 0; i < ell; i++) oc_intt(c, dc + (size_t)i * N, i);
+    uint64_t *acc = (uint64_t *)calloc(2 * (size_t)ext * N, 8);
+    uint64_t *tmp = (uint64_t *)malloc(8 * (size_t)N);
+    int beta = (ell + c->alpha - 1) / c->alpha;
+    for (int j = 0; j < beta; j++) {
+        int s0 = j * c->alpha, s1 = (j + 1) * c->alpha < ell ? (j + 1) * c->alpha : ell;
+        const uint64_t *src[MAXM];
+        int sidx[MAXM];
+        for (int s = s0; s < s1; s++) { src[s - s0] = dc + (size_t)s * N; sidx[s - s0] = s; }
+        const uint64_t *B = key + (size_t)j * 2 * comp, *A = B + comp;
+        for (int t = 0; t < ext; t++) {
+            int m = midx[t];
+            uint64_t q = c->mod[m];
+            const uint64_t *dt;
+            if (t >= s0 && t < s1) {
+                dt = d + (size_t)t * N;
+            } else {
+                bconv(c, src, sidx, s1 - s0, q, tmp);
+                oc_ntt(c, tmp, m);
+                dt = tmp;
+            }
+            uint64_t *a0 = acc + (size_t)t * N, *a1 = acc + (size_t)(ext + t) * N;
+            const uint64_t *kb = B + (size_t)m * N, *ka = A + (size_t)m * N;
+            for (int k = 0; k < N; k++) {
+                a0[k] = addmod(a0[k], mulmod(dt[k], kb[k], q), q);
+                a1[k] = addmod(a1[k], mulmod(dt[k], ka[k], q), q);
+            }
+        }
+    }
+    free(dc);
+    free(tmp);
+    return acc;
+}
+
+/* Relinearisation fused with `extra` rescales (one joint ModDown):
+ *   X_c = acc_c + [P]_{q_i} d_c on Q limbs, X_c = acc_c on P limbs;
+ *   S = {q_{ell-extra} .. q_{ell-1}} u P;  y_s = INTT(X_c[s]) for s in S;
+ *   out_c[i] = (X_c[i] - NTT_i(BConv_{S -> q_i}(y))) * (prod S)^-1,  i < ell - extra.
+ * d3 [3][ell][N] -> out [2][ell-extra][N]. */
+void oc_relin_rescale(const oc_ctx *c, const uint64_t *d3, const uint64_t *key, uint64_t *out, int ell, int extra) {
+    int N = c->N, L = c->L, K = c->K, ext = ell + K, lo = ell - extra;
+    size_t P = (size_t)ell * N;
+    uint64_t *acc = ks_inner(c, d3 + 2 * P, key, ell);
+    uint64_t *tmp = (uint64_t *)malloc(8 * (size_t)N);
+    for (int cc = 0; cc < 2; cc++) {
+        uint64_t *X = acc + (size_t)cc * ext * N;
+        const uint64_t *dcc = d3 + (size_t)cc * P;
+        for (int i = 0; i < ell; i++) {
+            uint64_t q = c->mod[i], pm = prod_p_mod(c, q);
+            for (int k = 0; k < N; k++) X[(size_t)i * N + k] = addmod(X[(size_t)i * N + k], mulmod(dcc[(size_t)i * N + k], pm, q), q);
+        }
+        const uint64_t *src[MAXM];
+        int sidx[MAXM], ns = 0;
+        for (int s = lo; s < ell; s++) {
+            oc_intt(c, X + (size_t)s * N, s);
+            src[ns] = X + (size_t)s * N;
+            sidx[ns++] = s;
+        }
+        for (int k = 0; k < K; k++) {
+            oc_intt(c, X + (size_t)(ell + k) * N, L + k);
+            src[ns] = X + (size_t)(ell + k) * N;
+            sidx[ns++] = L + k;
+        }
+        for (int i = 0; i < lo; i++) {
+            uint64_t q = c->mod[i];
+            bconv(c, src, sidx, ns, q, tmp);
+            oc_ntt(c, tmp, i);
+            uint64_t prod = prod_p_mod(c, q);
+            for (int s = lo; s < ell; s++) prod = mulmod(prod, c->mod[s] % q, q);
+            uint64_t inv = invmod(prod, q);
+            const uint64_t *x = X + (size_t)i * N;
+            uint64_t *o = out + ((size_t)cc * lo + i) * N;
+            for (int k = 0; k < N; k++) o[k] = mulmod(submod(x[k], tmp[k], q), inv, q);
+        }
+    }
+    free(acc);
+    free(tmp);
+}
+
 void oc_keyswitch(const oc_ctx *c, const uint64_t *d, const uint64_t *key, int ell, uint64_t *out0,
                   uint64_t *out1) {
     int N = c->N, L = c->L, K = c->K, total = L + K;

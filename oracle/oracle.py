@@ -71,6 +71,7 @@ def lib():
         L.oc_tensor.argtypes = [vp, u64p, u64p, u64p, C.c_int]
         L.oc_keyswitch.argtypes = [vp, u64p, u64p, C.c_int, u64p, u64p]
         L.oc_relin.argtypes = [vp, u64p, u64p, u64p, C.c_int]
+        L.oc_relin_rescale.argtypes = [vp, u64p, u64p, u64p, C.c_int, C.c_int]
         L.oc_rescale.argtypes = [vp, u64p, u64p, C.c_int, C.c_int]
         L.oc_automorphism.argtypes = [vp, u64p, C.c_uint32, u64p, C.c_int]
         L.oc_rotate.argtypes = [vp, u64p, C.c_uint32, u64p, u64p, C.c_int]
@@ -244,6 +245,13 @@ class Oracle:
         ell = d3.shape[1]
         out = np.zeros((2, ell, self.N), np.uint64)
         lib().oc_relin(self._h, _u64(d3), _u64(key), _u64(out), ell)
+        return out
+
+    def relin_rescale(self, d3, key, extra):
+        """relinearise + `extra` rescales as one joint ModDown (oc_relin_rescale)."""
+        ell = d3.shape[1]
+        out = np.zeros((2, ell - extra, self.N), np.uint64)
+        lib().oc_relin_rescale(self._h, _u64(np.ascontiguousarray(d3)), _u64(key), _u64(out), ell, extra)
         return out
 
     def rescale(self, ct):

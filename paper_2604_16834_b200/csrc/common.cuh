@@ -72,6 +72,7 @@ struct he_ctx {
 // host-side modular helpers (context.cu)
 uint64_t he_h_mulmod(uint64_t a, uint64_t b, uint64_t q);
 uint64_t he_h_shoup(uint64_t w, uint64_t q);
+uint64_t he_h_inv(uint64_t a, uint64_t q);
 // fused N = 2^16 key switching / rescale (fused.cu); pointer lists are HOST arrays
 int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d, const uint64_t *const *d_dev, int B,
                        int ell, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *const *add0,
@@ -243,6 +244,9 @@ int he_scratch_alloc(void **p, size_t bytes, cudaStream_t s);
 void he_scratch_free(void *p, cudaStream_t s);
 int he_get_modup_table(he_ctx *ctx, int ell, int digit, const BconvTable **out);
 int he_get_moddown_table(he_ctx *ctx, int ell, const BconvTable **out);
+int he_get_moddown_table_x(he_ctx *ctx, int ell, int extra, const BconvTable **out);
+int he_relin_rescale_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d3, const uint64_t *const *d2_dev,
+                           int B, int ell, int extra, uint64_t *const *out, cudaStream_t s);
 const uint64_t *he_get_key(he_ctx *ctx, uint32_t galois_elt);
 
 // NTT launchers (ntt.cu).  Polys: data + p*N for p in [0, n_polys); the

@@ -45,6 +45,7 @@ static uint64_t h_inv(uint64_t a, uint64_t q) { return h_pow(a % q, q - 2, q); }
 static uint64_t h_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((hu128)w << 64) / q); }
 uint64_t he_h_mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)((hu128)a * b % q); }
 uint64_t he_h_shoup(uint64_t w, uint64_t q) { return h_shoup(w, q); }
+uint64_t he_h_inv(uint64_t a, uint64_t q) { return h_inv(a, q); }
 static uint64_t h_mont(uint64_t w, uint64_t q) { return (uint64_t)(((hu128)(w % q) << 64) % q); }
 static bool h_is_prime(uint64_t n) {
     static const uint64_t B[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
@@ -426,16 +427,21 @@ int he_get_modup_table(he_ctx *c, int ell, int j, const BconvTable **out) {
     return HE_OK;
 }
 
-int he_get_moddown_table(he_ctx *c, int ell, const BconvTable **out) {
+int he_get_moddown_table(he_ctx *c, int ell, const BconvTable **out) { return he_get_moddown_table_x(c, ell, 0, out); }
+
+// ModDown over S = {q_{ell-extra} .. q_{ell-1}} u P -> targets q_0 .. q_{ell-extra-1}
+int he_get_moddown_table_x(he_ctx *c, int ell, int extra, const BconvTable **out) {
     std::lock_guard<std::mutex> g(c->mu);
-    auto it = c->moddown_tab.find(ell);
+    const int key = ell * 16 + extra;
+    auto it = c->moddown_tab.find(key);
     if (it == c->moddown_tab.end()) {
         std::vector<int> src, dst;
+        for (int s = ell - extra; s < ell; s++) src.push_back(s);
         for (int k = 0; k < c->K; k++) src.push_back(c->L + k);
-        for (int t = 0; t < ell; t++) dst.push_back(t);
+        for (int t = 0; t < ell - extra; t++) dst.push_back(t);
         BconvTable t;
         HE_TRY(make_table(c, src, dst, t));
-        it = c->moddown_tab.emplace(ell, t).first;
+        it = c->moddown_tab.emplace(key, t).first;
     }
     *out = &it->second;
     return HE_OK;

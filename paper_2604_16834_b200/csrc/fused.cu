@@ -38,6 +38,9 @@ struct Job {
     const uint64_t *tab;  // BConv Montgomery constants [ns]
     uint64_t cw, cwp;     // Shoup constant: inverse final scale / epilogue scale
     uint64_t ql;          // centred-lift source modulus
+    const uint64_t *src2; // inverse pass-1 addend: input = src + c2 * src2 (or nullptr)
+    const uint64_t *aux2; // epilogue: operand = aux + c2 * aux2 (or nullptr)
+    uint64_t c2, c2p;     // Shoup constant for src2 / aux2 (P mod q for the joint ModDown)
     int32_t mod;          // modulus index of this polynomial
     int32_t ns;           // BConv source count
 };
@@ -129,7 +132,9 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
             row[cc] = v;
         } else {
             const size_t idx = r * 256 + cc;
-            uint64_t y = shoup(sub_mod(jb.aux[idx], v, c.q), jb.cw, jb.cwp, c.q);
+            uint64_t base = jb.aux[idx];
+            if (jb.aux2) base = add_mod(base, shoup(jb.aux2[idx], jb.c2, jb.c2p, c.q), c.q);
+            uint64_t y = shoup(sub_mod(base, v, c.q), jb.cw, jb.cwp, c.q);
             if (jb.add) y = add_mod(y, jb.add[idx], c.q);
             jb.out[idx] = y;
         }
@@ -151,6 +156,12 @@ __global__ void __launch_bounds__(NTT_TPB) ki_rows(const Job *__restrict__ jobs,
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = in[g + 16 * j];
+    if (jb.src2) {  // joint ModDown: X = acc + (P mod q) * d on the dropped Q limbs
+        const uint64_t *in2 = jb.src2 + r * 256;
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            s[pad16(g + 16 * j)] = add_mod(s[pad16(g + 16 * j)], shoup(in2[g + 16 * j], jb.c2, jb.c2p, c.q), c.q);
+    }
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
@@ -305,24 +316,15 @@ Job blank() {
 
 }  // namespace
 
-// Fused hybrid key switch for B ciphertexts (N = 2^16).  Pointer arguments are
-// HOST arrays of device addresses; d_dev is the same list of d pointers in
-// device memory (read by the inner-product kernel).
-int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d, const uint64_t *const *d_dev, int B,
-                       int ell, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *const *add0,
-                       const uint64_t *const *add1, cudaStream_t s) {
+// ModUp of d + key inner product: acc [B][2][ell+K][N] (NTT domain).  dcv
+// [B][ell][N] and ext [B][beta][ell+K][N] are caller-provided scratch.
+static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, const uint64_t *const *d_dev, int B,
+                    int ell, uint64_t *dcv, uint64_t *ext, uint64_t *acc, cudaStream_t s) {
     const int L = c->L, K = c->K, alpha = c->alpha, M = L + K;
     const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
-    const size_t w_dc = (size_t)B * ell * NN, w_ext = (size_t)B * beta * ext_n * NN, w_acc = (size_t)B * 2 * ext_n * NN,
-                 w_md = (size_t)B * 2 * ell * NN;
-    void *scr = nullptr;
-    HE_TRY(he_scratch_alloc(&scr, (w_dc + w_ext + w_acc + w_md) * 8, s));
-    uint64_t *dcv = (uint64_t *)scr, *ext = dcv + w_dc, *acc = ext + w_ext, *md = acc + w_acc;
     int rc = HE_OK;
     std::vector<const BconvTable *> up(beta);
     for (int j = 0; j < beta && rc == HE_OK; j++) rc = he_get_modup_table(c, ell, j, &up[j]);
-    const BconvTable *dn = nullptr;
-    if (rc == HE_OK) rc = he_get_moddown_table(c, ell, &dn);
     // 1. v = INTT(d) * qhat_s^-1 (ModUp's per-source Shoup step folded into INTT's N^-1)
     if (rc == HE_OK) {
         std::vector<Job> jobs;
@@ -387,6 +389,25 @@ int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d,
         he_count_launch(1);
         if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
     }
+    return rc;
+}
+
+// Fused hybrid key switch for B ciphertexts (N = 2^16).  Pointer arguments are
+// HOST arrays of device addresses; d_dev is the same list of d pointers in
+// device memory (read by the inner-product kernel).
+int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d, const uint64_t *const *d_dev, int B,
+                       int ell, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *const *add0,
+                       const uint64_t *const *add1, cudaStream_t s) {
+    const int L = c->L, K = c->K, alpha = c->alpha;
+    const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
+    const size_t w_dc = (size_t)B * ell * NN, w_ext = (size_t)B * beta * ext_n * NN, w_acc = (size_t)B * 2 * ext_n * NN,
+                 w_md = (size_t)B * 2 * ell * NN;
+    void *scr = nullptr;
+    HE_TRY(he_scratch_alloc(&scr, (w_dc + w_ext + w_acc + w_md) * 8, s));
+    uint64_t *dcv = (uint64_t *)scr, *ext = dcv + w_dc, *acc = ext + w_ext, *md = acc + w_acc;
+    const BconvTable *dn = nullptr;
+    int rc = he_get_moddown_table(c, ell, &dn);
+    if (rc == HE_OK) rc = modup_ip(c, key, d, d_dev, B, ell, dcv, ext, acc, s);
     // 4. ModDown: INTT of the P limbs (times N^-1 * phat_k^-1), then the P->Q
     //    BConv NTT whose epilogue writes (acc - conv) * P^-1 (+ d0 / d1)
     if (rc == HE_OK) {
@@ -424,6 +445,77 @@ int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d,
                     jobs.push_back(j);
                 }
             }
+        rc = run_forward<L_BCONV, E_SUBSCALE>(c, jobs, s);
+    }
+    he_scratch_free(scr, s);
+    return rc;
+}
+
+// Relinearisation + `extra` rescales as one ModDown over S = {dropped Q limbs}
+// u P (oracle: oc_relin_rescale).  d3: HOST array of [3][ell][N] device
+// ciphertexts, d2_dev: device array of their d2 = d3 + 2 ell N pointers,
+// out: HOST array of [2][ell-extra][N].
+int he_relin_rescale_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d3, const uint64_t *const *d2_dev,
+                           int B, int ell, int extra, uint64_t *const *out, cudaStream_t s) {
+    const int L = c->L, K = c->K, alpha = c->alpha, lo = ell - extra, ns = extra + K;
+    const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
+    const size_t P = (size_t)ell * NN;
+    const size_t w_dc = (size_t)B * ell * NN, w_ext = (size_t)B * beta * ext_n * NN, w_acc = (size_t)B * 2 * ext_n * NN,
+                 w_md = (size_t)B * 2 * lo * NN;
+    void *scr = nullptr;
+    HE_TRY(he_scratch_alloc(&scr, (w_dc + w_ext + w_acc + w_md) * 8, s));
+    uint64_t *dcv = (uint64_t *)scr, *ext = dcv + w_dc, *acc = ext + w_ext, *md = acc + w_acc;
+    std::vector<const uint64_t *> d2(B);
+    for (int b = 0; b < B; b++) d2[b] = d3[b] + 2 * P;
+    const BconvTable *dn = nullptr;
+    int rc = he_get_moddown_table_x(c, ell, extra, &dn);
+    if (rc == HE_OK) rc = modup_ip(c, key, d2.data(), d2_dev, B, ell, dcv, ext, acc, s);
+    // joint ModDown, step 1: y_s = INTT(X_s) * N^-1 * shat_s^-1 for s in S, with
+    // X_s = acc_s + [P]_{q_s} d_s on the dropped Q limbs (acc's S limbs are contiguous)
+    if (rc == HE_OK) {
+        std::vector<Job> jobs;
+        for (int b = 0; b < B; b++)
+            for (int cc = 0; cc < 2; cc++)
+                for (int si = 0; si < ns; si++) {
+                    const int t = lo + si, m = t < ell ? t : L + (t - ell);
+                    Job j = blank();
+                    j.src = j.dst = acc + (((size_t)b * 2 + cc) * ext_n + t) * NN;
+                    if (t < ell) {
+                        j.src2 = d3[b] + (size_t)cc * P + (size_t)t * NN;
+                        j.c2 = c->h_pmodq[t];
+                        j.c2p = he_h_shoup(j.c2, c->mod[t]);
+                    }
+                    j.mod = m;
+                    j.cw = he_h_mulmod(c->h_ninv[m], dn->h_qhinv[si], c->mod[m]);
+                    j.cwp = he_h_shoup(j.cw, c->mod[m]);
+                    jobs.push_back(j);
+                }
+        rc = run_inverse(c, jobs, s);
+    }
+    // step 2: out_c[i] = (acc_i + [P] d_i - NTT_i(BConv_S(y))) * (prod S)^-1, i < ell - extra
+    if (rc == HE_OK) {
+        std::vector<Job> jobs;
+        for (int b = 0; b < B; b++)
+            for (int cc = 0; cc < 2; cc++)
+                for (int i = 0; i < lo; i++) {
+                    const uint64_t q = c->mod[i];
+                    uint64_t prod = c->h_pmodq[i];
+                    for (int t = lo; t < ell; t++) prod = he_h_mulmod(prod, c->mod[t] % q, q);
+                    Job j = blank();
+                    j.src = acc + (((size_t)b * 2 + cc) * ext_n + lo) * NN;
+                    j.ns = ns;
+                    j.tab = dn->d + 2 * ns + (size_t)i * ns;
+                    j.mod = i;
+                    j.dst = md + (((size_t)b * 2 + cc) * lo + i) * NN;
+                    j.aux = acc + (((size_t)b * 2 + cc) * ext_n + i) * NN;
+                    j.aux2 = d3[b] + (size_t)cc * P + (size_t)i * NN;
+                    j.c2 = c->h_pmodq[i];
+                    j.c2p = he_h_shoup(j.c2, q);
+                    j.out = out[b] + ((size_t)cc * lo + i) * NN;
+                    j.cw = he_h_inv(prod, q);
+                    j.cwp = he_h_shoup(j.cw, q);
+                    jobs.push_back(j);
+                }
         rc = run_forward<L_BCONV, E_SUBSCALE>(c, jobs, s);
     }
     he_scratch_free(scr, s);

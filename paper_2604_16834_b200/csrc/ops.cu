@@ -647,6 +647,37 @@ extern "C" int he_relin(he_ctx *c, const uint64_t *const *d3, uint64_t *const *o
     return HE_OK;
 }
 
+extern "C" int he_relin_rescale(he_ctx *c, const uint64_t *const *d3, uint64_t *const *out, int count, int ell,
+                                int extra, void *stream) {
+    HE_TRY(check_basic(c, count, ell, 3, "he_relin_rescale"));
+    if (extra < 0 || extra >= ell || extra > 8) {
+        he_set_error("he_relin_rescale: extra=%d must be in [0, min(ell-1, 8)] (ell=%d)", extra, ell);
+        return HE_ELEVEL;
+    }
+    if (c->logN != 16) {
+        he_set_error("he_relin_rescale: the joint ModDown is implemented for N = 2^16 only (log_n=%d)", c->logN);
+        return HE_EINVAL;
+    }
+    const uint64_t *key = he_get_key(c, 0);
+    if (!key) {
+        he_set_error("relinearisation key not generated");
+        return HE_ENOKEY;
+    }
+    if (!count) return HE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    size_t P = (size_t)ell * c->N;
+    std::vector<const uint64_t *> p2(count);
+    for (int i = 0; i < count; i++) p2[i] = d3[i] + 2 * P;
+    DevPtrs D2(s);
+    HE_TRY(D2.up((const void *const *)p2.data(), count));
+    int ch = chunk_of(ks_bytes_per_ct(c, ell), count);
+    for (int b0 = 0; b0 < count; b0 += ch) {
+        int B = std::min(ch, count - b0);
+        HE_TRY(he_relin_rescale_fused(c, key, d3 + b0, D2.as<const uint64_t>() + b0, B, ell, extra, out + b0, s));
+    }
+    return HE_OK;
+}
+
 extern "C" int he_rescale(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, int count, int ell, int nc,
                           void *stream) {
     HE_TRY(check_basic(c, count, ell, nc, "he_rescale"));

@@ -356,6 +356,7 @@ class GpuEngine:
         self._timing = None  # {category: [(start_event, end_event, units)]} when enabled
         # exact int8-digit tensor-core convolutions (he_conv_mma); False = CUDA-core kernel
         self.use_tensor_cores = True
+        self.joint_moddown = True  # relin + rescales as one ModDown (N = 2^16)
 
     # ------------------------------------------------------------ timing hooks (bench.py)
     def enable_timing(self, on: bool = True) -> None:
@@ -680,11 +681,23 @@ class GpuEngine:
         if any(c.level != level for c in cts) or level < drops:
             raise LevelExhausted(f"relin_rescale_batch needs equal levels >= {drops}")
         limbs = level + 1
+        pi = self._ptrs(cts)
+        scales = [c.scale for c in cts]
+        if drops >= 1 and self.joint_moddown and self.N == 1 << 16:
+            # one ModDown over P u {dropped limbs} (oracle oc_relin_rescale)
+            out = self._alloc(len(cts), 2, limbs - drops)
+            po = self._tptrs(out)
+            _lib.check(self._call("relin", self._L.he_relin_rescale, self._h, _lib.addr(pi), _lib.addr(po), len(cts),
+                                  limbs, drops, self.stream,
+                                  units=(len(cts) * (5.0 * limbs - 2 * drops) * self.N * 8, 0.0)), "relin_rescale")
+            for k in range(drops):
+                ql = self.moduli[limbs - 1 - k]
+                scales = [s / ql for s in scales]
+            return self._wrap_batch(out, level - drops, scales)
         cur = self._alloc(len(cts), 2, limbs)
-        pi, pm = self._ptrs(cts), self._tptrs(cur)
+        pm = self._tptrs(cur)
         _lib.check(self._call("relin", self._L.he_relin, self._h, _lib.addr(pi), _lib.addr(pm), len(cts), limbs,
                               self.stream, units=(len(cts) * 5.0 * limbs * self.N * 8, 0.0)), "relin")
-        scales = [c.scale for c in cts]
         for _ in range(drops):
             ql = self.moduli[limbs - 1]
             out = self._alloc(len(cts), 2, limbs - 1)

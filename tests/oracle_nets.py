@@ -78,10 +78,23 @@ def tensor(orc, a, b):
                      a.scale * b.scale)
 
 
-def relin_rescale(orc, rk, a):
-    """engine.relin_rescale_batch: relinearise the 3-component ct, then rescale."""
+def _relin_drops(orc, rk, a, drops):
+    """engine.relin_rescale_batch: at N = 2^16 one joint ModDown over P u
+    {dropped limbs} (oc_relin_rescale), else relin followed by `drops` rescales."""
+    s = a.scale
+    for k in range(drops):
+        s /= orc.moduli[a.ell - 1 - k]
+    if orc.N == 1 << 16:
+        return OracleCts(orc.relin_rescale(np.ascontiguousarray(a.data), rk, drops), s)
     r = orc.relin(np.ascontiguousarray(a.data), rk)
-    return OracleCts(orc.rescale(r), a.scale / orc.moduli[a.ell - 1])
+    for _ in range(drops):
+        r = orc.rescale(r)
+    return OracleCts(r, s)
+
+
+def relin_rescale(orc, rk, a):
+    """engine.relin_rescale_batch(drops=1)."""
+    return _relin_drops(orc, rk, a, 1)
 
 
 def activation_lazy(orc, cts, coeffs):
@@ -163,9 +176,8 @@ def conv3x3_deferred(orc, ins, w, bias, H, W, fold_ab, target_scale):
 
 
 def relin_rescale2(orc, rk, a):
-    r = orc.rescale(orc.relin(np.ascontiguousarray(a.data), rk))
-    s = a.scale / orc.moduli[a.ell - 1]
-    return OracleCts(orc.rescale(r), s / orc.moduli[a.ell - 2])
+    """engine.relin_rescale_batch(drops=2) after a deferred-rescale conv."""
+    return _relin_drops(orc, rk, a, 2)
 
 
 def encrypt_features(orc, feats, base_index=0):

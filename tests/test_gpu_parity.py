@@ -143,6 +143,34 @@ def test_rescale_bit_exact(pair):
     assert np.array_equal(to_np(out), orc.rescale(x))
 
 
+def test_relin_rescale_joint_moddown_bit_exact(pair):
+    """he_relin_rescale (one ModDown over P u dropped limbs) vs oc_relin_rescale."""
+    import torch
+
+    name, eng, orc = pair
+    if eng.N != 1 << 16:
+        pytest.skip("joint ModDown is the N = 2^16 path")
+    eng._ensure_relin()
+    rng = np.random.default_rng(21)
+    L = eng.context.n_q
+    rk = orc.switch_key(0)
+    for ell, extra in ((L, 1), (L, 2), (max(3, L // 2), 2), (2, 1)):
+        if extra >= ell:
+            continue
+        x = rand_residues(rng, eng.moduli[:ell], (3,), eng.N)
+        t = from_np(x, eng.device)
+        out = torch.empty((2, ell - extra, eng.N), dtype=torch.int64, device=eng.device)
+        pi, po = _ptrs([t]), _ptrs([out])
+        assert _lib(eng).he_relin_rescale(eng._h, pi.ctypes.data, po.ctypes.data, 1, ell, extra, None) == 0
+        assert np.array_equal(to_np(out), orc.relin_rescale(x, rk, extra)), (ell, extra)
+    # semantics: tensor -> joint relin+rescale(1) decrypts to the product
+    n = eng.context.n
+    a_v, b_v = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    a, b = eng.encrypt_batch(np.stack([a_v, b_v]))
+    (m,) = eng.relin_rescale_batch(eng.tensor_batch([a], [b]), drops=1)
+    assert np.max(np.abs(eng.decrypt(m) - a_v * b_v)) < 1e-5
+
+
 def test_mult_ct_and_rotate_bit_exact(pair):
     name, eng, orc = pair
     rng = np.random.default_rng(8)
