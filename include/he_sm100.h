@@ -189,6 +189,20 @@ int he_conv_mma(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *cons
 int he_square_sum(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
                   const int32_t *row_ptr, const int32_t *col, const uint64_t *residues, int ell, void *stream);
 
+/* conv -> lazy square -> window sum in ONE kernel (the conv map is never
+ * written): 3x3 / pad-1 conv of p channels over H x W (inputs in[i*H*W +
+ * y*W + x], [2][ell][N]) with weights [M][9p] (tap k = i*9 + (dy+1)*3 +
+ * (dx+1)) and bias[m][i] on component 0, for conv output rows [y0, y1); then
+ * per pixel the tensor square (y0^2, 2 y0 y1, y1^2); then
+ *   pool = 1: out[m*nwin + (y/2 - y0/2)*(W/2) + x/2] = 2x2-window sums
+ *   pool = 0: out[m] = sum over all pixels of the rows
+ * plus cst[i] on component 0 of every output ([3][ell][N]).  Equals
+ * he_conv_mma + he_square_sum bit for bit.  Bounds (else HE_EINVAL): 9p <= 160,
+ * M <= 32, |weights| < 2^23, every prime >= 2^36.  bias / cst may be NULL. */
+int he_conv_square_sum(he_ctx *ctx, const uint64_t *const *in, int p, int H, int W, uint64_t *const *out, int M,
+                       int pool, int y0, int y1, const int64_t *weights, const uint64_t *bias,
+                       const uint64_t *cst, int ell, void *stream);
+
 /* block until all work on `stream` is done; returns HE_ECUDA on async error */
 int he_sync(void *stream);
 /* number of kernels this library has launched in the process (bench evidence) */

@@ -39,6 +39,7 @@ from .errors import (
     LevelExhausted,
     MissingRotationKey,
     ScaleMismatch,
+    ShapeMismatch,
 )
 
 # relative scale difference tolerated by add() (error contribution <= 2^-20 * |x|)
@@ -357,6 +358,7 @@ class GpuEngine:
         # exact int8-digit tensor-core convolutions (he_conv_mma); False = CUDA-core kernel
         self.use_tensor_cores = True
         self.joint_moddown = True  # relin + rescales as one ModDown (N = 2^16)
+        self.use_fused_conv = True  # conv + square + pool/GAP in one kernel (he_conv_square_sum)
 
     # ------------------------------------------------------------ timing hooks (bench.py)
     def enable_timing(self, on: bool = True) -> None:
@@ -997,6 +999,70 @@ class GpuEngine:
         self._acct.bump("plain_mults", nnz * M)
         self._acct.bump("adds", nnz * M)
         return self._wrap_batch(out, level, [s_out] * n_out)
+
+    def conv_square_sum(self, inputs: Sequence[CipherVec], p: int, H: int, W: int, weights, weight_scale: float,
+                        bias, const: float, pool: bool, rows=None, scale_mult: float | None = None
+                        ) -> list[CipherVec] | None:
+        """Fused deferred-rescale 3x3 conv + lazy degree-2 activation + window
+        sum (he_conv_square_sum): equals conv_mma(weight_scale) -> tensor_batch
+        -> add_const_batch(const) -> 2x2-pool / GAP unit sum, bit for bit, but
+        the conv output map is never written.  inputs: p*H*W ciphertexts
+        (channel-major); weights [M][p*9] (already folded); conv output rows
+        ``rows`` (a contiguous range, default all).  Returns pool: M*(nr/2)*(W/2)
+        outputs indexed (m, r/2, x/2); GAP: M outputs.  3 components, scale
+        s_out^2 * scale_mult (default 4 for pool, pixel count for GAP).
+        None when a tensor-core bound does not hold (caller falls back)."""
+        for c in inputs:
+            self._check(c)
+        s_in = inputs[0].scale
+        if any(c.scale != s_in for c in inputs):
+            raise ScaleMismatch("conv_square_sum needs inputs at one scale")
+        if len(inputs) != p * H * W:
+            raise ShapeMismatch(f"{len(inputs)} inputs for {p}x{H}x{W}")
+        level = min(c.level for c in inputs)
+        if level < self.context.mult_level_cost:
+            raise LevelExhausted(f"level {level} < multiplication cost {self.context.mult_level_cost}")
+        limbs = level + 1
+        rows = list(range(H)) if rows is None else list(rows)
+        y0, y1 = rows[0], rows[-1] + 1
+        if rows != list(range(y0, y1)):
+            raise HebatchError("conv_square_sum needs a contiguous row range")
+        w = np.asarray(weights, np.float64)
+        M, T = w.shape
+        wi = np.ascontiguousarray(np.rint(w * float(weight_scale)).astype(np.int64))
+        if M > 32 or T != 9 * p or np.abs(wi).max(initial=0) >= 2 ** 23:
+            return None
+        s_out = s_in * float(weight_scale)
+        b = None if bias is None else np.asarray(bias, np.float64).reshape(M)
+        bres = (np.array([self._res(int(np.rint(bv * s_out)), limbs) for bv in b], np.uint64)
+                if b is not None and np.any(b != 0) else None)
+        npix_win = 4 if pool else (y1 - y0) * W
+        C = int(np.rint(const * (s_out * s_out)))
+        cres = np.array(self._res(npix_win * C, limbs), np.uint64) if const else None
+        nwin = ((y1 - y0) // 2) * (W // 2) if pool else 1
+        n_out = M * nwin
+        tins = self._at_level(inputs, level)
+        pin = _lib.ptr_array([t.data_ptr() for t in tins])
+        out = self._alloc(n_out, 3, limbs)
+        pout = self._tptrs(out)
+        from .featuremajor import conv3x3_fulltaps
+
+        nnz = int((conv3x3_fulltaps(p, H, W, rows) >= 0).sum())
+        poly = limbs * self.N
+        rc = self._call("conv_sqsum", self._L.he_conv_square_sum, self._h, _lib.addr(pin), p, H, W, _lib.addr(pout),
+                        M, int(bool(pool)), y0, y1, _lib.addr(wi), _lib.addr(bres) if bres is not None else None,
+                        _lib.addr(cres) if cres is not None else None, limbs, self.stream,
+                        units=((p * (y1 - y0 + 2) * W * 2 + n_out * 3) * poly * 8.0, 2.0 * nnz * M * poly))
+        if rc == _lib.HE_EINVAL:
+            return None
+        _lib.check(rc, "conv_square_sum")
+        npx = (y1 - y0) * W
+        self._acct.bump("plain_mults", nnz * M)
+        self._acct.bump("adds", nnz * M)
+        self._acct.bump("ct_mults", M * npx)
+        self._acct.bump("adds", M * npx + max(0, M * npx - n_out))
+        sm = scale_mult if scale_mult is not None else float(npix_win)
+        return self._wrap_batch(out, level, [s_out * s_out * sm] * n_out)
 
     def lincomb_int(self, inputs: Sequence[CipherVec], row_ptr, col, int_weights, out_scale: float,
                     count_adds: bool = True) -> list[CipherVec]:

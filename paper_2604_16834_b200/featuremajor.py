@@ -223,6 +223,29 @@ def fm_conv3x3(engine, inputs, weights, bias, H, W, out_channels=None, fold=(1.0
     return out
 
 
+def fm_conv_square_sum(engine, inputs, weights, bias, H, W, fold=(1.0, 0.0), rows=None, weight_scale=None,
+                       const=0.0, pool=True, scale_mult=None):
+    """Deferred-rescale conv fused with the lazy square activation and the
+    2x2-pool (pool=True) or GAP (pool=False) unit sum: one he_conv_square_sum
+    launch per <= 32 output channels.  Returns the window sums indexed
+    (o, r/2, x/2) / (o,), or None when the fused kernel does not apply."""
+    w = np.asarray(weights, np.float64)
+    q, p = w.shape[:2]
+    a, b = fold
+    out = []
+    for c0 in range(0, q, 32):
+        ch = list(range(c0, min(q, c0 + 32)))
+        wm = a * w[ch].reshape(len(ch), p * 9)
+        bias_ch = a * np.asarray(bias, np.float64)[ch] + b
+        res = engine.conv_square_sum(inputs, p, H, W, wm, weight_scale, bias_ch, const, pool, rows=rows,
+                                     scale_mult=scale_mult)
+        if res is None:
+            engine.release(*out)
+            return None
+        out.extend(res)
+    return out
+
+
 def conv3x3_fulltaps(p: int, H: int, W: int, rows=None) -> np.ndarray:
     """[pixels][9p] input index of every tap slot (-1 where the window leaves
     the image), tap order i*9 + (dy+1)*3 + (dx+1), pixels row-major over rows."""
@@ -347,21 +370,30 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
         # the activation's summed products drop two primes after relinearising
         defer = lazy and spec.act.degree == 2
         dw = deferred_weight_scale(engine, cur) if defer else None
+        # conv + square + pool/GAP in one kernel: no conv map in HBM, so the
+        # tiles only bound the 3-component window sums (about tile_outputs)
+        fused = defer and getattr(engine, "use_fused_conv", False) and (last or pool)
+        if fused and stream:
+            R = H if last else min(H, 2 * max(1, tile_outputs // (q * (W // 2))))
         for r0 in range(0, H, R):
             rows = list(range(r0, min(H, r0 + R)))
             nr = len(rows)
-            y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw)   # [o][r][x]
             if lazy and spec.act.degree == 2:
-                # fused: square (no relin) + constant + pool / GAP sum, one pass
                 c0, c1, c2 = spec.act.coeffs
                 cst = c0 - c1 * c1 / (4 * c2)
-                if last:
-                    rp, cols = gap_csr(q, nr * W)
-                    part = engine.square_sum_batch(y, rp, cols, cst, H * W)
-                else:
-                    rp, cols = pool2x2_csr(q, nr, W)
-                    part = engine.square_sum_batch(y, rp, cols, cst, 4.0)
-                engine.release(*y)
+                part = (fm_conv_square_sum(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw,
+                                           const=cst, pool=not last, scale_mult=H * W if last else 4.0)
+                        if fused else None)
+                if part is None:
+                    # conv, then square (no relin) + constant + pool / GAP sum in one pass
+                    y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw)
+                    if last:
+                        rp, cols = gap_csr(q, nr * W)
+                        part = engine.square_sum_batch(y, rp, cols, cst, H * W)
+                    else:
+                        rp, cols = pool2x2_csr(q, nr, W)
+                        part = engine.square_sum_batch(y, rp, cols, cst, 4.0)
+                    engine.release(*y)
                 if last:
                     if gap is None:
                         gap = part
@@ -379,6 +411,7 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
                         for x in range(Wo):
                             nxt[o * Ho * Wo + (y0 + r) * Wo + x] = z[(o * nr + r) * Wo + x]
                 continue
+            y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw)   # [o][r][x]
             z = apply_activation(engine, y, spec.act, lazy=lazy)
             engine.release(*y)
             if last:

@@ -171,6 +171,82 @@ def test_relin_rescale_joint_moddown_bit_exact(pair):
     assert np.max(np.abs(eng.decrypt(m) - a_v * b_v)) < 1e-5
 
 
+def _oracle_conv_square_sum(orc, ins, p, H, W, wi, bres, cst, pool, y0, y1):
+    """conv (oc_lincomb + bias on c0) -> tensor square -> window sum (+cst on c0)."""
+    M = wi.shape[0]
+    ell = ins[0].shape[1]
+    ys = {}
+    for y in range(y0, y1):
+        for x in range(W):
+            cols, taps = [], []
+            for i in range(p):
+                for t in range(9):
+                    yy, xx = y + t // 3 - 1, x + t % 3 - 1
+                    if 0 <= yy < H and 0 <= xx < W:
+                        cols.append(i * H * W + yy * W + xx)
+                        taps.append(i * 9 + t)
+            rows = [0]
+            for m in range(M):
+                rows.append(rows[-1] + len(cols))
+            wv = np.concatenate([wi[m, taps] for m in range(M)])
+            outs = orc.lincomb([ins[c] for c in cols], rows, list(range(len(cols))) * M, wv)
+            for m in range(M):
+                o = outs[m]
+                if bres is not None:
+                    o = orc.add_const(o, bres[m])
+                ys[(m, y, x)] = orc.tensor(o, o)
+    wins = []
+    if pool:
+        for wy in range(y0 // 2, y1 // 2):
+            for wx in range(W // 2):
+                wins.append([(2 * wy + a, 2 * wx + b) for a in (0, 1) for b in (0, 1)])
+    else:
+        wins.append([(y, x) for y in range(y0, y1) for x in range(W)])
+    res = []
+    for m in range(M):
+        for win in wins:
+            acc = ys[(m,) + win[0]]
+            for px in win[1:]:
+                acc = orc.add(acc, ys[(m,) + px])
+            if cst is not None:
+                acc = acc.copy()
+                acc[:2] = orc.add_const(np.ascontiguousarray(acc[:2]), cst)
+            res.append(acc)
+    return res
+
+
+@pytest.mark.parametrize("p,M,pool,H,rows,wbits", [(3, 16, 1, 4, (0, 4), 20), (16, 32, 0, 4, (0, 4), 14),
+                                                    (4, 8, 1, 4, (2, 4), 7), (2, 24, 0, 6, (1, 5), 20)])
+def test_conv_square_sum_fused_bit_exact(pair, p, M, pool, H, rows, wbits):
+    """he_conv_square_sum (conv + square + pool/GAP sum in one kernel) vs the
+    oracle's conv -> tensor -> add_const -> sum chain, on uniform residues."""
+    import torch
+
+    name, eng, orc = pair
+    if name == "cfg2" or (name == "cfg3" and p > 4):
+        pytest.skip("covered by the smaller parameter sets (oracle time)")
+    rng = np.random.default_rng(31 + p + M)
+    W = H
+    ell = eng.context.n_q if name != "cfg3" else 3
+    mods = eng.moduli[:ell]
+    x = rand_residues(rng, mods, (p * H * W, 2), eng.N)
+    ins = [from_np(x[i], eng.device) for i in range(p * H * W)]
+    lim = 1 << wbits
+    wi = rng.integers(-lim, lim, size=(M, 9 * p), dtype=np.int64)
+    bres = np.array([[int(rng.integers(0, q)) for q in mods] for _ in range(M)], np.uint64)
+    cst = np.array([int(rng.integers(0, q)) for q in mods], np.uint64)
+    y0, y1 = rows
+    nwin = ((y1 - y0) // 2) * (W // 2) if pool else 1
+    outs = [torch.empty((3, ell, eng.N), dtype=torch.int64, device=eng.device) for _ in range(M * nwin)]
+    pi, po = _ptrs(ins), _ptrs(outs)
+    rc = _lib(eng).he_conv_square_sum(eng._h, pi.ctypes.data, p, H, W, po.ctypes.data, M, pool, y0, y1,
+                                      wi.ctypes.data, bres.ctypes.data, cst.ctypes.data, ell, None)
+    assert rc == 0, eng._L.he_last_error()
+    ref = _oracle_conv_square_sum(orc, [x[i] for i in range(p * H * W)], p, H, W, wi, bres, cst, pool, y0, y1)
+    for k, (o, r) in enumerate(zip(outs, ref)):
+        assert np.array_equal(to_np(o), r), k
+
+
 def test_mult_ct_and_rotate_bit_exact(pair):
     name, eng, orc = pair
     rng = np.random.default_rng(8)
