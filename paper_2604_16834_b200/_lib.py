@@ -21,7 +21,7 @@ from .errors import (
     MissingRotationKey,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhe_sm100.so")
+LIB_PATH = os.environ.get("HE_SM100_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhe_sm100.so")
 
 HE_OK, HE_EINVAL, HE_ECUDA, HE_ENOKEY, HE_ELEVEL, HE_ENOMEM, HE_ECONTEXT, HE_ELENGTH = 0, -1, -2, -3, -4, -5, -6, -7
 

@@ -34,16 +34,21 @@ constexpr int CT = 128;  // 4 warps: MG channel groups x PS pixel streams
 constexpr int RS = 24;   // words per tap-word row of a digit plane (16 rows + 8 pad)
 
 struct SqArgs {
-    const uint64_t *const *in;  // [p*H*W] 2-component ciphertexts, ell limbs
+    const uint64_t *ptab;       // [npix][Tpad] input ciphertext address of every tap slot (0 = zero tap)
+    const int32_t *sched;       // [steps][PS] launch pixel of every (step, stream), -1 = idle
     uint64_t *const *out;       // 3-component outputs, ell limbs
     const uint32_t *bfrag;      // [MG][KB][E][32] uint2 B fragments
-    const int32_t *tapi;        // [Tpad] (i << 4) | ((dy+1) << 2) | (dx+1), -1 = padding
     const uint64_t *bias;       // [M][ell] bias * R^-1 mod q (component 0), or nullptr
     const uint64_t *cst;        // [ell] constant added to component 0 of every output, or nullptr
     const uint64_t *r4;         // [ell] R^4 mod q
     const ModConst *mc;
-    int p, H, W, M, ell, logN, pool, y0, y1, nwin, steps;
+    int M, ell, logN, pool, nwin, steps;
 };
+
+// acc += a * b (signed 32 x 32 -> 64, one IMAD.WIDE)
+__device__ __forceinline__ void madw(int64_t &acc, int a, int b) {
+    asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
+}
 
 __device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          const uint2 b) {
@@ -69,25 +74,6 @@ __device__ __forceinline__ uint64_t mont(uint64_t a, uint64_t b, const ModConst 
     return redc(mulhi(a, b), a * b, c.q, c.qinv);
 }
 
-// pixel handled by stream ps at step s; returns false past the end
-__device__ __forceinline__ bool step_pixel(const SqArgs &a, int PS, int ps, int s, int &y, int &x, int &win) {
-    if (a.pool) {
-        const int wq = s >> 2, k = s & 3, w = wq * PS + ps;
-        if (w >= a.nwin) return false;
-        const int Wo = a.W >> 1;
-        y = a.y0 + 2 * (w / Wo) + (k >> 1);
-        x = 2 * (w % Wo) + (k & 1);
-        win = w;
-        return true;
-    }
-    const int pix = s * PS + ps, npix = (a.y1 - a.y0) * a.W;
-    if (pix >= npix) return false;
-    y = a.y0 + pix / a.W;
-    x = pix % a.W;
-    win = 0;
-    return true;
-}
-
 template <int KB, int MG>
 struct Gather {
     static constexpr int PS = 4 / MG;
@@ -105,26 +91,22 @@ struct Gather {
         ps = r2 >> 1;
     }
 
-    __device__ __forceinline__ void load(const SqArgs &a, const int32_t *tapi_s, int s, int l, size_t coff) {
+    __device__ __forceinline__ void load(const SqArgs &a, int s, int l, size_t coff) {
         const size_t N = (size_t)1 << a.logN;
 #pragma unroll
         for (int i = 0; i < TASKS; i++) {
             int ps, comp, kw, j;
             decode(threadIdx.x + CT * i, ps, comp, kw, j);
-            int y, x, win;
-            const bool ok = step_pixel(a, PS, ps, s, y, x, win);
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                uint64_t w = 0;
-                const int ti = tapi_s[4 * kw + u];
-                if (ok && ti >= 0) {
-                    const int yy = y + ((ti >> 2) & 3) - 1, xx = x + (ti & 3) - 1;
-                    if (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) {
-                        const uint64_t *src = a.in[(ti >> 4) * a.H * a.W + yy * a.W + xx];
-                        w = __ldg(src + ((size_t)comp * a.ell + l) * N + coff + j);
-                    }
-                }
-                v[i][u] = w;
+            const int pix = __ldg(a.sched + s * PS + ps);
+            v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0;
+            if (pix >= 0) {
+                const ulonglong2 *pp = (const ulonglong2 *)(a.ptab + ((size_t)pix * KW + kw) * 4);
+                const ulonglong2 p01 = __ldg(pp), p23 = __ldg(pp + 1);
+                const size_t off = ((size_t)comp * a.ell + l) * N + coff + j;
+                if (p01.x) v[i][0] = __ldg((const uint64_t *)p01.x + off);
+                if (p01.y) v[i][1] = __ldg((const uint64_t *)p01.y + off);
+                if (p23.x) v[i][2] = __ldg((const uint64_t *)p23.x + off);
+                if (p23.y) v[i][3] = __ldg((const uint64_t *)p23.y + off);
             }
         }
     }
@@ -153,8 +135,7 @@ struct Gather {
 template <int KB, int E, int MG>
 __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
     constexpr int PS = 4 / MG, KW = KB * 8, PLANE = KW * RS, BUF = PS * 8 * PLANE;
-    extern __shared__ __align__(16) uint32_t xs[];  // [2][BUF] staging, then the tap table
-    int32_t *tapi_s = (int32_t *)(xs + 2 * BUF);
+    extern __shared__ __align__(16) uint32_t xs[];  // [2][BUF] digit-planar staging
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
     const int cg = warp % MG, ps = warp / MG;
@@ -163,7 +144,6 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
     const ModConst c = a.mc[l];
     const int nb = c.q < (1ull << 40) ? 5 : (c.q < (1ull << 48) ? 6 : (c.q < (1ull << 56) ? 7 : 8));
 
-    for (int i = tid; i < KB * 32; i += CT) tapi_s[i] = a.tapi[i];
     uint2 bw[KB][E];
 #pragma unroll
     for (int kb = 0; kb < KB; kb++)
@@ -175,19 +155,19 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
         if (m0 < a.M) bias[0] = a.bias[(size_t)m0 * a.ell + l];
         if (m0 + 1 < a.M) bias[1] = a.bias[(size_t)(m0 + 1) * a.ell + l];
     }
-    __syncthreads();
 
     Gather<KB, MG> g;
-    g.load(a, tapi_s, 0, l, coff);
+    g.load(a, 0, l, coff);
     g.store(xs, nb);
     __syncthreads();
 
-    uint64_t acc[3][2] = {{0, 0}, {0, 0}, {0, 0}};  // window sums (R^-3 domain)
+    // window sums of the products (y R^-1)(y' R^-1), exact 128-bit (hi kept < 2q)
+    u128 acc[3][2];
+#pragma unroll
+    for (int k = 0; k < 3; k++) acc[k][0] = acc[k][1] = u128{0, 0};
     for (int s = 0; s < a.steps; s++) {
-        if (s + 1 < a.steps) g.load(a, tapi_s, s + 1, l, coff);
-        int y, x, win;
-        const bool ok = step_pixel(a, PS, ps, s, y, x, win);
-        if (ok) {
+        if (s + 1 < a.steps) g.load(a, s + 1, l, coff);
+        if (__ldg(a.sched + s * PS + ps) >= 0) {
             const uint32_t *X = xs + (s & 1) * BUF + ps * 8 * PLANE + tig * RS + gid;
             int64_t P[3][4];  // partial sums at 2^0, 2^32, 2^64 for the 4 fragment values
 #pragma unroll
@@ -209,7 +189,7 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
                     for (int e = 0; e < E; e++) {
                         const int sh = d + e;
 #pragma unroll
-                        for (int q = 0; q < 4; q++) P[sh >> 2][q] += (int64_t)C[e][q] << (8 * (sh & 3));
+                        for (int q = 0; q < 4; q++) madw(P[sh >> 2][q], C[e][q], 1 << (8 * (sh & 3)));
                     }
                 }
             }
@@ -226,13 +206,20 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 const uint64_t y0 = add_mod(yv[h], bias[h], c.q), y1 = yv[2 + h];
-                const uint64_t s01 = mont(y0, y1, c);
-                acc[0][h] = add_mod(acc[0][h], mont(y0, y0, c), c.q);
-                acc[1][h] = add_mod(acc[1][h], add_mod(s01, s01, c.q), c.q);
-                acc[2][h] = add_mod(acc[2][h], mont(y1, y1, c), c.q);
+                mac128(acc[0][h], y0, y0);
+                mac128(acc[1][h], y0, y1);
+                mac128(acc[2][h], y1, y1);
+            }
+            if ((s & 7) == 7) {  // each product adds < q/16 to hi: fold every 8 pixels
+#pragma unroll
+                for (int k = 0; k < 3; k++)
+#pragma unroll
+                    for (int h = 0; h < 2; h++)
+                        if (acc[k][h].hi >= c.q) acc[k][h].hi -= c.q;
             }
             if (a.pool && (s & 3) == 3) {  // window complete
                 const uint64_t r4 = a.r4[l], cst = a.cst ? a.cst[l] : 0;
+                const int win = (s >> 2) * PS + ps;
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
                     const int m = m0 + h;
@@ -240,25 +227,37 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
                         uint64_t *o = a.out[(size_t)m * a.nwin + win] + coff + gid;
 #pragma unroll
                         for (int k = 0; k < 3; k++) {
-                            uint64_t v = mont(acc[k][h], r4, c);
+                            const uint64_t hi = acc[k][h].hi >= c.q ? acc[k][h].hi - c.q : acc[k][h].hi;
+                            uint64_t r = redc(hi, acc[k][h].lo, c.q, c.qinv);  // sum R^-3
+                            if (k == 1) r = add_mod(r, r, c.q);
+                            uint64_t v = mont(r, r4, c);
                             if (k == 0) v = add_mod(v, cst, c.q);
                             o[((size_t)k * a.ell + l) * N] = v;
                         }
                     }
-                    acc[0][h] = acc[1][h] = acc[2][h] = 0;
+#pragma unroll
+                    for (int k = 0; k < 3; k++) acc[k][h] = u128{0, 0};
                 }
             }
         }
         if (s + 1 < a.steps) g.store(xs + ((s + 1) & 1) * BUF, nb);
         __syncthreads();
     }
-    if (!a.pool) {  // global sum: combine the pixel streams, then store
+    if (!a.pool) {  // global sum: reduce, combine the pixel streams, then store
+        uint64_t r[3][2];
+#pragma unroll
+        for (int k = 0; k < 3; k++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint64_t hi = acc[k][h].hi >= c.q ? acc[k][h].hi - c.q : acc[k][h].hi;
+                r[k][h] = redc(hi, acc[k][h].lo, c.q, c.qinv);
+            }
         uint64_t *red = (uint64_t *)xs;
         if (PS > 1) {
 #pragma unroll
             for (int k = 0; k < 3; k++)
 #pragma unroll
-                for (int h = 0; h < 2; h++) red[((ps * MG + cg) * 32 + lane) * 6 + k * 2 + h] = acc[k][h];
+                for (int h = 0; h < 2; h++) red[((ps * MG + cg) * 32 + lane) * 6 + k * 2 + h] = r[k][h];
             __syncthreads();
             if (ps == 0)
                 for (int o = 1; o < PS; o++)
@@ -266,7 +265,7 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
                     for (int k = 0; k < 3; k++)
 #pragma unroll
                         for (int h = 0; h < 2; h++)
-                            acc[k][h] = add_mod(acc[k][h], red[((o * MG + cg) * 32 + lane) * 6 + k * 2 + h], c.q);
+                            r[k][h] = add_mod(r[k][h], red[((o * MG + cg) * 32 + lane) * 6 + k * 2 + h], c.q);
         }
         if (ps == 0) {
             const uint64_t r4 = a.r4[l], cst = a.cst ? a.cst[l] : 0;
@@ -277,7 +276,8 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
                 uint64_t *o = a.out[m] + coff + gid;
 #pragma unroll
                 for (int k = 0; k < 3; k++) {
-                    uint64_t v = mont(acc[k][h], r4, c);
+                    const uint64_t rr = k == 1 ? add_mod(r[k][h], r[k][h], c.q) : r[k][h];
+                    uint64_t v = mont(rr, r4, c);
                     if (k == 0) v = add_mod(v, cst, c.q);
                     o[((size_t)k * a.ell + l) * N] = v;
                 }
@@ -394,11 +394,6 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
                         bf[((((size_t)cg * KB + kb) * E + e) * 32 + lane) * 2 + r] = reg;
                     }
                 }
-    std::vector<int32_t> tapi(KB * 32, -1);
-    for (int k = 0; k < T; k++) {
-        const int i = k / 9, t = k % 9;
-        tapi[k] = (i << 4) | ((t / 3) << 2) | (t % 3);
-    }
     // per-limb constants: R^4, bias * R^-1
     std::vector<uint64_t> r4(ell), bres(bias ? (size_t)M * ell : 0);
     for (int l = 0; l < ell; l++) {
@@ -422,14 +417,33 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
     }
     cudaStream_t s = (cudaStream_t)stream;
     const int nwin = pool ? ((y1 - y0) / 2) * (W / 2) : 1;
-    const int n_in = p * H * W, n_out = pool ? M * nwin : M;
-    void **din = nullptr, **dout = nullptr;
-    HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
+    const int n_out = pool ? M * nwin : M, npix = (y1 - y0) * W, Tpad = KB * 32, PS = 4 / MGk;
+    const int steps = pool ? ((nwin + PS - 1) / PS) * 4 : (npix + PS - 1) / PS;
+    // tap address table [launch pixel][tap slot] and the (step, stream) -> pixel schedule
+    std::vector<uint64_t> ptab((size_t)npix * Tpad, 0);
+    for (int y = y0; y < y1; y++)
+        for (int x = 0; x < W; x++)
+            for (int k = 0; k < T; k++) {
+                const int i = k / 9, t = k % 9, yy = y + t / 3 - 1, xx = x + t % 3 - 1;
+                if (yy >= 0 && yy < H && xx >= 0 && xx < W)
+                    ptab[((size_t)(y - y0) * W + x) * Tpad + k] = (uint64_t)in[(size_t)i * H * W + yy * W + xx];
+            }
+    std::vector<int32_t> sched((size_t)steps * PS, -1);
+    for (int st = 0; st < steps; st++)
+        for (int q = 0; q < PS; q++) {
+            if (pool) {
+                const int w = (st >> 2) * PS + q, k = st & 3, Wo = W / 2;
+                if (w < nwin) sched[(size_t)st * PS + q] = (2 * (w / Wo) + (k >> 1)) * W + 2 * (w % Wo) + (k & 1);
+            } else if (st * PS + q < npix) {
+                sched[(size_t)st * PS + q] = st * PS + q;
+            }
+        }
+    void **dout = nullptr;
     HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
-    const size_t b_bf = bf.size() * 4, b_ti = tapi.size() * 4, b_r4 = (size_t)ell * 8, b_b = bres.size() * 8,
-                 b_c = cst ? (size_t)ell * 8 : 0;
+    const size_t b_bf = bf.size() * 4, b_pt = ptab.size() * 8, b_sc = sched.size() * 4, b_r4 = (size_t)ell * 8,
+                 b_b = bres.size() * 8, b_c = cst ? (size_t)ell * 8 : 0;
     char *meta = nullptr;
-    HE_TRY(he_scratch_alloc((void **)&meta, b_bf + b_ti + b_r4 + b_b + b_c + 64, s));
+    HE_TRY(he_scratch_alloc((void **)&meta, b_bf + b_pt + b_sc + b_r4 + b_b + b_c + 128, s));
     size_t off = 0;
     auto carve = [&](size_t bytes) {
         char *p = meta + off;
@@ -437,41 +451,36 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
         return p;
     };
     uint32_t *dbf = (uint32_t *)carve(b_bf);
-    int32_t *dti = (int32_t *)carve(b_ti);
+    uint64_t *dpt = (uint64_t *)carve(b_pt);
+    int32_t *dsc = (int32_t *)carve(b_sc);
     uint64_t *dr4 = (uint64_t *)carve(b_r4);
     uint64_t *db = bias ? (uint64_t *)carve(b_b) : nullptr;
     uint64_t *dc = cst ? (uint64_t *)carve(b_c) : nullptr;
     HE_CHECK_CUDA(cudaMemcpyAsync(dbf, bf.data(), b_bf, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dti, tapi.data(), b_ti, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(cudaMemcpyAsync(dpt, ptab.data(), b_pt, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(cudaMemcpyAsync(dsc, sched.data(), b_sc, cudaMemcpyHostToDevice, s));
     HE_CHECK_CUDA(cudaMemcpyAsync(dr4, r4.data(), b_r4, cudaMemcpyHostToDevice, s));
     if (db) HE_CHECK_CUDA(cudaMemcpyAsync(db, bres.data(), b_b, cudaMemcpyHostToDevice, s));
     if (dc) HE_CHECK_CUDA(cudaMemcpyAsync(dc, cst, b_c, cudaMemcpyHostToDevice, s));
     SqArgs a;
-    a.in = (const uint64_t *const *)din;
+    a.ptab = dpt;
+    a.sched = dsc;
     a.out = (uint64_t *const *)dout;
     a.bfrag = dbf;
-    a.tapi = dti;
     a.bias = db;
     a.cst = dc;
     a.r4 = dr4;
     a.mc = c->d_mc;
-    a.p = p;
-    a.H = H;
-    a.W = W;
     a.M = M;
     a.ell = ell;
     a.logN = c->logN;
     a.pool = pool;
-    a.y0 = y0;
-    a.y1 = y1;
     a.nwin = nwin;
-    const int PS = 4 / MGk;
-    a.steps = pool ? ((nwin + PS - 1) / PS) * 4 : ((y1 - y0) * W + PS - 1) / PS;
-    const size_t smem = (size_t)2 * PS * 8 * (KB * 8 * RS) * 4 + (size_t)KB * 32 * 4;
+    a.steps = steps;
+    const size_t smem = (size_t)2 * PS * 8 * (KB * 8 * RS) * 4;
     dim3 grid((unsigned)(c->N / 8), (unsigned)ell);
     int rc = dispatch_sq(KB, E, MGk, grid, smem, s, a);
     he_scratch_free(meta, s);
-    he_scratch_free(din, s);
     he_scratch_free(dout, s);
     return rc;
 }

@@ -63,22 +63,29 @@ __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs,
 #pragma unroll
         for (int j = 0; j < 16; j++) x[j] = jb.src[(g + 16 * j) * 256 + col];
     } else if (LD == L_BCONV) {
-        uint64_t t[8];
+        // source-major: 16 independent loads in flight per source limb; with
+        // v_s, t_s < q < 2^61 each product adds < q/8 to the high word, so
+        // ns <= 8 terms keep hi < q without folding (redc's precondition)
+        u128 acc[16];
 #pragma unroll
-        for (int s = 0; s < 8; s++) t[s] = s < jb.ns ? jb.tab[s] : 0;
+        for (int j = 0; j < 16; j++) acc[j] = u128{0, 0};
+        for (int s = 0; s < jb.ns; s++) {
+            const uint64_t t = __ldg(jb.tab + s);
+            const uint64_t *src = jb.src + (size_t)s * NN + col;
+            uint64_t v[16];
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const size_t idx = (g + 16 * j) * 256 + col;
-            u128 acc = {0, 0};
+            for (int j = 0; j < 16; j++) v[j] = __ldg(src + (g + 16 * j) * 256);
 #pragma unroll
-            for (int s = 0; s < 8; s++) {
-                if (s < jb.ns) {
-                    mac128(acc, jb.src[(size_t)s * NN + idx], t[s]);  // v_s < 2^61, t < q: hi < q kept by fold
-                    if (acc.hi >= c.q) acc.hi -= c.q;
-                }
-            }
-            x[j] = redc(acc.hi, acc.lo, c.q, c.qinv);
+            for (int j = 0; j < 16; j++) mac128(acc[j], v[j], t);
+            if ((s & 7) == 7)  // more than 8 sources: fold (hi < 2q -> < q)
+#pragma unroll
+                for (int j = 0; j < 16; j++) acc[j].hi = acc[j].hi >= c.q ? acc[j].hi - c.q : acc[j].hi;
         }
+        if (jb.ns > 8 && (jb.ns & 7))
+#pragma unroll
+            for (int j = 0; j < 16; j++) acc[j].hi = acc[j].hi >= c.q ? acc[j].hi - c.q : acc[j].hi;
+#pragma unroll
+        for (int j = 0; j < 16; j++) x[j] = redc(acc[j].hi, acc[j].lo, c.q, c.qinv);
     } else {
         const uint64_t half = (jb.ql - 1) >> 1;
 #pragma unroll
@@ -209,13 +216,18 @@ struct IpArgs {
     uint64_t *acc;        // [B][2][ext_n][N]
     const uint64_t *tw;
     const ModConst *mc;
-    int ell, ext_n, beta, alpha, L, M;
+    int ell, ext_n, beta, alpha, L, M, B;
 };
 
-__global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
+#ifndef HE_IP_MINB
+#define HE_IP_MINB 2
+#endif
+__global__ void __launch_bounds__(NTT_TPB, HE_IP_MINB) k_modup_ip(const IpArgs a) {
     __shared__ uint64_t sm[16 * 272];
-    const int rt = blockIdx.x & 15, bt = blockIdx.x >> 4;
-    const int t = bt % a.ext_n, b = bt / a.ext_n;
+    // ciphertext-fastest order: CTAs resident together read the same key rows
+    // (dnum x 2 x 16 rows of limb t), so the key streams from L2, not HBM
+    const int b = blockIdx.x % a.B, rest = blockIdx.x / a.B;
+    const int rt = rest & 15, t = rest >> 4;
     const int m = t < a.ell ? t : a.L + (t - a.ell);
     const ModConst c = a.mc[m];
     const ulonglong2 *W2 = tw_fwd(a.tw, m, LOGN);
@@ -223,9 +235,11 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
     const uint32_t r = rt * 16 + rl;
     const int jt = t < a.ell ? t / a.alpha : -1;
     uint64_t *s = sm + rl * 272;
-    uint64_t acc0[16], acc1[16];
+    // lazy inner product: exact 128-bit sums of x * key (key in Montgomery
+    // form), one REDC at the end; each product adds < q/8 to hi (q < 2^61)
+    u128 acc0[16], acc1[16];
 #pragma unroll
-    for (int j = 0; j < 16; j++) acc0[j] = acc1[j] = 0;
+    for (int j = 0; j < 16; j++) acc0[j] = acc1[j] = u128{0, 0};
     for (int dj = 0; dj < a.beta; dj++) {
         uint64_t x[16];
         if (dj == jt) {
@@ -257,16 +271,28 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
         for (int j = 0; j < 16; j++) {
             const int cc = g + 16 * j;
             const uint64_t w0 = __ldg(k0 + cc), w1 = __ldg(k1 + cc);
-            acc0[j] = add_mod(acc0[j], redc(mulhi(x[j], w0), x[j] * w0, c.q, c.qinv), c.q);
-            acc1[j] = add_mod(acc1[j], redc(mulhi(x[j], w1), x[j] * w1, c.q, c.qinv), c.q);
+            mac128(acc0[j], x[j], w0);
+            mac128(acc1[j], x[j], w1);
         }
+        if ((dj & 7) == 7)
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                acc0[j].hi = acc0[j].hi >= c.q ? acc0[j].hi - c.q : acc0[j].hi;
+                acc1[j].hi = acc1[j].hi >= c.q ? acc1[j].hi - c.q : acc1[j].hi;
+            }
     }
     uint64_t *o0 = a.acc + ((((size_t)b * 2) * a.ext_n + t) << LOGN) + r * 256;
     uint64_t *o1 = o0 + ((size_t)a.ext_n << LOGN);
+    const bool fold = a.beta > 8 && (a.beta & 7);
 #pragma unroll
     for (int j = 0; j < 16; j++) {
-        o0[g + 16 * j] = acc0[j];
-        o1[g + 16 * j] = acc1[j];
+        uint64_t h0 = acc0[j].hi, h1 = acc1[j].hi;
+        if (fold) {
+            h0 = h0 >= c.q ? h0 - c.q : h0;
+            h1 = h1 >= c.q ? h1 - c.q : h1;
+        }
+        o0[g + 16 * j] = redc(h0, acc0[j].lo, c.q, c.qinv);
+        o1[g + 16 * j] = redc(h1, acc1[j].lo, c.q, c.qinv);
     }
 }
 
@@ -385,6 +411,7 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
         a.alpha = alpha;
         a.L = L;
         a.M = M;
+        a.B = B;
         k_modup_ip<<<(unsigned)(B * ext_n * 16), NTT_TPB, 0, s>>>(a);
         he_count_launch(1);
         if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
