@@ -258,6 +258,14 @@ def main():
     traffic = _traffic().get(dom_name)
     breakdown = {k: {"calls": v[0], "ms": round(v[1], 2), "alg_GBps": round(v[2][0] / max(v[1], 1e-9) / 1e6, 1),
                      "GMACps": round(v[2][1] / max(v[1], 1e-9) / 1e6, 1)} for k, v in summ.items()}
+    # the key switch is integer-pipe bound: its second roofline is algorithmic modular
+    # multiplications (NTT butterflies + BConv + inner product) against the
+    # measured 64x64->128 multiply-accumulate rate of this GPU (he_microbench_intpipe)
+    ip = np.zeros(2)
+    _lib.check(_lib.load().he_microbench_intpipe(local, ip.ctypes.data), "microbench")
+    int_ach = units[1] / (dom_ms / 1e3)
+    int_roof = {"achieved": int_ach, "peak": float(ip[1]), "unit": "modmul/s", "frac": int_ach / float(ip[1]),
+                "peak_source": "measured mac128/s (he_microbench_intpipe)", "imad32_per_s": float(ip[0])}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -279,8 +287,7 @@ def main():
                     "d2h_bytes_per_step": int(out_host.numel() * 8)},
             "roofline": {"kernel": dom_name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "calls": calls, "avg_ms": dom_ms / calls,
-                         "int_GMACps": units[1] / (dom_ms / 1e3) / 1e9},
+                         "calls": calls, "avg_ms": dom_ms / calls, "int_pipe": int_roof},
             "breakdown": breakdown,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),

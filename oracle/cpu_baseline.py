@@ -23,9 +23,9 @@ import oracle as O  # noqa: E402
 
 def cfg3_op_counts():
     """Exact per-group op counts of the frozen config-3 plan (featuremajor.run_cnn):
-    conv1 at 14 limbs (deferred rescale) -> square+pool sums -> relin at 14 ->
-    2 rescales -> conv2 at 12 -> square+GAP sums -> relin at 12 -> 2 rescales
-    -> dense at 10 limbs -> rescale."""
+    conv1 at 14 limbs (deferred rescale) -> square+pool sums -> relin with a
+    joint 2-limb ModDown at 14 -> conv2 at 12 -> square+GAP sums -> relin with a
+    joint 2-limb ModDown at 12 -> dense at 10 limbs -> rescale."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
     from paper_2604_16834_b200.featuremajor import conv3x3_csr
@@ -38,8 +38,8 @@ def cfg3_op_counts():
         "lincomb_macs": nnz1 * 2 * 14 * N + nnz2 * 2 * 12 * N + 320 * 2 * 10 * N,
         # squares summed into pools / GAP: 4 modular products per coefficient
         "square_macs": 16384 * 4 * 14 * N + 8192 * 4 * 12 * N,
-        "relin": [(4096, 14), (32, 12)],
-        "rescale": [(4096, 14), (4096, 13), (32, 12), (32, 11), (10, 10)],
+        "relin_rescale2": [(4096, 14), (32, 12)],
+        "rescale": [(10, 10)],
     }
 
 
@@ -69,19 +69,19 @@ def measure(seconds_budget: float = 20.0, threads: int | None = None, seed: int 
     orc.lincomb(ins, rows, cols, w, n_threads=threads)
     dt = time.perf_counter() - t
     res["lincomb_mac_per_s"] = len(cols) * 2 * 14 * N / dt
-    # 2. relinearisation of 3-component ciphertexts, one per host thread
+    # 2. relinearisation + joint 2-limb ModDown of 3-component ciphertexts, one per host thread
     rk = orc.switch_key(0)
     per_relin = {}
     for ell in (14, 12):
         a = [rand_ct(ell, 3) for _ in range(threads)]
         t = time.perf_counter()
         with ThreadPoolExecutor(threads) as ex:
-            list(ex.map(lambda c: orc.relin(c, rk), a))
+            list(ex.map(lambda c: orc.relin_rescale(c, rk, 2), a))
         per_relin[ell] = (time.perf_counter() - t) / threads
     res["relin_s"] = per_relin
     # 3. rescale
     per_rs = {}
-    for ell in (14, 12):
+    for ell in (10,):
         a = [rand_ct(ell) for _ in range(threads)]
         t = time.perf_counter()
         with ThreadPoolExecutor(threads) as ex:
@@ -95,13 +95,13 @@ def measure(seconds_budget: float = 20.0, threads: int | None = None, seed: int 
         list(ex.map(lambda c: orc.tensor(c, c), a))
     res["square_mac_per_s"] = threads * 4 * 14 * N / (time.perf_counter() - t)
     total = ops["lincomb_macs"] / res["lincomb_mac_per_s"] + ops["square_macs"] / res["square_mac_per_s"]
-    total += sum(cnt * per_relin[14 if ell > 12 else 12] * ell / (14 if ell > 12 else 12) for cnt, ell in ops["relin"])
-    total += sum(cnt * per_rs[14 if ell > 12 else 12] * ell / (14 if ell > 12 else 12) for cnt, ell in ops["rescale"])
+    total += sum(cnt * per_relin[ell] for cnt, ell in ops["relin_rescale2"])
+    total += sum(cnt * per_rs[ell] for cnt, ell in ops["rescale"])
     res["group_seconds_extrapolated"] = total
     res["samples_per_s"] = 32768.0 / total
     res["sample"] = (f"oracle on {threads} host threads running the same plan as the GPU: {n_out}x{k}-term lincomb "
-                     f"at 14 limbs, {threads} relinearisations at 14 and 12 limbs, {threads} rescales at 14 and 12 "
-                     f"limbs, {threads} tensor products; extrapolated with the exact config-3 op counts of one "
+                     f"at 14 limbs, {threads} relinearisations with a joint 2-limb ModDown at 14 and 12 limbs, "
+                     f"{threads} rescales at 10 limbs, {threads} tensor products; extrapolated with the exact config-3 op counts of one "
                      f"32768-sample group")
     return res
 

@@ -671,6 +671,18 @@ class GpuEngine:
         self._acct.bump("adds", int(len(cl)) + max(0, int(len(cl)) - n_out))
         return self._wrap_batch(out, level, [s * s * scale_mult] * n_out)
 
+    def _ks_modmuls(self, limbs: int, drops: int) -> float:
+        """Algorithmic modular multiplications of one relinearisation with a
+        joint ModDown over P and ``drops`` limbs (SURVEY.md 8d key-switch row):
+        NTT butterflies + ModUp / ModDown BConv MACs + inner-product MACs."""
+        K, alpha, N = len(self.context.p_chain_bits), self.context.alpha, self.N
+        digits = [min(alpha, limbs - j * alpha) for j in range(-(-limbs // alpha))]
+        ext = limbs + K
+        n_ntt = limbs + sum(ext - a for a in digits) + 2 * (K + drops) + 2 * (limbs - drops)
+        bconv = sum(a * (ext - a) for a in digits) + 2 * (K + drops) * (limbs - drops)
+        ip = 2 * len(digits) * ext
+        return float(n_ntt * (N // 2) * int(math.log2(N)) + (bconv + ip) * N)
+
     def relin_rescale_batch(self, cts: Sequence[CipherVec], drops: int = 1) -> list[CipherVec]:
         """3-component ciphertexts -> relinearise (key switch of c2) -> rescale
         ``drops`` times (2 after a deferred-rescale linear layer)."""
@@ -691,7 +703,8 @@ class GpuEngine:
             po = self._tptrs(out)
             _lib.check(self._call("relin", self._L.he_relin_rescale, self._h, _lib.addr(pi), _lib.addr(po), len(cts),
                                   limbs, drops, self.stream,
-                                  units=(len(cts) * (5.0 * limbs - 2 * drops) * self.N * 8, 0.0)), "relin_rescale")
+                                  units=(len(cts) * (5.0 * limbs - 2 * drops) * self.N * 8,
+                                         len(cts) * self._ks_modmuls(limbs, drops))), "relin_rescale")
             for k in range(drops):
                 ql = self.moduli[limbs - 1 - k]
                 scales = [s / ql for s in scales]
