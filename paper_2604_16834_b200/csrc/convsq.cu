@@ -11,19 +11,24 @@
 //     C_d[(comp, j)][(e, m)] = sum_k  byte_d(x_{k, comp, j}) * W_e[m][k]
 // (rows: 2 components x 8 coefficients, so the lane holding row j of
 // component 0 also holds component 1 -- the square needs both), one
-// mma.sync m16n8k32 u8 x s8 per (digit plane d, 32-tap block, weight digit e).
-// Digit planes beyond the limb's byte length (5 for 40-bit primes) are
-// skipped.  The lane recombines its values exactly (int64 partial sums at
-// 2^0 / 2^32 / 2^64, one signed 128-bit total), reduces with ONE Montgomery
-// step (y R^-1), squares in the Montgomery domain and accumulates the window
-// sums; the window result is scaled back with R^4 and stored as three
-// components.  Bit-identical to conv -> tensor -> add_const -> sum, because
-// every step is exact arithmetic mod q.
+// mma.sync m16n8k32 u8 x s8 per (input byte plane d, 32-byte K block, weight
+// digit e).  Byte planes beyond the limb's length (5 for 40-bit primes) are
+// skipped.  The lane recombines its values exactly (int32 sums per byte
+// shift, IMAD.WIDE into int64 partial sums at 2^0 / 2^32 / 2^64, one signed
+// 128-bit total), reduces with ONE Montgomery step (y R^-1), accumulates the
+// window's squares as exact 128-bit sums and reduces them once; the window
+// result is scaled back with R^4 and stored as three components.
+// Bit-identical to conv -> tensor -> add_const -> sum: every step is exact
+// arithmetic mod q.
 //
-// Data path: taps are gathered from global memory one pixel ahead into
-// registers (software pipeline), byte-transposed with PRMT and stored
-// digit-planar ([d][tap word][row], 24-word rows: conflict-free STS and LDS);
-// the weight digits live in registers for the whole kernel.
+// Data path: the K dimension is ordered (tap, group of 4 input channels), so
+// one 32-bit A-operand word is "byte d of 4 channels at one input pixel".
+// Input rows are loaded ONCE per CTA into a shared-memory ring (R rows x
+// (W+2) pixels incl. a zero halo), byte-transposed with PRMT into that
+// digit-planar, channel-interleaved layout; every output pixel then reads its
+// 9 taps straight from the ring (no per-tap gather).  Strides are chosen so
+// the A-fragment loads are bank-conflict free.  Weight digits stay in
+// registers for the whole kernel.
 #include <algorithm>
 
 #include "common.cuh"
@@ -31,18 +36,20 @@
 namespace {
 
 constexpr int CT = 128;  // 4 warps: MG channel groups x PS pixel streams
-constexpr int RS = 24;   // words per tap-word row of a digit plane (16 rows + 8 pad)
 
 struct SqArgs {
-    const uint64_t *ptab;       // [npix][Tpad] input ciphertext address of every tap slot (0 = zero tap)
-    const int32_t *sched;       // [steps][PS] launch pixel of every (step, stream), -1 = idle
+    const uint64_t *const *in;  // [p*H*W] 2-component input ciphertexts (device array of addresses)
     uint64_t *const *out;       // 3-component outputs, ell limbs
     const uint32_t *bfrag;      // [MG][KB][E][32] uint2 B fragments
     const uint64_t *bias;       // [M][ell] bias * R^-1 mod q (component 0), or nullptr
     const uint64_t *cst;        // [ell] constant added to component 0 of every output, or nullptr
     const uint64_t *r4;         // [ell] R^4 mod q
     const ModConst *mc;
-    int M, ell, logN, pool, nwin, steps;
+    const int32_t *limbs;       // [gridDim.y] limb handled by blockIdx.y (one byte-plane count per launch)
+    int p, H, W, M, ell, logN, pool, y0, y1, nwin;
+    int ncg, nb, R;             // channel groups of 4, byte planes stored, ring rows
+    int pstr, rstr;             // ring strides in 32-bit words: pixel, ring row
+    int mul[4];                 // 1, 2^8, 2^16, 2^24
 };
 
 // acc += a * b (signed 32 x 32 -> 64, one IMAD.WIDE)
@@ -74,152 +81,204 @@ __device__ __forceinline__ uint64_t mont(uint64_t a, uint64_t b, const ModConst 
     return redc(mulhi(a, b), a * b, c.q, c.qinv);
 }
 
-template <int KB, int MG>
-struct Gather {
-    static constexpr int PS = 4 / MG;
-    static constexpr int KW = KB * 8;
-    static constexpr int TASKS = PS * KB;  // per thread: PS streams x 2 comps x KW/4 quads x 32 lanes / CT
-    uint64_t v[TASKS][4];
+// row r of channel group cg inside a pixel: groups 2, 3 swap their halves so
+// the four groups read by one A-fragment load hit 32 distinct banks
+__device__ __forceinline__ int rowpos(int cg, int r) { return cg * 16 + (r ^ (8 * ((cg >> 1) & 1))); }
 
-    // task t = tid + CT * i -> (stream, comp, quad of tap words, kw sub, coefficient j)
-    __device__ __forceinline__ static void decode(int t, int &ps, int &comp, int &kw, int &j) {
-        const int ln = t & 31, rest = t >> 5;
-        j = ln & 7;
-        const int kq = rest % (KW / 4), r2 = rest / (KW / 4);
-        kw = kq * 4 + (ln >> 3);
-        comp = r2 & 1;
-        ps = r2 >> 1;
-    }
-
-    __device__ __forceinline__ void load(const SqArgs &a, int s, int l, size_t coff) {
-        const size_t N = (size_t)1 << a.logN;
+// Input row yy -> ring slot: word (x' + 1) * pstr + d * (16 ncg) + rowpos(cg, comp*8 + j)
+// holds byte d of channels 4cg .. 4cg+3 at pixel (yy, x'), coefficient j of component comp.
+__device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, int yy, int l, size_t coff) {
+    const size_t N = (size_t)1 << a.logN;
+    const int dstr = 16 * a.ncg, ntask = a.W * a.ncg * 16;
+    const bool inside = yy >= 0 && yy < a.H;
+    for (int t = threadIdx.x; t < ntask; t += CT) {
+        const int r = t & 15, rest = t >> 4, cg = rest % a.ncg, x = rest / a.ncg;
+        uint64_t v[4] = {0, 0, 0, 0};
+        if (inside) {
+            const size_t off = ((size_t)(r >> 3) * a.ell + l) * N + coff + (r & 7);
 #pragma unroll
-        for (int i = 0; i < TASKS; i++) {
-            int ps, comp, kw, j;
-            decode(threadIdx.x + CT * i, ps, comp, kw, j);
-            const int pix = __ldg(a.sched + s * PS + ps);
-            v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0;
-            if (pix >= 0) {
-                const ulonglong2 *pp = (const ulonglong2 *)(a.ptab + ((size_t)pix * KW + kw) * 4);
-                const ulonglong2 p01 = __ldg(pp), p23 = __ldg(pp + 1);
-                const size_t off = ((size_t)comp * a.ell + l) * N + coff + j;
-                if (p01.x) v[i][0] = __ldg((const uint64_t *)p01.x + off);
-                if (p01.y) v[i][1] = __ldg((const uint64_t *)p01.y + off);
-                if (p23.x) v[i][2] = __ldg((const uint64_t *)p23.x + off);
-                if (p23.y) v[i][3] = __ldg((const uint64_t *)p23.y + off);
+            for (int u = 0; u < 4; u++) {
+                const int i = cg * 4 + u;
+                if (i < a.p) v[u] = __ldg(a.in[(size_t)i * a.H * a.W + yy * a.W + x] + off);
             }
         }
+        uint32_t lo[4], hi[4];
+        tr4((uint32_t)v[0], (uint32_t)v[1], (uint32_t)v[2], (uint32_t)v[3], lo);
+        tr4((uint32_t)(v[0] >> 32), (uint32_t)(v[1] >> 32), (uint32_t)(v[2] >> 32), (uint32_t)(v[3] >> 32), hi);
+        uint32_t *dst = slot + (x + 1) * a.pstr + rowpos(cg, r);
+#pragma unroll
+        for (int d = 0; d < 4; d++) dst[d * dstr] = lo[d];
+#pragma unroll
+        for (int d = 0; d < 4; d++)
+            if (d + 4 < a.nb) dst[(d + 4) * dstr] = hi[d];
     }
+}
 
-    // digit-planar store: word (d, kw, row = comp*8 + j) of the stream's buffer
-    __device__ __forceinline__ void store(uint32_t *buf, int nb) const {
-        constexpr int PLANE = KW * RS;
+// One input byte plane D: C[e] = sum_k byte_D(x_k) W_e[k] on the tensor cores,
+// then the exact recombination.  W[j][q] is the int32 sum of the products with
+// byte shift D + j still open (|C| < 2^23, <= E terms: no overflow); a
+// completed shift s is folded into P[s/4] with one IMAD.WIDE by 2^(8 (s%4))
+// (multipliers held in registers so ptxas keeps IMAD.WIDE).
+template <int D, int KB, int E, int NB>
+__device__ __forceinline__ void digit_plane(const uint32_t *X, int dstr, const int (&o0)[KB][2], const int (&o1)[KB][2],
+                                            const uint2 (&bw)[KB][E], int (&W)[E][4], int64_t (&P)[3][4],
+                                            const int (&mul)[4]) {
+    if (D >= NB) return;
+    const uint32_t *Xd = X + D * dstr;
+    int C[E][4];
 #pragma unroll
-        for (int i = 0; i < TASKS; i++) {
-            int ps, comp, kw, j;
-            decode(threadIdx.x + CT * i, ps, comp, kw, j);
-            uint32_t lo[4], hi[4];
-            tr4((uint32_t)v[i][0], (uint32_t)v[i][1], (uint32_t)v[i][2], (uint32_t)v[i][3], lo);
-            tr4((uint32_t)(v[i][0] >> 32), (uint32_t)(v[i][1] >> 32), (uint32_t)(v[i][2] >> 32),
-                (uint32_t)(v[i][3] >> 32), hi);
-            uint32_t *dst = buf + (size_t)ps * 8 * PLANE + kw * RS + comp * 8 + j;
+    for (int e = 0; e < E; e++) C[e][0] = C[e][1] = C[e][2] = C[e][3] = 0;
 #pragma unroll
-            for (int d = 0; d < 4; d++) dst[d * PLANE] = lo[d];
+    for (int kb = 0; kb < KB; kb++) {
+        const uint32_t a0 = Xd[o0[kb][0]], a1 = Xd[o1[kb][0]], a2 = Xd[o0[kb][1]], a3 = Xd[o1[kb][1]];
 #pragma unroll
-            for (int d = 0; d < 4; d++)
-                if (d + 4 < nb) dst[(d + 4) * PLANE] = hi[d];
-        }
+        for (int e = 0; e < E; e++) mma_u8s8(C[e], a0, a1, a2, a3, bw[kb][e]);
     }
-};
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+#pragma unroll
+        for (int e = 0; e < E; e++) W[e][q] += C[e][q];
+        madw(P[D >> 2][q], W[0][q], mul[D & 3]);  // shift D is complete
+#pragma unroll
+        for (int j = 0; j + 1 < E; j++) W[j][q] = W[j + 1][q];
+        W[E - 1][q] = 0;
+    }
+    if (D == NB - 1) {  // last byte plane: flush shifts NB .. NB + E - 2
+#pragma unroll
+        for (int j = 0; j + 1 < E; j++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) madw(P[(D + 1 + j) >> 2][q], W[j][q], mul[(D + 1 + j) & 3]);
+    }
+}
 
-template <int KB, int E, int MG>
-__global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
-    constexpr int PS = 4 / MG, KW = KB * 8, PLANE = KW * RS, BUF = PS * 8 * PLANE;
-    extern __shared__ __align__(16) uint32_t xs[];  // [2][BUF] digit-planar staging
+template <int KB, int E, int MG, int NB>
+__global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs a) {
+    constexpr int PS = 4 / MG;
+    extern __shared__ __align__(16) uint32_t xs[];  // ring [R][rstr]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
     const int cg = warp % MG, ps = warp / MG;
-    const int l = blockIdx.y;
+    const int l = a.limbs[blockIdx.y];
     const size_t N = (size_t)1 << a.logN, coff = (size_t)blockIdx.x * 8;
     const ModConst c = a.mc[l];
-    const int nb = c.q < (1ull << 40) ? 5 : (c.q < (1ull << 48) ? 6 : (c.q < (1ull << 56) ? 7 : 8));
+    const int dstr = 16 * a.ncg;
 
     uint2 bw[KB][E];
 #pragma unroll
     for (int kb = 0; kb < KB; kb++)
 #pragma unroll
         for (int e = 0; e < E; e++) bw[kb][e] = ((const uint2 *)a.bfrag)[((cg * KB + kb) * E + e) * 32 + lane];
+    const int mul[4] = {a.mul[0], a.mul[1], a.mul[2], a.mul[3]};
     const int m0 = cg * 8 + 2 * tig;  // this lane's channels m0, m0 + 1
     uint64_t bias[2] = {0, 0};
     if (a.bias) {
         if (m0 < a.M) bias[0] = a.bias[(size_t)m0 * a.ell + l];
         if (m0 + 1 < a.M) bias[1] = a.bias[(size_t)(m0 + 1) * a.ell + l];
     }
+    // this lane's A words: word w = kb*8 + h*4 + tig -> (tap t, channel group g);
+    // words past the 9 taps carry zero weights and read tap 0
+    // packed per word: offset inside the ring row (dx * pstr + row position of
+    // component 0) in bits 3.., tap row dy in bits 0..1, bit 2 = component 1 sits 8 words lower
+    int wd[KB][2];
+#pragma unroll
+    for (int kb = 0; kb < KB; kb++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int w = kb * 8 + h * 4 + tig;
+            int t = w / a.ncg, g = w % a.ncg;
+            if (t >= 9) t %= 9;  // zero-weight word: any in-bounds tap, spread over the banks
+            const int r0 = rowpos(g, gid), r1 = rowpos(g, gid + 8);
+            wd[kb][h] = (((t % 3) * a.pstr + r0) << 3) | (r1 < r0 ? 4 : 0) | (t / 3);
+        }
 
-    Gather<KB, MG> g;
-    g.load(a, 0, l, coff);
-    g.store(xs, nb);
+    for (int i = tid; i < a.R * a.rstr; i += CT) xs[i] = 0;  // zero halo pixels stay zero
+    __syncthreads();
+    const int R = a.R, nrow0 = a.pool ? 4 : 3;
+    for (int k = 0; k < nrow0; k++) {
+        const int yy = a.y0 - 1 + k;
+        load_row(a, xs + ((yy + R) % R) * a.rstr, yy, l, coff);
+    }
     __syncthreads();
 
-    // window sums of the products (y R^-1)(y' R^-1), exact 128-bit (hi kept < 2q)
-    u128 acc[3][2];
+    u128 acc[3][2];  // window sums of (y R^-1)(y' R^-1), exact 128-bit (hi kept < 2q)
 #pragma unroll
     for (int k = 0; k < 3; k++) acc[k][0] = acc[k][1] = u128{0, 0};
-    for (int s = 0; s < a.steps; s++) {
-        if (s + 1 < a.steps) g.load(a, s + 1, l, coff);
-        if (__ldg(a.sched + s * PS + ps) >= 0) {
-            const uint32_t *X = xs + (s & 1) * BUF + ps * 8 * PLANE + tig * RS + gid;
-            int64_t P[3][4];  // partial sums at 2^0, 2^32, 2^64 for the 4 fragment values
+    int cnt = 0;  // products accumulated since the last fold
+    const int rows_per_blk = a.pool ? 2 : 1;
+    for (int yb = a.y0; yb < a.y1; yb += rows_per_blk) {
+        // ring-row bases of the input rows yb - 1 .. yb + 2
+        int sb[4];
 #pragma unroll
-            for (int h = 0; h < 3; h++) P[h][0] = P[h][1] = P[h][2] = P[h][3] = 0;
+        for (int k = 0; k < 4; k++) sb[k] = ((yb - 1 + k + R) % R) * a.rstr;
+        // A-word offsets at x = 0 for the block's two rows (dyb = 0, 1)
+        int bo[2][KB][2];
 #pragma unroll
-            for (int d = 0; d < 8; d++) {
-                if (d < nb) {
-                    int C[E][4];
+        for (int dyb = 0; dyb < 2; dyb++)
 #pragma unroll
-                    for (int e = 0; e < E; e++) C[e][0] = C[e][1] = C[e][2] = C[e][3] = 0;
+            for (int kb = 0; kb < KB; kb++)
 #pragma unroll
-                    for (int kb = 0; kb < KB; kb++) {
-                        const uint32_t *Pd = X + d * PLANE + kb * 8 * RS;
-                        const uint32_t a0 = Pd[0], a1 = Pd[8], a2 = Pd[4 * RS], a3 = Pd[4 * RS + 8];
+                for (int h = 0; h < 2; h++) {
+                    const int v = wd[kb][h], r = (v & 3) + dyb;
+                    bo[dyb][kb][h] = (r == 0 ? sb[0] : r == 1 ? sb[1] : r == 2 ? sb[2] : sb[3]) + (v >> 3);
+                }
+        int o0[KB][2], o1[KB][2];
+        // per-pixel work list: pool -> windows wx = ps, ps+PS, ... (4 pixels each); GAP -> x = ps, ps+PS, ...
+        const int nitems = a.pool ? (a.W / 2) : a.W, npx = a.pool ? 4 : 1;
+        for (int it = ps; it < nitems; it += PS) {
 #pragma unroll
-                        for (int e = 0; e < E; e++) mma_u8s8(C[e], a0, a1, a2, a3, bw[kb][e]);
+            for (int k = 0; k < 4; k++) {
+                if (k >= npx) break;
+                const int xo = (npx == 4 ? 2 * it + (k & 1) : it) * a.pstr;
+#pragma unroll
+                for (int kb = 0; kb < KB; kb++)
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        o0[kb][h] = bo[k >> 1][kb][h] + xo;
+                        o1[kb][h] = o0[kb][h] + ((wd[kb][h] & 4) ? -8 : 8);
                     }
+                int64_t P[3][4];  // partial sums at 2^0, 2^32, 2^64 for the 4 fragment values
 #pragma unroll
-                    for (int e = 0; e < E; e++) {
-                        const int sh = d + e;
+                for (int hh = 0; hh < 3; hh++) P[hh][0] = P[hh][1] = P[hh][2] = P[hh][3] = 0;
+                int W[E][4];
 #pragma unroll
-                        for (int q = 0; q < 4; q++) madw(P[sh >> 2][q], C[e][q], 1 << (8 * (sh & 3)));
-                    }
+                for (int j = 0; j < E; j++) W[j][0] = W[j][1] = W[j][2] = W[j][3] = 0;
+                digit_plane<0, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
+                digit_plane<1, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
+                digit_plane<2, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
+                digit_plane<3, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
+                digit_plane<4, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
+                digit_plane<5, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
+                digit_plane<6, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
+                digit_plane<7, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
+                // fragment values: q=0,1 -> component 0, channels m0, m0+1; q=2,3 -> component 1
+                uint64_t yv[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const uint64_t lo = (uint64_t)P[0][q] + ((uint64_t)P[1][q] << 32);
+                    const uint64_t cy = lo < (uint64_t)P[0][q] ? 1 : 0;
+                    const int64_t hi = (P[0][q] >> 63) + (P[1][q] >> 32) + (int64_t)cy + P[2][q];
+                    const uint64_t hic = hi < 0 ? (uint64_t)(hi + (int64_t)c.q) : (uint64_t)hi;  // |hi| < q
+                    yv[q] = redc(hic, lo, c.q, c.qinv);  // conv * R^-1
+                }
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const uint64_t y0 = add_mod(yv[h], bias[h], c.q), y1 = yv[2 + h];
+                    mac128(acc[0][h], y0, y0);
+                    mac128(acc[1][h], y0, y1);
+                    mac128(acc[2][h], y1, y1);
+                }
+                if (++cnt == 8) {  // each product adds < q/16 to hi: fold every 8 products
+                    cnt = 0;
+#pragma unroll
+                    for (int kk = 0; kk < 3; kk++)
+#pragma unroll
+                        for (int h = 0; h < 2; h++)
+                            if (acc[kk][h].hi >= c.q) acc[kk][h].hi -= c.q;
                 }
             }
-            // fragment values: q=0,1 -> component 0, channels m0, m0+1; q=2,3 -> component 1
-            uint64_t yv[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const uint64_t lo = (uint64_t)P[0][q] + ((uint64_t)P[1][q] << 32);
-                const uint64_t cy = lo < (uint64_t)P[0][q] ? 1 : 0;
-                const int64_t hi = (P[0][q] >> 63) + (P[1][q] >> 32) + (int64_t)cy + P[2][q];
-                const uint64_t hic = hi < 0 ? (uint64_t)(hi + (int64_t)c.q) : (uint64_t)hi;  // |hi| < q
-                yv[q] = redc(hic, lo, c.q, c.qinv);  // conv * R^-1
-            }
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const uint64_t y0 = add_mod(yv[h], bias[h], c.q), y1 = yv[2 + h];
-                mac128(acc[0][h], y0, y0);
-                mac128(acc[1][h], y0, y1);
-                mac128(acc[2][h], y1, y1);
-            }
-            if ((s & 7) == 7) {  // each product adds < q/16 to hi: fold every 8 pixels
-#pragma unroll
-                for (int k = 0; k < 3; k++)
-#pragma unroll
-                    for (int h = 0; h < 2; h++)
-                        if (acc[k][h].hi >= c.q) acc[k][h].hi -= c.q;
-            }
-            if (a.pool && (s & 3) == 3) {  // window complete
+            if (a.pool) {  // window complete
                 const uint64_t r4 = a.r4[l], cst = a.cst ? a.cst[l] : 0;
-                const int win = (s >> 2) * PS + ps;
+                const int win = ((yb - a.y0) >> 1) * (a.W >> 1) + it;
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
                     const int m = m0 + h;
@@ -238,10 +297,19 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
 #pragma unroll
                     for (int k = 0; k < 3; k++) acc[k][h] = u128{0, 0};
                 }
+                cnt = 0;
             }
         }
-        if (s + 1 < a.steps) g.store(xs + ((s + 1) & 1) * BUF, nb);
-        __syncthreads();
+        // slide the ring: the rows of this block's top are no longer needed
+        const int ynext = yb + rows_per_blk;
+        if (ynext < a.y1) {
+            __syncthreads();
+            for (int k = 0; k < rows_per_blk; k++) {
+                const int yy = ynext + 1 + k;  // pool: rows ynext+1, ynext+2; GAP: row ynext+1
+                load_row(a, xs + ((yy + R) % R) * a.rstr, yy, l, coff);
+            }
+            __syncthreads();
+        }
     }
     if (!a.pool) {  // global sum: reduce, combine the pixel streams, then store
         uint64_t r[3][2];
@@ -254,6 +322,7 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
             }
         uint64_t *red = (uint64_t *)xs;
         if (PS > 1) {
+            __syncthreads();
 #pragma unroll
             for (int k = 0; k < 3; k++)
 #pragma unroll
@@ -286,21 +355,26 @@ __global__ void __launch_bounds__(CT) k_conv_sqsum(const SqArgs a) {
     }
 }
 
-template <int KB, int E, int MG>
+template <int KB, int E, int MG, int NB>
 int launch_sq(dim3 grid, size_t smem, cudaStream_t s, const SqArgs &a) {
     if (smem > 48 * 1024)
-        HE_CHECK_CUDA(cudaFuncSetAttribute(k_conv_sqsum<KB, E, MG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        HE_CHECK_CUDA(cudaFuncSetAttribute(k_conv_sqsum<KB, E, MG, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
-    k_conv_sqsum<KB, E, MG><<<grid, CT, smem, s>>>(a);
+    k_conv_sqsum<KB, E, MG, NB><<<grid, CT, smem, s>>>(a);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
 
+template <int KB, int E, int MG>
+int dispatch_nb(dim3 grid, size_t smem, cudaStream_t s, const SqArgs &a) {
+    return a.nb == 5 ? launch_sq<KB, E, MG, 5>(grid, smem, s, a) : launch_sq<KB, E, MG, 8>(grid, smem, s, a);
+}
+
 template <int KB, int E>
 int dispatch_mg(int MG, dim3 grid, size_t smem, cudaStream_t s, const SqArgs &a) {
-    if (MG == 1) return launch_sq<KB, E, 1>(grid, smem, s, a);
-    if (MG == 2) return launch_sq<KB, E, 2>(grid, smem, s, a);
-    return launch_sq<KB, E, 4>(grid, smem, s, a);
+    if (MG == 1) return dispatch_nb<KB, E, 1>(grid, smem, s, a);
+    if (MG == 2) return dispatch_nb<KB, E, 2>(grid, smem, s, a);
+    return dispatch_nb<KB, E, 4>(grid, smem, s, a);
 }
 
 template <int KB>
@@ -312,7 +386,6 @@ int dispatch_e(int E, int MG, dim3 grid, size_t smem, cudaStream_t s, const SqAr
 
 int dispatch_sq(int KB, int E, int MG, dim3 grid, size_t smem, cudaStream_t s, const SqArgs &a) {
     switch (KB) {
-        case 1: return dispatch_e<1>(E, MG, grid, smem, s, a);
         case 2: return dispatch_e<2>(E, MG, grid, smem, s, a);
         case 3: return dispatch_e<3>(E, MG, grid, smem, s, a);
         case 4: return dispatch_e<4>(E, MG, grid, smem, s, a);
@@ -331,6 +404,11 @@ inline int digit_s8(int64_t w, int e) {
     return (int8_t)(uint8_t)(w & 0xFF);
 }
 
+int round_up_mod(int v, int mod, int rem) {  // smallest v' >= v with v' = rem (mod mod)
+    while (((v % mod) + mod) % mod != rem) v++;
+    return v;
+}
+
 }  // namespace
 
 // Fused 3x3/pad-1 conv (p -> M channels over an H x W map, conv output rows
@@ -341,7 +419,7 @@ inline int digit_s8(int64_t w, int e) {
 // component 0), then + cst on component 0.  Inputs in[i*H*W + y*W + x] are 2
 // components x ell limbs; outputs 3 components x ell limbs.  Tap order
 // k = i*9 + (dy+1)*3 + (dx+1).  Returns HE_EINVAL when a tensor-core bound
-// does not hold (9p > 160, M > 32, |w| >= 2^23 or a prime below 2^36).
+// does not hold (p > 16, M > 32, |w| >= 2^23 or a prime below 2^36).
 extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, int H, int W, uint64_t *const *out,
                                   int M, int pool, int y0, int y1, const int64_t *weights, const uint64_t *bias,
                                   const uint64_t *cst, int ell, void *stream) {
@@ -354,9 +432,9 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
         he_set_error("he_conv_square_sum: 2x2 pooling needs even H, W and row range");
         return HE_EINVAL;
     }
-    const int T = 9 * p, KB = (T + 31) / 32, MG = (M + 7) / 8;
-    if (KB > 5 || M > 32 || c->N % 8 || c->N < 8) {
-        he_set_error("he_conv_square_sum: 9p=%d taps / M=%d channels beyond the fused kernel", T, M);
+    const int T = 9 * p, ncg = (p + 3) / 4, KB = std::max(2, (9 * ncg + 7) / 8), MG = (M + 7) / 8;
+    if (p > 16 || M > 32 || c->N % 8 || c->N < 8) {
+        he_set_error("he_conv_square_sum: p=%d input / M=%d output channels beyond the fused kernel", p, M);
         return HE_EINVAL;
     }
     for (int l = 0; l < ell; l++)
@@ -377,7 +455,8 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
         return HE_EINVAL;
     }
     const int MGk = MG == 3 ? 4 : MG;  // kernels exist for 1, 2, 4 channel groups
-    // B fragments [MGk][KB][E][lane][2]: b.x = taps kb*32 + tig*4 + 0..3, b.y = +16; column gid -> channel
+    // B fragments [MGk][KB][E][lane][2]: b.x = K word kb*8 + tig, b.y = word kb*8 + 4 + tig;
+    // word w = (tap t = w / ncg, channel group g = w % ncg), byte u -> channel 4g + u; column gid -> channel m
     std::vector<uint32_t> bf((size_t)MGk * KB * E * 32 * 2, 0);
     for (int cg = 0; cg < MGk; cg++)
         for (int kb = 0; kb < KB; kb++)
@@ -385,11 +464,12 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
                 for (int lane = 0; lane < 32; lane++) {
                     const int gid = lane >> 2, tig = lane & 3, m = cg * 8 + gid;
                     for (int r = 0; r < 2; r++) {
+                        const int w = kb * 8 + r * 4 + tig, t = w / ncg, g = w % ncg;
                         uint32_t reg = 0;
-                        for (int i = 0; i < 4; i++) {
-                            const int k = kb * 32 + r * 16 + tig * 4 + i;
-                            const int dg = (m < M && k < T) ? digit_s8(weights[(size_t)m * T + k], e) : 0;
-                            reg |= (uint32_t)(uint8_t)(int8_t)dg << (8 * i);
+                        for (int u = 0; u < 4; u++) {
+                            const int i = 4 * g + u;
+                            const int dg = (m < M && t < 9 && i < p) ? digit_s8(weights[(size_t)m * T + i * 9 + t], e) : 0;
+                            reg |= (uint32_t)(uint8_t)(int8_t)dg << (8 * u);
                         }
                         bf[((((size_t)cg * KB + kb) * E + e) * 32 + lane) * 2 + r] = reg;
                     }
@@ -397,15 +477,15 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
     // per-limb constants: R^4, bias * R^-1
     std::vector<uint64_t> r4(ell), bres(bias ? (size_t)M * ell : 0);
     for (int l = 0; l < ell; l++) {
-        const uint64_t q = c->mod[l], R = (uint64_t)(((unsigned __int128)1 << 64) % q);
-        const uint64_t R2 = he_h_mulmod(R, R, q);
+        const uint64_t q = c->mod[l], Rm = (uint64_t)(((unsigned __int128)1 << 64) % q);
+        const uint64_t R2 = he_h_mulmod(Rm, Rm, q);
         r4[l] = he_h_mulmod(R2, R2, q);
         if (cst && cst[l] >= q) {
             he_set_error("he_conv_square_sum: residue not canonical");
             return HE_EINVAL;
         }
         if (bias) {
-            const uint64_t Rinv = he_h_inv(R, q);
+            const uint64_t Rinv = he_h_inv(Rm, q);
             for (int m = 0; m < M; m++) {
                 if (bias[(size_t)m * ell + l] >= q) {
                     he_set_error("he_conv_square_sum: residue not canonical");
@@ -415,35 +495,30 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
             }
         }
     }
-    cudaStream_t s = (cudaStream_t)stream;
-    const int nwin = pool ? ((y1 - y0) / 2) * (W / 2) : 1;
-    const int n_out = pool ? M * nwin : M, npix = (y1 - y0) * W, Tpad = KB * 32, PS = 4 / MGk;
-    const int steps = pool ? ((nwin + PS - 1) / PS) * 4 : (npix + PS - 1) / PS;
-    // tap address table [launch pixel][tap slot] and the (step, stream) -> pixel schedule
-    std::vector<uint64_t> ptab((size_t)npix * Tpad, 0);
-    for (int y = y0; y < y1; y++)
-        for (int x = 0; x < W; x++)
-            for (int k = 0; k < T; k++) {
-                const int i = k / 9, t = k % 9, yy = y + t / 3 - 1, xx = x + t % 3 - 1;
-                if (yy >= 0 && yy < H && xx >= 0 && xx < W)
-                    ptab[((size_t)(y - y0) * W + x) * Tpad + k] = (uint64_t)in[(size_t)i * H * W + yy * W + xx];
-            }
-    std::vector<int32_t> sched((size_t)steps * PS, -1);
-    for (int st = 0; st < steps; st++)
-        for (int q = 0; q < PS; q++) {
-            if (pool) {
-                const int w = (st >> 2) * PS + q, k = st & 3, Wo = W / 2;
-                if (w < nwin) sched[(size_t)st * PS + q] = (2 * (w / Wo) + (k >> 1)) * W + 2 * (w % Wo) + (k & 1);
-            } else if (st * PS + q < npix) {
-                sched[(size_t)st * PS + q] = st * PS + q;
+    // limbs grouped by byte length (one launch, one ring layout per group)
+    std::vector<int32_t> lorder;
+    std::vector<std::pair<int, int>> groups;  // (nb, count)
+    for (int nb = 5; nb <= 8; nb += 3) {  // 40-bit primes: 5 byte planes; anything longer: all 8
+        int n = 0;
+        for (int l = 0; l < ell; l++) {
+            const int b = c->mod[l] < (1ull << 40) ? 5 : 8;
+            if (b == nb) {
+                lorder.push_back(l);
+                n++;
             }
         }
-    void **dout = nullptr;
+        if (n) groups.push_back({nb, n});
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int nwin = pool ? ((y1 - y0) / 2) * (W / 2) : 1;
+    const int n_in = p * H * W, n_out = pool ? M * nwin : M;
+    void **din = nullptr, **dout = nullptr;
+    HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
     HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
-    const size_t b_bf = bf.size() * 4, b_pt = ptab.size() * 8, b_sc = sched.size() * 4, b_r4 = (size_t)ell * 8,
-                 b_b = bres.size() * 8, b_c = cst ? (size_t)ell * 8 : 0;
+    const size_t b_bf = bf.size() * 4, b_lo = lorder.size() * 4, b_r4 = (size_t)ell * 8, b_b = bres.size() * 8,
+                 b_c = cst ? (size_t)ell * 8 : 0;
     char *meta = nullptr;
-    HE_TRY(he_scratch_alloc((void **)&meta, b_bf + b_pt + b_sc + b_r4 + b_b + b_c + 128, s));
+    HE_TRY(he_scratch_alloc((void **)&meta, b_bf + b_lo + b_r4 + b_b + b_c + 128, s));
     size_t off = 0;
     auto carve = [&](size_t bytes) {
         char *p = meta + off;
@@ -451,36 +526,64 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
         return p;
     };
     uint32_t *dbf = (uint32_t *)carve(b_bf);
-    uint64_t *dpt = (uint64_t *)carve(b_pt);
-    int32_t *dsc = (int32_t *)carve(b_sc);
+    int32_t *dlo = (int32_t *)carve(b_lo);
     uint64_t *dr4 = (uint64_t *)carve(b_r4);
     uint64_t *db = bias ? (uint64_t *)carve(b_b) : nullptr;
     uint64_t *dc = cst ? (uint64_t *)carve(b_c) : nullptr;
     HE_CHECK_CUDA(cudaMemcpyAsync(dbf, bf.data(), b_bf, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dpt, ptab.data(), b_pt, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dsc, sched.data(), b_sc, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(cudaMemcpyAsync(dlo, lorder.data(), b_lo, cudaMemcpyHostToDevice, s));
     HE_CHECK_CUDA(cudaMemcpyAsync(dr4, r4.data(), b_r4, cudaMemcpyHostToDevice, s));
     if (db) HE_CHECK_CUDA(cudaMemcpyAsync(db, bres.data(), b_b, cudaMemcpyHostToDevice, s));
     if (dc) HE_CHECK_CUDA(cudaMemcpyAsync(dc, cst, b_c, cudaMemcpyHostToDevice, s));
     SqArgs a;
-    a.ptab = dpt;
-    a.sched = dsc;
+    a.in = (const uint64_t *const *)din;
     a.out = (uint64_t *const *)dout;
     a.bfrag = dbf;
     a.bias = db;
     a.cst = dc;
     a.r4 = dr4;
     a.mc = c->d_mc;
+    a.p = p;
+    a.H = H;
+    a.W = W;
     a.M = M;
     a.ell = ell;
     a.logN = c->logN;
     a.pool = pool;
+    a.y0 = y0;
+    a.y1 = y1;
     a.nwin = nwin;
-    a.steps = steps;
-    const size_t smem = (size_t)2 * PS * 8 * (KB * 8 * RS) * 4;
-    dim3 grid((unsigned)(c->N / 8), (unsigned)ell);
-    int rc = dispatch_sq(KB, E, MGk, grid, smem, s, a);
+    a.ncg = ncg;
+    for (int k = 0; k < 4; k++) a.mul[k] = 1 << (8 * k);
+    int rc = HE_OK, first = 0;
+    for (auto &g : groups) {
+        a.nb = g.first;
+        a.limbs = dlo + first;
+        // bank-conflict-free A loads: with 4 channel groups per tap the 4 groups
+        // fill the 32 banks by themselves; otherwise consecutive taps must sit
+        // 8 banks apart (pixel stride = 24, ring-row stride = 8 mod 32, 4 rows)
+        if (ncg % 4 == 0) {
+            a.pstr = a.nb * ncg * 16;
+            a.rstr = (W + 2) * a.pstr;
+            a.R = pool ? 4 : 3;
+        } else {
+            a.pstr = round_up_mod(a.nb * ncg * 16, 32, 24);
+            a.rstr = round_up_mod((W + 2) * a.pstr, 32, 8);
+            a.R = 4;
+        }
+        const size_t smem = (size_t)a.R * a.rstr * 4;
+        if (smem > 227 * 1024) {
+            he_set_error("he_conv_square_sum: row ring needs %zu bytes of shared memory (W=%d too wide)", smem, W);
+            rc = HE_EINVAL;
+            break;
+        }
+        dim3 grid((unsigned)(c->N / 8), (unsigned)g.second);
+        rc = dispatch_sq(KB, E, MGk, grid, smem, s, a);
+        if (rc != HE_OK) break;
+        first += g.second;
+    }
     he_scratch_free(meta, s);
+    he_scratch_free(din, s);
     he_scratch_free(dout, s);
     return rc;
 }
