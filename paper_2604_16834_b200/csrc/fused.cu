@@ -28,6 +28,9 @@ namespace {
 
 constexpr int LOGN = 16;
 constexpr size_t NN = (size_t)1 << LOGN;
+// primes below these bounds take the no-correction butterflies (ntt_core.cuh):
+// forward passes end below 33q, inverse passes below 2^17 q -- both < 2^64
+constexpr uint64_t NC_FWD = 1ull << 58, NC_INV = 1ull << 46;
 
 struct Job {
     const uint64_t *src;  // pass-1 input: direct poly / first BConv source limb / centred source
@@ -94,15 +97,22 @@ __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs,
             x[j] = v > half ? sub_mod(0, reduce64(jb.ql - v, c), c.q) : reduce64(v, c);
         }
     }
-    phase_ct<16, 0>(x, col + 256 * g, W2, c.q);
+    const bool nc = c.q < NC_FWD;  // no per-butterfly correction: output < 17q, else < 4q
+    if (nc)
+        phase_ct<16, 0, true>(x, col + 256 * g, W2, c.q);
+    else
+        phase_ct<16, 0>(x, col + 256 * g, W2, c.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) sm[(g + 16 * j) * 16 + lc] = x[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = sm[(16 * g + j) * 16 + lc];
-    phase_ct<16, 4>(x, col + 4096 * g, W2, c.q);
+    if (nc)
+        phase_ct<16, 4, true>(x, col + 4096 * g, W2, c.q);
+    else
+        phase_ct<16, 4>(x, col + 4096 * g, W2, c.q);
 #pragma unroll
-    for (int j = 0; j < 16; j++) jb.dst[(16 * g + j) * 256 + col] = x[j];  // lazy [0, 4q)
+    for (int j = 0; j < 16; j++) jb.dst[(16 * g + j) * 256 + col] = x[j];  // lazy
 }
 
 // ---------------------------------------------------------------- forward pass 2 (rows)
@@ -119,17 +129,27 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
-    phase_ct<16, 8>(x, r * 256 + g, W2, c.q);
+    const bool nc = c.q < NC_FWD;
+    if (nc)
+        phase_ct<16, 8, true>(x, r * 256 + g, W2, c.q);
+    else
+        phase_ct<16, 8>(x, r * 256 + g, W2, c.q);
     uint64_t *s = sm + rl * 272;
 #pragma unroll
     for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = x[j];
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
-    phase_ct<16, 12>(x, r * 256 + 16 * g, W2, c.q);
     __syncwarp();
+    if (nc) {
+        phase_ct<16, 12, true>(x, r * 256 + 16 * g, W2, c.q);
 #pragma unroll
-    for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], c.q);
+        for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce64(x[j], c);  // < 33q
+    } else {
+        phase_ct<16, 12>(x, r * 256 + 16 * g, W2, c.q);
+#pragma unroll
+        for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], c.q);
+    }
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 16; j++) {
@@ -172,17 +192,104 @@ __global__ void __launch_bounds__(NTT_TPB) ki_rows(const Job *__restrict__ jobs,
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
-    phase_gs<16, 0>(x, r * 256 + 16 * g, W2, c.q);
+    const bool nc = c.q < NC_INV;  // no sum correction: inputs < 2q, output < 2^9 q
+    if (nc)
+        phase_gs<16, 0, 1>(x, r * 256 + 16 * g, W2, c.q);
+    else
+        phase_gs<16, 0>(x, r * 256 + 16 * g, W2, c.q);
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = x[j];
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
-    phase_gs<16, 4>(x, r * 256 + g, W2, c.q);
+    if (nc)
+        phase_gs<16, 4, 5>(x, r * 256 + g, W2, c.q);
+    else
+        phase_gs<16, 4>(x, r * 256 + g, W2, c.q);
     uint64_t *out = jb.dst + r * 256;
 #pragma unroll
     for (int j = 0; j < 16; j++) out[g + 16 * j] = x[j];
+}
+
+// ---------------------------------------------------------------- async-pipelined passes
+// Persistent form of the row passes: each CTA walks tiles (job, 16-row tile)
+// with stride gridDim.x and keeps KS tiles in flight with cp.async (8-byte
+// copies straight into the padded shared layout, no register staging), so a
+// CTA computes one tile while the next ones stream in.
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+constexpr int KS = 3;            // tiles in flight per CTA
+constexpr int TILE_W = 16 * 272;  // padded words per 16-row tile
+
+__device__ __forceinline__ void ki_rows_issue(const Job *jobs, int ntiles, int tile, uint64_t *st) {
+    if (tile < ntiles) {
+        const Job &jb = jobs[tile >> 4];
+        const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+        const uint64_t *in = jb.src + ((tile & 15) * 16 + rl) * 256;
+        uint64_t *s = st + rl * 272;
+#pragma unroll
+        for (int j = 0; j < 16; j++) cp_async8(s + pad16(g + 16 * j), in + g + 16 * j);
+    }
+    cp_async_commit();  // (empty groups keep the wait counts uniform)
+}
+
+__global__ void __launch_bounds__(NTT_TPB, 2) ki_rows_p(const Job *__restrict__ jobs, int ntiles, const uint64_t *tw,
+                                                       const ModConst *mc) {
+    extern __shared__ uint64_t ring[];  // [KS][TILE_W]
+    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+#pragma unroll
+    for (int k = 0; k < KS - 1; k++) ki_rows_issue(jobs, ntiles, blockIdx.x + k * gridDim.x, ring + k * TILE_W);
+    for (int i = 0;; i++) {
+        const int tile = blockIdx.x + i * gridDim.x;
+        if (tile >= ntiles) break;
+        ki_rows_issue(jobs, ntiles, tile + (KS - 1) * gridDim.x, ring + ((i + KS - 1) % KS) * TILE_W);
+        cp_async_wait<KS - 1>();
+        __syncthreads();
+        const Job jb = jobs[tile >> 4];
+        const ModConst c = mc[jb.mod];
+        const ulonglong2 *W2 = tw_inv(tw, jb.mod, LOGN);
+        const uint32_t r = (tile & 15) * 16 + rl;
+        uint64_t *s = ring + (i % KS) * TILE_W + rl * 272;
+        uint64_t x[16];
+        if (jb.src2) {  // joint ModDown: X = acc + (P mod q) * d on the dropped Q limbs
+            const uint64_t *in2 = jb.src2 + r * 256;
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                s[pad16(g + 16 * j)] = add_mod(s[pad16(g + 16 * j)], shoup(in2[g + 16 * j], jb.c2, jb.c2p, c.q), c.q);
+            __syncwarp();
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
+        const bool nc = c.q < NC_INV;
+        if (nc)
+            phase_gs<16, 0, 1>(x, r * 256 + 16 * g, W2, c.q);
+        else
+            phase_gs<16, 0>(x, r * 256 + 16 * g, W2, c.q);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = x[j];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
+        if (nc)
+            phase_gs<16, 4, 5>(x, r * 256 + g, W2, c.q);
+        else
+            phase_gs<16, 4>(x, r * 256 + g, W2, c.q);
+        uint64_t *out = jb.dst + r * 256;
+#pragma unroll
+        for (int j = 0; j < 16; j++) out[g + 16 * j] = x[j];
+        __syncthreads();  // the stage is refilled by the next iteration's issue
+    }
+    cp_async_wait<0>();
 }
 
 // pass 2 (columns): in place on dst, GS stages 8..15, times (cw, cwp) = N^-1 * extra
@@ -197,13 +304,20 @@ __global__ void __launch_bounds__(NTT_TPB) ki_cols(const Job *__restrict__ jobs,
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = jb.dst[(16 * g + j) * 256 + col];
-    phase_gs<16, 8>(x, col + 4096 * g, W2, c.q);
+    const bool nc = c.q < NC_INV;  // inputs < 2^9 q (ki_rows), output < 2^17 q, then Shoup -> canonical
+    if (nc)
+        phase_gs<16, 8, 9>(x, col + 4096 * g, W2, c.q);
+    else
+        phase_gs<16, 8>(x, col + 4096 * g, W2, c.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) sm[(16 * g + j) * 16 + lc] = x[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = sm[(g + 16 * j) * 16 + lc];
-    phase_gs<16, 12>(x, col + 256 * g, W2, c.q);
+    if (nc)
+        phase_gs<16, 12, 13>(x, col + 256 * g, W2, c.q);
+    else
+        phase_gs<16, 12>(x, col + 256 * g, W2, c.q);
 #pragma unroll
     for (int j = 0; j < 16; j++) jb.dst[(g + 16 * j) * 256 + col] = shoup(x[j], jb.cw, jb.cwp, c.q);
 }
@@ -219,10 +333,7 @@ struct IpArgs {
     int ell, ext_n, beta, alpha, L, M, B;
 };
 
-#ifndef HE_IP_MINB
-#define HE_IP_MINB 2
-#endif
-__global__ void __launch_bounds__(NTT_TPB, HE_IP_MINB) k_modup_ip(const IpArgs a) {
+__global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
     __shared__ uint64_t sm[16 * 272];
     // ciphertext-fastest order: CTAs resident together read the same key rows
     // (dnum x 2 x 16 rows of limb t), so the key streams from L2, not HBM
@@ -250,16 +361,26 @@ __global__ void __launch_bounds__(NTT_TPB, HE_IP_MINB) k_modup_ip(const IpArgs a
             const uint64_t *row = a.ext + ((((size_t)b * a.beta + dj) * a.ext_n + t) << LOGN) + r * 256;
 #pragma unroll
             for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
-            phase_ct<16, 8>(x, r * 256 + g, W2, c.q);
+            const bool nc = c.q < NC_FWD;
+            if (nc)
+                phase_ct<16, 8, true>(x, r * 256 + g, W2, c.q);
+            else
+                phase_ct<16, 8>(x, r * 256 + g, W2, c.q);
 #pragma unroll
             for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = x[j];
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
-            phase_ct<16, 12>(x, r * 256 + 16 * g, W2, c.q);
             __syncwarp();
+            if (nc) {
+                phase_ct<16, 12, true>(x, r * 256 + 16 * g, W2, c.q);
 #pragma unroll
-            for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], c.q);
+                for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce64(x[j], c);
+            } else {
+                phase_ct<16, 12>(x, r * 256 + 16 * g, W2, c.q);
+#pragma unroll
+                for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], c.q);
+            }
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
@@ -314,7 +435,14 @@ int run_inverse(he_ctx *c, const std::vector<Job> &jobs, cudaStream_t s) {
     JobBuf jb(s);
     HE_TRY(jb.up(jobs));
     unsigned g = (unsigned)jobs.size() * 16;
-    ki_rows<<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+    static int sms = 0;
+    if (!sms) {
+        HE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+        HE_CHECK_CUDA(cudaFuncSetAttribute(ki_rows_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(KS * TILE_W * sizeof(uint64_t))));
+    }
+    const unsigned gp = std::min<unsigned>(g, 2u * (unsigned)sms);
+    ki_rows_p<<<gp, NTT_TPB, KS * TILE_W * sizeof(uint64_t), s>>>(jb.d, (int)g, c->d_tw, c->d_mc);
     HE_CHECK_LAUNCH();
     ki_cols<<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
     HE_CHECK_LAUNCH();
