@@ -137,7 +137,10 @@ class Oracle:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().oc_destroy(h)
+            try:
+                lib().oc_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     # -- transforms

@@ -75,6 +75,21 @@ alg_bytes = {
     "rotate_1024": B * (2 * poly + 2 * poly) + 2 * beta * (L + K) * N * 8,
     "rescale": B * (2 * poly + 2 * (L - 1) * N * 8),
 }
+digits = [min(eng.context.alpha, L - j * eng.context.alpha) for j in range(beta)]
+bfly = (N // 2) * 16
+
+
+def ks_modmuls(ell):  # NTT butterflies + BConv + inner-product MACs of one key switch
+    ext = ell + K
+    n_ntt = ell + sum(ext - a for a in digits) + 2 * K + 2 * ell
+    return n_ntt * bfly + (sum(a * (ext - a) for a in digits) + 2 * K * ell + 2 * beta * ext) * N
+
+
+modmuls = {
+    "ntt_fwd": 2 * B * L * bfly, "ntt_inv": 2 * B * L * bfly,
+    "keyswitch_relin": B * ks_modmuls(L), "rotate_1": B * ks_modmuls(L), "rotate_1024": B * ks_modmuls(L),
+    "rescale": B * 2 * (1 + (L - 1)) * bfly,
+}
 peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
 res = {}
@@ -97,6 +112,10 @@ for name, fn in ops.items():
 ip = np.zeros(2)
 _lib.check(Lb.he_microbench_intpipe(eng.context.device, A(ip)))
 res["intpipe"] = {"imad32_per_s": ip[0], "mac128_per_s": ip[1]}
+for name in ops:  # integer roofline: algorithmic modular multiplications vs the measured 64x64->128 MAC rate
+    rate = modmuls[name] / (res[name]["ms"] * 1e-3)
+    res[name]["Gmodmul_per_s"] = round(rate / 1e9, 1)
+    res[name]["int_frac"] = round(rate / ip[1], 3)
 
 if not args.no_oracle:   # bit-exact spot check of ct 0 for every op
     import oracle as O
