@@ -28,7 +28,7 @@ struct ModConst {
     uint64_t ninv;      // N^-1 mod q
     uint64_t ninv_sh;   // Shoup(ninv)
     uint64_t ratio;     // floor((2^64 - 1) / q): reduce64
-    uint64_t pad[2];
+    double qd, qid;     // q and 1/q as doubles (FP64 butterflies for q < 2^42)
 };
 
 // x mod q for any 64-bit x (one high product + one conditional subtract)
@@ -53,6 +53,7 @@ struct he_ctx {
     std::vector<uint64_t> mod, psi;
     ModConst *d_mc = nullptr;        // [L+K]
     uint64_t *d_tw = nullptr;        // [L+K][fwd|inv][N][2]  (psi^brv(i), Shoup) pairs
+    double *d_twd = nullptr;         // [L+K][fwd|inv][N]     psi^brv(i) as doubles (FP64 butterflies)
     uint64_t *d_sk = nullptr;        // [L+K][N]     canonical, NTT domain
     double *d_fftw = nullptr;        // [nslots][2]  omega^k
     double *d_twist = nullptr;       // [nslots][2]  zeta^j
@@ -67,6 +68,11 @@ struct he_ctx {
     std::vector<uint64_t> h_qlinv;                  // host copy of d_qlinv
     std::vector<uint64_t> h_ninv;                   // N^-1 mod every modulus
     std::mutex mu;
+    // side streams: independent chunks of a batched key switch run concurrently
+    // (fork/join with events on the caller's stream)
+    static constexpr int NSIDE = 2;
+    cudaStream_t side[NSIDE] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {};
 };
 
 // host-side modular helpers (context.cu)

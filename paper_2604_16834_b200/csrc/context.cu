@@ -224,9 +224,17 @@ static int build_tables(he_ctx *c) {
         c->h_ninv.push_back(k.ninv);
         k.ninv_sh = h_shoup(k.ninv, q);
         k.ratio = UINT64_MAX / q;
+        k.qd = (double)q;
+        k.qid = 1.0 / (double)q;
     }
     HE_CHECK_CUDA(cudaMalloc(&c->d_tw, tw.size() * 8));
     HE_CHECK_CUDA(cudaMemcpy(c->d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
+    {   // the same twiddles as doubles (exact: every value < q < 2^61 < 2^53 only matters for q < 2^42)
+        std::vector<double> twd((size_t)M * 2 * N);
+        for (size_t i = 0; i < twd.size(); i++) twd[i] = (double)tw[2 * i];
+        HE_CHECK_CUDA(cudaMalloc(&c->d_twd, twd.size() * 8));
+        HE_CHECK_CUDA(cudaMemcpy(c->d_twd, twd.data(), twd.size() * 8, cudaMemcpyHostToDevice));
+    }
     HE_CHECK_CUDA(cudaMalloc(&c->d_mc, sizeof(ModConst) * M));
     HE_CHECK_CUDA(cudaMemcpy(c->d_mc, mc.data(), sizeof(ModConst) * M, cudaMemcpyHostToDevice));
     // rescale constants q_l^-1 mod q_i, and P constants
@@ -304,6 +312,11 @@ extern "C" int he_ctx_create(const he_params *p, int device, he_ctx **out) {
     he_ctx *c = new he_ctx();
     c->prm = *p;
     c->device = device;
+    for (int k = 0; k < he_ctx::NSIDE; k++) {
+        HE_CHECK_CUDA(cudaStreamCreateWithFlags(&c->side[k], cudaStreamNonBlocking));
+        HE_CHECK_CUDA(cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming));
+    }
+    HE_CHECK_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     c->logN = p->log_n;
     c->N = 1 << p->log_n;
     c->L = p->n_q;
@@ -349,11 +362,17 @@ static void free_table(BconvTable &t) {
 extern "C" int he_ctx_destroy(he_ctx *c) {
     if (!c) return HE_OK;
     cudaDeviceSynchronize();
+    for (int k = 0; k < he_ctx::NSIDE; k++) {
+        cudaStreamDestroy(c->side[k]);
+        cudaEventDestroy(c->ev_join[k]);
+    }
+    cudaEventDestroy(c->ev_fork);
     for (auto &kv : c->keys) cudaFree(kv.second);
     for (auto &kv : c->modup_tab) free_table(kv.second);
     for (auto &kv : c->moddown_tab) free_table(kv.second);
     cudaFree(c->d_mc);
     cudaFree(c->d_tw);
+    cudaFree(c->d_twd);
     cudaFree(c->d_sk);
     cudaFree(c->d_fftw);
     cudaFree(c->d_twist);

@@ -54,7 +54,7 @@ enum { E_STORE = 0, E_SUBSCALE = 1 };
 // ---------------------------------------------------------------- forward pass 1 (columns)
 template <int LD>
 __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs, const uint64_t *tw,
-                                                  const ModConst *mc) {
+                                                  const double *twd, const ModConst *mc) {
     __shared__ uint64_t sm[256 * 16];
     const Job jb = jobs[blockIdx.x >> 4];
     const ModConst c = mc[jb.mod];
@@ -97,6 +97,22 @@ __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs,
             x[j] = v > half ? sub_mod(0, reduce64(jb.ql - v, c), c.q) : reduce64(v, c);
         }
     }
+    if (c.q < FP_QMAX) {  // FP64 butterflies; canonical output
+        const double *Wd = twd_fwd(twd, jb.mod, LOGN);
+        double xd[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
+        fphase_ct<16, 0>(xd, col + 256 * g, Wd, c.qd, c.qid);
+#pragma unroll
+        for (int j = 0; j < 16; j++) sm[(g + 16 * j) * 16 + lc] = (uint64_t)__double_as_longlong(xd[j]);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)sm[(16 * g + j) * 16 + lc]);
+        fphase_ct<16, 4>(xd, col + 4096 * g, Wd, c.qd, c.qid);
+#pragma unroll
+        for (int j = 0; j < 16; j++) jb.dst[(16 * g + j) * 256 + col] = fcanon(xd[j], c.qd, c.qid);
+        return;
+    }
     const bool nc = c.q < NC_FWD;  // no per-butterfly correction: output < 17q, else < 4q
     if (nc)
         phase_ct<16, 0, true>(x, col + 256 * g, W2, c.q);
@@ -118,7 +134,7 @@ __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs,
 // ---------------------------------------------------------------- forward pass 2 (rows)
 template <int EP>
 __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs, const uint64_t *tw,
-                                                  const ModConst *mc) {
+                                                  const double *twd, const ModConst *mc) {
     __shared__ uint64_t sm[16 * 272];
     const Job jb = jobs[blockIdx.x >> 4];
     const ModConst c = mc[jb.mod];
@@ -126,15 +142,31 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
     const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
     const uint32_t r = (blockIdx.x & 15) * 16 + rl;
     uint64_t *row = jb.dst + r * 256;
+    uint64_t *s = sm + rl * 272;
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
     const bool nc = c.q < NC_FWD;
+    if (c.q < FP_QMAX) {
+        const double *Wd = twd_fwd(twd, jb.mod, LOGN);
+        double xd[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
+        fphase_ct<16, 8>(xd, r * 256 + g, Wd, c.qd, c.qid);
+#pragma unroll
+        for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = (uint64_t)__double_as_longlong(xd[j]);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(16 * g + j)]);
+        __syncwarp();
+        fphase_ct<16, 12>(xd, r * 256 + 16 * g, Wd, c.qd, c.qid);
+#pragma unroll
+        for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = fcanon(xd[j], c.qd, c.qid);
+    } else {
     if (nc)
         phase_ct<16, 8, true>(x, r * 256 + g, W2, c.q);
     else
         phase_ct<16, 8>(x, r * 256 + g, W2, c.q);
-    uint64_t *s = sm + rl * 272;
 #pragma unroll
     for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = x[j];
     __syncwarp();
@@ -149,6 +181,7 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
         phase_ct<16, 12>(x, r * 256 + 16 * g, W2, c.q);
 #pragma unroll
         for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], c.q);
+    }
     }
     __syncwarp();
 #pragma unroll
@@ -169,49 +202,6 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
 }
 
 // ---------------------------------------------------------------- inverse passes
-// pass 1 (rows): reads src, writes dst (may alias), GS stages 0..7, lazy [0, 2q)
-__global__ void __launch_bounds__(NTT_TPB) ki_rows(const Job *__restrict__ jobs, const uint64_t *tw,
-                                                  const ModConst *mc) {
-    __shared__ uint64_t sm[16 * 272];
-    const Job jb = jobs[blockIdx.x >> 4];
-    const ModConst c = mc[jb.mod];
-    const ulonglong2 *W2 = tw_inv(tw, jb.mod, LOGN);
-    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
-    const uint32_t r = (blockIdx.x & 15) * 16 + rl;
-    const uint64_t *in = jb.src + r * 256;
-    uint64_t *s = sm + rl * 272;
-    uint64_t x[16];
-#pragma unroll
-    for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = in[g + 16 * j];
-    if (jb.src2) {  // joint ModDown: X = acc + (P mod q) * d on the dropped Q limbs
-        const uint64_t *in2 = jb.src2 + r * 256;
-#pragma unroll
-        for (int j = 0; j < 16; j++)
-            s[pad16(g + 16 * j)] = add_mod(s[pad16(g + 16 * j)], shoup(in2[g + 16 * j], jb.c2, jb.c2p, c.q), c.q);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
-    const bool nc = c.q < NC_INV;  // no sum correction: inputs < 2q, output < 2^9 q
-    if (nc)
-        phase_gs<16, 0, 1>(x, r * 256 + 16 * g, W2, c.q);
-    else
-        phase_gs<16, 0>(x, r * 256 + 16 * g, W2, c.q);
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = x[j];
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
-    if (nc)
-        phase_gs<16, 4, 5>(x, r * 256 + g, W2, c.q);
-    else
-        phase_gs<16, 4>(x, r * 256 + g, W2, c.q);
-    uint64_t *out = jb.dst + r * 256;
-#pragma unroll
-    for (int j = 0; j < 16; j++) out[g + 16 * j] = x[j];
-}
-
 // ---------------------------------------------------------------- async-pipelined passes
 // Persistent form of the row passes: each CTA walks tiles (job, 16-row tile)
 // with stride gridDim.x and keeps KS tiles in flight with cp.async (8-byte
@@ -243,7 +233,7 @@ __device__ __forceinline__ void ki_rows_issue(const Job *jobs, int ntiles, int t
 }
 
 __global__ void __launch_bounds__(NTT_TPB, 2) ki_rows_p(const Job *__restrict__ jobs, int ntiles, const uint64_t *tw,
-                                                       const ModConst *mc) {
+                                                       const double *twd, const ModConst *mc) {
     extern __shared__ uint64_t ring[];  // [KS][TILE_W]
     const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
 #pragma unroll
@@ -269,6 +259,22 @@ __global__ void __launch_bounds__(NTT_TPB, 2) ki_rows_p(const Job *__restrict__ 
         }
 #pragma unroll
         for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
+        if (c.q < FP_QMAX) {  // FP64 butterflies, canonical output
+            const double *Wd = twd_inv(twd, jb.mod, LOGN);
+            double xd[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
+            fphase_gs<16, 0>(xd, r * 256 + 16 * g, Wd, c.qd, c.qid);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = (uint64_t)__double_as_longlong(xd[j]);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(g + 16 * j)]);
+            fphase_gs<16, 4>(xd, r * 256 + g, Wd, c.qd, c.qid);
+#pragma unroll
+            for (int j = 0; j < 16; j++) x[j] = fcanon(xd[j], c.qd, c.qid);
+        } else {
         const bool nc = c.q < NC_INV;
         if (nc)
             phase_gs<16, 0, 1>(x, r * 256 + 16 * g, W2, c.q);
@@ -284,6 +290,7 @@ __global__ void __launch_bounds__(NTT_TPB, 2) ki_rows_p(const Job *__restrict__ 
             phase_gs<16, 4, 5>(x, r * 256 + g, W2, c.q);
         else
             phase_gs<16, 4>(x, r * 256 + g, W2, c.q);
+        }
         uint64_t *out = jb.dst + r * 256;
 #pragma unroll
         for (int j = 0; j < 16; j++) out[g + 16 * j] = x[j];
@@ -294,7 +301,7 @@ __global__ void __launch_bounds__(NTT_TPB, 2) ki_rows_p(const Job *__restrict__ 
 
 // pass 2 (columns): in place on dst, GS stages 8..15, times (cw, cwp) = N^-1 * extra
 __global__ void __launch_bounds__(NTT_TPB) ki_cols(const Job *__restrict__ jobs, const uint64_t *tw,
-                                                  const ModConst *mc) {
+                                                  const double *twd, const ModConst *mc) {
     __shared__ uint64_t sm[256 * 16];
     const Job jb = jobs[blockIdx.x >> 4];
     const ModConst c = mc[jb.mod];
@@ -304,6 +311,24 @@ __global__ void __launch_bounds__(NTT_TPB) ki_cols(const Job *__restrict__ jobs,
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = jb.dst[(16 * g + j) * 256 + col];
+    if (c.q < FP_QMAX) {  // FP64 butterflies; the final scale is one more FP64 product
+        const double *Wd = twd_inv(twd, jb.mod, LOGN);
+        double xd[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
+        fphase_gs<16, 8>(xd, col + 4096 * g, Wd, c.qd, c.qid);
+#pragma unroll
+        for (int j = 0; j < 16; j++) sm[(16 * g + j) * 16 + lc] = (uint64_t)__double_as_longlong(xd[j]);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)sm[(g + 16 * j) * 16 + lc]);
+        fphase_gs<16, 12>(xd, col + 256 * g, Wd, c.qd, c.qid);
+        const double cwd = u2d(jb.cw);
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            jb.dst[(g + 16 * j) * 256 + col] = fcanon(fmulmod(xd[j], cwd, c.qd, c.qid), c.qd, c.qid);
+        return;
+    }
     const bool nc = c.q < NC_INV;  // inputs < 2^9 q (ki_rows), output < 2^17 q, then Shoup -> canonical
     if (nc)
         phase_gs<16, 8, 9>(x, col + 4096 * g, W2, c.q);
@@ -329,6 +354,7 @@ struct IpArgs {
     const uint64_t *key;  // [dnum][2][M][N] Montgomery form
     uint64_t *acc;        // [B][2][ext_n][N]
     const uint64_t *tw;
+    const double *twd;
     const ModConst *mc;
     int ell, ext_n, beta, alpha, L, M, B;
 };
@@ -362,6 +388,22 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
 #pragma unroll
             for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
             const bool nc = c.q < NC_FWD;
+            if (c.q < FP_QMAX) {
+                const double *Wd = twd_fwd(a.twd, m, LOGN);
+                double xd[16];
+#pragma unroll
+                for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
+                fphase_ct<16, 8>(xd, r * 256 + g, Wd, c.qd, c.qid);
+#pragma unroll
+                for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = (uint64_t)__double_as_longlong(xd[j]);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(16 * g + j)]);
+                __syncwarp();
+                fphase_ct<16, 12>(xd, r * 256 + 16 * g, Wd, c.qd, c.qid);
+#pragma unroll
+                for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = fcanon(xd[j], c.qd, c.qid);
+            } else {
             if (nc)
                 phase_ct<16, 8, true>(x, r * 256 + g, W2, c.q);
             else
@@ -380,6 +422,7 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
                 phase_ct<16, 12>(x, r * 256 + 16 * g, W2, c.q);
 #pragma unroll
                 for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], c.q);
+            }
             }
             __syncwarp();
 #pragma unroll
@@ -442,9 +485,9 @@ int run_inverse(he_ctx *c, const std::vector<Job> &jobs, cudaStream_t s) {
                                           (int)(KS * TILE_W * sizeof(uint64_t))));
     }
     const unsigned gp = std::min<unsigned>(g, 2u * (unsigned)sms);
-    ki_rows_p<<<gp, NTT_TPB, KS * TILE_W * sizeof(uint64_t), s>>>(jb.d, (int)g, c->d_tw, c->d_mc);
+    ki_rows_p<<<gp, NTT_TPB, KS * TILE_W * sizeof(uint64_t), s>>>(jb.d, (int)g, c->d_tw, c->d_twd, c->d_mc);
     HE_CHECK_LAUNCH();
-    ki_cols<<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+    ki_cols<<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
@@ -455,9 +498,9 @@ int run_forward(he_ctx *c, const std::vector<Job> &jobs, cudaStream_t s) {
     JobBuf jb(s);
     HE_TRY(jb.up(jobs));
     unsigned g = (unsigned)jobs.size() * 16;
-    kf_cols<LD><<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+    kf_cols<LD><<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
     HE_CHECK_LAUNCH();
-    kf_rows<EP><<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+    kf_rows<EP><<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
@@ -518,7 +561,7 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
             JobBuf jb(s);
             rc = jb.up(jobs);
             if (rc == HE_OK) {
-                kf_cols<L_BCONV><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_mc);
+                kf_cols<L_BCONV><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
                 he_count_launch(1);
                 if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
             }
@@ -532,6 +575,7 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
         a.key = key;
         a.acc = acc;
         a.tw = c->d_tw;
+        a.twd = c->d_twd;
         a.mc = c->d_mc;
         a.ell = ell;
         a.ext_n = ext_n;

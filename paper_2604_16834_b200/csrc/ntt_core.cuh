@@ -79,6 +79,95 @@ __device__ __forceinline__ void phase_gs(uint64_t (&x)[16], uint32_t e0, const u
     stage_gs<LOGN, LT0 + 3, 8, (LOGB < 0 ? -1 : LOGB + 3)>(x, e0, W2, q);
 }
 
+// ---------------------------------------------------------------- FP64 butterflies
+// For primes q < 2^42 the butterflies run on the FP64 pipe (twice the
+// integer-Shoup rate on B200, scripts/mb_modmul.cu).  Residues are held as
+// doubles that are EXACT integers (|x| < 2^53):
+//   a*w mod q:  h = a*w (rounded), l = fma(a, w, -h) (exact error, integer),
+//               e = rint(h / q), r = fma(-e, q, h) + l = a*w - e*q exactly,
+//   with |a| < 2^51 the estimate e is off by < 2 so r lies in (-3q, 3q) and
+//   every intermediate is an integer below 2^53 (no rounding anywhere).
+// Forward: |x| grows by < 3q per stage; inverse: the sum path doubles per
+// stage -- 8 stages from canonical input stay below 2^51 for q < 2^42.  Each
+// pass converts canonical uint64 -> double on entry and canonicalises on exit,
+// so the bits at every kernel boundary are those of the integer path.
+constexpr uint64_t FP_QMAX = 1ull << 42;
+constexpr double FP_MAGIC = 4503599627370496.0;  // 2^52
+
+__device__ __forceinline__ double u2d(uint64_t x) {  // exact for x < 2^52
+    return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - FP_MAGIC;
+}
+__device__ __forceinline__ uint64_t d2u(double r) {  // r an integer in [0, 2^52)
+    return (uint64_t)__double_as_longlong(r + FP_MAGIC) - 0x4330000000000000ull;
+}
+__device__ __forceinline__ double fmulmod(double a, double w, double q, double qi) {
+    const double h = a * w;
+    const double l = fma(a, w, -h);
+    const double e = rint(h * qi);
+    return fma(-e, q, h) + l;
+}
+// exact integer |x| < 2^52 -> canonical residue as uint64
+__device__ __forceinline__ uint64_t fcanon(double x, double q, double qi) {
+    const double e = floor(x * qi);
+    double r = fma(-e, q, x);
+    r = r < 0.0 ? r + q : r;
+    r = r >= q ? r - q : r;
+    return d2u(r);
+}
+
+template <int LOGN, int LM, int D>
+__device__ __forceinline__ void fstage_ct(double (&x)[16], uint32_t e0, const double *__restrict__ W, double q,
+                                          double qi) {
+    const uint32_t base = (1u << LM) + (e0 >> (LOGN - LM));
+#pragma unroll
+    for (int k = 0; k < 8 / D; k++) {
+        const double w = __ldg(W + base + k);
+#pragma unroll
+        for (int jj = 0; jj < D; jj++) {
+            const double u = x[2 * D * k + jj], v = fmulmod(x[2 * D * k + jj + D], w, q, qi);
+            x[2 * D * k + jj] = u + v;
+            x[2 * D * k + jj + D] = u - v;
+        }
+    }
+}
+template <int LOGN, int LM0>
+__device__ __forceinline__ void fphase_ct(double (&x)[16], uint32_t e0, const double *__restrict__ W, double q,
+                                          double qi) {
+    fstage_ct<LOGN, LM0, 8>(x, e0, W, q, qi);
+    fstage_ct<LOGN, LM0 + 1, 4>(x, e0, W, q, qi);
+    fstage_ct<LOGN, LM0 + 2, 2>(x, e0, W, q, qi);
+    fstage_ct<LOGN, LM0 + 3, 1>(x, e0, W, q, qi);
+}
+template <int LOGN, int LT, int D>
+__device__ __forceinline__ void fstage_gs(double (&x)[16], uint32_t e0, const double *__restrict__ W, double q,
+                                          double qi) {
+    const uint32_t base = (1u << (LOGN - 1 - LT)) + (e0 >> (LT + 1));
+#pragma unroll
+    for (int k = 0; k < 8 / D; k++) {
+        const double w = __ldg(W + base + k);
+#pragma unroll
+        for (int jj = 0; jj < D; jj++) {
+            const double u = x[2 * D * k + jj], v = x[2 * D * k + jj + D];
+            x[2 * D * k + jj] = u + v;
+            x[2 * D * k + jj + D] = fmulmod(u - v, w, q, qi);
+        }
+    }
+}
+template <int LOGN, int LT0>
+__device__ __forceinline__ void fphase_gs(double (&x)[16], uint32_t e0, const double *__restrict__ W, double q,
+                                          double qi) {
+    fstage_gs<LOGN, LT0, 1>(x, e0, W, q, qi);
+    fstage_gs<LOGN, LT0 + 1, 2>(x, e0, W, q, qi);
+    fstage_gs<LOGN, LT0 + 2, 4>(x, e0, W, q, qi);
+    fstage_gs<LOGN, LT0 + 3, 8>(x, e0, W, q, qi);
+}
+__device__ __forceinline__ const double *twd_fwd(const double *twd, int m, int logN) {
+    return twd + ((size_t)m << (logN + 1));
+}
+__device__ __forceinline__ const double *twd_inv(const double *twd, int m, int logN) {
+    return twd + ((size_t)m << (logN + 1)) + ((size_t)1 << logN);
+}
+
 __device__ __forceinline__ int pad16(int e) { return e + (e >> 4); }
 
 // twiddle pair tables of modulus m (layout of he_ctx::d_tw)
