@@ -119,12 +119,12 @@ __device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, int yy
 // byte shift D + j still open (|C| < 2^23, <= E terms: no overflow); a
 // completed shift s is folded into P[s/4] with one IMAD.WIDE by 2^(8 (s%4))
 // (multipliers held in registers so ptxas keeps IMAD.WIDE).
-template <int D, int KB, int E, int NB>
-__device__ __forceinline__ void digit_plane(const uint32_t *X, int dstr, const int (&o0)[KB][2], const int (&o1)[KB][2],
+template <int D, int KB, int E, int NB, int DSTR>
+__device__ __forceinline__ void digit_plane(const uint32_t *X, const int (&o0)[KB][2], const int (&o1)[KB][2],
                                             const uint2 (&bw)[KB][E], int (&W)[E][4], int64_t (&P)[3][4],
                                             const int (&mul)[4]) {
     if (D >= NB) return;
-    const uint32_t *Xd = X + D * dstr;
+    const uint32_t *Xd = X + D * DSTR;  // compile-time plane offset: an LDS immediate
     int C[E][4];
 #pragma unroll
     for (int e = 0; e < E; e++) C[e][0] = C[e][1] = C[e][2] = C[e][3] = 0;
@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
     const int l = a.limbs[blockIdx.y];
     const size_t N = (size_t)1 << a.logN, coff = (size_t)blockIdx.x * 8;
     const ModConst c = a.mc[l];
-    const int dstr = 16 * a.ncg;
+    constexpr int NCG = KB == 2 ? 1 : KB - 1;  // channel groups of 4 implied by the K blocks
+    constexpr int DSTR = 16 * NCG;
 
     uint2 bw[KB][E];
 #pragma unroll
@@ -242,14 +243,14 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
                 int W[E][4];
 #pragma unroll
                 for (int j = 0; j < E; j++) W[j][0] = W[j][1] = W[j][2] = W[j][3] = 0;
-                digit_plane<0, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
-                digit_plane<1, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
-                digit_plane<2, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
-                digit_plane<3, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
-                digit_plane<4, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
-                digit_plane<5, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
-                digit_plane<6, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
-                digit_plane<7, KB, E, NB>(xs, dstr, o0, o1, bw, W, P, mul);
+                digit_plane<0, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
+                digit_plane<1, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
+                digit_plane<2, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
+                digit_plane<3, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
+                digit_plane<4, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
+                digit_plane<5, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
+                digit_plane<6, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
+                digit_plane<7, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
                 // fragment values: q=0,1 -> component 0, channels m0, m0+1; q=2,3 -> component 1
                 uint64_t yv[4];
 #pragma unroll
