@@ -770,6 +770,38 @@ class GpuEngine:
                                         self.stream), "mul_const")
         return self._rescale_tensor(tmp, limbs, outs)
 
+    def rescale_batch(self, cts: Sequence[CipherVec], out_scale: float | None = None) -> list[CipherVec]:
+        """Divide-and-round by the last prime (one level); the declared output
+        scale is ``out_scale`` when given (callers that encoded weights for an
+        exact target scale), else scale / q_last."""
+        for c in cts:
+            self._check(c)
+        level = cts[0].level
+        if any(c.level != level for c in cts) or level < 1:
+            raise LevelExhausted("rescale_batch needs equal levels >= 1")
+        limbs = level + 1
+        nc = self._ncomp(cts)
+        out = self._alloc(len(cts), nc, limbs - 1)
+        pi, po = self._ptrs(cts), self._tptrs(out)
+        _lib.check(self._call("rescale", self._L.he_rescale, self._h, _lib.addr(pi), _lib.addr(po), len(cts), limbs,
+                              nc, self.stream, units=(len(cts) * (2 * limbs - 1) * nc * self.N * 8.0, 0.0)),
+                   "rescale")
+        ql = self.moduli[limbs - 1]
+        return self._wrap_batch(out, level - 1, [out_scale if out_scale is not None else c.scale / ql for c in cts])
+
+    def pack_batch(self, cts: Sequence[CipherVec]):
+        """Ciphertexts of one level and scale -> (int64 tensor [k, n_comp, limbs, N], level, scale):
+        the payload a collective moves between ranks (sharded_cnn)."""
+        torch = _torch()
+        level, scale = cts[0].level, cts[0].scale
+        if any(c.level != level or c.scale != scale for c in cts):
+            raise HebatchError("pack_batch needs one level and one scale")
+        return torch.stack([c.data for c in cts]), level, scale
+
+    def unpack_batch(self, t, level: int, scale: float) -> list[CipherVec]:
+        """Inverse of pack_batch: fresh handles over the rows of ``t`` (owned by the engine)."""
+        return self._wrap_batch(t, level, [scale] * t.shape[0])
+
     def _rescale_tensor(self, t, limbs: int, scales) -> list[CipherVec]:
         out = self._alloc(t.shape[0], 2, limbs - 1)
         pi, po = self._tptrs(t), self._tptrs(out)
@@ -891,8 +923,14 @@ class GpuEngine:
 
     def lincomb_grouped(self, inputs: Sequence[CipherVec], term_ptr, term_col, term_tap, out_base, out_stride: int,
                         weights, n_out: int, bias=None, out_scale: float | None = None,
-                        weight_scale: float | None = None) -> list[CipherVec]:
+                        weight_scale: float | None = None, skip_rescale: bool = False) -> list[CipherVec]:
         """Grouped linear combination (he_lincomb_grouped) + rescale + bias.
+
+        ``skip_rescale`` keeps the ordinary weight encoding round(w q_l s_out /
+        s_in) but returns the exact sums before the rescale (and without the
+        bias), at declared scale q_l * s_out: partial sums over input-channel
+        blocks that are added and then rescaled once (rescale_batch with
+        out_scale=s_out) equal the unsplit call bit for bit (sharded_cnn).
 
         Group g (an output pixel) gathers inputs col[t] (t in its term range)
         and produces M = weights.shape[0] outputs
@@ -948,6 +986,12 @@ class GpuEngine:
                               _lib.addr(ob), int(out_stride), M, T, _lib.addr(wi),
                               _lib.addr(fused_res) if fused_res is not None else None, limbs, 2, self.stream,
                               units=((n_used + n_out) * poly * 8.0, float(len(tc)) * M * poly)), "lincomb_grouped")
+        if skip_rescale:
+            if deferred or has_bias:
+                raise HebatchError("skip_rescale excludes weight_scale and bias (add the bias after rescale_batch)")
+            self._acct.bump("plain_mults", int(len(tc)) * M)
+            self._acct.bump("adds", int(len(tc)) * M)
+            return self._wrap_batch(acc, limbs - 1, [ql * s_out] * n_out)
         if deferred:
             out, pout = acc, pacc
         else:

@@ -1,0 +1,74 @@
+"""Config 4 (deep CNN, 24 x 50-bit limbs, degree-3 activations) with output-channel
+sharding over the ranks of one node (sharded_cnn.run_cnn_sharded over NCCL).
+
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 \
+        --master-port 29511 scripts/run_cfg4.py [--hw 32] [--samples 32768]
+
+Prints one JSON line on rank 0: samples/s (device time, max over ranks) and the
+decrypt error of the first 64 samples against the float64 forward pass.  The full
+32x32 map needs >= 2 GPUs (config 4's first activation map alone is ~330 GB); use
+--hw 8 on a single GPU.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "backend:cudaMallocAsync")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--hw", type=int, default=32)
+    ap.add_argument("--seed", type=int, default=0)
+    args = ap.parse_args()
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2604_16834_b200 import configs
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.featuremajor import CnnSpec
+    from paper_2604_16834_b200.packing import pack_features
+    from paper_2604_16834_b200.sharded_cnn import TorchRing, run_cnn_sharded
+    from paper_2604_16834_b200.sharding import max_over_ranks
+
+    base = configs.CNN4
+    spec = CnnSpec(channels=base.channels, H=args.hw, W=args.hw, act=base.act, pool_after=base.pool_after)
+    wts = spec.make_weights(1234)
+    eng = GpuEngine(configs.context(4, seed=42, device=local))
+    n = eng.context.n
+    rng = np.random.default_rng(args.seed)
+    images = rng.uniform(0.0, 1.0, size=(n, 3 * args.hw * args.hw))
+    x = pack_features(eng, images)                     # replicated layer-0 input
+    eng._ensure_relin()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = run_cnn_sharded(eng, x, spec, wts, rank, world, ring=TorchRing(rank, world))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world, device="cuda")
+    got = eng.decrypt_batch(out).T[:64]
+    ref = spec.forward_plain(wts, images[:64].reshape(64, 3, args.hw, args.hw))
+    if rank == 0:
+        print(json.dumps({"config": f"cfg4 CNN {base.channels} on {args.hw}x{args.hw}", "n_gpus": world,
+                          "samples": n, "ms": ms, "samples_per_s": n / (ms / 1e3),
+                          "max_abs_err_64": float(np.max(np.abs(got - ref))),
+                          "parallelism": f"output-channel shards x{world}, ring exchange"}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -11,6 +11,8 @@ PARAMS = {
     "cfg2": (16, (50,) * 24, (50,) * 4, 4, 50),
     "cfg3": (16, (60,) + (40,) * 13, (60,) * 3, 3, 40),
     "cfg4": (16, (50,) * 24, (50,) * 4, 4, 50),
+    # config 4's prime sizes on a small ring (degree-3 CNN tests on one GPU)
+    "cfg4s": (12, (50,) * 10, (50,) * 2, 2, 50),
 }
 
 

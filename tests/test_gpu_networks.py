@@ -162,3 +162,32 @@ def test_cfg3_network_decrypt_and_sampled_bit_exact():
     got = eng.decrypt_batch(out).T
     ref = spec.forward_plain(wts, images[:256])
     assert np.max(np.abs(got[:256] - ref)) < TOL
+
+
+def test_cfg4_layout_sharded_runner_world1_bit_exact_vs_run_cnn():
+    """sharded_cnn (config 4's output-channel layout) at world size 1 on the
+    GPU equals featuremajor.run_cnn's non-lazy plan bit for bit (partial sums
+    over the ring added mod q == the full sum), and decrypts to the float64
+    forward pass: a degree-3 CNN on config 4's prime sizes (small ring)."""
+    from helpers import engine_context
+
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.featuremajor import Activation, CnnSpec, run_cnn
+    from paper_2604_16834_b200.packing import pack_features
+    from paper_2604_16834_b200.sharded_cnn import run_cnn_sharded
+
+    spec = CnnSpec(channels=(3, 4, 4), H=8, W=8, act=Activation((0.5, 0.5, 0.0, 0.0625)), pool_after=(0, 1))
+    wts = spec.make_weights(5)
+    eng = GpuEngine(engine_context("cfg4s", seed=3))
+    n = eng.context.n
+    rng = np.random.default_rng(2)
+    images = rng.uniform(0.0, 1.0, size=(n, 3 * 64))
+    x = pack_features(eng, images)
+    ref_out = run_cnn(eng, x, spec, wts, release_inputs=False, lazy_relin=False)
+    sh_out = run_cnn_sharded(eng, x, spec, wts, 0, 1, release_inputs=False)
+    for o in range(10):
+        assert np.array_equal(to_np(sh_out[o].data), to_np(ref_out[o].data)), o
+        assert sh_out[o].scale == ref_out[o].scale and sh_out[o].level == ref_out[o].level
+    got = eng.decrypt_batch(sh_out).T
+    ref = spec.forward_plain(wts, images.reshape(n, 3, 8, 8))
+    assert np.max(np.abs(got - ref)) < TOL

@@ -1,0 +1,88 @@
+"""Output-channel sharded CNN (config 4's layout, sharded_cnn.py) over gloo.
+
+World sizes 1, 2 and 3 run the same small degree-3 CNN with the float test
+engine; every rank must produce the float64 forward pass.  World 3 does not
+divide the channel counts, so uneven shards and padded ring payloads are
+covered.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2604_16834_b200.featuremajor import Activation, CnnSpec
+
+SPEC = CnnSpec(channels=(3, 4, 5), H=4, W=4, act=Activation((0.5, 0.5, 0.0, 0.0625)), pool_after=(0, 1))
+SAMPLES = 6
+
+
+def _images():
+    rng = np.random.default_rng(3)
+    return rng.uniform(0.0, 1.0, size=(SAMPLES, 3, SPEC.H, SPEC.W))
+
+
+def _run(rank, world):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from toy_engine import ToyEngine
+
+    from paper_2604_16834_b200.sharded_cnn import TorchRing, run_cnn_sharded
+
+    wts = SPEC.make_weights(7)
+    eng = ToyEngine(SAMPLES)
+    imgs = _images()
+    x = eng.encrypt_batch(imgs.reshape(SAMPLES, -1).T)          # feature-major: ct f = pixel f of every sample
+    out = run_cnn_sharded(eng, x, SPEC, wts, rank, world, ring=TorchRing(rank, world))
+    got = np.stack(eng.decrypt_batch(out)).T                     # [samples, classes]
+    eng.release(*out)
+    return got, eng.live
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        got, live = _run(rank, world)
+        q.put((rank, got, live))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_cnn_world1_matches_float_forward():
+    got, live = _run(0, 1)
+    ref = SPEC.forward_plain(SPEC.make_weights(7), _images())
+    assert np.max(np.abs(got - ref)) < 1e-9
+    assert live == 0                          # every intermediate released
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_cnn_over_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = SPEC.forward_plain(SPEC.make_weights(7), _images())
+    for rank, got, live in res:
+        assert np.max(np.abs(got - ref)) < 1e-9, rank
+        assert live == 0, rank
