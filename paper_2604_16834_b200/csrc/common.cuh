@@ -54,6 +54,7 @@ struct he_ctx {
     ModConst *d_mc = nullptr;        // [L+K]
     uint64_t *d_tw = nullptr;        // [L+K][fwd|inv][N][2]  (psi^brv(i), Shoup) pairs
     double *d_twd = nullptr;         // [L+K][fwd|inv][N]     psi^brv(i) as doubles (FP64 butterflies)
+    double *d_rinvd = nullptr;       // [L+K]  2^-64 mod q as doubles (undo Montgomery factors on the FP64 path)
     uint64_t *d_sk = nullptr;        // [L+K][N]     canonical, NTT domain
     double *d_fftw = nullptr;        // [nslots][2]  omega^k
     double *d_twist = nullptr;       // [nslots][2]  zeta^j

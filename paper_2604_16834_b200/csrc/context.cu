@@ -234,6 +234,13 @@ static int build_tables(he_ctx *c) {
         for (size_t i = 0; i < twd.size(); i++) twd[i] = (double)tw[2 * i];
         HE_CHECK_CUDA(cudaMalloc(&c->d_twd, twd.size() * 8));
         HE_CHECK_CUDA(cudaMemcpy(c->d_twd, twd.data(), twd.size() * 8, cudaMemcpyHostToDevice));
+        std::vector<double> rinv(M);
+        for (int m = 0; m < M; m++) {
+            const uint64_t q = c->mod[m], R = (uint64_t)(((hu128)1 << 64) % q);
+            rinv[m] = (double)h_inv(R, q);
+        }
+        HE_CHECK_CUDA(cudaMalloc(&c->d_rinvd, M * sizeof(double)));
+        HE_CHECK_CUDA(cudaMemcpy(c->d_rinvd, rinv.data(), M * sizeof(double), cudaMemcpyHostToDevice));
     }
     HE_CHECK_CUDA(cudaMalloc(&c->d_mc, sizeof(ModConst) * M));
     HE_CHECK_CUDA(cudaMemcpy(c->d_mc, mc.data(), sizeof(ModConst) * M, cudaMemcpyHostToDevice));
@@ -373,6 +380,7 @@ extern "C" int he_ctx_destroy(he_ctx *c) {
     cudaFree(c->d_mc);
     cudaFree(c->d_tw);
     cudaFree(c->d_twd);
+    cudaFree(c->d_rinvd);
     cudaFree(c->d_sk);
     cudaFree(c->d_fftw);
     cudaFree(c->d_twist);

@@ -356,15 +356,81 @@ struct IpArgs {
     const uint64_t *tw;
     const double *twd;
     const ModConst *mc;
+    const double *rinvd;  // [M] 2^-64 mod q (as doubles): undoes the key's Montgomery factor
+    const int32_t *tlist; // targets handled by this launch (indices into the extended basis)
     int ell, ext_n, beta, alpha, L, M, B;
 };
+
+// FP64 form for targets with q < 2^42: pass 2 of every digit's NTT on the
+// FP64 pipe, inner product as exact FP64 modular products against the
+// Montgomery-form key (sum < 10 beta q, no overflow), one R^-1 product and one
+// canonicalisation at the end.  Half the registers of the 128-bit integer
+// accumulators (no spills) and twice the multiply rate.
+__global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip_fp(const IpArgs a) {
+    __shared__ uint64_t sm[16 * 272];
+    const int b = blockIdx.x % a.B, rest = blockIdx.x / a.B;
+    const int rt = rest & 15, t = a.tlist[rest >> 4];
+    const int m = t < a.ell ? t : a.L + (t - a.ell);
+    const ModConst c = a.mc[m];
+    const double *Wd = twd_fwd(a.twd, m, LOGN);
+    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+    const uint32_t r = rt * 16 + rl;
+    const int jt = t < a.ell ? t / a.alpha : -1;
+    uint64_t *s = sm + rl * 272;
+    double acc0[16], acc1[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) acc0[j] = acc1[j] = 0.0;
+    for (int dj = 0; dj < a.beta; dj++) {
+        double xd[16];
+        if (dj == jt) {
+            const uint64_t *dp = a.d[b] + (size_t)t * NN + r * 256;
+#pragma unroll
+            for (int j = 0; j < 16; j++) xd[j] = u2d(dp[g + 16 * j]);
+        } else {
+            const uint64_t *row = a.ext + ((((size_t)b * a.beta + dj) * a.ext_n + t) << LOGN) + r * 256;
+#pragma unroll
+            for (int j = 0; j < 16; j++) xd[j] = u2d(row[g + 16 * j]);
+            fphase_ct<16, 8>(xd, r * 256 + g, Wd, c.qd, c.qid);
+#pragma unroll
+            for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = (uint64_t)__double_as_longlong(xd[j]);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(16 * g + j)]);
+            __syncwarp();
+            fphase_ct<16, 12>(xd, r * 256 + 16 * g, Wd, c.qd, c.qid);  // |x| < 17q: no reduction needed
+#pragma unroll
+            for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = (uint64_t)__double_as_longlong(xd[j]);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(g + 16 * j)]);
+            __syncwarp();
+        }
+        const uint64_t *k0 = a.key + (((size_t)dj * 2 * a.M + m) << LOGN) + r * 256;
+        const uint64_t *k1 = k0 + ((size_t)a.M << LOGN);
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const int cc = g + 16 * j;
+            const double w0 = u2d(__ldg(k0 + cc)), w1 = u2d(__ldg(k1 + cc));
+            acc0[j] += fmulmod(xd[j], w0, c.qd, c.qid);
+            acc1[j] += fmulmod(xd[j], w1, c.qd, c.qid);
+        }
+    }
+    const double ri = a.rinvd[m];
+    uint64_t *o0 = a.acc + ((((size_t)b * 2) * a.ext_n + t) << LOGN) + r * 256;
+    uint64_t *o1 = o0 + ((size_t)a.ext_n << LOGN);
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        o0[g + 16 * j] = fcanon(fmulmod(acc0[j], ri, c.qd, c.qid), c.qd, c.qid);
+        o1[g + 16 * j] = fcanon(fmulmod(acc1[j], ri, c.qd, c.qid), c.qd, c.qid);
+    }
+}
 
 __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
     __shared__ uint64_t sm[16 * 272];
     // ciphertext-fastest order: CTAs resident together read the same key rows
     // (dnum x 2 x 16 rows of limb t), so the key streams from L2, not HBM
     const int b = blockIdx.x % a.B, rest = blockIdx.x / a.B;
-    const int rt = rest & 15, t = rest >> 4;
+    const int rt = rest & 15, t = a.tlist[rest >> 4];
     const int m = t < a.ell ? t : a.L + (t - a.ell);
     const ModConst c = a.mc[m];
     const ulonglong2 *W2 = tw_fwd(a.tw, m, LOGN);
@@ -372,11 +438,11 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
     const uint32_t r = rt * 16 + rl;
     const int jt = t < a.ell ? t / a.alpha : -1;
     uint64_t *s = sm + rl * 272;
-    // lazy inner product: exact 128-bit sums of x * key (key in Montgomery
-    // form), one REDC at the end; each product adds < q/8 to hi (q < 2^61)
-    u128 acc0[16], acc1[16];
+    // inner product with the Montgomery-form key: one REDC per product, canonical
+    // accumulators (64-bit: these wide-prime targets keep the register budget)
+    uint64_t acc0[16], acc1[16];
 #pragma unroll
-    for (int j = 0; j < 16; j++) acc0[j] = acc1[j] = u128{0, 0};
+    for (int j = 0; j < 16; j++) acc0[j] = acc1[j] = 0;
     for (int dj = 0; dj < a.beta; dj++) {
         uint64_t x[16];
         if (dj == jt) {
@@ -387,23 +453,7 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
             const uint64_t *row = a.ext + ((((size_t)b * a.beta + dj) * a.ext_n + t) << LOGN) + r * 256;
 #pragma unroll
             for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
-            const bool nc = c.q < NC_FWD;
-            if (c.q < FP_QMAX) {
-                const double *Wd = twd_fwd(a.twd, m, LOGN);
-                double xd[16];
-#pragma unroll
-                for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
-                fphase_ct<16, 8>(xd, r * 256 + g, Wd, c.qd, c.qid);
-#pragma unroll
-                for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = (uint64_t)__double_as_longlong(xd[j]);
-                __syncwarp();
-#pragma unroll
-                for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(16 * g + j)]);
-                __syncwarp();
-                fphase_ct<16, 12>(xd, r * 256 + 16 * g, Wd, c.qd, c.qid);
-#pragma unroll
-                for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = fcanon(xd[j], c.qd, c.qid);
-            } else {
+            const bool nc = c.q < NC_FWD;  // (targets below 2^42 go to k_modup_ip_fp)
             if (nc)
                 phase_ct<16, 8, true>(x, r * 256 + g, W2, c.q);
             else
@@ -423,7 +473,6 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
 #pragma unroll
                 for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = reduce4q(x[j], c.q);
             }
-            }
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
@@ -435,28 +484,16 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
         for (int j = 0; j < 16; j++) {
             const int cc = g + 16 * j;
             const uint64_t w0 = __ldg(k0 + cc), w1 = __ldg(k1 + cc);
-            mac128(acc0[j], x[j], w0);
-            mac128(acc1[j], x[j], w1);
+            acc0[j] = add_mod(acc0[j], redc(mulhi(x[j], w0), x[j] * w0, c.q, c.qinv), c.q);
+            acc1[j] = add_mod(acc1[j], redc(mulhi(x[j], w1), x[j] * w1, c.q, c.qinv), c.q);
         }
-        if ((dj & 7) == 7)
-#pragma unroll
-            for (int j = 0; j < 16; j++) {
-                acc0[j].hi = acc0[j].hi >= c.q ? acc0[j].hi - c.q : acc0[j].hi;
-                acc1[j].hi = acc1[j].hi >= c.q ? acc1[j].hi - c.q : acc1[j].hi;
-            }
     }
     uint64_t *o0 = a.acc + ((((size_t)b * 2) * a.ext_n + t) << LOGN) + r * 256;
     uint64_t *o1 = o0 + ((size_t)a.ext_n << LOGN);
-    const bool fold = a.beta > 8 && (a.beta & 7);
 #pragma unroll
     for (int j = 0; j < 16; j++) {
-        uint64_t h0 = acc0[j].hi, h1 = acc1[j].hi;
-        if (fold) {
-            h0 = h0 >= c.q ? h0 - c.q : h0;
-            h1 = h1 >= c.q ? h1 - c.q : h1;
-        }
-        o0[g + 16 * j] = redc(h0, acc0[j].lo, c.q, c.qinv);
-        o1[g + 16 * j] = redc(h1, acc1[j].lo, c.q, c.qinv);
+        o0[g + 16 * j] = acc0[j];
+        o1[g + 16 * j] = acc1[j];
     }
 }
 
@@ -584,9 +621,35 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
         a.L = L;
         a.M = M;
         a.B = B;
-        k_modup_ip<<<(unsigned)(B * ext_n * 16), NTT_TPB, 0, s>>>(a);
-        he_count_launch(1);
-        if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+        a.rinvd = c->d_rinvd;
+        // targets split by prime size: FP64 kernel below 2^42, integer kernel otherwise
+        std::vector<int32_t> tl;
+        int nfp = 0;
+        for (int pass = 0; pass < 2; pass++)
+            for (int t = 0; t < ext_n; t++) {
+                const int m = t < ell ? t : L + (t - ell);
+                if ((c->mod[m] < FP_QMAX) == (pass == 0)) {
+                    tl.push_back(t);
+                    nfp += pass == 0;
+                }
+            }
+        int32_t *dtl = nullptr;
+        rc = he_scratch_alloc((void **)&dtl, tl.size() * 4, s);
+        if (rc == HE_OK && cudaMemcpyAsync(dtl, tl.data(), tl.size() * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            rc = HE_ECUDA;
+        if (rc == HE_OK && nfp) {
+            a.tlist = dtl;
+            k_modup_ip_fp<<<(unsigned)(B * nfp * 16), NTT_TPB, 0, s>>>(a);
+            he_count_launch(1);
+            if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+        }
+        if (rc == HE_OK && nfp < ext_n) {
+            a.tlist = dtl + nfp;
+            k_modup_ip<<<(unsigned)(B * (ext_n - nfp) * 16), NTT_TPB, 0, s>>>(a);
+            he_count_launch(1);
+            if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+        }
+        he_scratch_free(dtl, s);
     }
     return rc;
 }
