@@ -69,11 +69,6 @@ struct he_ctx {
     std::vector<uint64_t> h_qlinv;                  // host copy of d_qlinv
     std::vector<uint64_t> h_ninv;                   // N^-1 mod every modulus
     std::mutex mu;
-    // side streams: independent chunks of a batched key switch run concurrently
-    // (fork/join with events on the caller's stream)
-    static constexpr int NSIDE = 2;
-    cudaStream_t side[NSIDE] = {};
-    cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {};
 };
 
 // host-side modular helpers (context.cu)

@@ -319,11 +319,6 @@ extern "C" int he_ctx_create(const he_params *p, int device, he_ctx **out) {
     he_ctx *c = new he_ctx();
     c->prm = *p;
     c->device = device;
-    for (int k = 0; k < he_ctx::NSIDE; k++) {
-        HE_CHECK_CUDA(cudaStreamCreateWithFlags(&c->side[k], cudaStreamNonBlocking));
-        HE_CHECK_CUDA(cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming));
-    }
-    HE_CHECK_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     c->logN = p->log_n;
     c->N = 1 << p->log_n;
     c->L = p->n_q;
@@ -369,11 +364,6 @@ static void free_table(BconvTable &t) {
 extern "C" int he_ctx_destroy(he_ctx *c) {
     if (!c) return HE_OK;
     cudaDeviceSynchronize();
-    for (int k = 0; k < he_ctx::NSIDE; k++) {
-        cudaStreamDestroy(c->side[k]);
-        cudaEventDestroy(c->ev_join[k]);
-    }
-    cudaEventDestroy(c->ev_fork);
     for (auto &kv : c->keys) cudaFree(kv.second);
     for (auto &kv : c->modup_tab) free_table(kv.second);
     for (auto &kv : c->moddown_tab) free_table(kv.second);

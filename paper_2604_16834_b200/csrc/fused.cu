@@ -48,7 +48,7 @@ struct Job {
     int32_t ns;           // BConv source count
 };
 
-enum { L_DIRECT = 0, L_BCONV = 1, L_CENTER = 2 };
+enum { L_DIRECT = 0, L_BCONV = 1, L_CENTER = 2, L_BCONV_FP = 3 };
 enum { E_STORE = 0, E_SUBSCALE = 1 };
 
 // ---------------------------------------------------------------- forward pass 1 (columns)
@@ -61,6 +61,37 @@ __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs,
     const ulonglong2 *W2 = tw_fwd(tw, jb.mod, LOGN);
     const int tid = threadIdx.x, lc = tid & 15, g = tid >> 4;
     const uint32_t col = (blockIdx.x & 15) * 16 + lc;
+    if (LD == L_BCONV_FP) {
+        // every source and the target below 2^42: the BConv is FP64 modular
+        // products against the Montgomery-form table (sum < 2 ns q), one R^-1
+        // product, and the NTT runs on the FP64 pipe without leaving doubles
+        const double *Wd = twd_fwd(twd, jb.mod, LOGN);
+        double xd[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) xd[j] = 0.0;
+        for (int s = 0; s < jb.ns; s++) {
+            const double t = u2d(__ldg(jb.tab + s));
+            const uint64_t *src = jb.src + (size_t)s * NN + col;
+            double v[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) v[j] = u2d(__ldg(src + (g + 16 * j) * 256));
+#pragma unroll
+            for (int j = 0; j < 16; j++) xd[j] += fmulmod(v[j], t, c.qd, c.qid);
+        }
+        const double ri = u2d(jb.cw);  // R^-1 mod q (host)
+#pragma unroll
+        for (int j = 0; j < 16; j++) xd[j] = fmulmod(xd[j], ri, c.qd, c.qid);  // |x| < 2q
+        fphase_ct<16, 0>(xd, col + 256 * g, Wd, c.qd, c.qid);
+#pragma unroll
+        for (int j = 0; j < 16; j++) sm[(g + 16 * j) * 16 + lc] = (uint64_t)__double_as_longlong(xd[j]);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)sm[(16 * g + j) * 16 + lc]);
+        fphase_ct<16, 4>(xd, col + 4096 * g, Wd, c.qd, c.qid);
+#pragma unroll
+        for (int j = 0; j < 16; j++) jb.dst[(16 * g + j) * 256 + col] = fcanon(xd[j], c.qd, c.qid);
+        return;
+    }
     uint64_t x[16];
     if (LD == L_DIRECT) {
 #pragma unroll
@@ -576,12 +607,15 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
         rc = run_inverse(c, jobs, s);
     }
     // 2. ModUp pass 1: BConv loaded straight into the NTT of every target limb
+    //    (FP64 loader when the digit's sources and the target are all below 2^42)
     if (rc == HE_OK) {
-        std::vector<Job> jobs;
+        std::vector<Job> jobs, jobs_fp;
         for (int b = 0; b < B; b++)
             for (int dj = 0; dj < beta; dj++) {
                 const BconvTable *tb = up[dj];
                 const int s0 = dj * alpha, ns = tb->n_src;
+                bool src_small = true;
+                for (int k = 0; k < ns; k++) src_small = src_small && c->mod[s0 + k] < FP_QMAX;
                 for (int dst = 0; dst < tb->n_dst; dst++) {
                     const int m = tb->h_dst_mod[dst];
                     const int t = m < L ? m : ell + (m - L);
@@ -591,10 +625,26 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
                     j.tab = tb->d + 2 * ns + (size_t)dst * ns;
                     j.mod = m;
                     j.dst = ext + (((size_t)b * beta + dj) * ext_n + t) * NN;
-                    jobs.push_back(j);
+                    if (src_small && c->mod[m] < FP_QMAX) {
+                        const uint64_t q = c->mod[m];
+                        j.cw = he_h_inv((uint64_t)(((unsigned __int128)1 << 64) % q), q);  // R^-1 mod q
+                        jobs_fp.push_back(j);
+                    } else {
+                        jobs.push_back(j);
+                    }
                 }
             }
-        if (!jobs.empty()) {
+        if (!jobs_fp.empty()) {
+            JobBuf jb(s);
+            rc = jb.up(jobs_fp);
+            if (rc == HE_OK) {
+                kf_cols<L_BCONV_FP><<<(unsigned)jobs_fp.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd,
+                                                                                     c->d_mc);
+                he_count_launch(1);
+                if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+            }
+        }
+        if (rc == HE_OK && !jobs.empty()) {
             JobBuf jb(s);
             rc = jb.up(jobs);
             if (rc == HE_OK) {

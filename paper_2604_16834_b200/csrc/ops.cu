@@ -670,26 +670,12 @@ extern "C" int he_relin_rescale(he_ctx *c, const uint64_t *const *d3, uint64_t *
     for (int i = 0; i < count; i++) p2[i] = d3[i] + 2 * P;
     DevPtrs D2(s);
     HE_TRY(D2.up((const void *const *)p2.data(), count));
-    // chunks alternate between the context's side streams (forked from and
-    // joined back into the caller's stream): one chunk's latency-bound passes
-    // overlap the other's, and kernel tails overlap
     int ch = chunk_of(ks_bytes_per_ct(c, ell), count);
-    if (count > 1) ch = std::min(ch, (count + 1) / 2);  // at least two chunks: both side streams get work
-    const int nside = count > 1 ? he_ctx::NSIDE : 1;
-    HE_CHECK_CUDA(cudaEventRecord(c->ev_fork, s));
-    for (int k = 0; k < nside; k++) HE_CHECK_CUDA(cudaStreamWaitEvent(c->side[k], c->ev_fork, 0));
-    int rc = HE_OK, k = 0;
-    for (int b0 = 0; b0 < count && rc == HE_OK; b0 += ch, k++) {
+    for (int b0 = 0; b0 < count; b0 += ch) {
         int B = std::min(ch, count - b0);
-        cudaStream_t sk = nside > 1 ? c->side[k % nside] : s;
-        rc = he_relin_rescale_fused(c, key, d3 + b0, D2.as<const uint64_t>() + b0, B, ell, extra, out + b0, sk);
+        HE_TRY(he_relin_rescale_fused(c, key, d3 + b0, D2.as<const uint64_t>() + b0, B, ell, extra, out + b0, s));
     }
-    for (int j = 0; j < nside; j++) {
-        if (nside == 1) break;
-        HE_CHECK_CUDA(cudaEventRecord(c->ev_join[j], c->side[j]));
-        HE_CHECK_CUDA(cudaStreamWaitEvent(s, c->ev_join[j], 0));
-    }
-    return rc;
+    return HE_OK;
 }
 
 extern "C" int he_rescale(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, int count, int ell, int nc,
