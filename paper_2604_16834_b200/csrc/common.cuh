@@ -242,6 +242,8 @@ __device__ __forceinline__ uint64_t sample_uniform(uint64_t seed, uint32_t dom, 
 
 // ---------------------------------------------------------------- host helpers (defined in context.cu)
 int he_upload_ptrs(const void *const *host_ptrs, int count, void ***dev_out, cudaStream_t s);
+// host -> device copy through the pinned staging ring (returns immediately; src may be reused)
+cudaError_t he_h2d(void *dst, const void *src, size_t bytes, cudaStream_t s);
 int he_scratch_alloc(void **p, size_t bytes, cudaStream_t s);
 void he_scratch_free(void *p, cudaStream_t s);
 int he_get_modup_table(he_ctx *ctx, int ell, int digit, const BconvTable **out);

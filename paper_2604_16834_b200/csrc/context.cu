@@ -24,6 +24,7 @@ void he_set_error(const char *fmt, ...) {
 extern "C" const char *he_last_error(void) { return g_err; }
 
 #include <atomic>
+#include <deque>
 static std::atomic<unsigned long long> g_launches{0};
 void he_count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 extern "C" unsigned long long he_launch_count(void) { return g_launches.load(); }
@@ -75,6 +76,69 @@ static uint32_t h_brv(uint32_t x, int bits) {
     return r;
 }
 
+// ---------------------------------------------------------------- pinned staging ring
+// Every small host->device upload (pointer tables, job lists, weights) goes
+// through one process-wide pinned ring: the bytes are copied into the ring at
+// call time and the DMA is queued on the stream, so the host never waits for
+// the GPU to drain (a pageable cudaMemcpyAsync stages synchronously in stream
+// order).  A region is reused only after the event recorded behind its copy
+// has completed; ring allocation is sequential, so the regions to retire are
+// always at the front of the FIFO.
+namespace {
+struct Staging {
+    std::mutex mu;
+    char *buf = nullptr;
+    size_t cap = 0, head = 0;
+    bool tried = false;
+    struct Ent {
+        size_t lo, hi;
+        cudaEvent_t ev;
+    };
+    std::deque<Ent> fifo;
+    std::vector<cudaEvent_t> spare;
+};
+Staging g_stage;
+}  // namespace
+
+cudaError_t he_h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    if (!bytes) return cudaSuccess;
+    std::lock_guard<std::mutex> lk(g_stage.mu);
+    if (!g_stage.tried) {
+        g_stage.tried = true;
+        if (cudaHostAlloc((void **)&g_stage.buf, (size_t)256 << 20, cudaHostAllocDefault) == cudaSuccess)
+            g_stage.cap = (size_t)256 << 20;
+        else
+            g_stage.buf = nullptr;
+    }
+    if (!g_stage.buf || bytes > g_stage.cap / 4) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+    size_t lo = (g_stage.head + 15) & ~(size_t)15;
+    if (lo + bytes > g_stage.cap) lo = 0;
+    const size_t hi = lo + bytes;
+    while (!g_stage.fifo.empty()) {  // retire completed copies; wait only on overlapping ones
+        Staging::Ent &f = g_stage.fifo.front();
+        const bool overlap = f.lo < hi && lo < f.hi;
+        if (!overlap && cudaEventQuery(f.ev) != cudaSuccess) break;
+        if (overlap) cudaEventSynchronize(f.ev);
+        g_stage.spare.push_back(f.ev);
+        g_stage.fifo.pop_front();
+    }
+    memcpy(g_stage.buf + lo, src, bytes);
+    cudaError_t e = cudaMemcpyAsync(dst, g_stage.buf + lo, bytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    cudaEvent_t ev;
+    if (g_stage.spare.empty()) {
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    } else {
+        ev = g_stage.spare.back();
+        g_stage.spare.pop_back();
+    }
+    e = cudaEventRecord(ev, s);
+    g_stage.fifo.push_back({lo, hi, ev});
+    g_stage.head = hi;
+    return e;
+}
+
 // ---------------------------------------------------------------- scratch / pointer upload
 int he_scratch_alloc(void **p, size_t bytes, cudaStream_t s) {
     if (bytes == 0) bytes = 8;
@@ -91,7 +155,7 @@ void he_scratch_free(void *p, cudaStream_t s) {
 int he_upload_ptrs(const void *const *host_ptrs, int count, void ***dev_out, cudaStream_t s) {
     HE_TRY(he_scratch_alloc((void **)dev_out, sizeof(void *) * (size_t)(count > 0 ? count : 1), s));
     if (count > 0)
-        HE_CHECK_CUDA(cudaMemcpyAsync(*dev_out, host_ptrs, sizeof(void *) * count, cudaMemcpyHostToDevice, s));
+        HE_CHECK_CUDA(he_h2d(*dev_out, host_ptrs, sizeof(void *) * count, s));
     return HE_OK;
 }
 
@@ -489,7 +553,7 @@ extern "C" int he_gen_switch_key(he_ctx *c, uint32_t g, void *stream) {
     HE_TRY(he_scratch_alloc((void **)&err, tot * 8, s));
     HE_TRY(he_scratch_alloc((void **)&sp, (size_t)L * N * 8, s));
     HE_TRY(he_scratch_alloc((void **)&pm, (size_t)L * 8, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(pm, c->h_pmodq.data(), L * 8, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(pm, c->h_pmodq.data(), L * 8, s));
     if (g == 0)
         k_sk_square<<<ceil_div((size_t)L * N, 256), 256, 0, s>>>(sp, c->d_sk, c->d_mc, N, L);
     else

@@ -531,11 +531,11 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
     uint64_t *dr4 = (uint64_t *)carve(b_r4);
     uint64_t *db = bias ? (uint64_t *)carve(b_b) : nullptr;
     uint64_t *dc = cst ? (uint64_t *)carve(b_c) : nullptr;
-    HE_CHECK_CUDA(cudaMemcpyAsync(dbf, bf.data(), b_bf, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dlo, lorder.data(), b_lo, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dr4, r4.data(), b_r4, cudaMemcpyHostToDevice, s));
-    if (db) HE_CHECK_CUDA(cudaMemcpyAsync(db, bres.data(), b_b, cudaMemcpyHostToDevice, s));
-    if (dc) HE_CHECK_CUDA(cudaMemcpyAsync(dc, cst, b_c, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(dbf, bf.data(), b_bf, s));
+    HE_CHECK_CUDA(he_h2d(dlo, lorder.data(), b_lo, s));
+    HE_CHECK_CUDA(he_h2d(dr4, r4.data(), b_r4, s));
+    if (db) HE_CHECK_CUDA(he_h2d(db, bres.data(), b_b, s));
+    if (dc) HE_CHECK_CUDA(he_h2d(dc, cst, b_c, s));
     SqArgs a;
     a.in = (const uint64_t *const *)din;
     a.out = (uint64_t *const *)dout;

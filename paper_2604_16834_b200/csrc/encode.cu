@@ -201,7 +201,7 @@ int encode_into(he_ctx *c, const double *vals, int count, int nvals, double scal
 
 int upload_map(const std::vector<uint8_t> &m, Buf &b, cudaStream_t s) {
     HE_TRY(he_scratch_alloc(&b.p, m.size(), s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(b.p, m.data(), m.size(), cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(b.p, m.data(), m.size(), s));
     return HE_OK;
 }
 
@@ -301,7 +301,7 @@ extern "C" int he_decrypt(he_ctx *c, const uint64_t *const *cts, int count, int 
     HE_TRY(he_scratch_alloc(&co.p, (size_t)count * N * 8, s));
     HE_TRY(decrypt_to_coeffs(c, cts, count, ell, (double *)co.p, s));
     HE_TRY(he_scratch_alloc(&sc.p, (size_t)count * 8, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(sc.p, scales, (size_t)count * 8, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(sc.p, scales, (size_t)count * 8, s));
     HE_TRY(he_scratch_alloc(&fft.p, (size_t)count * n * 16, s));
     double *re = (double *)fft.p, *im = re + (size_t)count * n;
     k_decode_twist<<<gridn((size_t)count * n), EW, 0, s>>>(re, im, (const double *)co.p, count, c->logN,

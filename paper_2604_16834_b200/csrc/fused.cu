@@ -46,25 +46,29 @@ struct Job {
     uint64_t c2, c2p;     // Shoup constant for src2 / aux2 (P mod q for the joint ModDown)
     int32_t mod;          // modulus index of this polynomial
     int32_t ns;           // BConv source count
+    int32_t wide;         // L_BCONV_FP: bit s set when source s is a prime >= 2^42 (split in 30-bit halves)
+    int32_t pad_;
 };
 
-enum { L_DIRECT = 0, L_BCONV = 1, L_CENTER = 2, L_BCONV_FP = 3 };
+enum { L_DIRECT = 0, L_BCONV = 1, L_CENTER = 2, L_BCONV_FP = 3, L_BCONV_FPW = 4 };  // FPW: wide sources allowed
 enum { E_STORE = 0, E_SUBSCALE = 1 };
 
 // ---------------------------------------------------------------- forward pass 1 (columns)
 template <int LD>
 __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs, const uint64_t *tw,
-                                                  const double *twd, const ModConst *mc) {
+                                                  const double *twd, const ModConst *mc, const double *rinvd) {
     __shared__ uint64_t sm[256 * 16];
     const Job jb = jobs[blockIdx.x >> 4];
     const ModConst c = mc[jb.mod];
     const ulonglong2 *W2 = tw_fwd(tw, jb.mod, LOGN);
     const int tid = threadIdx.x, lc = tid & 15, g = tid >> 4;
     const uint32_t col = (blockIdx.x & 15) * 16 + lc;
-    if (LD == L_BCONV_FP) {
-        // every source and the target below 2^42: the BConv is FP64 modular
-        // products against the Montgomery-form table (sum < 2 ns q), one R^-1
-        // product, and the NTT runs on the FP64 pipe without leaving doubles
+    if (LD == L_BCONV_FP || LD == L_BCONV_FPW) {
+        // target below 2^42: the BConv is FP64 modular products against the
+        // Montgomery-form table (sum < 4 ns q), one R^-1 product, and the NTT
+        // runs on the FP64 pipe without leaving doubles.  A source residue from a
+        // prime >= 2^42 is split v = hi 2^30 + lo (both exact, < 2^31) and takes
+        // two products, the high one against t 2^30 mod q.
         const double *Wd = twd_fwd(twd, jb.mod, LOGN);
         double xd[16];
 #pragma unroll
@@ -72,13 +76,21 @@ __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs,
         for (int s = 0; s < jb.ns; s++) {
             const double t = u2d(__ldg(jb.tab + s));
             const uint64_t *src = jb.src + (size_t)s * NN + col;
-            double v[16];
+            uint64_t v[16];
 #pragma unroll
-            for (int j = 0; j < 16; j++) v[j] = u2d(__ldg(src + (g + 16 * j) * 256));
+            for (int j = 0; j < 16; j++) v[j] = __ldg(src + (g + 16 * j) * 256);
+            if (LD == L_BCONV_FPW && ((jb.wide >> s) & 1)) {
+                const double t30 = fmulmod(t, 1073741824.0, c.qd, c.qid);
 #pragma unroll
-            for (int j = 0; j < 16; j++) xd[j] += fmulmod(v[j], t, c.qd, c.qid);
+                for (int j = 0; j < 16; j++)
+                    xd[j] += fmulmod(u2d(v[j] & 0x3FFFFFFFull), t, c.qd, c.qid) +
+                             fmulmod(u2d(v[j] >> 30), t30, c.qd, c.qid);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; j++) xd[j] += fmulmod(u2d(v[j]), t, c.qd, c.qid);
+            }
         }
-        const double ri = u2d(jb.cw);  // R^-1 mod q (host)
+        const double ri = rinvd[jb.mod];  // 2^-64 mod q
 #pragma unroll
         for (int j = 0; j < 16; j++) xd[j] = fmulmod(xd[j], ri, c.qd, c.qid);  // |x| < 2q
         fphase_ct<16, 0>(xd, col + 256 * g, Wd, c.qd, c.qid);
@@ -536,7 +548,7 @@ struct JobBuf {
     ~JobBuf() { he_scratch_free(d, s); }
     int up(const std::vector<Job> &v) {
         HE_TRY(he_scratch_alloc((void **)&d, v.size() * sizeof(Job), s));
-        HE_CHECK_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(Job), cudaMemcpyHostToDevice, s));
+        HE_CHECK_CUDA(he_h2d(d, v.data(), v.size() * sizeof(Job), s));
         return HE_OK;
     }
 };
@@ -561,14 +573,32 @@ int run_inverse(he_ctx *c, const std::vector<Job> &jobs, cudaStream_t s) {
 }
 
 template <int LD, int EP>
-int run_forward(he_ctx *c, const std::vector<Job> &jobs, cudaStream_t s) {
-    if (jobs.empty()) return HE_OK;
+int run_forward(he_ctx *c, const std::vector<Job> &jobs_in, cudaStream_t s) {
+    if (jobs_in.empty()) return HE_OK;
+    // BConv passes: targets below 2^42 take the FP64 loader (own launch), listed first
+    std::vector<Job> jobs;
+    size_t nfp = 0;
+    if (LD == L_BCONV) {
+        for (const Job &j : jobs_in)
+            if (c->mod[j.mod] < FP_QMAX) jobs.push_back(j);
+        nfp = jobs.size();
+        for (const Job &j : jobs_in)
+            if (c->mod[j.mod] >= FP_QMAX) jobs.push_back(j);
+    } else {
+        jobs = jobs_in;
+    }
     JobBuf jb(s);
     HE_TRY(jb.up(jobs));
-    unsigned g = (unsigned)jobs.size() * 16;
-    kf_cols<LD><<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
-    HE_CHECK_LAUNCH();
-    kf_rows<EP><<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
+    if (nfp) {
+        kf_cols<L_BCONV_FPW><<<(unsigned)nfp * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc, c->d_rinvd);
+        HE_CHECK_LAUNCH();
+    }
+    if (jobs.size() > nfp) {
+        kf_cols<LD><<<(unsigned)(jobs.size() - nfp) * 16, NTT_TPB, 0, s>>>(jb.d + nfp, c->d_tw, c->d_twd, c->d_mc,
+                                                                          c->d_rinvd);
+        HE_CHECK_LAUNCH();
+    }
+    kf_rows<EP><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
@@ -607,15 +637,15 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
         rc = run_inverse(c, jobs, s);
     }
     // 2. ModUp pass 1: BConv loaded straight into the NTT of every target limb
-    //    (FP64 loader when the digit's sources and the target are all below 2^42)
+    //    (FP64 loader for targets below 2^42)
     if (rc == HE_OK) {
         std::vector<Job> jobs, jobs_fp;
         for (int b = 0; b < B; b++)
             for (int dj = 0; dj < beta; dj++) {
                 const BconvTable *tb = up[dj];
                 const int s0 = dj * alpha, ns = tb->n_src;
-                bool src_small = true;
-                for (int k = 0; k < ns; k++) src_small = src_small && c->mod[s0 + k] < FP_QMAX;
+                int wide = 0;
+                for (int k = 0; k < ns; k++) wide |= (c->mod[s0 + k] >= FP_QMAX ? 1 : 0) << k;
                 for (int dst = 0; dst < tb->n_dst; dst++) {
                     const int m = tb->h_dst_mod[dst];
                     const int t = m < L ? m : ell + (m - L);
@@ -625,21 +655,29 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
                     j.tab = tb->d + 2 * ns + (size_t)dst * ns;
                     j.mod = m;
                     j.dst = ext + (((size_t)b * beta + dj) * ext_n + t) * NN;
-                    if (src_small && c->mod[m] < FP_QMAX) {
-                        const uint64_t q = c->mod[m];
-                        j.cw = he_h_inv((uint64_t)(((unsigned __int128)1 << 64) % q), q);  // R^-1 mod q
+                    if (c->mod[m] < FP_QMAX) {
+                        j.wide = wide;
                         jobs_fp.push_back(j);
                     } else {
                         jobs.push_back(j);
                     }
                 }
             }
-        if (!jobs_fp.empty()) {
+        if (!jobs_fp.empty()) {  // narrow-source jobs first (64-register instantiation), then wide
+            std::stable_partition(jobs_fp.begin(), jobs_fp.end(), [](const Job &j) { return j.wide == 0; });
+            size_t nn = 0;
+            while (nn < jobs_fp.size() && jobs_fp[nn].wide == 0) nn++;
             JobBuf jb(s);
             rc = jb.up(jobs_fp);
-            if (rc == HE_OK) {
-                kf_cols<L_BCONV_FP><<<(unsigned)jobs_fp.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd,
-                                                                                     c->d_mc);
+            if (rc == HE_OK && nn) {
+                kf_cols<L_BCONV_FP><<<(unsigned)nn * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc,
+                                                                         c->d_rinvd);
+                he_count_launch(1);
+                if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+            }
+            if (rc == HE_OK && jobs_fp.size() > nn) {
+                kf_cols<L_BCONV_FPW><<<(unsigned)(jobs_fp.size() - nn) * 16, NTT_TPB, 0, s>>>(
+                    jb.d + nn, c->d_tw, c->d_twd, c->d_mc, c->d_rinvd);
                 he_count_launch(1);
                 if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
             }
@@ -648,7 +686,7 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
             JobBuf jb(s);
             rc = jb.up(jobs);
             if (rc == HE_OK) {
-                kf_cols<L_BCONV><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
+                kf_cols<L_BCONV><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc, c->d_rinvd);
                 he_count_launch(1);
                 if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
             }
@@ -685,7 +723,7 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
             }
         int32_t *dtl = nullptr;
         rc = he_scratch_alloc((void **)&dtl, tl.size() * 4, s);
-        if (rc == HE_OK && cudaMemcpyAsync(dtl, tl.data(), tl.size() * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        if (rc == HE_OK && he_h2d(dtl, tl.data(), tl.size() * 4, s) != cudaSuccess)
             rc = HE_ECUDA;
         if (rc == HE_OK && nfp) {
             a.tlist = dtl;
@@ -747,6 +785,7 @@ int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d,
                     j.src = acc + (((size_t)b * 2 + cc) * ext_n + ell) * NN;
                     j.ns = K;
                     j.tab = dn->d + 2 * K + (size_t)i * K;
+                    for (int k = 0; k < K; k++) j.wide |= (c->mod[L + k] >= FP_QMAX ? 1 : 0) << k;
                     j.mod = i;
                     j.dst = md + (((size_t)b * 2 + cc) * ell + i) * NN;
                     j.aux = acc + (((size_t)b * 2 + cc) * ext_n + i) * NN;
@@ -817,6 +856,10 @@ int he_relin_rescale_fused(he_ctx *c, const uint64_t *key, const uint64_t *const
                     j.src = acc + (((size_t)b * 2 + cc) * ext_n + lo) * NN;
                     j.ns = ns;
                     j.tab = dn->d + 2 * ns + (size_t)i * ns;
+                    for (int si = 0; si < ns; si++) {  // sources: dropped Q limbs, then P
+                        const int sm_ = si < extra ? lo + si : L + (si - extra);
+                        j.wide |= (c->mod[sm_] >= FP_QMAX ? 1 : 0) << si;
+                    }
                     j.mod = i;
                     j.dst = md + (((size_t)b * 2 + cc) * lo + i) * NN;
                     j.aux = acc + (((size_t)b * 2 + cc) * ext_n + i) * NN;

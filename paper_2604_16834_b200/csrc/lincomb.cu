@@ -271,9 +271,9 @@ extern "C" int he_square_sum(he_ctx *c, const uint64_t *const *in, int n_in, uin
     HE_TRY(he_scratch_alloc((void **)&meta, b_res + b_rp + b_col + 64, s));
     uint64_t *dres = residues ? (uint64_t *)meta : nullptr;
     int32_t *drp = (int32_t *)(meta + b_res), *dcol = (int32_t *)(meta + b_res + b_rp);
-    if (residues) HE_CHECK_CUDA(cudaMemcpyAsync(dres, residues, b_res, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(drp, row_ptr, b_rp, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dcol, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s));
+    if (residues) HE_CHECK_CUDA(he_h2d(dres, residues, b_res, s));
+    HE_CHECK_CUDA(he_h2d(drp, row_ptr, b_rp, s));
+    HE_CHECK_CUDA(he_h2d(dcol, col, (size_t)nnz * 4, s));
     int rc = HE_OK;
     const int cpp = c->N / LB;
     for (int o0 = 0; o0 < n_out && rc == HE_OK; o0 += 65535) {
@@ -353,16 +353,16 @@ extern "C" int he_lincomb_grouped(he_ctx *c, const uint64_t *const *in, int n_in
     HE_TRY(he_scratch_alloc((void **)&meta, b_wM + b_terms + b_w + b_tp + b_ob + b_res + 64, s));
     uint64_t *dres =
         residues ? (uint64_t *)(meta + ((b_wM + b_terms + b_w + b_tp + b_ob + 7) & ~(size_t)7)) : nullptr;
-    if (residues) HE_CHECK_CUDA(cudaMemcpyAsync(dres, residues, b_res, cudaMemcpyHostToDevice, s));
+    if (residues) HE_CHECK_CUDA(he_h2d(dres, residues, b_res, s));
     uint64_t *wM = (uint64_t *)meta;
     Term *dterms = (Term *)(meta + b_wM);
     int64_t *dw = (int64_t *)(meta + b_wM + b_terms);
     int32_t *dtp = (int32_t *)(meta + b_wM + b_terms + b_w);
     int32_t *dob = (int32_t *)(meta + b_wM + b_terms + b_w + b_tp);
-    HE_CHECK_CUDA(cudaMemcpyAsync(dterms, terms.data(), b_terms, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dw, weights, b_w, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dtp, term_ptr, b_tp, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dob, out_base, b_ob, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(dterms, terms.data(), b_terms, s));
+    HE_CHECK_CUDA(he_h2d(dw, weights, b_w, s));
+    HE_CHECK_CUDA(he_h2d(dtp, term_ptr, b_tp, s));
+    HE_CHECK_CUDA(he_h2d(dob, out_base, b_ob, s));
     k_group_weights<<<ceil_div((size_t)ell * T * MM, 256), 256, 0, s>>>(wM, dw, M, MM, T, ell, c->d_mc);
     HE_CHECK_LAUNCH();
     const int gpb = std::max(1, std::min(8, n_groups / 148));

@@ -309,10 +309,10 @@ extern "C" int he_conv_mma(he_ctx *c, const uint64_t *const *in, int n_in, uint6
     int32_t *dgc = (int32_t *)(meta + b_bf);
     int32_t *dob = (int32_t *)(meta + b_bf + b_gc);
     uint64_t *dres = residues ? (uint64_t *)(meta + ((b_bf + b_gc + b_ob + 7) & ~(size_t)7)) : nullptr;
-    HE_CHECK_CUDA(cudaMemcpyAsync(dbf, bf.data(), b_bf, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dgc, gc.data(), b_gc, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dob, out_base, b_ob, cudaMemcpyHostToDevice, s));
-    if (residues) HE_CHECK_CUDA(cudaMemcpyAsync(dres, residues, b_res, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(dbf, bf.data(), b_bf, s));
+    HE_CHECK_CUDA(he_h2d(dgc, gc.data(), b_gc, s));
+    HE_CHECK_CUDA(he_h2d(dob, out_base, b_ob, s));
+    if (residues) HE_CHECK_CUDA(he_h2d(dres, residues, b_res, s));
     MmaArgs a;
     a.out = (uint64_t *const *)dout;
     a.in = (const uint64_t *const *)din;

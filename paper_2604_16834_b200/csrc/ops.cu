@@ -411,7 +411,7 @@ int keyswitch_chunk(he_ctx *c, const uint64_t *key, uint64_t *const *d_dev, int 
     }
     Scratch dmap(s);
     HE_TRY(dmap.alloc(map.size()));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dmap.p, map.data(), map.size(), cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(dmap.p, map.data(), map.size(), s));
     HE_TRY(he_ntt_fwd(c, ext, B * beta * ext_n, (const uint8_t *)dmap.p, beta * ext_n, s));
     // 3. inner product with the key
     k_ks_inner<<<grid_flat((size_t)B * ext_n * Nw), EW, 0, s>>>(acc, ext, (const uint64_t *const *)d_dev, key, B, ell,
@@ -425,7 +425,7 @@ int keyswitch_chunk(he_ctx *c, const uint64_t *key, uint64_t *const *d_dev, int 
     }
     Scratch dpmap(s);
     HE_TRY(dpmap.alloc(pmap.size()));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dpmap.p, pmap.data(), pmap.size(), cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(dpmap.p, pmap.data(), pmap.size(), s));
     HE_TRY(he_ntt_inv(c, acc, B * 2 * ext_n, (const uint8_t *)dpmap.p, 2 * ext_n, s));
     const BconvTable *dt;
     HE_TRY(he_get_moddown_table(c, ell, &dt));
@@ -517,7 +517,7 @@ static int const_op(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, 
     HE_TRY(O.up((const void *const *)out, count));
     Scratch R(s);
     HE_TRY(R.alloc((size_t)count * ell * 8));
-    HE_CHECK_CUDA(cudaMemcpyAsync(R.p, res, (size_t)count * ell * 8, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(R.p, res, (size_t)count * ell * 8, s));
     k_const<<<grid_ew((size_t)nc * ell * c->N, count, 2), EW, 0, s>>>(O.as<uint64_t>(), I.as<const uint64_t>(), count,
                                                                        ell, nc, c->logN, c->d_mc, R.u(), mul);
     HE_CHECK_LAUNCH();
@@ -864,9 +864,9 @@ extern "C" int he_lincomb(he_ctx *c, const uint64_t *const *in, int n_in, uint64
     uint64_t *wM = (uint64_t *)(base + nz * 8);
     int32_t *drp = (int32_t *)(base + nz * 8 + nz * ell * 8);
     int32_t *dcol = drp + n_out + 1;
-    HE_CHECK_CUDA(cudaMemcpyAsync(dw, w, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(drp, row_ptr, ((size_t)n_out + 1) * 4, cudaMemcpyHostToDevice, s));
-    HE_CHECK_CUDA(cudaMemcpyAsync(dcol, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, s));
+    HE_CHECK_CUDA(he_h2d(dw, w, (size_t)nnz * 8, s));
+    HE_CHECK_CUDA(he_h2d(drp, row_ptr, ((size_t)n_out + 1) * 4, s));
+    HE_CHECK_CUDA(he_h2d(dcol, col, (size_t)nnz * 4, s));
     if (nnz) {
         k_lincomb_weights<<<ceil_div((size_t)nnz * ell, EW), EW, 0, s>>>(wM, dw, nnz, ell, c->d_mc);
         HE_CHECK_LAUNCH();

@@ -29,6 +29,10 @@ def main():
     images = rng.uniform(0.0, 1.0, size=(S, 3 * 32 * 32))
     feat_host = torch.from_numpy(np.ascontiguousarray(images.T)).pin_memory()
     out_host = torch.empty((10, S), dtype=torch.float64).pin_memory()
+    if os.environ.get("PROBE_NOGC"):
+        import gc
+
+        gc.disable()
     if os.environ.get("PROBE_MODE") == "bench":   # bench.py's order: resident phase, release, e2e without syncs
         from paper_2604_16834_b200.packing import pack_features
 
