@@ -53,6 +53,17 @@ struct Job {
 enum { L_DIRECT = 0, L_BCONV = 1, L_CENTER = 2, L_BCONV_FP = 3, L_BCONV_FPW = 4 };  // FPW: wide sources allowed
 enum { E_STORE = 0, E_SUBSCALE = 1 };
 
+// 8-byte cp.async (global -> shared, no register staging) and its group fences
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
 // ---------------------------------------------------------------- forward pass 1 (columns)
 template <int LD>
 __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs, const uint64_t *tw,
@@ -175,10 +186,14 @@ __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs,
 }
 
 // ---------------------------------------------------------------- forward pass 2 (rows)
+// E_SUBSCALE: the epilogue operands (aux, and aux2 or add) stream into shared
+// memory with cp.async while the NTT phases run (dynamic smem [2][16][256]):
+// each thread prefetches exactly the 16 + 16 words it will consume.
 template <int EP>
 __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs, const uint64_t *tw,
                                                   const double *twd, const ModConst *mc) {
     __shared__ uint64_t sm[16 * 272];
+    extern __shared__ uint64_t pre[];
     const Job jb = jobs[blockIdx.x >> 4];
     const ModConst c = mc[jb.mod];
     const ulonglong2 *W2 = tw_fwd(tw, jb.mod, LOGN);
@@ -186,6 +201,16 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
     const uint32_t r = (blockIdx.x & 15) * 16 + rl;
     uint64_t *row = jb.dst + r * 256;
     uint64_t *s = sm + rl * 272;
+    const uint64_t *second = jb.aux2 ? jb.aux2 : jb.add;
+    uint64_t *pa = pre + rl * 256, *pb = pre + 4096 + rl * 256;
+    if (EP == E_SUBSCALE) {
+#pragma unroll
+        for (int j = 0; j < 16; j++) cp_async8(pa + g + 16 * j, jb.aux + r * 256 + g + 16 * j);
+        if (second)
+#pragma unroll
+            for (int j = 0; j < 16; j++) cp_async8(pb + g + 16 * j, second + r * 256 + g + 16 * j);
+        cp_async_commit();
+    }
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
@@ -227,6 +252,7 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
     }
     }
     __syncwarp();
+    if (EP == E_SUBSCALE) cp_async_wait<0>();
 #pragma unroll
     for (int j = 0; j < 16; j++) {
         const int cc = g + 16 * j;
@@ -235,10 +261,10 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
             row[cc] = v;
         } else {
             const size_t idx = r * 256 + cc;
-            uint64_t base = jb.aux[idx];
-            if (jb.aux2) base = add_mod(base, shoup(jb.aux2[idx], jb.c2, jb.c2p, c.q), c.q);
+            uint64_t base = pa[cc];
+            if (jb.aux2) base = add_mod(base, shoup(pb[cc], jb.c2, jb.c2p, c.q), c.q);
             uint64_t y = shoup(sub_mod(base, v, c.q), jb.cw, jb.cwp, c.q);
-            if (jb.add) y = add_mod(y, jb.add[idx], c.q);
+            if (jb.add) y = add_mod(y, jb.aux2 ? jb.add[idx] : pb[cc], c.q);
             jb.out[idx] = y;
         }
     }
@@ -250,15 +276,6 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
 // with stride gridDim.x and keeps KS tiles in flight with cp.async (8-byte
 // copies straight into the padded shared layout, no register staging), so a
 // CTA computes one tile while the next ones stream in.
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N));
-}
 
 constexpr int KS = 3;            // tiles in flight per CTA
 constexpr int TILE_W = 16 * 272;  // padded words per 16-row tile
@@ -598,7 +615,14 @@ int run_forward(he_ctx *c, const std::vector<Job> &jobs_in, cudaStream_t s) {
                                                                           c->d_rinvd);
         HE_CHECK_LAUNCH();
     }
-    kf_rows<EP><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
+    const size_t pre_bytes = EP == E_SUBSCALE ? (size_t)2 * 4096 * sizeof(uint64_t) : 0;
+    static bool attr = false;
+    if (EP == E_SUBSCALE && !attr) {
+        HE_CHECK_CUDA(cudaFuncSetAttribute(kf_rows<E_SUBSCALE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)pre_bytes));
+        attr = true;
+    }
+    kf_rows<EP><<<(unsigned)jobs.size() * 16, NTT_TPB, pre_bytes, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
