@@ -31,7 +31,7 @@
 // registers for the whole kernel.
 #include <algorithm>
 
-#include "common.cuh"
+#include "ntt_core.cuh"  // u2d / d2u / fmulmod / fcanon (FP64 modular products)
 
 namespace {
 
@@ -151,6 +151,60 @@ __device__ __forceinline__ void digit_plane(const uint32_t *X, const int (&o0)[K
     }
 }
 
+// Window sums of the squares (y0^2, y0 y1, y1^2) of y = conv * R^-1.
+// 40-bit primes (NB = 5): exact FP64 modular products accumulated as doubles
+// (|sum| < 2q per product, folded every 64), which moves the squares to the FP64
+// pipe while the integer pipe recombines; wider primes: exact 128-bit sums.
+// value(k) returns the canonical sum in the plain domain (times R^2, or R^4
+// after the 128-bit path's extra Montgomery step).
+template <bool FP>
+struct SqAcc;
+template <>
+struct SqAcc<true> {
+    double a[3] = {0.0, 0.0, 0.0};
+    int n = 0;
+    __device__ __forceinline__ void add(uint64_t y0, uint64_t y1, const ModConst &c) {
+        const double d0 = u2d(y0), d1 = u2d(y1);
+        a[0] += fmulmod(d0, d0, c.qd, c.qid);
+        a[1] += fmulmod(d0, d1, c.qd, c.qid);
+        a[2] += fmulmod(d1, d1, c.qd, c.qid);
+        if (++n == 64) {
+            n = 0;
+#pragma unroll
+            for (int k = 0; k < 3; k++) a[k] = u2d(fcanon(a[k], c.qd, c.qid));
+        }
+    }
+    __device__ __forceinline__ uint64_t value(int k, const ModConst &c, uint64_t) const {
+        const double r2 = u2d(c.r2);  // R^2 mod q
+        return fcanon(fmulmod(u2d(fcanon(a[k], c.qd, c.qid)), r2, c.qd, c.qid), c.qd, c.qid);
+    }
+    __device__ __forceinline__ void reset() { a[0] = a[1] = a[2] = 0.0; n = 0; }
+};
+template <>
+struct SqAcc<false> {
+    u128 a[3] = {{0, 0}, {0, 0}, {0, 0}};
+    int n = 0;
+    __device__ __forceinline__ void add(uint64_t y0, uint64_t y1, const ModConst &c) {
+        mac128(a[0], y0, y0);
+        mac128(a[1], y0, y1);
+        mac128(a[2], y1, y1);
+        if (++n == 8) {  // each product adds < q/16 to hi: fold every 8
+            n = 0;
+#pragma unroll
+            for (int k = 0; k < 3; k++)
+                if (a[k].hi >= c.q) a[k].hi -= c.q;
+        }
+    }
+    __device__ __forceinline__ uint64_t value(int k, const ModConst &c, uint64_t r4) const {
+        const uint64_t hi = a[k].hi >= c.q ? a[k].hi - c.q : a[k].hi;
+        return mont(redc(hi, a[k].lo, c.q, c.qinv), r4, c);  // sum R^-3 -> plain
+    }
+    __device__ __forceinline__ void reset() {
+        a[0] = a[1] = a[2] = u128{0, 0};
+        n = 0;
+    }
+};
+
 template <int KB, int E, int MG, int NB>
 __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs a) {
     constexpr int PS = 4 / MG;
@@ -201,10 +255,7 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
     }
     __syncthreads();
 
-    u128 acc[3][2];  // window sums of (y R^-1)(y' R^-1), exact 128-bit (hi kept < 2q)
-#pragma unroll
-    for (int k = 0; k < 3; k++) acc[k][0] = acc[k][1] = u128{0, 0};
-    int cnt = 0;  // products accumulated since the last fold
+    SqAcc<NB == 5> acc[2];  // window sums for this lane's two channels
     const int rows_per_blk = a.pool ? 2 : 1;
     for (int yb = a.y0; yb < a.y1; yb += rows_per_blk) {
         // ring-row bases of the input rows yb - 1 .. yb + 2
@@ -262,20 +313,7 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
                     yv[q] = redc(hic, lo, c.q, c.qinv);  // conv * R^-1
                 }
 #pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const uint64_t y0 = add_mod(yv[h], bias[h], c.q), y1 = yv[2 + h];
-                    mac128(acc[0][h], y0, y0);
-                    mac128(acc[1][h], y0, y1);
-                    mac128(acc[2][h], y1, y1);
-                }
-                if (++cnt == 8) {  // each product adds < q/16 to hi: fold every 8 products
-                    cnt = 0;
-#pragma unroll
-                    for (int kk = 0; kk < 3; kk++)
-#pragma unroll
-                        for (int h = 0; h < 2; h++)
-                            if (acc[kk][h].hi >= c.q) acc[kk][h].hi -= c.q;
-                }
+                for (int h = 0; h < 2; h++) acc[h].add(add_mod(yv[h], bias[h], c.q), yv[2 + h], c);
             }
             if (a.pool) {  // window complete
                 const uint64_t r4 = a.r4[l], cst = a.cst ? a.cst[l] : 0;
@@ -287,18 +325,14 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
                         uint64_t *o = a.out[(size_t)m * a.nwin + win] + coff + gid;
 #pragma unroll
                         for (int k = 0; k < 3; k++) {
-                            const uint64_t hi = acc[k][h].hi >= c.q ? acc[k][h].hi - c.q : acc[k][h].hi;
-                            uint64_t r = redc(hi, acc[k][h].lo, c.q, c.qinv);  // sum R^-3
-                            if (k == 1) r = add_mod(r, r, c.q);
-                            uint64_t v = mont(r, r4, c);
+                            uint64_t v = acc[h].value(k, c, r4);
+                            if (k == 1) v = add_mod(v, v, c.q);
                             if (k == 0) v = add_mod(v, cst, c.q);
                             o[((size_t)k * a.ell + l) * N] = v;
                         }
                     }
-#pragma unroll
-                    for (int k = 0; k < 3; k++) acc[k][h] = u128{0, 0};
+                    acc[h].reset();
                 }
-                cnt = 0;
             }
         }
         // slide the ring: the rows of this block's top are no longer needed
@@ -314,13 +348,11 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
     }
     if (!a.pool) {  // global sum: reduce, combine the pixel streams, then store
         uint64_t r[3][2];
+        const uint64_t r4v = a.r4[l];
 #pragma unroll
         for (int k = 0; k < 3; k++)
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const uint64_t hi = acc[k][h].hi >= c.q ? acc[k][h].hi - c.q : acc[k][h].hi;
-                r[k][h] = redc(hi, acc[k][h].lo, c.q, c.qinv);
-            }
+            for (int h = 0; h < 2; h++) r[k][h] = acc[h].value(k, c, r4v);
         uint64_t *red = (uint64_t *)xs;
         if (PS > 1) {
             __syncthreads();
@@ -338,7 +370,7 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
                             r[k][h] = add_mod(r[k][h], red[((o * MG + cg) * 32 + lane) * 6 + k * 2 + h], c.q);
         }
         if (ps == 0) {
-            const uint64_t r4 = a.r4[l], cst = a.cst ? a.cst[l] : 0;
+            const uint64_t cst = a.cst ? a.cst[l] : 0;
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 const int m = m0 + h;
@@ -346,8 +378,7 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
                 uint64_t *o = a.out[m] + coff + gid;
 #pragma unroll
                 for (int k = 0; k < 3; k++) {
-                    const uint64_t rr = k == 1 ? add_mod(r[k][h], r[k][h], c.q) : r[k][h];
-                    uint64_t v = mont(rr, r4, c);
+                    uint64_t v = k == 1 ? add_mod(r[k][h], r[k][h], c.q) : r[k][h];
                     if (k == 0) v = add_mod(v, cst, c.q);
                     o[((size_t)k * a.ell + l) * N] = v;
                 }
