@@ -44,6 +44,7 @@ struct SqArgs {
     const uint64_t *bias;       // [M][ell] bias * R^-1 mod q (component 0), or nullptr
     const uint64_t *cst;        // [ell] constant added to component 0 of every output, or nullptr
     const uint64_t *r4;         // [ell] R^4 mod q
+    const double *yc;           // [ell][2] R^-1 and 2^32 R^-1 mod q as doubles (FP64 recombination)
     const ModConst *mc;
     const int32_t *limbs;       // [gridDim.y] limb handled by blockIdx.y (one byte-plane count per launch)
     int p, H, W, M, ell, logN, pool, y0, y1, nwin;
@@ -163,8 +164,8 @@ template <>
 struct SqAcc<true> {
     double a[3] = {0.0, 0.0, 0.0};
     int n = 0;
-    __device__ __forceinline__ void add(uint64_t y0, uint64_t y1, const ModConst &c) {
-        const double d0 = u2d(y0), d1 = u2d(y1);
+    __device__ __forceinline__ void add(uint64_t y0, uint64_t y1, const ModConst &c) { addd(u2d(y0), u2d(y1), c); }
+    __device__ __forceinline__ void addd(double d0, double d1, const ModConst &c) {  // canonical doubles
         a[0] += fmulmod(d0, d0, c.qd, c.qid);
         a[1] += fmulmod(d0, d1, c.qd, c.qid);
         a[2] += fmulmod(d1, d1, c.qd, c.qid);
@@ -230,6 +231,8 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
         if (m0 < a.M) bias[0] = a.bias[(size_t)m0 * a.ell + l];
         if (m0 + 1 < a.M) bias[1] = a.bias[(size_t)(m0 + 1) * a.ell + l];
     }
+    const double biasd[2] = {u2d(bias[0]), u2d(bias[1])};
+    const double yc0 = a.yc[2 * l], yc1 = a.yc[2 * l + 1];
     // this lane's A words: word w = kb*8 + h*4 + tig -> (tap t, channel group g);
     // words past the 9 taps carry zero weights and read tap 0
     // packed per word: offset inside the ring row (dx * pstr + row position of
@@ -303,17 +306,32 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
                 digit_plane<6, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
                 digit_plane<7, KB, E, NB, DSTR>(xs, o0, o1, bw, W, P, mul);
                 // fragment values: q=0,1 -> component 0, channels m0, m0+1; q=2,3 -> component 1
-                uint64_t yv[4];
+                if constexpr (NB == 5) {
+                    // 40-bit primes: shifts stop at 6, so T = P0 + P1 2^32 with |P0|, |P1| < 2^50;
+                    // y = T R^-1 mod q as two FP64 modular products (exact, see fmulmod)
+                    double yd[4];
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const uint64_t lo = (uint64_t)P[0][q] + ((uint64_t)P[1][q] << 32);
-                    const uint64_t cy = lo < (uint64_t)P[0][q] ? 1 : 0;
-                    const int64_t hi = (P[0][q] >> 63) + (P[1][q] >> 32) + (int64_t)cy + P[2][q];
-                    const uint64_t hic = hi < 0 ? (uint64_t)(hi + (int64_t)c.q) : (uint64_t)hi;  // |hi| < q
-                    yv[q] = redc(hic, lo, c.q, c.qinv);  // conv * R^-1
+                    for (int q = 0; q < 4; q++) {
+                        const double p0 = __longlong_as_double(0x4338000000000000ll + P[0][q]) - 6755399441055744.0;
+                        const double p1 = __longlong_as_double(0x4338000000000000ll + P[1][q]) - 6755399441055744.0;
+                        yd[q] = fmulmod(p0, yc0, c.qd, c.qid) + fmulmod(p1, yc1, c.qd, c.qid);
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; h++)
+                        acc[h].addd(fcanond(yd[h] + biasd[h], c.qd, c.qid), fcanond(yd[2 + h], c.qd, c.qid), c);
+                } else {
+                    uint64_t yv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const uint64_t lo = (uint64_t)P[0][q] + ((uint64_t)P[1][q] << 32);
+                        const uint64_t cy = lo < (uint64_t)P[0][q] ? 1 : 0;
+                        const int64_t hi = (P[0][q] >> 63) + (P[1][q] >> 32) + (int64_t)cy + P[2][q];
+                        const uint64_t hic = hi < 0 ? (uint64_t)(hi + (int64_t)c.q) : (uint64_t)hi;  // |hi| < q
+                        yv[q] = redc(hic, lo, c.q, c.qinv);  // conv * R^-1
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; h++) acc[h].add(add_mod(yv[h], bias[h], c.q), yv[2 + h], c);
                 }
-#pragma unroll
-                for (int h = 0; h < 2; h++) acc[h].add(add_mod(yv[h], bias[h], c.q), yv[2 + h], c);
             }
             if (a.pool) {  // window complete
                 const uint64_t r4 = a.r4[l], cst = a.cst ? a.cst[l] : 0;
@@ -506,12 +524,16 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
                         bf[((((size_t)cg * KB + kb) * E + e) * 32 + lane) * 2 + r] = reg;
                     }
                 }
-    // per-limb constants: R^4, bias * R^-1
+    // per-limb constants: R^4, bias * R^-1, and R^-1, 2^32 R^-1 as doubles
     std::vector<uint64_t> r4(ell), bres(bias ? (size_t)M * ell : 0);
+    std::vector<double> yc(2 * (size_t)ell);
     for (int l = 0; l < ell; l++) {
         const uint64_t q = c->mod[l], Rm = (uint64_t)(((unsigned __int128)1 << 64) % q);
         const uint64_t R2 = he_h_mulmod(Rm, Rm, q);
         r4[l] = he_h_mulmod(R2, R2, q);
+        const uint64_t Ri = he_h_inv(Rm, q);
+        yc[2 * l] = (double)Ri;
+        yc[2 * l + 1] = (double)he_h_mulmod(Ri, ((uint64_t)1 << 32) % q, q);
         if (cst && cst[l] >= q) {
             he_set_error("he_conv_square_sum: residue not canonical");
             return HE_EINVAL;
@@ -548,9 +570,9 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
     HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
     HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
     const size_t b_bf = bf.size() * 4, b_lo = lorder.size() * 4, b_r4 = (size_t)ell * 8, b_b = bres.size() * 8,
-                 b_c = cst ? (size_t)ell * 8 : 0;
+                 b_c = cst ? (size_t)ell * 8 : 0, b_yc = yc.size() * 8;
     char *meta = nullptr;
-    HE_TRY(he_scratch_alloc((void **)&meta, b_bf + b_lo + b_r4 + b_b + b_c + 128, s));
+    HE_TRY(he_scratch_alloc((void **)&meta, b_bf + b_lo + b_r4 + b_b + b_c + b_yc + 160, s));
     size_t off = 0;
     auto carve = [&](size_t bytes) {
         char *p = meta + off;
@@ -562,6 +584,8 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
     uint64_t *dr4 = (uint64_t *)carve(b_r4);
     uint64_t *db = bias ? (uint64_t *)carve(b_b) : nullptr;
     uint64_t *dc = cst ? (uint64_t *)carve(b_c) : nullptr;
+    double *dyc = (double *)carve(b_yc);
+    HE_CHECK_CUDA(he_h2d(dyc, yc.data(), b_yc, s));
     HE_CHECK_CUDA(he_h2d(dbf, bf.data(), b_bf, s));
     HE_CHECK_CUDA(he_h2d(dlo, lorder.data(), b_lo, s));
     HE_CHECK_CUDA(he_h2d(dr4, r4.data(), b_r4, s));
@@ -574,6 +598,7 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
     a.bias = db;
     a.cst = dc;
     a.r4 = dr4;
+    a.yc = dyc;
     a.mc = c->d_mc;
     a.p = p;
     a.H = H;

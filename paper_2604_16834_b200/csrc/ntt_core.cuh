@@ -106,6 +106,13 @@ __device__ __forceinline__ double fmulmod(double a, double w, double q, double q
     const double e = rint(h * qi);
     return fma(-e, q, h) + l;
 }
+// exact integer |x| < 2^52 -> canonical residue (as an integer-valued double)
+__device__ __forceinline__ double fcanond(double x, double q, double qi) {
+    const double e = floor(x * qi);
+    double r = fma(-e, q, x);
+    r = r < 0.0 ? r + q : r;
+    return r >= q ? r - q : r;
+}
 // exact integer |x| < 2^52 -> canonical residue as uint64
 __device__ __forceinline__ uint64_t fcanon(double x, double q, double qi) {
     const double e = floor(x * qi);
