@@ -46,7 +46,7 @@ def cfg3_op_counts():
 def measure(seconds_budget: float = 20.0, threads: int | None = None, seed: int = 0) -> dict:
     """Time the oracle on a bounded sample; returns samples/s for one 32768-sample group."""
     threads = threads or len(os.sched_getaffinity(0))
-    orc = O.Oracle(16, [60] + [40] * 13, [60] * 3, 3, seed=seed, scale=2.0 ** 40)
+    orc = O.Oracle(16, [40] * 14, [42] * 3, 3, seed=seed, scale=2.0 ** 40)
     rng = np.random.default_rng(seed)
     N = orc.N
     mods = orc.moduli

@@ -3,7 +3,9 @@
 Appendix decisions of SURVEY.md (recorded in DESIGN.md section 3):
   * config 1: Q = 60 + 4x40 bits, P = 1x60, key_switch_digits 5 (alpha = 1),
     bootstrap_reserve = 1 (the reference default 10 violates 0 < r < max_level).
-  * config 3: Q = 60 + 13x40, P = 3x60, digits 5 (alpha = 3), scale 2^40.
+  * config 3: Q = 14x40, P = 3x42, digits 5 (alpha = 3), scale 2^40: every prime
+    below 2^42, so every NTT / BConv / inner product runs on the FP64 path
+    (DESIGN.md section 3); P = 2^126 exceeds every 3-limb digit (2^120).
   * configs 2 and 4: Q = 24x50, P = 4x50, digits 6 (alpha = 4), scale 2^50.
   * config 4 head: GAP then dense 64 -> 10.  Biases: zero everywhere.
 """
@@ -24,8 +26,8 @@ def context(cfg: int, seed: int = 0, device: int = 0) -> EngineContext:
                              key_switch_digits=6, noise_seed=seed, special_prime_bits=(50,) * 4, scale_bits=50,
                              device=device)
     if cfg in (3, 5):
-        return EngineContext(n=32768, max_level=13, bootstrap_reserve=1, first_modulus_bits=60, rescale_bits=40,
-                             key_switch_digits=5, noise_seed=seed, special_prime_bits=(60,) * 3, scale_bits=40,
+        return EngineContext(n=32768, max_level=13, bootstrap_reserve=1, first_modulus_bits=40, rescale_bits=40,
+                             key_switch_digits=5, noise_seed=seed, special_prime_bits=(42,) * 3, scale_bits=40,
                              device=device)
     raise ValueError(f"unknown config {cfg}")
 

@@ -9,7 +9,7 @@ PARAMS = {
     "tiny": (5, (60, 40, 40, 40), (60, 60), 2, 40),
     "cfg1": (12, (60, 40, 40, 40, 40), (60,), 1, 40),
     "cfg2": (16, (50,) * 24, (50,) * 4, 4, 50),
-    "cfg3": (16, (60,) + (40,) * 13, (60,) * 3, 3, 40),
+    "cfg3": (16, (40,) * 14, (42,) * 3, 3, 40),
     "cfg4": (16, (50,) * 24, (50,) * 4, 4, 50),
     # config 4's prime sizes on a small ring (degree-3 CNN tests on one GPU)
     "cfg4s": (12, (50,) * 10, (50,) * 2, 2, 50),

@@ -80,7 +80,7 @@ def test_engine_context_validation_matches_reference():
     with pytest.raises(ValueError):
         EngineContext(n=8, max_level=4, bootstrap_reserve=1, mult_level_cost=0)
     c = configs.context(3)
-    assert (c.ring_degree, c.n_q, c.alpha, c.q_chain_bits[:2], c.p_chain_bits) == (65536, 14, 3, (60, 40), (60,) * 3)
+    assert (c.ring_degree, c.n_q, c.alpha, c.q_chain_bits[:2], c.p_chain_bits) == (65536, 14, 3, (40, 40), (42,) * 3)
     c1 = configs.context(1)
     assert (c1.n_q, c1.alpha, c1.p_chain_bits, c1.scale) == (5, 1, (60,), 2.0 ** 40)
     c2 = configs.context(2)
