@@ -273,11 +273,16 @@ def main():
     # the key switch is integer-pipe bound: its second roofline is algorithmic modular
     # multiplications (NTT butterflies + BConv + inner product) against the
     # measured 64x64->128 multiply-accumulate rate of this GPU (he_microbench_intpipe)
-    ip = np.zeros(2)
+    ip, fp = np.zeros(2), np.zeros(1)
     _lib.check(_lib.load().he_microbench_intpipe(local, ip.ctypes.data), "microbench")
+    _lib.check(_lib.load().he_microbench_fp64(local, fp.ctypes.data), "microbench")
+    # config 3's primes are all below 2^42, so the key switch multiplies on the FP64
+    # datapath: the peak is the faster of the two measured modular-product rates
+    peak_mm = max(float(ip[1]), float(fp[0]))
     int_ach = units[1] / (dom_ms / 1e3)
-    int_roof = {"achieved": int_ach, "peak": float(ip[1]), "unit": "modmul/s", "frac": int_ach / float(ip[1]),
-                "peak_source": "measured mac128/s (he_microbench_intpipe)", "imad32_per_s": float(ip[0])}
+    int_roof = {"achieved": int_ach, "peak": peak_mm, "unit": "modmul/s", "frac": int_ach / peak_mm,
+                "peak_source": "measured: max(64x64->128 MAC/s, FP64 modular products/s) (he_microbench_*)",
+                "mac128_per_s": float(ip[1]), "fp64_modmul_per_s": float(fp[0]), "imad32_per_s": float(ip[0])}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

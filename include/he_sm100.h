@@ -210,6 +210,9 @@ unsigned long long he_launch_count(void);
 /* integer-pipe peak on `device`: ops_per_s[0] = 32-bit IMAD/s,
  * ops_per_s[1] = 64x64->128 multiply-accumulates/s (roofline denominators) */
 int he_microbench_intpipe(int device, double *ops_per_s);
+/* FP64 modular products per second (the a*w mod q form of the < 2^42 prime
+ * datapath, ntt_core.cuh fmulmod): the key switch's second roofline peak. */
+int he_microbench_fp64(int device, double *modmul_per_s);
 
 #ifdef __cplusplus
 }

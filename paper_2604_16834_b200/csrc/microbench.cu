@@ -5,7 +5,7 @@
 // engine measures the pipe it runs on: independent 32-bit IMAD chains
 // (8 per thread, full grid) and the 64x64->128 multiply-accumulate the
 // kernels use (mad.lo.cc.u64 + madc.hi.u64).
-#include "common.cuh"
+#include "ntt_core.cuh"  // fmulmod: the FP64 modular product of the < 2^42 prime path
 
 namespace {
 
@@ -36,7 +36,53 @@ __global__ void k_mac128(uint64_t *sink, int iters, uint64_t seed) {
     if (s == 0x123456789ull) sink[0] = s;
 }
 
+// FP64 modular products (fmulmod, the key-switch / NTT datapath for primes
+// below 2^42): 8 independent chains per thread on a 40-bit prime
+__global__ void k_fmulmod(double *sink, int iters, double q, double w) {
+    const double qi = 1.0 / q;
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = (double)(threadIdx.x * 8 + k + blockIdx.x);
+    for (int i = 0; i < iters; i++)
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const double r = fmulmod(x[k], w, q, qi);
+            x[k] = r < 0.0 ? r + q : r;
+        }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) s += x[k];
+    if (s == 12345.0) sink[0] = s;
+}
+
 }  // namespace
+
+// FP64 modular products per second (fmulmod on a 40-bit prime, full grid)
+extern "C" int he_microbench_fp64(int device, double *modmul_per_s) {
+    HE_CHECK_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    HE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    void *sink;
+    HE_CHECK_CUDA(cudaMalloc(&sink, 64));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    float ms = 0;
+    for (int rep = 0; rep < 2; rep++) {
+        cudaEventRecord(e0);
+        k_fmulmod<<<blocks, threads>>>((double *)sink, iters, 1099511480321.0, 123456789012.0);
+        cudaEventRecord(e1);
+        HE_CHECK_CUDA(cudaEventSynchronize(e1));
+    }
+    cudaEventElapsedTime(&ms, e0, e1);
+    *modmul_per_s = (double)blocks * threads * iters * 8 / (ms * 1e-3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
 
 // ops_per_s[0] = 32-bit IMAD/s, ops_per_s[1] = 64x64->128 MAC/s (blocking)
 extern "C" int he_microbench_intpipe(int device, double *ops_per_s) {
