@@ -296,7 +296,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64 (RNS residues mod 40/60-bit primes)",
+            "vs_baseline": None, "dtype": "u64 (RNS residues mod 40/42-bit primes; FP64-exact modular products)",
             "data": "synthetic (seeded U[0,1] CIFAR-shaped images, N(0,1/fan_in) weights)",
             "config": _config(world),
             "e2e": {"value": e2e, "unit": "samples/s", "steps": e2e_steps,

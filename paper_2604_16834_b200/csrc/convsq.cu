@@ -44,7 +44,7 @@ struct SqArgs {
     const uint64_t *bias;       // [M][ell] bias * R^-1 mod q (component 0), or nullptr
     const uint64_t *cst;        // [ell] constant added to component 0 of every output, or nullptr
     const uint64_t *r4;         // [ell] R^4 mod q
-    const double *yc;           // [ell][2] R^-1 and 2^32 R^-1 mod q as doubles (FP64 recombination)
+    const double *yc;           // [ell][2] R mod q and 2^32 mod q as doubles (FP64 recombination)
     const ModConst *mc;
     const int32_t *limbs;       // [gridDim.y] limb handled by blockIdx.y (one byte-plane count per launch)
     int p, H, W, M, ell, logN, pool, y0, y1, nwin;
@@ -176,8 +176,7 @@ struct SqAcc<true> {
         }
     }
     __device__ __forceinline__ uint64_t value(int k, const ModConst &c, uint64_t) const {
-        const double r2 = u2d(c.r2);  // R^2 mod q
-        return fcanon(fmulmod(u2d(fcanon(a[k], c.qd, c.qid)), r2, c.qd, c.qid), c.qd, c.qid);
+        return fcanon(a[k], c.qd, c.qid);  // the FP path squares the plain conv value
     }
     __device__ __forceinline__ void reset() { a[0] = a[1] = a[2] = 0.0; n = 0; }
 };
@@ -231,8 +230,10 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
         if (m0 < a.M) bias[0] = a.bias[(size_t)m0 * a.ell + l];
         if (m0 + 1 < a.M) bias[1] = a.bias[(size_t)(m0 + 1) * a.ell + l];
     }
-    const double biasd[2] = {u2d(bias[0]), u2d(bias[1])};
+    // FP path: plain-domain bias (bias R^-1 * R) and 2^32 mod q
     const double yc0 = a.yc[2 * l], yc1 = a.yc[2 * l + 1];
+    const double biasd[2] = {fcanond(fmulmod(u2d(bias[0]), yc0, c.qd, c.qid), c.qd, c.qid),
+                             fcanond(fmulmod(u2d(bias[1]), yc0, c.qd, c.qid), c.qd, c.qid)};
     // this lane's A words: word w = kb*8 + h*4 + tig -> (tap t, channel group g);
     // words past the 9 taps carry zero weights and read tap 0
     // packed per word: offset inside the ring row (dx * pstr + row position of
@@ -308,13 +309,14 @@ __global__ void __launch_bounds__(CT, KB <= 2 ? 4 : 3) k_conv_sqsum(const SqArgs
                 // fragment values: q=0,1 -> component 0, channels m0, m0+1; q=2,3 -> component 1
                 if constexpr (NB == 5) {
                     // 40-bit primes: shifts stop at 6, so T = P0 + P1 2^32 with |P0|, |P1| < 2^50;
-                    // y = T R^-1 mod q as two FP64 modular products (exact, see fmulmod)
+                    // y = T mod q with one FP64 modular product (exact, see fmulmod); the
+                    // squares are taken of the plain value (no Montgomery factor on this path)
                     double yd[4];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
                         const double p0 = __longlong_as_double(0x4338000000000000ll + P[0][q]) - 6755399441055744.0;
                         const double p1 = __longlong_as_double(0x4338000000000000ll + P[1][q]) - 6755399441055744.0;
-                        yd[q] = fmulmod(p0, yc0, c.qd, c.qid) + fmulmod(p1, yc1, c.qd, c.qid);
+                        yd[q] = p0 + fmulmod(p1, yc1, c.qd, c.qid);  // T = P0 + P1 2^32 (mod q), |T'| < 2^51
                     }
 #pragma unroll
                     for (int h = 0; h < 2; h++)
@@ -532,8 +534,9 @@ extern "C" int he_conv_square_sum(he_ctx *c, const uint64_t *const *in, int p, i
         const uint64_t R2 = he_h_mulmod(Rm, Rm, q);
         r4[l] = he_h_mulmod(R2, R2, q);
         const uint64_t Ri = he_h_inv(Rm, q);
-        yc[2 * l] = (double)Ri;
-        yc[2 * l + 1] = (double)he_h_mulmod(Ri, ((uint64_t)1 << 32) % q, q);
+        yc[2 * l] = (double)Rm;                          // R mod q: bias R^-1 -> plain
+        yc[2 * l + 1] = (double)(((uint64_t)1 << 32) % q);  // 2^32 mod q
+        (void)Ri;
         if (cst && cst[l] >= q) {
             he_set_error("he_conv_square_sum: residue not canonical");
             return HE_EINVAL;
