@@ -249,6 +249,20 @@ extern "C" int he_encrypt(he_ctx *c, const double *vals, int count, int nvals, d
     Buf ptrs(s), map(s);
     HE_TRY(he_upload_ptrs((const void *const *)out, count, (void ***)&ptrs.p, s));
     uint64_t *const *op = (uint64_t *const *)ptrs.p;
+    if (c->logN == 16) {  // fused encode -> NTT -> encrypt (encrypt16.cu)
+        const size_t n = c->nslots;
+        Buf f(s);
+        HE_TRY(he_scratch_alloc(&f.p, (size_t)count * n * 16, s));
+        double *re = (double *)f.p, *im = re + (size_t)count * n;
+        HE_CHECK_CUDA(cudaMemsetAsync(re, 0, (size_t)count * n * 16, s));
+        if (nvals > 0) {
+            k_scatter_slots2<<<gridn((size_t)count * nvals), EW, 0, s>>>(re, vals, count, nvals, (int)n,
+                                                                         c->d_slot_brv);
+            HE_CHECK_LAUNCH();
+        }
+        HE_TRY(run_fft(c, re, im, count, -1, s));
+        return he_encrypt16(c, re, im, count, scale, ct_index0, op, s);
+    }
     HE_TRY(encode_into(c, vals, count, nvals, scale, op, c->L, 1, ct_index0, s));
     std::vector<uint8_t> m(2 * (size_t)c->L, 0xFF);
     for (int l = 0; l < c->L; l++) m[l] = (uint8_t)l;

@@ -45,10 +45,7 @@ __global__ void k_fmulmod(double *sink, int iters, double q, double w) {
     for (int k = 0; k < 8; k++) x[k] = (double)(threadIdx.x * 8 + k + blockIdx.x);
     for (int i = 0; i < iters; i++)
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            const double r = fmulmod(x[k], w, q, qi);
-            x[k] = r < 0.0 ? r + q : r;
-        }
+        for (int k = 0; k < 8; k++) x[k] = fmulmod(x[k], w, q, qi);  // lazy: |x| < 3q stays exact
     double s = 0;
 #pragma unroll
     for (int k = 0; k < 8; k++) s += x[k];
