@@ -71,8 +71,9 @@ int he_ctx_create(const he_params *p, int device, he_ctx **out);
 int he_ctx_destroy(he_ctx *ctx);
 int he_ctx_moduli(const he_ctx *ctx, uint64_t *moduli /* L+K */, uint64_t *psi /* L+K */);
 
-/* keys.  galois_elt 0 = relinearisation key (s^2); otherwise the key for
- * X -> X^galois_elt.  Replaces register_rotation_keys / unload_rotation_keys
+/* keys.  galois_elt 0 = relinearisation key (s^2); 2 and 4 = the power keys
+ * s^3, s^4 of 5-component relinearisation (he_relin_rescale_n); odd values =
+ * the key for X -> X^galois_elt.  Replaces register_rotation_keys / unload_rotation_keys
  * (engine.py:343-354; RotationKeySet engine.py:93-136). */
 int he_gen_switch_key(he_ctx *ctx, uint32_t galois_elt, void *stream);
 int he_drop_switch_key(he_ctx *ctx, uint32_t galois_elt);
@@ -135,6 +136,14 @@ int he_relin(he_ctx *ctx, const uint64_t *const *d3, uint64_t *const *out, int c
  * N = 2^16 only, HE_EINVAL otherwise; extra in [0, min(ell-1, 8)]). */
 int he_relin_rescale(he_ctx *ctx, const uint64_t *const *d3, uint64_t *const *out, int count, int ell,
                      int extra, void *stream);
+/* nc-component form (nc = 3 or 5): component k >= 2 is key-switched with the
+ * s^k key (codes 0, 2, 4; he_gen_switch_key) and the inner products are summed
+ * before the one joint ModDown: [nc][ell][N] -> [2][ell-extra][N].  Lets a
+ * degree-2 activation's 3-component output feed the next linear layer
+ * unrelinearised; the squares of that layer (5 components) are relinearised
+ * once after the global sum (featuremajor.run_cnn). */
+int he_relin_rescale_n(he_ctx *ctx, const uint64_t *const *d, uint64_t *const *out, int count, int ell,
+                       int extra, int nc, void *stream);
 int he_keyswitch(he_ctx *ctx, uint32_t galois_elt, const uint64_t *const *d, uint64_t *const *out0,
                  uint64_t *const *out1, int count, int ell, void *stream);
 int he_rescale(he_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int ell,
@@ -202,6 +211,13 @@ int he_square_sum(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *co
 int he_conv_square_sum(he_ctx *ctx, const uint64_t *const *in, int p, int H, int W, uint64_t *const *out, int M,
                        int pool, int y0, int y1, const int64_t *weights, const uint64_t *bias,
                        const uint64_t *cst, int ell, void *stream);
+/* the same with nci = 2 or 3 input components: 3-component inputs (the
+ * unrelinearised squares of the previous block) give 5-component outputs
+ * (y0^2, 2 y0 y1, 2 y0 y2 + y1^2, 2 y1 y2, y2^2) summed, relinearised later
+ * by he_relin_rescale_n; needs even W (pixel pairs share a tensor-core tile). */
+int he_conv_square_sum_n(he_ctx *ctx, const uint64_t *const *in, int nci, int p, int H, int W,
+                         uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
+                         const uint64_t *bias, const uint64_t *cst, int ell, void *stream);
 
 /* block until all work on `stream` is done; returns HE_ECUDA on async error */
 int he_sync(void *stream);

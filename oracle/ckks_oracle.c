@@ -416,12 +416,19 @@ static uint64_t prod_p_mod(const oc_ctx *c, uint64_t q) {
 void oc_gen_switch_key(const oc_ctx *c, uint32_t g, uint64_t *key) {
     int N = c->N, L = c->L, K = c->K, total = L + K;
     size_t poly = N, comp = (size_t)total * N;
-    /* s' = s^2 (relin) or sigma_g(s) (galois), NTT domain per modulus */
+    /* s' = s^2 (g = 0, relin), s^(g/2+2) (even g: the power keys of 5-component
+     * relinearisation, s^3 at g = 2, s^4 at g = 4) or sigma_g(s) (odd g, galois),
+     * NTT domain per modulus */
     uint64_t *sp = (uint64_t *)malloc(8 * comp);
     for (int m = 0; m < L; m++) {
         const uint64_t *s = c->sk + (size_t)m * N;
-        if (g == 0) {
-            for (int k = 0; k < N; k++) sp[m * poly + k] = mulmod(s[k], s[k], c->mod[m]);
+        if (g % 2 == 0) {
+            const int power = g == 0 ? 2 : (int)(g / 2) + 2;
+            for (int k = 0; k < N; k++) {
+                uint64_t v = s[k];
+                for (int e = 1; e < power; e++) v = mulmod(v, s[k], c->mod[m]);
+                sp[m * poly + k] = v;
+            }
         } else {
             automorph_poly(c, s, g, sp + m * poly);
         }
@@ -587,6 +594,24 @@ void oc_tensor(const oc_ctx *c, const uint64_t *a, const uint64_t *b, uint64_t *
     }
 }
 
+/* square of an nc-component ciphertext: out_k = sum_{i+j=k} a_i a_j, 2nc-1 components */
+void oc_tensor_sq(const oc_ctx *c, const uint64_t *a, int nc, uint64_t *out, int ell) {
+    size_t N = c->N, P = (size_t)ell * N;
+    for (int k = 0; k < 2 * nc - 1; k++)
+        for (int i = 0; i < ell; i++) {
+            uint64_t q = c->mod[i];
+            for (size_t x = i * N; x < (i + 1) * N; x++) {
+                uint64_t v = 0;
+                for (int u = 0; u < nc; u++) {
+                    const int w = k - u;
+                    if (w < 0 || w >= nc) continue;
+                    v = addmod(v, mulmod(a[u * P + x], a[w * P + x], q), q);
+                }
+                out[k * P + x] = v;
+            }
+        }
+}
+
 /* fast basis conversion of coefficient-domain limbs src (moduli sidx[0..ns))
  * to target modulus tq: y = sum_s [x_s * qhat_s^-1]_{q_s} * (qhat_s mod tq) mod tq */
 static void bconv(const oc_ctx *c, const uint64_t *const *src, const int *sidx, int ns, uint64_t tq,
@@ -664,9 +689,31 @@ static uint64_t *ks_inner(const oc_ctx *c, const uint64_t *d, const uint64_t *ke
  *   out_c[i] = (X_c[i] - NTT_i(BConv_{S -> q_i}(y))) * (prod S)^-1,  i < ell - extra.
  * d3 [3][ell][N] -> out [2][ell-extra][N]. */
 void oc_relin_rescale(const oc_ctx *c, const uint64_t *d3, const uint64_t *key, uint64_t *out, int ell, int extra) {
+    const uint64_t *keys[1] = {key};
+    oc_relin_rescale_n(c, d3, 3, keys, out, ell, extra);
+}
+
+/* nc-component form (nc = 3 or 5): component k >= 2 is key-switched with
+ * keys[k-2] (the s^k key) and the inner products are summed in the extended
+ * basis before the one joint ModDown:  acc = sum_k ks_inner(d_k, keys[k-2]). */
+void oc_relin_rescale_n(const oc_ctx *c, const uint64_t *d3, int nc, const uint64_t *const *keys, uint64_t *out,
+                        int ell, int extra) {
     int N = c->N, L = c->L, K = c->K, ext = ell + K, lo = ell - extra;
     size_t P = (size_t)ell * N;
-    uint64_t *acc = ks_inner(c, d3 + 2 * P, key, ell);
+    uint64_t *acc = ks_inner(c, d3 + 2 * P, keys[0], ell);
+    for (int k = 3; k < nc; k++) {
+        uint64_t *a2 = ks_inner(c, d3 + (size_t)k * P, keys[k - 2], ell);
+        for (int t = 0; t < ext; t++) {
+            const int m = t < ell ? t : L + (t - ell);
+            const uint64_t q = c->mod[m];
+            for (int cc = 0; cc < 2; cc++) {
+                uint64_t *x = acc + ((size_t)cc * ext + t) * N;
+                const uint64_t *y = a2 + ((size_t)cc * ext + t) * N;
+                for (int j = 0; j < N; j++) x[j] = addmod(x[j], y[j], q);
+            }
+        }
+        free(a2);
+    }
     uint64_t *tmp = (uint64_t *)malloc(8 * (size_t)N);
     for (int cc = 0; cc < 2; cc++) {
         uint64_t *X = acc + (size_t)cc * ext * N;

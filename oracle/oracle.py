@@ -72,6 +72,8 @@ def lib():
         L.oc_keyswitch.argtypes = [vp, u64p, u64p, C.c_int, u64p, u64p]
         L.oc_relin.argtypes = [vp, u64p, u64p, u64p, C.c_int]
         L.oc_relin_rescale.argtypes = [vp, u64p, u64p, u64p, C.c_int, C.c_int]
+        L.oc_relin_rescale_n.argtypes = [vp, u64p, C.c_int, C.POINTER(vp), u64p, C.c_int, C.c_int]
+        L.oc_tensor_sq.argtypes = [vp, u64p, C.c_int, u64p, C.c_int]
         L.oc_rescale.argtypes = [vp, u64p, u64p, C.c_int, C.c_int]
         L.oc_automorphism.argtypes = [vp, u64p, C.c_uint32, u64p, C.c_int]
         L.oc_rotate.argtypes = [vp, u64p, C.c_uint32, u64p, u64p, C.c_int]
@@ -257,6 +259,25 @@ class Oracle:
         lib().oc_relin_rescale(self._h, _u64(np.ascontiguousarray(d3)), _u64(key), _u64(out), ell, extra)
         return out
 
+    def relin_rescale_n(self, d, keys, extra):
+        """nc-component relinearisation (keys[k-2] = switch_key(power code of s^k), see
+        power_key_elt) + `extra` rescales as one joint ModDown (oc_relin_rescale_n)."""
+        d = np.ascontiguousarray(d, dtype=np.uint64)
+        nc, ell = d.shape[0], d.shape[1]
+        assert len(keys) == nc - 2
+        kp = (C.c_void_p * len(keys))(*[k.ctypes.data for k in keys])
+        out = np.zeros((2, ell - extra, self.N), np.uint64)
+        lib().oc_relin_rescale_n(self._h, _u64(d), nc, kp, _u64(out), ell, extra)
+        return out
+
+    def tensor_sq(self, a):
+        """square of an nc-component ciphertext: 2nc-1 components (oc_tensor_sq)."""
+        a = np.ascontiguousarray(a, dtype=np.uint64)
+        nc, ell = a.shape[0], a.shape[1]
+        out = np.zeros((2 * nc - 1, ell, self.N), np.uint64)
+        lib().oc_tensor_sq(self._h, _u64(a), nc, _u64(out), ell)
+        return out
+
     def rescale(self, ct):
         nc, ell = ct.shape[0], ct.shape[1]
         out = np.zeros((nc, ell - 1, self.N), np.uint64)
@@ -293,6 +314,12 @@ class Oracle:
         lib().oc_lincomb(self._h, in_p, out_p, n_out, _p(rp, C.c_int32), _p(cl, C.c_int32),
                          _p(ww, C.c_int64), ell, nc, n_threads)
         return outs
+
+
+def power_key_elt(power: int) -> int:
+    """Key code of the s^power switching key: 0 for s^2 (relinearisation), the even
+    code 2 (power - 2) for s^3, s^4 (never a Galois element, which is odd)."""
+    return 0 if power == 2 else 2 * (power - 2)
 
 
 def galois_elt(k: int, N: int) -> int:

@@ -248,8 +248,9 @@ class PyRef:
                 en = self.ntt([x % q for x in e], m)
                 b = [(x - y * z) % q for x, y, z in zip(en, a, s)]
                 if m < L and j * self.alpha <= m < (j + 1) * self.alpha:
-                    if g == 0:
-                        sp = [x * x % q for x in s]
+                    if g % 2 == 0:  # s^2 (g = 0) or the power key s^(g/2+2)
+                        pw = 2 if g == 0 else g // 2 + 2
+                        sp = [pow(x, pw, q) for x in s]
                     else:
                         sp = self.automorphism(s, g)
                     b = [(x + P * y) % q for x, y in zip(b, sp)]

@@ -33,7 +33,7 @@ EXPORTS = [
     "he_encode_plain", "he_add", "he_sub", "he_add_const", "he_mul_const", "he_mul_plain",
     "he_drop_limbs", "he_tensor", "he_relin", "he_keyswitch", "he_rescale", "he_mult_ct",
     "he_automorphism", "he_rotate", "he_lincomb", "he_sync", "he_launch_count", "he_lincomb_grouped",
-    "he_microbench_intpipe", "he_square_sum", "he_conv_mma", "he_relin_rescale", "he_conv_square_sum",
+    "he_microbench_intpipe", "he_square_sum", "he_conv_mma", "he_relin_rescale", "he_relin_rescale_n", "he_conv_square_sum", "he_conv_square_sum_n",
     "he_microbench_fp64",
 ]
 
@@ -96,6 +96,7 @@ def load():
         "he_tensor": (i, [vp, pp, pp, pp, i, i, vp]),
         "he_relin": (i, [vp, pp, pp, i, i, vp]),
         "he_relin_rescale": (i, [vp, pp, pp, i, i, i, vp]),
+        "he_relin_rescale_n": (i, [vp, pp, pp, i, i, i, i, vp]),
         "he_keyswitch": (i, [vp, u32, pp, pp, pp, i, i, vp]),
         "he_rescale": (i, [vp, pp, pp, i, i, i, vp]),
         "he_mult_ct": (i, [vp, pp, pp, pp, i, i, vp]),
@@ -110,6 +111,7 @@ def load():
         "he_square_sum": (i, [vp, pp, i, pp, i, vp, vp, vp, i, vp]),
         "he_conv_mma": (i, [vp, pp, i, pp, i, i, vp, vp, i, i, i, vp, vp, i, i, vp]),
         "he_conv_square_sum": (i, [vp, pp, i, i, i, pp, i, i, i, i, vp, vp, vp, i, vp]),
+        "he_conv_square_sum_n": (i, [vp, pp, i, i, i, i, pp, i, i, i, i, vp, vp, vp, i, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -249,8 +249,9 @@ void he_scratch_free(void *p, cudaStream_t s);
 int he_get_modup_table(he_ctx *ctx, int ell, int digit, const BconvTable **out);
 int he_get_moddown_table(he_ctx *ctx, int ell, const BconvTable **out);
 int he_get_moddown_table_x(he_ctx *ctx, int ell, int extra, const BconvTable **out);
-int he_relin_rescale_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d3, const uint64_t *const *d2_dev,
-                           int B, int ell, int extra, uint64_t *const *out, cudaStream_t s);
+int he_relin_rescale_fused(he_ctx *c, const uint64_t *const *keys, int nk, const uint64_t *const *d3,
+                           const uint64_t *const *dk_dev, int B, int ell, int extra, uint64_t *const *out,
+                           cudaStream_t s);
 const uint64_t *he_get_key(he_ctx *ctx, uint32_t galois_elt);
 // fused N = 2^16 encryption from the encode FFT output (encrypt16.cu); out_dev: device pointer array
 int he_encrypt16(he_ctx *c, const double *re, const double *im, int count, double scale, uint32_t ct_index0,

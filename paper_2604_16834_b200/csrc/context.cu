@@ -202,11 +202,15 @@ __global__ void k_ksk_final(uint64_t *key, const uint64_t *err, const uint64_t *
     key[base + (size_t)M * N] = aM;
 }
 
-__global__ void k_sk_square(uint64_t *out, const uint64_t *sk, const ModConst *mc, int N, int L) {
+// s^power (NTT domain, Q limbs): the relinearisation target s^2 and the power
+// keys s^3, s^4 of 5-component relinearisation (oracle: oc_gen_switch_key, even g)
+__global__ void k_sk_power(uint64_t *out, const uint64_t *sk, const ModConst *mc, int N, int L, int power) {
     size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (idx >= (size_t)L * N) return;
     int m = (int)(idx / N);
-    out[idx] = mul_mod(sk[idx], sk[idx], mc[m]);
+    uint64_t v = sk[idx];
+    for (int e = 1; e < power; e++) v = mul_mod(v, sk[idx], mc[m]);
+    out[idx] = v;
 }
 
 // X -> X^g in bit-reversed evaluation order: out[k] = in[brv((e*g mod 2N - 1)/2)], e = 2 brv(k) + 1
@@ -538,8 +542,9 @@ const uint64_t *he_get_key(he_ctx *c, uint32_t g) {
 extern "C" int he_gen_switch_key(he_ctx *c, uint32_t g, void *stream) {
     if (!c) return HE_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
-    if (g != 0 && (g % 2 == 0 || g >= 2u * (uint32_t)c->N)) {
-        he_set_error("galois element %u must be odd and < 2N", g);
+    // g = 0: relinearisation key (s^2); even g = 2, 4: power keys s^(g/2+2); odd g: galois
+    if (g % 2 == 0 ? g > 4 : g >= 2u * (uint32_t)c->N) {
+        he_set_error("key code %u: galois elements are odd and < 2N, power keys are 0, 2, 4", g);
         return HE_EINVAL;
     }
     if (he_get_key(c, g)) return HE_OK;  // idempotent (RotationKeySet.register)
@@ -554,8 +559,8 @@ extern "C" int he_gen_switch_key(he_ctx *c, uint32_t g, void *stream) {
     HE_TRY(he_scratch_alloc((void **)&sp, (size_t)L * N * 8, s));
     HE_TRY(he_scratch_alloc((void **)&pm, (size_t)L * 8, s));
     HE_CHECK_CUDA(he_h2d(pm, c->h_pmodq.data(), L * 8, s));
-    if (g == 0)
-        k_sk_square<<<ceil_div((size_t)L * N, 256), 256, 0, s>>>(sp, c->d_sk, c->d_mc, N, L);
+    if (g % 2 == 0)
+        k_sk_power<<<ceil_div((size_t)L * N, 256), 256, 0, s>>>(sp, c->d_sk, c->d_mc, N, L, g == 0 ? 2 : (int)g / 2 + 2);
     else
         k_automorph<<<ceil_div((size_t)L * N, 256), 256, 0, s>>>(sp, c->d_sk, L, c->logN, g);
     k_ksk_err<<<ceil_div(tot, 256), 256, 0, s>>>(err, c->d_mc, N, M, c->dnum, g, c->prm.seed);

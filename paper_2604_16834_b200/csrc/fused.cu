@@ -408,10 +408,12 @@ __global__ void __launch_bounds__(NTT_TPB) ki_cols(const Job *__restrict__ jobs,
 }
 
 // ---------------------------------------------------------------- ModUp pass 2 + inner product
+constexpr int KS_MAXC = 3;  // key-switched components per inner product (s^2, s^3, s^4)
 struct IpArgs {
-    const uint64_t *ext;  // [B][beta][ext_n][N] ModUp pass-1 outputs (lazy)
-    const uint64_t *const *d;  // [B] device pointers to d (NTT domain, [ell][N])
-    const uint64_t *key;  // [dnum][2][M][N] Montgomery form
+    const uint64_t *ext;  // [nk][B][beta][ext_n][N] ModUp pass-1 outputs
+    const uint64_t *const *d;  // [nk][B] device pointers to the switched components (NTT domain, [ell][N])
+    const uint64_t *key[KS_MAXC];  // per component: [dnum][2][M][N] Montgomery form
+    int nk;               // components summed into one accumulator
     uint64_t *acc;        // [B][2][ext_n][N]
     const uint64_t *tw;
     const double *twd;
@@ -423,7 +425,7 @@ struct IpArgs {
 
 // FP64 form for targets with q < 2^42: pass 2 of every digit's NTT on the
 // FP64 pipe, inner product as exact FP64 modular products against the
-// Montgomery-form key (sum < 10 beta q, no overflow), one R^-1 product and one
+// Montgomery-form key (|sum| < 6 nk beta q < 2^51, exact), one R^-1 product and one
 // canonicalisation at the end.  Half the registers of the 128-bit integer
 // accumulators (no spills) and twice the multiply rate.
 __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip_fp(const IpArgs a) {
@@ -440,14 +442,17 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip_fp(const IpArgs a) {
     double acc0[16], acc1[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) acc0[j] = acc1[j] = 0.0;
+    for (int kc = 0; kc < a.nk; kc++)
     for (int dj = 0; dj < a.beta; dj++) {
+        const int bk = kc * a.B + b;
+        const uint64_t *kbase = kc == 0 ? a.key[0] : kc == 1 ? a.key[1] : a.key[2];  // (no param-array indexing)
         double xd[16];
         if (dj == jt) {
-            const uint64_t *dp = a.d[b] + (size_t)t * NN + r * 256;
+            const uint64_t *dp = a.d[bk] + (size_t)t * NN + r * 256;
 #pragma unroll
             for (int j = 0; j < 16; j++) xd[j] = u2d(dp[g + 16 * j]);
         } else {
-            const uint64_t *row = a.ext + ((((size_t)b * a.beta + dj) * a.ext_n + t) << LOGN) + r * 256;
+            const uint64_t *row = a.ext + ((((size_t)bk * a.beta + dj) * a.ext_n + t) << LOGN) + r * 256;
 #pragma unroll
             for (int j = 0; j < 16; j++) xd[j] = u2d(row[g + 16 * j]);
             fphase_ct<16, 8>(xd, r * 256 + g, Wd, c.qd, c.qid);
@@ -465,7 +470,7 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip_fp(const IpArgs a) {
             for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(g + 16 * j)]);
             __syncwarp();
         }
-        const uint64_t *k0 = a.key + (((size_t)dj * 2 * a.M + m) << LOGN) + r * 256;
+        const uint64_t *k0 = kbase + (((size_t)dj * 2 * a.M + m) << LOGN) + r * 256;
         const uint64_t *k1 = k0 + ((size_t)a.M << LOGN);
 #pragma unroll
         for (int j = 0; j < 16; j++) {
@@ -503,14 +508,17 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
     uint64_t acc0[16], acc1[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) acc0[j] = acc1[j] = 0;
+    for (int kc = 0; kc < a.nk; kc++)
     for (int dj = 0; dj < a.beta; dj++) {
+        const int bk = kc * a.B + b;
+        const uint64_t *kbase = kc == 0 ? a.key[0] : kc == 1 ? a.key[1] : a.key[2];
         uint64_t x[16];
         if (dj == jt) {
-            const uint64_t *dp = a.d[b] + (size_t)t * NN + r * 256;
+            const uint64_t *dp = a.d[bk] + (size_t)t * NN + r * 256;
 #pragma unroll
             for (int j = 0; j < 16; j++) x[j] = dp[g + 16 * j];
         } else {
-            const uint64_t *row = a.ext + ((((size_t)b * a.beta + dj) * a.ext_n + t) << LOGN) + r * 256;
+            const uint64_t *row = a.ext + ((((size_t)bk * a.beta + dj) * a.ext_n + t) << LOGN) + r * 256;
 #pragma unroll
             for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
             const bool nc = c.q < NC_FWD;  // (targets below 2^42 go to k_modup_ip_fp)
@@ -538,7 +546,7 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip(const IpArgs a) {
             for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
             __syncwarp();
         }
-        const uint64_t *k0 = a.key + (((size_t)dj * 2 * a.M + m) << LOGN) + r * 256;
+        const uint64_t *k0 = kbase + (((size_t)dj * 2 * a.M + m) << LOGN) + r * 256;
         const uint64_t *k1 = k0 + ((size_t)a.M << LOGN);
 #pragma unroll
         for (int j = 0; j < 16; j++) {
@@ -635,10 +643,13 @@ Job blank() {
 
 }  // namespace
 
-// ModUp of d + key inner product: acc [B][2][ell+K][N] (NTT domain).  dcv
-// [B][ell][N] and ext [B][beta][ell+K][N] are caller-provided scratch.
-static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, const uint64_t *const *d_dev, int B,
-                    int ell, uint64_t *dcv, uint64_t *ext, uint64_t *acc, cudaStream_t s) {
+// ModUp of nk components + key inner products summed into one accumulator:
+// acc [B][2][ell+K][N] (NTT domain) = sum_k ModUp(d_k) . keys[k].  d (HOST) and
+// d_dev (DEVICE) list the components [nk][B]; dcv [nk][B][ell][N] and ext
+// [nk][B][beta][ell+K][N] are caller-provided scratch.
+static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64_t *const *d,
+                    const uint64_t *const *d_dev, int B, int ell, uint64_t *dcv, uint64_t *ext, uint64_t *acc,
+                    cudaStream_t s) {
     const int L = c->L, K = c->K, alpha = c->alpha, M = L + K;
     const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
     int rc = HE_OK;
@@ -647,7 +658,7 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
     // 1. v = INTT(d) * qhat_s^-1 (ModUp's per-source Shoup step folded into INTT's N^-1)
     if (rc == HE_OK) {
         std::vector<Job> jobs;
-        for (int b = 0; b < B; b++)
+        for (int b = 0; b < nk * B; b++)
             for (int i = 0; i < ell; i++) {
                 Job j = blank();
                 j.src = d[b] + (size_t)i * NN;
@@ -664,7 +675,7 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
     //    (FP64 loader for targets below 2^42)
     if (rc == HE_OK) {
         std::vector<Job> jobs, jobs_fp;
-        for (int b = 0; b < B; b++)
+        for (int b = 0; b < nk * B; b++)
             for (int dj = 0; dj < beta; dj++) {
                 const BconvTable *tb = up[dj];
                 const int s0 = dj * alpha, ns = tb->n_src;
@@ -721,7 +732,8 @@ static int modup_ip(he_ctx *c, const uint64_t *key, const uint64_t *const *d, co
         IpArgs a;
         a.ext = ext;
         a.d = d_dev;
-        a.key = key;
+        a.nk = nk;
+        for (int k = 0; k < KS_MAXC; k++) a.key[k] = keys[k < nk ? k : 0];
         a.acc = acc;
         a.tw = c->d_tw;
         a.twd = c->d_twd;
@@ -781,7 +793,8 @@ int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d,
     uint64_t *dcv = (uint64_t *)scr, *ext = dcv + w_dc, *acc = ext + w_ext, *md = acc + w_acc;
     const BconvTable *dn = nullptr;
     int rc = he_get_moddown_table(c, ell, &dn);
-    if (rc == HE_OK) rc = modup_ip(c, key, d, d_dev, B, ell, dcv, ext, acc, s);
+    const uint64_t *keys[1] = {key};
+    if (rc == HE_OK) rc = modup_ip(c, keys, 1, d, d_dev, B, ell, dcv, ext, acc, s);
     // 4. ModDown: INTT of the P limbs (times N^-1 * phat_k^-1), then the P->Q
     //    BConv NTT whose epilogue writes (acc - conv) * P^-1 (+ d0 / d1)
     if (rc == HE_OK) {
@@ -827,24 +840,27 @@ int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d,
 }
 
 // Relinearisation + `extra` rescales as one ModDown over S = {dropped Q limbs}
-// u P (oracle: oc_relin_rescale).  d3: HOST array of [3][ell][N] device
-// ciphertexts, d2_dev: device array of their d2 = d3 + 2 ell N pointers,
+// u P (oracle: oc_relin_rescale_n).  d3: HOST array of [nc][ell][N] device
+// ciphertexts (nc = nk + 2; component k >= 2 switched with keys[k-2], the s^k
+// key), dk_dev: device array [nk][B] of their component pointers d3 + k ell N,
 // out: HOST array of [2][ell-extra][N].
-int he_relin_rescale_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d3, const uint64_t *const *d2_dev,
-                           int B, int ell, int extra, uint64_t *const *out, cudaStream_t s) {
+int he_relin_rescale_fused(he_ctx *c, const uint64_t *const *keys, int nk, const uint64_t *const *d3,
+                           const uint64_t *const *dk_dev, int B, int ell, int extra, uint64_t *const *out,
+                           cudaStream_t s) {
     const int L = c->L, K = c->K, alpha = c->alpha, lo = ell - extra, ns = extra + K;
     const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
     const size_t P = (size_t)ell * NN;
-    const size_t w_dc = (size_t)B * ell * NN, w_ext = (size_t)B * beta * ext_n * NN, w_acc = (size_t)B * 2 * ext_n * NN,
-                 w_md = (size_t)B * 2 * lo * NN;
+    const size_t w_dc = (size_t)nk * B * ell * NN, w_ext = (size_t)nk * B * beta * ext_n * NN,
+                 w_acc = (size_t)B * 2 * ext_n * NN, w_md = (size_t)B * 2 * lo * NN;
     void *scr = nullptr;
     HE_TRY(he_scratch_alloc(&scr, (w_dc + w_ext + w_acc + w_md) * 8, s));
     uint64_t *dcv = (uint64_t *)scr, *ext = dcv + w_dc, *acc = ext + w_ext, *md = acc + w_acc;
-    std::vector<const uint64_t *> d2(B);
-    for (int b = 0; b < B; b++) d2[b] = d3[b] + 2 * P;
+    std::vector<const uint64_t *> dk((size_t)nk * B);
+    for (int k = 0; k < nk; k++)
+        for (int b = 0; b < B; b++) dk[(size_t)k * B + b] = d3[b] + (size_t)(2 + k) * P;
     const BconvTable *dn = nullptr;
     int rc = he_get_moddown_table_x(c, ell, extra, &dn);
-    if (rc == HE_OK) rc = modup_ip(c, key, d2.data(), d2_dev, B, ell, dcv, ext, acc, s);
+    if (rc == HE_OK) rc = modup_ip(c, keys, nk, dk.data(), dk_dev, B, ell, dcv, ext, acc, s);
     // joint ModDown, step 1: y_s = INTT(X_s) * N^-1 * shat_s^-1 for s in S, with
     // X_s = acc_s + [P]_{q_s} d_s on the dropped Q limbs (acc's S limbs are contiguous)
     if (rc == HE_OK) {

@@ -363,7 +363,7 @@ int check_basic(he_ctx *c, int count, int ell, int nc, const char *fn) {
         he_set_error("%s: null context", fn);
         return HE_EINVAL;
     }
-    if (count < 0 || ell < 1 || ell > c->L || nc < 1 || nc > 3) {
+    if (count < 0 || ell < 1 || ell > c->L || nc < 1 || nc > 5) {
         he_set_error("%s: bad shape count=%d ell=%d n_comp=%d (L=%d)", fn, count, ell, nc, c->L);
         return HE_EINVAL;
     }
@@ -647,9 +647,13 @@ extern "C" int he_relin(he_ctx *c, const uint64_t *const *d3, uint64_t *const *o
     return HE_OK;
 }
 
-extern "C" int he_relin_rescale(he_ctx *c, const uint64_t *const *d3, uint64_t *const *out, int count, int ell,
-                                int extra, void *stream) {
-    HE_TRY(check_basic(c, count, ell, 3, "he_relin_rescale"));
+extern "C" int he_relin_rescale_n(he_ctx *c, const uint64_t *const *d, uint64_t *const *out, int count, int ell,
+                                  int extra, int nc, void *stream) {
+    if (nc != 3 && nc != 5) {
+        he_set_error("he_relin_rescale_n: nc=%d (3 or 5 components)", nc);
+        return HE_EINVAL;
+    }
+    HE_TRY(check_basic(c, count, ell, nc, "he_relin_rescale_n"));
     if (extra < 0 || extra >= ell || extra > 8) {
         he_set_error("he_relin_rescale: extra=%d must be in [0, min(ell-1, 8)] (ell=%d)", extra, ell);
         return HE_ELEVEL;
@@ -658,24 +662,34 @@ extern "C" int he_relin_rescale(he_ctx *c, const uint64_t *const *d3, uint64_t *
         he_set_error("he_relin_rescale: the joint ModDown is implemented for N = 2^16 only (log_n=%d)", c->logN);
         return HE_EINVAL;
     }
-    const uint64_t *key = he_get_key(c, 0);
-    if (!key) {
-        he_set_error("relinearisation key not generated");
-        return HE_ENOKEY;
+    const int nk = nc - 2;
+    const uint64_t *keys[3] = {nullptr, nullptr, nullptr};
+    for (int k = 0; k < nk; k++) {  // s^2: code 0; s^3, s^4: codes 2, 4
+        keys[k] = he_get_key(c, k == 0 ? 0u : 2u * (uint32_t)k);
+        if (!keys[k]) {
+            he_set_error(k == 0 ? "relinearisation key not generated" : "power key s^%d not generated", k + 2);
+            return HE_ENOKEY;
+        }
     }
     if (!count) return HE_OK;
     cudaStream_t s = (cudaStream_t)stream;
     size_t P = (size_t)ell * c->N;
-    std::vector<const uint64_t *> p2(count);
-    for (int i = 0; i < count; i++) p2[i] = d3[i] + 2 * P;
-    DevPtrs D2(s);
-    HE_TRY(D2.up((const void *const *)p2.data(), count));
-    int ch = chunk_of(ks_bytes_per_ct(c, ell), count);
+    int ch = chunk_of((size_t)nk * ks_bytes_per_ct(c, ell), count);
+    std::vector<const uint64_t *> pk((size_t)nk * ch);
     for (int b0 = 0; b0 < count; b0 += ch) {
         int B = std::min(ch, count - b0);
-        HE_TRY(he_relin_rescale_fused(c, key, d3 + b0, D2.as<const uint64_t>() + b0, B, ell, extra, out + b0, s));
+        for (int k = 0; k < nk; k++)
+            for (int b = 0; b < B; b++) pk[(size_t)k * B + b] = d[b0 + b] + (size_t)(2 + k) * P;
+        DevPtrs DK(s);
+        HE_TRY(DK.up((const void *const *)pk.data(), nk * B));
+        HE_TRY(he_relin_rescale_fused(c, keys, nk, d + b0, DK.as<const uint64_t>(), B, ell, extra, out + b0, s));
     }
     return HE_OK;
+}
+
+extern "C" int he_relin_rescale(he_ctx *c, const uint64_t *const *d3, uint64_t *const *out, int count, int ell,
+                                int extra, void *stream) {
+    return he_relin_rescale_n(c, d3, out, count, ell, extra, 3, stream);
 }
 
 extern "C" int he_rescale(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, int count, int ell, int nc,

@@ -671,27 +671,51 @@ class GpuEngine:
         self._acct.bump("adds", int(len(cl)) + max(0, int(len(cl)) - n_out))
         return self._wrap_batch(out, level, [s * s * scale_mult] * n_out)
 
-    def _ks_modmuls(self, limbs: int, drops: int) -> float:
-        """Algorithmic modular multiplications of one relinearisation with a
-        joint ModDown over P and ``drops`` limbs (SURVEY.md 8d key-switch row):
-        NTT butterflies + ModUp / ModDown BConv MACs + inner-product MACs."""
+    def _ks_modmuls(self, limbs: int, drops: int, nk: int = 1) -> float:
+        """Algorithmic modular multiplications of one relinearisation of ``nk``
+        switched components with a joint ModDown over P and ``drops`` limbs
+        (SURVEY.md 8d key-switch row): NTT butterflies + ModUp / ModDown BConv
+        MACs + inner-product MACs (ModUp and inner product once per component)."""
         K, alpha, N = len(self.context.p_chain_bits), self.context.alpha, self.N
         digits = [min(alpha, limbs - j * alpha) for j in range(-(-limbs // alpha))]
         ext = limbs + K
-        n_ntt = limbs + sum(ext - a for a in digits) + 2 * (K + drops) + 2 * (limbs - drops)
-        bconv = sum(a * (ext - a) for a in digits) + 2 * (K + drops) * (limbs - drops)
-        ip = 2 * len(digits) * ext
+        n_ntt = nk * (limbs + sum(ext - a for a in digits)) + 2 * (K + drops) + 2 * (limbs - drops)
+        bconv = nk * sum(a * (ext - a) for a in digits) + 2 * (K + drops) * (limbs - drops)
+        ip = nk * 2 * len(digits) * ext
         return float(n_ntt * (N // 2) * int(math.log2(N)) + (bconv + ip) * N)
 
     def relin_rescale_batch(self, cts: Sequence[CipherVec], drops: int = 1) -> list[CipherVec]:
         """3-component ciphertexts -> relinearise (key switch of c2) -> rescale
-        ``drops`` times (2 after a deferred-rescale linear layer)."""
+        ``drops`` times (2 after a deferred-rescale linear layer).  5-component
+        ciphertexts (squares of 3-component ones) switch c2, c3, c4 with the
+        s^2, s^3, s^4 keys into one accumulator and need the joint ModDown
+        (N = 2^16; oracle oc_relin_rescale_n)."""
         for c in cts:
             self._check(c)
-        if self._ncomp(cts) != 3:
-            raise HebatchError("relin_rescale_batch expects 3-component ciphertexts")
+        nc = self._ncomp(cts)
+        if nc not in (3, 5):
+            raise HebatchError("relin_rescale_batch expects 3- or 5-component ciphertexts")
         self._ensure_relin()
         level = cts[0].level
+        if nc == 5:
+            if not (self.joint_moddown and self.N == 1 << 16) or drops < 1:
+                raise HebatchError("5-component relinearisation needs the joint ModDown (N = 2^16, drops >= 1)")
+            self._ensure_power_keys()
+            if any(c.level != level for c in cts) or level < drops:
+                raise LevelExhausted(f"relin_rescale_batch needs equal levels >= {drops}")
+            limbs = level + 1
+            pi = self._ptrs(cts)
+            out = self._alloc(len(cts), 2, limbs - drops)
+            po = self._tptrs(out)
+            _lib.check(self._call("relin", self._L.he_relin_rescale_n, self._h, _lib.addr(pi), _lib.addr(po),
+                                  len(cts), limbs, drops, 5, self.stream,
+                                  units=(len(cts) * (9.0 * limbs - 2 * drops) * self.N * 8,
+                                         len(cts) * self._ks_modmuls(limbs, drops, 3))), "relin_rescale_n")
+            scales = [c.scale for c in cts]
+            for k in range(drops):
+                ql = self.moduli[limbs - 1 - k]
+                scales = [s_ / ql for s_ in scales]
+            return self._wrap_batch(out, level - drops, scales)
         if any(c.level != level for c in cts) or level < drops:
             raise LevelExhausted(f"relin_rescale_batch needs equal levels >= {drops}")
         limbs = level + 1
@@ -830,6 +854,12 @@ class GpuEngine:
         if not self._relin:
             _lib.check(self._L.he_gen_switch_key(self._h, 0, self.stream), "relin keygen")
             self._relin = True
+
+    def _ensure_power_keys(self) -> None:
+        """s^3 and s^4 switching keys (codes 2, 4) for 5-component relinearisation."""
+        for code in (2, 4):
+            if not self._L.he_has_switch_key(self._h, code):
+                _lib.check(self._L.he_gen_switch_key(self._h, code, self.stream), "power keygen")
 
     def _mult_ct_batch(self, A, B) -> list[CipherVec]:
         self._ensure_relin()
@@ -1066,11 +1096,15 @@ class GpuEngine:
         the conv output map is never written.  inputs: p*H*W ciphertexts
         (channel-major); weights [M][p*9] (already folded); conv output rows
         ``rows`` (a contiguous range, default all).  Returns pool: M*(nr/2)*(W/2)
-        outputs indexed (m, r/2, x/2); GAP: M outputs.  3 components, scale
+        outputs indexed (m, r/2, x/2); GAP: M outputs.  3 components (5 when
+        the inputs are unrelinearised 3-component squares), scale
         s_out^2 * scale_mult (default 4 for pool, pixel count for GAP).
         None when a tensor-core bound does not hold (caller falls back)."""
         for c in inputs:
             self._check(c)
+        nci = self._ncomp(inputs)
+        if nci == 3 and W % 2:
+            return None
         s_in = inputs[0].scale
         if any(c.scale != s_in for c in inputs):
             raise ScaleMismatch("conv_square_sum needs inputs at one scale")
@@ -1100,16 +1134,18 @@ class GpuEngine:
         n_out = M * nwin
         tins = self._at_level(inputs, level)
         pin = _lib.ptr_array([t.data_ptr() for t in tins])
-        out = self._alloc(n_out, 3, limbs)
+        nco = 2 * nci - 1
+        out = self._alloc(n_out, nco, limbs)
         pout = self._tptrs(out)
         from .featuremajor import conv3x3_fulltaps
 
         nnz = int((conv3x3_fulltaps(p, H, W, rows) >= 0).sum())
         poly = limbs * self.N
-        rc = self._call("conv_sqsum", self._L.he_conv_square_sum, self._h, _lib.addr(pin), p, H, W, _lib.addr(pout),
-                        M, int(bool(pool)), y0, y1, _lib.addr(wi), _lib.addr(bres) if bres is not None else None,
+        rc = self._call("conv_sqsum", self._L.he_conv_square_sum_n, self._h, _lib.addr(pin), nci, p, H, W,
+                        _lib.addr(pout), M, int(bool(pool)), y0, y1, _lib.addr(wi),
+                        _lib.addr(bres) if bres is not None else None,
                         _lib.addr(cres) if cres is not None else None, limbs, self.stream,
-                        units=((p * (y1 - y0 + 2) * W * 2 + n_out * 3) * poly * 8.0, 2.0 * nnz * M * poly))
+                        units=((p * (y1 - y0 + 2) * W * nci + n_out * nco) * poly * 8.0, 1.0 * nci * nnz * M * poly))
         if rc == _lib.HE_EINVAL:
             return None
         _lib.check(rc, "conv_square_sum")

@@ -171,6 +171,57 @@ def test_relin_rescale_joint_moddown_bit_exact(pair):
     assert np.max(np.abs(eng.decrypt(m) - a_v * b_v)) < 1e-5
 
 
+def test_relin_rescale_five_components_bit_exact(pair):
+    """he_relin_rescale_n (c2, c3, c4 switched with the s^2, s^3, s^4 keys into one
+    accumulator, one joint ModDown) vs oc_relin_rescale_n; power keys vs the
+    oracle's; a square of a square decrypts to a^4."""
+    import torch
+
+    import oracle as O
+
+    name, eng, orc = pair
+    if eng.N != 1 << 16:
+        pytest.skip("joint ModDown is the N = 2^16 path")
+    eng._ensure_relin()
+    eng._ensure_power_keys()
+    M = len(orc.moduli)
+    keys = [orc.switch_key(O.power_key_elt(k)) for k in (2, 3, 4)]
+    for code, ref in ((2, keys[1]), (4, keys[2])):
+        k = torch.empty((orc.dnum, 2, M, eng.N), dtype=torch.int64, device=eng.device)
+        assert _lib(eng).he_export_switch_key(eng._h, code, k.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np(k), ref), code
+    rng = np.random.default_rng(23)
+    L = eng.context.n_q
+    for ell, extra in ((L, 6), (L, 2), (max(3, L // 2), 1)):
+        if extra >= ell:
+            continue
+        x = rand_residues(rng, eng.moduli[:ell], (5,), eng.N)
+        t = from_np(x, eng.device)
+        out = torch.empty((2, ell - extra, eng.N), dtype=torch.int64, device=eng.device)
+        pi, po = _ptrs([t]), _ptrs([out])
+        rc = _lib(eng).he_relin_rescale_n(eng._h, pi.ctypes.data, po.ctypes.data, 1, ell, extra, 5, None)
+        assert rc == 0, eng._L.he_last_error()
+        assert np.array_equal(to_np(out), orc.relin_rescale_n(x, keys, extra)), (ell, extra)
+    # semantics: ((a x a) x (a x a)) -> joint relin + rescale decrypts to a^4
+    n = eng.context.n
+    a_v = rng.uniform(-1, 1, n)
+    (a,) = eng.encrypt_batch(a_v[None])
+    (a2,) = eng.tensor_batch([a], [a])
+    d5 = orc.tensor_sq(to_np(a2.data))
+    t5 = from_np(d5, eng.device)
+    extra = 3  # final scale Delta: the decrypt CRTs two limbs
+    ell = a2.level + 1
+    out = torch.empty((2, ell - extra, eng.N), dtype=torch.int64, device=eng.device)
+    pi, po = _ptrs([t5]), _ptrs([out])
+    assert _lib(eng).he_relin_rescale_n(eng._h, pi.ctypes.data, po.ctypes.data, 1, ell, extra, 5, None) == 0
+    sc = a2.scale ** 2
+    for k in range(extra):
+        sc /= eng.moduli[ell - 1 - k]
+    got = orc.decrypt(to_np(out), sc)
+    assert np.max(np.abs(got - a_v ** 4)) < 1e-4
+
+
 def _oracle_conv_square_sum(orc, ins, p, H, W, wi, bres, cst, pool, y0, y1):
     """conv (oc_lincomb + bias on c0) -> tensor square -> window sum (+cst on c0)."""
     M = wi.shape[0]
@@ -192,9 +243,10 @@ def _oracle_conv_square_sum(orc, ins, p, H, W, wi, bres, cst, pool, y0, y1):
             outs = orc.lincomb([ins[c] for c in cols], rows, list(range(len(cols))) * M, wv)
             for m in range(M):
                 o = outs[m]
-                if bres is not None:
-                    o = orc.add_const(o, bres[m])
-                ys[(m, y, x)] = orc.tensor(o, o)
+                if bres is not None:  # (component 0 only; oc_add_const handles 2 components)
+                    o = o.copy()
+                    o[:2] = orc.add_const(np.ascontiguousarray(o[:2]), bres[m])
+                ys[(m, y, x)] = orc.tensor_sq(o)  # (2 nc - 1 components)
     wins = []
     if pool:
         for wy in range(y0 // 2, y1 // 2):
@@ -215,11 +267,13 @@ def _oracle_conv_square_sum(orc, ins, p, H, W, wi, bres, cst, pool, y0, y1):
     return res
 
 
+@pytest.mark.parametrize("nci", [2, 3])
 @pytest.mark.parametrize("p,M,pool,H,rows,wbits", [(3, 16, 1, 4, (0, 4), 20), (16, 32, 0, 4, (0, 4), 14),
                                                     (4, 8, 1, 4, (2, 4), 7), (2, 24, 0, 6, (1, 5), 20)])
-def test_conv_square_sum_fused_bit_exact(pair, p, M, pool, H, rows, wbits):
-    """he_conv_square_sum (conv + square + pool/GAP sum in one kernel) vs the
-    oracle's conv -> tensor -> add_const -> sum chain, on uniform residues."""
+def test_conv_square_sum_fused_bit_exact(pair, p, M, pool, H, rows, wbits, nci):
+    """he_conv_square_sum_n (conv + square + pool/GAP sum in one kernel) vs the
+    oracle's conv -> tensor square -> add_const -> sum chain, on uniform
+    residues; nci = 3: unrelinearised 3-component inputs, 5-component sums."""
     import torch
 
     name, eng, orc = pair
@@ -229,7 +283,7 @@ def test_conv_square_sum_fused_bit_exact(pair, p, M, pool, H, rows, wbits):
     W = H
     ell = eng.context.n_q if name != "cfg3" else 3
     mods = eng.moduli[:ell]
-    x = rand_residues(rng, mods, (p * H * W, 2), eng.N)
+    x = rand_residues(rng, mods, (p * H * W, nci), eng.N)
     ins = [from_np(x[i], eng.device) for i in range(p * H * W)]
     lim = 1 << wbits
     wi = rng.integers(-lim, lim, size=(M, 9 * p), dtype=np.int64)
@@ -237,10 +291,10 @@ def test_conv_square_sum_fused_bit_exact(pair, p, M, pool, H, rows, wbits):
     cst = np.array([int(rng.integers(0, q)) for q in mods], np.uint64)
     y0, y1 = rows
     nwin = ((y1 - y0) // 2) * (W // 2) if pool else 1
-    outs = [torch.empty((3, ell, eng.N), dtype=torch.int64, device=eng.device) for _ in range(M * nwin)]
+    outs = [torch.empty((2 * nci - 1, ell, eng.N), dtype=torch.int64, device=eng.device) for _ in range(M * nwin)]
     pi, po = _ptrs(ins), _ptrs(outs)
-    rc = _lib(eng).he_conv_square_sum(eng._h, pi.ctypes.data, p, H, W, po.ctypes.data, M, pool, y0, y1,
-                                      wi.ctypes.data, bres.ctypes.data, cst.ctypes.data, ell, None)
+    rc = _lib(eng).he_conv_square_sum_n(eng._h, pi.ctypes.data, nci, p, H, W, po.ctypes.data, M, pool, y0, y1,
+                                        wi.ctypes.data, bres.ctypes.data, cst.ctypes.data, ell, None)
     assert rc == 0, eng._L.he_last_error()
     ref = _oracle_conv_square_sum(orc, [x[i] for i in range(p * H * W)], p, H, W, wi, bres, cst, pool, y0, y1)
     for k, (o, r) in enumerate(zip(outs, ref)):

@@ -42,7 +42,7 @@ def test_params_and_keys_match_bigint(both):
         assert (q - 1) % (2 * o.N) == 0
     sk = o.secret_key()
     assert all(list(map(int, sk[m])) == p.sk_ntt(m) for m in range(len(o.moduli)))
-    for g in (0, 5, 25):
+    for g in (0, 5, 25, O.power_key_elt(3), O.power_key_elt(4)):
         assert np.array_equal(o.switch_key(g), np.array(p.switch_key(g), np.uint64))
 
 
@@ -108,3 +108,26 @@ def test_homomorphic_identities_cfg1_ring():
                          o.mul_const(cs[1], [(-5) % q for q in o.moduli])),
                    o.mul_const(cs[2], [7 % q for q in o.moduli]))
     assert np.array_equal(out, manual)
+
+
+def test_five_component_relin_rescale():
+    """oc_relin_rescale_n: the 3-component form equals oc_relin_rescale bit for bit,
+    and a 5-component square-of-square (keys s^2, s^3, s^4) decrypts to a^4 after
+    the joint ModDown over P and the dropped limbs."""
+    o = O.Oracle(12, [60, 40, 40, 40, 40, 40, 40], [60, 60], 2, seed=3)
+    rng = np.random.default_rng(4)
+    a = rng.uniform(-1, 1, o.n)
+    ca = o.encrypt(a, 0)
+    keys = [o.switch_key(O.power_key_elt(k)) for k in (2, 3, 4)]
+    d3 = o.tensor_sq(ca)
+    assert np.array_equal(d3, o.tensor(ca, ca))
+    assert np.array_equal(o.relin_rescale_n(d3, keys[:1], 2), o.relin_rescale(d3, keys[0], 2))
+    d5 = o.tensor_sq(d3)
+    assert d5.shape[0] == 5
+    s = o.scale ** 4
+    for extra in (2, 3):  # final scale 2^80 / 2^40 (decrypt CRTs two limbs)
+        r = o.relin_rescale_n(d5, keys, extra)
+        sc = s
+        for k in range(extra):
+            sc /= o.moduli[6 - k]
+        assert np.max(np.abs(o.decrypt(r, sc) - a ** 4)) < 1e-5
