@@ -35,7 +35,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import ShapeMismatch
+from .errors import HebatchError, LevelExhausted, ShapeMismatch
 
 
 # ---------------------------------------------------------------- term builders (CSR)
@@ -260,13 +260,31 @@ def conv3x3_fulltaps(p: int, H: int, W: int, rows=None) -> np.ndarray:
     return np.ascontiguousarray(col.reshape(len(rows) * W, p * 9).astype(np.int32))
 
 
-def deferred_weight_scale(engine, cts) -> float:
+def deferred_weight_scale(engine, cts, drops: int = 2) -> float:
     """Weight scale for a deferred-rescale conv feeding a degree-2 activation:
-    (s_in * dw)^2 / (q_{l-1} q_{l-2}) = Delta, so after the activation's
-    relinearisation two dropped primes bring the scale back to Delta."""
+    (s_in * dw)^2 / (q_{l-1} ... q_{l-drops}) = Delta, so after the activation's
+    relinearisation `drops` dropped primes bring the scale back to Delta."""
     limbs = cts[0].level + 1
-    q1, q2 = engine.moduli[limbs - 1], engine.moduli[limbs - 2]
-    return math.sqrt(engine.context.scale * q1 * q2) / cts[0].scale
+    prod = 1.0
+    for k in range(drops):
+        prod *= engine.moduli[limbs - 1 - k]
+    return math.sqrt(engine.context.scale * prod) / cts[0].scale
+
+
+def _ncomp(engine, cts) -> int:
+    f = getattr(engine, "_ncomp", None)
+    return f(cts) if f is not None else 2
+
+
+def carried_drops(engine, cts, min_scale: float = 2.0 ** 16) -> int:
+    """Primes the 5-component relinearisation drops after a conv whose inputs are
+    unrelinearised squares (scale ~ Delta^3): the fewest that give the conv an
+    integer weight scale >= min_scale (2^18 for config 3: six 40-bit primes)."""
+    limbs = cts[0].level + 1
+    for d in range(2, limbs):
+        if deferred_weight_scale(engine, cts, d) >= min_scale:
+            return d
+    raise LevelExhausted("no level budget for the carried activation")
 
 
 def fm_avgpool2x2(engine, inputs, C, H, W):
@@ -340,7 +358,7 @@ class CnnSpec:
 
 
 def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, release_inputs: bool = True,
-            tile_outputs: int = 1024, lazy_relin: bool = True):
+            tile_outputs: int = 1024, lazy_relin: bool = True, carry: bool = True):
     """Encrypted forward pass of ``spec`` over feature-major input ciphertexts.
 
     x_cts: C0*H*W ciphertexts (channel-major).  Each block is streamed over
@@ -351,15 +369,36 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
     ``tile_outputs`` bounds ciphertexts per launch.  Releases its inputs
     unless ``release_inputs`` is False.  Returns the n_classes output
     ciphertexts.
+
+    ``carry`` (fused degree-2 plan, N = 2^16): the pooled 3-component squares of
+    the block before the last are NOT relinearised; the last block's fused conv
+    takes them as they are (5-component squares, he_conv_square_sum_n), and only
+    its global sums -- one per output channel -- are relinearised (keys s^2, s^3,
+    s^4, engine.relin_rescale_batch) with `carried_drops` primes dropped.  For
+    config 3 that replaces 4096 + 32 relinearisations by 32.
     """
     H, W = spec.H, spec.W
     cur = list(x_cts)
     nblk = len(wts.convs)
     a, b = spec.act.fold()
+    fused_ok = (lazy_relin and spec.act.degree == 2 and getattr(engine, "use_fused_conv", False)
+                and getattr(engine, "N", 0) == 1 << 16 and getattr(engine, "joint_moddown", False))
     for blk, (w, bias) in enumerate(wts.convs):
         q = w.shape[0]
         pool = blk in spec.pool_after
         last = blk == nblk - 1
+        # this block's pooled squares stay unrelinearised for the last block
+        carry_out = (carry and fused_ok and pool and blk == nblk - 2 and (W // 2) % 2 == 0)
+        drops = 2
+        if _ncomp(engine, cur) == 3:  # carried squares: one 5-component relinearisation after the GAP
+            drops = carried_drops(engine, cur)
+            p_in = w.shape[1]
+            wmax = np.abs(a * w).max() * deferred_weight_scale(engine, cur, drops)
+            if not (last and p_in <= 16 and W % 2 == 0 and np.rint(wmax) < 2 ** 23
+                    and min(engine.moduli[:cur[0].level + 1]) >= 2 ** 36):
+                z = engine.relin_rescale_batch(cur, drops=2)  # outside the fused kernel's bounds
+                engine.release(*cur)
+                cur, drops = z, 2
         R = max(2 if pool else 1, (tile_outputs // (q * W)) // 2 * 2 if pool else tile_outputs // (q * W))
         R = min(R, H) if stream else H
         Ho, Wo = (H // 2, W // 2) if pool else (H, W)
@@ -369,7 +408,7 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
         # deferred rescale: the conv output keeps its level (weights at ~2^20),
         # the activation's summed products drop two primes after relinearising
         defer = lazy and spec.act.degree == 2
-        dw = deferred_weight_scale(engine, cur) if defer else None
+        dw = deferred_weight_scale(engine, cur, drops) if defer else None
         # conv + square + pool/GAP in one kernel: no conv map in HBM, so the
         # tiles only bound the 3-component window sums (about tile_outputs)
         fused = defer and getattr(engine, "use_fused_conv", False) and (last or pool)
@@ -384,6 +423,8 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
                 part = (fm_conv_square_sum(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw,
                                            const=cst, pool=not last, scale_mult=H * W if last else 4.0)
                         if fused else None)
+                if part is None and _ncomp(engine, cur) == 3:
+                    raise HebatchError("fused conv declined carried 3-component inputs")
                 if part is None:
                     # conv, then square (no relin) + constant + pool / GAP sum in one pass
                     y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw)
@@ -402,8 +443,11 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
                         engine.release(*gap, *part)
                         gap = nsum
                     continue
-                z = engine.relin_rescale_batch(part, drops=2 if defer else 1)
-                engine.release(*part)
+                if carry_out:
+                    z = part  # stays 3-component: the last block squares it unrelinearised
+                else:
+                    z = engine.relin_rescale_batch(part, drops=2 if defer else 1)
+                    engine.release(*part)
                 nr //= 2
                 y0 = rows[0] // 2
                 for o in range(q):
@@ -444,7 +488,7 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
         if blk > 0 or release_inputs:
             engine.release(*cur)
         if last and lazy_relin:
-            g2 = engine.relin_rescale_batch(gap, drops=2 if defer else 1)
+            g2 = engine.relin_rescale_batch(gap, drops=drops if defer else 1)
             engine.release(*gap)
             gap = g2
         cur = gap if last else nxt
