@@ -209,12 +209,16 @@ def main():
     torch.cuda.synchronize()
     launches0 = _lib.load().he_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with Clocks(local) as clk:
         ev0.record()
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            step_ev[i].record()
             step()
+        step_ev[-1].record()
         ev1.record()
         torch.cuda.synchronize()
+    step_ms = [round(step_ev[i].elapsed_time(step_ev[i + 1]), 1) for i in range(args.steps)]
     barrier()
     launches = _lib.load().he_launch_count() - launches0
     ms = max_over_ranks(ev0.elapsed_time(ev1))
@@ -295,7 +299,8 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "step_ms": step_ms, "higher_is_better": True,
+            "scaling": "weak",
             "vs_baseline": None, "dtype": "u64 (RNS residues mod 40/42-bit primes; FP64-exact modular products)",
             "data": "synthetic (seeded U[0,1] CIFAR-shaped images, N(0,1/fan_in) weights)",
             "config": _config(world),

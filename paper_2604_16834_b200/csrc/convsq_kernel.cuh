@@ -128,72 +128,63 @@ __device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, int yy
     }
 }
 
-// One input byte plane D: C[e] = sum_k byte_D(x_k) W_e[k] on the tensor cores,
-// then the exact recombination.  W[j][q] is the int32 sum of the products with
-// byte shift D + j still open (|C| < 2^23, <= E terms: no overflow); a
-// completed shift s is folded into P[s/4] with one IMAD.WIDE by 2^(8 (s%4))
-// (multipliers held in registers so ptxas keeps IMAD.WIDE).
-template <int D, int KB, int E, int NB, int DSTR>
+// One input byte plane D on the tensor cores.  Products with the same byte
+// shift s = D + e accumulate in ONE int32 fragment C[s] (the mma's own
+// accumulator), so the exact recombination sees NB + E - 1 shift sums instead
+// of NB * E digit products: |C[s]| <= 3 * 144 * 255 * 128 < 2^24 for the
+// accepted shapes (p <= 16, |w| < 2^23), no overflow.
+template <int D, int KB, int E, int NB, int DSTR, int NSH>
 __device__ __forceinline__ void digit_plane(const uint32_t *X, const int (&o0)[KB][2], const int (&o1)[KB][2],
-                                            const uint2 (&bw)[KB][E], int (&W)[E][4], int64_t (&P)[3][4],
-                                            const int (&mul)[4]) {
+                                            const uint2 (&bw)[KB][E], int (&C)[NSH][4]) {
     if (D >= NB) return;
     const uint32_t *Xd = X + D * DSTR;  // compile-time plane offset: an LDS immediate
-    int C[E][4];
-#pragma unroll
-    for (int e = 0; e < E; e++) C[e][0] = C[e][1] = C[e][2] = C[e][3] = 0;
 #pragma unroll
     for (int kb = 0; kb < KB; kb++) {
         const uint32_t a0 = Xd[o0[kb][0]], a1 = Xd[o1[kb][0]], a2 = Xd[o0[kb][1]], a3 = Xd[o1[kb][1]];
 #pragma unroll
-        for (int e = 0; e < E; e++) mma_u8s8(C[e], a0, a1, a2, a3, bw[kb][e]);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-#pragma unroll
-        for (int e = 0; e < E; e++) W[e][q] += C[e][q];
-        madw(P[D >> 2][q], W[0][q], mul[D & 3]);  // shift D is complete
-#pragma unroll
-        for (int j = 0; j + 1 < E; j++) W[j][q] = W[j + 1][q];
-        W[E - 1][q] = 0;
-    }
-    if (D == NB - 1) {  // last byte plane: flush shifts NB .. NB + E - 2
-#pragma unroll
-        for (int j = 0; j + 1 < E; j++)
-#pragma unroll
-            for (int q = 0; q < 4; q++) madw(P[(D + 1 + j) >> 2][q], W[j][q], mul[(D + 1 + j) & 3]);
+        for (int e = 0; e < E; e++) mma_u8s8(C[D + e], a0, a1, a2, a3, bw[kb][e]);
     }
 }
 
 // The tile's four fragment values: exact conv over all byte planes (tile rows
-// from o0 / o1), recombined.  FP (40-bit primes): T = P0 + P1 2^32 with |P0|,
-// |P1| < 2^50, y = T mod q with one FP64 modular product, returned as
-// integer-valued doubles (not yet canonical, |y| < 2^51).  Integer path:
-// canonical y R^-1 (one Montgomery step) in yv.
+// from o0 / o1), recombined from the shift sums: P0 = sum_{s<4} C[s] 2^(8s),
+// P1 = sum_{4<=s<8} C[s] 2^(8(s-4)), P2 = the rest.  FP (40-bit primes):
+// T = P0 + P1 2^32 with |P0| < 2^48.1, |P1| < 2^40; y = P0 + [P1 2^32 mod q]
+// (one FP64 modular product) is returned as an integer-valued double,
+// NOT reduced: |y| < 2^48.2 (the square accumulator takes unreduced
+// operands).  Integer path: canonical y R^-1 (one Montgomery step) in yv.
 template <int KB, int E, int NB, int DSTR>
 __device__ __forceinline__ void tile_values(const uint32_t *X, const int (&o0)[KB][2], const int (&o1)[KB][2],
                                             const uint2 (&bw)[KB][E], const int (&mul)[4], const ModConst &c,
                                             double yc1, double (&yd)[4], uint64_t (&yv)[4]) {
-    int64_t P[3][4];  // partial sums at 2^0, 2^32, 2^64 for the 4 fragment values
+    constexpr int NSH = NB + E - 1;  // byte shifts 0 .. NB + E - 2
+    int C[NSH][4];
 #pragma unroll
-    for (int hh = 0; hh < 3; hh++) P[hh][0] = P[hh][1] = P[hh][2] = P[hh][3] = 0;
-    int W[E][4];
+    for (int s = 0; s < NSH; s++) C[s][0] = C[s][1] = C[s][2] = C[s][3] = 0;
+    digit_plane<0, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
+    digit_plane<1, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
+    digit_plane<2, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
+    digit_plane<3, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
+    digit_plane<4, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
+    digit_plane<5, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
+    digit_plane<6, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
+    digit_plane<7, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
+    int64_t P[3][4];
 #pragma unroll
-    for (int j = 0; j < E; j++) W[j][0] = W[j][1] = W[j][2] = W[j][3] = 0;
-    digit_plane<0, KB, E, NB, DSTR>(X, o0, o1, bw, W, P, mul);
-    digit_plane<1, KB, E, NB, DSTR>(X, o0, o1, bw, W, P, mul);
-    digit_plane<2, KB, E, NB, DSTR>(X, o0, o1, bw, W, P, mul);
-    digit_plane<3, KB, E, NB, DSTR>(X, o0, o1, bw, W, P, mul);
-    digit_plane<4, KB, E, NB, DSTR>(X, o0, o1, bw, W, P, mul);
-    digit_plane<5, KB, E, NB, DSTR>(X, o0, o1, bw, W, P, mul);
-    digit_plane<6, KB, E, NB, DSTR>(X, o0, o1, bw, W, P, mul);
-    digit_plane<7, KB, E, NB, DSTR>(X, o0, o1, bw, W, P, mul);
+    for (int q = 0; q < 4; q++) {
+        P[0][q] = C[0][q];
+        P[1][q] = NSH > 4 ? C[NSH > 4 ? 4 : 0][q] : 0;
+        P[2][q] = NSH > 8 ? C[NSH > 8 ? 8 : 0][q] : 0;
+#pragma unroll
+        for (int s = 1; s < NSH; s++)
+            if (s & 3) madw(P[s >> 2][q], C[s][q], mul[s & 3]);
+    }
     if constexpr (NB == 5) {
 #pragma unroll
         for (int q = 0; q < 4; q++) {
             const double p0 = __longlong_as_double(0x4338000000000000ll + P[0][q]) - 6755399441055744.0;
             const double p1 = __longlong_as_double(0x4338000000000000ll + P[1][q]) - 6755399441055744.0;
-            yd[q] = p0 + fmulmod(p1, yc1, c.qd, c.qid);  // T = P0 + P1 2^32 (mod q), |T'| < 2^51
+            yd[q] = p0 + fmulmod(p1, yc1, c.qd, c.qid);  // T = P0 + P1 2^32 (mod q), |T'| < 2^48.2
         }
     } else {
 #pragma unroll
@@ -210,9 +201,9 @@ __device__ __forceinline__ void tile_values(const uint32_t *X, const int (&o0)[K
 // Window sums of the products of y = conv (plain domain, FP path) or
 // y = conv * R^-1 (integer path).  NS = 3: (y0 y0, y0 y1, y1 y1);
 // NS = 6: (y0 y0, y0 y1, y0 y2, y1 y1, y1 y2, y2 y2).
-// 40-bit primes: exact FP64 modular products accumulated as doubles (each
-// |product| < 3q, folded every 64) on the FP64 pipe; wider primes: exact
-// 128-bit sums.  value(k) returns the canonical plain-domain sum.
+// 40-bit primes: exact FP64 modular products of the unreduced conv values
+// accumulated as doubles (folded every 32) on the FP64 pipe; wider primes:
+// exact 128-bit sums.  value(k) returns the canonical plain-domain sum.
 template <bool FP, int NS>
 struct SqAcc;
 template <int NS>
@@ -220,14 +211,17 @@ struct SqAcc<true, NS> {
     double a[NS];
     int n;
     __device__ __forceinline__ SqAcc() { reset(); }
+    // operands are unreduced integer-valued doubles, |y| < 2^49: each modular
+    // product is then below q/2 + 2^98-52 < 2^46.1 in magnitude, so 32 of them
+    // plus a centred residue stay exact (< 2^53); fold every 32
     __device__ __forceinline__ void fold(const ModConst &c) {
-        if (++n == 64) {
+        if (++n == 32) {
             n = 0;
 #pragma unroll
-            for (int k = 0; k < NS; k++) a[k] = u2d(fcanon(a[k], c.qd, c.qid));
+            for (int k = 0; k < NS; k++) a[k] = fma(-rint(a[k] * c.qid), c.qd, a[k]);  // |a| <= q/2 + 1
         }
     }
-    __device__ __forceinline__ void addd(double d0, double d1, const ModConst &c) {  // canonical doubles
+    __device__ __forceinline__ void addd(double d0, double d1, const ModConst &c) {  // |d| < 2^49
         a[0] += fmulmod(d0, d0, c.qd, c.qid);
         a[1] += fmulmod(d0, d1, c.qd, c.qid);
         a[NS == 3 ? 2 : 3] += fmulmod(d1, d1, c.qd, c.qid);
@@ -408,7 +402,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
                     if constexpr (NB == 5) {
 #pragma unroll
                         for (int h = 0; h < 2; h++)
-                            acc[h].addd(fcanond(yd[h] + biasd[h], c.qd, c.qid), fcanond(yd[2 + h], c.qd, c.qid), c);
+                            acc[h].addd(yd[h] + biasd[h], yd[2 + h], c);
                     } else {
 #pragma unroll
                         for (int h = 0; h < 2; h++) acc[h].add(add_mod(yv[h], bias[h], c.q), yv[2 + h], c);
@@ -467,8 +461,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
                         if constexpr (NB == 5) {
 #pragma unroll
                             for (int h = 0; h < 2; h++)
-                                acc[h].addd3(fcanond(yd[h] + biasd[h], c.qd, c.qid), fcanond(yd[2 + h], c.qd, c.qid),
-                                             fcanond(y2d[2 * k + h], c.qd, c.qid), c);
+                                acc[h].addd3(yd[h] + biasd[h], yd[2 + h], y2d[2 * k + h], c);
                         } else {
 #pragma unroll
                             for (int h = 0; h < 2; h++)
