@@ -229,6 +229,9 @@ int he_microbench_intpipe(int device, double *ops_per_s);
 /* FP64 modular products per second (the a*w mod q form of the < 2^42 prime
  * datapath, ntt_core.cuh fmulmod): the key switch's second roofline peak. */
 int he_microbench_fp64(int device, double *modmul_per_s);
+/* int8 multiply-accumulates per second through mma.sync.m16n8k32.u8.s8 (the
+ * fused conv's tensor-core instruction): the conv kernel's tensor roofline. */
+int he_microbench_imma(int device, double *mac_per_s);
 
 #ifdef __cplusplus
 }

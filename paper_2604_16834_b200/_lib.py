@@ -35,6 +35,7 @@ EXPORTS = [
     "he_automorphism", "he_rotate", "he_lincomb", "he_sync", "he_launch_count", "he_lincomb_grouped",
     "he_microbench_intpipe", "he_square_sum", "he_conv_mma", "he_relin_rescale", "he_relin_rescale_n", "he_conv_square_sum", "he_conv_square_sum_n",
     "he_microbench_fp64",
+    "he_microbench_imma",
 ]
 
 
@@ -108,6 +109,7 @@ def load():
         "he_lincomb_grouped": (i, [vp, pp, i, pp, i, i, vp, vp, vp, vp, i, i, i, vp, vp, i, i, vp]),
         "he_microbench_intpipe": (i, [i, vp]),
         "he_microbench_fp64": (i, [i, vp]),
+        "he_microbench_imma": (i, [i, vp]),
         "he_square_sum": (i, [vp, pp, i, pp, i, vp, vp, vp, i, vp]),
         "he_conv_mma": (i, [vp, pp, i, pp, i, i, vp, vp, i, i, i, vp, vp, i, i, vp]),
         "he_conv_square_sum": (i, [vp, pp, i, i, i, pp, i, i, i, i, vp, vp, vp, i, vp]),

@@ -208,7 +208,8 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
             a.rstr = round_up_mod((W + 2) * a.pstr, 32, 8);
             a.R = 4;
         }
-        const size_t smem = (size_t)a.R * a.rstr * 4;
+        // ring + one row's input-address table (8-byte aligned: rstr is even)
+        const size_t smem = (size_t)a.R * a.rstr * 4 + (size_t)p * W * 8;
         if (smem > 227 * 1024) {
             he_set_error("he_conv_square_sum: row ring needs %zu bytes of shared memory (W=%d too wide)", smem, W);
             rc = HE_EINVAL;

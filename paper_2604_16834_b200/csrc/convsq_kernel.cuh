@@ -91,40 +91,69 @@ __device__ __forceinline__ uint64_t mont(uint64_t a, uint64_t b, const ModConst 
 // plane.  NCI = 2: 16 rows per group, groups 2, 3 swap their halves so the
 // four groups read by one A-fragment load hit 32 distinct banks.  NCI = 3: 24
 // rows per group (group strides 24 words already spread the banks).
-template <int NCI>
+// LS (ldmatrix layout, NCI = 3 with 4 channel groups): the 4 groups of a row
+// are one contiguous 16-byte ldmatrix row, rows follow at 16 bytes.
+template <int NCI, bool LS = false>
 __device__ __forceinline__ int rowpos(int cg, int r) {
+    if constexpr (LS) return r * 4 + cg;
     if constexpr (NCI == 2) return cg * 16 + (r ^ (8 * ((cg >> 1) & 1)));
     return cg * 24 + r;
 }
 
 // Input row yy -> ring slot: word (x' + 1) * pstr + d * (8 NCI ncg) + rowpos(cg, comp*8 + j)
 // holds byte d of channels 4cg .. 4cg+3 at pixel (yy, x'), coefficient j of component comp.
-template <int NCI>
-__device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, int yy, int l, size_t coff) {
+template <int NCI, bool LS = false>
+__device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, const uint64_t **prow, int yy, int l,
+                                         size_t coff) {
     constexpr int RW = 8 * NCI;  // rows per channel group
     const size_t N = (size_t)1 << a.logN;
     const int dstr = RW * a.ncg, ntask = a.W * a.ncg * RW;
     const bool inside = yy >= 0 && yy < a.H;
-    for (int t = threadIdx.x; t < ntask; t += CT) {
-        const int r = t % RW, rest = t / RW, cg = rest % a.ncg, x = rest / a.ncg;
-        uint64_t v[4] = {0, 0, 0, 0};
-        if (inside) {
+    // the row's input addresses (p x W) are staged in shared memory once, so no
+    // task waits on a dependent address-table load
+    __syncthreads();  // the previous row's table is no longer read
+    if (inside)
+        for (int k = threadIdx.x; k < a.p * a.W; k += CT)
+            prow[k] = a.in[(size_t)(k / a.W) * a.H * a.W + yy * a.W + k % a.W];
+    __syncthreads();
+    // LU tasks per thread per batch: their address-table and data loads are all
+    // in flight before the first transpose (one memory latency per batch)
+    constexpr int LU = 4;
+    for (int t0 = threadIdx.x; t0 < ntask; t0 += LU * CT) {
+        const uint64_t *src[LU][4];
+#pragma unroll
+        for (int j = 0; j < LU; j++) {
+            const int t = t0 + j * CT;
+            // LS: channel group fastest, so a warp's stores are contiguous words
+            const int r = LS ? (t / 4) % RW : t % RW, cg = LS ? t % 4 : (t / RW) % a.ncg, x = t / (RW * a.ncg);
             const size_t off = ((size_t)(r >> 3) * a.ell + l) * N + coff + (r & 7);
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int i = cg * 4 + u;
-                if (i < a.p) v[u] = __ldg(a.in[(size_t)i * a.H * a.W + yy * a.W + x] + off);
+                src[j][u] = (inside && t < ntask && i < a.p) ? prow[i * a.W + x] + off : nullptr;
             }
         }
-        uint32_t lo[4], hi[4];
-        tr4((uint32_t)v[0], (uint32_t)v[1], (uint32_t)v[2], (uint32_t)v[3], lo);
-        tr4((uint32_t)(v[0] >> 32), (uint32_t)(v[1] >> 32), (uint32_t)(v[2] >> 32), (uint32_t)(v[3] >> 32), hi);
-        uint32_t *dst = slot + (x + 1) * a.pstr + rowpos<NCI>(cg, r);
+        uint64_t v[LU][4];
 #pragma unroll
-        for (int d = 0; d < 4; d++) dst[d * dstr] = lo[d];
+        for (int j = 0; j < LU; j++)
 #pragma unroll
-        for (int d = 0; d < 4; d++)
-            if (d + 4 < a.nb) dst[(d + 4) * dstr] = hi[d];
+            for (int u = 0; u < 4; u++) v[j][u] = src[j][u] ? __ldg(src[j][u]) : 0;
+#pragma unroll
+        for (int j = 0; j < LU; j++) {
+            const int t = t0 + j * CT;
+            if (t >= ntask) break;
+            const int r = LS ? (t / 4) % RW : t % RW, cg = LS ? t % 4 : (t / RW) % a.ncg, x = t / (RW * a.ncg);
+            uint32_t lo[4], hi[4];
+            tr4((uint32_t)v[j][0], (uint32_t)v[j][1], (uint32_t)v[j][2], (uint32_t)v[j][3], lo);
+            tr4((uint32_t)(v[j][0] >> 32), (uint32_t)(v[j][1] >> 32), (uint32_t)(v[j][2] >> 32),
+                (uint32_t)(v[j][3] >> 32), hi);
+            uint32_t *dst = slot + (x + 1) * a.pstr + rowpos<NCI, LS>(cg, r);
+#pragma unroll
+            for (int d = 0; d < 4; d++) dst[d * dstr] = lo[d];
+#pragma unroll
+            for (int d = 0; d < 4; d++)
+                if (d + 4 < a.nb) dst[(d + 4) * dstr] = hi[d];
+        }
     }
 }
 
@@ -196,6 +225,59 @@ __device__ __forceinline__ void tile_values(const uint32_t *X, const int (&o0)[K
             yv[q] = redc(hic, lo, c.q, c.qinv);  // conv * R^-1
         }
     }
+}
+
+__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr));
+}
+
+// shift sums -> value (as tile_values): FP path only (40-bit primes)
+template <int NSH>
+__device__ __forceinline__ void recombine_fp(const int (&C)[NSH][4], const int (&mul)[4], const ModConst &c,
+                                             double yc1, double (&yd)[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        int64_t p0 = C[0][q], p1 = NSH > 4 ? C[NSH > 4 ? 4 : 0][q] : 0;
+#pragma unroll
+        for (int s = 1; s < NSH && s < 4; s++) madw(p0, C[s][q], mul[s]);
+#pragma unroll
+        for (int s = 5; s < NSH; s++) madw(p1, C[s][q], mul[s - 4]);
+        const double d0 = __longlong_as_double(0x4338000000000000ll + p0) - 6755399441055744.0;
+        const double d1 = __longlong_as_double(0x4338000000000000ll + p1) - 6755399441055744.0;
+        yd[q] = d0 + fmulmod(d1, yc1, c.qd, c.qid);
+    }
+}
+
+// LS layout (NCI = 3, 4 channel groups, 40-bit primes): the A fragment of a
+// (plane, K block) is ONE ldmatrix.x4 -- this lane supplies the row address
+// ad[kb] (bytes, plane 0) of matrix lane/8, row lane%8.  NT independent tiles
+// (NT = 2: the two pixels of a pair) are interleaved so their mma chains
+// overlap.
+template <int NT, int KB, int E, int DSTRB>
+__device__ __forceinline__ void tile_values_ls(const uint32_t (&ad)[NT][KB], const uint2 (&bw)[KB][E],
+                                               const int (&mul)[4], const ModConst &c, double yc1,
+                                               double (&yd)[NT][4]) {
+    constexpr int NB = 5, NSH = NB + E - 1;
+    int C[NT][NSH][4];
+#pragma unroll
+    for (int t = 0; t < NT; t++)
+#pragma unroll
+        for (int s = 0; s < NSH; s++) C[t][s][0] = C[t][s][1] = C[t][s][2] = C[t][s][3] = 0;
+#pragma unroll
+    for (int d = 0; d < NB; d++)
+#pragma unroll
+        for (int kb = 0; kb < KB; kb++)
+#pragma unroll
+            for (int t = 0; t < NT; t++) {
+                uint32_t a0, a1, a2, a3;
+                ldsm4(ad[t][kb] + d * DSTRB, a0, a1, a2, a3);
+#pragma unroll
+                for (int e = 0; e < E; e++) mma_u8s8(C[t][d + e], a0, a1, a2, a3, bw[kb][e]);
+            }
+#pragma unroll
+    for (int t = 0; t < NT; t++) recombine_fp<NSH>(C[t], mul, c, yc1, yd[t]);
 }
 
 // Window sums of the products of y = conv (plain domain, FP path) or
@@ -319,6 +401,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
     const ModConst c = a.mc[l];
     constexpr int NCG = KB == 2 ? 1 : KB - 1;  // channel groups of 4 implied by the K blocks
     constexpr int DSTR = 8 * NCI * NCG;
+    constexpr bool LS = NCI == 3 && KB == 5 && NB == 5;  // ldmatrix layout (4 channel groups)
 
     uint2 bw[KB][E];
 #pragma unroll
@@ -352,12 +435,13 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
             wd[kb][h] = (((t % 3) * a.pstr + r0) << 3) | (r1 < r0 ? 4 : 0) | (t / 3);
         }
 
+    const uint64_t **prow = (const uint64_t **)(xs + a.R * a.rstr);  // [p * W] input addresses of one row
     for (int i = tid; i < a.R * a.rstr; i += CT) xs[i] = 0;  // zero halo pixels stay zero
     __syncthreads();
     const int R = a.R, nrow0 = a.pool ? 4 : 3;
     for (int k = 0; k < nrow0; k++) {
         const int yy = a.y0 - 1 + k;
-        load_row<NCI>(a, xs + ((yy + R) % R) * a.rstr, yy, l, coff);
+        load_row<NCI, LS>(a, xs + ((yy + R) % R) * a.rstr, prow, yy, l, coff);
     }
     __syncthreads();
 
@@ -407,6 +491,54 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
 #pragma unroll
                         for (int h = 0; h < 2; h++) acc[h].add(add_mod(yv[h], bias[h], c.q), yv[2 + h], c);
                     }
+                }
+                if (a.pool) {  // window complete
+                    const uint64_t r4 = a.r4[l], cst = a.cst ? a.cst[l] : 0;
+                    const int win = ((yb - a.y0) >> 1) * (a.W >> 1) + it;
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int m = m0 + h;
+                        if (m < a.M) {
+                            uint64_t *o = a.out[(size_t)m * a.nwin + win] + coff + gid;
+#pragma unroll
+                            for (int k = 0; k < NO; k++) {
+                                uint64_t v = square_comp<NCI>(acc[h], k, c, r4);
+                                if (k == 0) v = add_mod(v, cst, c.q);
+                                o[((size_t)k * a.ell + l) * N] = v;
+                            }
+                        }
+                        acc[h].reset();
+                    }
+                }
+            }
+        } else if constexpr (LS) {
+            // pixel pairs as below; A fragments by ldmatrix, the pair's two T0
+            // tiles interleaved.  Lane = (matrix mi, row rr): tap 2 kb + (mi >> 1),
+            // tile rows 8 (mi & 1) + rr.
+            const int mi = lane >> 3, rr = lane & 7;
+            const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(xs);
+            const int nitems = a.W / 2, npair = a.pool ? 2 : 1;
+            for (int it = ps; it < nitems; it += PS) {
+                for (int pr = 0; pr < npair; pr++) {
+                    uint32_t ad[3][KB];  // tile 0: T1 (component 2 of the pair), tiles 1, 2: T0 of x, x + 1
+#pragma unroll
+                    for (int kb = 0; kb < KB; kb++) {
+                        int t = 2 * kb + (mi >> 1);
+                        if (t >= 9) t -= 9;  // zero-weight half of the last K block
+                        const int dy = t / 3 + pr;
+                        const int w = (dy == 0 ? sb[0] : dy == 1 ? sb[1] : dy == 2 ? sb[2] : sb[3]) +
+                                      (2 * it + t % 3) * a.pstr + 4 * rr;
+                        ad[0][kb] = sbase + 4 * (w + (mi & 1) * a.pstr + 64);  // component 2, pixel x + (mi & 1)
+                        ad[1][kb] = sbase + 4 * (w + (mi & 1) * 32);           // components 0 / 1, pixel x
+                        ad[2][kb] = ad[1][kb] + 4 * a.pstr;                    // pixel x + 1
+                    }
+                    double y[3][4];
+                    tile_values_ls<3, KB, E, 4 * DSTR>(ad, bw, mul, c, yc1, y);
+#pragma unroll
+                    for (int k = 0; k < 2; k++)
+#pragma unroll
+                        for (int h = 0; h < 2; h++)
+                            acc[h].addd3(y[1 + k][h] + biasd[h], y[1 + k][2 + h], y[0][2 * k + h], c);
                 }
                 if (a.pool) {  // window complete
                     const uint64_t r4 = a.r4[l], cst = a.cst ? a.cst[l] : 0;
@@ -495,7 +627,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
             __syncthreads();
             for (int k = 0; k < rows_per_blk; k++) {
                 const int yy = ynext + 1 + k;  // pool: rows ynext+1, ynext+2; GAP: row ynext+1
-                load_row<NCI>(a, xs + ((yy + R) % R) * a.rstr, yy, l, coff);
+                load_row<NCI, LS>(a, xs + ((yy + R) % R) * a.rstr, prow, yy, l, coff);
             }
             __syncthreads();
         }

@@ -52,7 +52,59 @@ __global__ void k_fmulmod(double *sink, int iters, double q, double w) {
     if (s == 12345.0) sink[0] = s;
 }
 
+// mma.sync.m16n8k32 u8 x s8 -> s32 (the fused conv's tensor-core instruction):
+// 8 independent accumulators per warp, full grid
+__global__ void k_imma(int *sink, int iters, uint32_t seed) {
+    int c[8][4];
+#pragma unroll
+    for (int k = 0; k < 8; k++) c[k][0] = c[k][1] = c[k][2] = c[k][3] = 0;
+    uint32_t a0 = seed ^ threadIdx.x, a1 = a0 * 3, a2 = a0 * 5, a3 = a0 * 7;
+    const uint32_t b0 = seed * 11, b1 = seed * 13;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            asm volatile(
+                "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                "{%0,%1,%2,%3};"
+                : "+r"(c[k][0]), "+r"(c[k][1]), "+r"(c[k][2]), "+r"(c[k][3])
+                : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+        a0 += 1;
+    }
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) s ^= c[k][0] ^ c[k][3];
+    if (s == 0x12345678) sink[0] = s;
+}
+
 }  // namespace
+
+// int8 multiply-accumulates per second through mma.sync m16n8k32 (u8 x s8),
+// the instruction of the fused conv kernels (convsq_kernel.cuh)
+extern "C" int he_microbench_imma(int device, double *mac_per_s) {
+    HE_CHECK_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    HE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    void *sink;
+    HE_CHECK_CUDA(cudaMalloc(&sink, 64));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = sms * 4, threads = 256, iters = 2048;
+    float ms = 0;
+    for (int rep = 0; rep < 2; rep++) {
+        cudaEventRecord(e0);
+        k_imma<<<blocks, threads>>>((int *)sink, iters, 12345u);
+        cudaEventRecord(e1);
+        HE_CHECK_CUDA(cudaEventSynchronize(e1));
+    }
+    cudaEventElapsedTime(&ms, e0, e1);
+    *mac_per_s = (double)blocks * (threads / 32) * iters * 8 * (16.0 * 8 * 32) / (ms * 1e-3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
 
 // FP64 modular products per second (fmulmod on a 40-bit prime, full grid)
 extern "C" int he_microbench_fp64(int device, double *modmul_per_s) {

@@ -53,4 +53,4 @@ def case(p, H, W, M, pool, y0, y1, ell, wbits, nci=2):
 
 case(3, 32, 32, 16, 1, 0, 8, 14, 19)
 case(16, 16, 16, 32, 0, 0, 16, 12, 14)
-case(16, 16, 16, 32, 0, 0, 16, 14, 15, nci=3)
+case(16, 16, 16, 32, 0, 0, 16, 14, 14, nci=3)
