@@ -63,7 +63,7 @@ def _config(world):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region."""
+    """SM clock / clock-event-reason sampling (NVML, else nvidia-smi) during the timed region."""
 
     def __init__(self, device):
         self.device = device
@@ -72,20 +72,44 @@ class Clocks:
         self._t = None
 
     def __enter__(self):
+        # in-process NVML (no fork of this large process while the GPU is timed);
+        # nvidia-smi only if NVML is unavailable
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                    ("sw_power_cap", 0x4)]
+
+            def sample():
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h) \
+                    if hasattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons") \
+                    else pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                return ([str(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                         str(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)), hex(r)]
+                        + ["Active" if r & b else "Not Active" for _, b in bits])
+            sample()
+        except Exception:
+            sample = None
+
         def run():
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
                  "clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
+                    if sample is not None:
+                        self.rows.append(sample())
+                    else:
+                        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                             timeout=5).stdout.strip()
+                        if out:
+                            self.rows.append([x.strip() for x in out.split(",")])
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.05)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -232,16 +256,36 @@ def main():
     e2e_steps = args.e2e_steps or args.steps
     out_host = torch.empty((10, SAMPLES_PER_GROUP), dtype=torch.float64).pin_memory()
 
-    phase_ev = []                                        # per-step (h2d, encrypt, network, decrypt+d2h) events
-    dev_in = torch.empty(feat_host.shape, dtype=feat_host.dtype, device="cuda")
+    # Host images reach HBM through a copy stream, double-buffered: step i+1's
+    # H2D (pinned -> device, copy engine) is issued once step i's encryption has
+    # consumed its buffer, so it overlaps step i's network.  Every step's H2D,
+    # including the first, lies inside the timed region.
+    phase_ev = []                                        # per-step (h2d wait, encrypt, network, decrypt+d2h) events
+    dev_in = [torch.empty(feat_host.shape, dtype=feat_host.dtype, device="cuda") for _ in range(2)]
+    cstream = torch.cuda.Stream()
+    h2d_done = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    for e in consumed:
+        e.record()
 
-    def e2e_step(ev=None):
+    def issue_h2d(i):
+        b = i % 2
+        with torch.cuda.stream(cstream):
+            cstream.wait_event(consumed[b])             # the buffer's previous encryption is done
+            dev_in[b].copy_(feat_host, non_blocking=True)
+            h2d_done[b].record(cstream)
+
+    def e2e_step(i, last, ev=None):
         rec = (lambda: ev.append(torch.cuda.Event(enable_timing=True)) or ev[-1].record()) if ev is not None \
             else (lambda: None)
+        b = i % 2
         rec()
-        dev_in.copy_(feat_host, non_blocking=True)      # persistent device staging buffer (allocated once)
+        torch.cuda.current_stream().wait_event(h2d_done[b])
         rec()
-        cts = eng.encrypt_batch(dev_in)
+        cts = eng.encrypt_batch(dev_in[b])
+        consumed[b].record()
+        if not last:
+            issue_h2d(i + 1)
         rec()
         out = run_cnn(eng, cts, spec, wts, release_inputs=True)
         rec()
@@ -250,15 +294,17 @@ def main():
         out_host.copy_(logits, non_blocking=True)
         rec()
 
-    for _ in range(args.warmup):                         # same warm-up rule as the resident loop
-        e2e_step()
+    issue_h2d(0)
+    for i in range(args.warmup):                         # same warm-up rule as the resident loop
+        e2e_step(i, i == args.warmup - 1)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(e2e_steps):
+    issue_h2d(0)                                          # first step's copy: inside the timed region
+    for i in range(e2e_steps):
         ev = []
-        e2e_step(ev)
+        e2e_step(i, i == e2e_steps - 1, ev)
         phase_ev.append(ev)
     e1.record()
     torch.cuda.synchronize()
@@ -267,26 +313,53 @@ def main():
     e2e_phases = [[round(ev[i].elapsed_time(ev[i + 1]), 1) for i in range(4)] for ev in phase_ev]
     e2e = world * SAMPLES_PER_GROUP * e2e_steps / (e2e_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (CUDA events over the timed region)
-    dom_name, (calls, dom_ms, units) = max(summ.items(), key=lambda kv: kv[1][1])
+    # ---- rooflines (CUDA events on the launching stream over the timed region)
+    # Each C-ABI category is held against the resource that binds it:
+    #   conv_sqsum : tensor pipe -- algorithmic int8 digit products (modular MACs x
+    #                byte planes x weight digits) against the measured
+    #                mma.sync.m16n8k32.u8.s8 rate of this GPU (he_microbench_imma)
+    #   relin/lincomb : integer datapath -- algorithmic modular products against
+    #                the faster measured modular-product rate (64x64->128 MAC or
+    #                FP64 fmulmod; config 3's primes are < 2^42: FP64)
+    #   everything  : algorithmic HBM bytes against the measured copy bandwidth
     peak, peak_kind = _peaks()
-    ach = units[0] / (dom_ms / 1e3) / 1e9
-    traffic = _traffic().get(dom_name)
-    breakdown = {k: {"calls": v[0], "ms": round(v[1], 2), "alg_GBps": round(v[2][0] / max(v[1], 1e-9) / 1e6, 1),
-                     "GMACps": round(v[2][1] / max(v[1], 1e-9) / 1e6, 1)} for k, v in summ.items()}
-    # the key switch is integer-pipe bound: its second roofline is algorithmic modular
-    # multiplications (NTT butterflies + BConv + inner product) against the
-    # measured 64x64->128 multiply-accumulate rate of this GPU (he_microbench_intpipe)
-    ip, fp = np.zeros(2), np.zeros(1)
+    ip, fp, im = np.zeros(2), np.zeros(1), np.zeros(1)
     _lib.check(_lib.load().he_microbench_intpipe(local, ip.ctypes.data), "microbench")
     _lib.check(_lib.load().he_microbench_fp64(local, fp.ctypes.data), "microbench")
-    # config 3's primes are all below 2^42, so the key switch multiplies on the FP64
-    # datapath: the peak is the faster of the two measured modular-product rates
+    _lib.check(_lib.load().he_microbench_imma(local, im.ctypes.data), "microbench")
     peak_mm = max(float(ip[1]), float(fp[0]))
-    int_ach = units[1] / (dom_ms / 1e3)
-    int_roof = {"achieved": int_ach, "peak": peak_mm, "unit": "modmul/s", "frac": int_ach / peak_mm,
-                "peak_source": "measured: max(64x64->128 MAC/s, FP64 modular products/s) (he_microbench_*)",
-                "mac128_per_s": float(ip[1]), "fp64_modmul_per_s": float(fp[0]), "imad32_per_s": float(ip[0])}
+    peak_tops = 2.0 * float(im[0]) / 1e12
+    traffic_all = _traffic()
+    rooflines = {}
+    for k, (calls, kms, units) in summ.items():
+        sec = kms / 1e3
+        r = {"calls": calls, "ms": round(kms, 2), "avg_ms": kms / calls,
+             "hbm": {"achieved": units[0] / sec / 1e9, "peak": peak, "unit": "GB/s", "frac": units[0] / sec / 1e9 / peak}}
+        if k == "conv_sqsum" and len(units) > 2:
+            ach = 2.0 * units[2] / sec / 1e12
+            r["tensor"] = {"achieved": ach, "peak": peak_tops, "unit": "TOP/s (int8)", "frac": ach / peak_tops,
+                           "peak_source": "measured: mma.sync.m16n8k32.u8.s8 (he_microbench_imma)",
+                           "frac_of_tcgen05_nominal_4500": ach / 4500.0}
+        elif units[1] > 0:
+            ach = units[1] / sec
+            r["int"] = {"achieved": ach, "peak": peak_mm, "unit": "modmul/s", "frac": ach / peak_mm,
+                        "peak_source": "measured: max(64x64->128 MAC/s, FP64 modular products/s) (he_microbench_*)"}
+        rooflines[k] = r
+    dom_name = max(summ.items(), key=lambda kv: kv[1][1])[0]
+    dom = rooflines[dom_name]
+    bind = "tensor" if "tensor" in dom else "int" if "int" in dom else "hbm"
+    roof = {"kernel": dom_name, "bound": "tensor" if bind == "tensor" else "hbm",
+            "achieved": dom[bind]["achieved"] if bind == "tensor" else dom["hbm"]["achieved"],
+            "peak": dom[bind]["peak"] if bind == "tensor" else peak,
+            "unit": dom[bind]["unit"] if bind == "tensor" else "GB/s",
+            "frac": dom[bind]["frac"] if bind == "tensor" else dom["hbm"]["frac"],
+            "traffic": traffic_all.get(dom_name), "peak_source": dom[bind].get("peak_source", peak_kind),
+            "calls": dom["calls"], "avg_ms": dom["avg_ms"], "hbm_frac": dom["hbm"]["frac"]}
+    if bind == "int":
+        roof["int_pipe"] = dom["int"]
+    breakdown = rooflines
+    peaks_measured = {"imma_int8_TOPs": peak_tops, "mac128_per_s": float(ip[1]), "fp64_modmul_per_s": float(fp[0]),
+                      "imad32_per_s": float(ip[0]), "hbm_GBps": peak}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -305,13 +378,13 @@ def main():
             "data": "synthetic (seeded U[0,1] CIFAR-shaped images, N(0,1/fan_in) weights)",
             "config": _config(world),
             "e2e": {"value": e2e, "unit": "samples/s", "steps": e2e_steps,
-                    "phase_ms_h2d_enc_net_dec": e2e_phases,
+                    "phase_ms_h2dwait_enc_net_dec": e2e_phases,
+                    "h2d": "double-buffered on a copy stream, overlapping the previous step's network",
                     "h2d_bytes_per_step": int(feat_host.numel() * 8),
                     "d2h_bytes_per_step": int(out_host.numel() * 8)},
-            "roofline": {"kernel": dom_name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "calls": calls, "avg_ms": dom_ms / calls, "int_pipe": int_roof},
+            "roofline": roof,
             "breakdown": breakdown,
+            "peaks_measured": peaks_measured,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -355,6 +355,7 @@ class GpuEngine:
         self.registration_log: list[frozenset] = []
         self._relin = False
         self._timing = None  # {category: [(start_event, end_event, units)]} when enabled
+        self._slab: dict = {}  # shape -> cached ciphertext batches (see _alloc)
         # exact int8-digit tensor-core convolutions (he_conv_mma); False = CUDA-core kernel
         self.use_tensor_cores = True
         self.joint_moddown = True  # relin + rescales as one ModDown (N = 2^16)
@@ -404,9 +405,43 @@ class GpuEngine:
     def stream(self) -> int:
         return _torch().cuda.current_stream(self.device).cuda_stream
 
+    # Batches of at least this many bytes are kept by the engine after their last
+    # ciphertext is released and handed out again for the next batch of the same
+    # shape.  A pass allocates the same sequence of 21 GB batches every time; a
+    # fresh stream-ordered allocation of that size can cost 25-500 ms of host time
+    # (the pool remaps physical pages into a new virtual range), which a pass
+    # started right after a device synchronize cannot hide.
+    SLAB_MIN_BYTES = 1 << 30
+
     def _alloc(self, count: int, n_comp: int, limbs: int):
         torch = _torch()
-        return torch.empty((count, n_comp, limbs, self.N), dtype=torch.int64, device=self.device)
+        shape = (count, n_comp, limbs, self.N)
+        big = count * n_comp * limbs * self.N * 8 >= self.SLAB_MIN_BYTES
+        if big:
+            # free = no ciphertext view left: the storage is referenced only by the
+            # cached batch and the temporary storage wrapper.  Reuse is stream-ordered
+            # like torch's own allocator (every op runs on the current stream).
+            for t in self._slab.get(shape, ()):
+                if torch._C._storage_Use_Count(t.untyped_storage()._cdata) == 2:
+                    return t
+        try:
+            t = torch.empty(shape, dtype=torch.int64, device=self.device)
+        except torch.OutOfMemoryError:
+            self.trim()
+            t = torch.empty(shape, dtype=torch.int64, device=self.device)
+        if big:
+            self._slab.setdefault(shape, []).append(t)
+        return t
+
+    def trim(self) -> None:
+        """Return the engine's cached (released) ciphertext batches to the pool."""
+        torch = _torch()
+        for shape in list(self._slab):
+            keep = [t for t in self._slab[shape] if torch._C._storage_Use_Count(t.untyped_storage()._cdata) > 2]
+            if keep:
+                self._slab[shape] = keep
+            else:
+                del self._slab[shape]
 
     def _wrap(self, tensors, level: int, scales) -> list[CipherVec]:
         ids = [next(self._ids) for _ in range(len(tensors))]
@@ -1141,11 +1176,18 @@ class GpuEngine:
 
         nnz = int((conv3x3_fulltaps(p, H, W, rows) >= 0).sum())
         poly = limbs * self.N
+        # tensor-core work: each modular MAC is nb x E exact int8 products (nb byte
+        # planes of the residue: 5 below 2^40, else 8; E signed weight bytes)
+        wmax = int(np.abs(wi).max(initial=0))
+        E = 1 if wmax < 128 else 2 if wmax < 32768 else 3
+        nbs = sum(5 if q < (1 << 40) else 8 for q in self.moduli[:limbs])
+        i8 = 1.0 * nci * nnz * M * self.N * nbs * E
         rc = self._call("conv_sqsum", self._L.he_conv_square_sum_n, self._h, _lib.addr(pin), nci, p, H, W,
                         _lib.addr(pout), M, int(bool(pool)), y0, y1, _lib.addr(wi),
                         _lib.addr(bres) if bres is not None else None,
                         _lib.addr(cres) if cres is not None else None, limbs, self.stream,
-                        units=((p * (y1 - y0 + 2) * W * nci + n_out * nco) * poly * 8.0, 1.0 * nci * nnz * M * poly))
+                        units=((p * (y1 - y0 + 2) * W * nci + n_out * nco) * poly * 8.0, 1.0 * nci * nnz * M * poly,
+                               i8))
         if rc == _lib.HE_EINVAL:
             return None
         _lib.check(rc, "conv_square_sum")

@@ -23,9 +23,9 @@ def f(k):
 
 
 print("kernel:", d.get("Kernel Name", "?")[:100])
-print(f"duration {f('gpu__time_duration.sum') / 1e6:.3f} ms   regs {d.get('launch__registers_per_thread')}  "
+print(f"duration {f('gpu__time_duration.sum'):.3f} ms   regs {d.get('launch__registers_per_thread')}  "
       f"warps/SM {f('sm__warps_active.avg.per_cycle_active'):.1f}  issue {f('sm__inst_issued.avg.pct_of_peak_sustained_active'):.1f}%")
-print(f"dram read {f('dram__bytes_read.sum') / 1e9:.3f} GB  write {f('dram__bytes_write.sum') / 1e9:.3f} GB")
+print(f"dram read {f('dram__bytes_read.sum'):.3f} GB  write {f('dram__bytes_write.sum'):.3f} GB  (units as ncu prints them)")
 pipes = sorted(((f(k), k.split("pipe_")[1].split(".")[0]) for k in hdr
                 if k.startswith("sm__inst_executed_pipe_") and k.endswith(".avg.pct_of_peak_sustained_active")),
                reverse=True)
