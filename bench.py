@@ -57,7 +57,7 @@ def _dist():
 def _config(world):
     return {"workload": "cfg3/cfg5 CIFAR-shaped CNN, one 32768-sample ciphertext group per GPU per step",
             "ring_degree": 65536, "q_limbs": 14, "special_primes": 3, "scale_bits": 40,
-            "input_ciphertexts_per_group": 3072, "groups_per_step": world,
+            "input_ciphertexts_per_group": 3072, "input_limbs": None, "groups_per_step": world,
             "samples_per_step": SAMPLES_PER_GROUP * world, "parallelism": f"groups{world}",
             "l2_flush": "inputs (45 GB per group) >> 126 MB L2"}
 
@@ -189,7 +189,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2604_16834_b200 import _lib, configs
     from paper_2604_16834_b200.engine import GpuEngine
-    from paper_2604_16834_b200.featuremajor import run_cnn
+    from paper_2604_16834_b200.featuremajor import min_input_level, run_cnn
     from paper_2604_16834_b200.packing import pack_features
 
     spec = configs.CNN3
@@ -199,7 +199,10 @@ def main():
     rng = np.random.default_rng(group)
     images = rng.uniform(0.0, 1.0, size=(SAMPLES_PER_GROUP, 3 * 32 * 32))
     feat_host = torch.from_numpy(np.ascontiguousarray(images.T)).pin_memory()   # [3072, 32768] f64
-    x = pack_features(eng, images)                        # resident encrypted inputs
+    # inputs are encrypted at the level the plan needs (9 of the chain's 14
+    # limbs for config 3); the other limbs would never be read
+    level = min_input_level(eng, spec)
+    x = pack_features(eng, images, level=level)           # resident encrypted inputs
     eng._ensure_relin()
     del images
 
@@ -282,7 +285,7 @@ def main():
         rec()
         torch.cuda.current_stream().wait_event(h2d_done[b])
         rec()
-        cts = eng.encrypt_batch(dev_in[b])
+        cts = eng.encrypt_batch(dev_in[b], level=level)
         consumed[b].record()
         if not last:
             issue_h2d(i + 1)
@@ -376,7 +379,9 @@ def main():
             "scaling": "weak",
             "vs_baseline": None, "dtype": "u64 (RNS residues mod 40/42-bit primes; FP64-exact modular products)",
             "data": "synthetic (seeded U[0,1] CIFAR-shaped images, N(0,1/fan_in) weights)",
-            "config": _config(world),
+            "config": dict(_config(world), input_limbs=level + 1,
+                           level_plan="inputs at 9 of 14 limbs -> conv1+square+pool (carry, 9) -> conv2+square+GAP (9)"
+                                      " -> 5-component relin dropping 6 primes (3) -> dense+rescale (2)"),
             "e2e": {"value": e2e, "unit": "samples/s", "steps": e2e_steps,
                     "phase_ms_h2dwait_enc_net_dec": e2e_phases,
                     "h2d": "double-buffered on a copy stream, overlapping the previous step's network",

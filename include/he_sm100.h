@@ -91,6 +91,12 @@ int he_ntt(he_ctx *ctx, uint64_t *data, int batch, int ell, int inverse, void *s
  * per-channel loop of pack_inputs (packing.py:119-123). */
 int he_encrypt(he_ctx *ctx, const double *vals, int count, int nvals, double scale,
                uint32_t ct_index0, uint64_t *const *out, void *stream);
+/* the same at ell <= L limbs (out: [2][ell][N] each): a ciphertext encrypted
+ * directly at a lower level, equal limb for limb to the first ell limbs of the
+ * top-level encryption (the randomness is drawn per limb).  Used when the
+ * remaining circuit needs fewer limbs than the chain has. */
+int he_encrypt_level(he_ctx *ctx, const double *vals, int count, int nvals, double scale,
+                     uint32_t ct_index0, int ell, uint64_t *const *out, void *stream);
 /* decrypt + decode to device float64 [count][N/2].  scales: host [count].
  * Replaces decrypt (engine.py:266-268) / unpack_outputs (packing.py:126-135). */
 int he_decrypt(he_ctx *ctx, const uint64_t *const *cts, int count, int ell, const double *scales,

@@ -255,7 +255,7 @@ int he_relin_rescale_fused(he_ctx *c, const uint64_t *const *keys, int nk, const
 const uint64_t *he_get_key(he_ctx *ctx, uint32_t galois_elt);
 // fused N = 2^16 encryption from the encode FFT output (encrypt16.cu); out_dev: device pointer array
 int he_encrypt16(he_ctx *c, const double *re, const double *im, int count, double scale, uint32_t ct_index0,
-                 uint64_t *const *out_dev, cudaStream_t s);
+                 int ell, uint64_t *const *out_dev, cudaStream_t s);
 
 // NTT launchers (ntt.cu).  Polys: data + p*N for p in [0, n_polys); the
 // modulus of poly p is mod_map[p % per] (0xFF: skip the poly).

@@ -236,7 +236,16 @@ int decrypt_to_coeffs(he_ctx *c, const uint64_t *const *cts, int count, int ell,
 
 extern "C" int he_encrypt(he_ctx *c, const double *vals, int count, int nvals, double scale, uint32_t ct_index0,
                           uint64_t *const *out, void *stream) {
-    if (!c || count < 0 || nvals < 0 || (nvals > 0 && !vals) || !(scale > 0)) {
+    if (!c) {
+        he_set_error("he_encrypt: bad arguments");
+        return HE_EINVAL;
+    }
+    return he_encrypt_level(c, vals, count, nvals, scale, ct_index0, c->L, out, stream);
+}
+
+extern "C" int he_encrypt_level(he_ctx *c, const double *vals, int count, int nvals, double scale,
+                                uint32_t ct_index0, int ell, uint64_t *const *out, void *stream) {
+    if (!c || count < 0 || nvals < 0 || (nvals > 0 && !vals) || !(scale > 0) || ell < 1 || ell > c->L) {
         he_set_error("he_encrypt: bad arguments");
         return HE_EINVAL;
     }
@@ -261,14 +270,14 @@ extern "C" int he_encrypt(he_ctx *c, const double *vals, int count, int nvals, d
             HE_CHECK_LAUNCH();
         }
         HE_TRY(run_fft(c, re, im, count, -1, s));
-        return he_encrypt16(c, re, im, count, scale, ct_index0, op, s);
+        return he_encrypt16(c, re, im, count, scale, ct_index0, ell, op, s);
     }
-    HE_TRY(encode_into(c, vals, count, nvals, scale, op, c->L, 1, ct_index0, s));
-    std::vector<uint8_t> m(2 * (size_t)c->L, 0xFF);
-    for (int l = 0; l < c->L; l++) m[l] = (uint8_t)l;
+    HE_TRY(encode_into(c, vals, count, nvals, scale, op, ell, 1, ct_index0, s));
+    std::vector<uint8_t> m(2 * (size_t)ell, 0xFF);
+    for (int l = 0; l < ell; l++) m[l] = (uint8_t)l;
     HE_TRY(upload_map(m, map, s));
-    HE_TRY(he_ntt_fwd_ptrs(c, op, count, 2 * c->L, (const uint8_t *)map.p, s));
-    k_encrypt_finish<<<gridn((size_t)count * c->L * c->N), EW, 0, s>>>(op, count, c->logN, c->L, c->d_sk, c->d_mc,
+    HE_TRY(he_ntt_fwd_ptrs(c, op, count, 2 * ell, (const uint8_t *)map.p, s));
+    k_encrypt_finish<<<gridn((size_t)count * ell * c->N), EW, 0, s>>>(op, count, c->logN, ell, c->d_sk, c->d_mc,
                                                                        c->prm.seed, ct_index0);
     HE_CHECK_LAUNCH();
     return HE_OK;

@@ -162,10 +162,10 @@ __global__ void __launch_bounds__(NTT_TPB) k_enc16_rows(uint64_t *const *out, in
 
 }  // namespace
 
-// Fused encryption of `count` ciphertexts ([2][L][N] each, out_dev: DEVICE
+// Fused encryption of `count` ciphertexts ([2][ell][N] each, out_dev: DEVICE
 // array of their addresses) from the FFT output re/im ([count][N/2] each).
 int he_encrypt16(he_ctx *c, const double *re, const double *im, int count, double scale, uint32_t ct_index0,
-                 uint64_t *const *out_dev, cudaStream_t s) {
+                 int ell, uint64_t *const *out_dev, cudaStream_t s) {
     const size_t n = NN >> 1;
     int64_t *m = nullptr;
     HE_TRY(he_scratch_alloc((void **)&m, (size_t)count * NN * sizeof(int64_t), s));
@@ -174,12 +174,12 @@ int he_encrypt16(he_ctx *c, const double *re, const double *im, int count, doubl
     int rc = cudaGetLastError() == cudaSuccess ? HE_OK : HE_ECUDA;
     he_count_launch(1);
     if (rc == HE_OK) {
-        k_enc16_cols<<<(unsigned)count * 16, NTT_TPB, 0, s>>>(out_dev, m, c->L, c->d_tw, c->d_twd, c->d_mc);
+        k_enc16_cols<<<(unsigned)count * 16, NTT_TPB, 0, s>>>(out_dev, m, ell, c->d_tw, c->d_twd, c->d_mc);
         he_count_launch(1);
         if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
     }
     if (rc == HE_OK) {
-        k_enc16_rows<<<(unsigned)count * c->L * 16, NTT_TPB, 0, s>>>(out_dev, c->L, c->d_tw, c->d_twd, c->d_mc,
+        k_enc16_rows<<<(unsigned)count * ell * 16, NTT_TPB, 0, s>>>(out_dev, ell, c->d_tw, c->d_twd, c->d_mc,
                                                                     c->d_sk, c->prm.seed, ct_index0);
         he_count_launch(1);
         if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;

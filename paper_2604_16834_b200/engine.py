@@ -500,8 +500,11 @@ class GpuEngine:
     def encrypt(self, values) -> CipherVec:
         return self.encrypt_batch(np.asarray(values, dtype=np.float64).ravel()[None, :])[0]
 
-    def encrypt_batch(self, values) -> list[CipherVec]:
-        """Encode + encrypt each row of a [count, <=n] array (one launch sequence)."""
+    def encrypt_batch(self, values, level: int | None = None) -> list[CipherVec]:
+        """Encode + encrypt each row of a [count, <=n] array (one launch sequence),
+        at ``level`` (default: the top level max_level).  A lower level is a
+        direct encryption with level + 1 limbs, equal to the first limbs of the
+        top-level encryption (he_encrypt_level)."""
         torch = _torch()
         if isinstance(values, torch.Tensor):
             v = values.to(device=self.device, dtype=torch.float64)
@@ -513,12 +516,14 @@ class GpuEngine:
         if nvals > self.context.n:
             raise LengthExceedsSlots(f"{nvals} values > {self.context.n} slots")
         v = v.contiguous()
-        L = self.context.n_q
+        L = self.context.n_q if level is None else int(level) + 1
+        if not 1 <= L <= self.context.n_q:
+            raise LevelExhausted(f"encryption level {level} outside 0..{self.context.n_q - 1}")
         out = self._alloc(count, 2, L)
         ptrs = self._tptrs(out)
         base = self._next_enc(count)
-        _lib.check(self._call("encrypt", self._L.he_encrypt, self._h, v.data_ptr(), count, nvals, self.context.scale,
-                              base, _lib.addr(ptrs), self.stream,
+        _lib.check(self._call("encrypt", self._L.he_encrypt_level, self._h, v.data_ptr(), count, nvals,
+                              self.context.scale, base, L, _lib.addr(ptrs), self.stream,
                               units=(count * (2.0 * L * self.N + nvals) * 8, 0.0)), "encrypt")
         return self._wrap_batch(out, L - 1, [self.context.scale] * count)
 

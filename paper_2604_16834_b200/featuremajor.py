@@ -287,6 +287,39 @@ def carried_drops(engine, cts, min_scale: float = 2.0 ** 16) -> int:
     raise LevelExhausted("no level budget for the carried activation")
 
 
+def min_input_level(engine, spec: CnnSpec) -> int:
+    """Lowest input level at which run_cnn's fused carry plan (two blocks, the
+    first pooled, degree-2 activations, N = 2^16) completes with >= 2 limbs left
+    for decryption: the plan consumes no level before the carried activation's
+    5-component relinearisation (which drops carried_drops primes) and one for
+    the dense head.  Limbs above that level would be carried through every layer
+    and never used, so inputs are encrypted at it (he_encrypt_level) -- config 3:
+    9 of the chain's 14 limbs (6 dropped at the relinearisation, 1 by the dense
+    rescale, 2 decrypted).  Other plans: the top level."""
+    top = engine.context.n_q - 1
+    fused = (spec.act.degree == 2 and len(spec.pool_after) == 1 and 0 in spec.pool_after
+             and len(getattr(spec, "channels", (0, 0, 0))) == 3 and getattr(engine, "N", 0) == 1 << 16
+             and getattr(engine, "use_fused_conv", False) and getattr(engine, "joint_moddown", False))
+    if not fused:
+        return top
+
+    class _S:  # scale/level stand-in for the plan arithmetic
+        def __init__(self, level, scale):
+            self.level, self.scale = level, scale
+
+    for level in range(2, top + 1):
+        x = _S(level, engine.context.scale)
+        dw = deferred_weight_scale(engine, [x], 2)
+        carried = _S(level, (x.scale * dw) ** 2 * 4.0)
+        try:
+            d = carried_drops(engine, [carried])
+        except LevelExhausted:
+            continue
+        if level + 1 - d - 1 >= 2:
+            return level
+    return top
+
+
 def fm_avgpool2x2(engine, inputs, C, H, W):
     """2x2 average pool as unit-weight sums (no level): scale x4."""
     rp, cols = pool2x2_csr(C, H, W)

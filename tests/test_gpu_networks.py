@@ -191,3 +191,36 @@ def test_cfg4_layout_sharded_runner_world1_bit_exact_vs_run_cnn():
     got = eng.decrypt_batch(sh_out).T
     ref = spec.forward_plain(wts, images.reshape(n, 3, 8, 8))
     assert np.max(np.abs(got - ref)) < TOL
+
+
+@pytest.mark.gpu
+def test_cfg3_min_level_encryption_and_network():
+    """Inputs encrypted directly at featuremajor.min_input_level (config 3: 9 of
+    14 limbs): the limbs equal the first 9 of the top-level encryption bit for
+    bit, and the whole network decrypts to the float64 forward pass within TOL."""
+    from paper_2604_16834_b200 import configs
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.featuremajor import min_input_level, run_cnn
+    from paper_2604_16834_b200.packing import pack_features
+
+    rng = np.random.default_rng(21)
+    spec = configs.CNN3
+    images = rng.uniform(0.0, 1.0, size=(32768, 3 * 32 * 32))
+    wts = spec.make_weights(5)
+    eng = GpuEngine(configs.context(3, seed=4))
+    lv = min_input_level(eng, spec)
+    assert lv == 8
+    few = np.ascontiguousarray(images[:, :4].T)
+    top = eng.encrypt_batch(few)
+    eng._enc_counter -= 4  # same randomness indices for the low-level encryption
+    low = eng.encrypt_batch(few, level=lv)
+    for t, lo in zip(top, low):
+        assert lo.level == lv
+        assert np.array_equal(to_np(lo.data), to_np(t.data)[:, :lv + 1])
+    eng.release(*top, *low)
+    x = pack_features(eng, images, level=lv)
+    out = run_cnn(eng, x, spec, wts)
+    assert out[0].level == lv - 7
+    got = eng.decrypt_batch(out).T
+    ref = spec.forward_plain(wts, images[:512].reshape(512, 3, 32, 32))
+    assert np.max(np.abs(got[:512] - ref)) < TOL
