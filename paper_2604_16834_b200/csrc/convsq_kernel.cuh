@@ -102,12 +102,14 @@ __device__ __forceinline__ int rowpos(int cg, int r) {
 
 // Input row yy -> ring slot: word (x' + 1) * pstr + d * (8 NCI ncg) + rowpos(cg, comp*8 + j)
 // holds byte d of channels 4cg .. 4cg+3 at pixel (yy, x'), coefficient j of component comp.
-template <int NCI, bool LS = false>
+template <int NCI, bool LS, int NCG, int NB>
 __device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, const uint64_t **prow, int yy, int l,
                                          size_t coff) {
-    constexpr int RW = 8 * NCI;  // rows per channel group
-    const size_t N = (size_t)1 << a.logN;
-    const int dstr = RW * a.ncg, ntask = a.W * a.ncg * RW;
+    constexpr int RW = 8 * NCI;    // rows per channel group
+    constexpr int RC = RW * NCG;   // tasks per pixel: (row, channel group)
+    constexpr int DSTR = RC;       // words per byte plane of a pixel
+    const size_t N = (size_t)1 << a.logN, compstr = (size_t)a.ell * N, base = (size_t)l * N + coff;
+    const int ntask = a.W * RC;
     const bool inside = yy >= 0 && yy < a.H;
     // the row's input addresses (p x W) are staged in shared memory once, so no
     // task waits on a dependent address-table load
@@ -116,17 +118,17 @@ __device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, const 
         for (int k = threadIdx.x; k < a.p * a.W; k += CT)
             prow[k] = a.in[(size_t)(k / a.W) * a.H * a.W + yy * a.W + k % a.W];
     __syncthreads();
-    // LU tasks per thread per batch: their address-table and data loads are all
-    // in flight before the first transpose (one memory latency per batch)
+    // LU tasks per thread per batch: their data loads are all in flight before
+    // the first transpose (one memory latency per batch)
     constexpr int LU = 4;
     for (int t0 = threadIdx.x; t0 < ntask; t0 += LU * CT) {
         const uint64_t *src[LU][4];
 #pragma unroll
         for (int j = 0; j < LU; j++) {
-            const int t = t0 + j * CT;
+            const int t = t0 + j * CT, rc = t % RC, x = t / RC;  // compile-time divisors
             // LS: channel group fastest, so a warp's stores are contiguous words
-            const int r = LS ? (t / 4) % RW : t % RW, cg = LS ? t % 4 : (t / RW) % a.ncg, x = t / (RW * a.ncg);
-            const size_t off = ((size_t)(r >> 3) * a.ell + l) * N + coff + (r & 7);
+            const int r = LS ? rc / 4 : rc % RW, cg = LS ? rc % 4 : rc / RW;
+            const size_t off = (size_t)(r >> 3) * compstr + base + (r & 7);
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int i = cg * 4 + u;
@@ -140,19 +142,19 @@ __device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, const 
             for (int u = 0; u < 4; u++) v[j][u] = src[j][u] ? __ldg(src[j][u]) : 0;
 #pragma unroll
         for (int j = 0; j < LU; j++) {
-            const int t = t0 + j * CT;
+            const int t = t0 + j * CT, rc = t % RC, x = t / RC;
             if (t >= ntask) break;
-            const int r = LS ? (t / 4) % RW : t % RW, cg = LS ? t % 4 : (t / RW) % a.ncg, x = t / (RW * a.ncg);
+            const int r = LS ? rc / 4 : rc % RW, cg = LS ? rc % 4 : rc / RW;
             uint32_t lo[4], hi[4];
             tr4((uint32_t)v[j][0], (uint32_t)v[j][1], (uint32_t)v[j][2], (uint32_t)v[j][3], lo);
             tr4((uint32_t)(v[j][0] >> 32), (uint32_t)(v[j][1] >> 32), (uint32_t)(v[j][2] >> 32),
                 (uint32_t)(v[j][3] >> 32), hi);
             uint32_t *dst = slot + (x + 1) * a.pstr + rowpos<NCI, LS>(cg, r);
 #pragma unroll
-            for (int d = 0; d < 4; d++) dst[d * dstr] = lo[d];
+            for (int d = 0; d < 4; d++) dst[d * DSTR] = lo[d];
 #pragma unroll
             for (int d = 0; d < 4; d++)
-                if (d + 4 < a.nb) dst[(d + 4) * dstr] = hi[d];
+                if (d + 4 < NB) dst[(d + 4) * DSTR] = hi[d];
         }
     }
 }
@@ -250,34 +252,51 @@ __device__ __forceinline__ void recombine_fp(const int (&C)[NSH][4], const int (
     }
 }
 
+// ldmatrix.x4 at addr + OFF (OFF: compile-time byte offset, folded into the instruction)
+template <int OFF>
+__device__ __forceinline__ void ldsm4i(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4+%5];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr), "n"(OFF));
+}
+
 // LS layout (NCI = 3, 4 channel groups, 40-bit primes): the A fragment of a
 // (plane, K block) is ONE ldmatrix.x4 -- this lane supplies the row address
-// ad[kb] (bytes, plane 0) of matrix lane/8, row lane%8.  NT independent tiles
-// (NT = 2: the two pixels of a pair) are interleaved so their mma chains
-// overlap.
-template <int NT, int KB, int E, int DSTRB>
-__device__ __forceinline__ void tile_values_ls(const uint32_t (&ad)[NT][KB], const uint2 (&bw)[KB][E],
-                                               const int (&mul)[4], const ModConst &c, double yc1,
-                                               double (&yd)[NT][4]) {
-    constexpr int NB = 5, NSH = NB + E - 1;
-    int C[NT][NSH][4];
+// (bytes, plane 0) of matrix lane/8, row lane%8.  Three independent tiles are
+// interleaved so their mma chains overlap: y[0] = T1 at ad[0][kb], y[1] = T0 of
+// pixel x at ad[1][kb], y[2] = T0 of pixel x + 1 at ad[1][kb] + PSTRB.
+template <int D, int KB, int E, int DSTRB, int PSTRB, int NSH>
+__device__ __forceinline__ void plane_ls(const uint32_t (&ad)[2][KB], const uint2 (&bw)[KB][E], int (&C)[3][NSH][4]) {
 #pragma unroll
-    for (int t = 0; t < NT; t++)
+    for (int kb = 0; kb < KB; kb++) {
+        uint32_t a[3][4];
+        ldsm4i<D * DSTRB>(ad[0][kb], a[0][0], a[0][1], a[0][2], a[0][3]);
+        ldsm4i<D * DSTRB>(ad[1][kb], a[1][0], a[1][1], a[1][2], a[1][3]);
+        ldsm4i<D * DSTRB + PSTRB>(ad[1][kb], a[2][0], a[2][1], a[2][2], a[2][3]);
+#pragma unroll
+        for (int t = 0; t < 3; t++)
+#pragma unroll
+            for (int e = 0; e < E; e++) mma_u8s8(C[t][D + e], a[t][0], a[t][1], a[t][2], a[t][3], bw[kb][e]);
+    }
+}
+
+template <int KB, int E, int DSTRB, int PSTRB>
+__device__ __forceinline__ void tile_values_ls(const uint32_t (&ad)[2][KB], const uint2 (&bw)[KB][E],
+                                               const int (&mul)[4], const ModConst &c, double yc1,
+                                               double (&yd)[3][4]) {
+    constexpr int NB = 5, NSH = NB + E - 1;
+    int C[3][NSH][4];
+#pragma unroll
+    for (int t = 0; t < 3; t++)
 #pragma unroll
         for (int s = 0; s < NSH; s++) C[t][s][0] = C[t][s][1] = C[t][s][2] = C[t][s][3] = 0;
+    plane_ls<0, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
+    plane_ls<1, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
+    plane_ls<2, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
+    plane_ls<3, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
+    plane_ls<4, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
 #pragma unroll
-    for (int d = 0; d < NB; d++)
-#pragma unroll
-        for (int kb = 0; kb < KB; kb++)
-#pragma unroll
-            for (int t = 0; t < NT; t++) {
-                uint32_t a0, a1, a2, a3;
-                ldsm4(ad[t][kb] + d * DSTRB, a0, a1, a2, a3);
-#pragma unroll
-                for (int e = 0; e < E; e++) mma_u8s8(C[t][d + e], a0, a1, a2, a3, bw[kb][e]);
-            }
-#pragma unroll
-    for (int t = 0; t < NT; t++) recombine_fp<NSH>(C[t], mul, c, yc1, yd[t]);
+    for (int t = 0; t < 3; t++) recombine_fp<NSH>(C[t], mul, c, yc1, yd[t]);
 }
 
 // Window sums of the products of y = conv (plain domain, FP path) or
@@ -441,7 +460,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
     const int R = a.R, nrow0 = a.pool ? 4 : 3;
     for (int k = 0; k < nrow0; k++) {
         const int yy = a.y0 - 1 + k;
-        load_row<NCI, LS>(a, xs + ((yy + R) % R) * a.rstr, prow, yy, l, coff);
+        load_row<NCI, LS, NCG, NB>(a, xs + ((yy + R) % R) * a.rstr, prow, yy, l, coff);
     }
     __syncthreads();
 
@@ -516,24 +535,35 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
             // tiles interleaved.  Lane = (matrix mi, row rr): tap 2 kb + (mi >> 1),
             // tile rows 8 (mi & 1) + rr.
             const int mi = lane >> 3, rr = lane & 7;
+            constexpr int PSTR = NB * NCG * 8 * NCI;  // pixel stride (words) of the LS ring (host: ncg % 4 == 0)
             const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(xs);
             const int nitems = a.W / 2, npair = a.pool ? 2 : 1;
+            // per K block: this lane's T0 row address at pixel 0 of the block's rows
+            // (pr = 0, 1), bytes; T1 sits dT1 bytes further, T0(x + 1) PSTR words
+            uint32_t rbase[2][KB];
+#pragma unroll
+            for (int kb = 0; kb < KB; kb++) {
+                int t = 2 * kb + (mi >> 1);
+                if (t >= 9) t -= 9;  // zero-weight half of the last K block
+#pragma unroll
+                for (int pr = 0; pr < 2; pr++) {
+                    const int dy = t / 3 + pr;
+                    rbase[pr][kb] = sbase + 4 * ((dy == 0 ? sb[0] : dy == 1 ? sb[1] : dy == 2 ? sb[2] : sb[3]) +
+                                                 (t % 3) * PSTR + 4 * rr + (mi & 1) * 32);
+                }
+            }
+            const uint32_t dT1 = 4 * ((mi & 1) * (PSTR - 32) + 64);  // component 2, pixel x + (mi & 1)
             for (int it = ps; it < nitems; it += PS) {
                 for (int pr = 0; pr < npair; pr++) {
-                    uint32_t ad[3][KB];  // tile 0: T1 (component 2 of the pair), tiles 1, 2: T0 of x, x + 1
+                    uint32_t ad[2][KB];  // tile 0: T1 (component 2 of the pair), tile 1: T0 of x (x + 1 by offset)
+                    const uint32_t xoff = 4 * 2 * it * PSTR;
 #pragma unroll
                     for (int kb = 0; kb < KB; kb++) {
-                        int t = 2 * kb + (mi >> 1);
-                        if (t >= 9) t -= 9;  // zero-weight half of the last K block
-                        const int dy = t / 3 + pr;
-                        const int w = (dy == 0 ? sb[0] : dy == 1 ? sb[1] : dy == 2 ? sb[2] : sb[3]) +
-                                      (2 * it + t % 3) * a.pstr + 4 * rr;
-                        ad[0][kb] = sbase + 4 * (w + (mi & 1) * a.pstr + 64);  // component 2, pixel x + (mi & 1)
-                        ad[1][kb] = sbase + 4 * (w + (mi & 1) * 32);           // components 0 / 1, pixel x
-                        ad[2][kb] = ad[1][kb] + 4 * a.pstr;                    // pixel x + 1
+                        ad[1][kb] = rbase[pr][kb] + xoff;
+                        ad[0][kb] = ad[1][kb] + dT1;
                     }
                     double y[3][4];
-                    tile_values_ls<3, KB, E, 4 * DSTR>(ad, bw, mul, c, yc1, y);
+                    tile_values_ls<KB, E, 4 * DSTR, 4 * PSTR>(ad, bw, mul, c, yc1, y);
 #pragma unroll
                     for (int k = 0; k < 2; k++)
 #pragma unroll
@@ -627,7 +657,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
             __syncthreads();
             for (int k = 0; k < rows_per_blk; k++) {
                 const int yy = ynext + 1 + k;  // pool: rows ynext+1, ynext+2; GAP: row ynext+1
-                load_row<NCI, LS>(a, xs + ((yy + R) % R) * a.rstr, prow, yy, l, coff);
+                load_row<NCI, LS, NCG, NB>(a, xs + ((yy + R) % R) * a.rstr, prow, yy, l, coff);
             }
             __syncthreads();
         }
