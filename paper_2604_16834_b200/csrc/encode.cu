@@ -15,6 +15,24 @@ constexpr int EW = 256;
 __device__ __forceinline__ uint32_t brvb(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }
 
 // one radix-2 DIT stage over `count` vectors of n complex values (SoA re/im)
+// One radix-2 DIT butterfly with twiddle index tw: the operation order is part of
+// the bit-exact contract (oracle/ckks_oracle.c oc_fft, -ffp-contract=off here
+// via __dmul_rn / __dadd_rn), shared by every FFT kernel below.
+__device__ __forceinline__ void fft_bfly(double &ur, double &ui, double &vr0, double &vi0, const double *w, size_t tw,
+                                         int sign) {
+    const double wr = w[2 * tw];
+    const double wi = sign < 0 ? -w[2 * tw + 1] : w[2 * tw + 1];
+    const double t1 = __dmul_rn(vr0, wr), t2 = __dmul_rn(vi0, wi);
+    const double vr = __dsub_rn(t1, t2);
+    const double t3 = __dmul_rn(vr0, wi), t4 = __dmul_rn(vi0, wr);
+    const double vi = __dadd_rn(t3, t4);
+    const double a = ur, b = ui;
+    ur = __dadd_rn(a, vr);
+    ui = __dadd_rn(b, vi);
+    vr0 = __dsub_rn(a, vr);
+    vi0 = __dsub_rn(b, vi);
+}
+
 __global__ void k_fft_stage(double *re, double *im, size_t count, int logn, int len, int sign, const double *w) {
     size_t n = (size_t)1 << logn, halfn = n >> 1, tot = count * halfn;
     int half = len >> 1;
@@ -23,27 +41,94 @@ __global__ void k_fft_stage(double *re, double *im, size_t count, int logn, int 
         size_t v = b / halfn, r = b % halfn;
         size_t s = (r / half) * len, k = r % half;
         double *R = re + v * n, *I = im + v * n;
-        double wr = w[2 * (k * step)];
-        double wi = sign < 0 ? -w[2 * (k * step) + 1] : w[2 * (k * step) + 1];
-        double vr0 = R[s + k + half], vi0 = I[s + k + half];
-        double t1 = __dmul_rn(vr0, wr), t2 = __dmul_rn(vi0, wi);
-        double vr = __dsub_rn(t1, t2);
-        double t3 = __dmul_rn(vr0, wi), t4 = __dmul_rn(vi0, wr);
-        double vi = __dadd_rn(t3, t4);
-        double ur = R[s + k], ui = I[s + k];
-        R[s + k] = __dadd_rn(ur, vr);
-        I[s + k] = __dadd_rn(ui, vi);
-        R[s + k + half] = __dsub_rn(ur, vr);
-        I[s + k + half] = __dsub_rn(ui, vi);
+        fft_bfly(R[s + k], I[s + k], R[s + k + half], I[s + k + half], w, k * step, sign);
+    }
+}
+
+// Stages len = 2 .. 2^B of every aligned 2^B-element chunk in shared memory
+// (one CTA per chunk): the same butterflies as k_fft_stage, one HBM pass.
+constexpr int FFT_B = 11, FFT_TPB = 256;
+__global__ void __launch_bounds__(FFT_TPB) k_fft_chunk(double *re, double *im, int logn, int B, int sign,
+                                                       const double *w) {
+    __shared__ double sr[1 << FFT_B], si[1 << FFT_B];
+    const size_t n = (size_t)1 << logn, csz = (size_t)1 << B;
+    const size_t base = (size_t)blockIdx.x * csz;  // chunks of consecutive polynomials tile the batch
+    for (int i = threadIdx.x; i < (int)csz; i += FFT_TPB) {
+        sr[i] = re[base + i];
+        si[i] = im[base + i];
+    }
+    __syncthreads();
+    for (int lg = 1; lg <= B; lg++) {
+        const int len = 1 << lg, half = len >> 1;
+        const size_t step = n >> lg;
+        for (int b = threadIdx.x; b < (int)(csz >> 1); b += FFT_TPB) {
+            const int s = (b / half) * len, k = b % half;
+            fft_bfly(sr[s + k], si[s + k], sr[s + k + half], si[s + k + half], w, (size_t)k * step, sign);
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < (int)csz; i += FFT_TPB) {
+        re[base + i] = sr[i];
+        im[base + i] = si[i];
+    }
+}
+
+// Stages len = 2^(B+1) .. n (R = logn - B <= 4 of them) in registers: thread
+// (polynomial v, k0 < 2^B) owns the 2^R elements k0 + j 2^B, closed under those
+// stages.
+__global__ void k_fft_high(double *re, double *im, size_t count, int logn, int B, int sign, const double *w) {
+    const size_t n = (size_t)1 << logn, grp = (size_t)1 << B, tot = count * grp;
+    const int R = logn - B, m = 1 << R;
+    for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < tot; g += (size_t)gridDim.x * blockDim.x) {
+        const size_t v = g / grp, k0 = g % grp;
+        double *Rp = re + v * n + k0, *Ip = im + v * n + k0;
+        double xr[16], xi[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            if (j < m) {
+                xr[j] = Rp[(size_t)j << B];
+                xi[j] = Ip[(size_t)j << B];
+            }
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            if (r >= R) break;
+            const size_t step = n >> (B + r + 1);
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                if (j >= m || (j >> r) & 1) continue;
+                const size_t k = k0 + ((size_t)(j & ((1 << r) - 1)) << B);  // index inside the half
+                fft_bfly(xr[j], xi[j], xr[j + (1 << r)], xi[j + (1 << r)], w, k * step, sign);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            if (j < m) {
+                Rp[(size_t)j << B] = xr[j];
+                Ip[(size_t)j << B] = xi[j];
+            }
     }
 }
 
 int run_fft(he_ctx *c, double *re, double *im, size_t count, int sign, cudaStream_t s) {
-    int logn = c->logN - 1;
-    size_t n = (size_t)1 << logn;
-    unsigned grid = (unsigned)std::min<size_t>((count * (n / 2) + EW - 1) / EW, (size_t)148 * 32);
-    for (int len = 2; len <= (int)n; len <<= 1) {
-        k_fft_stage<<<grid, EW, 0, s>>>(re, im, count, logn, len, sign, c->d_fftw);
+    const int logn = c->logN - 1;
+    const size_t n = (size_t)1 << logn;
+    const int B = logn < FFT_B ? logn : FFT_B;
+    if (logn - B > 4) {  // (not reached for N <= 2^16) one launch per stage
+        unsigned grid = (unsigned)std::min<size_t>((count * (n / 2) + EW - 1) / EW, (size_t)148 * 32);
+        for (int len = 2; len <= (int)n; len <<= 1) {
+            k_fft_stage<<<grid, EW, 0, s>>>(re, im, count, logn, len, sign, c->d_fftw);
+            HE_CHECK_LAUNCH();
+        }
+        return HE_OK;
+    }
+    if (B >= 1) {
+        k_fft_chunk<<<(unsigned)(count * (n >> B)), FFT_TPB, 0, s>>>(re, im, logn, B, sign, c->d_fftw);
+        HE_CHECK_LAUNCH();
+    }
+    if (logn > B) {
+        const size_t tot = count << B;
+        unsigned grid = (unsigned)std::min<size_t>((tot + EW - 1) / EW, (size_t)148 * 32);
+        k_fft_high<<<grid, EW, 0, s>>>(re, im, count, logn, B, sign, c->d_fftw);
         HE_CHECK_LAUNCH();
     }
     return HE_OK;
