@@ -54,6 +54,8 @@ struct he_ctx {
     ModConst *d_mc = nullptr;        // [L+K]
     uint64_t *d_tw = nullptr;        // [L+K][fwd|inv][N][2]  (psi^brv(i), Shoup) pairs
     double *d_twd = nullptr;         // [L+K][fwd|inv][N]     psi^brv(i) as doubles (FP64 butterflies)
+    double *d_twdc = nullptr;        // [L+K][fwd|inv][N]     the same, centred into (-q/2, q/2] (q < 2^50 path)
+    bool fp50 = false;               // every modulus < 2^50: standalone NTTs use the centred FP64 path
     double *d_rinvd = nullptr;       // [L+K]  2^-64 mod q as doubles (undo Montgomery factors on the FP64 path)
     uint64_t *d_sk = nullptr;        // [L+K][N]     canonical, NTT domain
     double *d_fftw = nullptr;        // [nslots][2]  omega^k

@@ -302,6 +302,16 @@ static int build_tables(he_ctx *c) {
         for (size_t i = 0; i < twd.size(); i++) twd[i] = (double)tw[2 * i];
         HE_CHECK_CUDA(cudaMalloc(&c->d_twd, twd.size() * 8));
         HE_CHECK_CUDA(cudaMemcpy(c->d_twd, twd.data(), twd.size() * 8, cudaMemcpyHostToDevice));
+        // centred copy for the q < 2^50 FP64 NTT (ntt_core.cuh fphase_ct_c / fphase_gs_c)
+        c->fp50 = true;
+        for (int m = 0; m < M; m++) c->fp50 = c->fp50 && c->mod[m] < (1ull << 50);
+        std::vector<double> twdc(twd.size());
+        for (size_t i = 0; i < twd.size(); i++) {
+            const uint64_t q = c->mod[i / (2 * (size_t)N)], w = tw[2 * i];
+            twdc[i] = w > q / 2 ? -(double)(q - w) : (double)w;
+        }
+        HE_CHECK_CUDA(cudaMalloc(&c->d_twdc, twdc.size() * 8));
+        HE_CHECK_CUDA(cudaMemcpy(c->d_twdc, twdc.data(), twdc.size() * 8, cudaMemcpyHostToDevice));
         std::vector<double> rinv(M);
         for (int m = 0; m < M; m++) {
             const uint64_t q = c->mod[m], R = (uint64_t)(((hu128)1 << 64) % q);
@@ -438,6 +448,7 @@ extern "C" int he_ctx_destroy(he_ctx *c) {
     cudaFree(c->d_mc);
     cudaFree(c->d_tw);
     cudaFree(c->d_twd);
+    cudaFree(c->d_twdc);
     cudaFree(c->d_rinvd);
     cudaFree(c->d_sk);
     cudaFree(c->d_fftw);

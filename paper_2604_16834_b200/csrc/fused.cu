@@ -26,6 +26,25 @@
 
 namespace {
 
+// FP64 phases for any prime below 2^50: the lazy (non-reducing) form below
+// 2^42, the centred form (ntt_core.cuh fphase_*_c) from 2^42 to 2^50.  Both
+// take canonical or centred inputs and take centred twiddles (he_ctx::d_twdc).
+constexpr uint64_t FP_QMAX50 = 1ull << 50;
+template <int LOGN, int LM0>
+__device__ __forceinline__ void fphase_ct_any(double (&x)[16], uint32_t e0, const double *W, const ModConst &c) {
+    if (c.q < FP_QMAX)
+        fphase_ct<LOGN, LM0>(x, e0, W, c.qd, c.qid);
+    else
+        fphase_ct_c<LOGN, LM0>(x, e0, W, c.qd, c.qid);
+}
+template <int LOGN, int LT0>
+__device__ __forceinline__ void fphase_gs_any(double (&x)[16], uint32_t e0, const double *W, const ModConst &c) {
+    if (c.q < FP_QMAX)
+        fphase_gs<LOGN, LT0>(x, e0, W, c.qd, c.qid);
+    else
+        fphase_gs_c<LOGN, LT0>(x, e0, W, c.qd, c.qid);
+}
+
 constexpr int LOGN = 16;
 constexpr size_t NN = (size_t)1 << LOGN;
 // primes below these bounds take the no-correction butterflies (ntt_core.cuh):
@@ -151,18 +170,18 @@ __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs,
             x[j] = v > half ? sub_mod(0, reduce64(jb.ql - v, c), c.q) : reduce64(v, c);
         }
     }
-    if (c.q < FP_QMAX) {  // FP64 butterflies; canonical output
+    if (c.q < FP_QMAX50) {  // FP64 butterflies; canonical output
         const double *Wd = twd_fwd(twd, jb.mod, LOGN);
         double xd[16];
 #pragma unroll
         for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
-        fphase_ct<16, 0>(xd, col + 256 * g, Wd, c.qd, c.qid);
+        fphase_ct_any<16, 0>(xd, col + 256 * g, Wd, c);
 #pragma unroll
         for (int j = 0; j < 16; j++) sm[(g + 16 * j) * 16 + lc] = (uint64_t)__double_as_longlong(xd[j]);
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)sm[(16 * g + j) * 16 + lc]);
-        fphase_ct<16, 4>(xd, col + 4096 * g, Wd, c.qd, c.qid);
+        fphase_ct_any<16, 4>(xd, col + 4096 * g, Wd, c);
 #pragma unroll
         for (int j = 0; j < 16; j++) jb.dst[(16 * g + j) * 256 + col] = fcanon(xd[j], c.qd, c.qid);
         return;
@@ -215,19 +234,19 @@ __global__ void __launch_bounds__(NTT_TPB) kf_rows(const Job *__restrict__ jobs,
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = row[g + 16 * j];
     const bool nc = c.q < NC_FWD;
-    if (c.q < FP_QMAX) {
+    if (c.q < FP_QMAX50) {
         const double *Wd = twd_fwd(twd, jb.mod, LOGN);
         double xd[16];
 #pragma unroll
         for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
-        fphase_ct<16, 8>(xd, r * 256 + g, Wd, c.qd, c.qid);
+        fphase_ct_any<16, 8>(xd, r * 256 + g, Wd, c);
 #pragma unroll
         for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = (uint64_t)__double_as_longlong(xd[j]);
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(16 * g + j)]);
         __syncwarp();
-        fphase_ct<16, 12>(xd, r * 256 + 16 * g, Wd, c.qd, c.qid);
+        fphase_ct_any<16, 12>(xd, r * 256 + 16 * g, Wd, c);
 #pragma unroll
         for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = fcanon(xd[j], c.qd, c.qid);
     } else {
@@ -319,19 +338,19 @@ __global__ void __launch_bounds__(NTT_TPB, 2) ki_rows_p(const Job *__restrict__ 
         }
 #pragma unroll
         for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
-        if (c.q < FP_QMAX) {  // FP64 butterflies, canonical output
+        if (c.q < FP_QMAX50) {  // FP64 butterflies, canonical output
             const double *Wd = twd_inv(twd, jb.mod, LOGN);
             double xd[16];
 #pragma unroll
             for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
-            fphase_gs<16, 0>(xd, r * 256 + 16 * g, Wd, c.qd, c.qid);
+            fphase_gs_any<16, 0>(xd, r * 256 + 16 * g, Wd, c);
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = (uint64_t)__double_as_longlong(xd[j]);
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(g + 16 * j)]);
-            fphase_gs<16, 4>(xd, r * 256 + g, Wd, c.qd, c.qid);
+            fphase_gs_any<16, 4>(xd, r * 256 + g, Wd, c);
 #pragma unroll
             for (int j = 0; j < 16; j++) x[j] = fcanon(xd[j], c.qd, c.qid);
         } else {
@@ -371,18 +390,18 @@ __global__ void __launch_bounds__(NTT_TPB) ki_cols(const Job *__restrict__ jobs,
     uint64_t x[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) x[j] = jb.dst[(16 * g + j) * 256 + col];
-    if (c.q < FP_QMAX) {  // FP64 butterflies; the final scale is one more FP64 product
+    if (c.q < FP_QMAX50) {  // FP64 butterflies; the final scale is one more FP64 product
         const double *Wd = twd_inv(twd, jb.mod, LOGN);
         double xd[16];
 #pragma unroll
         for (int j = 0; j < 16; j++) xd[j] = u2d(x[j]);
-        fphase_gs<16, 8>(xd, col + 4096 * g, Wd, c.qd, c.qid);
+        fphase_gs_any<16, 8>(xd, col + 4096 * g, Wd, c);
 #pragma unroll
         for (int j = 0; j < 16; j++) sm[(16 * g + j) * 16 + lc] = (uint64_t)__double_as_longlong(xd[j]);
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)sm[(g + 16 * j) * 16 + lc]);
-        fphase_gs<16, 12>(xd, col + 256 * g, Wd, c.qd, c.qid);
+        fphase_gs_any<16, 12>(xd, col + 256 * g, Wd, c);
         const double cwd = u2d(jb.cw);
 #pragma unroll
         for (int j = 0; j < 16; j++)
@@ -455,14 +474,14 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip_fp(const IpArgs a) {
             const uint64_t *row = a.ext + ((((size_t)bk * a.beta + dj) * a.ext_n + t) << LOGN) + r * 256;
 #pragma unroll
             for (int j = 0; j < 16; j++) xd[j] = u2d(row[g + 16 * j]);
-            fphase_ct<16, 8>(xd, r * 256 + g, Wd, c.qd, c.qid);
+            fphase_ct_any<16, 8>(xd, r * 256 + g, Wd, c);
 #pragma unroll
             for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = (uint64_t)__double_as_longlong(xd[j]);
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 16; j++) xd[j] = __longlong_as_double((long long)s[pad16(16 * g + j)]);
             __syncwarp();
-            fphase_ct<16, 12>(xd, r * 256 + 16 * g, Wd, c.qd, c.qid);  // |x| < 17q: no reduction needed
+            fphase_ct_any<16, 12>(xd, r * 256 + 16 * g, Wd, c);  // < 2^42: |x| < 17q, no reduction needed
 #pragma unroll
             for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = (uint64_t)__double_as_longlong(xd[j]);
             __syncwarp();
@@ -479,6 +498,12 @@ __global__ void __launch_bounds__(NTT_TPB, 2) k_modup_ip_fp(const IpArgs a) {
             acc0[j] += fmulmod(xd[j], w0, c.qd, c.qid);
             acc1[j] += fmulmod(xd[j], w1, c.qd, c.qid);
         }
+        if (c.q >= FP_QMAX)  // 2^42 .. 2^50: each product < 1.01 q, keep the sums centred
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                acc0[j] = fred_c(acc0[j], c.qd, c.qid);
+                acc1[j] = fred_c(acc1[j], c.qd, c.qid);
+            }
     }
     const double ri = a.rinvd[m];
     uint64_t *o0 = a.acc + ((((size_t)b * 2) * a.ext_n + t) << LOGN) + r * 256;
@@ -590,9 +615,9 @@ int run_inverse(he_ctx *c, const std::vector<Job> &jobs, cudaStream_t s) {
                                           (int)(KS * TILE_W * sizeof(uint64_t))));
     }
     const unsigned gp = std::min<unsigned>(g, 2u * (unsigned)sms);
-    ki_rows_p<<<gp, NTT_TPB, KS * TILE_W * sizeof(uint64_t), s>>>(jb.d, (int)g, c->d_tw, c->d_twd, c->d_mc);
+    ki_rows_p<<<gp, NTT_TPB, KS * TILE_W * sizeof(uint64_t), s>>>(jb.d, (int)g, c->d_tw, c->d_twdc, c->d_mc);
     HE_CHECK_LAUNCH();
-    ki_cols<<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
+    ki_cols<<<g, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twdc, c->d_mc);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
@@ -615,11 +640,11 @@ int run_forward(he_ctx *c, const std::vector<Job> &jobs_in, cudaStream_t s) {
     JobBuf jb(s);
     HE_TRY(jb.up(jobs));
     if (nfp) {
-        kf_cols<L_BCONV_FPW><<<(unsigned)nfp * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc, c->d_rinvd);
+        kf_cols<L_BCONV_FPW><<<(unsigned)nfp * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twdc, c->d_mc, c->d_rinvd);
         HE_CHECK_LAUNCH();
     }
     if (jobs.size() > nfp) {
-        kf_cols<LD><<<(unsigned)(jobs.size() - nfp) * 16, NTT_TPB, 0, s>>>(jb.d + nfp, c->d_tw, c->d_twd, c->d_mc,
+        kf_cols<LD><<<(unsigned)(jobs.size() - nfp) * 16, NTT_TPB, 0, s>>>(jb.d + nfp, c->d_tw, c->d_twdc, c->d_mc,
                                                                           c->d_rinvd);
         HE_CHECK_LAUNCH();
     }
@@ -630,7 +655,7 @@ int run_forward(he_ctx *c, const std::vector<Job> &jobs_in, cudaStream_t s) {
                                           (int)pre_bytes));
         attr = true;
     }
-    kf_rows<EP><<<(unsigned)jobs.size() * 16, NTT_TPB, pre_bytes, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc);
+    kf_rows<EP><<<(unsigned)jobs.size() * 16, NTT_TPB, pre_bytes, s>>>(jb.d, c->d_tw, c->d_twdc, c->d_mc);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
@@ -705,14 +730,14 @@ static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64
             JobBuf jb(s);
             rc = jb.up(jobs_fp);
             if (rc == HE_OK && nn) {
-                kf_cols<L_BCONV_FP><<<(unsigned)nn * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc,
+                kf_cols<L_BCONV_FP><<<(unsigned)nn * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twdc, c->d_mc,
                                                                          c->d_rinvd);
                 he_count_launch(1);
                 if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
             }
             if (rc == HE_OK && jobs_fp.size() > nn) {
                 kf_cols<L_BCONV_FPW><<<(unsigned)(jobs_fp.size() - nn) * 16, NTT_TPB, 0, s>>>(
-                    jb.d + nn, c->d_tw, c->d_twd, c->d_mc, c->d_rinvd);
+                    jb.d + nn, c->d_tw, c->d_twdc, c->d_mc, c->d_rinvd);
                 he_count_launch(1);
                 if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
             }
@@ -721,7 +746,7 @@ static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64
             JobBuf jb(s);
             rc = jb.up(jobs);
             if (rc == HE_OK) {
-                kf_cols<L_BCONV><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twd, c->d_mc, c->d_rinvd);
+                kf_cols<L_BCONV><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twdc, c->d_mc, c->d_rinvd);
                 he_count_launch(1);
                 if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
             }
@@ -736,7 +761,7 @@ static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64
         for (int k = 0; k < KS_MAXC; k++) a.key[k] = keys[k < nk ? k : 0];
         a.acc = acc;
         a.tw = c->d_tw;
-        a.twd = c->d_twd;
+        a.twd = c->d_twdc;
         a.mc = c->d_mc;
         a.ell = ell;
         a.ext_n = ext_n;
@@ -746,13 +771,13 @@ static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64
         a.M = M;
         a.B = B;
         a.rinvd = c->d_rinvd;
-        // targets split by prime size: FP64 kernel below 2^42, integer kernel otherwise
+        // targets split by prime size: FP64 kernel below 2^50, integer kernel otherwise
         std::vector<int32_t> tl;
         int nfp = 0;
         for (int pass = 0; pass < 2; pass++)
             for (int t = 0; t < ext_n; t++) {
                 const int m = t < ell ? t : L + (t - ell);
-                if ((c->mod[m] < FP_QMAX) == (pass == 0)) {
+                if ((c->mod[m] < FP_QMAX50) == (pass == 0)) {
                     tl.push_back(t);
                     nfp += pass == 0;
                 }

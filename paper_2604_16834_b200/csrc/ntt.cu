@@ -148,6 +148,134 @@ __global__ void __launch_bounds__(TPB) k_inv16_cols(PolySrc data, const uint8_t 
     for (int j = 0; j < 16; j++) pi.p[(g + 16 * j) * 256 + col] = shoup(x[j], ni, nip, pi.q);
 }
 
+// ---------------------------------------------------------------- N = 2^16, centred FP64 (q < 2^50)
+// The same two-pass structure on the FP64 pipe (ntt_core.cuh fphase_*_c).
+// Between the passes the buffer holds centred residues as raw double bits
+// (private to the pair of kernels); both passes' outer boundaries are
+// canonical uint64.
+struct FpInfo {
+    uint64_t *p;
+    const double *W;
+    double q, qi;
+    const ModConst *mc;
+};
+__device__ __forceinline__ bool fp_info(FpInfo &fi, PolySrc src, size_t poly, const uint8_t *mod_map, int per,
+                                        const double *twdc, const ModConst *mc, bool inverse) {
+    const int m = mod_map[poly % per];
+    if (m == 0xFF) return false;
+    constexpr size_t N = (size_t)1 << 16;
+    fi.p = src.ptrs ? src.ptrs[poly / per] + (poly % per) * N : src.data + poly * N;
+    fi.W = inverse ? twd_inv(twdc, m, 16) : twd_fwd(twdc, m, 16);
+    fi.q = mc[m].qd;
+    fi.qi = mc[m].qid;
+    fi.mc = mc + m;
+    return true;
+}
+
+__global__ void __launch_bounds__(TPB) k_fwd16_cols_c(PolySrc data, const uint8_t *mod_map, int per,
+                                                      const double *twdc, const ModConst *mc) {
+    __shared__ double sm[256 * 16];
+    FpInfo fi;
+    if (!fp_info(fi, data, blockIdx.x >> 4, mod_map, per, twdc, mc, false)) return;
+    const int tid = threadIdx.x, lc = tid & 15, g = tid >> 4;
+    const uint32_t col = (blockIdx.x & 15) * 16 + lc;
+    double x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = u2d(fi.p[(g + 16 * j) * 256 + col]);
+    fphase_ct_c<16, 0>(x, col + 256 * g, fi.W, fi.q, fi.qi);
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[(g + 16 * j) * 16 + lc] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[(16 * g + j) * 16 + lc];
+    fphase_ct_c<16, 4>(x, col + 4096 * g, fi.W, fi.q, fi.qi);
+    double *pd = (double *)fi.p;
+#pragma unroll
+    for (int j = 0; j < 16; j++) pd[(16 * g + j) * 256 + col] = x[j];  // centred doubles between passes
+}
+
+__global__ void __launch_bounds__(TPB) k_fwd16_rows_c(PolySrc data, const uint8_t *mod_map, int per,
+                                                      const double *twdc, const ModConst *mc) {
+    __shared__ double sm[16 * 272];
+    FpInfo fi;
+    if (!fp_info(fi, data, blockIdx.x >> 4, mod_map, per, twdc, mc, false)) return;
+    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+    const uint32_t r = (blockIdx.x & 15) * 16 + rl;
+    uint64_t *row = fi.p + r * 256;
+    const double *rowd = (const double *)row;
+    double x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = rowd[g + 16 * j];
+    fphase_ct_c<16, 8>(x, r * 256 + g, fi.W, fi.q, fi.qi);
+    double *s = sm + rl * 272;
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
+    fphase_ct_c<16, 12>(x, r * 256 + 16 * g, fi.W, fi.q, fi.qi);
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) row[g + 16 * j] = fcanon(s[pad16(g + 16 * j)], fi.q, fi.qi);
+}
+
+__global__ void __launch_bounds__(TPB) k_inv16_rows_c(PolySrc data, const uint8_t *mod_map, int per,
+                                                      const double *twdc, const ModConst *mc) {
+    __shared__ double sm[16 * 272];
+    FpInfo fi;
+    if (!fp_info(fi, data, blockIdx.x >> 4, mod_map, per, twdc, mc, true)) return;
+    const int tid = threadIdx.x, g = tid & 15, rl = tid >> 4;
+    const uint32_t r = (blockIdx.x & 15) * 16 + rl;
+    uint64_t *row = fi.p + r * 256;
+    double *s = sm + rl * 272;
+    double x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(g + 16 * j)] = u2d(row[g + 16 * j]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = s[pad16(16 * g + j)];
+    fphase_gs_c<16, 0>(x, r * 256 + 16 * g, fi.W, fi.q, fi.qi);
+#pragma unroll
+    for (int j = 0; j < 16; j++) s[pad16(16 * g + j)] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = s[pad16(g + 16 * j)];
+    fphase_gs_c<16, 4>(x, r * 256 + g, fi.W, fi.q, fi.qi);
+    double *rowd = (double *)row;
+#pragma unroll
+    for (int j = 0; j < 16; j++) rowd[g + 16 * j] = x[j];  // centred doubles between passes
+}
+
+__global__ void __launch_bounds__(TPB) k_inv16_cols_c(PolySrc data, const uint8_t *mod_map, int per,
+                                                      const double *twdc, const ModConst *mc) {
+    __shared__ double sm[256 * 16];
+    FpInfo fi;
+    if (!fp_info(fi, data, blockIdx.x >> 4, mod_map, per, twdc, mc, true)) return;
+    const int tid = threadIdx.x, lc = tid & 15, g = tid >> 4;
+    const uint32_t col = (blockIdx.x & 15) * 16 + lc;
+    const double *pd = (const double *)fi.p;
+    double x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = pd[(16 * g + j) * 256 + col];
+    fphase_gs_c<16, 8>(x, col + 4096 * g, fi.W, fi.q, fi.qi);
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[(16 * g + j) * 16 + lc] = x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) x[j] = sm[(g + 16 * j) * 16 + lc];
+    fphase_gs_c<16, 12>(x, col + 256 * g, fi.W, fi.q, fi.qi);
+    const uint64_t ni = fi.mc->ninv, qq = fi.mc->q;
+    const double nic = ni > qq / 2 ? -(double)(qq - ni) : (double)ni;  // centred N^-1
+    __syncthreads();  // all reads of sm done before it is reused for the coalesced store
+#pragma unroll
+    for (int j = 0; j < 16; j++) sm[(g + 16 * j) * 16 + lc] = fmulmod_c(x[j], nic, fi.q, fi.qi);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; j++) fi.p[(g + 16 * j) * 256 + col] = fcanon(sm[(g + 16 * j) * 16 + lc], fi.q, fi.qi);
+}
+
 // ---------------------------------------------------------------- N = 2^12, one CTA per poly
 __global__ void __launch_bounds__(TPB) k_fwd12(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw,
                                                const ModConst *mc) {
@@ -260,7 +388,17 @@ __global__ void k_ntt_generic(PolySrc data, const uint8_t *mod_map, int per, con
 
 static int ntt_launch(he_ctx *c, PolySrc src, int n_polys, const uint8_t *mod_map, int per, bool inv, cudaStream_t s) {
     if (n_polys <= 0) return HE_OK;
-    if (c->logN == 16) {
+    if (c->logN == 16 && c->fp50) {  // every modulus < 2^50: centred FP64 butterflies
+        unsigned g = (unsigned)n_polys * 16;
+        if (!inv) {
+            k_fwd16_cols_c<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_twdc, c->d_mc);
+            k_fwd16_rows_c<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_twdc, c->d_mc);
+        } else {
+            k_inv16_rows_c<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_twdc, c->d_mc);
+            k_inv16_cols_c<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_twdc, c->d_mc);
+        }
+        he_count_launch(1);
+    } else if (c->logN == 16) {
         unsigned g = (unsigned)n_polys * 16;
         if (!inv) {
             k_fwd16_cols<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);

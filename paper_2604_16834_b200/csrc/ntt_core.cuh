@@ -168,6 +168,78 @@ __device__ __forceinline__ void fphase_gs(double (&x)[16], uint32_t e0, const do
     fstage_gs<LOGN, LT0 + 2, 4>(x, e0, W, q, qi);
     fstage_gs<LOGN, LT0 + 3, 8>(x, e0, W, q, qi);
 }
+// ---------------------------------------------------------------- centred FP64 butterflies, q < 2^50
+// For primes below 2^50 the residues are integer-valued doubles kept small by
+// CENTRED reductions, and rounding to the nearest integer uses the 1.5*2^52
+// magic constant (FP64 pipe, no FRND on the XU pipe):
+//   fmulmod_c(a, w): w centred (|w| <= q/2), |a| < 2^52: h = a w, l = fma(a, w, -h),
+//     e = round(h / q) (|h/q| < 2^51, so the magic add rounds exactly), r = fma(-e, q, h) + l
+//     = a w - e q exactly, |r| < 1.01 q; every intermediate is an integer below 2^53.
+//   fred_c(x): x - round(x/q) q, |x| < 2^53 -> |x| <= q/2 + 1.
+// Forward (CT): u +- v grows by < 1.01 q per stage; reducing after every second
+// stage keeps multiply inputs below 2.02 q and sums below 3.03 q < 2^53.
+// Inverse (GS): the sum is reduced every stage, the difference (< 2.02 q) feeds
+// the product.  Kernels convert canonical uint64 on entry and canonicalise on
+// exit, so the bits at kernel boundaries are those of the integer path.
+constexpr double FP_RND = 6755399441055744.0;  // 1.5 * 2^52
+__device__ __forceinline__ double fmulmod_c(double a, double w, double q, double qi) {
+    const double h = a * w;
+    const double l = fma(a, w, -h);
+    const double e = fma(h, qi, FP_RND) - FP_RND;
+    return fma(-e, q, h) + l;
+}
+__device__ __forceinline__ double fred_c(double x, double q, double qi) {
+    const double e = fma(x, qi, FP_RND) - FP_RND;
+    return fma(-e, q, x);
+}
+template <int LOGN, int LM, int D, bool RED>
+__device__ __forceinline__ void fstage_ct_c(double (&x)[16], uint32_t e0, const double *__restrict__ W, double q,
+                                            double qi) {
+    const uint32_t base = (1u << LM) + (e0 >> (LOGN - LM));
+#pragma unroll
+    for (int k = 0; k < 8 / D; k++) {
+        const double w = __ldg(W + base + k);
+#pragma unroll
+        for (int jj = 0; jj < D; jj++) {
+            const double u = x[2 * D * k + jj], v = fmulmod_c(x[2 * D * k + jj + D], w, q, qi);
+            const double a = u + v, b = u - v;
+            x[2 * D * k + jj] = RED ? fred_c(a, q, qi) : a;
+            x[2 * D * k + jj + D] = RED ? fred_c(b, q, qi) : b;
+        }
+    }
+}
+template <int LOGN, int LM0>
+__device__ __forceinline__ void fphase_ct_c(double (&x)[16], uint32_t e0, const double *__restrict__ W, double q,
+                                            double qi) {
+    fstage_ct_c<LOGN, LM0, 8, false>(x, e0, W, q, qi);
+    fstage_ct_c<LOGN, LM0 + 1, 4, true>(x, e0, W, q, qi);
+    fstage_ct_c<LOGN, LM0 + 2, 2, false>(x, e0, W, q, qi);
+    fstage_ct_c<LOGN, LM0 + 3, 1, true>(x, e0, W, q, qi);
+}
+template <int LOGN, int LT, int D>
+__device__ __forceinline__ void fstage_gs_c(double (&x)[16], uint32_t e0, const double *__restrict__ W, double q,
+                                            double qi) {
+    const uint32_t base = (1u << (LOGN - 1 - LT)) + (e0 >> (LT + 1));
+#pragma unroll
+    for (int k = 0; k < 8 / D; k++) {
+        const double w = __ldg(W + base + k);
+#pragma unroll
+        for (int jj = 0; jj < D; jj++) {
+            const double u = x[2 * D * k + jj], v = x[2 * D * k + jj + D];
+            x[2 * D * k + jj] = fred_c(u + v, q, qi);
+            x[2 * D * k + jj + D] = fmulmod_c(u - v, w, q, qi);
+        }
+    }
+}
+template <int LOGN, int LT0>
+__device__ __forceinline__ void fphase_gs_c(double (&x)[16], uint32_t e0, const double *__restrict__ W, double q,
+                                            double qi) {
+    fstage_gs_c<LOGN, LT0, 1>(x, e0, W, q, qi);
+    fstage_gs_c<LOGN, LT0 + 1, 2>(x, e0, W, q, qi);
+    fstage_gs_c<LOGN, LT0 + 2, 4>(x, e0, W, q, qi);
+    fstage_gs_c<LOGN, LT0 + 3, 8>(x, e0, W, q, qi);
+}
+
 __device__ __forceinline__ const double *twd_fwd(const double *twd, int m, int logN) {
     return twd + ((size_t)m << (logN + 1));
 }
