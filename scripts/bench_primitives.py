@@ -109,13 +109,22 @@ for name, fn in ops.items():
     if name.startswith("ntt"):
         bf = B * 2 * L * (N // 2) * 16
         res[name]["Gbutterfly_per_s"] = round(bf / (ms * 1e6), 1)
-ip = np.zeros(2)
+ip, fp = np.zeros(2), np.zeros(1)
 _lib.check(Lb.he_microbench_intpipe(eng.context.device, A(ip)))
-res["intpipe"] = {"imad32_per_s": ip[0], "mac128_per_s": ip[1]}
-for name in ops:  # integer roofline: algorithmic modular multiplications vs the measured 64x64->128 MAC rate
+_lib.check(Lb.he_microbench_fp64(eng.context.device, A(fp)))
+res["intpipe"] = {"imad32_per_s": ip[0], "mac128_per_s": ip[1], "fp64_modmul_per_s": fp[0]}
+# modular-product roofline: algorithmic modular multiplications (butterflies, BConv,
+# inner product) against the measured rate of the datapath they run on.  Every
+# config-2 prime is below 2^50, so the NTTs and every key-switch pass multiply on
+# the FP64 pipe (centred fmulmod_c); the BConv of the key switch stays integer.
+# int_frac: vs the faster measured rate (FP64 fmulmod), frac_vs_mac128: vs the
+# 64x64->128 multiply-accumulate rate (the integer datapath of round-1 v1).
+peak_mm = max(ip[1], fp[0])
+for name in ops:
     rate = modmuls[name] / (res[name]["ms"] * 1e-3)
     res[name]["Gmodmul_per_s"] = round(rate / 1e9, 1)
-    res[name]["int_frac"] = round(rate / ip[1], 3)
+    res[name]["int_frac"] = round(rate / peak_mm, 3)
+    res[name]["frac_vs_mac128"] = round(rate / ip[1], 3)
 
 if not args.no_oracle:   # bit-exact spot check of ct 0 for every op
     import oracle as O
