@@ -139,18 +139,35 @@ __global__ void __launch_bounds__(NTT_TPB) kf_cols(const Job *__restrict__ jobs,
 #pragma unroll
         for (int j = 0; j < 16; j++) x[j] = jb.src[(g + 16 * j) * 256 + col];
     } else if (LD == L_BCONV) {
-        // source-major: 16 independent loads in flight per source limb; with
+        // source-major, double-buffered: source s+1's 16 values per thread stream
+        // into shared memory with cp.async while source s is multiplied (each
+        // thread reads back only what it copied: no block barrier); with
         // v_s, t_s < q < 2^61 each product adds < q/8 to the high word, so
         // ns <= 8 terms keep hi < q without folding (redc's precondition)
+        extern __shared__ uint64_t stage[];  // [2][16 x 256]: this thread's slots (g + 16 j) * 16 + lc
+        auto issue = [&](int s) {
+            const uint64_t *src = jb.src + (size_t)s * NN + col;
+            uint64_t *dstp = stage + (s & 1) * 4096 + lc;
+#pragma unroll
+            for (int j = 0; j < 16; j++) cp_async8(dstp + (g + 16 * j) * 16, src + (g + 16 * j) * 256);
+            cp_async_commit();
+        };
         u128 acc[16];
 #pragma unroll
         for (int j = 0; j < 16; j++) acc[j] = u128{0, 0};
+        issue(0);
         for (int s = 0; s < jb.ns; s++) {
             const uint64_t t = __ldg(jb.tab + s);
-            const uint64_t *src = jb.src + (size_t)s * NN + col;
+            if (s + 1 < jb.ns) {
+                issue(s + 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            const uint64_t *vs = stage + (s & 1) * 4096 + lc;
             uint64_t v[16];
 #pragma unroll
-            for (int j = 0; j < 16; j++) v[j] = __ldg(src + (g + 16 * j) * 256);
+            for (int j = 0; j < 16; j++) v[j] = vs[(g + 16 * j) * 16];
 #pragma unroll
             for (int j = 0; j < 16; j++) mac128(acc[j], v[j], t);
             if ((s & 7) == 7)  // more than 8 sources: fold (hi < 2q -> < q)
@@ -622,6 +639,25 @@ int run_inverse(he_ctx *c, const std::vector<Job> &jobs, cudaStream_t s) {
     return HE_OK;
 }
 
+constexpr size_t KF_STAGE_BYTES = (size_t)2 * 4096 * sizeof(uint64_t);  // kf_cols<L_BCONV> source double buffer
+
+// kf_cols launch; the integer BConv loader stages its sources in 64 KB of dynamic smem
+template <int LD>
+int launch_kf_cols(unsigned grid, const Job *jobs, he_ctx *c, cudaStream_t s) {
+    const size_t smem = LD == L_BCONV ? KF_STAGE_BYTES : 0;
+    if (LD == L_BCONV) {
+        static bool attr = false;
+        if (!attr) {
+            HE_CHECK_CUDA(cudaFuncSetAttribute(kf_cols<L_BCONV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)KF_STAGE_BYTES));
+            attr = true;
+        }
+    }
+    kf_cols<LD><<<grid, NTT_TPB, smem, s>>>(jobs, c->d_tw, c->d_twdc, c->d_mc, c->d_rinvd);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
 template <int LD, int EP>
 int run_forward(he_ctx *c, const std::vector<Job> &jobs_in, cudaStream_t s) {
     if (jobs_in.empty()) return HE_OK;
@@ -643,11 +679,7 @@ int run_forward(he_ctx *c, const std::vector<Job> &jobs_in, cudaStream_t s) {
         kf_cols<L_BCONV_FPW><<<(unsigned)nfp * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twdc, c->d_mc, c->d_rinvd);
         HE_CHECK_LAUNCH();
     }
-    if (jobs.size() > nfp) {
-        kf_cols<LD><<<(unsigned)(jobs.size() - nfp) * 16, NTT_TPB, 0, s>>>(jb.d + nfp, c->d_tw, c->d_twdc, c->d_mc,
-                                                                          c->d_rinvd);
-        HE_CHECK_LAUNCH();
-    }
+    if (jobs.size() > nfp) HE_TRY(launch_kf_cols<LD>((unsigned)(jobs.size() - nfp) * 16, jb.d + nfp, c, s));
     const size_t pre_bytes = EP == E_SUBSCALE ? (size_t)2 * 4096 * sizeof(uint64_t) : 0;
     static bool attr = false;
     if (EP == E_SUBSCALE && !attr) {
@@ -746,9 +778,7 @@ static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64
             JobBuf jb(s);
             rc = jb.up(jobs);
             if (rc == HE_OK) {
-                kf_cols<L_BCONV><<<(unsigned)jobs.size() * 16, NTT_TPB, 0, s>>>(jb.d, c->d_tw, c->d_twdc, c->d_mc, c->d_rinvd);
-                he_count_launch(1);
-                if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+                rc = launch_kf_cols<L_BCONV>((unsigned)jobs.size() * 16, jb.d, c, s);  // counts the launch
             }
         }
     }

@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/ref.log 2>&1; echo "ref exit $?" >> gpurun_out/ref.log
-tail -2 gpurun_out/smoke.log; tail -2 gpurun_out/ref.log | cut -c1-700
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "pytest exit $?" >> gpurun_out/gpu_tests.log
+tail -2 gpurun_out/gpu_tests.log
+timeout 900 python scripts/bench_primitives.py > gpurun_out/prims.log 2>&1
+tail -1 gpurun_out/prims.log
