@@ -59,10 +59,10 @@ __global__ void __launch_bounds__(FFT_TPB) k_fft_chunk(double *re, double *im, i
     }
     __syncthreads();
     for (int lg = 1; lg <= B; lg++) {
-        const int len = 1 << lg, half = len >> 1;
+        const int half = 1 << (lg - 1);
         const size_t step = n >> lg;
         for (int b = threadIdx.x; b < (int)(csz >> 1); b += FFT_TPB) {
-            const int s = (b / half) * len, k = b % half;
+            const int s = (b >> (lg - 1)) << lg, k = b & (half - 1);
             fft_bfly(sr[s + k], si[s + k], sr[s + k + half], si[s + k + half], w, (size_t)k * step, sign);
         }
         __syncthreads();
