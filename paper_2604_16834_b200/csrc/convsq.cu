@@ -103,6 +103,28 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
                         bf[((((size_t)cg * KB + kb) * E + e) * 32 + lane) * 2 + r] = reg;
                     }
                 }
+    // tap-8 packing (one channel group, 40-bit limbs): [MGk][4 + E][lane][2], entry s = byte
+    // shift s; K word k (< 5) of the block is tap 8 of input byte plane k, so it carries
+    // weight digit s - k (zero outside 0 .. E-1); words 5..7 are zero
+    const int NSH8 = 4 + E;
+    std::vector<uint32_t> bf8(ncg == 1 ? (size_t)MGk * NSH8 * 32 * 2 : 0, 0);
+    if (ncg == 1)
+        for (int cg = 0; cg < MGk; cg++)
+            for (int sh = 0; sh < NSH8; sh++)
+                for (int lane = 0; lane < 32; lane++) {
+                    const int gid = lane >> 2, tig = lane & 3, m = cg * 8 + gid;
+                    for (int r = 0; r < 2; r++) {
+                        const int k = r * 4 + tig, e = sh - k;  // plane k, weight digit e
+                        uint32_t reg = 0;
+                        if (k < 5 && e >= 0 && e < E && m < M)
+                            for (int u = 0; u < 4; u++)
+                                if (u < p) {
+                                    const int dg = digit_s8(weights[(size_t)m * T + u * 9 + 8], e);
+                                    reg |= (uint32_t)(uint8_t)(int8_t)dg << (8 * u);
+                                }
+                        bf8[(((size_t)cg * NSH8 + sh) * 32 + lane) * 2 + r] = reg;
+                    }
+                }
     // per-limb constants: R^4, bias * R^-1, and R^-1, 2^32 R^-1 as doubles
     std::vector<uint64_t> r4(ell), bres(bias ? (size_t)M * ell : 0);
     std::vector<double> yc(2 * (size_t)ell);
@@ -149,10 +171,11 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
     void **din = nullptr, **dout = nullptr;
     HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
     HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
+    const size_t b_bf8 = bf8.size() * 4;
     const size_t b_bf = bf.size() * 4, b_lo = lorder.size() * 4, b_r4 = (size_t)ell * 8, b_b = bres.size() * 8,
                  b_c = cst ? (size_t)ell * 8 : 0, b_yc = yc.size() * 8;
     char *meta = nullptr;
-    HE_TRY(he_scratch_alloc((void **)&meta, b_bf + b_lo + b_r4 + b_b + b_c + b_yc + 160, s));
+    HE_TRY(he_scratch_alloc((void **)&meta, b_bf + b_bf8 + b_lo + b_r4 + b_b + b_c + b_yc + 192, s));
     size_t off = 0;
     auto carve = [&](size_t bytes) {
         char *p = meta + off;
@@ -160,6 +183,7 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
         return p;
     };
     uint32_t *dbf = (uint32_t *)carve(b_bf);
+    uint32_t *dbf8 = b_bf8 ? (uint32_t *)carve(b_bf8) : nullptr;
     int32_t *dlo = (int32_t *)carve(b_lo);
     uint64_t *dr4 = (uint64_t *)carve(b_r4);
     uint64_t *db = bias ? (uint64_t *)carve(b_b) : nullptr;
@@ -167,6 +191,7 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
     double *dyc = (double *)carve(b_yc);
     HE_CHECK_CUDA(he_h2d(dyc, yc.data(), b_yc, s));
     HE_CHECK_CUDA(he_h2d(dbf, bf.data(), b_bf, s));
+    if (dbf8) HE_CHECK_CUDA(he_h2d(dbf8, bf8.data(), b_bf8, s));
     HE_CHECK_CUDA(he_h2d(dlo, lorder.data(), b_lo, s));
     HE_CHECK_CUDA(he_h2d(dr4, r4.data(), b_r4, s));
     if (db) HE_CHECK_CUDA(he_h2d(db, bres.data(), b_b, s));
@@ -175,6 +200,7 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
     a.in = (const uint64_t *const *)din;
     a.out = (uint64_t *const *)dout;
     a.bfrag = dbf;
+    a.bfrag8 = dbf8;
     a.bias = db;
     a.cst = dc;
     a.r4 = dr4;

@@ -46,6 +46,7 @@ struct SqArgs {
     const uint64_t *const *in;  // [p*H*W] NCI-component input ciphertexts (device array of addresses)
     uint64_t *const *out;       // (2 NCI - 1)-component outputs, ell limbs
     const uint32_t *bfrag;      // [MG][KB][E][32] uint2 B fragments
+    const uint32_t *bfrag8;     // tap-8 packing (one channel group, 40-bit primes): [MG][4 + E][32] uint2
     const uint64_t *bias;       // [M][ell] bias * R^-1 mod q (component 0), or nullptr
     const uint64_t *cst;        // [ell] constant added to component 0 of every output, or nullptr
     const uint64_t *r4;         // [ell] R^4 mod q
@@ -184,22 +185,48 @@ __device__ __forceinline__ void digit_plane(const uint32_t *X, const int (&o0)[K
 // (one FP64 modular product) is returned as an integer-valued double,
 // NOT reduced: |y| < 2^48.2 (the square accumulator takes unreduced
 // operands).  Integer path: canonical y R^-1 (one Montgomery step) in yv.
-template <int KB, int E, int NB, int DSTR>
+// Tap-8 packing (one channel group: 9 taps = 9 K words, the second K block
+// would hold 1 real word): per plane only block 0 (taps 0..7) is multiplied;
+// tap 8 of ALL planes shares one block -- word k = tap 8 of plane k -- and is
+// multiplied once per byte shift s with B8[s] (word k = weight digit s - k),
+// which lands every product in its shift sum C[s].  NB * KB * E mma become
+// NB * E + NSH (conv1: 30 -> 22).  o0[1][0] / o1[1][0] carry this lane's tap-8
+// row offsets (plane 0); the block's words sit DSTR apart.
+template <int KB, int E, int NB, int DSTR, bool TP8 = false>
 __device__ __forceinline__ void tile_values(const uint32_t *X, const int (&o0)[KB][2], const int (&o1)[KB][2],
                                             const uint2 (&bw)[KB][E], const int (&mul)[4], const ModConst &c,
-                                            double yc1, double (&yd)[4], uint64_t (&yv)[4]) {
+                                            double yc1, double (&yd)[4], uint64_t (&yv)[4],
+                                            const uint2 *bw8 = nullptr) {
     constexpr int NSH = NB + E - 1;  // byte shifts 0 .. NB + E - 2
+    constexpr int KBM = TP8 ? 1 : KB;  // K blocks multiplied per plane
     int C[NSH][4];
 #pragma unroll
     for (int s = 0; s < NSH; s++) C[s][0] = C[s][1] = C[s][2] = C[s][3] = 0;
-    digit_plane<0, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
-    digit_plane<1, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
-    digit_plane<2, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
-    digit_plane<3, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
-    digit_plane<4, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
-    digit_plane<5, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
-    digit_plane<6, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
-    digit_plane<7, KB, E, NB, DSTR, NSH>(X, o0, o1, bw, C);
+    digit_plane<0, KBM, E, NB, DSTR, NSH>(X, (const int(&)[KBM][2])o0, (const int(&)[KBM][2])o1,
+                                          (const uint2(&)[KBM][E])bw, C);
+    digit_plane<1, KBM, E, NB, DSTR, NSH>(X, (const int(&)[KBM][2])o0, (const int(&)[KBM][2])o1,
+                                          (const uint2(&)[KBM][E])bw, C);
+    digit_plane<2, KBM, E, NB, DSTR, NSH>(X, (const int(&)[KBM][2])o0, (const int(&)[KBM][2])o1,
+                                          (const uint2(&)[KBM][E])bw, C);
+    digit_plane<3, KBM, E, NB, DSTR, NSH>(X, (const int(&)[KBM][2])o0, (const int(&)[KBM][2])o1,
+                                          (const uint2(&)[KBM][E])bw, C);
+    digit_plane<4, KBM, E, NB, DSTR, NSH>(X, (const int(&)[KBM][2])o0, (const int(&)[KBM][2])o1,
+                                          (const uint2(&)[KBM][E])bw, C);
+    digit_plane<5, KBM, E, NB, DSTR, NSH>(X, (const int(&)[KBM][2])o0, (const int(&)[KBM][2])o1,
+                                          (const uint2(&)[KBM][E])bw, C);
+    digit_plane<6, KBM, E, NB, DSTR, NSH>(X, (const int(&)[KBM][2])o0, (const int(&)[KBM][2])o1,
+                                          (const uint2(&)[KBM][E])bw, C);
+    digit_plane<7, KBM, E, NB, DSTR, NSH>(X, (const int(&)[KBM][2])o0, (const int(&)[KBM][2])o1,
+                                          (const uint2(&)[KBM][E])bw, C);
+    if constexpr (TP8) {
+        static_assert(NB <= 5, "tap-8 block holds one word per plane: planes 0..4 in words 0..4");
+        const int tig = threadIdx.x & 3;
+        const uint32_t *X0 = X + o0[1][0], *X1 = X + o1[1][0];
+        const uint32_t a0 = X0[tig * DSTR], a1 = X1[tig * DSTR];  // words tig: plane tig
+        const uint32_t a2 = tig == 0 ? X0[4 * DSTR] : 0u, a3 = tig == 0 ? X1[4 * DSTR] : 0u;  // word 4: plane 4
+#pragma unroll
+        for (int s = 0; s < NSH; s++) mma_u8s8(C[s], a0, a1, a2, a3, __ldg(bw8 + s * 32));
+    }
     int64_t P[3][4];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
@@ -421,12 +448,14 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
     constexpr int NCG = KB == 2 ? 1 : KB - 1;  // channel groups of 4 implied by the K blocks
     constexpr int DSTR = 8 * NCI * NCG;
     constexpr bool LS = NCI == 3 && KB == 5 && NB == 5;  // ldmatrix layout (4 channel groups)
+    constexpr bool TP8 = KB == 2 && NB == 5;               // tap-8 packing (one channel group)
 
     uint2 bw[KB][E];
 #pragma unroll
     for (int kb = 0; kb < KB; kb++)
 #pragma unroll
         for (int e = 0; e < E; e++) bw[kb][e] = ((const uint2 *)a.bfrag)[((cg * KB + kb) * E + e) * 32 + lane];
+    const uint2 *bw8 = TP8 ? (const uint2 *)a.bfrag8 + (size_t)cg * (4 + E) * 32 + lane : nullptr;
     const int mul[4] = {a.mul[0], a.mul[1], a.mul[2], a.mul[3]};
     const int m0 = cg * 8 + 2 * tig;  // this lane's channels m0, m0 + 1
     uint64_t bias[2] = {0, 0};
@@ -450,6 +479,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
             const int w = kb * 8 + h * 4 + tig;
             int t = w / a.ncg, g = w % a.ncg;
             if (t >= 9) t %= 9;  // zero-weight word: any in-bounds tap, spread over the banks
+            if (TP8 && kb == 1 && h == 0) t = 8, g = 0;  // tap-8 block base (every lane)
             const int r0 = rowpos<NCI>(g, gid), r1 = rowpos<NCI>(g, gid + 8);
             wd[kb][h] = (((t % 3) * a.pstr + r0) << 3) | (r1 < r0 ? 4 : 0) | (t / 3);
         }
@@ -501,7 +531,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
                     // fragment values: q=0,1 -> component 0, channels m0, m0+1; q=2,3 -> component 1
                     double yd[4];
                     uint64_t yv[4];
-                    tile_values<KB, E, NB, DSTR>(xs, o0, o1, bw, mul, c, yc1, yd, yv);
+                    tile_values<KB, E, NB, DSTR, TP8>(xs, o0, o1, bw, mul, c, yc1, yd, yv, bw8);
                     if constexpr (NB == 5) {
 #pragma unroll
                         for (int h = 0; h < 2; h++)
@@ -607,7 +637,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
                         }
                     double y2d[4];
                     uint64_t y2v[4];
-                    tile_values<KB, E, NB, DSTR>(xs, o0, o1, bw, mul, c, yc1, y2d, y2v);
+                    tile_values<KB, E, NB, DSTR, TP8>(xs, o0, o1, bw, mul, c, yc1, y2d, y2v, bw8);
 #pragma unroll
                     for (int k = 0; k < 2; k++) {  // T0 of pixel x + k
 #pragma unroll
@@ -619,7 +649,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
                             }
                         double yd[4];
                         uint64_t yv[4];
-                        tile_values<KB, E, NB, DSTR>(xs, o0, o1, bw, mul, c, yc1, yd, yv);
+                        tile_values<KB, E, NB, DSTR, TP8>(xs, o0, o1, bw, mul, c, yc1, yd, yv, bw8);
                         if constexpr (NB == 5) {
 #pragma unroll
                             for (int h = 0; h < 2; h++)
