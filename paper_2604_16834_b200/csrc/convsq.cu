@@ -107,7 +107,27 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
     // shift s; K word k (< 5) of the block is tap 8 of input byte plane k, so it carries
     // weight digit s - k (zero outside 0 .. E-1); words 5..7 are zero
     const int NSH8 = 4 + E;
-    std::vector<uint32_t> bf8(ncg == 1 ? (size_t)MGk * NSH8 * 32 * 2 : 0, 0);
+    const bool ls8 = ncg == 4 && nci == 3 && E == 2;  // ldmatrix path: [W0 | 0], [W0 | W1], [0 | W1] of tap 8
+    std::vector<uint32_t> bf8(ncg == 1 ? (size_t)MGk * NSH8 * 32 * 2 : ls8 ? (size_t)MGk * 3 * 32 * 2 : 0, 0);
+    if (ls8)
+        for (int cg = 0; cg < MGk; cg++)
+            for (int k = 0; k < 3; k++)
+                for (int lane = 0; lane < 32; lane++) {
+                    const int gid = lane >> 2, tig = lane & 3, m = cg * 8 + gid;
+                    for (int r = 0; r < 2; r++) {  // r = K half: 0 -> digit 0 (not for k = 2), 1 -> digit 1 (not k = 0)
+                        uint32_t reg = 0;
+                        const bool on = r == 0 ? k != 2 : k != 0;
+                        if (on && m < M)
+                            for (int u = 0; u < 4; u++) {
+                                const int i = 4 * tig + u;  // channel group tig of tap 8
+                                if (i < p) {
+                                    const int dg = digit_s8(weights[(size_t)m * T + i * 9 + 8], r);
+                                    reg |= (uint32_t)(uint8_t)(int8_t)dg << (8 * u);
+                                }
+                            }
+                        bf8[(((size_t)cg * 3 + k) * 32 + lane) * 2 + r] = reg;
+                    }
+                }
     if (ncg == 1)
         for (int cg = 0; cg < MGk; cg++)
             for (int sh = 0; sh < NSH8; sh++)

@@ -292,10 +292,10 @@ __device__ __forceinline__ void ldsm4i(uint32_t addr, uint32_t &a0, uint32_t &a1
 // (bytes, plane 0) of matrix lane/8, row lane%8.  Three independent tiles are
 // interleaved so their mma chains overlap: y[0] = T1 at ad[0][kb], y[1] = T0 of
 // pixel x at ad[1][kb], y[2] = T0 of pixel x + 1 at ad[1][kb] + PSTRB.
-template <int D, int KB, int E, int DSTRB, int PSTRB, int NSH>
+template <int D, int KB, int E, int DSTRB, int PSTRB, int NSH, int KBM = KB>
 __device__ __forceinline__ void plane_ls(const uint32_t (&ad)[2][KB], const uint2 (&bw)[KB][E], int (&C)[3][NSH][4]) {
 #pragma unroll
-    for (int kb = 0; kb < KB; kb++) {
+    for (int kb = 0; kb < KBM; kb++) {  // K blocks 0 .. KBM-1 of the plane
         uint32_t a[3][4];
         ldsm4i<D * DSTRB>(ad[0][kb], a[0][0], a[0][1], a[0][2], a[0][3]);
         ldsm4i<D * DSTRB>(ad[1][kb], a[1][0], a[1][1], a[1][2], a[1][3]);
@@ -307,21 +307,64 @@ __device__ __forceinline__ void plane_ls(const uint32_t (&ad)[2][KB], const uint
     }
 }
 
-template <int KB, int E, int DSTRB, int PSTRB>
+// LS8 (E = 2): the last K block (tap 8 + 4 zero words) is not multiplied per
+// plane; instead one block per byte shift s holds [tap 8 of plane s | tap 8 of
+// plane s - 1] against [W0 | W1] (halves outside 0..4 read a valid plane with
+// zero weights): 5 x 2 mma per tile become 6.  ad[*][KB-1] addresses tap 8 of
+// plane 0 for every lane; lanes of matrices 2, 3 (h1) read plane s - 1.
+template <int T, int S, int DSTRB, int PSTRB>
+__device__ __forceinline__ void tap8_ls(uint32_t base, uint32_t baseh, int (&C)[3][6][4], uint2 b) {
+    uint32_t a0, a1, a2, a3;
+    constexpr int OFF = (T == 2 ? PSTRB : 0);
+    if (S == 0)
+        ldsm4i<OFF>(base, a0, a1, a2, a3);
+    else if (S == 5)
+        ldsm4i<4 * DSTRB + OFF>(base, a0, a1, a2, a3);
+    else
+        ldsm4i<S * DSTRB + OFF>(baseh, a0, a1, a2, a3);
+    mma_u8s8(C[T][S], a0, a1, a2, a3, b);
+}
+
+template <int KB, int E, int DSTRB, int PSTRB, bool LS8 = false>
 __device__ __forceinline__ void tile_values_ls(const uint32_t (&ad)[2][KB], const uint2 (&bw)[KB][E],
                                                const int (&mul)[4], const ModConst &c, double yc1,
-                                               double (&yd)[3][4]) {
+                                               double (&yd)[3][4], const uint2 (&b8)[3] = {}, int h1 = 0) {
     constexpr int NB = 5, NSH = NB + E - 1;
+    constexpr int KBM = LS8 ? KB - 1 : KB;
     int C[3][NSH][4];
 #pragma unroll
     for (int t = 0; t < 3; t++)
 #pragma unroll
         for (int s = 0; s < NSH; s++) C[t][s][0] = C[t][s][1] = C[t][s][2] = C[t][s][3] = 0;
-    plane_ls<0, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
-    plane_ls<1, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
-    plane_ls<2, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
-    plane_ls<3, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
-    plane_ls<4, KB, E, DSTRB, PSTRB, NSH>(ad, bw, C);
+    plane_ls<0, KB, E, DSTRB, PSTRB, NSH, KBM>(ad, bw, C);
+    plane_ls<1, KB, E, DSTRB, PSTRB, NSH, KBM>(ad, bw, C);
+    plane_ls<2, KB, E, DSTRB, PSTRB, NSH, KBM>(ad, bw, C);
+    plane_ls<3, KB, E, DSTRB, PSTRB, NSH, KBM>(ad, bw, C);
+    plane_ls<4, KB, E, DSTRB, PSTRB, NSH, KBM>(ad, bw, C);
+    if constexpr (LS8) {
+        static_assert(E == 2, "two planes per tap-8 block");
+        const uint32_t dh = h1 ? (uint32_t)DSTRB : 0u;  // h1 lanes: plane s - 1
+        const uint32_t b1 = ad[1][KB - 1], b0 = ad[0][KB - 1];
+        // (tile T and shift S are template constants: unrolled by hand)
+        tap8_ls<0, 0, DSTRB, PSTRB>(b0, b0 - dh, (int(&)[3][6][4])C, b8[0]);
+        tap8_ls<1, 0, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[0]);
+        tap8_ls<2, 0, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[0]);
+        tap8_ls<0, 1, DSTRB, PSTRB>(b0, b0 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<1, 1, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<2, 1, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<0, 2, DSTRB, PSTRB>(b0, b0 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<1, 2, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<2, 2, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<0, 3, DSTRB, PSTRB>(b0, b0 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<1, 3, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<2, 3, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<0, 4, DSTRB, PSTRB>(b0, b0 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<1, 4, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<2, 4, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[1]);
+        tap8_ls<0, 5, DSTRB, PSTRB>(b0, b0 - dh, (int(&)[3][6][4])C, b8[2]);
+        tap8_ls<1, 5, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[2]);
+        tap8_ls<2, 5, DSTRB, PSTRB>(b1, b1 - dh, (int(&)[3][6][4])C, b8[2]);
+    }
 #pragma unroll
     for (int t = 0; t < 3; t++) recombine_fp<NSH>(C[t], mul, c, yc1, yd[t]);
 }
@@ -449,6 +492,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
     constexpr int DSTR = 8 * NCI * NCG;
     constexpr bool LS = NCI == 3 && KB == 5 && NB == 5;  // ldmatrix layout (4 channel groups)
     constexpr bool TP8 = KB == 2 && NB == 5;               // tap-8 packing (one channel group)
+    constexpr bool LS8 = LS && E == 2;                     // tap-8 packing on the ldmatrix path
 
     uint2 bw[KB][E];
 #pragma unroll
@@ -456,6 +500,11 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
 #pragma unroll
         for (int e = 0; e < E; e++) bw[kb][e] = ((const uint2 *)a.bfrag)[((cg * KB + kb) * E + e) * 32 + lane];
     const uint2 *bw8 = TP8 ? (const uint2 *)a.bfrag8 + (size_t)cg * (4 + E) * 32 + lane : nullptr;
+    // LS tap-8 block fragments: [W0 | 0] (shift 0), [W0 | W1] (shifts 1..4), [0 | W1] (shift 5)
+    uint2 bw8ls[3] = {};
+    if (LS8)
+#pragma unroll
+        for (int k = 0; k < 3; k++) bw8ls[k] = ((const uint2 *)a.bfrag8)[((size_t)cg * 3 + k) * 32 + lane];
     const int mul[4] = {a.mul[0], a.mul[1], a.mul[2], a.mul[3]};
     const int m0 = cg * 8 + 2 * tig;  // this lane's channels m0, m0 + 1
     uint64_t bias[2] = {0, 0};
@@ -575,6 +624,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
             for (int kb = 0; kb < KB; kb++) {
                 int t = 2 * kb + (mi >> 1);
                 if (t >= 9) t -= 9;  // zero-weight half of the last K block
+                if (LS8 && kb == KB - 1) t = 8;  // tap-8 block: every lane addresses tap 8
 #pragma unroll
                 for (int pr = 0; pr < 2; pr++) {
                     const int dy = t / 3 + pr;
@@ -593,7 +643,7 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
                         ad[0][kb] = ad[1][kb] + dT1;
                     }
                     double y[3][4];
-                    tile_values_ls<KB, E, 4 * DSTR, 4 * PSTR>(ad, bw, mul, c, yc1, y);
+                    tile_values_ls<KB, E, 4 * DSTR, 4 * PSTR, LS8>(ad, bw, mul, c, yc1, y, bw8ls, mi >> 1);
 #pragma unroll
                     for (int k = 0; k < 2; k++)
 #pragma unroll
