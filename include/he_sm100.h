@@ -163,6 +163,18 @@ int he_automorphism(he_ctx *ctx, uint32_t galois_elt, const uint64_t *const *in,
                     int count, int ell, int n_comp, void *stream);
 int he_rotate(he_ctx *ctx, uint32_t galois_elt, const uint64_t *const *in, uint64_t *const *out,
               int count, int ell, void *stream);
+/* Hoisted rotations of `count` ciphertexts by R Galois elements gs[0..R-1]
+ * (oracle oc_rotate_hoisted): the key switch runs on the UNROTATED c1 with the
+ * hoisting key sigma_g^-1(key_g), c0 is added, then sigma_g moves both
+ * components; N = 2^16 shares ONE ModUp (INTT + basis extension + NTT pass 1)
+ * of c1 among the R rotations.  out: host array [R][count] of [2][ell][N]
+ * outputs.  Decrypts like he_rotate (np.roll, engine.py:276-283); limbs follow
+ * the hoisted contract.  Keys must be registered (HE_ENOKEY otherwise); the
+ * hoisting keys are derived on first use (he_gen_hoist_key). */
+int he_rotate_hoisted(he_ctx *ctx, const uint32_t *galois_elts, int R, const uint64_t *const *in,
+                      uint64_t *const *out, int count, int ell, void *stream);
+/* derive the hoisting key of galois element g from its switch key */
+int he_gen_hoist_key(he_ctx *ctx, uint32_t galois_elt, void *stream);
 
 /* feature-major linear layer (the batched form of conv_forward's k=1 path,
  * conv.py:109-173, and of feature-major conv / pool):

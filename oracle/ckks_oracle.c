@@ -866,6 +866,35 @@ void oc_rotate(const oc_ctx *c, const uint64_t *ct, uint32_t g, const uint64_t *
     free(k1);
 }
 
+/* Hoisting key for Galois element g: every polynomial of the switch key moved by
+ * sigma_{g^-1} (the inverse automorphism, g g^-1 = 1 mod 2N).  key -> hkey, both
+ * [dnum][2][L+K][N]. */
+void oc_hoist_key(const oc_ctx *c, const uint64_t *key, uint32_t g, uint64_t *hkey) {
+    const uint64_t twoN = 2 * (uint64_t)c->N;
+    uint32_t gi = 1;
+    while (((uint64_t)gi * g) % twoN != 1) gi += 2; /* g odd: an inverse exists */
+    const int np = c->dnum * 2 * (c->L + c->K);
+    for (int p = 0; p < np; p++) automorph_poly(c, key + (size_t)p * c->N, gi, hkey + (size_t)p * c->N);
+}
+
+/* Hoisted rotation (the contract of he_rotate_hoisted): ModUp of the UNROTATED c1,
+ * inner product with the hoisting key sigma_g^-1(key_g), ModDown, add c0, then
+ * sigma_g on both components:
+ *   (t0, t1) = (c0 + KS(c1, hkey).0, KS(c1, hkey).1),  out = (sigma_g t0, sigma_g t1).
+ * t0 + t1 sigma_g^-1(s) = c0 + c1 s, so out decrypts to sigma_g(m) under s.  The
+ * basis extension of c1 is shared by every rotation of the same ciphertext. */
+void oc_rotate_hoisted(const oc_ctx *c, const uint64_t *ct, uint32_t g, const uint64_t *hkey, uint64_t *out,
+                       int ell) {
+    size_t P = (size_t)ell * c->N;
+    uint64_t *t = (uint64_t *)malloc(8 * 2 * P);
+    uint64_t *k0 = (uint64_t *)malloc(8 * P);
+    oc_keyswitch(c, ct + P, hkey, ell, k0, t + P);
+    oc_add(c, ct, k0, t, ell, 1);
+    oc_automorphism(c, t, g, out, 2 * ell);
+    free(t);
+    free(k0);
+}
+
 void oc_mult_ct(const oc_ctx *c, const uint64_t *a, const uint64_t *b, const uint64_t *rk, uint64_t *out,
                 int ell) {
     size_t P = (size_t)ell * c->N;

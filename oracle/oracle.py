@@ -77,6 +77,8 @@ def lib():
         L.oc_rescale.argtypes = [vp, u64p, u64p, C.c_int, C.c_int]
         L.oc_automorphism.argtypes = [vp, u64p, C.c_uint32, u64p, C.c_int]
         L.oc_rotate.argtypes = [vp, u64p, C.c_uint32, u64p, u64p, C.c_int]
+        L.oc_hoist_key.argtypes = [vp, u64p, C.c_uint32, u64p]
+        L.oc_rotate_hoisted.argtypes = [vp, u64p, C.c_uint32, u64p, u64p, C.c_int]
         L.oc_mult_ct.argtypes = [vp, u64p, u64p, u64p, u64p, C.c_int]
         L.oc_plain_to_ntt.argtypes = [vp, i64p, u64p, C.c_int]
         L.oc_lincomb.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.c_int, C.POINTER(C.c_int32),
@@ -288,6 +290,21 @@ class Oracle:
         polys = np.ascontiguousarray(polys, dtype=np.uint64)
         out = np.zeros_like(polys)
         lib().oc_automorphism(self._h, _u64(polys), g, _u64(out), polys.size // self.N)
+        return out
+
+    def hoist_key(self, key, g):
+        """sigma_{g^-1} applied to every polynomial of switch key `key` (oc_hoist_key)."""
+        key = np.ascontiguousarray(key, dtype=np.uint64)
+        out = np.zeros_like(key)
+        lib().oc_hoist_key(self._h, _u64(key), g, _u64(out))
+        return out
+
+    def rotate_hoisted(self, ct, g, hkey):
+        """Hoisted rotation (oc_rotate_hoisted): KS of the unrotated c1 with the
+        hoisting key, + c0, then sigma_g on both components."""
+        ct = np.ascontiguousarray(ct, dtype=np.uint64)
+        out = np.zeros_like(ct)
+        lib().oc_rotate_hoisted(self._h, _u64(ct), g, _u64(hkey), _u64(out), ct.shape[1])
         return out
 
     def rotate(self, ct, g, key):

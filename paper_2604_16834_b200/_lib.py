@@ -36,6 +36,8 @@ EXPORTS = [
     "he_microbench_intpipe", "he_square_sum", "he_conv_mma", "he_relin_rescale", "he_relin_rescale_n", "he_conv_square_sum", "he_conv_square_sum_n",
     "he_microbench_fp64",
     "he_microbench_imma",
+    "he_rotate_hoisted",
+    "he_gen_hoist_key",
 ]
 
 
@@ -111,6 +113,8 @@ def load():
         "he_microbench_intpipe": (i, [i, vp]),
         "he_microbench_fp64": (i, [i, vp]),
         "he_microbench_imma": (i, [i, vp]),
+        "he_rotate_hoisted": (i, [vp, vp, i, pp, pp, i, i, vp]),
+        "he_gen_hoist_key": (i, [vp, u32, vp]),
         "he_square_sum": (i, [vp, pp, i, pp, i, vp, vp, vp, i, vp]),
         "he_conv_mma": (i, [vp, pp, i, pp, i, i, vp, vp, i, i, i, vp, vp, i, i, vp]),
         "he_conv_square_sum": (i, [vp, pp, i, i, i, pp, i, i, i, i, vp, vp, vp, i, vp]),

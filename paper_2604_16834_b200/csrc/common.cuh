@@ -47,6 +47,8 @@ struct BconvTable {
     int32_t *d_dst_mod; // [n_dst] modulus index of each target
 };
 
+constexpr uint32_t HE_HOIST_CODE = 0x80000000u;  // key-map code of a hoisting key
+
 struct he_ctx {
     he_params prm;
     int N, logN, L, K, alpha, dnum, nslots, device;
@@ -62,7 +64,7 @@ struct he_ctx {
     double *d_twist = nullptr;       // [nslots][2]  zeta^j
     int32_t *d_slot_brv = nullptr;   // [nslots]     brv(pos[i]): slot i <-> FFT input index
     uint8_t *d_ident = nullptr;      // [HE_MAXM]    identity modulus map
-    std::map<uint32_t, uint64_t *> keys;            // [dnum][2][L+K][N] Montgomery form
+    std::map<uint32_t, uint64_t *> keys;            // [dnum][2][L+K][N] Montgomery form (HE_HOIST_CODE | g: hoisting keys)
     std::map<uint64_t, BconvTable> modup_tab;       // key = ell*64 + digit
     std::map<int, BconvTable> moddown_tab;          // key = ell
     std::vector<uint64_t> h_pmodq, h_pinv;          // P mod q_i, P^-1 mod q_i (i < L)
@@ -83,6 +85,9 @@ int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d,
                        const uint64_t *const *add1, cudaStream_t s);
 int he_rescale_fused(he_ctx *c, const uint64_t *const *in, uint64_t *const *out, int B, int ell, int nc,
                      cudaStream_t s);
+int he_hoisted_ks_fused(he_ctx *c, const uint64_t *const *hkeys, int R, const uint64_t *const *c0,
+                        const uint64_t *const *c1, const uint64_t *const *c1_dev, int B, int ell,
+                        uint64_t *const *t0, uint64_t *const *t1, cudaStream_t s);
 
 // ---------------------------------------------------------------- errors
 

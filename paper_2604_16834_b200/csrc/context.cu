@@ -589,14 +589,47 @@ extern "C" int he_gen_switch_key(he_ctx *c, uint32_t g, void *stream) {
     return HE_OK;
 }
 
+// Hoisting key of Galois element g (oracle oc_hoist_key): the switch key with
+// every polynomial moved by sigma_{g^-1}; stored under HE_HOIST_CODE | g.
+extern "C" int he_gen_hoist_key(he_ctx *c, uint32_t g, void *stream) {
+    if (!c || g % 2 == 0 || g >= 2u * (uint32_t)c->N) {
+        he_set_error("he_gen_hoist_key: %u is not a galois element", g);
+        return HE_EINVAL;
+    }
+    if (he_get_key(c, HE_HOIST_CODE | g)) return HE_OK;
+    const uint64_t *key = he_get_key(c, g);
+    if (!key) {
+        he_set_error("no rotation key for galois element %u", g);
+        return HE_ENOKEY;
+    }
+    const uint64_t twoN = 2 * (uint64_t)c->N;
+    uint32_t gi = 1;
+    while (((uint64_t)gi * g) % twoN != 1) gi += 2;
+    const size_t np = (size_t)c->dnum * 2 * (c->L + c->K);
+    uint64_t *hk = nullptr;
+    if (cudaMalloc(&hk, np * c->N * 8) != cudaSuccess) {
+        he_set_error("cudaMalloc hoisting key failed");
+        return HE_ENOMEM;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    k_automorph<<<ceil_div(np * c->N, 256), 256, 0, s>>>(hk, key, np, c->logN, gi);
+    HE_CHECK_LAUNCH();
+    HE_CHECK_CUDA(cudaStreamSynchronize(s));
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->keys[HE_HOIST_CODE | g] = hk;
+    return HE_OK;
+}
+
 extern "C" int he_drop_switch_key(he_ctx *c, uint32_t g) {
     if (!c) return HE_EINVAL;
     std::lock_guard<std::mutex> lk(c->mu);
-    auto it = c->keys.find(g);
-    if (it != c->keys.end()) {
-        cudaDeviceSynchronize();
-        cudaFree(it->second);
-        c->keys.erase(it);
+    for (uint32_t code : {g, HE_HOIST_CODE | g}) {  // the key and its hoisting key
+        auto it = c->keys.find(code);
+        if (it != c->keys.end()) {
+            cudaDeviceSynchronize();
+            cudaFree(it->second);
+            c->keys.erase(it);
+        }
     }
     return HE_OK;
 }

@@ -704,10 +704,12 @@ Job blank() {
 // acc [B][2][ell+K][N] (NTT domain) = sum_k ModUp(d_k) . keys[k].  d (HOST) and
 // d_dev (DEVICE) list the components [nk][B]; dcv [nk][B][ell][N] and ext
 // [nk][B][beta][ell+K][N] are caller-provided scratch.
-static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64_t *const *d,
-                    const uint64_t *const *d_dev, int B, int ell, uint64_t *dcv, uint64_t *ext, uint64_t *acc,
-                    cudaStream_t s) {
-    const int L = c->L, K = c->K, alpha = c->alpha, M = L + K;
+// ModUp steps 1-2 (INTT of d with the per-source q-hat^-1 folded in, BConv + NTT
+// pass 1 of every extended limb into ext).  ext is not modified by step 3, so
+// one ModUp serves every key applied to the same d (hoisted rotations).
+static int modup_prep(he_ctx *c, int nk, const uint64_t *const *d, int B, int ell, uint64_t *dcv, uint64_t *ext,
+                      cudaStream_t s) {
+    const int L = c->L, K = c->K, alpha = c->alpha;
     const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
     int rc = HE_OK;
     std::vector<const BconvTable *> up(beta);
@@ -782,8 +784,17 @@ static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64
             }
         }
     }
-    // 3. ModUp pass 2 fused with the key inner product
-    if (rc == HE_OK) {
+    return rc;
+}
+
+// ModUp step 3: NTT pass 2 of every extended limb fused with the inner product
+// against `keys` (sum over the nk components of d), into acc [B][2][ext_n][N].
+static int modup_ip3(he_ctx *c, const uint64_t *const *keys, int nk, const uint64_t *const *d_dev, int B, int ell,
+                     uint64_t *ext, uint64_t *acc, cudaStream_t s) {
+    const int L = c->L, K = c->K, alpha = c->alpha, M = L + K;
+    const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
+    int rc = HE_OK;
+    {
         IpArgs a;
         a.ext = ext;
         a.d = d_dev;
@@ -833,25 +844,21 @@ static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64
     return rc;
 }
 
-// Fused hybrid key switch for B ciphertexts (N = 2^16).  Pointer arguments are
-// HOST arrays of device addresses; d_dev is the same list of d pointers in
-// device memory (read by the inner-product kernel).
-int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d, const uint64_t *const *d_dev, int B,
-                       int ell, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *const *add0,
+static int modup_ip(he_ctx *c, const uint64_t *const *keys, int nk, const uint64_t *const *d,
+                    const uint64_t *const *d_dev, int B, int ell, uint64_t *dcv, uint64_t *ext, uint64_t *acc,
+                    cudaStream_t s) {
+    HE_TRY(modup_prep(c, nk, d, B, ell, dcv, ext, s));
+    return modup_ip3(c, keys, nk, d_dev, B, ell, ext, acc, s);
+}
+
+// ModDown of acc [B][2][ext_n][N]: INTT of the P limbs (times N^-1 phat_k^-1),
+// then the P -> Q BConv NTT whose epilogue writes (acc - conv) P^-1 (+ add0/add1)
+// to out0 / out1 (HOST arrays of device addresses; md: scratch [B][2][ell][N]).
+static int moddown_add(he_ctx *c, const BconvTable *dn, uint64_t *acc, uint64_t *md, int B, int ell,
+                       uint64_t *const *out0, uint64_t *const *out1, const uint64_t *const *add0,
                        const uint64_t *const *add1, cudaStream_t s) {
-    const int L = c->L, K = c->K, alpha = c->alpha;
-    const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
-    const size_t w_dc = (size_t)B * ell * NN, w_ext = (size_t)B * beta * ext_n * NN, w_acc = (size_t)B * 2 * ext_n * NN,
-                 w_md = (size_t)B * 2 * ell * NN;
-    void *scr = nullptr;
-    HE_TRY(he_scratch_alloc(&scr, (w_dc + w_ext + w_acc + w_md) * 8, s));
-    uint64_t *dcv = (uint64_t *)scr, *ext = dcv + w_dc, *acc = ext + w_ext, *md = acc + w_acc;
-    const BconvTable *dn = nullptr;
-    int rc = he_get_moddown_table(c, ell, &dn);
-    const uint64_t *keys[1] = {key};
-    if (rc == HE_OK) rc = modup_ip(c, keys, 1, d, d_dev, B, ell, dcv, ext, acc, s);
-    // 4. ModDown: INTT of the P limbs (times N^-1 * phat_k^-1), then the P->Q
-    //    BConv NTT whose epilogue writes (acc - conv) * P^-1 (+ d0 / d1)
+    const int L = c->L, K = c->K, ext_n = ell + K;
+    int rc = HE_OK;
     if (rc == HE_OK) {
         std::vector<Job> jobs;
         for (int b = 0; b < B; b++)
@@ -889,6 +896,54 @@ int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d,
                 }
             }
         rc = run_forward<L_BCONV, E_SUBSCALE>(c, jobs, s);
+    }
+    return rc;
+}
+
+// Fused hybrid key switch for B ciphertexts (N = 2^16).  Pointer arguments are
+// HOST arrays of device addresses; d_dev is the same list of d pointers in
+// device memory (read by the inner-product kernel).
+int he_keyswitch_fused(he_ctx *c, const uint64_t *key, const uint64_t *const *d, const uint64_t *const *d_dev, int B,
+                       int ell, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *const *add0,
+                       const uint64_t *const *add1, cudaStream_t s) {
+    const int L = c->L, K = c->K, alpha = c->alpha;
+    const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
+    const size_t w_dc = (size_t)B * ell * NN, w_ext = (size_t)B * beta * ext_n * NN, w_acc = (size_t)B * 2 * ext_n * NN,
+                 w_md = (size_t)B * 2 * ell * NN;
+    void *scr = nullptr;
+    HE_TRY(he_scratch_alloc(&scr, (w_dc + w_ext + w_acc + w_md) * 8, s));
+    uint64_t *dcv = (uint64_t *)scr, *ext = dcv + w_dc, *acc = ext + w_ext, *md = acc + w_acc;
+    const BconvTable *dn = nullptr;
+    int rc = he_get_moddown_table(c, ell, &dn);
+    const uint64_t *keys[1] = {key};
+    if (rc == HE_OK) rc = modup_ip(c, keys, 1, d, d_dev, B, ell, dcv, ext, acc, s);
+    if (rc == HE_OK) rc = moddown_add(c, dn, acc, md, B, ell, out0, out1, add0, add1, s);
+    he_scratch_free(scr, s);
+    return rc;
+}
+
+// Hoisted rotations, step 1 of he_rotate_hoisted (N = 2^16): for R hoisting keys,
+// t_r = (c0 + KS(c1, hkey_r).0, KS(c1, hkey_r).1) with ONE ModUp of c1 shared by
+// every rotation (oracle oc_rotate_hoisted; the caller applies sigma_g to t_r).
+// c0, c1: HOST arrays [B]; c1_dev: device array [B]; t0, t1: HOST arrays [R][B].
+int he_hoisted_ks_fused(he_ctx *c, const uint64_t *const *hkeys, int R, const uint64_t *const *c0,
+                        const uint64_t *const *c1, const uint64_t *const *c1_dev, int B, int ell,
+                        uint64_t *const *t0, uint64_t *const *t1, cudaStream_t s) {
+    const int K = c->K, alpha = c->alpha;
+    const int beta = (ell + alpha - 1) / alpha, ext_n = ell + K;
+    const size_t w_dc = (size_t)B * ell * NN, w_ext = (size_t)B * beta * ext_n * NN, w_acc = (size_t)B * 2 * ext_n * NN,
+                 w_md = (size_t)B * 2 * ell * NN;
+    void *scr = nullptr;
+    HE_TRY(he_scratch_alloc(&scr, (w_dc + w_ext + w_acc + w_md) * 8, s));
+    uint64_t *dcv = (uint64_t *)scr, *ext = dcv + w_dc, *acc = ext + w_ext, *md = acc + w_acc;
+    const BconvTable *dn = nullptr;
+    int rc = he_get_moddown_table(c, ell, &dn);
+    if (rc == HE_OK) rc = modup_prep(c, 1, c1, B, ell, dcv, ext, s);
+    for (int r = 0; r < R && rc == HE_OK; r++) {
+        const uint64_t *keys[1] = {hkeys[r]};
+        rc = modup_ip3(c, keys, 1, c1_dev, B, ell, ext, acc, s);
+        if (rc == HE_OK)
+            rc = moddown_add(c, dn, acc, md, B, ell, t0 + (size_t)r * B, t1 + (size_t)r * B, c0, nullptr, s);
     }
     he_scratch_free(scr, s);
     return rc;

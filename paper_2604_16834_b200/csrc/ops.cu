@@ -838,6 +838,75 @@ extern "C" int he_rotate(he_ctx *c, uint32_t g, const uint64_t *const *in, uint6
     return HE_OK;
 }
 
+// Hoisted rotations of `count` ciphertexts by R Galois elements (oracle
+// oc_rotate_hoisted): KS of the unrotated c1 with each hoisting key, + c0, then
+// sigma_g.  N = 2^16 shares one ModUp of c1 among the R rotations.
+// out: HOST array [R][count] of device [2][ell][N] outputs.
+extern "C" int he_rotate_hoisted(he_ctx *c, const uint32_t *gs, int R, const uint64_t *const *in,
+                                 uint64_t *const *out, int count, int ell, void *stream) {
+    HE_TRY(check_basic(c, count, ell, 2, "he_rotate_hoisted"));
+    if (R < 1 || !gs) {
+        he_set_error("he_rotate_hoisted: no rotations");
+        return HE_EINVAL;
+    }
+    std::vector<const uint64_t *> hk(R);
+    for (int r = 0; r < R; r++) {
+        if (!he_get_key(c, gs[r])) {
+            he_set_error("no rotation key for galois element %u", gs[r]);
+            return HE_ENOKEY;
+        }
+        HE_TRY(he_gen_hoist_key(c, gs[r], stream));
+        hk[r] = he_get_key(c, HE_HOIST_CODE | gs[r]);
+    }
+    if (!count) return HE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t P = (size_t)ell * c->N;
+    int ch = chunk_of(ks_bytes_per_ct(c, ell) + (size_t)R * 2 * P * 8, count);
+    for (int b0 = 0; b0 < count; b0 += ch) {
+        const int Bn = std::min(ch, count - b0);
+        Scratch sc(s);  // t_r for every rotation of the chunk: [R][Bn][2][ell][N]
+        HE_TRY(sc.alloc((size_t)R * Bn * 2 * P * 8));
+        std::vector<const uint64_t *> c0(Bn), c1(Bn);
+        std::vector<uint64_t *> t(R * (size_t)Bn), t0(R * (size_t)Bn), t1(R * (size_t)Bn), o(R * (size_t)Bn);
+        for (int i = 0; i < Bn; i++) {
+            c0[i] = in[b0 + i];
+            c1[i] = in[b0 + i] + P;
+        }
+        for (int r = 0; r < R; r++)
+            for (int i = 0; i < Bn; i++) {
+                const size_t k = (size_t)r * Bn + i;
+                t[k] = t0[k] = sc.u() + k * 2 * P;
+                t1[k] = t0[k] + P;
+                o[k] = out[(size_t)r * count + b0 + i];
+            }
+        DevPtrs C1(s);
+        HE_TRY(C1.up((const void *const *)c1.data(), Bn));
+        if (c->logN == 16) {
+            HE_TRY(he_hoisted_ks_fused(c, hk.data(), R, c0.data(), c1.data(), C1.as<const uint64_t>(), Bn, ell,
+                                       t0.data(), t1.data(), s));
+        } else {
+            DevPtrs C0(s);
+            HE_TRY(C0.up((const void *const *)c0.data(), Bn));
+            for (int r = 0; r < R; r++) {
+                DevPtrs T0(s), T1(s);
+                HE_TRY(T0.up((const void *const *)(t0.data() + (size_t)r * Bn), Bn));
+                HE_TRY(T1.up((const void *const *)(t1.data() + (size_t)r * Bn), Bn));
+                HE_TRY(keyswitch_chunk(c, hk[r], (uint64_t *const *)C1.as<uint64_t>(), Bn, ell, T0.as<uint64_t>(),
+                                       T1.as<uint64_t>(), C0.as<const uint64_t>(), nullptr, s));
+            }
+        }
+        for (int r = 0; r < R; r++) {  // sigma_g on both components of every t_r
+            DevPtrs T(s), O(s);
+            HE_TRY(T.up((const void *const *)(t.data() + (size_t)r * Bn), Bn));
+            HE_TRY(O.up((const void *const *)(o.data() + (size_t)r * Bn), Bn));
+            k_automorph_ptrs<<<grid_ew(2 * P, Bn), EW, 0, s>>>(O.as<uint64_t>(), T.as<const uint64_t>(), Bn, 2 * ell,
+                                                                c->logN, gs[r]);
+            HE_CHECK_LAUNCH();
+        }
+    }
+    return HE_OK;
+}
+
 extern "C" int he_lincomb(he_ctx *c, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
                           const int32_t *row_ptr, const int32_t *col, const int64_t *w, int ell, int nc, void *stream) {
     HE_TRY(check_basic(c, n_out, ell, nc, "he_lincomb"));

@@ -577,6 +577,48 @@ class GpuEngine:
         self._acct.bump("rotations")
         return self._rotate_batch([ct], k)[0]
 
+    def rotate_hoisted(self, cts: Sequence[CipherVec], ks: Sequence[int]) -> list[list[CipherVec]]:
+        """Rotate every ciphertext by every offset in ``ks`` with hoisted key
+        switching (he_rotate_hoisted): one basis extension of each c1 serves all
+        offsets -- the rotation set of the CBC convolution (conv.py:78-99,
+        PAPER.md:309-346).  Returns out[j][i] = rotate(cts[i], ks[j]) up to the
+        hoisted limb contract (same decryption).  Offsets k = 0 (mod n) return
+        the input handle (engine.py:278-279); others need a registered key
+        (MissingRotationKey, raised before any work) and count as rotations."""
+        for c in cts:
+            self._check(c)
+        if not cts:
+            return [[] for _ in ks]
+        if len({(c.level, c.data.shape[0]) for c in cts}) != 1:
+            raise HebatchError("rotate_hoisted needs 2-component inputs at one level")
+        live = []
+        for k in ks:
+            if k % self.context.n and not self.keys.holds(k):
+                raise MissingRotationKey(k)
+            if k % self.context.n and k % self.context.n not in live:
+                live.append(k % self.context.n)
+        res = {}
+        if live:
+            level = cts[0].level
+            gs = np.array([pow(5, k, 2 * self.N) for k in live], np.uint32)
+            out = self._alloc(len(live) * len(cts), 2, level + 1)
+            src = self._ptrs(cts)
+            dst = self._tptrs(out)
+            _lib.check(self._L.he_rotate_hoisted(self._h, _lib.addr(gs), len(live), _lib.addr(src), _lib.addr(dst),
+                                                 len(cts), level + 1, self.stream), "rotate_hoisted")
+            wrapped = self._wrap_batch(out, level, [c.scale for c in cts] * len(live))
+            for j, k in enumerate(live):
+                res[k] = wrapped[j * len(cts):(j + 1) * len(cts)]
+        outs = []
+        for k in ks:
+            kk = k % self.context.n
+            if kk == 0:
+                outs.append(list(cts))
+            else:
+                outs.append(res[kk])
+                self._acct.bump("rotations", len(cts))
+        return outs
+
     def _rotate_batch(self, cts: Sequence[CipherVec], k: int) -> list[CipherVec]:
         level = cts[0].level
         g = pow(5, k % self.context.n, 2 * self.N)

@@ -131,3 +131,22 @@ def test_five_component_relin_rescale():
         for k in range(extra):
             sc /= o.moduli[6 - k]
         assert np.max(np.abs(o.decrypt(r, sc) - a ** 4)) < 1e-5
+
+
+def test_hoisted_rotation_contract():
+    """oc_rotate_hoisted: KS of the unrotated c1 with sigma_g^-1(key_g), + c0, then
+    sigma_g -- decrypts to np.roll like the plain rotation, and equals that
+    composition of the oracle's own keyswitch / automorphism."""
+    o = O.Oracle(12, [60, 40, 40, 40, 40], [60], 1, seed=4)
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1, 1, o.n)
+    ca = o.encrypt(a, 0)
+    ell = ca.shape[1]
+    for k in (1, 5, o.n - 3):
+        g = O.galois_elt(k, o.N)
+        hk = o.hoist_key(o.switch_key(g), g)
+        r = o.rotate_hoisted(ca, g, hk)
+        assert np.max(np.abs(o.decrypt(r, o.scale) - np.roll(a, -k))) < 1e-5
+        k0, k1 = o.keyswitch(ca[1].copy(), hk)
+        t = np.stack([o.add(ca[:1], k0[None])[0], k1])
+        assert np.array_equal(r, o.automorphism(t, g).reshape(2, ell, o.N))
