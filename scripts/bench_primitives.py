@@ -40,6 +40,7 @@ g.manual_seed(1)
 for i, q in enumerate(eng.moduli[:L]):
     x[:, :, i] = torch.randint(0, q, (B, 2, N), generator=g, device=dev, dtype=torch.int64)
 out = torch.empty_like(x)
+out2 = torch.empty((2 * B, 2, L, N), dtype=torch.int64, device=dev)  # hoisted pair [rotation][ct]
 out_rs = torch.empty((B, 2, L - 1, N), dtype=torch.int64, device=dev)
 Lb = eng._L
 eng._ensure_relin()
@@ -50,6 +51,8 @@ torch.cuda.synchronize()
 
 ptr = lambda t: _lib.ptr_array([t.data_ptr() + i * t.stride(0) * 8 for i in range(t.shape[0])])
 px, po, prs = ptr(x), ptr(out), ptr(out_rs)
+po2 = ptr(out2)
+gpair = np.array([g1, g1024], np.uint32)
 pc1 = _lib.ptr_array([x.data_ptr() + i * x.stride(0) * 8 + L * N * 8 for i in range(B)])
 po0 = po
 po1 = _lib.ptr_array([out.data_ptr() + i * out.stride(0) * 8 + L * N * 8 for i in range(B)])
@@ -64,6 +67,8 @@ ops = {
     "rotate_1": lambda: Lb.he_rotate(eng._h, g1, A(px), A(po), B, L, s),
     "rotate_1024": lambda: Lb.he_rotate(eng._h, g1024, A(px), A(po), B, L, s),
     "rescale": lambda: Lb.he_rescale(eng._h, A(px), A(prs), B, L, 2, s),
+    # both rotations of every ciphertext with ONE ModUp of c1 (he_rotate_hoisted)
+    "rotate_1_and_1024_hoisted": lambda: Lb.he_rotate_hoisted(eng._h, A(gpair), 2, A(px), A(po2), B, L, s),
 }
 beta = -(-L // eng.context.alpha)
 poly = L * N * 8
@@ -74,6 +79,7 @@ alg_bytes = {
     "rotate_1": B * (2 * poly + 2 * poly) + 2 * beta * (L + K) * N * 8,
     "rotate_1024": B * (2 * poly + 2 * poly) + 2 * beta * (L + K) * N * 8,
     "rescale": B * (2 * poly + 2 * (L - 1) * N * 8),
+    "rotate_1_and_1024_hoisted": B * (2 * poly + 2 * 2 * poly) + 2 * 2 * beta * (L + K) * N * 8,
 }
 digits = [min(eng.context.alpha, L - j * eng.context.alpha) for j in range(beta)]
 bfly = (N // 2) * 16
@@ -89,6 +95,8 @@ modmuls = {
     "ntt_fwd": 2 * B * L * bfly, "ntt_inv": 2 * B * L * bfly,
     "keyswitch_relin": B * ks_modmuls(L), "rotate_1": B * ks_modmuls(L), "rotate_1024": B * ks_modmuls(L),
     "rescale": B * 2 * (1 + (L - 1)) * bfly,
+    # algorithmic work of two independent rotations (the hoisted form does less)
+    "rotate_1_and_1024_hoisted": 2 * B * ks_modmuls(L),
 }
 peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
@@ -145,6 +153,11 @@ if not args.no_oracle:   # bit-exact spot check of ct 0 for every op
     _lib.check(ops["keyswitch_relin"]())
     k0, k1 = orc.keyswitch(xn[1].copy(), orc.switch_key(0))
     chk["keyswitch_relin"] = bool(np.array_equal(out[0].cpu().numpy().view(np.uint64), np.stack([k0, k1])))
+    _lib.check(ops["rotate_1_and_1024_hoisted"]())
+    chk["rotate_hoisted"] = all(
+        bool(np.array_equal(out2[r * B].cpu().numpy().view(np.uint64),
+                            orc.rotate_hoisted(xn, gg, orc.hoist_key(orc.switch_key(gg), gg))))
+        for r, gg in enumerate((g1, g1024)))
     res["bit_exact_vs_oracle"] = chk
 print(json.dumps({"config": "cfg2: N=2^16, 24x50 + 4x50 bits, dnum 6", "cts": B, "reps": args.reps,
                   "hbm_peak_GBps": peaks["hbm_gbs"], "ops": res}))
