@@ -849,7 +849,7 @@ class GpuEngine:
         tmp = self._alloc(1, 2, limbs)
         pi, pt_, pm = self._ptrs([ct]), pt.data_ptr(), self._tptrs(tmp)
         _lib.check(self._L.he_mul_plain(self._h, _lib.addr(pi), pt_, _lib.addr(pm), 1, limbs, 2, self.stream))
-        return self._rescale_tensor(tmp, limbs, [ct.scale])
+        return self._rescale_tensor(tmp, limbs, [ct.scale])[0]
 
     def mul_const_batch(self, cts: Sequence[CipherVec], values: Sequence[float], count: bool = True,
                         out_scales: Sequence[float] | None = None) -> list[CipherVec]:

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python scripts/bench_primitives.py > gpurun_out/prims.log 2>&1
-tail -1 gpurun_out/prims.log
+timeout 1500 python -m pytest tests/test_gpu_networks.py -m gpu -x -q -k "cbc" > gpurun_out/t_cbc.log 2>&1; echo "exit $?" >> gpurun_out/t_cbc.log
+tail -25 gpurun_out/t_cbc.log

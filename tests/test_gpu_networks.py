@@ -224,3 +224,29 @@ def test_cfg3_min_level_encryption_and_network():
     got = eng.decrypt_batch(out).T
     ref = spec.forward_plain(wts, images[:512].reshape(512, 3, 32, 32))
     assert np.max(np.abs(got[:512] - ref)) < TOL
+
+
+def test_cbc_conv_forward_hoisted_rotations_cfg1_ring():
+    """The reference's CBC 3x3 layer (conv_forward k=3: align_inputs' 8 rotations
+    from 4 keys, here hoisted) through GpuEngine: decrypts to the direct
+    zero-padded convolution, rotation count as the reference loop's."""
+    from paper_2604_16834_b200 import configs
+    from paper_2604_16834_b200.conv import ConvSpec, conv_forward, conv_keys
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.packing import PackingLayout, pack_inputs, unpack_outputs
+
+    eng = GpuEngine(configs.context(1, seed=2))
+    lay = PackingLayout(n=2048, H=8, W=8, b=4, p=3)
+    eng.register_rotation_keys(conv_keys(lay))
+    rng = np.random.default_rng(5)
+    imgs = [rng.uniform(-1, 1, size=(3, 8, 8)) for _ in range(4)]
+    w = rng.normal(0, 0.3, size=(4, 3, 3, 3))
+    before = eng.snapshot_counters().rotations
+    outs = conv_forward(eng, pack_inputs(eng, imgs, lay), ConvSpec(w, np.zeros(4), lay))
+    assert eng.snapshot_counters().rotations - before == 3 * 8
+    x = np.stack(imgs)
+    xp = np.pad(x, ((0, 0), (0, 0), (1, 1), (1, 1)))
+    ref = sum(np.einsum("oi,bihw->bohw", w[:, :, dy, dx], xp[:, :, dy:dy + 8, dx:dx + 8])
+              for dy in range(3) for dx in range(3))
+    got = np.stack([unpack_outputs(o, lay, engine=eng) for o in outs], axis=1)
+    assert np.max(np.abs(got - ref.reshape(4, 4, 64))) < TOL
