@@ -391,7 +391,8 @@ class CnnSpec:
 
 
 def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, release_inputs: bool = True,
-            tile_outputs: int = 1024, lazy_relin: bool = True, carry: bool = True):
+            tile_outputs: int = 1024, lazy_relin: bool = True, carry: bool = True,
+            fused_tile_outputs: int = 1024):
     """Encrypted forward pass of ``spec`` over feature-major input ciphertexts.
 
     x_cts: C0*H*W ciphertexts (channel-major).  Each block is streamed over
@@ -399,7 +400,9 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
     channel (<= 32 per launch), then the tile is activated and pooled (or
     GAP-summed) before the next tile starts, so the full pre-pool activation
     map is never resident (config 3's conv1 output alone would be 223 GB).
-    ``tile_outputs`` bounds ciphertexts per launch.  Releases its inputs
+    ``tile_outputs`` bounds ciphertexts per launch (``fused_tile_outputs`` the
+    pooled window sums per fused conv launch: config 3's conv1 runs as 4 launches
+    of 1024; one launch of 4096 measured the same).  Releases its inputs
     unless ``release_inputs`` is False.  Returns the n_classes output
     ciphertexts.
 
@@ -446,7 +449,7 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
         # tiles only bound the 3-component window sums (about tile_outputs)
         fused = defer and getattr(engine, "use_fused_conv", False) and (last or pool)
         if fused and stream:
-            R = H if last else min(H, 2 * max(1, tile_outputs // (q * (W // 2))))
+            R = H if last else min(H, 2 * max(1, fused_tile_outputs // (q * (W // 2))))
         for r0 in range(0, H, R):
             rows = list(range(r0, min(H, r0 + R)))
             nr = len(rows)
