@@ -58,12 +58,38 @@ __global__ void __launch_bounds__(FFT_TPB) k_fft_chunk(double *re, double *im, i
         si[i] = im[base + i];
     }
     __syncthreads();
-    for (int lg = 1; lg <= B; lg++) {
-        const int half = 1 << (lg - 1);
-        const size_t step = n >> lg;
-        for (int b = threadIdx.x; b < (int)(csz >> 1); b += FFT_TPB) {
-            const int s = (b >> (lg - 1)) << lg, k = b & (half - 1);
-            fft_bfly(sr[s + k], si[s + k], sr[s + k + half], si[s + k + half], w, (size_t)k * step, sign);
+    // stages in register groups of up to three (radix-8 passes): a thread owns the
+    // 2^nst elements gbase + j 2^(lg0-1), closed under stages lg0 .. lg0+nst-1;
+    // every butterfly is the one k_fft_stage computes, in the same stage order
+    for (int lg0 = 1; lg0 <= B; lg0 += 3) {
+        const int nst = B - lg0 + 1 < 3 ? B - lg0 + 1 : 3, m = 1 << nst, h = 1 << (lg0 - 1);
+        for (int grp = threadIdx.x; grp < (int)(csz >> nst); grp += FFT_TPB) {
+            const int gbase = (grp & (h - 1)) + ((grp >> (lg0 - 1)) << (lg0 - 1 + nst));
+            double xr[8], xi[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (j < m) {
+                    xr[j] = sr[gbase + j * h];
+                    xi[j] = si[gbase + j * h];
+                }
+#pragma unroll
+            for (int st = 0; st < 3; st++) {
+                if (st >= nst) break;
+                const int lg = lg0 + st;
+                const size_t step = n >> lg;
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    if (j >= m || (j >> st) & 1) continue;
+                    const int k = (gbase & (h - 1)) + (j & ((1 << st) - 1)) * h;  // index inside the half
+                    fft_bfly(xr[j], xi[j], xr[j + (1 << st)], xi[j + (1 << st)], w, (size_t)k * step, sign);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (j < m) {
+                    sr[gbase + j * h] = xr[j];
+                    si[gbase + j * h] = xi[j];
+                }
         }
         __syncthreads();
     }
