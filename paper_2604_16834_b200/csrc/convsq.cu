@@ -45,6 +45,18 @@ int round_up_mod(int v, int mod, int rem) {  // smallest v' >= v with v' = rem (
 // (y0^2, 2 y0 y1, y1^2) or (y0^2, 2 y0 y1, 2 y0 y2 + y1^2, 2 y1 y2, y2^2) summed.  Tap order
 // k = i*9 + (dy+1)*3 + (dx+1).  Returns HE_EINVAL when a tensor-core bound
 // does not hold (p > 16, M > 32, |w| >= 2^23 or a prime below 2^36).
+// out[m] (canonical, [NO][ell][N]) += part[m] (mod q of the limb)
+__global__ void k_add_parts(uint64_t *const *out, const uint64_t *part, int M, int polys, int ell, int logN,
+                            const ModConst *mc) {
+    const size_t N = (size_t)1 << logN, per = (size_t)polys * N, tot = (size_t)M * per;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t m = i / per, r = i % per;
+        const uint64_t q = mc[(r >> logN) % ell].q;
+        uint64_t *o = out[m] + r;
+        *o = add_mod(*o, part[i], q);
+    }
+}
+
 extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nci, int p, int H, int W,
                                     uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
                                     const uint64_t *bias, const uint64_t *cst, int ell, void *stream) {
@@ -190,7 +202,21 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
     const int n_in = p * H * W, n_out = pool ? M * nwin : M;
     void **din = nullptr, **dout = nullptr;
     HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
-    HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
+    // column tiles (3-component GAP on the ldmatrix path, 40-bit limbs): two CTAs per
+    // (limb, coefficient chunk) each own half the columns, so the ring (and shared
+    // memory per CTA) halves and three CTAs fit an SM; tile 1 writes partial sums to
+    // scratch, added into out afterwards
+    const int tiles = (nci == 3 && !pool && ncg % 4 == 0 && W % 4 == 0 && W >= 16) ? 2 : 1;
+    const int NO = 2 * nci - 1;
+    uint64_t *part = nullptr;
+    std::vector<const uint64_t *> outs((const uint64_t *const *)out, (const uint64_t *const *)out + n_out);
+    if (tiles == 2) {
+        const size_t per = (size_t)NO * ell * c->N;
+        HE_TRY(he_scratch_alloc((void **)&part, (size_t)M * per * 8, s));
+        HE_CHECK_CUDA(cudaMemsetAsync(part, 0, (size_t)M * per * 8, s));
+        for (int m = 0; m < M; m++) outs.push_back(part + (size_t)m * per);
+    }
+    HE_TRY(he_upload_ptrs((const void *const *)outs.data(), (int)outs.size(), &dout, s));
     const size_t b_bf8 = bf8.size() * 4;
     const size_t b_bf = bf.size() * 4, b_lo = lorder.size() * 4, b_r4 = (size_t)ell * 8, b_b = bres.size() * 8,
                  b_c = cst ? (size_t)ell * 8 : 0, b_yc = yc.size() * 8;
@@ -245,9 +271,12 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
         // bank-conflict-free A loads: with 4 channel groups per tap the 4 groups
         // fill the 32 banks by themselves; otherwise consecutive taps must sit
         // 8 banks apart (pixel stride = 24, ring-row stride = 8 mod 32, 4 rows)
+        const bool tile_g = tiles == 2 && a.nb == 5;  // the ldmatrix kernel of this group takes tiles
+        a.x0 = 0;
+        a.Wt = tile_g ? W / 2 : W;
         if (ncg % 4 == 0) {
             a.pstr = a.nb * ncg * 8 * nci;
-            a.rstr = (W + 2) * a.pstr;
+            a.rstr = (a.Wt + 2) * a.pstr;
             a.R = pool ? 4 : 3;
         } else {
             a.pstr = round_up_mod(a.nb * ncg * 8 * nci, 32, 24);
@@ -255,17 +284,24 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
             a.R = 4;
         }
         // ring + one row's input-address table (8-byte aligned: rstr is even)
-        const size_t smem = (size_t)a.R * a.rstr * 4 + (size_t)p * W * 8;
+        const size_t smem = (size_t)a.R * a.rstr * 4 + (size_t)p * (a.Wt + 2) * 8;
         if (smem > 227 * 1024) {
             he_set_error("he_conv_square_sum: row ring needs %zu bytes of shared memory (W=%d too wide)", smem, W);
             rc = HE_EINVAL;
             break;
         }
-        dim3 grid((unsigned)(c->N / 8), (unsigned)g.second);
+        dim3 grid((unsigned)(c->N / 8), (unsigned)g.second, tile_g ? 2u : 1u);
         rc = nci == 2 ? dispatch_sq2(KB, E, MGk, grid, smem, s, a) : dispatch_sq3(KB, E, MGk, grid, smem, s, a);
         if (rc != HE_OK) break;
         first += g.second;
     }
+    if (rc == HE_OK && part) {  // out += tile-1 partial sums (zero for untiled limb groups)
+        k_add_parts<<<(unsigned)std::min<size_t>(((size_t)M * NO * ell * c->N + 255) / 256, (size_t)148 * 64), 256, 0,
+                      s>>>((uint64_t *const *)dout, part, M, NO * ell, ell, c->logN, c->d_mc);
+        he_count_launch(1);
+        if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+    }
+    if (part) he_scratch_free(part, s);
     he_scratch_free(meta, s);
     he_scratch_free(din, s);
     he_scratch_free(dout, s);

@@ -54,6 +54,7 @@ struct SqArgs {
     const ModConst *mc;
     const int32_t *limbs;       // [gridDim.y] limb handled by blockIdx.y (one byte-plane count per launch)
     int p, H, W, M, ell, logN, pool, y0, y1, nwin;
+    int x0, Wt;                 // column tile of blockIdx.z: output columns [x0 + z Wt, x0 + (z+1) Wt) (GAP)
     int ncg, nb, R;             // channel groups of 4, byte planes stored, ring rows
     int pstr, rstr;             // ring strides in 32-bit words: pixel, ring row
     int mul[4];                 // 1, 2^8, 2^16, 2^24
@@ -110,14 +111,20 @@ __device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, const 
     constexpr int RC = RW * NCG;   // tasks per pixel: (row, channel group)
     constexpr int DSTR = RC;       // words per byte plane of a pixel
     const size_t N = (size_t)1 << a.logN, compstr = (size_t)a.ell * N, base = (size_t)l * N + coff;
-    const int ntask = a.W * RC;
+    // ring slots [s_lo, s_lo + ns) <-> image columns xb - 1 + slot: the whole row
+    // (slots 1..W; the halo slots stay zero) or a column tile with its halo
+    const bool tiled = a.Wt < a.W;
+    const int xb = a.x0 + (int)blockIdx.z * a.Wt, s_lo = tiled ? 0 : 1, ns = tiled ? a.Wt + 2 : a.W;
+    const int ntask = ns * RC;
     const bool inside = yy >= 0 && yy < a.H;
-    // the row's input addresses (p x W) are staged in shared memory once, so no
+    // the row's input addresses (p x ns) are staged in shared memory once, so no
     // task waits on a dependent address-table load
     __syncthreads();  // the previous row's table is no longer read
     if (inside)
-        for (int k = threadIdx.x; k < a.p * a.W; k += CT)
-            prow[k] = a.in[(size_t)(k / a.W) * a.H * a.W + yy * a.W + k % a.W];
+        for (int k = threadIdx.x; k < a.p * ns; k += CT) {
+            const int x = xb - 1 + s_lo + k % ns;
+            prow[k] = (x >= 0 && x < a.W) ? a.in[(size_t)(k / ns) * a.H * a.W + yy * a.W + x] : nullptr;
+        }
     __syncthreads();
     // LU tasks per thread per batch: their data loads are all in flight before
     // the first transpose (one memory latency per batch)
@@ -133,7 +140,8 @@ __device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, const 
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int i = cg * 4 + u;
-                src[j][u] = (inside && t < ntask && i < a.p) ? prow[i * a.W + x] + off : nullptr;
+                const uint64_t *pr = (inside && t < ntask && i < a.p) ? prow[i * ns + x] : nullptr;
+                src[j][u] = pr ? pr + off : nullptr;
             }
         }
         uint64_t v[LU][4];
@@ -150,7 +158,7 @@ __device__ __forceinline__ void load_row(const SqArgs &a, uint32_t *slot, const 
             tr4((uint32_t)v[j][0], (uint32_t)v[j][1], (uint32_t)v[j][2], (uint32_t)v[j][3], lo);
             tr4((uint32_t)(v[j][0] >> 32), (uint32_t)(v[j][1] >> 32), (uint32_t)(v[j][2] >> 32),
                 (uint32_t)(v[j][3] >> 32), hi);
-            uint32_t *dst = slot + (x + 1) * a.pstr + rowpos<NCI, LS>(cg, r);
+            uint32_t *dst = slot + (x + s_lo) * a.pstr + rowpos<NCI, LS>(cg, r);
 #pragma unroll
             for (int d = 0; d < 4; d++) dst[d * DSTR] = lo[d];
 #pragma unroll
@@ -478,7 +486,7 @@ __device__ __forceinline__ uint64_t square_comp(const Acc &acc, int k, const Mod
 }
 
 template <int KB, int E, int MG, int NB, int NCI>
-__global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_sqsum(const SqArgs a) {
+__global__ void __launch_bounds__(CT, NCI == 3 ? 3 : (KB <= 2 ? 4 : 3)) k_conv_sqsum(const SqArgs a) {
     constexpr int PS = 4 / MG;
     constexpr int NO = 2 * NCI - 1;  // output components
     extern __shared__ __align__(16) uint32_t xs[];  // ring [R][rstr]
@@ -633,7 +641,8 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
                 }
             }
             const uint32_t dT1 = 4 * ((mi & 1) * (PSTR - 32) + 64);  // component 2, pixel x + (mi & 1)
-            for (int it = ps; it < nitems; it += PS) {
+            const int nit = a.Wt / 2;  // pixel pairs of this CTA's column tile
+            for (int it = ps; it < nit; it += PS) {
                 for (int pr = 0; pr < npair; pr++) {
                     uint32_t ad[2][KB];  // tile 0: T1 (component 2 of the pair), tile 1: T0 of x (x + 1 by offset)
                     const uint32_t xoff = 4 * 2 * it * PSTR;
@@ -766,12 +775,12 @@ __global__ void __launch_bounds__(CT, NCI == 3 ? 2 : (KB <= 2 ? 4 : 3)) k_conv_s
                             r[k][h] = add_mod(r[k][h], red[((o * MG + cg) * 32 + lane) * 2 * NO + k * 2 + h], c.q);
         }
         if (ps == 0) {
-            const uint64_t cst = a.cst ? a.cst[l] : 0;
+            const uint64_t cst = a.cst && blockIdx.z == 0 ? a.cst[l] : 0;  // the GAP constant once, not per tile
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 const int m = m0 + h;
                 if (m >= a.M) continue;
-                uint64_t *o = a.out[m] + coff + gid;
+                uint64_t *o = a.out[m + blockIdx.z * a.M] + coff + gid;  // tile z's partial sums
 #pragma unroll
                 for (int k = 0; k < NO; k++) {
                     uint64_t v = r[k][h];

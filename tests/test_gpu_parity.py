@@ -447,3 +447,32 @@ def test_rotate_hoisted_bit_exact(pair):
             # fresh-encryption noise at scale 2^40 over 32768 slots reaches ~1e-5 (the
             # oracle's own hoisted and plain rotations: 1.1e-5 / 4.6e-6 at N = 2^16)
             assert np.max(np.abs(eng.decrypt(outs[j][i]) - np.roll(vals[i], -k))) < 1e-4
+
+
+@pytest.mark.parametrize("nci", [3])
+def test_conv_square_sum_column_tiles_bit_exact(pair, nci):
+    """16-column GAP on the ldmatrix path runs as two column tiles (half rings,
+    3 CTAs/SM) whose partial sums are added: equal to the oracle chain."""
+    import torch
+
+    name, eng, orc = pair
+    if name not in ("tiny", "cfg1"):
+        pytest.skip("oracle time")
+    rng = np.random.default_rng(77)
+    p, M, H = 16, 32, 16
+    W = H
+    ell = eng.context.n_q
+    mods = eng.moduli[:ell]
+    x = rand_residues(rng, mods, (p * H * W, nci), eng.N)
+    ins = [from_np(x[i], eng.device) for i in range(p * H * W)]
+    wi = rng.integers(-(1 << 14), 1 << 14, size=(M, 9 * p), dtype=np.int64)
+    bres = np.array([[int(rng.integers(0, q)) for q in mods] for _ in range(M)], np.uint64)
+    cst = np.array([int(rng.integers(0, q)) for q in mods], np.uint64)
+    outs = [torch.empty((2 * nci - 1, ell, eng.N), dtype=torch.int64, device=eng.device) for _ in range(M)]
+    pi, po = _ptrs(ins), _ptrs(outs)
+    rc = _lib(eng).he_conv_square_sum_n(eng._h, pi.ctypes.data, nci, p, H, W, po.ctypes.data, M, 0, 0, H,
+                                        wi.ctypes.data, bres.ctypes.data, cst.ctypes.data, ell, None)
+    assert rc == 0, eng._L.he_last_error()
+    ref = _oracle_conv_square_sum(orc, [x[i] for i in range(p * H * W)], p, H, W, wi, bres, cst, 0, 0, H)
+    for k, (o, r) in enumerate(zip(outs, ref)):
+        assert np.array_equal(to_np(o), r), k
