@@ -210,11 +210,12 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
     const int NO = 2 * nci - 1;
     uint64_t *part = nullptr;
     std::vector<const uint64_t *> outs((const uint64_t *const *)out, (const uint64_t *const *)out + n_out);
-    if (tiles == 2) {
-        const size_t per = (size_t)NO * ell * c->N;
-        HE_TRY(he_scratch_alloc((void **)&part, (size_t)M * per * 8, s));
-        HE_CHECK_CUDA(cudaMemsetAsync(part, 0, (size_t)M * per * 8, s));
-        for (int m = 0; m < M; m++) outs.push_back(part + (size_t)m * per);
+    if (tiles > 1) {  // tiles 1 .. T-1 write partial sums to scratch [T-1][M][NO][ell][N]
+        const size_t per = (size_t)NO * ell * c->N, bytes = (size_t)(tiles - 1) * M * per * 8;
+        HE_TRY(he_scratch_alloc((void **)&part, bytes, s));
+        HE_CHECK_CUDA(cudaMemsetAsync(part, 0, bytes, s));
+        for (int z = 1; z < tiles; z++)
+            for (int m = 0; m < M; m++) outs.push_back(part + ((size_t)(z - 1) * M + m) * per);
     }
     HE_TRY(he_upload_ptrs((const void *const *)outs.data(), (int)outs.size(), &dout, s));
     const size_t b_bf8 = bf8.size() * 4;
@@ -271,9 +272,9 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
         // bank-conflict-free A loads: with 4 channel groups per tap the 4 groups
         // fill the 32 banks by themselves; otherwise consecutive taps must sit
         // 8 banks apart (pixel stride = 24, ring-row stride = 8 mod 32, 4 rows)
-        const bool tile_g = tiles == 2 && a.nb == 5;  // the ldmatrix kernel of this group takes tiles
+        const bool tile_g = tiles > 1 && a.nb == 5;  // the ldmatrix kernel of this group takes tiles
         a.x0 = 0;
-        a.Wt = tile_g ? W / 2 : W;
+        a.Wt = tile_g ? W / tiles : W;
         if (ncg % 4 == 0) {
             a.pstr = a.nb * ncg * 8 * nci;
             a.rstr = (a.Wt + 2) * a.pstr;
@@ -290,16 +291,19 @@ extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nc
             rc = HE_EINVAL;
             break;
         }
-        dim3 grid((unsigned)(c->N / 8), (unsigned)g.second, tile_g ? 2u : 1u);
+        dim3 grid((unsigned)(c->N / 8), (unsigned)g.second, tile_g ? (unsigned)tiles : 1u);
         rc = nci == 2 ? dispatch_sq2(KB, E, MGk, grid, smem, s, a) : dispatch_sq3(KB, E, MGk, grid, smem, s, a);
         if (rc != HE_OK) break;
         first += g.second;
     }
     if (rc == HE_OK && part) {  // out += tile-1 partial sums (zero for untiled limb groups)
-        k_add_parts<<<(unsigned)std::min<size_t>(((size_t)M * NO * ell * c->N + 255) / 256, (size_t)148 * 64), 256, 0,
-                      s>>>((uint64_t *const *)dout, part, M, NO * ell, ell, c->logN, c->d_mc);
-        he_count_launch(1);
-        if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+        for (int z = 1; z < tiles && rc == HE_OK; z++) {
+            k_add_parts<<<(unsigned)std::min<size_t>(((size_t)M * NO * ell * c->N + 255) / 256, (size_t)148 * 64), 256,
+                          0, s>>>((uint64_t *const *)dout, part + (size_t)(z - 1) * M * NO * ell * c->N, M, NO * ell,
+                                  ell, c->logN, c->d_mc);
+            he_count_launch(1);
+            if (cudaGetLastError() != cudaSuccess) rc = HE_ECUDA;
+        }
     }
     if (part) he_scratch_free(part, s);
     he_scratch_free(meta, s);

@@ -40,6 +40,10 @@
 
 namespace convsq {
 
+#ifndef CONV2_CTAS
+#define CONV2_CTAS 3  // resident CTAs/SM of the 3-component, 4-group kernel (2 column tiles; 4 tiles at 4 CTAs measured slower)
+#endif
+
 constexpr int CT = 128;  // 4 warps: MG channel groups x PS pixel streams
 
 struct SqArgs {
@@ -486,7 +490,7 @@ __device__ __forceinline__ uint64_t square_comp(const Acc &acc, int k, const Mod
 }
 
 template <int KB, int E, int MG, int NB, int NCI>
-__global__ void __launch_bounds__(CT, NCI == 3 ? 3 : (KB <= 2 ? 4 : 3)) k_conv_sqsum(const SqArgs a) {
+__global__ void __launch_bounds__(CT, NCI == 3 ? (KB == 5 ? CONV2_CTAS : 2) : (KB <= 2 ? 4 : 3)) k_conv_sqsum(const SqArgs a) {
     constexpr int PS = 4 / MG;
     constexpr int NO = 2 * NCI - 1;  // output components
     extern __shared__ __align__(16) uint32_t xs[];  // ring [R][rstr]
