@@ -201,3 +201,34 @@ def test_activation_folding_algebra():
     y = a * x
     assert np.allclose(y * (y * y + 0.5 / a) + 0.5, cub(x))
     assert configs.CNN3.levels_needed() == 5 and configs.CNN4.levels_needed() == 13
+
+
+class HoistSlotEngine(SlotEngine):
+    """SlotEngine with the batched rotate_hoisted entry (out[j][i] = rotate(cts[i], ks[j]))."""
+
+    def __init__(self, n):
+        super().__init__(n)
+        self.hoist_calls = []
+
+    def rotate_hoisted(self, cts, ks):
+        self.hoist_calls.append((len(cts), tuple(ks)))
+        return [[self.rotate(c, k) for c in cts] for k in ks]
+
+
+def test_align_inputs_hoisted_path_matches_rotation_path():
+    """conv.align_inputs on an engine with rotate_hoisted: two hoisted calls (+-1 on
+    the input, +-W on the three row copies), the same nine aligned slot vectors and
+    the same 8 rotations as the reference's rotation loop."""
+    from paper_2604_16834_b200.conv import align_inputs
+
+    lay = PackingLayout(n=256, H=8, W=8, b=2, p=1)
+    plain, hoisted = SlotEngine(256), HoistSlotEngine(256)
+    for e in (plain, hoisted):
+        e.register_rotation_keys(conv_keys(lay))
+    v = np.random.default_rng(1).normal(size=256)
+    a = align_inputs(plain, plain.encrypt(v), lay)
+    b = align_inputs(hoisted, hoisted.encrypt(v), lay)
+    assert hoisted.hoist_calls == [(1, (-1, 1)), (3, (-8, 8))]
+    assert plain.rot == hoisted.rot == 8
+    for key in a:
+        assert np.array_equal(a[key].data, b[key].data), key
