@@ -54,6 +54,28 @@ def _dist():
     return rank, world, local
 
 
+def _self_launch(args):
+    """`bench.py --gpus N` without a launcher: re-exec under torch.distributed.run
+    with N ranks (one per GPU, rendezvous on 127.0.0.1), so a plain invocation
+    can never record a one-GPU number as an N-GPU run.  Under a launcher the
+    world size must equal --gpus."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 LEVEL_PLAN = ("inputs at 9 of 14 limbs -> conv1+square+pool (carry, 9) -> conv2+square+GAP (9) -> 5-component relin "
               "dropping 6 primes (3) -> dense+rescale (2)")
 
@@ -180,6 +202,7 @@ def run_reference(args, rank, world):
 
 def main():
     args = _args()
+    _self_launch(args)
     rank, world, local = _dist()
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -200,7 +223,9 @@ def main():
     spec = configs.CNN3
     wts = spec.make_weights(1234)                       # same model on every rank
     group = rank                                         # config 5: group g seeded g
-    eng = GpuEngine(configs.context(3, seed=42, device=local))
+    # per-rank key seed: groups on different ranks never share a secret key or
+    # encryption randomness (equal (seed, index) pairs would leak m - m')
+    eng = GpuEngine(configs.context(3, seed=42 + 7919 * rank, device=local))
     rng = np.random.default_rng(group)
     images = rng.uniform(0.0, 1.0, size=(SAMPLES_PER_GROUP, 3 * 32 * 32))
     feat_host = torch.from_numpy(np.ascontiguousarray(images.T)).pin_memory()   # [3072, 32768] f64

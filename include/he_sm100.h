@@ -250,6 +250,26 @@ int he_microbench_fp64(int device, double *modmul_per_s);
 /* int8 multiply-accumulates per second through mma.sync.m16n8k32.u8.s8 (the
  * fused conv's tensor-core instruction): the conv kernel's tensor roofline. */
 int he_microbench_imma(int device, double *mac_per_s);
+/* tcgen05.mma kind::i8 (u8 x s8 -> s32, M = 128, accumulators in TMEM): the
+ * Blackwell tensor-core path of the fused conv kernels (csrc/convtc.cu).
+ * he_tc5_selftest writes D = A B (128 x n int32, row-major) of a fixed
+ * deterministic A (128 x 64 u8) and B (n x 64 s8) to the DEVICE buffer d_out;
+ * layout 0/1 selects the shared-memory operand layout exercised.
+ * he_microbench_tc5: rates[0] = int8 MAC/s over all SMs of back-to-back
+ * M=128 x N=n x K=32 MMAs from shared memory, rates[1] = cycles per MMA. */
+int he_tc5_selftest(int device, int n, int layout, int32_t *d_out);
+int he_microbench_tc5(int device, int n, double *rates);
+/* The fused conv + square + pool / global-sum layer on the 5th-generation
+ * tensor cores (tcgen05.mma kind::i8, TMEM accumulators, warp-specialised
+ * producer / MMA / epilogue; csrc/convtc.cu).  Same arguments and results as
+ * he_conv_square_sum_n; returns HE_EINVAL without enqueuing work when the
+ * shape is not covered (primes outside [2^36, 2^40), W not a multiple of 16,
+ * ...).  he_conv_square_sum_n routes every covered shape here unless
+ * he_set_conv_tc(0) was called (returns the previous setting). */
+int he_conv_square_sum_tc(he_ctx *ctx, const uint64_t *const *in, int nci, int p, int H, int W,
+                          uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
+                          const uint64_t *bias, const uint64_t *cst, int ell, void *stream);
+int he_set_conv_tc(int on);
 
 #ifdef __cplusplus
 }

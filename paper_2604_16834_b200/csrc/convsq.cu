@@ -57,9 +57,16 @@ __global__ void k_add_parts(uint64_t *const *out, const uint64_t *part, int M, i
     }
 }
 
+int he_conv_tc_enabled();  // convtc.cu
+
 extern "C" int he_conv_square_sum_n(he_ctx *c, const uint64_t *const *in, int nci, int p, int H, int W,
                                     uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
                                     const uint64_t *bias, const uint64_t *cst, int ell, void *stream) {
+    // the tcgen05 kernels (convtc.cu) take every shape they cover; the mma.sync
+    // kernels below handle the rest (and serve as the A/B reference in tests)
+    if (he_conv_tc_enabled() && he_conv_square_sum_tc(c, in, nci, p, H, W, out, M, pool, y0, y1, weights, bias, cst,
+                                                       ell, stream) == HE_OK)
+        return HE_OK;
     if (!c || !in || !out || !weights || p < 1 || H < 1 || W < 1 || M < 1 || ell < 1 || ell > c->L || y0 < 0 ||
         y1 > H || y0 >= y1 || (nci != 2 && nci != 3)) {
         he_set_error("he_conv_square_sum: bad arguments");

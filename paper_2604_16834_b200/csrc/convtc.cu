@@ -1,0 +1,521 @@
+// convtc.cu -- the fused conv3x3 -> square -> 2x2 pool / global sum of
+// featuremajor.run_cnn on the 5th-generation tensor cores (tcgen05).
+//
+// Same arithmetic contract as convsq_kernel.cuh (exact int8 digit GEMMs, exact
+// recombination, FP64 modular products of the window/GAP squares; results
+// are canonical residues identical to the conv -> tensor -> add_const -> sum
+// chain), restructured for Blackwell:
+//
+//   * The MMA is tcgen05.mma.cta_group::1.kind::i8 (u8 x s8 -> s32), issued by
+//     one thread, accumulators in TMEM.  M = 128 rows = 16 output pixels of one
+//     image row x 8 coefficients of one limb; the CTA owns one (limb,
+//     8-coefficient chunk) work item at a time (persistent grid).
+//   * Inputs are byte-transposed ONCE per input row into a shared-memory ring
+//     laid out as UMMA core matrices (8 coefficients x 16 bytes), so every tap
+//     is a plain shared-memory descriptor: the 8-row groups of the A operand are
+//     consecutive pixels (SBO = pixel stride) and the two 16-byte K chunks of a
+//     K step are two taps (LBO = tap distance) -- an implicit GEMM with no
+//     im2col copy.  Taps pair as (dy,0)+(dy,1) for dy = 0,1,2, then (0,2)+(1,2)
+//     (ring-order dependent: a swapped B variant covers the wrap), then (2,2)
+//     with a zero-weight partner: 5 K steps for 9 taps.
+//   * Packing P1 (p <= 3 input channels, conv1): one 16-byte K chunk holds all
+//     five byte planes of the three channels (byte 5 i + d), and the byte shift
+//     goes into N: B[(i,d)][(s,m)] = digit_{s-d}(w[m][i][tap]), so one MMA
+//     (N = NSH x 16) produces every shift sum C[s] of all 16 output channels.
+//   * Warp roles: warps 0-7 epilogue (two per TMEM lane quarter, 8 channels
+//     each: tcgen05.ld -> exact recombination -> FP64 products -> window sums
+//     -> stores), warps 8-10 producers (128-bit global loads -> PRMT byte
+//     packing -> shared ring), warp 11 TMEM allocator + MMA issuer.  mbarriers
+//     connect them: ring row full (producers -> MMA), ring row empty
+//     (tcgen05.commit -> producers), TMEM slot full (commit -> epilogue), TMEM
+//     slot empty (epilogue -> MMA).  Four TMEM slots of 128 columns (one per
+//     (row step, component)) let the MMAs of the next components run while
+//     the epilogue does its FP64 work.
+#include <algorithm>
+#include <vector>
+
+#include "ntt_core.cuh"  // u2d / d2u / fmulmod / fcanon
+#include "tc5.cuh"
+
+namespace convtc {
+
+constexpr int NB = 5;            // byte planes of a 40-bit residue
+constexpr int EPI_WARPS = 8;     // warps 0-7
+constexpr int PROD_WARPS = 3;    // warps 8-10
+constexpr int MMA_WARP = 11;
+constexpr int THREADS = 32 * 12;  // 12 warps = 3 per SM sub-partition: 168 registers per thread
+constexpr int NSLOT = 4;         // TMEM accumulator slots (128 columns each)
+constexpr int MC = 16;           // output channels per CTA
+
+struct TcArgs {
+    const uint64_t *const *in;   // [p*H*W] input ciphertexts (NCI components x ell limbs)
+    uint64_t *const *out;        // pool: [M][nwin] (3 components); GAP: [M]
+    const uint8_t *btiles;       // B tiles (global), copied to shared memory once per CTA
+    const double *biasd;         // [MC][ell] plain-domain bias (component 0), canonical
+    const uint64_t *cst;         // [ell] constant added to component 0 of every output (or nullptr)
+    const double *yc;            // [ell] 2^32 mod q
+    const ModConst *mc;
+    const int32_t *limbs;        // [nlimbs] limb of limb-index
+    int nlimbs, ell, logN, p, H, W, M, y0, y1, nwin, nitems;
+    int btile_bytes, nshift;     // bytes per B tile, shift sums (N = nshift * 16)
+};
+
+// ---------------------------------------------------------------- shared layout
+// ring row: (W + 3) pixel slots (halo, W pixels, halo, pad) x NCI components x
+// 128 bytes (8 coefficients x 16-byte chunk); RR rows
+template <int NCI>
+struct P1Layout {
+    static constexpr int PS = NCI * 128;  // pixel stride (bytes) = A operand SBO
+    static constexpr int RR = 6;          // ring rows (4 in use for a pool step + 2 prefetched)
+};
+
+__device__ __forceinline__ int64_t madw(int64_t acc, int a, int b) {
+    asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
+    return acc;
+}
+
+// shift sums C[0..NSH) -> y = sum_s C[s] 2^(8s) mod q as an unreduced integer-valued
+// double (|y| < 2^48.2): P0 = sum_{s<4}, P1 = sum_{s>=4} (x 2^32, one FP64 modular product)
+template <int NSH>
+__device__ __forceinline__ double recombine(const int (&C)[NSH], double yc, const ModConst &c) {
+    int64_t p0 = C[0], p1 = NSH > 4 ? C[NSH > 4 ? 4 : 0] : 0;
+    if (NSH > 1) p0 = madw(p0, C[NSH > 1 ? 1 : 0], 1 << 8);
+    if (NSH > 2) p0 = madw(p0, C[NSH > 2 ? 2 : 0], 1 << 16);
+    if (NSH > 3) p0 = madw(p0, C[NSH > 3 ? 3 : 0], 1 << 24);
+    if (NSH > 5) p1 = madw(p1, C[NSH > 5 ? 5 : 0], 1 << 8);
+    if (NSH > 6) p1 = madw(p1, C[NSH > 6 ? 6 : 0], 1 << 16);
+    const double d0 = __longlong_as_double(0x4338000000000000ll + p0) - 6755399441055744.0;
+    const double d1 = __longlong_as_double(0x4338000000000000ll + p1) - 6755399441055744.0;
+    return d0 + fmulmod(d1, yc, c.qd, c.qid);
+}
+
+__device__ __forceinline__ void ldg128(const uint64_t *p, uint64_t &a, uint64_t &b) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d));
+}
+
+// P1 chunk of one coefficient: byte 5 i + d = byte d of channel i (i < 3, d < 5), byte 15 = 0
+__device__ __forceinline__ void pack_p1(uint64_t v0, uint64_t v1, uint64_t v2, uint32_t (&w)[4]) {
+    const uint32_t l0 = (uint32_t)v0, h0 = (uint32_t)(v0 >> 32);
+    const uint32_t l1 = (uint32_t)v1, h1 = (uint32_t)(v1 >> 32);
+    const uint32_t l2 = (uint32_t)v2, h2 = (uint32_t)(v2 >> 32);
+    w[0] = l0;
+    w[1] = __byte_perm(h0, l1, 0x6540);                        // h0.b0, l1.b0, l1.b1, l1.b2
+    w[2] = __byte_perm(__byte_perm(l1, h1, 0x0043), l2, 0x5410);  // l1.b3, h1.b0 | l2.b0, l2.b1
+    w[3] = __byte_perm(l2, h2, 0x0432) & 0x00FFFFFFu;          // l2.b2, l2.b3, h2.b0, 0
+}
+
+// ---------------------------------------------------------------- the P1 kernel (conv1 shape)
+// NCI = 2 input components, p <= 3 channels, MC = 16 output channels, 2x2 pool, W % 16 == 0.
+template <int NSH>
+__global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
+    constexpr int NCI = 2;
+    using LY = P1Layout<NCI>;
+    constexpr int PS = LY::PS, RR = LY::RR;
+    constexpr int NCOL = NSH * MC;  // MMA N
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar_full[RR], bar_empty[RR], bar_dfull[NSLOT], bar_dempty[NSLOT], bar_b;
+    __shared__ uint32_t taddr_s;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int W = a.W, H = a.H, XB = W / 16;
+    const int RS = (W + 3) * PS;  // ring row stride
+    uint8_t *ring = smem;
+    uint8_t *bsm = smem + (size_t)RR * RS;
+    const size_t N = (size_t)1 << a.logN;
+    const int nchunk = (int)(N / 8);
+    const int rows_in = a.y1 - a.y0 + 2;
+    const int npairs = (a.y1 - a.y0) / 2;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RR; i++) {
+            tc5::mbar_init(&bar_full[i], PROD_WARPS * 32);
+            tc5::mbar_init(&bar_empty[i], 1);
+        }
+        for (int i = 0; i < NSLOT; i++) {
+            tc5::mbar_init(&bar_dfull[i], 1);
+            tc5::mbar_init(&bar_dempty[i], EPI_WARPS * 32);
+        }
+        tc5::mbar_init(&bar_b, 1);
+        tc5::mbar_fence_init();
+    }
+    // zero the whole ring once: halo pixel slots are never written again
+    for (int i = threadIdx.x * 16; i < RR * RS; i += THREADS * 16) *(uint4 *)(ring + i) = make_uint4(0, 0, 0, 0);
+    // B tiles: one bulk copy per CTA (TMA engine, completes on bar_b)
+    if (threadIdx.x == 0) {
+        tc5::mbar_arrive_expect_tx(&bar_b, (uint32_t)(6 * a.btile_bytes));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         tc5::smem_u32(bsm)),
+                     "l"(a.btiles), "r"((uint32_t)(6 * a.btile_bytes)), "r"(tc5::smem_u32(&bar_b))
+                     : "memory");
+    }
+    if (warp == MMA_WARP) tc5::tmem_alloc<512>(&taddr_s);
+    tc5::fence_async_smem();
+    tc5::tc_fence_before();
+    __syncthreads();
+    tc5::tc_fence_after();
+    const uint32_t tmem = taddr_s;
+
+    if (warp >= EPI_WARPS && warp < EPI_WARPS + PROD_WARPS) {
+        // ======================= producers: input rows -> packed ring rows
+        const int pt = threadIdx.x - EPI_WARPS * 32;  // 0..95
+        constexpr int PT = PROD_WARPS * 32;
+        const uint32_t ring_s = tc5::smem_u32(ring);
+        const int ntask = W * NCI * 4;  // (pixel, component, coefficient pair)
+        int k = 0;
+        for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
+            const int l = a.limbs[item / nchunk];
+            const size_t coff = (size_t)(item % nchunk) * 8;
+            for (int rr = 0; rr < rows_in; rr++) {
+                const int G = k * rows_in + rr, slot = G % RR, use = G / RR;
+                if (use > 0) tc5::mbar_wait(&bar_empty[slot], (use - 1) & 1);
+                const int y = a.y0 - 1 + rr;
+                const bool inside = y >= 0 && y < H;
+                const uint32_t rbase = ring_s + slot * RS;
+                for (int t0 = pt; t0 < ntask; t0 += 2 * PT) {
+                    uint64_t v[2][3][2];
+                    int tt[2];
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        const int t = t0 + u * PT;
+                        tt[u] = t;
+                        const int jp = t & 3, c = (t >> 2) % NCI, x = (t >> 2) / NCI;
+#pragma unroll
+                        for (int i = 0; i < 3; i++) {
+                            v[u][i][0] = v[u][i][1] = 0;
+                            if (t < ntask && inside && i < a.p) {
+                                const uint64_t *src = a.in[(size_t)i * H * W + (size_t)y * W + x];
+                                ldg128(src + ((size_t)c * a.ell + l) * N + coff + 2 * jp, v[u][i][0], v[u][i][1]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        const int t = tt[u];
+                        if (t >= ntask) break;
+                        const int jp = t & 3, c = (t >> 2) % NCI, x = (t >> 2) / NCI;
+                        const uint32_t dst = rbase + (x + 1) * PS + c * 128 + jp * 32;
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            uint32_t w[4];
+                            pack_p1(v[u][0][h], v[u][1][h], v[u][2][h], w);
+                            sts128(dst + h * 16, w[0], w[1], w[2], w[3]);
+                        }
+                    }
+                }
+                tc5::fence_async_smem();
+                tc5::mbar_arrive(&bar_full[slot]);
+            }
+        }
+    } else if (warp == MMA_WARP) {
+        // ======================= MMA issuer
+        if (lane == 0) {
+            tc5::mbar_wait(&bar_b, 0);
+            const uint32_t ring_s = tc5::smem_u32(ring), b_s = tc5::smem_u32(bsm);
+            const uint32_t idesc = tc5::idesc_u8s8(128, NCOL);
+            const uint32_t blbo = NCOL * 16;  // B: chunk 0 rows then chunk 1 rows
+            int k = 0, S = 0;
+            for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
+                const int Gb = k * rows_in;  // ring index of input row y0 - 1
+                auto slot_of = [&](int y) { return (Gb + (y - (a.y0 - 1))) % RR; };
+                for (int pr = 0; pr < npairs; pr++) {
+                    const int yp = a.y0 + 2 * pr;
+                    // rows yp-1 .. yp+2 must be resident
+                    for (int y = yp - 1; y <= yp + 2; y++) {
+                        const int G = Gb + (y - (a.y0 - 1));
+                        tc5::mbar_wait(&bar_full[G % RR], (G / RR) & 1);
+                    }
+                    tc5::tc_fence_after();
+                    for (int xb = 0; xb < XB; xb++)
+                        for (int dyb = 0; dyb < 2; dyb++) {
+                            const int y = yp + dyb;
+                            const uint32_t r0 = ring_s + slot_of(y - 1) * RS, r1 = ring_s + slot_of(y) * RS,
+                                           r2 = ring_s + slot_of(y + 1) * RS;
+                            const uint32_t xo = (uint32_t)(xb * 16) * PS;
+                            for (int c = 0; c < NCI; c++, S++) {
+                                const int ds = S % NSLOT;
+                                if (S >= NSLOT) tc5::mbar_wait(&bar_dempty[ds], ((S / NSLOT) - 1) & 1);
+                                tc5::tc_fence_after();
+                                const uint32_t d = tmem + (uint32_t)ds * 128;
+                                const uint32_t co = xo + c * 128;
+                                // K steps: (dy,0)+(dy,1) for dy = 0..2; (0,2)+(1,2); (2,2)+pad
+                                tc5::mma_i8(d, tc5::sdesc(r0 + co, PS, PS), tc5::sdesc(b_s + 0 * a.btile_bytes, blbo, 128),
+                                            idesc, 0);
+                                tc5::mma_i8(d, tc5::sdesc(r1 + co, PS, PS), tc5::sdesc(b_s + 1 * a.btile_bytes, blbo, 128),
+                                            idesc, 1);
+                                tc5::mma_i8(d, tc5::sdesc(r2 + co, PS, PS), tc5::sdesc(b_s + 2 * a.btile_bytes, blbo, 128),
+                                            idesc, 1);
+                                if (r1 > r0)
+                                    tc5::mma_i8(d, tc5::sdesc(r0 + co + 2 * PS, r1 - r0, PS),
+                                                tc5::sdesc(b_s + 3 * a.btile_bytes, blbo, 128), idesc, 1);
+                                else  // ring wrap: (1,2) first, swapped B tile
+                                    tc5::mma_i8(d, tc5::sdesc(r1 + co + 2 * PS, r0 - r1, PS),
+                                                tc5::sdesc(b_s + 5 * a.btile_bytes, blbo, 128), idesc, 1);
+                                tc5::mma_i8(d, tc5::sdesc(r2 + co + 2 * PS, PS, PS),
+                                            tc5::sdesc(b_s + 4 * a.btile_bytes, blbo, 128), idesc, 1);
+                                tc5::tc_commit(&bar_dfull[ds]);
+                            }
+                        }
+                    // rows yp-1, yp are not read by later pairs
+                    tc5::tc_commit(&bar_empty[slot_of(yp - 1)]);
+                    tc5::tc_commit(&bar_empty[slot_of(yp)]);
+                }
+                tc5::tc_commit(&bar_empty[slot_of(a.y1 - 1)]);
+                tc5::tc_commit(&bar_empty[slot_of(a.y1)]);
+            }
+        }
+        __syncwarp();
+    } else if (warp < EPI_WARPS) {
+        // ======================= epilogue
+        const int qd = warp & 3, hf = warp >> 2;  // TMEM lane quarter, channel half
+        const int row = qd * 32 + lane, xl = row >> 3, j = row & 7;
+        const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
+        int k = 0, S = 0;
+        for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
+            const int li = item / nchunk, l = a.limbs[li];
+            const size_t coff = (size_t)(item % nchunk) * 8;
+            const ModConst c = a.mc[l];
+            const double yc = a.yc[l];
+            const uint64_t cst = a.cst ? a.cst[l] : 0;
+            double biasd[8];
+#pragma unroll
+            for (int m = 0; m < 8; m++) biasd[m] = a.biasd[(size_t)(hf * 8 + m) * a.ell + l];
+            for (int pr = 0; pr < npairs; pr++) {
+                for (int xb = 0; xb < XB; xb++) {
+                    double acc[8][3];
+#pragma unroll
+                    for (int m = 0; m < 8; m++) acc[m][0] = acc[m][1] = acc[m][2] = 0.0;
+                    for (int dyb = 0; dyb < 2; dyb++) {
+                        double yv[2][8];
+#pragma unroll
+                        for (int cc = 0; cc < NCI; cc++, S++) {
+                            const int ds = S % NSLOT;
+                            tc5::mbar_wait(&bar_dfull[ds], (S / NSLOT) & 1);
+                            tc5::tc_fence_after();
+                            int C[8][NSH];
+                            const uint32_t ta = tq + (uint32_t)ds * 128 + hf * 8;
+#pragma unroll
+                            for (int s = 0; s < NSH; s++) {
+                                uint32_t r[8];
+                                tc5::tld8(ta + s * 16, r);
+#pragma unroll
+                                for (int m = 0; m < 8; m++) C[m][s] = (int)r[m];
+                            }
+                            tc5::tld_wait();
+                            tc5::tc_fence_before();
+                            tc5::mbar_arrive(&bar_dempty[ds]);
+#pragma unroll
+                            for (int m = 0; m < 8; m++) yv[cc][m] = recombine<NSH>(C[m], yc, c);
+                        }
+#pragma unroll
+                        for (int m = 0; m < 8; m++) {
+                            const double d0 = yv[0][m] + biasd[m], d1 = yv[1][m];
+                            acc[m][0] += fmulmod(d0, d0, c.qd, c.qid);
+                            acc[m][1] += fmulmod(d0, d1, c.qd, c.qid);
+                            acc[m][2] += fmulmod(d1, d1, c.qd, c.qid);
+                        }
+                    }
+                    // window = this pixel + its x-neighbour (lane ^ 8), rows yp, yp+1
+#pragma unroll
+                    for (int m = 0; m < 8; m++)
+#pragma unroll
+                        for (int s = 0; s < 3; s++) acc[m][s] += __shfl_xor_sync(0xffffffffu, acc[m][s], 8);
+                    if ((xl & 1) == 0) {
+                        const int x = xb * 16 + xl;
+                        const int win = pr * (W / 2) + x / 2;
+#pragma unroll
+                        for (int m = 0; m < 8; m++) {
+                            const int mo = hf * 8 + m;
+                            if (mo >= a.M) break;
+                            uint64_t *o = a.out[(size_t)mo * a.nwin + win] + coff + j;
+                            uint64_t v0 = fcanon(acc[m][0], c.qd, c.qid);
+                            uint64_t v1 = fcanon(acc[m][1], c.qd, c.qid);
+                            const uint64_t v2 = fcanon(acc[m][2], c.qd, c.qid);
+                            v0 = add_mod(v0, cst, c.q);
+                            v1 = add_mod(v1, v1, c.q);
+                            o[((size_t)0 * a.ell + l) * N] = v0;
+                            o[((size_t)1 * a.ell + l) * N] = v1;
+                            o[((size_t)2 * a.ell + l) * N] = v2;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    tc5::tc_fence_before();
+    __syncthreads();
+    if (warp == MMA_WARP) tc5::tmem_free<512>(tmem);
+}
+
+// balanced signed base-256 digit e of w
+inline int digit_s8(int64_t w, int e) {
+    for (int i = 0; i < e; i++) {
+        int64_t d = (int8_t)(uint8_t)(w & 0xFF);
+        w = (w - d) >> 8;
+    }
+    return (int8_t)(uint8_t)(w & 0xFF);
+}
+
+}  // namespace convtc
+
+using namespace convtc;
+
+// B tiles of the P1 packing: tile t (0..5) = K step t; tile 5 = K step 3 with its two taps swapped.
+// Tile layout (K-major, no swizzle): [chunk k][row group n/8][8 rows x 16 bytes], row n = s * 16 + m.
+static void build_btiles_p1(const int64_t *weights, int M, int p, int E, int NSH, std::vector<uint8_t> &bt) {
+    const int NCOL = NSH * MC, TB = NCOL * 32;
+    // taps (dy, dx) of the two chunks of each K step; (-1,-1) = zero chunk
+    const int ks[6][2][2] = {{{0, 0}, {0, 1}}, {{1, 0}, {1, 1}}, {{2, 0}, {2, 1}},
+                             {{0, 2}, {1, 2}}, {{2, 2}, {-1, -1}}, {{1, 2}, {0, 2}}};
+    bt.assign((size_t)6 * TB, 0);
+    for (int t = 0; t < 6; t++)
+        for (int k = 0; k < 2; k++) {
+            const int dy = ks[t][k][0], dx = ks[t][k][1];
+            if (dy < 0) continue;
+            const int tap = dy * 3 + dx;
+            for (int n = 0; n < NCOL; n++) {
+                const int s = n / MC, m = n % MC;
+                if (m >= M) continue;
+                for (int kb = 0; kb < 15; kb++) {
+                    const int i = kb / 5, d = kb % 5, e = s - d;
+                    if (i >= p || e < 0 || e >= E) continue;
+                    const int dg = digit_s8(weights[(size_t)m * p * 9 + i * 9 + tap], e);
+                    bt[(size_t)t * TB + (size_t)k * NCOL * 16 + (size_t)(n / 8) * 128 + (n % 8) * 16 + kb] =
+                        (uint8_t)(int8_t)dg;
+                }
+            }
+        }
+}
+
+static int g_conv_tc = 1;  // he_set_conv_tc: 0 forces the mma.sync kernels (A/B tests)
+
+extern "C" int he_set_conv_tc(int on) {
+    const int old = g_conv_tc;
+    g_conv_tc = on;
+    return old;
+}
+
+// Eligibility + launch of the tcgen05 path; HE_EINVAL (no work enqueued) when the shape is not covered.
+extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int nci, int p, int H, int W,
+                                     uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
+                                     const uint64_t *bias, const uint64_t *cst, int ell, void *stream) {
+    if (!c || !in || !out || !weights || ell < 1 || ell > c->L || y0 < 0 || y1 > H || y0 >= y1) {
+        he_set_error("he_conv_square_sum_tc: bad arguments");
+        return HE_EINVAL;
+    }
+    const bool p1 = nci == 2 && p <= 3 && pool && M <= MC && W % 16 == 0 && W <= 64 && !((y0 | y1 | H) & 1);
+    if (!p1) {
+        he_set_error("he_conv_square_sum_tc: shape (nci=%d p=%d M=%d W=%d pool=%d) not covered", nci, p, M, W, pool);
+        return HE_EINVAL;
+    }
+    for (int l = 0; l < ell; l++)
+        if (c->mod[l] < (1ull << 36) || c->mod[l] >= (1ull << 40)) {
+            he_set_error("he_conv_square_sum_tc: prime %d outside [2^36, 2^40)", l);
+            return HE_EINVAL;
+        }
+    int64_t wmax = 0;
+    for (int i = 0; i < M * p * 9; i++) wmax = std::max<int64_t>(wmax, weights[i] < 0 ? -weights[i] : weights[i]);
+    int E = 1;
+    int64_t cap = 127;
+    while (wmax > cap && E < 3) {
+        E++;
+        cap = cap * 256 + 127;
+    }
+    if (wmax > cap) {
+        he_set_error("he_conv_square_sum_tc: weights need more than 3 signed byte digits");
+        return HE_EINVAL;
+    }
+    const int NSH = NB + E - 1;
+    std::vector<uint8_t> bt;
+    build_btiles_p1(weights, M, p, E, NSH, bt);
+    const int TB = NSH * MC * 32;
+    std::vector<double> biasd((size_t)MC * ell, 0.0), yc(ell);
+    for (int l = 0; l < ell; l++) {
+        const uint64_t q = c->mod[l];
+        yc[l] = (double)(((uint64_t)1 << 32) % q);
+        if (cst && cst[l] >= q) {
+            he_set_error("he_conv_square_sum_tc: residue not canonical");
+            return HE_EINVAL;
+        }
+        if (bias)
+            for (int m = 0; m < M; m++) {
+                if (bias[(size_t)m * ell + l] >= q) {
+                    he_set_error("he_conv_square_sum_tc: residue not canonical");
+                    return HE_EINVAL;
+                }
+                biasd[(size_t)m * ell + l] = (double)bias[(size_t)m * ell + l];
+            }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int nwin = ((y1 - y0) / 2) * (W / 2);
+    const int n_in = p * H * W, n_out = M * nwin;
+    void **din = nullptr, **dout = nullptr;
+    HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
+    HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
+    std::vector<int32_t> lorder(ell);
+    for (int l = 0; l < ell; l++) lorder[l] = l;
+    const size_t b_bt = bt.size(), b_bias = biasd.size() * 8, b_yc = (size_t)ell * 8, b_lo = (size_t)ell * 4,
+                 b_c = cst ? (size_t)ell * 8 : 0;
+    char *meta = nullptr;
+    HE_TRY(he_scratch_alloc((void **)&meta, b_bt + b_bias + b_yc + b_lo + b_c + 256, s));
+    size_t off = 0;
+    auto carve = [&](size_t bytes) {
+        char *q = meta + off;
+        off = (off + bytes + 127) & ~(size_t)127;
+        return q;
+    };
+    uint8_t *dbt = (uint8_t *)carve(b_bt);
+    double *dbias = (double *)carve(b_bias);
+    double *dyc = (double *)carve(b_yc);
+    int32_t *dlo = (int32_t *)carve(b_lo);
+    uint64_t *dc = cst ? (uint64_t *)carve(b_c) : nullptr;
+    HE_CHECK_CUDA(he_h2d(dbt, bt.data(), b_bt, s));
+    HE_CHECK_CUDA(he_h2d(dbias, biasd.data(), b_bias, s));
+    HE_CHECK_CUDA(he_h2d(dyc, yc.data(), b_yc, s));
+    HE_CHECK_CUDA(he_h2d(dlo, lorder.data(), b_lo, s));
+    if (dc) HE_CHECK_CUDA(he_h2d(dc, cst, b_c, s));
+    TcArgs a;
+    a.in = (const uint64_t *const *)din;
+    a.out = (uint64_t *const *)dout;
+    a.btiles = dbt;
+    a.biasd = dbias;
+    a.cst = dc;
+    a.yc = dyc;
+    a.mc = c->d_mc;
+    a.limbs = dlo;
+    a.nlimbs = ell;
+    a.ell = ell;
+    a.logN = c->logN;
+    a.p = p;
+    a.H = H;
+    a.W = W;
+    a.M = M;
+    a.y0 = y0;
+    a.y1 = y1;
+    a.nwin = nwin;
+    a.nitems = ell * (c->N / 8);
+    a.btile_bytes = TB;
+    a.nshift = NSH;
+    const size_t smem = (size_t)P1Layout<2>::RR * (W + 3) * P1Layout<2>::PS + 6 * (size_t)TB;
+    int sms = 0;
+    HE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    const dim3 grid((unsigned)std::min(sms, a.nitems));
+    int rc = HE_OK;
+    auto launch = [&](auto kern) -> int {
+        HE_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, THREADS, smem, s>>>(a);
+        HE_CHECK_LAUNCH();
+        return HE_OK;
+    };
+    if (NSH == 5) rc = launch(k_convtc_p1_pool<5>);
+    else if (NSH == 6) rc = launch(k_convtc_p1_pool<6>);
+    else rc = launch(k_convtc_p1_pool<7>);
+    he_scratch_free(meta, s);
+    he_scratch_free(din, s);
+    he_scratch_free(dout, s);
+    return rc;
+}
+
+int he_conv_tc_enabled() { return g_conv_tc; }

@@ -198,30 +198,24 @@ class RotationKeySet:
     def canonical(self, offset: int) -> int:
         return offset % self._n
 
-    def register(self, offsets: Iterable[int]) -> list[int]:
-        """Add keys; returns the newly resident canonical offsets."""
-        new = []
+    def register(self, offsets: Iterable[int]) -> int:
+        """Add keys; returns how many became newly resident (idempotent), as
+        the reference does (engine.py:108-119)."""
+        added = 0
         for off in offsets:
             c = self.canonical(off)
             if c and c not in self._offsets:
                 self._offsets.add(c)
-                new.append(c)
-        self.generation_count += len(new)
-        return new
+                added += 1
+        self.generation_count += added
+        return added
 
-    def unload(self, offsets: Iterable[int]) -> list[int]:
-        gone = []
+    def unload(self, offsets: Iterable[int]) -> None:
         for off in offsets:
-            c = self.canonical(off)
-            if c in self._offsets:
-                self._offsets.discard(c)
-                gone.append(c)
-        return gone
+            self._offsets.discard(self.canonical(off))
 
-    def unload_all(self) -> list[int]:
-        gone = sorted(self._offsets)
+    def unload_all(self) -> None:
         self._offsets.clear()
-        return gone
 
     def holds(self, offset: int) -> bool:
         return self.canonical(offset) in self._offsets
@@ -535,6 +529,7 @@ class GpuEngine:
         torch = _torch()
         for c in cts:
             self._check(c)
+        self._need_two(cts, "decrypt")
         out = torch.empty((len(cts), self.context.n), dtype=torch.float64, device=self.device)
         by_level: dict[int, list[int]] = {}
         for i, c in enumerate(cts):
@@ -557,6 +552,7 @@ class GpuEngine:
     def decrypt_coeffs(self, ct: CipherVec) -> np.ndarray:
         torch = _torch()
         self._check(ct)
+        self._need_two([ct], "decrypt_coeffs")
         out = torch.empty((1, self.N), dtype=torch.float64, device=self.device)
         ptrs = self._ptrs([ct])
         _lib.check(self._L.he_decrypt_coeffs(self._h, _lib.addr(ptrs), 1, ct.level + 1, out.data_ptr(), self.stream))
@@ -570,6 +566,7 @@ class GpuEngine:
     # ------------------------------------------------------------ arithmetic
     def rotate(self, ct: CipherVec, k: int) -> CipherVec:
         self._check(ct)
+        self._need_two([ct], "rotate")
         if k % self.context.n == 0:
             return ct
         if not self.keys.holds(k):
@@ -587,6 +584,7 @@ class GpuEngine:
         (MissingRotationKey, raised before any work) and count as rotations."""
         for c in cts:
             self._check(c)
+        self._need_two(cts, "rotate_hoisted")
         if not cts:
             return [[] for _ in ks]
         if len({(c.level, c.data.shape[0]) for c in cts}) != 1:
@@ -668,8 +666,9 @@ class GpuEngine:
         vv = torch.as_tensor(v, device=self.device)
         _lib.check(self._L.he_encode_plain(self._h, vv.data_ptr(), self.context.n, a.scale, limbs, pt.data_ptr(),
                                            self.stream), "encode_plain")
-        out = self._alloc(1, 2, limbs)
-        out[0, 1].copy_(a.data[1])
+        nc = a.data.shape[0]
+        out = self._alloc(1, nc, limbs)
+        out[0, 1:].copy_(a.data[1:])
         pa = _lib.ptr_array([a.ptr])
         pp = _lib.ptr_array([pt.data_ptr()])
         po = self._tptrs(out)
@@ -701,6 +700,17 @@ class GpuEngine:
         if any(c.data.shape[0] != nc for c in cts):
             raise HebatchError("mixed 2- and 3-component ciphertexts in one batch")
         return nc
+
+    @staticmethod
+    def _need_two(cts: Sequence[CipherVec], op: str) -> None:
+        """Operations defined only on relinearised (2-component) ciphertexts:
+        rotation (the Galois key switches c1 alone) and decryption.  An
+        unrelinearised product (3 or 5 components, tensor_batch /
+        conv_square_sum) must be relinearised first (relin_rescale_batch)."""
+        for c in cts:
+            if c.data.shape[0] != 2:
+                raise HebatchError(f"{op} needs a relinearised 2-component ciphertext, got {c.data.shape[0]} "
+                                   f"components (relinearise it first)")
 
     def tensor_batch(self, A: Sequence[CipherVec], B: Sequence[CipherVec]) -> list[CipherVec]:
         """ct x ct WITHOUT relinearisation or rescale: 3-component results at the
@@ -846,9 +856,10 @@ class GpuEngine:
         vv = torch.as_tensor(v, device=self.device)
         _lib.check(self._L.he_encode_plain(self._h, vv.data_ptr(), self.context.n, float(ql), limbs, pt.data_ptr(),
                                            self.stream), "encode_plain")
-        tmp = self._alloc(1, 2, limbs)
+        nc = ct.data.shape[0]
+        tmp = self._alloc(1, nc, limbs)
         pi, pt_, pm = self._ptrs([ct]), pt.data_ptr(), self._tptrs(tmp)
-        _lib.check(self._L.he_mul_plain(self._h, _lib.addr(pi), pt_, _lib.addr(pm), 1, limbs, 2, self.stream))
+        _lib.check(self._L.he_mul_plain(self._h, _lib.addr(pi), pt_, _lib.addr(pm), 1, limbs, nc, self.stream))
         return self._rescale_tensor(tmp, limbs, [ct.scale])[0]
 
     def mul_const_batch(self, cts: Sequence[CipherVec], values: Sequence[float], count: bool = True,
@@ -870,9 +881,10 @@ class GpuEngine:
         outs = list(out_scales) if out_scales is not None else [c.scale for c in cts]
         res = np.array([self._res(int(np.rint(v * ql * (o / c.scale))), limbs) for v, c, o in zip(values, cts, outs)],
                        np.uint64)
-        tmp = self._alloc(len(cts), 2, limbs)
+        nc = self._ncomp(cts)
+        tmp = self._alloc(len(cts), nc, limbs)
         pi, pm = self._ptrs(cts), self._tptrs(tmp)
-        _lib.check(self._L.he_mul_const(self._h, _lib.addr(pi), _lib.addr(pm), len(cts), limbs, 2, _lib.addr(res),
+        _lib.check(self._L.he_mul_const(self._h, _lib.addr(pi), _lib.addr(pm), len(cts), limbs, nc, _lib.addr(res),
                                         self.stream), "mul_const")
         return self._rescale_tensor(tmp, limbs, outs)
 
@@ -909,9 +921,10 @@ class GpuEngine:
         return self._wrap_batch(t, level, [scale] * t.shape[0])
 
     def _rescale_tensor(self, t, limbs: int, scales) -> list[CipherVec]:
-        out = self._alloc(t.shape[0], 2, limbs - 1)
+        nc = t.shape[1]
+        out = self._alloc(t.shape[0], nc, limbs - 1)
         pi, po = self._tptrs(t), self._tptrs(out)
-        _lib.check(self._L.he_rescale(self._h, _lib.addr(pi), _lib.addr(po), t.shape[0], limbs, 2, self.stream),
+        _lib.check(self._L.he_rescale(self._h, _lib.addr(pi), _lib.addr(po), t.shape[0], limbs, nc, self.stream),
                    "rescale")
         return self._wrap_batch(out, limbs - 2, scales)
 
@@ -963,7 +976,7 @@ class GpuEngine:
             self._check(c)
             if c.level < level:
                 raise LevelExhausted(f"cannot raise level {c.level} to {level}")
-        out = self._alloc(len(cts), 2, level + 1)
+        out = self._alloc(len(cts), self._ncomp(cts), level + 1)
         for i, c in enumerate(cts):
             out[i].copy_(c.data[:, : level + 1])
         return self._wrap_batch(out, level, [c.scale for c in cts])
@@ -1280,20 +1293,25 @@ class GpuEngine:
     # ------------------------------------------------------------ keys
     def register_rotation_keys(self, offsets: Iterable[int]) -> None:
         offsets = list(offsets)
-        new = self.keys.register(offsets)
-        for c in new:
+        before = self.keys.resident
+        added = self.keys.register(offsets)
+        for c in sorted(self.keys.resident - before):
             _lib.check(self._L.he_gen_switch_key(self._h, pow(5, c, 2 * self.N), self.stream), "galois keygen")
-        if new:
-            self._acct.bump("key_loads", len(new))
+        if added:
+            self._acct.bump("key_loads", added)
         self.registration_log.append(
             frozenset(self.keys.canonical(o) for o in offsets if self.keys.canonical(o) != 0))
 
     def unload_rotation_keys(self, offsets: Iterable[int]) -> None:
-        for c in self.keys.unload(offsets):
+        before = self.keys.resident
+        self.keys.unload(offsets)
+        for c in sorted(before - self.keys.resident):
             self._L.he_drop_switch_key(self._h, pow(5, c, 2 * self.N))
 
     def unload_all_rotation_keys(self) -> None:
-        for c in self.keys.unload_all():
+        before = self.keys.resident
+        self.keys.unload_all()
+        for c in sorted(before):
             self._L.he_drop_switch_key(self._h, pow(5, c, 2 * self.N))
 
     @property

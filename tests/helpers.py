@@ -13,6 +13,8 @@ PARAMS = {
     "cfg4": (16, (50,) * 24, (50,) * 4, 4, 50),
     # config 4's prime sizes on a small ring (degree-3 CNN tests on one GPU)
     "cfg4s": (12, (50,) * 10, (50,) * 2, 2, 50),
+    # config 3's prime sizes on a small ring (tcgen05 conv kernels vs the oracle)
+    "cfg3s": (12, (40,) * 6, (42,) * 2, 3, 40),
 }
 
 

@@ -1,0 +1,105 @@
+"""The tcgen05 fused conv kernels (csrc/convtc.cu) on the B200.
+
+Two levels of evidence, both bit-exact:
+  * against the CPU oracle's conv -> tensor square -> add_const -> window-sum
+    chain (tests/test_gpu_parity._oracle_conv_square_sum) on config 3's prime
+    sizes at N = 2^12 (ring "cfg3s"), at the image widths the kernels tile
+    (16 and 32 pixels), every weight-digit count and ring-wrap position;
+  * against the mma.sync kernels (themselves pinned to the oracle by
+    test_gpu_parity) on the config-3 ring at N = 2^16 and 9 limbs, the exact
+    launch shapes run_cnn / bench.py issue.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import engine_context, from_np, oracle_for, rand_residues, to_np
+from test_gpu_parity import _oracle_conv_square_sum
+
+pytestmark = pytest.mark.gpu
+
+
+def _ptrs(ts):
+    return np.array([t.data_ptr() for t in ts], np.uint64)
+
+
+@pytest.fixture(scope="module")
+def small():
+    from paper_2604_16834_b200.engine import GpuEngine
+
+    return GpuEngine(engine_context("cfg3s")), oracle_for("cfg3s")
+
+
+def _run(eng, fn, ins, nci, p, H, W, M, pool, y0, y1, wi, bres, cst, ell):
+    import torch
+
+    nwin = ((y1 - y0) // 2) * (W // 2) if pool else 1
+    outs = [torch.zeros((2 * nci - 1, ell, eng.N), dtype=torch.int64, device=eng.device) for _ in range(M * nwin)]
+    pi, po = _ptrs(ins), _ptrs(outs)
+    rc = fn(eng._h, pi.ctypes.data, nci, p, H, W, po.ctypes.data, M, pool, y0, y1, wi.ctypes.data,
+            bres.ctypes.data if bres is not None else None, cst.ctypes.data if cst is not None else None, ell, None)
+    assert rc == 0, eng._L.he_last_error()
+    return outs
+
+
+@pytest.mark.parametrize("W,H,rows,wbits,p,M", [(16, 4, (0, 4), 20, 3, 16), (32, 4, (2, 4), 14, 3, 16),
+                                                (16, 8, (2, 8), 7, 2, 11), (32, 2, (0, 2), 20, 1, 16)])
+def test_convtc_pool_vs_oracle(small, W, H, rows, wbits, p, M):
+    """conv1 shape class (2-component inputs, p <= 3, 2x2 pool) vs the oracle chain."""
+    eng, orc = small
+    rng = np.random.default_rng(100 + W + H + wbits)
+    ell = 3
+    mods = eng.moduli[:ell]
+    x = rand_residues(rng, mods, (p * H * W, 2), eng.N)
+    ins = [from_np(x[i], eng.device) for i in range(p * H * W)]
+    lim = 1 << wbits
+    wi = rng.integers(-lim, lim, size=(M, 9 * p), dtype=np.int64)
+    bres = np.array([[int(rng.integers(0, q)) for q in mods] for _ in range(M)], np.uint64)
+    cst = np.array([int(rng.integers(0, q)) for q in mods], np.uint64)
+    y0, y1 = rows
+    got = _run(eng, eng._L.he_conv_square_sum_tc, ins, 2, p, H, W, M, 1, y0, y1, wi, bres, cst, ell)
+    ref = _oracle_conv_square_sum(orc, [x[i] for i in range(p * H * W)], p, H, W, wi, bres, cst, 1, y0, y1)
+    for k, (o, r) in enumerate(zip(got, ref)):
+        assert np.array_equal(to_np(o), r), k
+
+
+def _rand_dev(eng, count, nci, ell, seed):
+    import torch
+
+    g = torch.Generator(device=eng.device)
+    g.manual_seed(seed)
+    out = torch.empty((count, nci, ell, eng.N), dtype=torch.int64, device=eng.device)
+    for l, q in enumerate(eng.moduli[:ell]):
+        out[:, :, l] = torch.randint(0, int(q), (count, nci, eng.N), generator=g, device=eng.device,
+                                     dtype=torch.int64)
+    return out
+
+
+def test_convtc_conv1_shape_vs_mma_sync():
+    """config 3's conv1 launch (p=3 -> 16, 32 wide, 9 limbs, N = 2^16, 20-bit weights) on a
+    reduced 8-row image: tcgen05 kernel == mma.sync kernel, every output limb."""
+    import torch
+
+    from paper_2604_16834_b200.engine import GpuEngine
+
+    eng = GpuEngine(engine_context("cfg3"))
+    L = eng._L
+    p, H, W, M, ell = 3, 8, 32, 16, 9
+    x = _rand_dev(eng, p * H * W, 2, ell, 5)
+    ins = [x[i] for i in range(p * H * W)]
+    rng = np.random.default_rng(7)
+    wi = rng.integers(-(1 << 20), 1 << 20, size=(M, 27), dtype=np.int64)
+    bres = np.array([[int(rng.integers(0, q)) for q in eng.moduli[:ell]] for _ in range(M)], np.uint64)
+    cst = np.array([int(rng.integers(0, q)) for q in eng.moduli[:ell]], np.uint64)
+    for y0, y1 in ((0, 8), (2, 6)):
+        got = _run(eng, L.he_conv_square_sum_tc, ins, 2, p, H, W, M, 1, y0, y1, wi, bres, cst, ell)
+        old = L.he_set_conv_tc(0)
+        try:
+            ref = _run(eng, L.he_conv_square_sum_n, ins, 2, p, H, W, M, 1, y0, y1, wi, bres, cst, ell)
+        finally:
+            L.he_set_conv_tc(old)
+        torch.cuda.synchronize()
+        for k, (o, r) in enumerate(zip(got, ref)):
+            assert torch.equal(o, r), (y0, y1, k)

@@ -89,9 +89,9 @@ def test_engine_context_validation_matches_reference():
 
 def test_rotation_keyset_and_counters():
     ks = RotationKeySet(16)
-    assert sorted(ks.register([-1, 1, -8, 8])) == [1, 8, 15]
-    assert len(ks) == 3 and ks.register([1]) == [] and ks.generation_count == 3
-    ks.unload([1])
+    assert ks.register([-1, 1, -8, 8]) == 3 and ks.resident == frozenset({1, 8, 15})
+    assert len(ks) == 3 and ks.register([1]) == 0 and ks.generation_count == 3
+    assert ks.unload([1]) is None
     assert not ks.holds(1) and ks.holds(-1)
     a, b = OpCounters(rotations=5, adds=3, peak_live_ciphertexts=9), OpCounters(rotations=2, adds=1)
     assert a.delta(b) == OpCounters(rotations=3, adds=2, peak_live_ciphertexts=9)
