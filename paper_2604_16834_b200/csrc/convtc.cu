@@ -22,10 +22,11 @@
 //     five byte planes of the three channels (byte 5 i + d), and the byte shift
 //     goes into N: B[(i,d)][(s,m)] = digit_{s-d}(w[m][i][tap]), so one MMA
 //     (N = NSH x 16) produces every shift sum C[s] of all 16 output channels.
-//   * Warp roles: warps 0-7 epilogue (two per TMEM lane quarter, 8 channels
+//   * Warp roles: warps 0-15 epilogue (four per TMEM lane quarter, 4 channels
 //     each: tcgen05.ld -> exact recombination -> FP64 products -> window sums
-//     -> stores), warps 8-10 producers (128-bit global loads -> PRMT byte
-//     packing -> shared ring), warp 11 TMEM allocator + MMA issuer.  mbarriers
+//     -> stores; the FP64 work is latency-bound, so it gets the warps), warps
+//     16-18 producers (128-bit global loads -> PRMT byte packing -> shared
+//     ring), warp 19 TMEM allocator + MMA issuer.  mbarriers
 //     connect them: ring row full (producers -> MMA), ring row empty
 //     (tcgen05.commit -> producers), TMEM slot full (commit -> epilogue), TMEM
 //     slot empty (epilogue -> MMA).  Four TMEM slots of 128 columns (one per
@@ -40,16 +41,19 @@
 namespace convtc {
 
 constexpr int NB = 5;            // byte planes of a 40-bit residue
-constexpr int EPI_WARPS = 8;     // warps 0-7
-constexpr int PROD_WARPS = 3;    // warps 8-10
-constexpr int MMA_WARP = 11;
-constexpr int THREADS = 32 * 12;  // 12 warps = 3 per SM sub-partition: 168 registers per thread
+constexpr int EPI_WARPS = 16;    // warps 0-15: four per TMEM lane quarter, CPT channels each
+constexpr int CPT = 4;           // output channels per epilogue thread
+constexpr int PROD_WARPS = 3;    // warps 16-18
+constexpr int MMA_WARP = 19;
+constexpr int THREADS = 32 * 20;  // 5 warps per SM sub-partition: 96 registers per thread
 constexpr int NSLOT = 4;         // TMEM accumulator slots (128 columns each)
 constexpr int MC = 16;           // output channels per CTA
 
 struct TcArgs {
     const uint64_t *const *in;   // [p*H*W] input ciphertexts (NCI components x ell limbs)
     uint64_t *const *out;        // pool: [M][nwin] (3 components); GAP: [M]
+    uint64_t *obase;             // != nullptr: out[k] = obase + k * ostride (one batch allocation)
+    long long ostride;           // elements
     const uint8_t *btiles;       // B tiles (global), copied to shared memory once per CTA
     const double *biasd;         // [MC][ell] plain-domain bias (component 0), canonical
     const uint64_t *cst;         // [ell] constant added to component 0 of every output (or nullptr)
@@ -78,15 +82,24 @@ __device__ __forceinline__ int64_t madw(int64_t acc, int a, int b) {
 // double (|y| < 2^48.2): P0 = sum_{s<4}, P1 = sum_{s>=4} (x 2^32, one FP64 modular product)
 template <int NSH>
 __device__ __forceinline__ double recombine(const int (&C)[NSH], double yc, const ModConst &c) {
-    int64_t p0 = C[0], p1 = NSH > 4 ? C[NSH > 4 ? 4 : 0] : 0;
-    if (NSH > 1) p0 = madw(p0, C[NSH > 1 ? 1 : 0], 1 << 8);
-    if (NSH > 2) p0 = madw(p0, C[NSH > 2 ? 2 : 0], 1 << 16);
-    if (NSH > 3) p0 = madw(p0, C[NSH > 3 ? 3 : 0], 1 << 24);
-    if (NSH > 5) p1 = madw(p1, C[NSH > 5 ? 5 : 0], 1 << 8);
-    if (NSH > 6) p1 = madw(p1, C[NSH > 6 ? 6 : 0], 1 << 16);
+    static_assert(NSH >= 5 && NSH <= 7, "40-bit limbs: 5 byte planes, 1-3 weight digits");
+    // |C[s]| < 2^22, so pairs of shifts combine in 32 bits (|C0 + 2^8 C1| < 2^30.1)
+    const int q0 = C[0] + C[1] * 256, q1 = C[2] + C[3] * 256;
+    const int q2 = NSH > 5 ? C[4] + C[NSH > 5 ? 5 : 4] * 256 : C[4];
+    const int64_t p0 = madw((int64_t)q0, q1, 1 << 16);
+    const int64_t p1 = NSH > 6 ? madw((int64_t)q2, C[NSH > 6 ? 6 : 4], 1 << 16) : (int64_t)q2;
     const double d0 = __longlong_as_double(0x4338000000000000ll + p0) - 6755399441055744.0;
     const double d1 = __longlong_as_double(0x4338000000000000ll + p1) - 6755399441055744.0;
     return d0 + fmulmod(d1, yc, c.qd, c.qid);
+}
+
+// exact integer-valued double |x| < 2^50 -> canonical residue (magic-constant
+// rounding: |x / q| < 2^14, so x q^-1 + 1.5 2^52 rounds to the nearest integer)
+__device__ __forceinline__ uint64_t canon_fast(double x, double q, double qi) {
+    const double e = fma(x, qi, 6755399441055744.0) - 6755399441055744.0;
+    double r = fma(-e, q, x);  // exact, in (-q, q)
+    r = r < 0.0 ? r + q : r;
+    return (uint64_t)(__double_as_longlong(r + 4503599627370496.0) - 0x4330000000000000ll);
 }
 
 __device__ __forceinline__ void ldg128(const uint64_t *p, uint64_t &a, uint64_t &b) {
@@ -124,6 +137,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
     const int RS = (W + 3) * PS;  // ring row stride
     uint8_t *ring = smem;
     uint8_t *bsm = smem + (size_t)RR * RS;
+    // input address table, staged once (every work item reads the same ciphertexts)
+    const uint64_t **ptab = (const uint64_t **)(bsm + 6 * (size_t)a.btile_bytes);
+    for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.in[i];
     const size_t N = (size_t)1 << a.logN;
     const int nchunk = (int)(N / 8);
     const int rows_in = a.y1 - a.y0 + 2;
@@ -163,7 +179,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
         const int pt = threadIdx.x - EPI_WARPS * 32;  // 0..95
         constexpr int PT = PROD_WARPS * 32;
         const uint32_t ring_s = tc5::smem_u32(ring);
-        const int ntask = W * NCI * 4;  // (pixel, component, coefficient pair)
+        const int ntask = W * NCI * 4;  // (pixel, component, coefficient pair); <= 3 per thread for W <= 32
+        constexpr int TPT = 3;
         int k = 0;
         for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
             const int l = a.limbs[item / nchunk];
@@ -174,26 +191,25 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                 const int y = a.y0 - 1 + rr;
                 const bool inside = y >= 0 && y < H;
                 const uint32_t rbase = ring_s + slot * RS;
-                for (int t0 = pt; t0 < ntask; t0 += 2 * PT) {
-                    uint64_t v[2][3][2];
-                    int tt[2];
+                for (int t0 = pt; t0 < ntask; t0 += TPT * PT) {
+                    // every load of the batch is in flight before the first pack
+                    uint64_t v[TPT][3][2];
 #pragma unroll
-                    for (int u = 0; u < 2; u++) {
+                    for (int u = 0; u < TPT; u++) {
                         const int t = t0 + u * PT;
-                        tt[u] = t;
                         const int jp = t & 3, c = (t >> 2) % NCI, x = (t >> 2) / NCI;
 #pragma unroll
                         for (int i = 0; i < 3; i++) {
                             v[u][i][0] = v[u][i][1] = 0;
                             if (t < ntask && inside && i < a.p) {
-                                const uint64_t *src = a.in[(size_t)i * H * W + (size_t)y * W + x];
+                                const uint64_t *src = ptab[(size_t)i * H * W + (size_t)y * W + x];
                                 ldg128(src + ((size_t)c * a.ell + l) * N + coff + 2 * jp, v[u][i][0], v[u][i][1]);
                             }
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < 2; u++) {
-                        const int t = tt[u];
+                    for (int u = 0; u < TPT; u++) {
+                        const int t = t0 + u * PT;
                         if (t >= ntask) break;
                         const int jp = t & 3, c = (t >> 2) % NCI, x = (t >> 2) / NCI;
                         const uint32_t dst = rbase + (x + 1) * PS + c * 128 + jp * 32;
@@ -269,75 +285,83 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
         __syncwarp();
     } else if (warp < EPI_WARPS) {
         // ======================= epilogue
-        const int qd = warp & 3, hf = warp >> 2;  // TMEM lane quarter, channel half
+        const int qd = warp & 3, cg = warp >> 2;  // TMEM lane quarter, channel group (CPT channels)
         const int row = qd * 32 + lane, xl = row >> 3, j = row & 7;
-        const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
+        const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(cg * CPT);
+        const int par = xl & 1;  // window partners (x, x+1) split the stores: par 0 -> comps 0, 2; par 1 -> comp 1
         int k = 0, S = 0;
         for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
             const int li = item / nchunk, l = a.limbs[li];
             const size_t coff = (size_t)(item % nchunk) * 8;
             const ModConst c = a.mc[l];
             const double yc = a.yc[l];
-            const uint64_t cst = a.cst ? a.cst[l] : 0;
-            double biasd[8];
+            const double cstd = a.cst ? (double)a.cst[l] : 0.0;  // canonical, < 2^40
+            double biasd[CPT];
 #pragma unroll
-            for (int m = 0; m < 8; m++) biasd[m] = a.biasd[(size_t)(hf * 8 + m) * a.ell + l];
+            for (int m = 0; m < CPT; m++) biasd[m] = a.biasd[(size_t)(cg * CPT + m) * a.ell + l];
+            const size_t lo = (size_t)l * N + coff + j;  // limb / coefficient offset inside an output
+            const size_t cs = (size_t)a.ell * N;         // component stride
+            uint64_t *obm[CPT];                          // strided outputs: window 0 of channel cg CPT + m
+#pragma unroll
+            for (int m = 0; m < CPT; m++)
+                obm[m] = a.obase ? a.obase + (size_t)(cg * CPT + m) * a.nwin * a.ostride + lo : nullptr;
             for (int pr = 0; pr < npairs; pr++) {
                 for (int xb = 0; xb < XB; xb++) {
-                    double acc[8][3];
+                    double acc[CPT][3];
 #pragma unroll
-                    for (int m = 0; m < 8; m++) acc[m][0] = acc[m][1] = acc[m][2] = 0.0;
+                    for (int m = 0; m < CPT; m++) acc[m][0] = acc[m][1] = acc[m][2] = 0.0;
                     for (int dyb = 0; dyb < 2; dyb++) {
-                        double yv[2][8];
+                        double yv[2][CPT];
 #pragma unroll
                         for (int cc = 0; cc < NCI; cc++, S++) {
                             const int ds = S % NSLOT;
                             tc5::mbar_wait(&bar_dfull[ds], (S / NSLOT) & 1);
                             tc5::tc_fence_after();
-                            int C[8][NSH];
-                            const uint32_t ta = tq + (uint32_t)ds * 128 + hf * 8;
+                            int C[CPT][NSH];
+                            const uint32_t ta = tq + (uint32_t)ds * 128;
 #pragma unroll
-                            for (int s = 0; s < NSH; s++) {
-                                uint32_t r[8];
-                                tc5::tld8(ta + s * 16, r);
+                            for (int s2 = 0; s2 < NSH; s2++) {
+                                uint32_t r[4];
+                                tc5::tld4(ta + s2 * 16, r);
 #pragma unroll
-                                for (int m = 0; m < 8; m++) C[m][s] = (int)r[m];
+                                for (int m = 0; m < CPT; m++) C[m][s2] = (int)r[m];
                             }
                             tc5::tld_wait();
                             tc5::tc_fence_before();
                             tc5::mbar_arrive(&bar_dempty[ds]);
 #pragma unroll
-                            for (int m = 0; m < 8; m++) yv[cc][m] = recombine<NSH>(C[m], yc, c);
+                            for (int m = 0; m < CPT; m++) yv[cc][m] = recombine<NSH>(C[m], yc, c);
                         }
 #pragma unroll
-                        for (int m = 0; m < 8; m++) {
+                        for (int m = 0; m < CPT; m++) {
                             const double d0 = yv[0][m] + biasd[m], d1 = yv[1][m];
                             acc[m][0] += fmulmod(d0, d0, c.qd, c.qid);
                             acc[m][1] += fmulmod(d0, d1, c.qd, c.qid);
                             acc[m][2] += fmulmod(d1, d1, c.qd, c.qid);
                         }
                     }
-                    // window = this pixel + its x-neighbour (lane ^ 8), rows yp, yp+1
+                    // window = this pixel + its x-neighbour (lane ^ 8), rows yp, yp+1.  Reduce-scatter
+                    // over the pair: lane par keeps channels 2 par, 2 par + 1 of its window (no
+                    // divergent finalisation).  The constant (added once per window) and the factor 2
+                    // of the cross term are folded into the exact FP64 sums (|sum| < 2^50).
+                    const int x = xb * 16 + xl;
+                    const int win = pr * (W / 2) + x / 2;
 #pragma unroll
-                    for (int m = 0; m < 8; m++)
+                    for (int h = 0; h < 2; h++) {
+                        double keep[3];
 #pragma unroll
-                        for (int s = 0; s < 3; s++) acc[m][s] += __shfl_xor_sync(0xffffffffu, acc[m][s], 8);
-                    if ((xl & 1) == 0) {
-                        const int x = xb * 16 + xl;
-                        const int win = pr * (W / 2) + x / 2;
-#pragma unroll
-                        for (int m = 0; m < 8; m++) {
-                            const int mo = hf * 8 + m;
-                            if (mo >= a.M) break;
-                            uint64_t *o = a.out[(size_t)mo * a.nwin + win] + coff + j;
-                            uint64_t v0 = fcanon(acc[m][0], c.qd, c.qid);
-                            uint64_t v1 = fcanon(acc[m][1], c.qd, c.qid);
-                            const uint64_t v2 = fcanon(acc[m][2], c.qd, c.qid);
-                            v0 = add_mod(v0, cst, c.q);
-                            v1 = add_mod(v1, v1, c.q);
-                            o[((size_t)0 * a.ell + l) * N] = v0;
-                            o[((size_t)1 * a.ell + l) * N] = v1;
-                            o[((size_t)2 * a.ell + l) * N] = v2;
+                        for (int s2 = 0; s2 < 3; s2++) {
+                            const double mine = par ? acc[2 + h][s2] : acc[h][s2];
+                            const double give = par ? acc[h][s2] : acc[2 + h][s2];
+                            keep[s2] = mine + __shfl_xor_sync(0xffffffffu, give, 8);
+                        }
+                        const int mo = cg * CPT + 2 * par + h;
+                        if (mo < a.M) {
+                            uint64_t *o = a.obase ? (par ? obm[2 + h] : obm[h]) + (size_t)win * a.ostride
+                                                  : a.out[(size_t)mo * a.nwin + win] + lo;
+                            o[0] = canon_fast(keep[0] + cstd, c.qd, c.qid);
+                            o[cs] = canon_fast(2.0 * keep[1], c.qd, c.qid);
+                            o[2 * cs] = canon_fast(keep[2], c.qd, c.qid);
                         }
                     }
                 }
@@ -451,6 +475,11 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     cudaStream_t s = (cudaStream_t)stream;
     const int nwin = ((y1 - y0) / 2) * (W / 2);
     const int n_in = p * H * W, n_out = M * nwin;
+    const size_t smem = (size_t)P1Layout<2>::RR * (W + 3) * P1Layout<2>::PS + 6 * (size_t)TB + (size_t)n_in * 8;
+    if (smem > 227 * 1024) {
+        he_set_error("he_conv_square_sum_tc: %zu bytes of shared memory (input table of %d)", smem, n_in);
+        return HE_EINVAL;
+    }
     void **din = nullptr, **dout = nullptr;
     HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
     HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
@@ -479,6 +508,17 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     TcArgs a;
     a.in = (const uint64_t *const *)din;
     a.out = (uint64_t *const *)dout;
+    a.obase = nullptr;
+    a.ostride = 0;
+    if (n_out > 1) {  // outputs of one batch allocation: strided addressing, no pointer loads
+        const long long st = (long long)(out[1] - out[0]);
+        bool uni = st > 0;
+        for (int i = 2; i < n_out && uni; i++) uni = (out[i] - out[i - 1]) == st;
+        if (uni) {
+            a.obase = out[0];
+            a.ostride = st;
+        }
+    }
     a.btiles = dbt;
     a.biasd = dbias;
     a.cst = dc;
@@ -498,7 +538,6 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     a.nitems = ell * (c->N / 8);
     a.btile_bytes = TB;
     a.nshift = NSH;
-    const size_t smem = (size_t)P1Layout<2>::RR * (W + 3) * P1Layout<2>::PS + 6 * (size_t)TB;
     int sms = 0;
     HE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
     const dim3 grid((unsigned)std::min(sms, a.nitems));

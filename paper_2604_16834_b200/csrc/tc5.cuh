@@ -21,15 +21,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-// spin until the barrier's phase with the given parity has completed
+// wait until the barrier's phase with the given parity has completed; the
+// suspend-time hint lets the hardware park the warp until the phase flips
+// (no spinning warps stealing issue slots from the epilogue)
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)
         : "memory");
 }
 
