@@ -187,7 +187,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
             const size_t coff = (size_t)(item % nchunk) * 8;
             for (int rr = 0; rr < rows_in; rr++) {
                 const int G = k * rows_in + rr, slot = G % RR, use = G / RR;
-                if (use > 0) tc5::mbar_wait(&bar_empty[slot], (use - 1) & 1);
+                if (use > 0) {  // one warp polls the slot barrier, the others park on a named barrier
+                    if (warp == EPI_WARPS) tc5::mbar_wait(&bar_empty[slot], (use - 1) & 1);
+                    asm volatile("bar.sync 1, %0;" ::"n"(PROD_WARPS * 32) : "memory");
+                }
                 const int y = a.y0 - 1 + rr;
                 const bool inside = y >= 0 && y < H;
                 const uint32_t rbase = ring_s + slot * RS;
@@ -373,6 +376,315 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
     if (warp == MMA_WARP) tc5::tmem_free<512>(tmem);
 }
 
+// ---------------------------------------------------------------- the P16 kernel (conv2 shape)
+// NCI = 3 input components (carried, unrelinearised squares), p = 16 input channels,
+// MC = 16 output channels per CTA (blockIdx parity selects the channel half), W = 16,
+// global sum over rows [y0, y1) -> 5-component outputs.
+//
+// Packing P16: one 16-byte K chunk = byte plane d of the 16 input channels at one
+// pixel (core matrix = 8 coefficients x 16 channels).  Planes are multiplied
+// separately; the byte shift lives in the accumulator's TMEM COLUMN offset: plane
+// d's MMA (N = 32 = 2 weight digits x 16 channels) writes columns d*16 .. d*16+31,
+// i.e. shift blocks d and d+1, so the shift sums accumulate in place.  The first
+// MMA of a (row step, component) uses an N = 96 B tile whose blocks 2..5 are zero,
+// which initialises all six shift blocks (no TMEM clearing pass).
+struct P16Layout {
+    static constexpr int NCI = 3, PLANES = 5;
+    static constexpr int PS = NCI * PLANES * 128;  // pixel stride (bytes)
+    static constexpr int RR = 4;                   // ring rows (3 in use + 1 prefetched)
+    static constexpr int TB = 32 * 32;             // B tile (N = 32 rows x 32 bytes)
+    static constexpr int TB0 = 96 * 32;            // zero-extended K step 0 (N = 96)
+    static constexpr int BBYTES = 6 * TB + TB0;
+};
+
+__device__ __forceinline__ void tr4b(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&o)[4]) {
+    const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w2, w3, 0x5140);
+    const uint32_t t2 = __byte_perm(w0, w1, 0x7362), t3 = __byte_perm(w2, w3, 0x7362);
+    o[0] = __byte_perm(t0, t1, 0x5410);
+    o[1] = __byte_perm(t0, t1, 0x7632);
+    o[2] = __byte_perm(t2, t3, 0x5410);
+    o[3] = __byte_perm(t2, t3, 0x7632);
+}
+
+__global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
+    using LY = P16Layout;
+    constexpr int NCI = 3, PS = LY::PS, RR = LY::RR, NSH = 6;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar_full[RR], bar_empty[RR], bar_dfull[NSLOT], bar_dempty[NSLOT], bar_b;
+    __shared__ uint32_t taddr_s;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int W = a.W, H = a.H;
+    const int RS = (W + 3) * PS;
+    uint8_t *ring = smem;
+    uint8_t *bsm = smem + (size_t)RR * RS;
+    const uint64_t **ptab = (const uint64_t **)(bsm + LY::BBYTES);
+    double *red = (double *)(ptab + a.p * a.H * a.W);  // [4 cg][4 m][5 s][8 j] cross-quarter GAP sums
+    for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.in[i];
+    const size_t N = (size_t)1 << a.logN;
+    const int nchunk = (int)(N / 8);
+    const int rows_in = a.y1 - a.y0 + 2;
+    const int nrows = a.y1 - a.y0;
+    const int half = blockIdx.x & 1;  // grid is even: a CTA always owns the same channel half
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RR; i++) {
+            tc5::mbar_init(&bar_full[i], PROD_WARPS * 32);
+            tc5::mbar_init(&bar_empty[i], 1);
+        }
+        for (int i = 0; i < NSLOT; i++) {
+            tc5::mbar_init(&bar_dfull[i], 1);
+            tc5::mbar_init(&bar_dempty[i], EPI_WARPS * 32);
+        }
+        tc5::mbar_init(&bar_b, 1);
+        tc5::mbar_fence_init();
+    }
+    for (int i = threadIdx.x * 16; i < RR * RS; i += THREADS * 16) *(uint4 *)(ring + i) = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        tc5::mbar_arrive_expect_tx(&bar_b, (uint32_t)LY::BBYTES);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         tc5::smem_u32(bsm)),
+                     "l"(a.btiles + (size_t)half * LY::BBYTES), "r"((uint32_t)LY::BBYTES), "r"(tc5::smem_u32(&bar_b))
+                     : "memory");
+    }
+    if (warp == MMA_WARP) tc5::tmem_alloc<512>(&taddr_s);
+    tc5::fence_async_smem();
+    tc5::tc_fence_before();
+    __syncthreads();
+    tc5::tc_fence_after();
+    const uint32_t tmem = taddr_s;
+
+    if (warp >= EPI_WARPS && warp < EPI_WARPS + PROD_WARPS) {
+        // ======================= producers: input rows -> plane-separated ring rows
+        const int pt = threadIdx.x - EPI_WARPS * 32;
+        constexpr int PT = PROD_WARPS * 32;
+        const uint32_t ring_s = tc5::smem_u32(ring);
+        const int ntask = W * NCI * 16;  // (pixel, component, coefficient pair, channel group of 4)
+        constexpr int TPT = 4;
+        const int kflip = (lane >> 4) & 1;  // half-warps store opposite coefficients first (no bank conflicts)
+        int k = 0;
+        for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
+            const int it = item >> 1;
+            const int l = a.limbs[it / nchunk];
+            const size_t coff = (size_t)(it % nchunk) * 8;
+            for (int rr = 0; rr < rows_in; rr++) {
+                const int G = k * rows_in + rr, slot = G % RR, use = G / RR;
+                if (use > 0) {
+                    if (warp == EPI_WARPS) tc5::mbar_wait(&bar_empty[slot], (use - 1) & 1);
+                    asm volatile("bar.sync 1, %0;" ::"n"(PROD_WARPS * 32) : "memory");
+                }
+                const int y = a.y0 - 1 + rr;
+                const bool inside = y >= 0 && y < H;
+                const uint32_t rbase = ring_s + slot * RS;
+                for (int t0 = pt; t0 < ntask; t0 += TPT * PT) {
+                    uint64_t v[TPT][4][2];
+#pragma unroll
+                    for (int u = 0; u < TPT; u++) {
+                        const int t = t0 + u * PT;
+                        const int g = t & 3, jp = (t >> 2) & 3, cx = t >> 4, c = cx % NCI, x = cx / NCI;
+#pragma unroll
+                        for (int ch = 0; ch < 4; ch++) {
+                            v[u][ch][0] = v[u][ch][1] = 0;
+                            const int i = 4 * g + ch;
+                            if (t < ntask && inside && i < a.p) {
+                                const uint64_t *src = ptab[(size_t)i * H * W + (size_t)y * W + x];
+                                ldg128(src + ((size_t)c * a.ell + l) * N + coff + 2 * jp, v[u][ch][0], v[u][ch][1]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < TPT; u++) {
+                        const int t = t0 + u * PT;
+                        if (t >= ntask) break;
+                        const int g = t & 3, jp = (t >> 2) & 3, cx = t >> 4, c = cx % NCI, x = cx / NCI;
+                        const uint32_t base = rbase + (x + 1) * PS + c * (5 * 128) + g * 4;
+#pragma unroll
+                        for (int kk = 0; kk < 2; kk++) {
+                            const int kc = kk ^ kflip;  // coefficient 2 jp + kc
+                            uint32_t lo[4], hi[4];
+                            const uint64_t a0 = kc ? v[u][0][1] : v[u][0][0], a1 = kc ? v[u][1][1] : v[u][1][0];
+                            const uint64_t a2 = kc ? v[u][2][1] : v[u][2][0], a3 = kc ? v[u][3][1] : v[u][3][0];
+                            tr4b((uint32_t)a0, (uint32_t)a1, (uint32_t)a2, (uint32_t)a3, lo);
+                            tr4b((uint32_t)(a0 >> 32), (uint32_t)(a1 >> 32), (uint32_t)(a2 >> 32), (uint32_t)(a3 >> 32),
+                                 hi);
+                            const uint32_t dst = base + (2 * jp + kc) * 16;
+#pragma unroll
+                            for (int d = 0; d < 4; d++)
+                                asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst + d * 128), "r"(lo[d]));
+                            asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst + 4 * 128), "r"(hi[0]));
+                        }
+                    }
+                }
+                tc5::fence_async_smem();
+                tc5::mbar_arrive(&bar_full[slot]);
+            }
+        }
+    } else if (warp == MMA_WARP) {
+        // ======================= MMA issuer
+        if (lane == 0) {
+            tc5::mbar_wait(&bar_b, 0);
+            const uint32_t ring_s = tc5::smem_u32(ring), b_s = tc5::smem_u32(bsm);
+            const uint32_t idesc32 = tc5::idesc_u8s8(128, 32), idesc96 = tc5::idesc_u8s8(128, 96);
+            const uint32_t blbo = 32 * 16, blbo0 = 96 * 16;
+            int k = 0, S = 0;
+            for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
+                const int Gb = k * rows_in;
+                auto slot_of = [&](int y) { return (Gb + (y - (a.y0 - 1))) % RR; };
+                for (int y = a.y0; y < a.y1; y++) {
+                    for (int yy = y - 1; yy <= y + 1; yy++) {
+                        const int G = Gb + (yy - (a.y0 - 1));
+                        tc5::mbar_wait(&bar_full[G % RR], (G / RR) & 1);
+                    }
+                    tc5::tc_fence_after();
+                    const uint32_t r0 = ring_s + slot_of(y - 1) * RS, r1 = ring_s + slot_of(y) * RS,
+                                   r2 = ring_s + slot_of(y + 1) * RS;
+                    const bool fwd = r1 > r0;  // K step 3 pairs (0,2)+(1,2) in ring order
+                    for (int c = 0; c < NCI; c++, S++) {
+                        const int ds = S % NSLOT;
+                        if (S >= NSLOT) tc5::mbar_wait(&bar_dempty[ds], ((S / NSLOT) - 1) & 1);
+                        tc5::tc_fence_after();
+#pragma unroll 1
+                        for (int d = 0; d < 5; d++) {
+                            const uint32_t dcol = tmem + (uint32_t)ds * 128 + d * 16;
+                            const uint32_t co = (uint32_t)(c * 5 + d) * 128;
+                            if (d == 0)
+                                tc5::mma_i8(dcol, tc5::sdesc(r0 + co, PS, PS),
+                                            tc5::sdesc(b_s + 6 * LY::TB, blbo0, 128), idesc96, 0);
+                            else
+                                tc5::mma_i8(dcol, tc5::sdesc(r0 + co, PS, PS), tc5::sdesc(b_s + 0 * LY::TB, blbo, 128),
+                                            idesc32, 1);
+                            tc5::mma_i8(dcol, tc5::sdesc(r1 + co, PS, PS), tc5::sdesc(b_s + 1 * LY::TB, blbo, 128),
+                                        idesc32, 1);
+                            tc5::mma_i8(dcol, tc5::sdesc(r2 + co, PS, PS), tc5::sdesc(b_s + 2 * LY::TB, blbo, 128),
+                                        idesc32, 1);
+                            if (fwd)
+                                tc5::mma_i8(dcol, tc5::sdesc(r0 + co + 2 * PS, r1 - r0, PS),
+                                            tc5::sdesc(b_s + 3 * LY::TB, blbo, 128), idesc32, 1);
+                            else
+                                tc5::mma_i8(dcol, tc5::sdesc(r1 + co + 2 * PS, r0 - r1, PS),
+                                            tc5::sdesc(b_s + 5 * LY::TB, blbo, 128), idesc32, 1);
+                            tc5::mma_i8(dcol, tc5::sdesc(r2 + co + 2 * PS, PS, PS),
+                                        tc5::sdesc(b_s + 4 * LY::TB, blbo, 128), idesc32, 1);
+                        }
+                        tc5::tc_commit(&bar_dfull[ds]);
+                    }
+                    tc5::tc_commit(&bar_empty[slot_of(y - 1)]);  // row y-1 is not read again
+                }
+                tc5::tc_commit(&bar_empty[slot_of(a.y1 - 1)]);
+                tc5::tc_commit(&bar_empty[slot_of(a.y1)]);
+            }
+        }
+        __syncwarp();
+    } else if (warp < EPI_WARPS) {
+        // ======================= epilogue
+        const int qd = warp & 3, cg = warp >> 2;
+        const int row = qd * 32 + lane, j = row & 7;
+        const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(cg * CPT);
+        int k = 0, S = 0;
+        for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
+            const int it = item >> 1;
+            const int l = a.limbs[it / nchunk];
+            const size_t coff = (size_t)(it % nchunk) * 8;
+            const ModConst c = a.mc[l];
+            const double yc = a.yc[l];
+            const int m0 = half * MC + cg * CPT;  // this thread's first output channel
+            double gs[CPT][5];  // (y0 y0, y0 y1, 2 y0 y2 + y1 y1, y1 y2, y2 y2) over the thread's pixel column
+#pragma unroll
+            for (int m = 0; m < CPT; m++)
+#pragma unroll
+                for (int s2 = 0; s2 < 5; s2++) gs[m][s2] = 0.0;
+            for (int yr = 0; yr < nrows; yr++) {
+                double yv[NCI][CPT];
+#pragma unroll
+                for (int cc = 0; cc < NCI; cc++, S++) {
+                    const int ds = S % NSLOT;
+                    tc5::mbar_wait(&bar_dfull[ds], (S / NSLOT) & 1);
+                    tc5::tc_fence_after();
+                    int C[CPT][NSH];
+                    const uint32_t ta = tq + (uint32_t)ds * 128;
+#pragma unroll
+                    for (int s2 = 0; s2 < NSH; s2++) {
+                        uint32_t r[4];
+                        tc5::tld4(ta + s2 * 16, r);
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) C[m][s2] = (int)r[m];
+                    }
+                    tc5::tld_wait();
+                    tc5::tc_fence_before();
+                    tc5::mbar_arrive(&bar_dempty[ds]);
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) yv[cc][m] = recombine<NSH>(C[m], yc, c);
+                }
+#pragma unroll
+                for (int m = 0; m < CPT; m++) {
+                    const double d0 = yv[0][m] + a.biasd[(size_t)(m0 + m) * a.ell + l], d1 = yv[1][m], d2 = yv[2][m];
+                    gs[m][0] += fmulmod(d0, d0, c.qd, c.qid);
+                    gs[m][1] += fmulmod(d0, d1, c.qd, c.qid);
+                    gs[m][2] += fmulmod(d0 + d0, d2, c.qd, c.qid) + fmulmod(d1, d1, c.qd, c.qid);
+                    gs[m][3] += fmulmod(d1, d2, c.qd, c.qid);
+                    gs[m][4] += fmulmod(d2, d2, c.qd, c.qid);
+                }
+                if ((yr & 15) == 15)  // keep the exact sums below 2^53: centre every 16 rows
+#pragma unroll
+                    for (int m = 0; m < CPT; m++)
+#pragma unroll
+                        for (int s2 = 0; s2 < 5; s2++) {
+                            const double e = fma(gs[m][s2], c.qid, 6755399441055744.0) - 6755399441055744.0;
+                            gs[m][s2] = fma(-e, c.qd, gs[m][s2]);
+                        }
+            }
+            // centre, then sum the 16 pixels of the row: 4 per warp (lanes ^ 8, ^ 16), 4 quarters via shared memory
+#pragma unroll
+            for (int m = 0; m < CPT; m++)
+#pragma unroll
+                for (int s2 = 0; s2 < 5; s2++) {
+                    double v = gs[m][s2];
+                    const double e = fma(v, c.qid, 6755399441055744.0) - 6755399441055744.0;
+                    v = fma(-e, c.qd, v);  // |v| <= q/2 + 1
+                    v += __shfl_xor_sync(0xffffffffu, v, 8);
+                    v += __shfl_xor_sync(0xffffffffu, v, 16);
+                    gs[m][s2] = v;
+                }
+            // quarters 0..3 add into red[cg] in turn (named barrier over the epilogue warps)
+            double *rr2 = red + (size_t)cg * (CPT * 5 * 8);
+            for (int q2 = 0; q2 < 4; q2++) {
+                if (qd == q2 && lane < 8)
+#pragma unroll
+                    for (int m = 0; m < CPT; m++)
+#pragma unroll
+                        for (int s2 = 0; s2 < 5; s2++) {
+                            double *p = rr2 + (m * 5 + s2) * 8 + lane;
+                            const double v = q2 ? *p + gs[m][s2] : gs[m][s2];
+                            if (q2 < 3)
+                                *p = v;
+                            else
+                                gs[m][s2] = v;
+                        }
+                asm volatile("bar.sync 2, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+            }
+            if (qd == 3 && lane < 8) {
+                const size_t lo = (size_t)l * N + coff + j;
+                const size_t cs = (size_t)a.ell * N;
+                const double cstd = a.cst ? (double)a.cst[l] : 0.0;
+#pragma unroll
+                for (int m = 0; m < CPT; m++) {
+                    const int mo = m0 + m;
+                    if (mo >= a.M) break;
+                    uint64_t *o = (a.obase ? a.obase + (size_t)mo * a.ostride : a.out[mo]) + lo;
+                    o[0] = canon_fast(gs[m][0] + cstd, c.qd, c.qid);
+                    o[cs] = canon_fast(2.0 * gs[m][1], c.qd, c.qid);
+                    o[2 * cs] = canon_fast(gs[m][2], c.qd, c.qid);
+                    o[3 * cs] = canon_fast(2.0 * gs[m][3], c.qd, c.qid);
+                    o[4 * cs] = canon_fast(gs[m][4], c.qd, c.qid);
+                }
+            }
+        }
+    }
+    tc5::tc_fence_before();
+    __syncthreads();
+    if (warp == MMA_WARP) tc5::tmem_free<512>(tmem);
+}
+
 // balanced signed base-256 digit e of w
 inline int digit_s8(int64_t w, int e) {
     for (int i = 0; i < e; i++) {
@@ -413,6 +725,32 @@ static void build_btiles_p1(const int64_t *weights, int M, int p, int E, int NSH
         }
 }
 
+// B tiles of the P16 packing for channel half h (rows n = e * 16 + m, m = output channel 16 h + m):
+// tiles 0..5 as P1 (N = 32), tile 6 = K step 0 zero-extended to N = 96 (initialises all six shift blocks).
+static void build_btiles_p16(const int64_t *weights, int M, int p, std::vector<uint8_t> &bt) {
+    const int ks[6][2][2] = {{{0, 0}, {0, 1}}, {{1, 0}, {1, 1}}, {{2, 0}, {2, 1}},
+                             {{0, 2}, {1, 2}}, {{2, 2}, {-1, -1}}, {{1, 2}, {0, 2}}};
+    const int BB = P16Layout::BBYTES;
+    bt.assign((size_t)2 * BB, 0);
+    for (int h = 0; h < 2; h++)
+        for (int t = 0; t < 7; t++) {
+            const int kt = t == 6 ? 0 : t, NR = t == 6 ? 96 : 32;
+            uint8_t *tile = bt.data() + (size_t)h * BB + (size_t)t * P16Layout::TB;
+            for (int k = 0; k < 2; k++) {
+                const int dy = ks[kt][k][0], dx = ks[kt][k][1];
+                if (dy < 0) continue;
+                const int tap = dy * 3 + dx;
+                for (int n = 0; n < 32; n++) {
+                    const int e = n / 16, m = h * 16 + n % 16;
+                    if (m >= M) continue;
+                    for (int i = 0; i < p && i < 16; i++)
+                        tile[(size_t)k * NR * 16 + (size_t)(n / 8) * 128 + (n % 8) * 16 + i] =
+                            (uint8_t)(int8_t)digit_s8(weights[(size_t)m * p * 9 + i * 9 + tap], e);
+                }
+            }
+        }
+}
+
 static int g_conv_tc = 1;  // he_set_conv_tc: 0 forces the mma.sync kernels (A/B tests)
 
 extern "C" int he_set_conv_tc(int on) {
@@ -430,7 +768,8 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
         return HE_EINVAL;
     }
     const bool p1 = nci == 2 && p <= 3 && pool && M <= MC && W % 16 == 0 && W <= 64 && !((y0 | y1 | H) & 1);
-    if (!p1) {
+    const bool p16 = nci == 3 && p == 16 && !pool && M <= 2 * MC && W == 16;
+    if (!p1 && !p16) {
         he_set_error("he_conv_square_sum_tc: shape (nci=%d p=%d M=%d W=%d pool=%d) not covered", nci, p, M, W, pool);
         return HE_EINVAL;
     }
@@ -447,15 +786,18 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
         E++;
         cap = cap * 256 + 127;
     }
-    if (wmax > cap) {
-        he_set_error("he_conv_square_sum_tc: weights need more than 3 signed byte digits");
+    if (wmax > cap || (p16 && E > 2)) {
+        he_set_error("he_conv_square_sum_tc: weights need more than %d signed byte digits", p16 ? 2 : 3);
         return HE_EINVAL;
     }
-    const int NSH = NB + E - 1;
+    const int NSH = p16 ? 6 : NB + E - 1;
     std::vector<uint8_t> bt;
-    build_btiles_p1(weights, M, p, E, NSH, bt);
-    const int TB = NSH * MC * 32;
-    std::vector<double> biasd((size_t)MC * ell, 0.0), yc(ell);
+    if (p16)
+        build_btiles_p16(weights, M, p, bt);
+    else
+        build_btiles_p1(weights, M, p, E, NSH, bt);
+    const int TB = p16 ? P16Layout::TB : NSH * MC * 32;
+    std::vector<double> biasd((size_t)2 * MC * ell, 0.0), yc(ell);
     for (int l = 0; l < ell; l++) {
         const uint64_t q = c->mod[l];
         yc[l] = (double)(((uint64_t)1 << 32) % q);
@@ -473,9 +815,11 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
             }
     }
     cudaStream_t s = (cudaStream_t)stream;
-    const int nwin = ((y1 - y0) / 2) * (W / 2);
+    const int nwin = pool ? ((y1 - y0) / 2) * (W / 2) : 1;
     const int n_in = p * H * W, n_out = M * nwin;
-    const size_t smem = (size_t)P1Layout<2>::RR * (W + 3) * P1Layout<2>::PS + 6 * (size_t)TB + (size_t)n_in * 8;
+    const size_t smem = p16 ? (size_t)P16Layout::RR * (W + 3) * P16Layout::PS + P16Layout::BBYTES + (size_t)n_in * 8 +
+                                  (size_t)4 * MC * 5 * 8 * 8
+                            : (size_t)P1Layout<2>::RR * (W + 3) * P1Layout<2>::PS + 6 * (size_t)TB + (size_t)n_in * 8;
     if (smem > 227 * 1024) {
         he_set_error("he_conv_square_sum_tc: %zu bytes of shared memory (input table of %d)", smem, n_in);
         return HE_EINVAL;
@@ -535,12 +879,12 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     a.y0 = y0;
     a.y1 = y1;
     a.nwin = nwin;
-    a.nitems = ell * (c->N / 8);
+    a.nitems = ell * (c->N / 8) * (p16 ? 2 : 1);
     a.btile_bytes = TB;
     a.nshift = NSH;
     int sms = 0;
     HE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-    const dim3 grid((unsigned)std::min(sms, a.nitems));
+    const dim3 grid((unsigned)(p16 ? std::min(sms, a.nitems) & ~1 : std::min(sms, a.nitems)));  // P16: even
     int rc = HE_OK;
     auto launch = [&](auto kern) -> int {
         HE_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -548,7 +892,8 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
         HE_CHECK_LAUNCH();
         return HE_OK;
     };
-    if (NSH == 5) rc = launch(k_convtc_p1_pool<5>);
+    if (p16) rc = launch(k_convtc_p16_gap);
+    else if (NSH == 5) rc = launch(k_convtc_p1_pool<5>);
     else if (NSH == 6) rc = launch(k_convtc_p1_pool<6>);
     else rc = launch(k_convtc_p1_pool<7>);
     he_scratch_free(meta, s);

@@ -65,6 +65,27 @@ def test_convtc_pool_vs_oracle(small, W, H, rows, wbits, p, M):
         assert np.array_equal(to_np(o), r), k
 
 
+@pytest.mark.parametrize("H,rows,wbits,M", [(2, (0, 2), 14, 18), (4, (1, 3), 9, 32)])
+def test_convtc_gap_vs_oracle(small, H, rows, wbits, M):
+    """conv2 shape class (3-component carried inputs, 16 -> M channels, 16 wide, global sum)
+    vs the oracle chain: 5-component window sums, both channel halves."""
+    eng, orc = small
+    rng = np.random.default_rng(200 + H + wbits)
+    ell, p, W = 3, 16, 16
+    mods = eng.moduli[:ell]
+    x = rand_residues(rng, mods, (p * H * W, 3), eng.N)
+    ins = [from_np(x[i], eng.device) for i in range(p * H * W)]
+    lim = 1 << wbits
+    wi = rng.integers(-lim, lim, size=(M, 9 * p), dtype=np.int64)
+    bres = np.array([[int(rng.integers(0, q)) for q in mods] for _ in range(M)], np.uint64)
+    cst = np.array([int(rng.integers(0, q)) for q in mods], np.uint64)
+    y0, y1 = rows
+    got = _run(eng, eng._L.he_conv_square_sum_tc, ins, 3, p, H, W, M, 0, y0, y1, wi, bres, cst, ell)
+    ref = _oracle_conv_square_sum(orc, [x[i] for i in range(p * H * W)], p, H, W, wi, bres, cst, 0, y0, y1)
+    for k, (o, r) in enumerate(zip(got, ref)):
+        assert np.array_equal(to_np(o), r), k
+
+
 def _rand_dev(eng, count, nci, ell, seed):
     import torch
 
@@ -98,6 +119,34 @@ def test_convtc_conv1_shape_vs_mma_sync():
         old = L.he_set_conv_tc(0)
         try:
             ref = _run(eng, L.he_conv_square_sum_n, ins, 2, p, H, W, M, 1, y0, y1, wi, bres, cst, ell)
+        finally:
+            L.he_set_conv_tc(old)
+        torch.cuda.synchronize()
+        for k, (o, r) in enumerate(zip(got, ref)):
+            assert torch.equal(o, r), (y0, y1, k)
+
+
+def test_convtc_conv2_shape_vs_mma_sync():
+    """config 3's conv2 launch (carried 3-component inputs, 16 -> 32, 16 wide, 9 limbs, N = 2^16,
+    14-bit weights, global sum) on an 8-row image: tcgen05 kernel == mma.sync kernel."""
+    import torch
+
+    from paper_2604_16834_b200.engine import GpuEngine
+
+    eng = GpuEngine(engine_context("cfg3"))
+    L = eng._L
+    p, H, W, M, ell = 16, 8, 16, 32, 9
+    x = _rand_dev(eng, p * H * W, 3, ell, 6)
+    ins = [x[i] for i in range(p * H * W)]
+    rng = np.random.default_rng(9)
+    wi = rng.integers(-(1 << 14), 1 << 14, size=(M, 9 * p), dtype=np.int64)
+    bres = np.array([[int(rng.integers(0, q)) for q in eng.moduli[:ell]] for _ in range(M)], np.uint64)
+    cst = np.array([int(rng.integers(0, q)) for q in eng.moduli[:ell]], np.uint64)
+    for y0, y1 in ((0, 8), (2, 6)):
+        got = _run(eng, L.he_conv_square_sum_tc, ins, 3, p, H, W, M, 0, y0, y1, wi, bres, cst, ell)
+        old = L.he_set_conv_tc(0)
+        try:
+            ref = _run(eng, L.he_conv_square_sum_n, ins, 3, p, H, W, M, 0, y0, y1, wi, bres, cst, ell)
         finally:
             L.he_set_conv_tc(old)
         torch.cuda.synchronize()
