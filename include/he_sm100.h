@@ -259,6 +259,9 @@ int he_microbench_imma(int device, double *mac_per_s);
  * M=128 x N=n x K=32 MMAs from shared memory, rates[1] = cycles per MMA. */
 int he_tc5_selftest(int device, int n, int layout, int32_t *d_out);
 int he_microbench_tc5(int device, int n, double *rates);
+/* the same with the A operand's 8-row groups a_sbo bytes apart and its K chunks
+ * a_lbo bytes apart (pixel-strided conv rings) */
+int he_microbench_tc5_strided(int device, int n, int a_sbo, int a_lbo, double *rates);
 /* The fused conv + square + pool / global-sum layer on the 5th-generation
  * tensor cores (tcgen05.mma kind::i8, TMEM accumulators, warp-specialised
  * producer / MMA / epilogue; csrc/convtc.cu).  Same arguments and results as
@@ -270,6 +273,11 @@ int he_conv_square_sum_tc(he_ctx *ctx, const uint64_t *const *in, int nci, int p
                           uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
                           const uint64_t *bias, const uint64_t *cst, int ell, void *stream);
 int he_set_conv_tc(int on);
+/* diagnostics: per-role cycle counters of the tcgen05 conv kernels.  on != 0
+ * enables and zeroes them; on == 0 writes out[7] = summed cycles (producer
+ * wait-empty, producer total, MMA wait-full, MMA wait-dempty, MMA total,
+ * epilogue wait-dfull, epilogue total; one sampled thread per role per CTA). */
+int he_convtc_profile(int on, double *out);
 
 #ifdef __cplusplus
 }

@@ -38,8 +38,10 @@ EXPORTS = [
     "he_microbench_imma",
     "he_tc5_selftest",
     "he_microbench_tc5",
+    "he_microbench_tc5_strided",
     "he_conv_square_sum_tc",
     "he_set_conv_tc",
+    "he_convtc_profile",
     "he_rotate_hoisted",
     "he_gen_hoist_key",
 ]
@@ -119,8 +121,10 @@ def load():
         "he_microbench_imma": (i, [i, vp]),
         "he_tc5_selftest": (i, [i, i, i, vp]),
         "he_microbench_tc5": (i, [i, i, vp]),
+        "he_microbench_tc5_strided": (i, [i, i, i, i, vp]),
         "he_conv_square_sum_tc": (i, [vp, vp, i, i, i, i, vp, i, i, i, i, vp, vp, vp, i, vp]),
         "he_set_conv_tc": (i, [i]),
+        "he_convtc_profile": (i, [i, vp]),
         "he_rotate_hoisted": (i, [vp, vp, i, pp, pp, i, i, vp]),
         "he_gen_hoist_key": (i, [vp, u32, vp]),
         "he_square_sum": (i, [vp, pp, i, pp, i, vp, vp, vp, i, vp]),

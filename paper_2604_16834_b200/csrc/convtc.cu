@@ -33,6 +33,7 @@
 //     (row step, component)) let the MMAs of the next components run while
 //     the epilogue does its FP64 work.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "ntt_core.cuh"  // u2d / d2u / fmulmod / fcanon
@@ -51,6 +52,8 @@ constexpr int MC = 16;           // output channels per CTA
 
 struct TcArgs {
     const uint64_t *const *in;   // [p*H*W] input ciphertexts (NCI components x ell limbs)
+    const uint64_t *ibase;       // input i = ibase + ioff[i] * 32 words (256-byte units; staged in shared memory)
+    const uint32_t *ioff;
     uint64_t *const *out;        // pool: [M][nwin] (3 components); GAP: [M]
     uint64_t *obase;             // != nullptr: out[k] = obase + k * ostride (one batch allocation)
     long long ostride;           // elements
@@ -62,7 +65,19 @@ struct TcArgs {
     const int32_t *limbs;        // [nlimbs] limb of limb-index
     int nlimbs, ell, logN, p, H, W, M, y0, y1, nwin, nitems;
     int btile_bytes, nshift;     // bytes per B tile, shift sums (N = nshift * 16)
+    unsigned long long *prof;    // != nullptr: per-role cycle counters (he_convtc_profile)
+    int exp;                     // diagnostics (CONVTC_EXP): 1 = epilogue skips the products
 };
+
+// role timing (he_convtc_profile): [0] producer wait-empty, [1] producer total, [2] MMA wait-full,
+// [3] MMA wait-dempty, [4] MMA total, [5] epilogue wait-dfull, [6] epilogue total (one sampled
+// thread per role, summed over CTAs)
+#define PWAIT(slot, call)                                       \
+    do {                                                        \
+        const long long _t0 = prof_on ? clock64() : 0;          \
+        call;                                                   \
+        if (prof_on) pc[slot] += clock64() - _t0;               \
+    } while (0)
 
 // ---------------------------------------------------------------- shared layout
 // ring row: (W + 3) pixel slots (halo, W pixels, halo, pad) x NCI components x
@@ -137,9 +152,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
     const int RS = (W + 3) * PS;  // ring row stride
     uint8_t *ring = smem;
     uint8_t *bsm = smem + (size_t)RR * RS;
-    // input address table, staged once (every work item reads the same ciphertexts)
-    const uint64_t **ptab = (const uint64_t **)(bsm + 6 * (size_t)a.btile_bytes);
-    for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.in[i];
+    // input address table (32-bit offsets), staged once: every work item reads the same ciphertexts
+    uint32_t *ptab = (uint32_t *)(bsm + 6 * (size_t)a.btile_bytes);
+    for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.ioff[i];
     const size_t N = (size_t)1 << a.logN;
     const int nchunk = (int)(N / 8);
     const int rows_in = a.y1 - a.y0 + 2;
@@ -173,6 +188,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
     __syncthreads();
     tc5::tc_fence_after();
     const uint32_t tmem = taddr_s;
+    const bool prof_on = a.prof && (threadIdx.x == 0 || threadIdx.x == EPI_WARPS * 32 || threadIdx.x == MMA_WARP * 32);
+    long long pc[7] = {0, 0, 0, 0, 0, 0, 0};
+    const long long t_start = clock64();
 
     if (warp >= EPI_WARPS && warp < EPI_WARPS + PROD_WARPS) {
         // ======================= producers: input rows -> packed ring rows
@@ -188,7 +206,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
             for (int rr = 0; rr < rows_in; rr++) {
                 const int G = k * rows_in + rr, slot = G % RR, use = G / RR;
                 if (use > 0) {  // one warp polls the slot barrier, the others park on a named barrier
-                    if (warp == EPI_WARPS) tc5::mbar_wait(&bar_empty[slot], (use - 1) & 1);
+                    if (warp == EPI_WARPS) PWAIT(0, tc5::mbar_wait(&bar_empty[slot], (use - 1) & 1));
                     asm volatile("bar.sync 1, %0;" ::"n"(PROD_WARPS * 32) : "memory");
                 }
                 const int y = a.y0 - 1 + rr;
@@ -205,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                         for (int i = 0; i < 3; i++) {
                             v[u][i][0] = v[u][i][1] = 0;
                             if (t < ntask && inside && i < a.p) {
-                                const uint64_t *src = ptab[(size_t)i * H * W + (size_t)y * W + x];
+                                const uint64_t *src = a.ibase + (size_t)ptab[i * H * W + y * W + x] * 32;
                                 ldg128(src + ((size_t)c * a.ell + l) * N + coff + 2 * jp, v[u][i][0], v[u][i][1]);
                             }
                         }
@@ -235,6 +253,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
             const uint32_t ring_s = tc5::smem_u32(ring), b_s = tc5::smem_u32(bsm);
             const uint32_t idesc = tc5::idesc_u8s8(128, NCOL);
             const uint32_t blbo = NCOL * 16;  // B: chunk 0 rows then chunk 1 rows
+            const uint32_t ahi = tc5::sdesc_hi(PS), lps = tc5::sdesc_lbo(PS);
+            uint64_t bd[6];
+            for (int t = 0; t < 6; t++) bd[t] = tc5::sdesc(b_s + t * a.btile_bytes, blbo, 128);
             int k = 0, S = 0;
             for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
                 const int Gb = k * rows_in;  // ring index of input row y0 - 1
@@ -244,36 +265,32 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                     // rows yp-1 .. yp+2 must be resident
                     for (int y = yp - 1; y <= yp + 2; y++) {
                         const int G = Gb + (y - (a.y0 - 1));
-                        tc5::mbar_wait(&bar_full[G % RR], (G / RR) & 1);
+                        PWAIT(2, tc5::mbar_wait(&bar_full[G % RR], (G / RR) & 1));
                     }
                     tc5::tc_fence_after();
                     for (int xb = 0; xb < XB; xb++)
                         for (int dyb = 0; dyb < 2; dyb++) {
                             const int y = yp + dyb;
-                            const uint32_t r0 = ring_s + slot_of(y - 1) * RS, r1 = ring_s + slot_of(y) * RS,
-                                           r2 = ring_s + slot_of(y + 1) * RS;
-                            const uint32_t xo = (uint32_t)(xb * 16) * PS;
+                            // descriptor low words: (address >> 4) | LBO field
+                            const uint32_t r0 = (ring_s + slot_of(y - 1) * RS) >> 4,
+                                           r1 = (ring_s + slot_of(y) * RS) >> 4,
+                                           r2 = (ring_s + slot_of(y + 1) * RS) >> 4;
+                            const uint32_t xo = (uint32_t)(xb * 16) * (PS >> 4);
+                            const uint32_t lv = r1 > r0 ? tc5::sdesc_lbo((r1 - r0) << 4) : tc5::sdesc_lbo((r0 - r1) << 4);
+                            const uint32_t a3 = (r1 > r0 ? r0 : r1) + 2 * (PS >> 4) + lv;
+                            const uint64_t b3 = r1 > r0 ? bd[3] : bd[5];
                             for (int c = 0; c < NCI; c++, S++) {
                                 const int ds = S % NSLOT;
-                                if (S >= NSLOT) tc5::mbar_wait(&bar_dempty[ds], ((S / NSLOT) - 1) & 1);
+                                if (S >= NSLOT) PWAIT(3, tc5::mbar_wait(&bar_dempty[ds], ((S / NSLOT) - 1) & 1));
                                 tc5::tc_fence_after();
                                 const uint32_t d = tmem + (uint32_t)ds * 128;
-                                const uint32_t co = xo + c * 128;
+                                const uint32_t co = xo + c * (128 >> 4);
                                 // K steps: (dy,0)+(dy,1) for dy = 0..2; (0,2)+(1,2); (2,2)+pad
-                                tc5::mma_i8(d, tc5::sdesc(r0 + co, PS, PS), tc5::sdesc(b_s + 0 * a.btile_bytes, blbo, 128),
-                                            idesc, 0);
-                                tc5::mma_i8(d, tc5::sdesc(r1 + co, PS, PS), tc5::sdesc(b_s + 1 * a.btile_bytes, blbo, 128),
-                                            idesc, 1);
-                                tc5::mma_i8(d, tc5::sdesc(r2 + co, PS, PS), tc5::sdesc(b_s + 2 * a.btile_bytes, blbo, 128),
-                                            idesc, 1);
-                                if (r1 > r0)
-                                    tc5::mma_i8(d, tc5::sdesc(r0 + co + 2 * PS, r1 - r0, PS),
-                                                tc5::sdesc(b_s + 3 * a.btile_bytes, blbo, 128), idesc, 1);
-                                else  // ring wrap: (1,2) first, swapped B tile
-                                    tc5::mma_i8(d, tc5::sdesc(r1 + co + 2 * PS, r0 - r1, PS),
-                                                tc5::sdesc(b_s + 5 * a.btile_bytes, blbo, 128), idesc, 1);
-                                tc5::mma_i8(d, tc5::sdesc(r2 + co + 2 * PS, PS, PS),
-                                            tc5::sdesc(b_s + 4 * a.btile_bytes, blbo, 128), idesc, 1);
+                                tc5::mma_i8_set(d, tc5::sdesc_hl(ahi, r0 + co + lps), bd[0], idesc);
+                                tc5::mma_i8_acc(d, tc5::sdesc_hl(ahi, r1 + co + lps), bd[1], idesc);
+                                tc5::mma_i8_acc(d, tc5::sdesc_hl(ahi, r2 + co + lps), bd[2], idesc);
+                                tc5::mma_i8_acc(d, tc5::sdesc_hl(ahi, a3 + co), b3, idesc);
+                                tc5::mma_i8_acc(d, tc5::sdesc_hl(ahi, r2 + co + 2 * (PS >> 4) + lps), bd[4], idesc);
                                 tc5::tc_commit(&bar_dfull[ds]);
                             }
                         }
@@ -318,7 +335,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
 #pragma unroll
                         for (int cc = 0; cc < NCI; cc++, S++) {
                             const int ds = S % NSLOT;
-                            tc5::mbar_wait(&bar_dfull[ds], (S / NSLOT) & 1);
+                            PWAIT(5, tc5::mbar_wait(&bar_dfull[ds], (S / NSLOT) & 1));
                             tc5::tc_fence_after();
                             int C[CPT][NSH];
                             const uint32_t ta = tq + (uint32_t)ds * 128;
@@ -371,6 +388,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
             }
         }
     }
+    if (prof_on) {
+        const int tot = threadIdx.x == 0 ? 6 : threadIdx.x == EPI_WARPS * 32 ? 1 : 4;
+        pc[tot] = clock64() - t_start;
+        for (int i = 0; i < 7; i++)
+            if (pc[i]) atomicAdd(a.prof + i, (unsigned long long)pc[i]);
+    }
     tc5::tc_fence_before();
     __syncthreads();
     if (warp == MMA_WARP) tc5::tmem_free<512>(tmem);
@@ -391,7 +414,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
 struct P16Layout {
     static constexpr int NCI = 3, PLANES = 5;
     static constexpr int PS = NCI * PLANES * 128;  // pixel stride (bytes)
-    static constexpr int RR = 4;                   // ring rows (3 in use + 1 prefetched)
+    static constexpr int RR = 4;                   // ring rows (3 in use + 1; plus 2 half rows staged)
+    static constexpr int STG = 2 * 8 * NCI * 16 * 64;  // cp.async staging: 2 half rows
     static constexpr int TB = 32 * 32;             // B tile (N = 32 rows x 32 bytes)
     static constexpr int TB0 = 96 * 32;            // zero-extended K step 0 (N = 96)
     static constexpr int BBYTES = 6 * TB + TB0;
@@ -409,8 +433,9 @@ __device__ __forceinline__ void tr4b(uint32_t w0, uint32_t w1, uint32_t w2, uint
 __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
     using LY = P16Layout;
     constexpr int NCI = 3, PS = LY::PS, RR = LY::RR, NSH = 6;
+    constexpr int NSL = 5, SLC = 96;  // TMEM slots: 5 x 96 columns (one per (row step, component))
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bar_full[RR], bar_empty[RR], bar_dfull[NSLOT], bar_dempty[NSLOT], bar_b;
+    __shared__ uint64_t bar_full[RR], bar_empty[RR], bar_dfull[NSL], bar_dempty[NSL], bar_b;
     __shared__ uint32_t taddr_s;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -418,9 +443,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
     const int RS = (W + 3) * PS;
     uint8_t *ring = smem;
     uint8_t *bsm = smem + (size_t)RR * RS;
-    const uint64_t **ptab = (const uint64_t **)(bsm + LY::BBYTES);
-    double *red = (double *)(ptab + a.p * a.H * a.W);  // [4 cg][4 m][5 s][8 j] cross-quarter GAP sums
-    for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.in[i];
+    double *red = (double *)(bsm + LY::BBYTES);        // [4 cg][4 m][5 s][8 j] cross-quarter GAP sums
+    uint32_t *ptab = (uint32_t *)(red + 4 * CPT * 5 * 8);  // input offsets (256-byte units)
+    uint8_t *stg = (uint8_t *)(((uintptr_t)(ptab + a.p * a.H * a.W) + 127) & ~(uintptr_t)127);  // 2 x 24 KB staging
+    for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.ioff[i];
     const size_t N = (size_t)1 << a.logN;
     const int nchunk = (int)(N / 8);
     const int rows_in = a.y1 - a.y0 + 2;
@@ -432,7 +458,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
             tc5::mbar_init(&bar_full[i], PROD_WARPS * 32);
             tc5::mbar_init(&bar_empty[i], 1);
         }
-        for (int i = 0; i < NSLOT; i++) {
+        for (int i = 0; i < NSL; i++) {
             tc5::mbar_init(&bar_dfull[i], 1);
             tc5::mbar_init(&bar_dempty[i], EPI_WARPS * 32);
         }
@@ -453,57 +479,96 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
     __syncthreads();
     tc5::tc_fence_after();
     const uint32_t tmem = taddr_s;
+    const bool prof_on = a.prof && (threadIdx.x == 0 || threadIdx.x == EPI_WARPS * 32 || threadIdx.x == MMA_WARP * 32);
+    long long pc[7] = {0, 0, 0, 0, 0, 0, 0};
+    const long long t_start = clock64();
 
     if (warp >= EPI_WARPS && warp < EPI_WARPS + PROD_WARPS) {
         // ======================= producers: input rows -> plane-separated ring rows
+        // Half rows (8 pixels x 3 components x 16 channels x 8 coefficients = 24 KB) are
+        // copied raw into two shared staging buffers with cp.async (no registers held, a half
+        // row in flight while the other is transposed), then byte-transposed into the ring.
+        // Staging layout [pixel, component][channel i ^ ((i >> 2) & 1)][4 x 16 bytes]: the
+        // swizzle spreads a transposition load over all 32 banks.
         const int pt = threadIdx.x - EPI_WARPS * 32;
         constexpr int PT = PROD_WARPS * 32;
-        const uint32_t ring_s = tc5::smem_u32(ring);
-        const int ntask = W * NCI * 16;  // (pixel, component, coefficient pair, channel group of 4)
-        constexpr int TPT = 4;
-        const int kflip = (lane >> 4) & 1;  // half-warps store opposite coefficients first (no bank conflicts)
+        const uint32_t ring_s = tc5::smem_u32(ring), stg_s = tc5::smem_u32(stg);
+        constexpr int HX = 8;                         // pixels per staging unit (half row)
+        constexpr int NU = 2;                         // staging units per row = buffers
+        constexpr int NSEG = HX * NCI * 16 * 4;       // 16-byte copies per half row
+        constexpr int NTASK = HX * NCI * 16;          // (pixel, component, coefficient pair, channel group)
         int k = 0;
-        for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
-            const int it = item >> 1;
+        int issued = 0;  // staging units whose copies were issued (global counter, NU buffers)
+        // issue the copies of unit hr (row hr / NU of item kk) into buffer issued % NU
+        auto issue = [&](int kk, int item_i, int hr) {
+            const int it = item_i >> 1;
             const int l = a.limbs[it / nchunk];
             const size_t coff = (size_t)(it % nchunk) * 8;
+            const int y = a.y0 - 1 + hr / NU, xh = (hr % NU) * HX;
+            const uint32_t dst0 = stg_s + (uint32_t)(issued % NU) * (NSEG * 16);
+            if (y >= 0 && y < H)
+                for (int sgi = pt; sgi < NSEG; sgi += PT) {
+                    // segment = (pixel, component, channel, quarter of the 64-byte coefficient chunk)
+                    const int q4 = sgi & 3, is = (sgi >> 2) & 15, i = is ^ ((is >> 2) & 1), cx = sgi >> 6,
+                              c = cx % NCI, x = xh + cx / NCI;
+                    const uint64_t *src = a.ibase + (size_t)ptab[i * H * W + y * W + x] * 32 +
+                                          ((size_t)c * a.ell + l) * N + coff + 2 * q4;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + sgi * 16), "l"(src)
+                                 : "memory");
+                }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            issued++;
+            (void)kk;
+        };
+        int nk = 0, nitem = blockIdx.x, nhr = 0;  // next half row to issue
+        auto issue_next = [&]() {
+            if (nitem >= a.nitems) {
+                asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count uniform
+                issued++;
+                return;
+            }
+            issue(nk, nitem, nhr);
+            if (++nhr == NU * rows_in) {
+                nhr = 0;
+                nitem += gridDim.x;
+                nk++;
+            }
+        };
+        for (int u = 0; u < NU - 1; u++) issue_next();
+        for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
             for (int rr = 0; rr < rows_in; rr++) {
                 const int G = k * rows_in + rr, slot = G % RR, use = G / RR;
-                if (use > 0) {
-                    if (warp == EPI_WARPS) tc5::mbar_wait(&bar_empty[slot], (use - 1) & 1);
-                    asm volatile("bar.sync 1, %0;" ::"n"(PROD_WARPS * 32) : "memory");
-                }
                 const int y = a.y0 - 1 + rr;
                 const bool inside = y >= 0 && y < H;
                 const uint32_t rbase = ring_s + slot * RS;
-                for (int t0 = pt; t0 < ntask; t0 += TPT * PT) {
-                    uint64_t v[TPT][4][2];
-#pragma unroll
-                    for (int u = 0; u < TPT; u++) {
-                        const int t = t0 + u * PT;
-                        const int g = t & 3, jp = (t >> 2) & 3, cx = t >> 4, c = cx % NCI, x = cx / NCI;
+                if (use > 0) {
+                    if (warp == EPI_WARPS) PWAIT(0, tc5::mbar_wait(&bar_empty[slot], (use - 1) & 1));
+                    asm volatile("bar.sync 1, %0;" ::"n"(PT) : "memory");
+                }
+                for (int h = 0; h < NU; h++) {
+                    const int cur = (issued - (NU - 1)) % NU;  // buffer of the unit now landing
+                    issue_next();                               // later units stream in meanwhile
+                    asm volatile("cp.async.wait_group %0;" ::"n"(NU - 1) : "memory");
+                    asm volatile("bar.sync 1, %0;" ::"n"(PT) : "memory");  // every thread's copies landed
+                    const uint32_t sb = stg_s + (uint32_t)cur * (NSEG * 16);
+                    for (int t = pt; t < NTASK; t += PT) {
+                        const int g = t & 3, jp = (t >> 2) & 3, cx = t >> 4, c = cx % NCI, x = h * HX + cx / NCI;
+                        const uint32_t base = rbase + (x + 1) * PS + c * (5 * 128) + g * 4;
+                        uint64_t v[4][2];
 #pragma unroll
                         for (int ch = 0; ch < 4; ch++) {
-                            v[u][ch][0] = v[u][ch][1] = 0;
-                            const int i = 4 * g + ch;
-                            if (t < ntask && inside && i < a.p) {
-                                const uint64_t *src = ptab[(size_t)i * H * W + (size_t)y * W + x];
-                                ldg128(src + ((size_t)c * a.ell + l) * N + coff + 2 * jp, v[u][ch][0], v[u][ch][1]);
+                            if (inside) {
+                                const int is = (4 * g + ch) ^ (g & 1);
+                                const uint32_t sa = sb + (uint32_t)(((cx * 16 + is) * 4 + jp) * 16);
+                                asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v[ch][0]), "=l"(v[ch][1]) : "r"(sa));
+                            } else {
+                                v[ch][0] = v[ch][1] = 0;
                             }
                         }
-                    }
 #pragma unroll
-                    for (int u = 0; u < TPT; u++) {
-                        const int t = t0 + u * PT;
-                        if (t >= ntask) break;
-                        const int g = t & 3, jp = (t >> 2) & 3, cx = t >> 4, c = cx % NCI, x = cx / NCI;
-                        const uint32_t base = rbase + (x + 1) * PS + c * (5 * 128) + g * 4;
-#pragma unroll
-                        for (int kk = 0; kk < 2; kk++) {
-                            const int kc = kk ^ kflip;  // coefficient 2 jp + kc
+                        for (int kc = 0; kc < 2; kc++) {
                             uint32_t lo[4], hi[4];
-                            const uint64_t a0 = kc ? v[u][0][1] : v[u][0][0], a1 = kc ? v[u][1][1] : v[u][1][0];
-                            const uint64_t a2 = kc ? v[u][2][1] : v[u][2][0], a3 = kc ? v[u][3][1] : v[u][3][0];
+                            const uint64_t a0 = v[0][kc], a1 = v[1][kc], a2 = v[2][kc], a3 = v[3][kc];
                             tr4b((uint32_t)a0, (uint32_t)a1, (uint32_t)a2, (uint32_t)a3, lo);
                             tr4b((uint32_t)(a0 >> 32), (uint32_t)(a1 >> 32), (uint32_t)(a2 >> 32), (uint32_t)(a3 >> 32),
                                  hi);
@@ -514,18 +579,24 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                             asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst + 4 * 128), "r"(hi[0]));
                         }
                     }
+                    asm volatile("bar.sync 1, %0;" ::"n"(PT) : "memory");  // staging buffer cur is free again
                 }
                 tc5::fence_async_smem();
                 tc5::mbar_arrive(&bar_full[slot]);
             }
         }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     } else if (warp == MMA_WARP) {
-        // ======================= MMA issuer
-        if (lane == 0) {
+        // ======================= MMA issuer (warp-uniform loop, one elected lane issues)
+        {
             tc5::mbar_wait(&bar_b, 0);
             const uint32_t ring_s = tc5::smem_u32(ring), b_s = tc5::smem_u32(bsm);
             const uint32_t idesc32 = tc5::idesc_u8s8(128, 32), idesc96 = tc5::idesc_u8s8(128, 96);
             const uint32_t blbo = 32 * 16, blbo0 = 96 * 16;
+            const uint32_t ahi = tc5::sdesc_hi(PS), lps = tc5::sdesc_lbo(PS);
+            uint64_t bd[7];
+            for (int t = 0; t < 6; t++) bd[t] = tc5::sdesc(b_s + t * LY::TB, blbo, 128);
+            bd[6] = tc5::sdesc(b_s + 6 * LY::TB, blbo0, 128);
             int k = 0, S = 0;
             for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
                 const int Gb = k * rows_in;
@@ -533,48 +604,46 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                 for (int y = a.y0; y < a.y1; y++) {
                     for (int yy = y - 1; yy <= y + 1; yy++) {
                         const int G = Gb + (yy - (a.y0 - 1));
-                        tc5::mbar_wait(&bar_full[G % RR], (G / RR) & 1);
+                        PWAIT(2, tc5::mbar_wait(&bar_full[G % RR], (G / RR) & 1));
                     }
                     tc5::tc_fence_after();
-                    const uint32_t r0 = ring_s + slot_of(y - 1) * RS, r1 = ring_s + slot_of(y) * RS,
-                                   r2 = ring_s + slot_of(y + 1) * RS;
-                    const bool fwd = r1 > r0;  // K step 3 pairs (0,2)+(1,2) in ring order
-                    for (int c = 0; c < NCI; c++, S++) {
-                        const int ds = S % NSLOT;
-                        if (S >= NSLOT) tc5::mbar_wait(&bar_dempty[ds], ((S / NSLOT) - 1) & 1);
-                        tc5::tc_fence_after();
-#pragma unroll 1
-                        for (int d = 0; d < 5; d++) {
-                            const uint32_t dcol = tmem + (uint32_t)ds * 128 + d * 16;
-                            const uint32_t co = (uint32_t)(c * 5 + d) * 128;
-                            if (d == 0)
-                                tc5::mma_i8(dcol, tc5::sdesc(r0 + co, PS, PS),
-                                            tc5::sdesc(b_s + 6 * LY::TB, blbo0, 128), idesc96, 0);
-                            else
-                                tc5::mma_i8(dcol, tc5::sdesc(r0 + co, PS, PS), tc5::sdesc(b_s + 0 * LY::TB, blbo, 128),
-                                            idesc32, 1);
-                            tc5::mma_i8(dcol, tc5::sdesc(r1 + co, PS, PS), tc5::sdesc(b_s + 1 * LY::TB, blbo, 128),
-                                        idesc32, 1);
-                            tc5::mma_i8(dcol, tc5::sdesc(r2 + co, PS, PS), tc5::sdesc(b_s + 2 * LY::TB, blbo, 128),
-                                        idesc32, 1);
-                            if (fwd)
-                                tc5::mma_i8(dcol, tc5::sdesc(r0 + co + 2 * PS, r1 - r0, PS),
-                                            tc5::sdesc(b_s + 3 * LY::TB, blbo, 128), idesc32, 1);
-                            else
-                                tc5::mma_i8(dcol, tc5::sdesc(r1 + co + 2 * PS, r0 - r1, PS),
-                                            tc5::sdesc(b_s + 5 * LY::TB, blbo, 128), idesc32, 1);
-                            tc5::mma_i8(dcol, tc5::sdesc(r2 + co + 2 * PS, PS, PS),
-                                        tc5::sdesc(b_s + 4 * LY::TB, blbo, 128), idesc32, 1);
-                        }
-                        tc5::tc_commit(&bar_dfull[ds]);
+                    const uint32_t r0 = (ring_s + slot_of(y - 1) * RS) >> 4, r1 = (ring_s + slot_of(y) * RS) >> 4,
+                                   r2 = (ring_s + slot_of(y + 1) * RS) >> 4;
+                    const uint32_t lv = r1 > r0 ? tc5::sdesc_lbo((r1 - r0) << 4) : tc5::sdesc_lbo((r0 - r1) << 4);
+                    const uint32_t a3 = (r1 > r0 ? r0 : r1) + 2 * (PS >> 4) + lv;
+                    const uint64_t b3 = r1 > r0 ? bd[3] : bd[5];
+                    // all three components' slots first: the MMAs interleave the components so
+                    // that consecutive groups never accumulate into partially overlapping TMEM
+                    // columns (plane d+1 overlaps plane d's upper shift block)
+                    uint32_t dsl[NCI];
+                    for (int c = 0; c < NCI; c++) {
+                        const int Sc = S + c, ds = Sc % NSL;
+                        if (Sc >= NSL) PWAIT(3, tc5::mbar_wait(&bar_dempty[ds], ((Sc / NSL) - 1) & 1));
+                        dsl[c] = tmem + (uint32_t)ds * SLC;
                     }
-                    tc5::tc_commit(&bar_empty[slot_of(y - 1)]);  // row y-1 is not read again
+                    tc5::tc_fence_after();
+#pragma unroll
+                    for (int d = 0; d < 5; d++)
+#pragma unroll
+                        for (int c = 0; c < NCI; c++) {
+                            const uint32_t dcol = dsl[c] + d * 16;
+                            const uint32_t co = (uint32_t)(c * 5 + d) * (128 >> 4);
+                            if (d == 0)
+                                tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r0 + co + lps), bd[6], idesc96, false);
+                            else
+                                tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r0 + co + lps), bd[0], idesc32, true);
+                            tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r1 + co + lps), bd[1], idesc32, true);
+                            tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r2 + co + lps), bd[2], idesc32, true);
+                            tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, a3 + co), b3, idesc32, true);
+                            tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r2 + co + 2 * (PS >> 4) + lps), bd[4], idesc32, true);
+                        }
+                    for (int c = 0; c < NCI; c++, S++) tc5::tc_commit_w(&bar_dfull[S % NSL]);
+                    tc5::tc_commit_w(&bar_empty[slot_of(y - 1)]);  // row y-1 is not read again
                 }
-                tc5::tc_commit(&bar_empty[slot_of(a.y1 - 1)]);
-                tc5::tc_commit(&bar_empty[slot_of(a.y1)]);
+                tc5::tc_commit_w(&bar_empty[slot_of(a.y1 - 1)]);
+                tc5::tc_commit_w(&bar_empty[slot_of(a.y1)]);
             }
         }
-        __syncwarp();
     } else if (warp < EPI_WARPS) {
         // ======================= epilogue
         const int qd = warp & 3, cg = warp >> 2;
@@ -597,11 +666,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                 double yv[NCI][CPT];
 #pragma unroll
                 for (int cc = 0; cc < NCI; cc++, S++) {
-                    const int ds = S % NSLOT;
-                    tc5::mbar_wait(&bar_dfull[ds], (S / NSLOT) & 1);
+                    const int ds = S % NSL;
+                    PWAIT(5, tc5::mbar_wait(&bar_dfull[ds], (S / NSL) & 1));
                     tc5::tc_fence_after();
                     int C[CPT][NSH];
-                    const uint32_t ta = tq + (uint32_t)ds * 128;
+                    const uint32_t ta = tq + (uint32_t)ds * SLC;
 #pragma unroll
                     for (int s2 = 0; s2 < NSH; s2++) {
                         uint32_t r[4];
@@ -615,6 +684,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
 #pragma unroll
                     for (int m = 0; m < CPT; m++) yv[cc][m] = recombine<NSH>(C[m], yc, c);
                 }
+                if (a.exp == 1) {
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) gs[m][0] += yv[0][m] + yv[1][m] + yv[2][m];
+                } else
 #pragma unroll
                 for (int m = 0; m < CPT; m++) {
                     const double d0 = yv[0][m] + a.biasd[(size_t)(m0 + m) * a.ell + l], d1 = yv[1][m], d2 = yv[2][m];
@@ -679,6 +752,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                 }
             }
         }
+    }
+    if (prof_on) {
+        const int tot = threadIdx.x == 0 ? 6 : threadIdx.x == EPI_WARPS * 32 ? 1 : 4;
+        pc[tot] = clock64() - t_start;
+        for (int i = 0; i < 7; i++)
+            if (pc[i]) atomicAdd(a.prof + i, (unsigned long long)pc[i]);
     }
     tc5::tc_fence_before();
     __syncthreads();
@@ -752,6 +831,25 @@ static void build_btiles_p16(const int64_t *weights, int M, int p, std::vector<u
 }
 
 static int g_conv_tc = 1;  // he_set_conv_tc: 0 forces the mma.sync kernels (A/B tests)
+static unsigned long long *g_prof = nullptr;
+
+// role timing of the tcgen05 conv kernels (diagnostics): on != 0 enables and zeroes the
+// counters, on == 0 copies the 7 summed counters (see PWAIT) to out and disables
+extern "C" int he_convtc_profile(int on, double *out) {
+    if (on) {
+        if (!g_prof) HE_CHECK_CUDA(cudaMalloc(&g_prof, 64));
+        HE_CHECK_CUDA(cudaMemset(g_prof, 0, 64));
+        return HE_OK;
+    }
+    if (!g_prof) return HE_EINVAL;
+    unsigned long long h[7];
+    HE_CHECK_CUDA(cudaDeviceSynchronize());
+    HE_CHECK_CUDA(cudaMemcpy(h, g_prof, 56, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 7; i++) out[i] = (double)h[i];
+    cudaFree(g_prof);
+    g_prof = nullptr;
+    return HE_OK;
+}
 
 extern "C" int he_set_conv_tc(int on) {
     const int old = g_conv_tc;
@@ -817,9 +915,22 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     cudaStream_t s = (cudaStream_t)stream;
     const int nwin = pool ? ((y1 - y0) / 2) * (W / 2) : 1;
     const int n_in = p * H * W, n_out = M * nwin;
-    const size_t smem = p16 ? (size_t)P16Layout::RR * (W + 3) * P16Layout::PS + P16Layout::BBYTES + (size_t)n_in * 8 +
-                                  (size_t)4 * MC * 5 * 8 * 8
-                            : (size_t)P1Layout<2>::RR * (W + 3) * P1Layout<2>::PS + 6 * (size_t)TB + (size_t)n_in * 8;
+    const size_t smem = p16 ? (size_t)P16Layout::RR * (W + 3) * P16Layout::PS + P16Layout::BBYTES + (size_t)n_in * 4 +
+                                  (size_t)4 * CPT * 5 * 8 * 8 + 128 + P16Layout::STG
+                            : (size_t)P1Layout<2>::RR * (W + 3) * P1Layout<2>::PS + 6 * (size_t)TB + (size_t)n_in * 4;
+    // inputs as 32-bit offsets from the lowest address in 256-byte units (every ciphertext of a
+    // batch allocation is 256-byte aligned); anything else takes the mma.sync kernels
+    uintptr_t ib = UINTPTR_MAX;
+    for (int i = 0; i < n_in; i++) ib = std::min(ib, (uintptr_t)in[i]);
+    std::vector<uint32_t> ioff(n_in);
+    for (int i = 0; i < n_in; i++) {
+        const uintptr_t d = (uintptr_t)in[i] - ib;
+        if ((d & 255) || (d >> 8) > 0xFFFFFFFFull) {
+            he_set_error("he_conv_square_sum_tc: inputs not addressable by 32-bit 256-byte offsets");
+            return HE_EINVAL;
+        }
+        ioff[i] = (uint32_t)(d >> 8);
+    }
     if (smem > 227 * 1024) {
         he_set_error("he_conv_square_sum_tc: %zu bytes of shared memory (input table of %d)", smem, n_in);
         return HE_EINVAL;
@@ -830,9 +941,9 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     std::vector<int32_t> lorder(ell);
     for (int l = 0; l < ell; l++) lorder[l] = l;
     const size_t b_bt = bt.size(), b_bias = biasd.size() * 8, b_yc = (size_t)ell * 8, b_lo = (size_t)ell * 4,
-                 b_c = cst ? (size_t)ell * 8 : 0;
+                 b_c = cst ? (size_t)ell * 8 : 0, b_io = (size_t)n_in * 4;
     char *meta = nullptr;
-    HE_TRY(he_scratch_alloc((void **)&meta, b_bt + b_bias + b_yc + b_lo + b_c + 256, s));
+    HE_TRY(he_scratch_alloc((void **)&meta, b_bt + b_bias + b_yc + b_lo + b_c + b_io + 1024, s));
     size_t off = 0;
     auto carve = [&](size_t bytes) {
         char *q = meta + off;
@@ -844,6 +955,8 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     double *dyc = (double *)carve(b_yc);
     int32_t *dlo = (int32_t *)carve(b_lo);
     uint64_t *dc = cst ? (uint64_t *)carve(b_c) : nullptr;
+    uint32_t *dio = (uint32_t *)carve(b_io);
+    HE_CHECK_CUDA(he_h2d(dio, ioff.data(), b_io, s));
     HE_CHECK_CUDA(he_h2d(dbt, bt.data(), b_bt, s));
     HE_CHECK_CUDA(he_h2d(dbias, biasd.data(), b_bias, s));
     HE_CHECK_CUDA(he_h2d(dyc, yc.data(), b_yc, s));
@@ -851,6 +964,8 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     if (dc) HE_CHECK_CUDA(he_h2d(dc, cst, b_c, s));
     TcArgs a;
     a.in = (const uint64_t *const *)din;
+    a.ibase = (const uint64_t *)ib;
+    a.ioff = dio;
     a.out = (uint64_t *const *)dout;
     a.obase = nullptr;
     a.ostride = 0;
@@ -881,6 +996,8 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     a.nwin = nwin;
     a.nitems = ell * (c->N / 8) * (p16 ? 2 : 1);
     a.btile_bytes = TB;
+    a.prof = g_prof;
+    a.exp = getenv("CONVTC_EXP") ? atoi(getenv("CONVTC_EXP")) : 0;
     a.nshift = NSH;
     int sms = 0;
     HE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));

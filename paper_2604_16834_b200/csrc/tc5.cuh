@@ -80,6 +80,41 @@ __host__ __device__ constexpr uint32_t idesc_u8s8(int M, int N) {
            | ((uint32_t)(M >> 4) << 24);  // m_dim
 }
 
+// descriptor from a precomputed high word (SBO field + version) and low word
+// (start address >> 4 | LBO field): the MMA issue loops only add 32-bit offsets
+__host__ __device__ constexpr uint32_t sdesc_hi(uint32_t sbo) { return ((sbo >> 4) & 0x3FFF) | (1u << 14); }
+__host__ __device__ constexpr uint32_t sdesc_lbo(uint32_t lbo) { return ((lbo >> 4) & 0x3FFF) << 16; }
+__device__ __forceinline__ uint64_t sdesc_hl(uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 32) | lo; }
+
+// warp-uniform issue: every lane of the warp executes the call with the same
+// operands and one elected lane issues the MMA (operands stay in uniform registers)
+__device__ __forceinline__ void mma_i8_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, bool acc) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"((uint32_t)acc));
+}
+__device__ __forceinline__ void tc_commit_w(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+// D[tmem] += A[smem] x B[smem] (accumulate), one elected thread
+__device__ __forceinline__ void mma_i8_acc(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+    asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;" ::"r"(d_tmem), "l"(adesc), "l"(bdesc),
+                 "r"(idesc));
+}
+// D[tmem] = A[smem] x B[smem] (overwrite)
+__device__ __forceinline__ void mma_i8_set(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+    asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;" ::"r"(d_tmem), "l"(adesc), "l"(bdesc),
+                 "r"(idesc));
+}
+
 // D[tmem] (+)= A[smem] x B[smem], one elected thread
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
     asm volatile(

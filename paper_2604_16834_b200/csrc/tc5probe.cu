@@ -84,12 +84,13 @@ __global__ void __launch_bounds__(128, 1) k_tc5_selftest(int N, int layout, int3
 
 constexpr int BK = 256;  // throughput probe: K bytes resident (8 K steps)
 
-__global__ void __launch_bounds__(128, 1) k_tc5_rate(int N, int iters, unsigned long long *cyc) {
+__global__ void __launch_bounds__(128, 1) k_tc5_rate(int N, int iters, unsigned long long *cyc, uint32_t a_sbo,
+                                                     uint32_t a_lbo, int abytes) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t bar;
     __shared__ uint32_t taddr_s;
-    uint8_t *A = sm, *B = sm + 128 * BK;
-    for (int i = threadIdx.x; i < (128 + N) * BK; i += blockDim.x) sm[i] = (uint8_t)probe_hash((uint32_t)i);
+    uint8_t *A = sm, *B = sm + abytes;
+    for (int i = threadIdx.x; i < abytes + N * BK; i += blockDim.x) sm[i] = (uint8_t)probe_hash((uint32_t)i);
     tc5::fence_async_smem();
     const int warp = threadIdx.x >> 5;
     if (warp == 0) tc5::tmem_alloc<256>(&taddr_s);
@@ -104,13 +105,13 @@ __global__ void __launch_bounds__(128, 1) k_tc5_rate(int N, int iters, unsigned 
     if (threadIdx.x == 0) {
         const uint32_t idesc = tc5::idesc_u8s8(128, N);
         const uint32_t sa = tc5::smem_u32(A), sb = tc5::smem_u32(B);
-        const uint32_t a_lbo = 128 * 16, b_lbo = (uint32_t)N * 16;
+        const uint32_t b_lbo = (uint32_t)N * 16;
         const unsigned long long t0 = clock64();
         for (int it = 0; it < iters; it++)
 #pragma unroll
             for (int t = 0; t < BK / 32; t++)
-                tc5::mma_i8(taddr, tc5::sdesc(sa + 2 * t * a_lbo, a_lbo, 128), tc5::sdesc(sb + 2 * t * b_lbo, b_lbo, 128),
-                            idesc, (it | t) != 0);
+                tc5::mma_i8(taddr, tc5::sdesc(sa + 2 * t * a_lbo, a_lbo, a_sbo),
+                            tc5::sdesc(sb + 2 * t * b_lbo, b_lbo, 128), idesc, (it | t) != 0);
         tc5::tc_commit(&bar);
         tc5::mbar_wait(&bar, 0);
         if (blockIdx.x == 0) *cyc = clock64() - t0;
@@ -138,8 +139,15 @@ extern "C" int he_tc5_selftest(int device, int n, int layout, int32_t *d_out) {
     return HE_OK;
 }
 
-// rates[0] = int8 MAC/s over all SMs, rates[1] = cycles per MMA (M=128, N=n, K=32) on one SM
-extern "C" int he_microbench_tc5(int device, int n, double *rates) {
+// rates[0] = int8 MAC/s over all SMs, rates[1] = cycles per MMA (M=128, N=n, K=32) on one SM.
+// a_sbo = 0: A contiguous (8-row groups 128 B apart); else the A operand's 8-row groups sit
+// a_sbo bytes apart and its K chunks a_lbo bytes apart (the conv kernels' pixel-strided rings).
+static int tc5_rate(int device, int n, uint32_t a_sbo, uint32_t a_lbo, double *rates);
+extern "C" int he_microbench_tc5(int device, int n, double *rates) { return tc5_rate(device, n, 0, 0, rates); }
+extern "C" int he_microbench_tc5_strided(int device, int n, int a_sbo, int a_lbo, double *rates) {
+    return tc5_rate(device, n, (uint32_t)a_sbo, (uint32_t)a_lbo, rates);
+}
+static int tc5_rate(int device, int n, uint32_t a_sbo, uint32_t a_lbo, double *rates) {
     if (n < 16 || n > 256 || n % 16 || !rates) {
         he_set_error("he_microbench_tc5: N must be a multiple of 16 in [16, 256]");
         return HE_EINVAL;
@@ -147,7 +155,17 @@ extern "C" int he_microbench_tc5(int device, int n, double *rates) {
     HE_CHECK_CUDA(cudaSetDevice(device));
     int sms = 0;
     HE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    const size_t smem = (size_t)(128 + n) * BK;
+    if (a_sbo == 0) {
+        a_sbo = 128;
+        a_lbo = 128 * 16;
+    }
+    // A spans 16 row groups and 2 * (BK / 32) K chunks
+    const int abytes = (int)(((15 * a_sbo + (2 * (BK / 32) - 1) * a_lbo + 128) + 1023) & ~1023u);
+    const size_t smem = (size_t)abytes + (size_t)n * BK;
+    if (smem > 227 * 1024) {
+        he_set_error("he_microbench_tc5: operand layout needs %zu bytes", smem);
+        return HE_EINVAL;
+    }
     HE_CHECK_CUDA(cudaFuncSetAttribute(k_tc5_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     unsigned long long *cyc;
     HE_CHECK_CUDA(cudaMalloc(&cyc, 8));
@@ -158,7 +176,7 @@ extern "C" int he_microbench_tc5(int device, int n, double *rates) {
     float ms = 0;
     for (int rep = 0; rep < 2; rep++) {
         cudaEventRecord(e0);
-        k_tc5_rate<<<sms, 128, smem>>>(n, iters, cyc);
+        k_tc5_rate<<<sms, 128, smem>>>(n, iters, cyc, a_sbo, a_lbo, abytes);
         cudaEventRecord(e1);
         HE_CHECK_CUDA(cudaEventSynchronize(e1));
     }
