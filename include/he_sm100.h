@@ -278,6 +278,23 @@ int he_set_conv_tc(int on);
  * wait-empty, producer total, MMA wait-full, MMA wait-dempty, MMA total,
  * epilogue wait-dfull, epilogue total; one sampled thread per role per CTA). */
 int he_convtc_profile(int on, double *out);
+/* Planar carry between the two fused convs of the config-3 plan: C <= 16
+ * channels x H x W of 3-component ciphertexts on ell limbs of < 2^40 primes,
+ * laid out [limb][N/8 coefficient chunks][y][x][component][byte plane 0..4]
+ * [8 coefficients][16 channels] (one byte per residue byte): the conv2 kernel's
+ * shared-memory ring layout, so one image row is one contiguous bulk copy, and
+ * 5 bytes per residue instead of 8.  he_conv_square_sum_pl = he_conv_square_sum_tc
+ * with the inputs read from pl_in (conv2 shape: p = 16, W = 16, GAP) or the
+ * pooled outputs written to pl_out (conv1 shape, M = 16) instead of the
+ * pointer lists.  he_planar_pack / he_planar_unpack convert C*H*W ciphertexts
+ * (channel-major) to / from the layout (pl holds ell * N/8 * H * W * 1920 bytes). */
+int he_conv_square_sum_pl(he_ctx *ctx, const uint64_t *const *in, int nci, int p, int H, int W,
+                          uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
+                          const uint64_t *bias, const uint64_t *cst, int ell, const void *pl_in, void *pl_out,
+                          void *stream);
+int he_planar_pack(he_ctx *ctx, const uint64_t *const *in, int C, int H, int W, int ell, void *pl, void *stream);
+int he_planar_unpack(he_ctx *ctx, const void *pl, int C, int H, int W, int ell, uint64_t *const *out,
+                     void *stream);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,9 @@ EXPORTS = [
     "he_conv_square_sum_tc",
     "he_set_conv_tc",
     "he_convtc_profile",
+    "he_conv_square_sum_pl",
+    "he_planar_pack",
+    "he_planar_unpack",
     "he_rotate_hoisted",
     "he_gen_hoist_key",
 ]
@@ -125,6 +128,9 @@ def load():
         "he_conv_square_sum_tc": (i, [vp, vp, i, i, i, i, vp, i, i, i, i, vp, vp, vp, i, vp]),
         "he_set_conv_tc": (i, [i]),
         "he_convtc_profile": (i, [i, vp]),
+        "he_conv_square_sum_pl": (i, [vp, vp, i, i, i, i, vp, i, i, i, i, vp, vp, vp, i, vp, vp, vp]),
+        "he_planar_pack": (i, [vp, vp, i, i, i, i, vp, vp]),
+        "he_planar_unpack": (i, [vp, vp, i, i, i, i, vp, vp]),
         "he_rotate_hoisted": (i, [vp, vp, i, pp, pp, i, i, vp]),
         "he_gen_hoist_key": (i, [vp, u32, vp]),
         "he_square_sum": (i, [vp, pp, i, pp, i, vp, vp, vp, i, vp]),

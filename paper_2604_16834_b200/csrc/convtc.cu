@@ -67,6 +67,11 @@ struct TcArgs {
     int btile_bytes, nshift;     // bytes per B tile, shift sums (N = nshift * 16)
     unsigned long long *prof;    // != nullptr: per-role cycle counters (he_convtc_profile)
     int exp;                     // diagnostics (CONVTC_EXP): 1 = epilogue skips the products
+    // planar carry (conv1 -> conv2 of the config-3 plan): layout [limb][N/8 coefficient chunks]
+    // [y][x][component][byte plane][8 coefficients x 16 channels] -- conv2's ring row layout, so
+    // one input row of one (limb, chunk) is a contiguous (W x 1920)-byte block
+    uint8_t *pl_out;             // P1: pooled outputs written planar (16 channels, H/2 x W/2)
+    const uint8_t *pl_in;        // P16: inputs read planar (p = 16 channels, H x W)
 };
 
 // role timing (he_convtc_profile): [0] producer wait-empty, [1] producer total, [2] MMA wait-full,
@@ -366,6 +371,30 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                     // of the cross term are folded into the exact FP64 sums (|sum| < 2^50).
                     const int x = xb * 16 + xl;
                     const int win = pr * (W / 2) + x / 2;
+                    if (a.pl_out) {  // planar carry: 5 byte planes, channels (2 par + h) as 16-bit pairs
+                        uint64_t v[2][3];
+#pragma unroll
+                        for (int h = 0; h < 2; h++)
+#pragma unroll
+                            for (int s2 = 0; s2 < 3; s2++) {
+                                const double mine = par ? acc[2 + h][s2] : acc[h][s2];
+                                const double give = par ? acc[h][s2] : acc[2 + h][s2];
+                                const double keep = mine + __shfl_xor_sync(0xffffffffu, give, 8);
+                                v[h][s2] = canon_fast(s2 == 0 ? keep + cstd : s2 == 1 ? 2.0 * keep : keep, c.qd, c.qid);
+                            }
+                        const int H2 = a.H >> 1, W2 = W >> 1, y2 = (a.y0 >> 1) + pr, x2 = x >> 1;
+                        uint8_t *pb = a.pl_out +
+                                      ((((size_t)l * nchunk + (size_t)(item % nchunk)) * H2 + y2) * W2 + x2) * (3 * 5 * 128) +
+                                      j * 16 + cg * CPT + 2 * par;
+#pragma unroll
+                        for (int s2 = 0; s2 < 3; s2++)
+#pragma unroll
+                            for (int d = 0; d < 5; d++) {
+                                const unsigned short u = (unsigned short)(((v[0][s2] >> (8 * d)) & 0xFF) |
+                                                                          (((v[1][s2] >> (8 * d)) & 0xFF) << 8));
+                                *(unsigned short *)(pb + (s2 * 5 + d) * 128) = u;
+                            }
+                    } else
 #pragma unroll
                     for (int h = 0; h < 2; h++) {
                         double keep[3];
@@ -446,7 +475,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
     double *red = (double *)(bsm + LY::BBYTES);        // [4 cg][4 m][5 s][8 j] cross-quarter GAP sums
     uint32_t *ptab = (uint32_t *)(red + 4 * CPT * 5 * 8);  // input offsets (256-byte units)
     uint8_t *stg = (uint8_t *)(((uintptr_t)(ptab + a.p * a.H * a.W) + 127) & ~(uintptr_t)127);  // 2 x 24 KB staging
-    for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.ioff[i];
+    if (!a.pl_in)
+        for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.ioff[i];
     const size_t N = (size_t)1 << a.logN;
     const int nchunk = (int)(N / 8);
     const int rows_in = a.y1 - a.y0 + 2;
@@ -455,7 +485,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < RR; i++) {
-            tc5::mbar_init(&bar_full[i], PROD_WARPS * 32);
+            tc5::mbar_init(&bar_full[i], a.pl_in ? 1 : PROD_WARPS * 32);
             tc5::mbar_init(&bar_empty[i], 1);
         }
         for (int i = 0; i < NSL; i++) {
@@ -520,6 +550,42 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
             issued++;
             (void)kk;
         };
+        if (a.pl_in) {
+            // planar carry: one bulk copy (TMA engine) per input row into pixel slots 1..W
+            const uint32_t rowb = (uint32_t)W * PS;
+            for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
+                const int it = item >> 1;
+                const int l = a.limbs[it / nchunk];
+                const size_t chunk = (size_t)(it % nchunk);
+                for (int rr = 0; rr < rows_in; rr++) {
+                    const int G = k * rows_in + rr, slot = G % RR, use = G / RR;
+                    const int y = a.y0 - 1 + rr;
+                    const bool inside = y >= 0 && y < H;
+                    if (use > 0) {
+                        if (warp == EPI_WARPS) PWAIT(0, tc5::mbar_wait(&bar_empty[slot], (use - 1) & 1));
+                        asm volatile("bar.sync 1, %0;" ::"n"(PT) : "memory");
+                    }
+                    if (inside) {
+                        if (pt == 0) {
+                            tc5::mbar_arrive_expect_tx(&bar_full[slot], rowb);
+                            const uint8_t *src = a.pl_in + (((size_t)l * nchunk + chunk) * H + y) * rowb;
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                    ring_s + slot * RS + PS),
+                                "l"(src), "r"(rowb), "r"(tc5::smem_u32(&bar_full[slot]))
+                                : "memory");
+                        }
+                    } else {  // zero padding row
+                        for (uint32_t o = (uint32_t)pt * 16; o < rowb; o += PT * 16)
+                            asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ring_s + slot * RS + PS + o),
+                                         "r"(0u));
+                        tc5::fence_async_smem();
+                        asm volatile("bar.sync 1, %0;" ::"n"(PT) : "memory");
+                        if (pt == 0) tc5::mbar_arrive(&bar_full[slot]);
+                    }
+                }
+            }
+        } else {
         int nk = 0, nitem = blockIdx.x, nhr = 0;  // next half row to issue
         auto issue_next = [&]() {
             if (nitem >= a.nitems) {
@@ -586,6 +652,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
             }
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
     } else if (warp == MMA_WARP) {
         // ======================= MMA issuer (warp-uniform loop, one elected lane issues)
         {
@@ -858,15 +925,21 @@ extern "C" int he_set_conv_tc(int on) {
 }
 
 // Eligibility + launch of the tcgen05 path; HE_EINVAL (no work enqueued) when the shape is not covered.
-extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int nci, int p, int H, int W,
-                                     uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
-                                     const uint64_t *bias, const uint64_t *cst, int ell, void *stream) {
-    if (!c || !in || !out || !weights || ell < 1 || ell > c->L || y0 < 0 || y1 > H || y0 >= y1) {
+// pl_in / pl_out: planar carry input (P16) / output (P1) instead of ciphertext pointer lists.
+static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, int H, int W, uint64_t *const *out,
+                         int M, int pool, int y0, int y1, const int64_t *weights, const uint64_t *bias,
+                         const uint64_t *cst, int ell, const uint8_t *pl_in, uint8_t *pl_out, void *stream) {
+    if (!c || (!in && !pl_in) || (!out && !pl_out) || !weights || ell < 1 || ell > c->L || y0 < 0 || y1 > H ||
+        y0 >= y1) {
         he_set_error("he_conv_square_sum_tc: bad arguments");
         return HE_EINVAL;
     }
     const bool p1 = nci == 2 && p <= 3 && pool && M <= MC && W % 16 == 0 && W <= 64 && !((y0 | y1 | H) & 1);
     const bool p16 = nci == 3 && p == 16 && !pool && M <= 2 * MC && W == 16;
+    if ((pl_in && !p16) || (pl_out && !(p1 && M == MC))) {
+        he_set_error("he_conv_square_sum_pl: planar carry needs the conv2 shape (input) / 16 pooled channels (output)");
+        return HE_EINVAL;
+    }
     if (!p1 && !p16) {
         he_set_error("he_conv_square_sum_tc: shape (nci=%d p=%d M=%d W=%d pool=%d) not covered", nci, p, M, W, pool);
         return HE_EINVAL;
@@ -915,15 +988,15 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     cudaStream_t s = (cudaStream_t)stream;
     const int nwin = pool ? ((y1 - y0) / 2) * (W / 2) : 1;
     const int n_in = p * H * W, n_out = M * nwin;
-    const size_t smem = p16 ? (size_t)P16Layout::RR * (W + 3) * P16Layout::PS + P16Layout::BBYTES + (size_t)n_in * 4 +
-                                  (size_t)4 * CPT * 5 * 8 * 8 + 128 + P16Layout::STG
+    const size_t smem = p16 ? (size_t)P16Layout::RR * (W + 3) * P16Layout::PS + P16Layout::BBYTES +
+                                  (pl_in ? 0 : (size_t)n_in * 4 + 128 + P16Layout::STG) + (size_t)4 * CPT * 5 * 8 * 8
                             : (size_t)P1Layout<2>::RR * (W + 3) * P1Layout<2>::PS + 6 * (size_t)TB + (size_t)n_in * 4;
     // inputs as 32-bit offsets from the lowest address in 256-byte units (every ciphertext of a
     // batch allocation is 256-byte aligned); anything else takes the mma.sync kernels
     uintptr_t ib = UINTPTR_MAX;
-    for (int i = 0; i < n_in; i++) ib = std::min(ib, (uintptr_t)in[i]);
-    std::vector<uint32_t> ioff(n_in);
-    for (int i = 0; i < n_in; i++) {
+    for (int i = 0; i < n_in && in; i++) ib = std::min(ib, (uintptr_t)in[i]);
+    std::vector<uint32_t> ioff(in ? n_in : 0);
+    for (int i = 0; i < n_in && in; i++) {
         const uintptr_t d = (uintptr_t)in[i] - ib;
         if ((d & 255) || (d >> 8) > 0xFFFFFFFFull) {
             he_set_error("he_conv_square_sum_tc: inputs not addressable by 32-bit 256-byte offsets");
@@ -936,12 +1009,12 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
         return HE_EINVAL;
     }
     void **din = nullptr, **dout = nullptr;
-    HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
-    HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
+    if (in) HE_TRY(he_upload_ptrs((const void *const *)in, n_in, &din, s));
+    if (out) HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
     std::vector<int32_t> lorder(ell);
     for (int l = 0; l < ell; l++) lorder[l] = l;
     const size_t b_bt = bt.size(), b_bias = biasd.size() * 8, b_yc = (size_t)ell * 8, b_lo = (size_t)ell * 4,
-                 b_c = cst ? (size_t)ell * 8 : 0, b_io = (size_t)n_in * 4;
+                 b_c = cst ? (size_t)ell * 8 : 0, b_io = in ? (size_t)n_in * 4 : 16;
     char *meta = nullptr;
     HE_TRY(he_scratch_alloc((void **)&meta, b_bt + b_bias + b_yc + b_lo + b_c + b_io + 1024, s));
     size_t off = 0;
@@ -956,7 +1029,7 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     int32_t *dlo = (int32_t *)carve(b_lo);
     uint64_t *dc = cst ? (uint64_t *)carve(b_c) : nullptr;
     uint32_t *dio = (uint32_t *)carve(b_io);
-    HE_CHECK_CUDA(he_h2d(dio, ioff.data(), b_io, s));
+    if (in) HE_CHECK_CUDA(he_h2d(dio, ioff.data(), b_io, s));
     HE_CHECK_CUDA(he_h2d(dbt, bt.data(), b_bt, s));
     HE_CHECK_CUDA(he_h2d(dbias, biasd.data(), b_bias, s));
     HE_CHECK_CUDA(he_h2d(dyc, yc.data(), b_yc, s));
@@ -969,7 +1042,9 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     a.out = (uint64_t *const *)dout;
     a.obase = nullptr;
     a.ostride = 0;
-    if (n_out > 1) {  // outputs of one batch allocation: strided addressing, no pointer loads
+    a.pl_in = pl_in;
+    a.pl_out = pl_out;
+    if (out && n_out > 1) {  // outputs of one batch allocation: strided addressing, no pointer loads
         const long long st = (long long)(out[1] - out[0]);
         bool uni = st > 0;
         for (int i = 2; i < n_out && uni; i++) uni = (out[i] - out[i - 1]) == st;
@@ -1014,9 +1089,110 @@ extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int n
     else if (NSH == 6) rc = launch(k_convtc_p1_pool<6>);
     else rc = launch(k_convtc_p1_pool<7>);
     he_scratch_free(meta, s);
-    he_scratch_free(din, s);
-    he_scratch_free(dout, s);
+    if (din) he_scratch_free(din, s);
+    if (dout) he_scratch_free(dout, s);
     return rc;
 }
+
+extern "C" int he_conv_square_sum_tc(he_ctx *c, const uint64_t *const *in, int nci, int p, int H, int W,
+                                     uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
+                                     const uint64_t *bias, const uint64_t *cst, int ell, void *stream) {
+    if (!in || !out) {
+        he_set_error("he_conv_square_sum_tc: bad arguments");
+        return HE_EINVAL;
+    }
+    return convtc_launch(c, in, nci, p, H, W, out, M, pool, y0, y1, weights, bias, cst, ell, nullptr, nullptr, stream);
+}
+
+extern "C" int he_conv_square_sum_pl(he_ctx *c, const uint64_t *const *in, int nci, int p, int H, int W,
+                                     uint64_t *const *out, int M, int pool, int y0, int y1, const int64_t *weights,
+                                     const uint64_t *bias, const uint64_t *cst, int ell, const void *pl_in,
+                                     void *pl_out, void *stream) {
+    return convtc_launch(c, pl_in ? nullptr : in, nci, p, H, W, pl_out ? nullptr : out, M, pool, y0, y1, weights,
+                         bias, cst, ell, (const uint8_t *)pl_in, (uint8_t *)pl_out, stream);
+}
+
+// ---------------------------------------------------------------- planar carry <-> ciphertexts
+// planar byte offset of (limb l, coefficient k, y, x, component cp, plane d, channel m), C = 16 channels
+__device__ __forceinline__ size_t pl_off(int l, size_t k, int y, int x, int cp, int d, int m, int H, int W,
+                                        size_t nchunk) {
+    return ((((size_t)l * nchunk + (k >> 3)) * H + y) * W + x) * (3 * 5 * 128) + (size_t)(cp * 5 + d) * 128 +
+           (k & 7) * 16 + m;
+}
+// one thread per (channel group of 4, coefficient, pixel, component, limb)
+__global__ void k_planar_pack(const uint64_t *const *in, int C, int H, int W, int ell, int logN, uint8_t *pl) {
+    const size_t N = (size_t)1 << logN, nchunk = N >> 3;
+    const size_t tot = (size_t)ell * 3 * H * W * N * 4;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < tot; t += (size_t)gridDim.x * blockDim.x) {
+        const int g = (int)(t & 3);
+        size_t r = t >> 2;
+        const size_t k = r % N;
+        r /= N;
+        const int px = (int)(r % ((size_t)H * W));
+        r /= (size_t)H * W;
+        const int cp = (int)(r % 3), l = (int)(r / 3);
+        uint64_t v[4];
+        for (int u = 0; u < 4; u++) {
+            const int ch = 4 * g + u;
+            v[u] = ch < C ? in[(size_t)ch * H * W + px][((size_t)cp * ell + l) * N + k] : 0;
+        }
+        const size_t o = pl_off(l, k, px / W, px % W, cp, 0, 4 * g, H, W, nchunk);
+        for (int d = 0; d < 5; d++) {
+            uint32_t w = 0;
+            for (int u = 0; u < 4; u++) w |= (uint32_t)((v[u] >> (8 * d)) & 0xFF) << (8 * u);
+            *(uint32_t *)(pl + o + (size_t)d * 128) = w;
+        }
+    }
+}
+__global__ void k_planar_unpack(const uint8_t *pl, int C, int H, int W, int ell, int logN, uint64_t *const *out) {
+    const size_t N = (size_t)1 << logN, nchunk = N >> 3;
+    const size_t tot = (size_t)ell * 3 * H * W * N * C;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < tot; t += (size_t)gridDim.x * blockDim.x) {
+        size_t r = t;
+        const size_t k = r % N;
+        r /= N;
+        const int px = (int)(r % ((size_t)H * W));
+        r /= (size_t)H * W;
+        const int ch = (int)(r % C);
+        r /= C;
+        const int cp = (int)(r % 3), l = (int)(r / 3);
+        const size_t o = pl_off(l, k, px / W, px % W, cp, 0, ch, H, W, nchunk);
+        uint64_t v = 0;
+        for (int d = 0; d < 5; d++) v |= (uint64_t)pl[o + (size_t)d * 128] << (8 * d);
+        out[(size_t)ch * H * W + px][((size_t)cp * ell + l) * N + k] = v;
+    }
+}
+
+// ciphertexts (C <= 16 channels x H x W, 3 components, residues < 2^40 on ell limbs) -> planar carry
+extern "C" int he_planar_pack(he_ctx *c, const uint64_t *const *in, int C, int H, int W, int ell, void *pl,
+                              void *stream) {
+    if (!c || !in || !pl || C < 1 || C > 16 || H < 1 || W < 1 || ell < 1 || ell > c->L) {
+        he_set_error("he_planar_pack: bad arguments");
+        return HE_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    void **din = nullptr;
+    HE_TRY(he_upload_ptrs((const void *const *)in, C * H * W, &din, s));
+    HE_CHECK_CUDA(cudaMemsetAsync(pl, 0, (size_t)ell * (c->N / 8) * H * W * 1920, s));
+    k_planar_pack<<<148 * 16, 256, 0, s>>>((const uint64_t *const *)din, C, H, W, ell, c->logN, (uint8_t *)pl);
+    HE_CHECK_LAUNCH();
+    he_scratch_free(din, s);
+    return HE_OK;
+}
+extern "C" int he_planar_unpack(he_ctx *c, const void *pl, int C, int H, int W, int ell, uint64_t *const *out,
+                                void *stream) {
+    if (!c || !out || !pl || C < 1 || C > 16 || H < 1 || W < 1 || ell < 1 || ell > c->L) {
+        he_set_error("he_planar_unpack: bad arguments");
+        return HE_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    void **dout = nullptr;
+    HE_TRY(he_upload_ptrs((const void *const *)out, C * H * W, &dout, s));
+    k_planar_unpack<<<148 * 16, 256, 0, s>>>((const uint8_t *)pl, C, H, W, ell, c->logN, (uint64_t *const *)dout);
+    HE_CHECK_LAUNCH();
+    he_scratch_free(dout, s);
+    return HE_OK;
+}
+
 
 int he_conv_tc_enabled() { return g_conv_tc; }

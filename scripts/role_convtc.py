@@ -23,3 +23,15 @@ for name, (p, H, W, M, pool, y0, y1, ell, wbits, nci) in {
     names = ["prod wait-empty", "prod total", "mma wait-full", "mma wait-dempty", "mma total", "epi wait-dfull", "epi total"]
     print(name, {n: f"{v/1e6:.2f}M" for n, v in zip(names, r)}, flush=True)
     del x, out; torch.cuda.empty_cache()
+# planar conv2
+ell = 9
+pl = torch.empty(ell * (N // 8) * 16 * 16 * 1920, dtype=torch.uint8, device=eng.device)
+w2 = np.random.default_rng(0).integers(-(1 << 14), 1 << 14, size=(32, 144), dtype=np.int64)
+out2 = torch.empty((32, 5, ell, N), dtype=torch.int64, device=eng.device)
+po2 = _lib.ptr_array([out2[i].data_ptr() for i in range(32)])
+run = lambda: _lib.check(L.he_conv_square_sum_pl(eng._h, None, 3, 16, 16, 16, _lib.addr(po2), 32, 0, 0, 16, _lib.addr(w2), None, None, ell, pl.data_ptr(), None, torch.cuda.current_stream().cuda_stream))
+run(); torch.cuda.synchronize()
+_lib.check(L.he_convtc_profile(1, None)); run(); torch.cuda.synchronize()
+r = np.zeros(7); _lib.check(L.he_convtc_profile(0, r.ctypes.data)); r /= 148
+names = ["prod wait-empty", "prod total", "mma wait-full", "mma wait-dempty", "mma total", "epi wait-dfull", "epi total"]
+print("conv2 planar", {n: f"{v/1e6:.2f}M" for n, v in zip(names, r)}, flush=True)

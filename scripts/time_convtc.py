@@ -65,3 +65,41 @@ def case(p, H, W, M, pool, y0, y1, ell, wbits, nci=2):
 case(3, 32, 32, 16, 1, 0, 8, 9, 20)
 case(3, 32, 32, 16, 1, 0, 32, 9, 20)
 case(16, 16, 16, 32, 0, 0, 16, 9, 14, nci=3)
+
+
+def planar_case(reps=3):
+    """conv1 -> planar carry -> conv2 (the run_cnn chain) at config 3's shapes, 9 limbs."""
+    ell = 9
+    p1, H, W, M1 = 3, 32, 32, 16
+    x = torch.empty((p1 * H * W, 2, ell, N), dtype=torch.int64, device=eng.device)
+    for i, q in enumerate(eng.moduli[:ell]):
+        x[:, :, i] = torch.randint(0, q, (p1 * H * W, 2, N), device=eng.device, dtype=torch.int64)
+    pi = _lib.ptr_array([x[i].data_ptr() for i in range(p1 * H * W)])
+    pl = torch.empty(ell * (N // 8) * 16 * 16 * 1920, dtype=torch.uint8, device=eng.device)
+    w1 = rng.integers(-(1 << 20), 1 << 20, size=(M1, 27), dtype=np.int64)
+    w2 = rng.integers(-(1 << 14), 1 << 14, size=(32, 144), dtype=np.int64)
+    out2 = torch.empty((32, 5, ell, N), dtype=torch.int64, device=eng.device)
+    po2 = _lib.ptr_array([out2[i].data_ptr() for i in range(32)])
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def c1():
+        _lib.check(L.he_conv_square_sum_pl(eng._h, _lib.addr(pi), 2, p1, H, W, None, M1, 1, 0, H, _lib.addr(w1),
+                                           None, None, ell, None, pl.data_ptr(), stream))
+
+    def c2():
+        _lib.check(L.he_conv_square_sum_pl(eng._h, None, 3, 16, 16, 16, _lib.addr(po2), 32, 0, 0, 16,
+                                           _lib.addr(w2), None, None, ell, pl.data_ptr(), None, stream))
+
+    for name, f in (("conv1 -> planar (32 rows)", c1), ("planar -> conv2 (16 rows)", c2)):
+        f()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"{name}: {e0.elapsed_time(e1) / reps:.2f} ms", flush=True)
+
+
+planar_case(reps)

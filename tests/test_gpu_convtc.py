@@ -152,3 +152,88 @@ def test_convtc_conv2_shape_vs_mma_sync():
         torch.cuda.synchronize()
         for k, (o, r) in enumerate(zip(got, ref)):
             assert torch.equal(o, r), (y0, y1, k)
+
+
+def _planar(eng, C, H, W, ell):
+    import torch
+
+    return torch.zeros(ell * (eng.N // 8) * H * W * 1920, dtype=torch.uint8, device=eng.device)
+
+
+def test_planar_pack_roundtrip(small):
+    import torch
+
+    eng, _ = small
+    rng = np.random.default_rng(5)
+    C, H, W, ell = 16, 3, 5, 3
+    x = rand_residues(rng, eng.moduli[:ell], (C * H * W, 3), eng.N)
+    ins = [from_np(x[i], eng.device) for i in range(C * H * W)]
+    pl = _planar(eng, C, H, W, ell)
+    assert eng._L.he_planar_pack(eng._h, _ptrs(ins).ctypes.data, C, H, W, ell, pl.data_ptr(), None) == 0
+    outs = [torch.zeros_like(t) for t in ins]
+    assert eng._L.he_planar_unpack(eng._h, pl.data_ptr(), C, H, W, ell, _ptrs(outs).ctypes.data, None) == 0
+    for a, b in zip(ins, outs):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("ring", ["cfg3s", "cfg3"])
+def test_planar_carry_conv2_equals_pointer_path(small, ring):
+    """conv2 reading the planar carry (one bulk copy per row) == conv2 reading ciphertexts."""
+    import torch
+
+    from paper_2604_16834_b200.engine import GpuEngine
+
+    eng = small[0] if ring == "cfg3s" else GpuEngine(engine_context("cfg3"))
+    L = eng._L
+    p, H, W, M = 16, 6, 16, 32
+    ell = 3 if ring == "cfg3s" else 9
+    x = _rand_dev(eng, p * H * W, 3, ell, 11)
+    ins = [x[i] for i in range(p * H * W)]
+    rng = np.random.default_rng(12)
+    wi = rng.integers(-(1 << 14), 1 << 14, size=(M, 9 * p), dtype=np.int64)
+    bres = np.array([[int(rng.integers(0, q)) for q in eng.moduli[:ell]] for _ in range(M)], np.uint64)
+    cst = np.array([int(rng.integers(0, q)) for q in eng.moduli[:ell]], np.uint64)
+    pl = _planar(eng, p, H, W, ell)
+    assert L.he_planar_pack(eng._h, _ptrs(ins).ctypes.data, p, H, W, ell, pl.data_ptr(), None) == 0
+    for y0, y1 in ((0, 6), (1, 4)):
+        ref = _run(eng, L.he_conv_square_sum_tc, ins, 3, p, H, W, M, 0, y0, y1, wi, bres, cst, ell)
+        got = [torch.zeros_like(t) for t in ref]
+        rc = L.he_conv_square_sum_pl(eng._h, None, 3, p, H, W, _ptrs(got).ctypes.data, M, 0, y0, y1,
+                                     wi.ctypes.data, bres.ctypes.data, cst.ctypes.data, ell, pl.data_ptr(), None,
+                                     None)
+        assert rc == 0, L.he_last_error()
+        torch.cuda.synchronize()
+        for k, (o, r) in enumerate(zip(got, ref)):
+            assert torch.equal(o, r), (y0, y1, k)
+
+
+@pytest.mark.parametrize("ring", ["cfg3s", "cfg3"])
+def test_planar_carry_conv1_equals_pointer_path(small, ring):
+    """conv1 writing the planar carry == conv1's pooled ciphertexts, packed."""
+    import torch
+
+    from paper_2604_16834_b200.engine import GpuEngine
+
+    eng = small[0] if ring == "cfg3s" else GpuEngine(engine_context("cfg3"))
+    L = eng._L
+    p, H, W, M = 3, 8, 32, 16
+    ell = 3 if ring == "cfg3s" else 9
+    x = _rand_dev(eng, p * H * W, 2, ell, 13)
+    ins = [x[i] for i in range(p * H * W)]
+    rng = np.random.default_rng(14)
+    wi = rng.integers(-(1 << 20), 1 << 20, size=(M, 27), dtype=np.int64)
+    bres = np.array([[int(rng.integers(0, q)) for q in eng.moduli[:ell]] for _ in range(M)], np.uint64)
+    cst = np.array([int(rng.integers(0, q)) for q in eng.moduli[:ell]], np.uint64)
+    H2, W2 = H // 2, W // 2
+    pl = _planar(eng, M, H2, W2, ell)
+    for y0, y1 in ((0, 4), (4, 8)):  # two tiles filling the map
+        rc = L.he_conv_square_sum_pl(eng._h, _ptrs(ins).ctypes.data, 2, p, H, W, None, M, 1, y0, y1,
+                                     wi.ctypes.data, bres.ctypes.data, cst.ctypes.data, ell, None, pl.data_ptr(),
+                                     None)
+        assert rc == 0, L.he_last_error()
+    ref = _run(eng, L.he_conv_square_sum_tc, ins, 2, p, H, W, M, 1, 0, H, wi, bres, cst, ell)  # [m][y2][x2]
+    got = [torch.zeros_like(t) for t in ref]
+    assert L.he_planar_unpack(eng._h, pl.data_ptr(), M, H2, W2, ell, _ptrs(got).ctypes.data, None) == 0
+    torch.cuda.synchronize()
+    for k, (o, r) in enumerate(zip(got, ref)):
+        assert torch.equal(o, r), k
