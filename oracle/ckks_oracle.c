@@ -263,6 +263,28 @@ void oc_destroy(oc_ctx *c) {
     free(c);
 }
 
+/* Coefficient view: the same moduli with N = n evaluation points and no tables.
+ * Every element-wise operation in the NTT domain (add, sub, add_const, mul_const,
+ * mul_plain, tensor, tensor_sq, lincomb) acts on each evaluation point
+ * independently, so running them on n sampled points of [nc][ell][N] ciphertexts
+ * (packed as [nc][ell][n]) gives exactly those points of the full result.  NTT,
+ * key switching, rescale and encryption need the tables and must not be called
+ * on a view (the Python wrapper refuses them).  Free with oc_destroy. */
+oc_ctx *oc_coeff_view(const oc_ctx *c, int n) {
+    oc_ctx *v = (oc_ctx *)calloc(1, sizeof(oc_ctx));
+    v->prm = c->prm;
+    v->logN = c->logN;
+    v->N = n;
+    v->L = c->L;
+    v->K = c->K;
+    v->alpha = c->alpha;
+    v->dnum = c->dnum;
+    v->nslots = 0;
+    memcpy(v->mod, c->mod, sizeof(c->mod));
+    memcpy(v->psi, c->psi, sizeof(c->psi));
+    return v;
+}
+
 void oc_moduli(const oc_ctx *c, uint64_t *moduli, uint64_t *psi) {
     for (int m = 0; m < c->L + c->K; m++) {
         if (moduli) moduli[m] = c->mod[m];

@@ -52,6 +52,8 @@ def lib():
         L.oc_create.restype = vp
         L.oc_create.argtypes = [C.POINTER(OcParams)]
         L.oc_destroy.argtypes = [vp]
+        L.oc_coeff_view.restype = vp
+        L.oc_coeff_view.argtypes = [vp, C.c_int]
         L.oc_moduli.argtypes = [vp, u64p, u64p]
         L.oc_philox.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.oc_ntt.argtypes = [vp, u64p, C.c_int]
@@ -137,6 +139,13 @@ class Oracle:
         lib().oc_moduli(self._h, _u64(mods), _u64(psi))
         self.moduli = [int(x) for x in mods]
         self.psi = [int(x) for x in psi]
+
+    def coeff_view(self, n):
+        """Element-wise-only oracle over n sampled evaluation points (oc_coeff_view):
+        add/sub/add_const/mul_const/mul_plain/tensor/tensor_sq/lincomb on
+        [nc][ell][n] arrays give exactly those points of the full-ring results.
+        Pack a ciphertext's sampled points with ``ct[..., idx]``."""
+        return CoeffView(self, n)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -331,6 +340,28 @@ class Oracle:
         lib().oc_lincomb(self._h, in_p, out_p, n_out, _p(rp, C.c_int32), _p(cl, C.c_int32),
                          _p(ww, C.c_int64), ell, nc, n_threads)
         return outs
+
+
+class CoeffView(Oracle):
+    """Oracle.coeff_view: same moduli, N = n sampled points, element-wise ops only."""
+
+    _ELEMENTWISE = {"add", "sub", "add_const", "mul_const", "mul_plain", "tensor", "tensor_sq", "lincomb"}
+
+    def __init__(self, parent, n):  # noqa: D107 -- no oc_create: the tables stay with the parent
+        self.params = parent.params
+        self.N = n
+        self.n = 0
+        self.L, self.K, self.alpha, self.dnum = parent.L, parent.K, parent.alpha, parent.dnum
+        self.scale = parent.scale
+        self.moduli, self.psi = parent.moduli, parent.psi
+        self._parent = parent
+        self._h = lib().oc_coeff_view(parent._h, n)
+
+    def __getattribute__(self, name):
+        if (not name.startswith("_") and name not in CoeffView._ELEMENTWISE and callable(getattr(Oracle, name, None))
+                and name not in ("coeff_view",)):
+            raise TypeError(f"CoeffView supports element-wise operations only, not {name}")
+        return object.__getattribute__(self, name)
 
 
 def power_key_elt(power: int) -> int:

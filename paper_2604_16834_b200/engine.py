@@ -168,6 +168,32 @@ class CipherVec:
         return self.data.data_ptr()
 
 
+@dataclass(eq=False)
+class PlanarCarry:
+    """The pooled, unrelinearised 3-component squares of the block before the
+    last (run_cnn's carry), held in the conv2 kernel's shared-memory ring layout
+    instead of as C*H*W ciphertexts: [limb][N/8 coefficient chunks][y][x]
+    [component][byte plane][8 coefficients x 16 channels], one byte per residue
+    byte, 5 bytes per 40-bit residue (include/he_sm100.h he_conv_square_sum_pl).
+    conv1's epilogue writes it, conv2 fills its ring with one bulk copy per row.
+    Every residue is canonical, so he_planar_unpack recovers the ciphertexts
+    bit for bit."""
+
+    data: object          # torch uint8 [limbs * N/8 * H * W * 1920]
+    channels: int
+    H: int
+    W: int
+    level: int
+    scale: float
+    owner: int
+
+    BYTES_PER_PIXEL = 3 * 5 * 128
+
+    @property
+    def limbs(self) -> int:
+        return self.level + 1
+
+
 @dataclass(frozen=True)
 class PlainVec:
     """A plaintext slot vector, full slot width (engine.py:83-90).
@@ -1183,8 +1209,8 @@ class GpuEngine:
         return self._wrap_batch(out, level, [s_out] * n_out)
 
     def conv_square_sum(self, inputs: Sequence[CipherVec], p: int, H: int, W: int, weights, weight_scale: float,
-                        bias, const: float, pool: bool, rows=None, scale_mult: float | None = None
-                        ) -> list[CipherVec] | None:
+                        bias, const: float, pool: bool, rows=None, scale_mult: float | None = None,
+                        planar_out: PlanarCarry | None = None) -> list[CipherVec] | None:
         """Fused deferred-rescale 3x3 conv + lazy degree-2 activation + window
         sum (he_conv_square_sum): equals conv_mma(weight_scale) -> tensor_batch
         -> add_const_batch(const) -> 2x2-pool / GAP unit sum, bit for bit, but
@@ -1195,17 +1221,25 @@ class GpuEngine:
         the inputs are unrelinearised 3-component squares), scale
         s_out^2 * scale_mult (default 4 for pool, pixel count for GAP).
         None when a tensor-core bound does not hold (caller falls back)."""
-        for c in inputs:
-            self._check(c)
-        nci = self._ncomp(inputs)
-        if nci == 3 and W % 2:
-            return None
-        s_in = inputs[0].scale
-        if any(c.scale != s_in for c in inputs):
-            raise ScaleMismatch("conv_square_sum needs inputs at one scale")
-        if len(inputs) != p * H * W:
-            raise ShapeMismatch(f"{len(inputs)} inputs for {p}x{H}x{W}")
-        level = min(c.level for c in inputs)
+        planar_in = isinstance(inputs, PlanarCarry)
+        if planar_in:
+            if inputs.owner != id(self) or inputs.data is None:
+                raise ContextMismatch("planar carry does not belong to this engine (or was released)")
+            if (inputs.channels, inputs.H, inputs.W) != (p, H, W):
+                raise ShapeMismatch(f"planar carry {inputs.channels}x{inputs.H}x{inputs.W} for {p}x{H}x{W}")
+            nci, s_in, level = 3, inputs.scale, inputs.level
+        else:
+            for c in inputs:
+                self._check(c)
+            nci = self._ncomp(inputs)
+            if nci == 3 and W % 2:
+                return None
+            s_in = inputs[0].scale
+            if any(c.scale != s_in for c in inputs):
+                raise ScaleMismatch("conv_square_sum needs inputs at one scale")
+            if len(inputs) != p * H * W:
+                raise ShapeMismatch(f"{len(inputs)} inputs for {p}x{H}x{W}")
+            level = min(c.level for c in inputs)
         if level < self.context.mult_level_cost:
             raise LevelExhausted(f"level {level} < multiplication cost {self.context.mult_level_cost}")
         limbs = level + 1
@@ -1227,11 +1261,18 @@ class GpuEngine:
         cres = np.array(self._res(npix_win * C, limbs), np.uint64) if const else None
         nwin = ((y1 - y0) // 2) * (W // 2) if pool else 1
         n_out = M * nwin
-        tins = self._at_level(inputs, level)
-        pin = _lib.ptr_array([t.data_ptr() for t in tins])
         nco = 2 * nci - 1
-        out = self._alloc(n_out, nco, limbs)
-        pout = self._tptrs(out)
+        if planar_out is not None:
+            if (planar_out.owner != id(self) or planar_out.level != level or planar_out.channels != M or not pool
+                    or (planar_out.H, planar_out.W) != (H // 2, W // 2)):
+                raise ShapeMismatch("planar carry output does not match this pooled conv")
+            if planar_out.scale is None:
+                planar_out.scale = s_out * s_out * (scale_mult if scale_mult is not None else 4.0)
+        pin = None if planar_in else _lib.ptr_array([t.data_ptr() for t in self._at_level(inputs, level)])
+        out = pout = None
+        if planar_out is None:
+            out = self._alloc(n_out, nco, limbs)
+            pout = self._tptrs(out)
         from .featuremajor import conv3x3_fulltaps
 
         nnz = int((conv3x3_fulltaps(p, H, W, rows) >= 0).sum())
@@ -1242,22 +1283,58 @@ class GpuEngine:
         E = 1 if wmax < 128 else 2 if wmax < 32768 else 3
         nbs = sum(5 if q < (1 << 40) else 8 for q in self.moduli[:limbs])
         i8 = 1.0 * nci * nnz * M * self.N * nbs * E
-        rc = self._call("conv_sqsum", self._L.he_conv_square_sum_n, self._h, _lib.addr(pin), nci, p, H, W,
-                        _lib.addr(pout), M, int(bool(pool)), y0, y1, _lib.addr(wi),
-                        _lib.addr(bres) if bres is not None else None,
-                        _lib.addr(cres) if cres is not None else None, limbs, self.stream,
-                        units=((p * (y1 - y0 + 2) * W * nci + n_out * nco) * poly * 8.0, 1.0 * nci * nnz * M * poly,
-                               i8))
-        if rc == _lib.HE_EINVAL:
-            return None
-        _lib.check(rc, "conv_square_sum")
+        # algorithmic bytes: inputs once (+ the 2-row halo), outputs once; a planar carry
+        # moves 5 bytes per residue instead of 8
+        in_b = p * (y1 - y0 + 2) * W * nci * poly * (5.0 if planar_in else 8.0)
+        out_b = n_out * nco * poly * (5.0 if planar_out is not None else 8.0)
+        args = (self._h, _lib.addr(pin) if pin is not None else None, nci, p, H, W,
+                _lib.addr(pout) if pout is not None else None, M, int(bool(pool)), y0, y1, _lib.addr(wi),
+                _lib.addr(bres) if bres is not None else None, _lib.addr(cres) if cres is not None else None, limbs)
+        units = (in_b + out_b, 1.0 * nci * nnz * M * poly, i8)
+        if planar_in or planar_out is not None:
+            rc = self._call("conv_sqsum", self._L.he_conv_square_sum_pl, *args,
+                            inputs.data.data_ptr() if planar_in else None,
+                            planar_out.data.data_ptr() if planar_out is not None else None, self.stream, units=units)
+            _lib.check(rc, "conv_square_sum (planar carry)")
+        else:
+            rc = self._call("conv_sqsum", self._L.he_conv_square_sum_n, *args, self.stream, units=units)
+            if rc == _lib.HE_EINVAL:
+                return None
+            _lib.check(rc, "conv_square_sum")
         npx = (y1 - y0) * W
         self._acct.bump("plain_mults", nnz * M)
         self._acct.bump("adds", nnz * M)
         self._acct.bump("ct_mults", M * npx)
         self._acct.bump("adds", M * npx + max(0, M * npx - n_out))
         sm = scale_mult if scale_mult is not None else float(npix_win)
+        if planar_out is not None:
+            return []
         return self._wrap_batch(out, level, [s_out * s_out * sm] * n_out)
+
+    def planar_carry(self, channels: int, H: int, W: int, level: int) -> PlanarCarry:
+        """An empty planar carry for `channels` pooled H x W maps at `level`
+        (filled by conv_square_sum(planar_out=...); scale set by the first fill)."""
+        if channels != 16 or W != 16:
+            raise ShapeMismatch("the planar carry holds 16 channels of 16-pixel rows (config 3's conv1 -> conv2)")
+        torch = _torch()
+        n = (level + 1) * (self.N // 8) * H * W * PlanarCarry.BYTES_PER_PIXEL
+        return PlanarCarry(torch.empty(n, dtype=torch.uint8, device=self.device), channels, H, W, level, None, id(self))
+
+    def planar_ok(self, p_in: int, H: int, W: int, q: int, q_next: int, level: int) -> bool:
+        """Whether run_cnn's carry can go through the planar layout: conv1 on the
+        tcgen05 P1 kernel (p_in <= 3, 16 output channels, W % 16 == 0, pooled) feeding
+        conv2 on the P16 kernel (16 input channels, 16-pixel rows), primes in [2^36, 2^40)."""
+        return (self.use_tensor_cores and self.N == 1 << 16 and p_in <= 3 and q == 16 and W == 32 and H % 2 == 0
+                and q_next <= 32 and all((1 << 36) <= m < (1 << 40) for m in self.moduli[:level + 1]))
+
+    def unpack_planar(self, pc: PlanarCarry) -> list[CipherVec]:
+        """The planar carry as channel-major 3-component ciphertexts (tests, tracing)."""
+        n = pc.channels * pc.H * pc.W
+        out = self._alloc(n, 3, pc.limbs)
+        po = self._tptrs(out)
+        _lib.check(self._L.he_planar_unpack(self._h, pc.data.data_ptr(), pc.channels, pc.H, pc.W, pc.limbs,
+                                            _lib.addr(po), self.stream), "planar_unpack")
+        return self._wrap_batch(out, pc.level, [pc.scale] * n)
 
     def lincomb_int(self, inputs: Sequence[CipherVec], row_ptr, col, int_weights, out_scale: float,
                     count_adds: bool = True) -> list[CipherVec]:

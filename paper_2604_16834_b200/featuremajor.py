@@ -224,11 +224,13 @@ def fm_conv3x3(engine, inputs, weights, bias, H, W, out_channels=None, fold=(1.0
 
 
 def fm_conv_square_sum(engine, inputs, weights, bias, H, W, fold=(1.0, 0.0), rows=None, weight_scale=None,
-                       const=0.0, pool=True, scale_mult=None):
+                       const=0.0, pool=True, scale_mult=None, planar_out=None):
     """Deferred-rescale conv fused with the lazy square activation and the
     2x2-pool (pool=True) or GAP (pool=False) unit sum: one he_conv_square_sum
     launch per <= 32 output channels.  Returns the window sums indexed
-    (o, r/2, x/2) / (o,), or None when the fused kernel does not apply."""
+    (o, r/2, x/2) / (o,), or None when the fused kernel does not apply.
+    ``planar_out`` (engine.planar_carry): the pooled sums are written into the
+    planar carry instead (returns [])."""
     w = np.asarray(weights, np.float64)
     q, p = w.shape[:2]
     a, b = fold
@@ -237,8 +239,9 @@ def fm_conv_square_sum(engine, inputs, weights, bias, H, W, fold=(1.0, 0.0), row
         ch = list(range(c0, min(q, c0 + 32)))
         wm = a * w[ch].reshape(len(ch), p * 9)
         bias_ch = a * np.asarray(bias, np.float64)[ch] + b
+        kw = {"planar_out": planar_out} if planar_out is not None else {}
         res = engine.conv_square_sum(inputs, p, H, W, wm, weight_scale, bias_ch, const, pool, rows=rows,
-                                     scale_mult=scale_mult)
+                                     scale_mult=scale_mult, **kw)
         if res is None:
             engine.release(*out)
             return None
@@ -390,9 +393,16 @@ class CnnSpec:
         return g @ wts.dense[0].T + wts.dense[1]
 
 
+def _free_planar(engine, pc, unpack=True):
+    """Drop a planar carry; with ``unpack`` return its ciphertexts first."""
+    cts = engine.unpack_planar(pc) if unpack else None
+    pc.data = None
+    return cts
+
+
 def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, release_inputs: bool = True,
             tile_outputs: int = 1024, lazy_relin: bool = True, carry: bool = True,
-            fused_tile_outputs: int = 1024):
+            fused_tile_outputs: int = 1024, trace=None):
     """Encrypted forward pass of ``spec`` over feature-major input ciphertexts.
 
     x_cts: C0*H*W ciphertexts (channel-major).  Each block is streamed over
@@ -412,6 +422,12 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
     its global sums -- one per output channel -- are relinearised (keys s^2, s^3,
     s^4, engine.relin_rescale_batch) with `carried_drops` primes dropped.  For
     config 3 that replaces 4096 + 32 relinearisations by 32.
+
+    ``trace`` (tests): called as trace(stage, cts, info) with every layer's
+    outputs before they are released -- ("block", tile outputs, {"blk", "rows"})
+    per row tile, ("planar", engine.PlanarCarry, {"blk"}) once a planar carry
+    is complete, ("gap", ...) before the last relinearisation, ("relin", ...)
+    after it and ("dense", ...) at the end.
     """
     H, W = spec.H, spec.W
     cur = list(x_cts)
@@ -425,26 +441,36 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
         last = blk == nblk - 1
         # this block's pooled squares stay unrelinearised for the last block
         carry_out = (carry and fused_ok and pool and blk == nblk - 2 and (W // 2) % 2 == 0)
+        # ... and, where both tcgen05 kernels take the shapes, in the planar layout
+        # (5 bytes per residue, conv2's ring layout) instead of as ciphertexts
+        planar = (carry_out and hasattr(engine, "planar_ok")
+                  and engine.planar_ok(w.shape[1], H, W, q, wts.convs[blk + 1][0].shape[0], cur[0].level))
+        planar_in = not isinstance(cur, list)
+        ref = [cur] if planar_in else cur  # level / scale of the block's inputs
         drops = 2
-        if _ncomp(engine, cur) == 3:  # carried squares: one 5-component relinearisation after the GAP
-            drops = carried_drops(engine, cur)
+        if planar_in or _ncomp(engine, cur) == 3:  # carried squares: one 5-component relin after the GAP
+            drops = carried_drops(engine, ref)
             p_in = w.shape[1]
-            wmax = np.abs(a * w).max() * deferred_weight_scale(engine, cur, drops)
+            wmax = np.abs(a * w).max() * deferred_weight_scale(engine, ref, drops)
             if not (last and p_in <= 16 and W % 2 == 0 and np.rint(wmax) < 2 ** 23
-                    and min(engine.moduli[:cur[0].level + 1]) >= 2 ** 36):
+                    and min(engine.moduli[:ref[0].level + 1]) >= 2 ** 36):
+                if planar_in:
+                    cur = _free_planar(engine, cur)
                 z = engine.relin_rescale_batch(cur, drops=2)  # outside the fused kernel's bounds
                 engine.release(*cur)
                 cur, drops = z, 2
+                planar_in, ref = False, z
         R = max(2 if pool else 1, (tile_outputs // (q * W)) // 2 * 2 if pool else tile_outputs // (q * W))
         R = min(R, H) if stream else H
         Ho, Wo = (H // 2, W // 2) if pool else (H, W)
         nxt = [None] * (q * Ho * Wo) if not last else None
+        pc = engine.planar_carry(q, Ho, Wo, cur[0].level) if planar else None
         gap = None
         lazy = lazy_relin and (pool or last)
         # deferred rescale: the conv output keeps its level (weights at ~2^20),
         # the activation's summed products drop two primes after relinearising
         defer = lazy and spec.act.degree == 2
-        dw = deferred_weight_scale(engine, cur, drops) if defer else None
+        dw = deferred_weight_scale(engine, ref, drops) if defer else None
         # conv + square + pool/GAP in one kernel: no conv map in HBM, so the
         # tiles only bound the 3-component window sums (about tile_outputs)
         fused = defer and getattr(engine, "use_fused_conv", False) and (last or pool)
@@ -457,10 +483,13 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
                 c0, c1, c2 = spec.act.coeffs
                 cst = c0 - c1 * c1 / (4 * c2)
                 part = (fm_conv_square_sum(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw,
-                                           const=cst, pool=not last, scale_mult=H * W if last else 4.0)
+                                           const=cst, pool=not last, scale_mult=H * W if last else 4.0,
+                                           planar_out=pc)
                         if fused else None)
-                if part is None and _ncomp(engine, cur) == 3:
+                if part is None and (planar_in or pc is not None or _ncomp(engine, cur) == 3):
                     raise HebatchError("fused conv declined carried 3-component inputs")
+                if pc is not None:
+                    continue  # the pooled rows are in the planar carry
                 if part is None:
                     # conv, then square (no relin) + constant + pool / GAP sum in one pass
                     y = fm_conv3x3(engine, cur, w, bias, H, W, fold=(a, b), rows=rows, weight_scale=dw)
@@ -471,6 +500,8 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
                         rp, cols = pool2x2_csr(q, nr, W)
                         part = engine.square_sum_batch(y, rp, cols, cst, 4.0)
                     engine.release(*y)
+                if trace is not None:
+                    trace("block", part, {"blk": blk, "rows": rows, "fused": fused})
                 if last:
                     if gap is None:
                         gap = part
@@ -521,16 +552,28 @@ def run_cnn(engine, x_cts, spec: CnnSpec, wts: CnnWeights, stream: bool = True, 
                 for r in range(nr):
                     for x in range(Wo):
                         nxt[o * Ho * Wo + (y0 + r) * Wo + x] = z[(o * nr + r) * Wo + x]
-        if blk > 0 or release_inputs:
+        if planar_in:
+            _free_planar(engine, cur, unpack=False)
+        elif blk > 0 or release_inputs:
             engine.release(*cur)
+        if pc is not None:
+            if trace is not None:
+                trace("planar", pc, {"blk": blk})
+            nxt = pc
         if last and lazy_relin:
+            if trace is not None:
+                trace("gap", gap, {"blk": blk, "drops": drops if defer else 1})
             g2 = engine.relin_rescale_batch(gap, drops=drops if defer else 1)
             engine.release(*gap)
             gap = g2
+            if trace is not None:
+                trace("relin", gap, {"blk": blk})
         cur = gap if last else nxt
         H, W = Ho, Wo
     out = fm_dense(engine, cur, wts.dense[0], wts.dense[1])
     engine.release(*cur)
+    if trace is not None:
+        trace("dense", out, {})
     return out
 
 

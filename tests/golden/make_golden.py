@@ -13,6 +13,9 @@ Fixtures:
   fm_cnn_small.npz  a small feature-major CNN (conv3x3 + act 0.125x^2+0.5x+0.25
                     + 2x2 avg pool + GAP + dense) written with the reference's
                     own constant / mult_plain / add / mult_ct primitives.
+  fm_cnn2_small.npz two conv blocks (2->3 channels at 4x4 + act + 2x2 avg pool,
+                    3->4 at 2x2 + act + GAP, dense 4->5), the shape of config 3's
+                    network, for the carry-plan replay (tests/test_golden.py).
   spec_examples.json  results of the SPEC.md operation examples on the reference.
 """
 
@@ -115,6 +118,67 @@ def fm_cnn_small():
                         logits=np.stack(logits, axis=1))
 
 
+def _ref_conv_act(eng, x, w, p, q, H, W):
+    """conv3x3 (pad 1) + 0.125 v^2 + 0.5 v + 0.25 with the reference primitives."""
+    act = {}
+    for o in range(q):
+        for y in range(H):
+            for xx in range(W):
+                acc = None
+                for i in range(p):
+                    for dy in (-1, 0, 1):
+                        for dx in (-1, 0, 1):
+                            yy, xs = y + dy, xx + dx
+                            if 0 <= yy < H and 0 <= xs < W:
+                                t = eng.mult_plain(x[(i, yy, xs)], eng.constant(w[o, i, dy + 1, dx + 1]))
+                                acc = t if acc is None else eng.add(acc, t)
+                sq = eng.mult_plain(eng.mult_ct(acc, acc), eng.constant(0.125))
+                lin = eng.mult_plain(acc, eng.constant(0.5))
+                act[(o, y, xx)] = eng.add_plain(eng.add(sq, lin), eng.constant(0.25))
+    return act
+
+
+def fm_cnn2_small():
+    """Two conv blocks in the reference primitives (config 3's layer sequence)."""
+    n, p, q1, q2, H, W = 16, 2, 3, 4, 4, 4
+    rng = np.random.default_rng(5)
+    imgs = rng.uniform(0.0, 1.0, size=(n, p, H, W))
+    w1 = rng.normal(0.0, np.sqrt(1 / (9 * p)), (q1, p, 3, 3))
+    w2 = rng.normal(0.0, np.sqrt(1 / (9 * q1)), (q2, q1, 3, 3))
+    wd = rng.normal(0.0, np.sqrt(1 / q2), (5, q2))
+    eng = SimulatorEngine(EngineContext(n=n, max_level=12, bootstrap_reserve=1))
+    x = {(c, y, xx): eng.encrypt(imgs[:, c, y, xx]) for c in range(p) for y in range(H) for xx in range(W)}
+    a1 = _ref_conv_act(eng, x, w1, p, q1, H, W)
+    pooled = {}
+    for o in range(q1):
+        for y in range(H // 2):
+            for xx in range(W // 2):
+                s = None
+                for a in (0, 1):
+                    for b in (0, 1):
+                        t = eng.mult_plain(a1[(o, 2 * y + a, 2 * xx + b)], eng.constant(0.25))
+                        s = t if s is None else eng.add(s, t)
+                pooled[(o, y, xx)] = s
+    a2 = _ref_conv_act(eng, pooled, w2, q1, q2, H // 2, W // 2)
+    gap = []
+    for o in range(q2):
+        s = None
+        for y in range(H // 2):
+            for xx in range(W // 2):
+                t = eng.mult_plain(a2[(o, y, xx)], eng.constant(1.0 / ((H // 2) * (W // 2))))
+                s = t if s is None else eng.add(s, t)
+        gap.append(s)
+    logits = []
+    for k in range(5):
+        s = None
+        for o in range(q2):
+            t = eng.mult_plain(gap[o], eng.constant(wd[k, o]))
+            s = t if s is None else eng.add(s, t)
+        logits.append(eng.decrypt(s))
+    np.savez_compressed(os.path.join(HERE, "fm_cnn2_small.npz"), images=imgs, w1=w1, w2=w2, wd=wd,
+                        logits=np.stack(logits, axis=1))
+
+
 def spec_examples():
     out = {}
     e = SimulatorEngine(EngineContext(n=4, max_level=25, bootstrap_reserve=10))
@@ -173,5 +237,6 @@ def spec_examples():
 if __name__ == "__main__":
     cfg1()
     fm_cnn_small()
+    fm_cnn2_small()
     spec_examples()
     print("golden fixtures written to", HERE)

@@ -15,6 +15,8 @@ PARAMS = {
     "cfg4s": (12, (50,) * 10, (50,) * 2, 2, 50),
     # config 3's prime sizes on a small ring (tcgen05 conv kernels vs the oracle)
     "cfg3s": (12, (40,) * 6, (42,) * 2, 3, 40),
+    # config 3's 9-limb carry plan (inputs at 9 of 14 limbs) on a 64-point ring (CPU tests)
+    "carry9": (6, (40,) * 9, (42,) * 3, 3, 40),
 }
 
 

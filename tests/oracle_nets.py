@@ -183,3 +183,118 @@ def relin_rescale2(orc, rk, a):
 def encrypt_features(orc, feats, base_index=0):
     """feature-major packing: column f of feats -> ciphertext f."""
     return [OracleCts(orc.encrypt(feats[:, f], base_index + f), orc.scale) for f in range(feats.shape[1])]
+
+
+# ---------------------------------------------------------------- the carry plan (bench path)
+def _deferred_dw(moduli, delta, limbs, s_in, drops):
+    """featuremajor.deferred_weight_scale restated: (s_in dw)^2 / (q_{l-1}..q_{l-drops}) = Delta."""
+    prod = 1.0
+    for k in range(drops):
+        prod *= moduli[limbs - 1 - k]
+    return math.sqrt(delta * prod) / s_in
+
+
+def _carried_drops(moduli, delta, limbs, s_in, min_scale=2.0 ** 16):
+    """featuremajor.carried_drops restated: the fewest primes giving an integer weight scale >= 2^16."""
+    for d in range(2, limbs):
+        if _deferred_dw(moduli, delta, limbs, s_in, d) >= min_scale:
+            return d
+    raise AssertionError("no level budget for the carried activation")
+
+
+def _fulltaps(p, H, W):
+    """[pixel][9p] input index per tap slot i*9 + (dy+1)*3 + (dx+1) (-1 outside), pixels row-major."""
+    out = np.full((H * W, 9 * p), -1, np.int64)
+    for y in range(H):
+        for x in range(W):
+            for i in range(p):
+                for k in range(9):
+                    yy, xx = y + k // 3 - 1, x + k % 3 - 1
+                    if 0 <= yy < H and 0 <= xx < W:
+                        out[y * W + x, i * 9 + k] = i * H * W + yy * W + xx
+    return out
+
+
+def conv_square_sum_sampled(view, ins, p, H, W, wi, bres, cres, pool):
+    """engine.conv_square_sum restated on sampled evaluation points (view =
+    Oracle.coeff_view): deferred conv (integer weights, no rescale) -> + bias on
+    component 0 -> square (oc_tensor_sq: 3 components from 2, 5 from 3) -> sum
+    over each 2x2 window (pool) or every pixel (GAP) -> + the window constant on
+    component 0.  ins: p*H*W arrays [nc][ell][S]; returns [M][nwin] (pool,
+    window-major per channel) or [M] (GAP) arrays [2nc-1][ell][S]."""
+    M = wi.shape[0]
+    taps = _fulltaps(p, H, W)
+    rows, cols, ws = [0], [], []
+    for m in range(M):
+        for px in range(H * W):
+            for t in np.nonzero(taps[px] >= 0)[0]:
+                cols.append(int(taps[px, t]))
+                ws.append(int(wi[m, t]))
+            rows.append(len(cols))
+    conv = view.lincomb(ins, rows, cols, ws)
+    nc = ins[0].shape[0]
+    sq = []
+    for k, o in enumerate(conv):
+        m = k // (H * W)
+        if bres is not None:
+            o = o.copy()
+            o[:2] = view.add_const(np.ascontiguousarray(o[:2]), [int(v) for v in bres[m]])
+        sq.append(view.tensor_sq(o) if nc == 3 else view.tensor(o, o))
+    if pool:
+        wins = [[(2 * wy + a) * W + 2 * wx + b for a in (0, 1) for b in (0, 1)]
+                for wy in range(H // 2) for wx in range(W // 2)]
+    else:
+        wins = [list(range(H * W))]
+    out = []
+    for m in range(M):
+        for win in wins:
+            acc = sq[m * H * W + win[0]]
+            for px in win[1:]:
+                acc = view.add(acc, sq[m * H * W + px])
+            acc = acc.copy()
+            acc[:2] = view.add_const(np.ascontiguousarray(acc[:2]), [int(v) for v in cres])
+            out.append(acc)
+    return out
+
+
+def carry_plan_convs_sampled(view, moduli, delta, x_samp, x_scale, spec, wts):
+    """featuremajor.run_cnn's fused carry plan (config 3: conv1 + square + 2x2
+    pool left UNrelinearised, conv2 over the 3-component squares + square + GAP
+    as 5-component sums) restated with the oracle on sampled evaluation points.
+
+    x_samp: the C0*H*W input ciphertexts' sampled points [2][ell][S].  Returns
+    (block-0 outputs [16*(H/2)*(W/2)] in run_cnn's (o, y, x) order, their scale,
+    GAP outputs [32], their scale, the relinearisation's drop count)."""
+    assert len(wts.convs) == 2 and spec.pool_after == (0,) and spec.act.degree == 2
+    c0, c1, c2 = spec.act.coeffs
+    a = math.sqrt(c2)
+    b = c1 / (2 * a)
+    cst = c0 - c1 * c1 / (4 * c2)
+    H, W = spec.H, spec.W
+    ell = x_samp[0].shape[1]
+    res = []
+    cur, s_in = x_samp, x_scale
+    drops = 2
+    for blk, (w, bias) in enumerate(wts.convs):
+        q, p = w.shape[:2]
+        pool = blk == 0
+        if blk == 1:
+            drops = _carried_drops(moduli, delta, ell, s_in)
+        dw = _deferred_dw(moduli, delta, ell, s_in, drops)
+        wi = np.rint((a * w.reshape(q, p * 9)) * float(dw)).astype(np.int64)
+        assert np.abs(wi).max() < 2 ** 23
+        s_out = s_in * float(dw)
+        bv = a * np.asarray(bias, np.float64) + b
+        bres = (np.array([[int(np.rint(v * s_out)) % m for m in moduli[:ell]] for v in bv], np.uint64)
+                if np.any(bv != 0) else None)
+        npix = 4 if pool else H * W
+        C = int(np.rint(cst * (s_out * s_out)))
+        cres = [npix * C % m for m in moduli[:ell]]
+        out = conv_square_sum_sampled(view, cur, p, H, W, wi, bres, cres, pool)
+        s_next = s_out * s_out * npix
+        res.append((out, s_next))
+        cur, s_in = out, s_next
+        if pool:
+            H, W = H // 2, W // 2
+    (b0, s0), (g, sg) = res
+    return b0, s0, g, sg, drops

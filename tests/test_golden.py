@@ -131,3 +131,39 @@ def test_spec_examples_fixture_is_the_reference_behaviour():
     assert ex["rotate_-3"] == ex["rotate_1"]
     assert ex["conv_p3_q16_counts"] == [432, 24]
     assert ex["mult_plain_ones"][1] == 24
+
+
+def test_carry_plan_oracle_replay_decrypts_to_reference():
+    """The plan bench.py times (run_cnn's fused carry plan: conv1 + square + pool
+    kept as 3-component sums, conv2 over them + square + GAP as 5-component sums,
+    ONE 5-component relinearisation dropping carried_drops primes, dense +
+    rescale) replayed on the oracle end to end decrypts to the reference
+    simulator's two-block CNN (fm_cnn2_small.npz) within 1e-3.  The same replay
+    (oracle_nets.carry_plan_convs_sampled) is the limb-level checker of the GPU
+    network in tests/test_gpu_networks.py."""
+    import oracle as O
+    import oracle_nets as ON
+
+    from paper_2604_16834_b200.featuremajor import Activation, CnnSpec, CnnWeights, dense_csr
+
+    g = np.load(os.path.join(GOLD, "fm_cnn2_small.npz"))
+    spec = CnnSpec(channels=(2, 3, 4), H=4, W=4, act=Activation((0.25, 0.5, 0.125)), pool_after=(0,), n_classes=5)
+    wts = CnnWeights([(g["w1"], np.zeros(3)), (g["w2"], np.zeros(4))], (g["wd"], np.zeros(5)))
+    assert np.max(np.abs(spec.forward_plain(wts, g["images"]) - g["logits"])) < 1e-9
+    orc = oracle_for("carry9", seed=6)
+    x = [o.data for o in ON.encrypt_features(orc, g["images"].reshape(16, -1))]
+    b0, s0, gap, sg, drops = ON.carry_plan_convs_sampled(orc, orc.moduli, orc.scale, x, orc.scale, spec, wts)
+    assert len(b0) == 3 * 2 * 2 and b0[0].shape[0] == 3 and gap[0].shape[0] == 5
+    assert drops == 6                      # config 3's level plan: 9 limbs -> 3 after the relinearisation
+    keys = [orc.switch_key(O.power_key_elt(k)) for k in (2, 3, 4)]
+    rel = []
+    for c in gap:
+        s = sg
+        for k in range(drops):
+            s /= orc.moduli[c.shape[1] - 1 - k]
+        rel.append(ON.OracleCts(orc.relin_rescale_n(c, keys, drops), s))
+    rp, cols = dense_csr(5, 4)
+    out = ON.lincomb(orc, rel, rp, cols, wts.dense[0].reshape(-1), bias=np.zeros(5), out_scale=orc.scale)
+    assert out[0].ell == 2
+    got = np.stack([orc.decrypt(o.data, o.scale) for o in out], axis=1)[:16]
+    assert np.max(np.abs(got - g["logits"])) < 1e-3

@@ -21,8 +21,14 @@ from test_gpu_parity import _oracle_conv_square_sum
 pytestmark = pytest.mark.gpu
 
 
+_KEEP = []  # pointer arrays passed as `_ptrs(x).ctypes.data` must outlive the call
+
+
 def _ptrs(ts):
-    return np.array([t.data_ptr() for t in ts], np.uint64)
+    a = np.array([t.data_ptr() for t in ts], np.uint64)
+    _KEEP.append(a)
+    del _KEEP[:-16]
+    return a
 
 
 @pytest.fixture(scope="module")

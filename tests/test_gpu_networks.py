@@ -250,3 +250,105 @@ def test_cbc_conv_forward_hoisted_rotations_cfg1_ring():
               for dy in range(3) for dx in range(3))
     got = np.stack([unpack_outputs(o, lay, engine=eng) for o in outs], axis=1)
     assert np.max(np.abs(got - ref.reshape(4, 4, 64))) < TOL
+
+
+@pytest.mark.slow
+def test_cfg3_carry_plan_every_layer_bit_exact_vs_oracle_replay():
+    """The exact path bench.py times -- config 3 at full size, inputs encrypted at
+    min_input_level (9 limbs), run_cnn's fused carry plan on the kernels the bench
+    launches (tcgen05 conv1 tiles with pooled 3-component squares, tcgen05 conv2 +
+    5-component GAP sums, 5-component relinearisation dropping 6 primes, dense) --
+    compared layer by layer with the oracle:
+      * conv layers: every limb of 24 sampled evaluation points of EVERY output
+        ciphertext, replayed from the encrypted inputs by the oracle's element-wise
+        operations (oracle_nets.carry_plan_convs_sampled on Oracle.coeff_view; the
+        same replay decrypts to the reference's two-block CNN in test_golden.py);
+      * relinearisation: full polynomials, oc_relin_rescale_n on the GPU's GAP sums;
+      * dense head: full polynomials, the oracle lincomb on the GPU's relinearised sums;
+    and the logits decrypt to the float64 forward pass within 1e-3."""
+    import torch
+
+    import oracle as O
+    import oracle_nets as ON
+    from paper_2604_16834_b200 import configs
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.featuremajor import dense_csr, min_input_level, run_cnn
+    from paper_2604_16834_b200.packing import pack_features
+
+    spec = configs.CNN3
+    wts = spec.make_weights(11)
+    rng = np.random.default_rng(17)
+    images = rng.uniform(0.0, 1.0, size=(32768, 3 * 32 * 32))
+    eng = GpuEngine(configs.context(3, seed=9))
+    orc = oracle_for("cfg3", seed=9)
+    level = min_input_level(eng, spec)
+    assert level == 8
+    x = pack_features(eng, images, level=level)
+    idx = np.unique(np.concatenate([[0, eng.N - 1], rng.choice(eng.N, 22, replace=False)]))
+    tidx = torch.as_tensor(idx, device=eng.device)
+
+    def samp(cts):
+        return torch.stack([c.data.index_select(-1, tidx) for c in cts]).cpu().numpy().view(np.uint64)
+
+    xs = samp(x)
+    rec = {"block0": {}, "scales": {}}
+
+    def trace(stage, cts, info):
+        if stage == "block" and info["blk"] == 0:
+            rows = info["rows"]
+            nr, Wo = len(rows) // 2, 16
+            s = samp(cts)
+            for o in range(16):
+                for r in range(nr):
+                    for xx in range(Wo):
+                        rec["block0"][o * 256 + (rows[0] // 2 + r) * Wo + xx] = s[(o * nr + r) * Wo + xx]
+            rec["scales"]["block0"] = cts[0].scale
+            assert all(c.level == level for c in cts) and eng._ncomp(cts) == 3
+        elif stage == "planar":
+            # decode the documented layout [limb][N/8][y][x][component][byte plane][8 coeffs][16 channels]
+            pc = cts
+            assert (pc.channels, pc.H, pc.W, pc.level) == (16, 16, 16, level)
+            d = pc.data.view(pc.limbs, eng.N // 8, 16, 16, 3, 5, 8, 16)
+            ch, jj = torch.as_tensor(idx // 8, device=eng.device), torch.as_tensor(idx % 8, device=eng.device)
+            t = d[:, ch, :, :, :, :, jj, :].to(torch.int64)           # [S][limb][y][x][comp][plane][channel]
+            v = sum(t[:, :, :, :, :, k] << (8 * k) for k in range(5))  # [S][limb][y][x][comp][channel]
+            v = v.permute(5, 2, 3, 4, 1, 0).reshape(4096, 3, pc.limbs, len(idx))
+            v = v.cpu().numpy().view(np.uint64)
+            for k in range(4096):
+                rec["block0"][k] = v[k]
+            rec["scales"]["block0"] = pc.scale
+            rec["planar"] = True
+        elif stage in ("gap", "relin", "dense"):
+            rec[stage] = ([to_np(c.data) for c in cts], [c.scale for c in cts], info)
+
+    out = run_cnn(eng, x, spec, wts, trace=trace)
+    view = orc.coeff_view(len(idx))
+    b0, s0, gap, sg, drops = ON.carry_plan_convs_sampled(view, orc.moduli, orc.scale, list(xs), eng.context.scale,
+                                                         spec, wts)
+    # conv1 + square + pool (3-component carry, planar layout on the tcgen05 path), every output
+    assert rec.get("planar"), "the bench path carries conv1's squares in the planar layout"
+    assert len(rec["block0"]) == len(b0) == 4096
+    assert rec["scales"]["block0"] == s0
+    for k in range(4096):
+        assert np.array_equal(rec["block0"][k], b0[k]), ("block0", k)
+    # conv2 + square + GAP (5 components), every output ciphertext
+    g_gpu, g_sc, g_info = rec["gap"]
+    assert g_info["drops"] == drops == 6 and len(g_gpu) == len(gap) == 32
+    for k in range(32):
+        assert g_sc[k] == sg
+        assert np.array_equal(g_gpu[k][..., idx], gap[k]), ("gap", k)
+    # 5-component relinearisation + joint ModDown over P u {6 dropped primes}
+    keys = [orc.switch_key(O.power_key_elt(k)) for k in (2, 3, 4)]
+    r_gpu, r_sc, _ = rec["relin"]
+    for k in (0, 13, 31):
+        assert np.array_equal(r_gpu[k], orc.relin_rescale_n(g_gpu[k], keys, drops)), ("relin", k)
+    # dense head (lincomb + rescale + bias) on the GPU's relinearised sums
+    rp, cols = dense_csr(10, 32)
+    ref = ON.lincomb(orc, [ON.OracleCts(r, s) for r, s in zip(r_gpu, r_sc)], rp, cols, wts.dense[0].reshape(-1),
+                     bias=np.asarray(wts.dense[1], np.float64), out_scale=eng.context.scale)
+    d_gpu, d_sc, _ = rec["dense"]
+    for k in range(10):
+        assert d_sc[k] == ref[k].scale and np.array_equal(d_gpu[k], ref[k].data), ("dense", k)
+    got = eng.decrypt_batch(out).T
+    want = spec.forward_plain(wts, images[:256].reshape(256, 3, 32, 32))
+    assert np.max(np.abs(got[:256] - want)) < TOL
