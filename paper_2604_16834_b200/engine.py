@@ -680,6 +680,27 @@ class GpuEngine:
         self._acct.bump("adds", len(A))
         return self._add_batch(A, B)
 
+    def add_inplace(self, A: Sequence[CipherVec], B: Sequence[CipherVec]) -> None:
+        """A[i] += B[i] (mod q) in place: accumulators of partial sums (sharded_cnn).
+        Equal levels, scales and component counts; B is left untouched."""
+        for c in list(A) + list(B):
+            self._check(c)
+        if len(A) != len(B):
+            raise ShapeMismatch(f"add_inplace: {len(A)} accumulators, {len(B)} addends")
+        if not A:
+            return
+        level = A[0].level
+        nc = self._ncomp(list(A) + list(B))
+        for a, b in zip(A, B):
+            if a.level != level or b.level != level:
+                raise HebatchError("add_inplace needs one level")
+            if abs(a.scale / b.scale - 1.0) > SCALE_RTOL:
+                raise ScaleMismatch(f"scales {a.scale:.6g} and {b.scale:.6g} differ")
+        self._acct.bump("adds", len(A))
+        pa, pb = self._ptrs(A), self._ptrs(B)
+        _lib.check(self._L.he_add(self._h, _lib.addr(pa), _lib.addr(pb), _lib.addr(pa), len(A), level + 1, nc,
+                                  self.stream), "add_inplace")
+
     def add_plain(self, a: CipherVec, p: PlainVec) -> CipherVec:
         self._check(a)
         v = self._check_plain(p)

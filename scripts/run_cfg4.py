@@ -4,10 +4,11 @@ sharding over the ranks of one node (sharded_cnn.run_cnn_sharded over NCCL).
     python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 \
         --master-port 29511 scripts/run_cfg4.py [--hw 32] [--samples 32768]
 
-Prints one JSON line on rank 0: samples/s (device time, max over ranks) and the
-decrypt error of the first 64 samples against the float64 forward pass.  The full
-32x32 map needs >= 2 GPUs (config 4's first activation map alone is ~330 GB); use
---hw 8 on a single GPU.
+Prints one JSON line on rank 0: samples/s (device time, max over ranks), the peak
+HBM held by torch on rank 0, and the decrypt error of the first 64 samples against
+the float64 forward pass.  The network is streamed over image rows, so the full
+32x32 maps run on one GPU (inputs encrypted at sharded_cnn.plan_input_level: 15 of
+the 24 limbs).
 """
 import argparse
 import json
@@ -23,6 +24,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--hw", type=int, default=32)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--tile-rows", type=int, default=2)
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -38,7 +40,7 @@ def main():
     from paper_2604_16834_b200.engine import GpuEngine
     from paper_2604_16834_b200.featuremajor import CnnSpec
     from paper_2604_16834_b200.packing import pack_features
-    from paper_2604_16834_b200.sharded_cnn import TorchRing, run_cnn_sharded
+    from paper_2604_16834_b200.sharded_cnn import TorchRing, plan_input_level, run_cnn_sharded
     from paper_2604_16834_b200.sharding import max_over_ranks
 
     base = configs.CNN4
@@ -48,14 +50,17 @@ def main():
     n = eng.context.n
     rng = np.random.default_rng(args.seed)
     images = rng.uniform(0.0, 1.0, size=(n, 3 * args.hw * args.hw))
-    x = pack_features(eng, images)                     # replicated layer-0 input
+    level = plan_input_level(spec)
+    x = pack_features(eng, images, level=level)        # replicated layer-0 input
     eng._ensure_relin()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.reset_peak_memory_stats()
+    eng.enable_timing(True)
     e0.record()
-    out = run_cnn_sharded(eng, x, spec, wts, rank, world, ring=TorchRing(rank, world))
+    out = run_cnn_sharded(eng, x, spec, wts, rank, world, ring=TorchRing(rank, world), tile_rows=args.tile_rows)
     e1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world, device="cuda")
@@ -64,7 +69,9 @@ def main():
     if rank == 0:
         print(json.dumps({"config": f"cfg4 CNN {base.channels} on {args.hw}x{args.hw}", "n_gpus": world,
                           "samples": n, "ms": ms, "samples_per_s": n / (ms / 1e3),
-                          "max_abs_err_64": float(np.max(np.abs(got - ref))),
+                          "max_abs_err_64": float(np.max(np.abs(got - ref))), "input_limbs": level + 1,
+                          "peak_hbm_gb_rank0": torch.cuda.max_memory_allocated() / 1e9,
+                          "tile_rows": args.tile_rows, "ms_by_category": {k: [v[0], round(v[1], 1)] for k, v in eng.timing_summary().items()},
                           "parallelism": f"output-channel shards x{world}, ring exchange"}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

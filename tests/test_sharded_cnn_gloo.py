@@ -86,3 +86,58 @@ def test_sharded_cnn_over_gloo(world):
     for rank, got, live in res:
         assert np.max(np.abs(got - ref)) < 1e-9, rank
         assert live == 0, rank
+
+
+def test_window_groups_equal_full_map_groups():
+    """conv3x3_window_groups over a row window == featuremajor.conv3x3_groups on
+    the full map, with column indices translated into the window."""
+    from paper_2604_16834_b200.featuremajor import conv3x3_groups
+    from paper_2604_16834_b200.sharded_cnn import conv3x3_window_groups
+
+    p, H, W = 3, 8, 6
+    for r0, r1 in [(0, 2), (2, 4), (6, 8), (3, 4), (0, 8)]:
+        ya, yb = max(0, r0 - 1), min(H, r1 + 1)
+        tp, col, tap, n = conv3x3_groups(p, H, W, range(r0, r1))
+        wtp, wcol, wtap, wn = conv3x3_window_groups(p, H, W, r0, r1, ya, yb)
+        assert n == wn and np.array_equal(tp, wtp) and np.array_equal(tap, wtap)
+        i, rest = col // (H * W), col % (H * W)
+        y, x = rest // W, rest % W
+        assert np.array_equal(wcol, i * (yb - ya) * W + (y - ya) * W + x)
+    with pytest.raises(ValueError):
+        conv3x3_window_groups(p, H, W, 2, 4, 2, 5)   # row 1 missing
+
+
+def test_streamed_rows_bound_resident_ciphertexts():
+    """Row streaming: on a 24x4, three-block network the peak number of live
+    ciphertexts stays well below one full activation map, and the result still
+    equals the float64 forward pass for every tile size."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from toy_engine import ToyEngine
+
+    from paper_2604_16834_b200.sharded_cnn import run_cnn_sharded
+
+    spec = CnnSpec(channels=(2, 4, 4, 3), H=24, W=4, act=Activation((0.5, 0.5, 0.0, 0.0625)), pool_after=(1, 2))
+    wts = spec.make_weights(9)
+    imgs = np.random.default_rng(4).uniform(0.0, 1.0, size=(5, 2, 24, 4))
+    ref = spec.forward_plain(wts, imgs)
+    for tile in (1, 2, 4):
+        eng = ToyEngine(5)
+        peak = [0]
+        ct0 = eng._ct
+
+        def _ct(*a, **k):
+            c = ct0(*a, **k)
+            peak[0] = max(peak[0], eng.live)
+            return c
+
+        eng._ct = _ct
+        x = eng.encrypt_batch(imgs.reshape(5, -1).T)
+        out = run_cnn_sharded(eng, x, spec, wts, 0, 1, tile_rows=tile)
+        got = np.stack(eng.decrypt_batch(out)).T
+        eng.release(*out)
+        assert np.max(np.abs(got - ref)) < 1e-9, tile
+        assert eng.live == 0
+        inputs, full_map = 2 * 24 * 4, 4 * 24 * 4   # block 1's whole output map: 384 ciphertexts
+        assert peak[0] - inputs < full_map, (tile, peak[0])   # windows + one tile's temporaries only
