@@ -44,6 +44,9 @@ def _args():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=None, help="(ncu) run exactly this many network passes")
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg2"],
+                    help="cfg3: the CNN (default line); cfg2: only the config-2 primitive microbenchmark")
+    ap.add_argument("--no-primitives", action="store_true", help="skip the config-2 primitives in the cfg3 line")
     return ap.parse_args()
 
 
@@ -177,27 +180,147 @@ def _traffic():
 
 
 def run_reference(args, rank, world):
+    """The reference arm (rank 0 only): the CPU RNS-CKKS oracle port (oracle/,
+    C + OpenMP on every host thread) replaying the GPU's config-3 plan on a
+    bounded sample per step, extrapolated to one 32768-sample group with the
+    exact op counts -- ``ms_per_step`` is the MEASURED wall time of a step's
+    sample and ``extrapolation_factor`` says how far it is scaled.  The reference
+    package itself (hebatch.SimulatorEngine from baseline/_ref, float64 slots
+    without cryptography) is timed once on the same network
+    and reported beside it as ``reference_simulator``."""
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import cpu_baseline
 
     t = time.perf_counter()
-    # each "step" = one bounded oracle sample, extrapolated to one group
-    vals = []
-    for _ in range(max(1, args.steps)):
-        r = cpu_baseline.measure()
-        vals.append(r["samples_per_s"])
-    v = float(sorted(vals)[len(vals) // 2])
+    runs = [cpu_baseline.measure() for _ in range(max(1, args.steps))]
+    r = sorted(runs, key=lambda x: x["samples_per_s"])[len(runs) // 2]
+    v = float(r["samples_per_s"])
+    wall_ms = 1e3 * sum(x["wall_s"] for x in runs) / len(runs)
+    sim = None
+    sys.path.insert(0, os.path.join(ROOT, "baseline"))
+    import ref_simulator
+
+    why = ref_simulator.available()
+    if why is None:
+        s = ref_simulator.measure()
+        sim = {"value": s["samples_per_s"], "unit": "samples/s", "cores": s["threads"], "kind": "reference",
+               "measured_s": s["measured_s"], "extrapolation_factor": s["extrapolation_factor"],
+               "layers": s["layers"], "sample": s["sample"]}
+    else:
+        sim = {"unavailable": why}
     line = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * SAMPLES_PER_GROUP / v, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": wall_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic",
             "config": _config(1, input_limbs=cpu_baseline.ELL), "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": r["threads"], "kind": "port",
-                             "sample": r["sample"]},
+                             "sample": r["sample"], "measured_wall_s_per_step": wall_ms / 1e3,
+                             "extrapolation_factor": r["extrapolation_factor"]},
+            "reference_simulator": sim,
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.perf_counter() - t}
     print(json.dumps(line), flush=True)
+
+
+def primitives_cfg2(device: int = 0, cts: int = 256, reps: int = 5) -> dict:
+    """BASELINE.json configs[1]: N = 2^16, 24 x 50-bit Q limbs + 4 x 50-bit P (dnum 6),
+    256 ciphertexts of uniform residues (seeded).  Times forward / inverse NTT, the
+    relinearisation key switch, rotation by +1 and +1024 (and both hoisted), and
+    rescale 24 -> 23 over all ciphertexts with CUDA events on the launching stream
+    (2 warm-up launches each).  Rooflines: algorithmic bytes against the measured HBM
+    copy bandwidth; algorithmic modular products (butterflies, BConv and inner-product
+    MACs) against the faster measured modular-product rate (FP64
+    fmulmod; every config-2 prime is < 2^50).  Reference ops:
+    /root/reference/pkg/src/hebatch/engine.py:276-313.  Bit-exactness of every op
+    vs the CPU oracle: tests/test_gpu_parity.py on the cfg2 ring."""
+    import numpy as np
+    import torch
+
+    from paper_2604_16834_b200 import _lib, configs
+    from paper_2604_16834_b200.engine import GpuEngine
+
+    eng = GpuEngine(configs.context(2, seed=7, device=device))
+    L, N, B = eng.context.n_q, eng.N, cts
+    K = len(eng.context.p_chain_bits)
+    dev = eng.device
+    x = torch.empty((B, 2, L, N), dtype=torch.int64, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1)
+    for i, q in enumerate(eng.moduli[:L]):
+        x[:, :, i] = torch.randint(0, q, (B, 2, N), generator=g, device=dev, dtype=torch.int64)
+    out = torch.empty_like(x)
+    out2 = torch.empty((2 * B, 2, L, N), dtype=torch.int64, device=dev)
+    out_rs = torch.empty((B, 2, L - 1, N), dtype=torch.int64, device=dev)
+    Lb = eng._L
+    eng._ensure_relin()
+    g1, g1024 = pow(5, 1, 2 * N), pow(5, 1024, 2 * N)
+    for gg in (g1, g1024):
+        _lib.check(Lb.he_gen_switch_key(eng._h, gg, None))
+    torch.cuda.synchronize()
+
+    def ptr(t, off=0):
+        return _lib.ptr_array([t.data_ptr() + i * t.stride(0) * 8 + off for i in range(t.shape[0])])
+
+    px, po, prs, po2 = ptr(x), ptr(out), ptr(out_rs), ptr(out2)
+    pc1, po1 = ptr(x, L * N * 8), ptr(out, L * N * 8)
+    gpair = np.array([g1, g1024], np.uint32)
+    work = x.clone()
+    s, A = eng.stream, _lib.addr
+    ops = {
+        "ntt_fwd": lambda: Lb.he_ntt(eng._h, work.data_ptr(), 2 * B, L, 0, s),
+        "ntt_inv": lambda: Lb.he_ntt(eng._h, work.data_ptr(), 2 * B, L, 1, s),
+        "keyswitch_relin": lambda: Lb.he_keyswitch(eng._h, 0, A(pc1), A(po), A(po1), B, L, s),
+        "rotate_1": lambda: Lb.he_rotate(eng._h, g1, A(px), A(po), B, L, s),
+        "rotate_1024": lambda: Lb.he_rotate(eng._h, g1024, A(px), A(po), B, L, s),
+        "rescale": lambda: Lb.he_rescale(eng._h, A(px), A(prs), B, L, 2, s),
+        "rotate_1_and_1024_hoisted": lambda: Lb.he_rotate_hoisted(eng._h, A(gpair), 2, A(px), A(po2), B, L, s),
+    }
+    beta = -(-L // eng.context.alpha)
+    poly = L * N * 8
+    key = 2 * beta * (L + K) * N * 8
+    alg_bytes = {"ntt_fwd": 2 * B * 2 * poly, "ntt_inv": 2 * B * 2 * poly,
+                 "keyswitch_relin": B * 3 * poly + key, "rotate_1": B * 4 * poly + key,
+                 "rotate_1024": B * 4 * poly + key, "rescale": B * (2 * poly + 2 * (L - 1) * N * 8),
+                 "rotate_1_and_1024_hoisted": B * 6 * poly + 2 * key}
+    digits = [min(eng.context.alpha, L - j * eng.context.alpha) for j in range(beta)]
+    bfly = (N // 2) * 16
+
+    def ks_modmuls(ell):
+        ext = ell + K
+        n_ntt = ell + sum(ext - a for a in digits) + 2 * K + 2 * ell
+        return n_ntt * bfly + (sum(a * (ext - a) for a in digits) + 2 * K * ell + 2 * beta * ext) * N
+
+    modmuls = {"ntt_fwd": 2 * B * L * bfly, "ntt_inv": 2 * B * L * bfly, "keyswitch_relin": B * ks_modmuls(L),
+               "rotate_1": B * ks_modmuls(L), "rotate_1024": B * ks_modmuls(L), "rescale": B * 2 * L * bfly,
+               "rotate_1_and_1024_hoisted": 2 * B * ks_modmuls(L)}
+    hbm, hbm_kind = _peaks()
+    fp = np.zeros(1)
+    _lib.check(Lb.he_microbench_fp64(eng.context.device, fp.ctypes.data), "microbench")
+    res = {}
+    for name, fn in ops.items():
+        for _ in range(2):
+            _lib.check(fn(), name)
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            _lib.check(fn(), name)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = alg_bytes[name] / (ms * 1e6)
+        rate = modmuls[name] / (ms * 1e-3)
+        res[name] = {"ms": round(ms, 3), "hbm": {"achieved_GBps": round(gbs, 1), "frac": round(gbs / hbm, 3)},
+                     "modmul": {"achieved_per_s": rate, "frac": round(rate / float(fp[0]), 3)}}
+    del x, out, out2, out_rs, work
+    eng.trim()
+    return {"workload": "cfg2 primitives: N=2^16, 24x50 + 4x50-bit primes, dnum 6, %d uniform ciphertexts" % B,
+            "reps": reps, "ops": res, "peaks": {"hbm_GBps": hbm, "hbm_kind": hbm_kind,
+                                                 "fp64_modmul_per_s": float(fp[0])},
+            "parity": "bit-exact vs the CPU oracle: tests/test_gpu_parity.py (cfg2 ring: ntt, keyswitch, "
+                      "rescale, mult_ct, rotate, rotate_hoisted)"}
 
 
 def main():
@@ -211,6 +334,10 @@ def main():
     import torch
 
     torch.cuda.set_device(local)
+    if args.workload == "cfg2":
+        if rank == 0:
+            print(json.dumps(primitives_cfg2(local)), flush=True)
+        return
     if world > 1:
         import torch.distributed as dist
 
@@ -400,6 +527,10 @@ def main():
     peaks_measured = {"imma_int8_TOPs": peak_tops, "mac128_per_s": float(ip[1]), "fp64_modmul_per_s": float(fp[0]),
                       "imad32_per_s": float(ip[0]), "hbm_GBps": peak}
 
+    prim = None
+    if rank == 0 and not args.no_primitives:            # after every timed region: config-2 primitives
+        eng.trim()
+        prim = primitives_cfg2(local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -407,7 +538,15 @@ def main():
 
         r = cpu_baseline.measure()
         cpu = {"value": r["samples_per_s"], "unit": "samples/s", "cores": r["threads"], "kind": "port",
-               "sample": r["sample"]}
+               "sample": r["sample"], "measured_wall_s": r["wall_s"], "extrapolation_factor": r["extrapolation_factor"]}
+        sys.path.insert(0, os.path.join(ROOT, "baseline"))
+        import ref_simulator
+
+        if ref_simulator.available() is None:
+            s = ref_simulator.measure()
+            cpu["reference_simulator"] = {"value": s["samples_per_s"], "cores": 1, "kind": "reference",
+                                          "measured_s": s["measured_s"],
+                                          "extrapolation_factor": s["extrapolation_factor"]}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
@@ -425,6 +564,7 @@ def main():
             "breakdown": breakdown,
             "peaks_measured": peaks_measured,
             "cpu_baseline": cpu,
+            "primitives_cfg2": prim,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

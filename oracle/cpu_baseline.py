@@ -51,6 +51,7 @@ def cfg3_op_counts(ell: int = ELL):
 def measure(seconds_budget: float = 20.0, threads: int | None = None, seed: int = 0, ell: int = ELL) -> dict:
     """Time the oracle on a bounded sample; returns samples/s for one 32768-sample group."""
     threads = threads or len(os.sched_getaffinity(0))
+    wall0 = time.perf_counter()
     orc = O.Oracle(16, [40] * 14, [42] * 3, 3, seed=seed, scale=2.0 ** 40)
     rng = np.random.default_rng(seed)
     N = orc.N
@@ -100,6 +101,8 @@ def measure(seconds_budget: float = 20.0, threads: int | None = None, seed: int 
     total += sum(cnt * per_rs for cnt, _ in ops["rescale"])
     res["group_seconds_extrapolated"] = total
     res["samples_per_s"] = 32768.0 / total
+    res["wall_s"] = time.perf_counter() - wall0          # the measured sample (incl. key generation)
+    res["extrapolation_factor"] = total / res["wall_s"]
     res["sample"] = (f"oracle on {threads} host threads running the GPU's plan at {ell} limbs: {n_out}x{k}-term "
                      f"lincomb, {threads} five-component relinearisations with a joint 6-limb ModDown, {threads} "
                      f"rescales at {ell - 6} limbs, {threads} tensor products; extrapolated with the exact config-3 op "

@@ -329,6 +329,18 @@ class _Ledger:
             return OpCounters(peak_live_ciphertexts=self.peak, **self.counts)
 
 
+def _storage_uses(t) -> int:
+    """References to ``t``'s storage (tensors and views sharing it + the
+    temporary wrapper).  Uses torch's storage use count when this torch build
+    exposes it; otherwise reports every cached batch as in use (no slab reuse:
+    correct, only slower)."""
+    torch = _torch()
+    f = getattr(torch._C, "_storage_Use_Count", None)
+    if f is None:
+        return 1 << 30
+    return f(t.untyped_storage()._cdata)
+
+
 def _torch():
     import torch
 
@@ -442,12 +454,16 @@ class GpuEngine:
             # cached batch and the temporary storage wrapper.  Reuse is stream-ordered
             # like torch's own allocator (every op runs on the current stream).
             for t in self._slab.get(shape, ()):
-                if torch._C._storage_Use_Count(t.untyped_storage()._cdata) == 2:
+                if _storage_uses(t) == 2:
                     return t
         try:
             t = torch.empty(shape, dtype=torch.int64, device=self.device)
         except torch.OutOfMemoryError:
+            # drop the cached batches and hand the pool's unused pages back, so a
+            # large request is not refused for want of one contiguous free range
             self.trim()
+            torch.cuda.synchronize(self.device)
+            torch.cuda.empty_cache()
             t = torch.empty(shape, dtype=torch.int64, device=self.device)
         if big:
             self._slab.setdefault(shape, []).append(t)
@@ -455,9 +471,8 @@ class GpuEngine:
 
     def trim(self) -> None:
         """Return the engine's cached (released) ciphertext batches to the pool."""
-        torch = _torch()
         for shape in list(self._slab):
-            keep = [t for t in self._slab[shape] if torch._C._storage_Use_Count(t.untyped_storage()._cdata) > 2]
+            keep = [t for t in self._slab[shape] if _storage_uses(t) > 2]
             if keep:
                 self._slab[shape] = keep
             else:

@@ -175,7 +175,8 @@ class _BlockStage:
 
     replicated = False
 
-    def __init__(self, engine, up, w, bias, act, fold, pool, H, W, rank, world, ring, tile_rows, trace, blk):
+    def __init__(self, engine, up, w, bias, act, fold, pool, H, W, rank, world, ring, tile_rows, trace, blk,
+                 max_outputs=512):
         self.engine, self.up = engine, up
         self.q, self.p = w.shape[:2]
         self.mine = list(channel_shards(self.q, world)[rank])
@@ -190,6 +191,7 @@ class _BlockStage:
         R = max(1, int(tile_rows))
         self.R = R + (R % 2) if pool else R
         self.trace, self.blk = trace, blk
+        self.max_outputs = max_outputs
         self.rows = {}
         self.done = 0          # conv rows produced so far
         self.released = 0      # output rows below this index are freed
@@ -252,38 +254,45 @@ class _BlockStage:
                                     "weights": self.wm})
         del local
         self.up.release_below(r1 - 1)          # rows below r1 - 1 are not read by later tiles
-        z = eng.rescale_batch(acc, out_scale=s_out)
-        eng.release(*acc)
-        nr = r1 - r0
-        if np.any(self.bias != 0):
-            zb = eng.add_const_batch(z, np.repeat(self.bias, nr * W))
+        nr, nq = r1 - r0, len(self.mine)
+        Wo, nro, y0 = (W // 2, nr // 2, r0 // 2) if self.pool else (W, nr, r0)
+        outs = [None] * (nq * nro * Wo)
+        # rescale, bias, activation and pool in chunks of output channels: the
+        # activation holds three or four batches of its inputs' size at once, which
+        # bounds one tile's temporaries to ~max_outputs ciphertexts per batch
+        cc = max(1, self.max_outputs // (nr * W))
+        for c0 in range(0, nq, cc):
+            c1 = min(nq, c0 + cc)
+            a_ch = acc[c0 * nr * W:c1 * nr * W]
+            z = eng.rescale_batch(a_ch, out_scale=s_out)
+            eng.release(*a_ch)
+            if np.any(self.bias[c0:c1] != 0):
+                zb = eng.add_const_batch(z, np.repeat(self.bias[c0:c1], nr * W))
+                eng.release(*z)
+                z = zb
+            y = apply_activation(eng, z, self.act, lazy=False)
+            if self.trace is not None:
+                self.trace("act", y, {"blk": self.blk, "rows": (r0, r1), "pre": z, "channels": (c0, c1)})
             eng.release(*z)
-            z = zb
-        y = apply_activation(eng, z, self.act, lazy=False)
-        if self.trace is not None:
-            self.trace("act", y, {"blk": self.blk, "rows": (r0, r1), "pre": z})
-        eng.release(*z)
-        if self.pool:
-            rp, cols = pool2x2_csr(len(self.mine), nr, W)
-            yp = eng.lincomb_int(y, rp, cols, np.ones(len(cols), np.int64), out_scale=4.0 * y[0].scale)
-            eng.release(*y)
-            y, nr, Wo = yp, nr // 2, W // 2
-            y0 = r0 // 2
-        else:
-            Wo, y0 = W, r0
-        nq = len(self.mine)
-        for r in range(nr):
-            self.rows[y0 + r] = [y[(o * nr + r) * Wo + x] for o in range(nq) for x in range(Wo)]
+            if self.pool:
+                rp, cols = pool2x2_csr(c1 - c0, nr, W)
+                yp = eng.lincomb_int(y, rp, cols, np.ones(len(cols), np.int64), out_scale=4.0 * y[0].scale)
+                eng.release(*y)
+                y = yp
+            outs[c0 * nro * Wo:c1 * nro * Wo] = y
+        for r in range(nro):
+            self.rows[y0 + r] = [outs[(o * nro + r) * Wo + x] for o in range(nq) for x in range(Wo)]
         self.done = r1
 
 
 def run_cnn_sharded(engine, x_cts, spec, wts, rank: int, world: int, ring=None, release_inputs: bool = True,
-                    tile_rows: int = 2, trace=None):
+                    tile_rows: int = 2, trace=None, max_outputs: int = 512):
     """Encrypted forward pass of ``spec`` with output channels sharded over
     ``world`` ranks, streamed over image rows (module docstring).
 
     x_cts: the C0*H*W input ciphertexts (channel-major), replicated on every rank.
-    ``tile_rows``: conv rows per tile (even for pooled blocks).  ``trace``
+    ``tile_rows``: conv rows per tile (even for pooled blocks); ``max_outputs``:
+    ciphertexts per batch of a tile's rescale / activation / pool.  ``trace``
     (tests): trace(stage, cts, info) with stage "acc" (a tile's exact conv sums
     before the rescale), "act" (the activation outputs, info["pre"] its inputs),
     "gap" and "dense".  Returns the n_classes output ciphertexts on every rank."""
@@ -297,7 +306,8 @@ def run_cnn_sharded(engine, x_cts, spec, wts, rank: int, world: int, ring=None, 
         # (as run_cnn: a pool right before the GAP is skipped -- GAP of the pooled
         # sums is the same sum over every pixel)
         pool = blk in spec.pool_after and blk != nblk - 1
-        st = _BlockStage(engine, src, w, bias, spec.act, fold, pool, H, W, rank, world, ring, tile_rows, trace, blk)
+        st = _BlockStage(engine, src, w, bias, spec.act, fold, pool, H, W, rank, world, ring, tile_rows, trace, blk,
+                         max_outputs)
         stages.append(st)
         src = st
         if pool:

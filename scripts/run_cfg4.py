@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--hw", type=int, default=32)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--tile-rows", type=int, default=2)
+    ap.add_argument("--mem-trace", action="store_true", help="print HBM use at every tile")
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -60,7 +61,14 @@ def main():
     torch.cuda.reset_peak_memory_stats()
     eng.enable_timing(True)
     e0.record()
-    out = run_cnn_sharded(eng, x, spec, wts, rank, world, ring=TorchRing(rank, world), tile_rows=args.tile_rows)
+    def mem_trace(stage, cts, info):
+        free, total = torch.cuda.mem_get_info()
+        print(f"{stage} blk {info.get('blk')} rows {info.get('rows')} ch {info.get('channels')}: torch alloc "
+              f"{torch.cuda.memory_allocated() / 1e9:.1f} GB, device used {(total - free) / 1e9:.1f} GB, "
+              f"slab {sum(t.numel() * 8 for v in eng._slab.values() for t in v) / 1e9:.1f} GB", flush=True)
+
+    out = run_cnn_sharded(eng, x, spec, wts, rank, world, ring=TorchRing(rank, world), tile_rows=args.tile_rows,
+                          trace=mem_trace if args.mem_trace else None)
     e1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world, device="cuda")

@@ -81,8 +81,9 @@ def test_cfg4_full_shape_streamed_layerwise_bit_exact_vs_oracle():
                                      full0=to_np(cts[5].data), out_scale=cts[0].scale)
         else:  # act
             pre = info["pre"]
+            assert info["channels"][0] == 0
             rec[("act", blk)] = dict(pre=to_np(pre[5].data), pre_scale=pre[5].scale, y=to_np(cts[5].data),
-                                     y_scale=cts[5].scale, ys=samp(cts), n=len(cts))
+                                     y_scale=cts[5].scale, ys=samp(cts), n=len(cts), chans=info["channels"])
 
     out = run_cnn_sharded(eng, x, spec, wts, 0, 1, trace=trace)
     assert len(out) == 10
@@ -125,7 +126,7 @@ def test_cfg4_full_shape_streamed_layerwise_bit_exact_vs_oracle():
         if blk in (1, 3) and blk + 1 < 4:
             nxt = rec[("acc", blk + 1)]
             ys, Wc = C["ys"], Wb
-            for o in range(q):
+            for o in range(C["chans"][1]):   # the first channel chunk of the tile
                 for xo in range(Wc // 2):
                     four = [ys[(o * 2 + dy) * Wc + 2 * xo + dx] for dy in (0, 1) for dx in (0, 1)]
                     s = four[0]
