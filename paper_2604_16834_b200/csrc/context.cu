@@ -144,6 +144,7 @@ int he_scratch_alloc(void **p, size_t bytes, cudaStream_t s) {
     if (bytes == 0) bytes = 8;
     cudaError_t e = cudaMallocAsync(p, bytes, s);
     if (e != cudaSuccess) {
+        (void)cudaGetLastError();  // not sticky: clear it so the caller can free memory and retry
         he_set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
         return HE_ENOMEM;
     }

@@ -413,12 +413,19 @@ class GpuEngine:
         """Run one C-ABI call; with timing on, bracket it with CUDA events.
         ``units`` = (algorithmic HBM bytes, algorithmic modular MACs)."""
         if self._timing is None:
-            return fn(*args)
+            rc = fn(*args)
+            if rc == _lib.HE_ENOMEM:   # the library's scratch did not fit: return parked batches, once
+                self._release_pool()
+                rc = fn(*args)
+            return rc
         torch = _torch()
         st = torch.cuda.current_stream(self.device)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(st)
         rc = fn(*args)
+        if rc == _lib.HE_ENOMEM:
+            self._release_pool()
+            rc = fn(*args)
         e.record(st)
         self._timing.setdefault(cat, []).append((s, e, units))
         return rc
@@ -444,6 +451,11 @@ class GpuEngine:
     # (the pool remaps physical pages into a new virtual range), which a pass
     # started right after a device synchronize cannot hide.
     SLAB_MIN_BYTES = 1 << 30
+    # At most this many bytes of FREE cached batches are kept when a new batch
+    # shape is allocated (a pass whose shapes vary -- the row-streamed config-4
+    # runner -- would otherwise park released batches of every shape it ever
+    # used; the library's own scratch comes from the same pool).
+    SLAB_FREE_CAP = 16 << 30
 
     def _alloc(self, count: int, n_comp: int, limbs: int):
         torch = _torch()
@@ -456,18 +468,37 @@ class GpuEngine:
             for t in self._slab.get(shape, ()):
                 if _storage_uses(t) == 2:
                     return t
+            self._cap_free_slabs()
         try:
             t = torch.empty(shape, dtype=torch.int64, device=self.device)
         except torch.OutOfMemoryError:
             # drop the cached batches and hand the pool's unused pages back, so a
             # large request is not refused for want of one contiguous free range
-            self.trim()
-            torch.cuda.synchronize(self.device)
-            torch.cuda.empty_cache()
+            self._release_pool()
             t = torch.empty(shape, dtype=torch.int64, device=self.device)
         if big:
             self._slab.setdefault(shape, []).append(t)
         return t
+
+    def _cap_free_slabs(self) -> None:
+        """Drop free cached batches (largest first) until at most SLAB_FREE_CAP bytes stay parked."""
+        free = [(t.numel() * 8, shape, t) for shape, ts in self._slab.items() for t in ts if _storage_uses(t) == 2]
+        total = sum(b for b, _, _ in free)
+        for b, shape, t in sorted(free, key=lambda x: -x[0]):
+            if total <= self.SLAB_FREE_CAP:
+                break
+            self._slab[shape] = [u for u in self._slab[shape] if u is not t]
+            if not self._slab[shape]:
+                del self._slab[shape]
+            total -= b
+
+    def _release_pool(self) -> None:
+        """Drop the cached batches and hand the pool's unused pages back to the
+        device, so a large request is not refused for want of one free range."""
+        torch = _torch()
+        self.trim()
+        torch.cuda.synchronize(self.device)
+        torch.cuda.empty_cache()
 
     def trim(self) -> None:
         """Return the engine's cached (released) ciphertext batches to the pool."""
