@@ -149,8 +149,11 @@ class _InputRows:
 
     replicated = True
 
-    def __init__(self, cts, p, H, W):
-        self.cts, self.p, self.H, self.W = list(cts), p, H, W
+    def __init__(self, cts, p, H, W, engine=None):
+        """``engine``: release input rows as soon as no later tile reads them
+        (run_cnn_sharded(release_inputs=True)); None keeps them for the caller."""
+        self.cts, self.p, self.H, self.W, self.engine = list(cts), p, H, W, engine
+        self.released = 0
 
     def ensure(self, upto):
         pass
@@ -161,10 +164,16 @@ class _InputRows:
         return [self.cts[i * H * W + y * W + x] for i in range(self.p) for y in range(ya, yb) for x in range(W)]
 
     def release_below(self, y):
-        pass
+        if self.engine is None:
+            return
+        H, W = self.H, self.W
+        for r in range(self.released, min(y, H)):
+            self.engine.release(*[self.cts[i * H * W + r * W + x] for i in range(self.p) for x in range(W)])
+        self.released = max(self.released, min(y, H))
 
     def release_all(self, engine):
-        engine.release(*self.cts)
+        if self.engine is not None:
+            self.release_below(self.H)
         self.cts = []
 
 
@@ -300,7 +309,7 @@ def run_cnn_sharded(engine, x_cts, spec, wts, rank: int, world: int, ring=None, 
     H, W = spec.H, spec.W
     fold = spec.act.fold()
     nblk = len(wts.convs)
-    src = _InputRows(x_cts, wts.convs[0][0].shape[1], H, W)
+    src = _InputRows(x_cts, wts.convs[0][0].shape[1], H, W, engine if release_inputs else None)
     stages = []
     for blk, (w, bias) in enumerate(wts.convs):
         # (as run_cnn: a pool right before the GAP is skipped -- GAP of the pooled
@@ -326,8 +335,7 @@ def run_cnn_sharded(engine, x_cts, spec, wts, rank: int, world: int, ring=None, 
         last.release_below(y + 1)
     for st in stages:
         st.release_all(engine)
-    if release_inputs:
-        stages[0].up.release_all(engine)
+    stages[0].up.release_all(engine)
     q = wts.convs[-1][0].shape[0]
     if world > 1:
         shards = channel_shards(q, world)
