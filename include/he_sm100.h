@@ -81,6 +81,11 @@ int he_has_switch_key(const he_ctx *ctx, uint32_t galois_elt);
 /* copies (canonical form) for parity tests: sk [L+K][N]; key [dnum][2][L+K][N] */
 int he_export_secret_key(he_ctx *ctx, uint64_t *dev_out, void *stream);
 int he_export_switch_key(he_ctx *ctx, uint32_t galois_elt, uint64_t *dev_out, void *stream);
+/* install a key received over the wire (canonical residues, he_export_switch_key's
+ * layout; residues >= q are rejected with HE_EINVAL).  The server side of the
+ * client/server threat model evaluates with imported keys and
+ * never holds the client's secret key.  Replaces an existing key of that code. */
+int he_import_switch_key(he_ctx *ctx, uint32_t galois_elt, const uint64_t *dev_in, void *stream);
 
 /* batched NTT / INTT over data [batch][ell][N]; limb i uses Q-prime i. */
 int he_ntt(he_ctx *ctx, uint64_t *data, int batch, int ell, int inverse, void *stream);
@@ -262,6 +267,8 @@ int he_microbench_tc5(int device, int n, double *rates);
 /* the same with the A operand's 8-row groups a_sbo bytes apart and its K chunks
  * a_lbo bytes apart (pixel-strided conv rings) */
 int he_microbench_tc5_strided(int device, int n, int a_sbo, int a_lbo, double *rates);
+/* the same with the MMAs rotating over ndst disjoint TMEM accumulators (independent chains) */
+int he_microbench_tc5_indep(int device, int n, int ndst, double *rates);
 /* The fused conv + square + pool / global-sum layer on the 5th-generation
  * tensor cores (tcgen05.mma kind::i8, TMEM accumulators, warp-specialised
  * producer / MMA / epilogue; csrc/convtc.cu).  Same arguments and results as

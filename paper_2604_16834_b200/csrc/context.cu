@@ -659,6 +659,53 @@ extern "C" int he_export_switch_key(he_ctx *c, uint32_t g, uint64_t *dev_out, vo
     return HE_OK;
 }
 
+// canonical residues -> Montgomery form (x 2^64 mod q = redc(x r2)); flags any residue >= q
+__global__ void k_to_mont(uint64_t *out, const uint64_t *in, const ModConst *mc, int N, int M, size_t total,
+                          int *bad) {
+    size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    const ModConst &c = mc[(idx / N) % M];
+    const uint64_t x = in[idx];
+    if (x >= c.q) atomicOr(bad, 1);
+    out[idx] = redc(mulhi(x, c.r2), x * c.r2, c.q, c.qinv);
+}
+
+// Install an evaluation key received over the wire (canonical residues, layout of
+// he_export_switch_key).  The server side of the threat model
+// holds evaluation keys but never the secret key.
+extern "C" int he_import_switch_key(he_ctx *c, uint32_t g, const uint64_t *dev_in, void *stream) {
+    if (!c || !dev_in) return HE_EINVAL;
+    if (g % 2 == 0 ? g > 4 : g >= 2u * (uint32_t)c->N) {
+        he_set_error("key code %u: galois elements are odd and < 2N, power keys are 0, 2, 4", g);
+        return HE_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t tot = (size_t)c->dnum * 2 * (c->L + c->K) * c->N;
+    uint64_t *key = nullptr;
+    int *bad = nullptr, hbad = 0;
+    if (cudaMalloc(&key, tot * 8) != cudaSuccess) {
+        (void)cudaGetLastError();
+        he_set_error("cudaMalloc switch key (%zu MB) failed", tot * 8 >> 20);
+        return HE_ENOMEM;
+    }
+    HE_TRY(he_scratch_alloc((void **)&bad, sizeof(int), s));
+    HE_CHECK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    k_to_mont<<<ceil_div(tot, 256), 256, 0, s>>>(key, dev_in, c->d_mc, c->N, c->L + c->K, tot, bad);
+    HE_CHECK_LAUNCH();
+    HE_CHECK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    he_scratch_free(bad, s);
+    HE_CHECK_CUDA(cudaStreamSynchronize(s));
+    if (hbad) {
+        cudaFree(key);
+        he_set_error("imported key %u holds residues outside [0, q)", g);
+        return HE_EINVAL;
+    }
+    he_drop_switch_key(c, g);  // replaces an existing key (and its hoisting key)
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->keys[g] = key;
+    return HE_OK;
+}
+
 extern "C" int he_sync(void *stream) {
     HE_CHECK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     return HE_OK;

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(128, 1) k_tc5_selftest(int N, int layout, int3
 constexpr int BK = 256;  // throughput probe: K bytes resident (8 K steps)
 
 __global__ void __launch_bounds__(128, 1) k_tc5_rate(int N, int iters, unsigned long long *cyc, uint32_t a_sbo,
-                                                     uint32_t a_lbo, int abytes) {
+                                                     uint32_t a_lbo, int abytes, int ndst) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t bar;
     __shared__ uint32_t taddr_s;
@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(128, 1) k_tc5_rate(int N, int iters, unsigned 
         for (int it = 0; it < iters; it++)
 #pragma unroll
             for (int t = 0; t < BK / 32; t++)
-                tc5::mma_i8(taddr, tc5::sdesc(sa + 2 * t * a_lbo, a_lbo, a_sbo),
-                            tc5::sdesc(sb + 2 * t * b_lbo, b_lbo, 128), idesc, (it | t) != 0);
+                tc5::mma_i8(taddr + (uint32_t)((t % ndst) * N), tc5::sdesc(sa + 2 * t * a_lbo, a_lbo, a_sbo),
+                            tc5::sdesc(sb + 2 * t * b_lbo, b_lbo, 128), idesc, it != 0);
         tc5::tc_commit(&bar);
         tc5::mbar_wait(&bar, 0);
         if (blockIdx.x == 0) *cyc = clock64() - t0;
@@ -142,14 +142,18 @@ extern "C" int he_tc5_selftest(int device, int n, int layout, int32_t *d_out) {
 // rates[0] = int8 MAC/s over all SMs, rates[1] = cycles per MMA (M=128, N=n, K=32) on one SM.
 // a_sbo = 0: A contiguous (8-row groups 128 B apart); else the A operand's 8-row groups sit
 // a_sbo bytes apart and its K chunks a_lbo bytes apart (the conv kernels' pixel-strided rings).
-static int tc5_rate(int device, int n, uint32_t a_sbo, uint32_t a_lbo, double *rates);
+// ndst: the MMAs rotate over ndst disjoint accumulators (ndst = 1: one dependent chain)
+static int tc5_rate(int device, int n, uint32_t a_sbo, uint32_t a_lbo, double *rates, int ndst = 1);
 extern "C" int he_microbench_tc5(int device, int n, double *rates) { return tc5_rate(device, n, 0, 0, rates); }
 extern "C" int he_microbench_tc5_strided(int device, int n, int a_sbo, int a_lbo, double *rates) {
     return tc5_rate(device, n, (uint32_t)a_sbo, (uint32_t)a_lbo, rates);
 }
-static int tc5_rate(int device, int n, uint32_t a_sbo, uint32_t a_lbo, double *rates) {
-    if (n < 16 || n > 256 || n % 16 || !rates) {
-        he_set_error("he_microbench_tc5: N must be a multiple of 16 in [16, 256]");
+extern "C" int he_microbench_tc5_indep(int device, int n, int ndst, double *rates) {
+    return tc5_rate(device, n, 0, 0, rates, ndst);
+}
+static int tc5_rate(int device, int n, uint32_t a_sbo, uint32_t a_lbo, double *rates, int ndst) {
+    if (n < 16 || n > 256 || n % 16 || !rates || ndst < 1 || ndst > BK / 32 || ndst * n > 256) {
+        he_set_error("he_microbench_tc5: N must be a multiple of 16 in [16, 256], ndst * N <= 256, ndst <= 8");
         return HE_EINVAL;
     }
     HE_CHECK_CUDA(cudaSetDevice(device));
@@ -176,7 +180,7 @@ static int tc5_rate(int device, int n, uint32_t a_sbo, uint32_t a_lbo, double *r
     float ms = 0;
     for (int rep = 0; rep < 2; rep++) {
         cudaEventRecord(e0);
-        k_tc5_rate<<<sms, 128, smem>>>(n, iters, cyc, a_sbo, a_lbo, abytes);
+        k_tc5_rate<<<sms, 128, smem>>>(n, iters, cyc, a_sbo, a_lbo, abytes, ndst);
         cudaEventRecord(e1);
         HE_CHECK_CUDA(cudaEventSynchronize(e1));
     }

@@ -386,6 +386,7 @@ class GpuEngine:
         self._enc_lock = threading.Lock()
         self.registration_log: list[frozenset] = []
         self._relin = False
+        self._dnum = -(-context.n_q // context.alpha)  # key-switch digits (key layout [dnum][2][L+K][N])
         self._timing = None  # {category: [(start_event, end_event, units)]} when enabled
         self._slab: dict = {}  # shape -> cached ciphertext batches (see _alloc)
         # exact int8-digit tensor-core convolutions (he_conv_mma); False = CUDA-core kernel

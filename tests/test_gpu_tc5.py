@@ -51,3 +51,7 @@ def test_tc5_rate_report():
         _lib.check(lib.he_microbench_tc5(0, n, r.ctypes.data), "he_microbench_tc5")
         print(f"tcgen05 kind::i8 M=128 N={n}: {r[0] / 1e12:.1f} TMAC/s, {r[1]:.1f} cycles/MMA")
         assert r[0] > 0
+        for nd in (2, 4, 8):
+            if nd * n <= 256:
+                _lib.check(lib.he_microbench_tc5_indep(0, n, nd, r.ctypes.data), "he_microbench_tc5_indep")
+                print(f"  {nd} independent accumulators: {r[0] / 1e12:.1f} TMAC/s, {r[1]:.1f} cycles/MMA")

@@ -232,3 +232,45 @@ def test_align_inputs_hoisted_path_matches_rotation_path():
     assert plain.rot == hoisted.rot == 8
     for key in a:
         assert np.array_equal(a[key].data, b[key].data), key
+
+
+def test_accumulator_eq29_on_slot_engine():
+    """Eq. 29: g compacted blocks land in slots [i*sts', (i+1)*sts') of one
+    ciphertext (SPEC.md:435-442 examples), inputs consumed incrementally; the
+    stride-2 compaction + accumulator pipeline equals the concatenation of the
+    compacted images; OccupancyOverflow / MissingRotationKey before any work."""
+    from paper_2604_16834_b200.conv import Accumulator, accumulate, accumulator_offsets
+    from paper_2604_16834_b200.errors import OccupancyOverflow
+
+    n = 64
+    eng = SlotEngine(n, max_level=30)
+    blocks = [np.arange(4, dtype=float) + 10 * (i + 1) for i in range(4)]
+    cts = [eng.encrypt(np.concatenate([b, np.full(n - 4, 7.0)])) for b in blocks]   # junk beyond sts'
+    with pytest.raises(MissingRotationKey):
+        accumulate(eng, cts, 4)
+    eng.register_rotation_keys(accumulator_offsets(4, 4, n))
+    assert accumulator_offsets(4, 4, n) == frozenset({60, 56, 52})
+    out = accumulate(eng, cts, 4).data
+    want = np.zeros(n)
+    want[:16] = np.concatenate(blocks)
+    assert np.array_equal(out, want)                      # [A|B|C|D], junk masked away
+    assert accumulate(eng, [eng.encrypt(np.arange(n, dtype=float))], 8).data[:8].tolist() == list(range(8))
+    with pytest.raises(OccupancyOverflow):
+        Accumulator(eng, 5, 16)
+    # compaction of 4 stride-2 tiles (2 images of 4x4 each), then the accumulator: effective batch x4
+    lay = PackingLayout(n=n, H=4, W=4, b=2)
+    eng.register_rotation_keys(compaction_offsets(lay))
+    sts_p = lay.b * (lay.H // 2) * (lay.W // 2)          # 8 slots after compaction
+    eng.register_rotation_keys(accumulator_offsets(4, sts_p, n))
+    rng = np.random.default_rng(5)
+    tiles = [np.concatenate([rng.uniform(size=32), np.zeros(32)]) for _ in range(4)]
+    acc = Accumulator(eng, 4, sts_p)
+    for t in tiles:
+        acc.add(compact_strided(eng, eng.encrypt(t), lay))
+    got = acc.result().data
+    for i, t in enumerate(tiles):
+        for j in range(2):
+            for y in range(2):
+                for x in range(2):
+                    assert got[i * sts_p + j * 4 + y * 2 + x] == t[j * 16 + 2 * y * 4 + 2 * x]
+    assert not got[4 * sts_p:].any()
