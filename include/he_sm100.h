@@ -269,6 +269,9 @@ int he_microbench_tc5(int device, int n, double *rates);
 int he_microbench_tc5_strided(int device, int n, int a_sbo, int a_lbo, double *rates);
 /* the same with the MMAs rotating over ndst disjoint TMEM accumulators (independent chains) */
 int he_microbench_tc5_indep(int device, int n, int ndst, double *rates);
+/* TMEM read throughput: rates[0] = bytes per cycle per SM with `warps` warps loading
+ * 32x32b.x{cols} (cols 4, 8, 16), rates[1] = cycles */
+int he_microbench_tmem_ld(int device, int warps, int cols, double *rates);
 /* The fused conv + square + pool / global-sum layer on the 5th-generation
  * tensor cores (tcgen05.mma kind::i8, TMEM accumulators, warp-specialised
  * producer / MMA / epilogue; csrc/convtc.cu).  Same arguments and results as

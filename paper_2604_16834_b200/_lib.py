@@ -40,6 +40,7 @@ EXPORTS = [
     "he_microbench_tc5",
     "he_microbench_tc5_strided",
     "he_microbench_tc5_indep",
+    "he_microbench_tmem_ld",
     "he_conv_square_sum_tc",
     "he_set_conv_tc",
     "he_convtc_profile",
@@ -128,6 +129,7 @@ def load():
         "he_microbench_tc5": (i, [i, i, vp]),
         "he_microbench_tc5_strided": (i, [i, i, i, i, vp]),
         "he_microbench_tc5_indep": (i, [i, i, i, vp]),
+        "he_microbench_tmem_ld": (i, [i, i, i, vp]),
         "he_conv_square_sum_tc": (i, [vp, vp, i, i, i, i, vp, i, i, i, i, vp, vp, vp, i, vp]),
         "he_set_conv_tc": (i, [i]),
         "he_convtc_profile": (i, [i, vp]),

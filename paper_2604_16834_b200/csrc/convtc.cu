@@ -41,6 +41,7 @@
 
 namespace convtc {
 
+constexpr int P1_NCOL = 128;     // P1 MMA N: 4 channel groups x 32 columns (NSH x 4 used)
 constexpr int NB = 5;            // byte planes of a 40-bit residue
 constexpr int EPI_WARPS = 16;    // warps 0-15: four per TMEM lane quarter, CPT channels each
 constexpr int CPT = 4;           // output channels per epilogue thread
@@ -147,7 +148,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
     constexpr int NCI = 2;
     using LY = P1Layout<NCI>;
     constexpr int PS = LY::PS, RR = LY::RR;
-    constexpr int NCOL = NSH * MC;  // MMA N
+    // MMA N = 128: column block cg*32 + s*4 + mm holds shift sum s of channel 4 cg + mm, so
+    // an epilogue thread's NSH x 4 sums are contiguous (one x16 + one x8/x4 TMEM load)
+    constexpr int NCOL = P1_NCOL;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar_full[RR], bar_empty[RR], bar_dfull[NSLOT], bar_dempty[NSLOT], bar_b;
     __shared__ uint32_t taddr_s;
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
         // ======================= epilogue
         const int qd = warp & 3, cg = warp >> 2;  // TMEM lane quarter, channel group (CPT channels)
         const int row = qd * 32 + lane, xl = row >> 3, j = row & 7;
-        const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(cg * CPT);
+        const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(cg * 32);
         const int par = xl & 1;  // window partners (x, x+1) split the stores: par 0 -> comps 0, 2; par 1 -> comp 1
         int k = 0, S = 0;
         for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
@@ -344,14 +347,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                             tc5::tc_fence_after();
                             int C[CPT][NSH];
                             const uint32_t ta = tq + (uint32_t)ds * 128;
-#pragma unroll
-                            for (int s2 = 0; s2 < NSH; s2++) {
-                                uint32_t r[4];
-                                tc5::tld4(ta + s2 * 16, r);
-#pragma unroll
-                                for (int m = 0; m < CPT; m++) C[m][s2] = (int)r[m];
-                            }
+                            uint32_t r0[16], r1[8], r2[4];
+                            tc5::tld16(ta, r0);
+                            if constexpr (NSH >= 6) tc5::tld8(ta + 16, r1);
+                            if constexpr (NSH == 5) tc5::tld4(ta + 16, r2);
+                            if constexpr (NSH == 7) tc5::tld4(ta + 24, r2);
                             tc5::tld_wait();
+#pragma unroll
+                            for (int s2 = 0; s2 < NSH; s2++)
+#pragma unroll
+                                for (int m = 0; m < CPT; m++)
+                                    C[m][s2] = (int)(s2 < 4 ? r0[s2 * 4 + m]
+                                                     : NSH == 5 ? r2[m]
+                                                     : s2 < 6 ? r1[(s2 - 4) * 4 + m] : r2[m]);
                             tc5::tc_fence_before();
                             tc5::mbar_arrive(&bar_dempty[ds]);
 #pragma unroll
@@ -387,13 +395,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                                       ((((size_t)l * nchunk + (size_t)(item % nchunk)) * H2 + y2) * W2 + x2) * (3 * 5 * 128) +
                                       j * 16 + cg * CPT + 2 * par;
 #pragma unroll
-                        for (int s2 = 0; s2 < 3; s2++)
+                        for (int s2 = 0; s2 < 3; s2++) {
+                            // byte d of both channels -> one 16-bit store per byte plane (one PRMT each)
+                            const uint32_t al = (uint32_t)v[0][s2], ah = (uint32_t)(v[0][s2] >> 32);
+                            const uint32_t bl = (uint32_t)v[1][s2], bh = (uint32_t)(v[1][s2] >> 32);
 #pragma unroll
                             for (int d = 0; d < 5; d++) {
-                                const unsigned short u = (unsigned short)(((v[0][s2] >> (8 * d)) & 0xFF) |
-                                                                          (((v[1][s2] >> (8 * d)) & 0xFF) << 8));
-                                *(unsigned short *)(pb + (s2 * 5 + d) * 128) = u;
+                                const uint32_t u = d < 4 ? __byte_perm(al, bl, 0x0040 + 0x0011 * d)
+                                                         : __byte_perm(ah, bh, 0x0040);
+                                *(unsigned short *)(pb + (s2 * 5 + d) * 128) = (unsigned short)u;
                             }
+                        }
                     } else
 #pragma unroll
                     for (int h = 0; h < 2; h++) {
@@ -845,9 +857,9 @@ inline int digit_s8(int64_t w, int e) {
 using namespace convtc;
 
 // B tiles of the P1 packing: tile t (0..5) = K step t; tile 5 = K step 3 with its two taps swapped.
-// Tile layout (K-major, no swizzle): [chunk k][row group n/8][8 rows x 16 bytes], row n = s * 16 + m.
+// Tile layout (K-major, no swizzle): [chunk k][row group n/8][8 rows x 16 bytes], row n = (m / 4) * 32 + s * 4 + m % 4 (P1_NCOL columns, s < NSH).
 static void build_btiles_p1(const int64_t *weights, int M, int p, int E, int NSH, std::vector<uint8_t> &bt) {
-    const int NCOL = NSH * MC, TB = NCOL * 32;
+    const int NCOL = P1_NCOL, TB = NCOL * 32;
     // taps (dy, dx) of the two chunks of each K step; (-1,-1) = zero chunk
     const int ks[6][2][2] = {{{0, 0}, {0, 1}}, {{1, 0}, {1, 1}}, {{2, 0}, {2, 1}},
                              {{0, 2}, {1, 2}}, {{2, 2}, {-1, -1}}, {{1, 2}, {0, 2}}};
@@ -858,8 +870,9 @@ static void build_btiles_p1(const int64_t *weights, int M, int p, int E, int NSH
             if (dy < 0) continue;
             const int tap = dy * 3 + dx;
             for (int n = 0; n < NCOL; n++) {
-                const int s = n / MC, m = n % MC;
-                if (m >= M) continue;
+                // column block cg*32 + s*4 + mm: shift s of channel m = 4 cg + mm (s >= NSH: zero)
+                const int s = (n % 32) / 4, m = (n / 32) * 4 + n % 4;
+                if (m >= M || s >= NSH) continue;
                 for (int kb = 0; kb < 15; kb++) {
                     const int i = kb / 5, d = kb % 5, e = s - d;
                     if (i >= p || e < 0 || e >= E) continue;
@@ -967,7 +980,7 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
         build_btiles_p16(weights, M, p, bt);
     else
         build_btiles_p1(weights, M, p, E, NSH, bt);
-    const int TB = p16 ? P16Layout::TB : NSH * MC * 32;
+    const int TB = p16 ? P16Layout::TB : P1_NCOL * 32;
     std::vector<double> biasd((size_t)2 * MC * ell, 0.0), yc(ell);
     for (int l = 0; l < ell; l++) {
         const uint64_t q = c->mod[l];

@@ -123,7 +123,76 @@ __global__ void __launch_bounds__(128, 1) k_tc5_rate(int N, int iters, unsigned 
     if (warp == 0) tc5::tmem_free<256>(taddr);
 }
 
+// TMEM -> register read throughput: `warps` warps each load `cols` consecutive columns of
+// their lane quarter (32x32b.x{cols}) per iteration, waiting after every `batch` loads
+template <int COLS>
+__global__ void k_tmem_ld_rate(int iters, int batch, unsigned long long *cyc, uint32_t *sink) {
+    __shared__ uint32_t taddr_s;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) tc5::tmem_alloc<512>(&taddr_s);
+    tc5::tc_fence_before();
+    __syncthreads();
+    tc5::tc_fence_after();
+    const uint32_t t0 = taddr_s + ((uint32_t)((warp & 3) * 32) << 16);
+    uint32_t acc = 0;
+    __syncthreads();
+    const unsigned long long c0 = clock64();
+    for (int it = 0; it < iters; it++) {
+        uint32_t r[COLS];
+        for (int b = 0; b < batch; b++) {
+            const uint32_t a = t0 + (uint32_t)(((it * batch + b) * COLS + (warp >> 2) * 8) & 511 & ~(COLS - 1));
+            if constexpr (COLS == 4) {
+                uint32_t (&rr)[4] = *reinterpret_cast<uint32_t(*)[4]>(r);
+                tc5::tld4(a, rr);
+            } else if constexpr (COLS == 8) {
+                uint32_t (&rr)[8] = *reinterpret_cast<uint32_t(*)[8]>(r);
+                tc5::tld8(a, rr);
+            } else {
+                uint32_t (&rr)[16] = *reinterpret_cast<uint32_t(*)[16]>(r);
+                tc5::tld16(a, rr);
+            }
+            tc5::tld_wait();
+#pragma unroll
+            for (int k = 0; k < COLS; k++) acc += r[k];
+        }
+    }
+    __syncthreads();
+    const unsigned long long c1 = clock64();
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = c1 - c0;
+    if (acc == 0x12345678u) *sink = acc;
+    tc5::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tc5::tmem_free<512>(taddr_s);
+}
+
 }  // namespace
+
+// rates[0] = bytes / cycle / SM read from TMEM by `warps` warps (32x32b.x{cols}), rates[1] = cycles
+extern "C" int he_microbench_tmem_ld(int device, int warps, int cols, double *rates) {
+    if (!rates || warps < 4 || warps > 32 || warps % 4 || (cols != 4 && cols != 8 && cols != 16)) {
+        he_set_error("he_microbench_tmem_ld: warps in {4..32} (multiple of 4), cols in {4, 8, 16}");
+        return HE_EINVAL;
+    }
+    HE_CHECK_CUDA(cudaSetDevice(device));
+    unsigned long long *cyc;
+    uint32_t *sink;
+    HE_CHECK_CUDA(cudaMalloc(&cyc, 8));
+    HE_CHECK_CUDA(cudaMalloc(&sink, 4));
+    const int iters = 2048, batch = 4;
+    for (int rep = 0; rep < 2; rep++) {
+        if (cols == 4) k_tmem_ld_rate<4><<<1, warps * 32>>>(iters, batch, cyc, sink);
+        else if (cols == 8) k_tmem_ld_rate<8><<<1, warps * 32>>>(iters, batch, cyc, sink);
+        else k_tmem_ld_rate<16><<<1, warps * 32>>>(iters, batch, cyc, sink);
+        HE_CHECK_CUDA(cudaDeviceSynchronize());
+    }
+    unsigned long long c = 0;
+    HE_CHECK_CUDA(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
+    rates[0] = (double)warps * 32 * 4 * cols * iters * batch / (double)c;
+    rates[1] = (double)c;
+    cudaFree(cyc);
+    cudaFree(sink);
+    return HE_OK;
+}
 
 extern "C" int he_tc5_selftest(int device, int n, int layout, int32_t *d_out) {
     if (n < 16 || n > 256 || n % 16 || (layout != 0 && layout != 1) || !d_out) {

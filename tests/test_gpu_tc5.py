@@ -55,3 +55,15 @@ def test_tc5_rate_report():
             if nd * n <= 256:
                 _lib.check(lib.he_microbench_tc5_indep(0, n, nd, r.ctypes.data), "he_microbench_tc5_indep")
                 print(f"  {nd} independent accumulators: {r[0] / 1e12:.1f} TMAC/s, {r[1]:.1f} cycles/MMA")
+
+
+def test_tmem_read_rate_report():
+    from paper_2604_16834_b200 import _lib
+
+    lib = _lib.load()
+    for warps in (4, 8, 16, 32):
+        for cols in (4, 8, 16):
+            r = np.zeros(2)
+            _lib.check(lib.he_microbench_tmem_ld(0, warps, cols, r.ctypes.data), "he_microbench_tmem_ld")
+            print(f"TMEM read {warps} warps 32x32b.x{cols}: {r[0]:.1f} B/cycle/SM")
+            assert r[0] > 0

@@ -56,7 +56,8 @@ def test_wire_client_server_roundtrip(name):
     with pytest.raises(ContextMismatch):
         import_ciphertexts(other, blob)
     bad = bytearray(blob)
-    bad[-1] = 0xFF                                                           # top byte of a residue
+    w = (client.moduli[client.context.n_q - 1].bit_length() + 7) // 8
+    bad[-w:] = b"\xff" * w                                                  # last residue := 2^(8w) - 1 >= q
     with pytest.raises(HebatchError):
         import_ciphertexts(server, bytes(bad))
     torch.cuda.synchronize()
