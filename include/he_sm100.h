@@ -113,6 +113,10 @@ int he_decrypt_coeffs(he_ctx *ctx, const uint64_t *const *cts, int count, int el
  * (PlainVec encoding inside mult_plain / add_plain, engine.py:291-304). */
 int he_encode_plain(he_ctx *ctx, const double *vals, int nvals, double scale, int ell,
                     uint64_t *pt_out, void *stream);
+/* he_encode_plain for `count` vectors at once: vals [count][nvals] (device),
+ * pt_out [count][ell][N] (contiguous); one FFT and one NTT launch sequence. */
+int he_encode_plain_batch(he_ctx *ctx, const double *vals, int count, int nvals, double scale, int ell,
+                          uint64_t *pt_out, void *stream);
 
 /* element-wise.  add/sub: engine.py:285-289.  add_const: add_plain with a
  * constant over the occupied span (engine.py:291-295, conv.py:160-166);
@@ -189,6 +193,16 @@ int he_gen_hoist_key(he_ctx *ctx, uint32_t galois_elt, void *stream);
 int he_lincomb(he_ctx *ctx, const uint64_t *const *in, int n_in, uint64_t *const *out, int n_out,
                const int32_t *row_ptr, const int32_t *col, const int64_t *w, int ell, int n_comp,
                void *stream);
+
+/* the batched channel-by-channel conv fold (conv_forward k=3, conv.py:137-156):
+ *   out[o] = sum_{j < n_in} in[j] (.) pts[o * n_in + j]      (element-wise, mod q_i)
+ * in: n_in 2-component ciphertexts (the tap-aligned inputs); pts: n_out * n_in
+ * encoded plaintexts [ell][N] (NTT domain); out: n_out 2-component ciphertexts.
+ * Exact 128-bit accumulation, one reduction per value; NOT rescaled (call
+ * he_rescale once per output).  n_in <= 1024; primes above 2^52 bound n_in by
+ * n_in q^2 < 2^128. */
+int he_lincomb_plain(he_ctx *ctx, const uint64_t *const *in, int n_in, const uint64_t *const *pts,
+                     uint64_t *const *out, int n_out, int ell, void *stream);
 
 /* grouped form of he_lincomb for feature-major convolutions: every group g
  * (an output pixel) shares one input gather and feeds M outputs:

@@ -1,3 +1,4 @@
+#include <vector>
 // encode.cu -- canonical-embedding encode/decode, encryption and decryption.
 //
 // Replaces SimulatorEngine.encrypt / decrypt (engine.py:257-268) and the
@@ -410,6 +411,28 @@ extern "C" int he_encode_plain(he_ctx *c, const double *vals, int nvals, double 
     HE_TRY(he_upload_ptrs((const void *const *)h, 1, (void ***)&ptrs.p, s));
     HE_TRY(encode_into(c, vals, 1, nvals, scale, (uint64_t *const *)ptrs.p, ell, 0, 0, s));
     HE_TRY(he_ntt_fwd(c, pt_out, ell, c->d_ident, ell, s));
+    return HE_OK;
+}
+
+// count full-width plaintexts at once: vals [count][nvals] (device), pt_out [count][ell][N]
+extern "C" int he_encode_plain_batch(he_ctx *c, const double *vals, int count, int nvals, double scale, int ell,
+                                     uint64_t *pt_out, void *stream) {
+    if (!c || count < 0 || nvals < 0 || ell < 1 || ell > c->L || !pt_out || !(scale > 0)) {
+        he_set_error("he_encode_plain_batch: bad arguments");
+        return HE_EINVAL;
+    }
+    if (nvals > c->nslots) {
+        he_set_error("%d values > %d slots", nvals, c->nslots);
+        return HE_ELENGTH;
+    }
+    if (!count) return HE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<const uint64_t *> h(count);
+    for (int i = 0; i < count; i++) h[i] = pt_out + (size_t)i * ell * c->N;
+    Buf ptrs(s);
+    HE_TRY(he_upload_ptrs((const void *const *)h.data(), count, (void ***)&ptrs.p, s));
+    HE_TRY(encode_into(c, vals, count, nvals, scale, (uint64_t *const *)ptrs.p, ell, 0, 0, s));
+    HE_TRY(he_ntt_fwd(c, pt_out, count * ell, c->d_ident, ell, s));
     return HE_OK;
 }
 

@@ -1231,6 +1231,55 @@ class GpuEngine:
         self._acct.bump("adds", int(len(tc)) * M)
         return self._wrap_batch(out, out_limbs - 1, [s_out] * n_out)
 
+    # plaintext bytes one he_lincomb_plain launch may hold (larger folds are split over outputs)
+    PLAIN_CHUNK_BYTES = 4 << 30
+
+    def lincomb_plain(self, inputs: Sequence[CipherVec], plains, n_out: int) -> list[CipherVec]:
+        """The batched channel-by-channel fold (conv.py:137-156 as one kernel):
+        out[o] = rescale(sum_j inputs[j] (.) encode(plains[o, j], q_last)) for
+        full-width float64 plaintext slot vectors plains [n_out][n_in][<= n].
+        Every plaintext is encoded at q_last exactly as mult_plain encodes it
+        (he_encode_plain_batch), the products are summed exactly
+        (he_lincomb_plain) and each output is rescaled ONCE, so the output
+        scale is the input scale and the level drops by one, as for the
+        reference's per-term mult_plain + add fold.  Counters are the caller's."""
+        torch = _torch()
+        for c in inputs:
+            self._check(c)
+        self._need_two(inputs, "lincomb_plain")
+        n_in = len(inputs)
+        level, s_in = inputs[0].level, inputs[0].scale
+        if any(c.level != level or c.scale != s_in for c in inputs):
+            raise HebatchError("lincomb_plain needs inputs at one level and scale")
+        if level < self.context.mult_level_cost:
+            raise LevelExhausted(f"level {level} < multiplication cost {self.context.mult_level_cost}")
+        P = torch.as_tensor(np.asarray(plains, np.float64) if not isinstance(plains, torch.Tensor) else plains,
+                            dtype=torch.float64, device=self.device)
+        if P.dim() != 3 or P.shape[0] != n_out or P.shape[1] != n_in or P.shape[2] > self.context.n:
+            raise ShapeMismatch(f"plains {tuple(P.shape)} for {n_out} outputs x {n_in} inputs x <= {self.context.n}")
+        limbs = level + 1
+        ql = float(self.moduli[limbs - 1])
+        pin = self._ptrs(inputs)
+        acc = self._alloc(n_out, 2, limbs)
+        per_out = n_in * limbs * self.N * 8
+        step = max(1, min(n_out, self.PLAIN_CHUNK_BYTES // per_out))
+        for o0 in range(0, n_out, step):
+            o1 = min(n_out, o0 + step)
+            vals = P[o0:o1].reshape((o1 - o0) * n_in, P.shape[2]).contiguous()
+            pt = torch.empty(((o1 - o0) * n_in, limbs, self.N), dtype=torch.int64, device=self.device)
+            _lib.check(self._call("encode_plain", self._L.he_encode_plain_batch, self._h, vals.data_ptr(),
+                                  vals.shape[0], vals.shape[1], ql, limbs, pt.data_ptr(), self.stream,
+                                  units=(vals.numel() * 8.0 + pt.numel() * 8.0, 0.0)), "encode_plain_batch")
+            ppt = self._tptrs(pt)
+            pout = _lib.ptr_array([acc.data_ptr() + o * acc.stride(0) * 8 for o in range(o0, o1)])
+            poly = 2 * limbs * self.N
+            _lib.check(self._call("lincomb_plain", self._L.he_lincomb_plain, self._h, _lib.addr(pin), n_in,
+                                  _lib.addr(ppt), _lib.addr(pout), o1 - o0, limbs, self.stream,
+                                  units=(((o1 - o0) * n_in * limbs * self.N + (n_in + o1 - o0) * poly) * 8.0,
+                                         float((o1 - o0) * n_in) * poly)), "lincomb_plain")
+            del pt
+        return self._rescale_tensor(acc, limbs, [s_in] * n_out)
+
     def conv_mma(self, inputs: Sequence[CipherVec], gcol, out_base, out_stride: int, weights, n_out: int,
                  weight_scale: float, bias=None) -> list[CipherVec] | None:
         """Tensor-core (int8-digit, mma.sync) form of a deferred-rescale

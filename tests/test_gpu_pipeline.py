@@ -109,3 +109,57 @@ def test_compaction_and_accumulator_bit_exact_vs_oracle():
     assert np.max(np.abs(got - want)) < 1e-6
     c = eng.snapshot_counters()
     assert c.rotations > 0 and c.plain_mults > 0
+
+
+def test_cbc_batched_fold_bit_exact_vs_oracle_and_counters():
+    """The batched CBC 3x3 layer (conv_forward k=3 on GpuEngine: hoisted
+    alignment + ONE he_lincomb_plain fold + one rescale per output + bias):
+    limbs equal the oracle's replay of the same semantics (every product
+    oc_mul_plain, sums oc_add, oc_rescale once, bias plaintext added to c0);
+    decrypts to the direct convolution; counters advance as the reference fold's
+    (reference conv.py:137-166)."""
+    from paper_2604_16834_b200 import configs
+    from paper_2604_16834_b200.conv import ConvSpec, align_inputs, cbc_plaintexts, conv_forward, conv_keys
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.packing import PackingLayout, pack_inputs, unpack_outputs
+
+    eng = GpuEngine(configs.context(1, seed=2))
+    orc = oracle_for("cfg1", seed=2)
+    lay = PackingLayout(n=2048, H=8, W=8, b=4, p=3)
+    eng.register_rotation_keys(conv_keys(lay))
+    rng = np.random.default_rng(7)
+    imgs = [rng.uniform(-1, 1, size=(3, 8, 8)) for _ in range(4)]
+    w = rng.normal(0, 0.3, size=(4, 3, 3, 3))
+    bias = rng.normal(0, 0.1, size=4)
+    spec = ConvSpec(w, bias, lay)
+    cts = pack_inputs(eng, imgs, lay)
+    c0 = eng.snapshot_counters()
+    outs = conv_forward(eng, cts, spec)
+    c1 = eng.snapshot_counters()
+    assert c1.plain_mults - c0.plain_mults == 4 * 3 * 9
+    assert c1.adds - c0.adds == 4 * (27 - 1) + 4
+    assert c1.rotations - c0.rotations == 3 * 8
+    # oracle replay of the batched semantics on the same aligned inputs
+    taps = [(dy, dx) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
+    al = [align_inputs(eng, ct, lay) for ct in cts]
+    flat = [to_np(a[t].data) for a in al for t in taps]
+    ell = cts[0].level + 1
+    ql = float(orc.moduli[ell - 1])
+    P = cbc_plaintexts(spec)
+    for o in range(4):
+        acc = None
+        for j, a in enumerate(flat):
+            prod = orc.mul_plain(a, orc.plain_to_ntt(orc.encode(P[o, j], ql), ell))
+            acc = prod if acc is None else orc.add(acc, prod)
+        r = orc.rescale(acc)
+        bslots = np.zeros(lay.n)
+        bslots[: lay.occupied] = bias[o]
+        pt = orc.plain_to_ntt(orc.encode(bslots, cts[0].scale), ell - 1)
+        r[0] = orc.add(r[:1], pt[None])[0]
+        assert np.array_equal(to_np(outs[o].data), r), o
+    x = np.stack(imgs)
+    xp = np.pad(x, ((0, 0), (0, 0), (1, 1), (1, 1)))
+    ref = sum(np.einsum("oi,bihw->bohw", w[:, :, dy, dx], xp[:, :, dy:dy + 8, dx:dx + 8])
+              for dy in range(3) for dx in range(3)) + bias[None, :, None, None]
+    got = np.stack([unpack_outputs(o, lay, engine=eng) for o in outs], axis=1)
+    assert np.max(np.abs(got - ref.reshape(4, 4, 64))) < 1e-6
