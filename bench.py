@@ -347,9 +347,13 @@ def main():
     from paper_2604_16834_b200.featuremajor import min_input_level, run_cnn
     from paper_2604_16834_b200.packing import pack_features
 
+    from paper_2604_16834_b200.sharding import assign_groups, max_over_ranks as _max_over_ranks
+
     spec = configs.CNN3
     wts = spec.make_weights(1234)                       # same model on every rank
-    group = rank                                         # config 5: group g seeded g
+    # config 5: groups round-robin over ranks, one group per GPU per step (weak
+    # scaling, no data-path collective); group g's images are seeded g
+    (group,) = assign_groups(world, world, rank)
     # per-rank key seed: groups on different ranks never share a secret key or
     # encryption randomness (equal (seed, index) pairs would leak m - m')
     eng = GpuEngine(configs.context(3, seed=42 + 7919 * rank, device=local))
@@ -378,11 +382,7 @@ def main():
             torch.distributed.barrier()
 
     def max_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        return _max_over_ranks(v, world, device="cuda")
 
     for _ in range(args.warmup):
         step()

@@ -4,12 +4,11 @@
   each GPU evaluates the whole network on its groups.  There is no
   data-path collective -- only the max-over-ranks of the timed region and
   an optional gather of the decrypted logits at the end.
-* Output-channel ciphertexts (config 4): rank r owns a contiguous block of
-  every conv layer's output channels; the next layer needs every input
-  channel, so activations are exchanged with a chunked all-gather over
-  input-channel blocks (``allgather_chunks``).  Chunks bound the staging
-  memory: config 4's first activation map (16384 ciphertexts at >= 11 limbs)
-  cannot be replicated on one 180 GB device.
+* Output-channel ciphertexts (config 4): rank r owns the contiguous block
+  ``channel_shards(q, G)[r]`` of every conv layer's output channels; the next
+  layer needs every input channel, so sharded_cnn.py passes each tile's
+  input-row window around a ring of the ranks (the whole first activation map,
+  16384 ciphertexts at 12 limbs, could not be replicated on one device).
 
 One process per GPU; torch.distributed carries the collectives (NCCL on the
 B200 box, gloo for the CPU tests).
@@ -38,27 +37,6 @@ def channel_shards(q: int, world: int) -> list[range]:
     return out
 
 
-def allgather_chunks(n_items: int, world: int, chunk: int) -> list[list[tuple[int, range]]]:
-    """Schedule of a chunked all-gather of per-rank item blocks.
-
-    Returns rounds; round k lists, for every rank r, the slice of r's block
-    sent in that round.  Every item of every block appears exactly once."""
-    blocks = channel_shards(n_items, world)
-    rounds = []
-    k = 0
-    while True:
-        step = []
-        for r, b in enumerate(blocks):
-            lo = b.start + k * chunk
-            hi = min(b.stop, lo + chunk)
-            if lo < hi:
-                step.append((r, range(lo, hi)))
-        if not step:
-            return rounds
-        rounds.append(step)
-        k += 1
-
-
 def max_over_ranks(value: float, world: int, device=None) -> float:
     """Max of a scalar over ranks (timed regions: slowest rank defines the job)."""
     if world == 1:
@@ -82,17 +60,4 @@ def gather_group_results(local: dict, world: int) -> dict:
     out = {}
     for p in parts:
         out.update(p)
-    return out
-
-
-def allgather_tensor_blocks(block, world: int):
-    """All-gather equally sized tensor blocks (e.g. one chunk of ciphertexts,
-    int64 [items, n_comp, limbs, N]) -> [world * items, ...]."""
-    import torch
-    import torch.distributed as dist
-
-    if world == 1:
-        return block
-    out = torch.empty((world * block.shape[0],) + tuple(block.shape[1:]), dtype=block.dtype, device=block.device)
-    dist.all_gather_into_tensor(out, block.contiguous())
     return out

@@ -7,7 +7,6 @@ import socket
 
 import numpy as np
 import pytest
-import torch
 import torch.multiprocessing as mp
 
 from paper_2604_16834_b200 import sharding
@@ -20,9 +19,6 @@ def test_partitions_cover_exactly_once():
         blocks = sharding.channel_shards(n, w)
         assert [i for b in blocks for i in b] == list(range(n))
         assert max(len(b) for b in blocks) - min(len(b) for b in blocks) <= 1
-        sched = sharding.allgather_chunks(n, w, chunk=3)
-        seen = sorted(i for rnd in sched for _, rg in rnd for i in rg)
-        assert seen == list(range(n))
 
 
 def _free_port():
@@ -43,10 +39,7 @@ def _worker(rank, world, port, q):
         local = {g: np.full(4, g * 10.0 + rank) for g in groups}
         allres = sharding.gather_group_results(local, world)
         t = sharding.max_over_ranks(1.5 + rank, world)
-        # chunked all-gather of ciphertext-shaped blocks
-        blk = torch.full((3, 2, 2, 8), rank, dtype=torch.int64)
-        gathered = sharding.allgather_tensor_blocks(blk, world)
-        q.put((rank, sorted(allres), float(t), gathered[:, 0, 0, 0].tolist()))
+        q.put((rank, sorted(allres), float(t)))
     finally:
         dist.destroy_process_group()
 
@@ -62,7 +55,6 @@ def test_group_sharding_over_gloo_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, groups, t, gathered in res:
+    for rank, groups, t in res:
         assert groups == list(range(8))          # every group evaluated exactly once, visible everywhere
         assert t == 2.5                          # max over ranks
-        assert gathered == [0, 0, 0, 1, 1, 1]    # rank-ordered blocks
