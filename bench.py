@@ -47,6 +47,9 @@ def _args():
     ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg2"],
                     help="cfg3: the CNN (default line); cfg2: only the config-2 primitive microbenchmark")
     ap.add_argument("--no-primitives", action="store_true", help="skip the config-2 primitives in the cfg3 line")
+    ap.add_argument("--h2d-overlap", default="network", choices=["encrypt", "network", "serial"],
+                    help="e2e: which phase of step i the H2D copy of step i+1's images overlaps "
+                         "(serial: each step's own copy, not overlapped)")
     return ap.parse_args()
 
 
@@ -428,11 +431,16 @@ def main():
     for e in consumed:
         e.record()
 
+    during_net = args.h2d_overlap == "network"
+
     def issue_h2d(i):
+        if args.h2d_overlap == "serial":
+            return
         b = i % 2
         with torch.cuda.stream(cstream):
             cstream.wait_event(consumed[b])             # the buffer's previous encryption is done
-            cstream.wait_event(consumed[1 - b])         # and the current step's: the copy overlaps a network
+            if during_net:
+                cstream.wait_event(consumed[1 - b])     # and the current step's: the copy overlaps a network
             dev_in[b].copy_(feat_host, non_blocking=True)  # one DMA from pinned memory
             h2d_done[b].record(cstream)
 
@@ -441,11 +449,16 @@ def main():
             else (lambda: None)
         b = i % 2
         rec()
-        torch.cuda.current_stream().wait_event(h2d_done[b])
+        if args.h2d_overlap == "serial":
+            dev_in[b].copy_(feat_host, non_blocking=True)   # on the work stream, before this step's encryption
+        else:
+            torch.cuda.current_stream().wait_event(h2d_done[b])
         rec()
+        if not last and args.h2d_overlap == "encrypt":
+            issue_h2d(i + 1)       # next step's copy overlaps this step's encryption (not the network)
         cts = eng.encrypt_batch(dev_in[b], level=level)
         consumed[b].record()
-        if not last:
+        if not last and during_net:
             issue_h2d(i + 1)
         rec()
         out = run_cnn(eng, cts, spec, wts, release_inputs=True)
@@ -489,12 +502,13 @@ def main():
     #                FP64 fmulmod; config 3's primes are < 2^42: FP64)
     #   everything  : algorithmic HBM bytes against the measured copy bandwidth
     peak, peak_kind = _peaks()
-    ip, fp, im = np.zeros(2), np.zeros(1), np.zeros(1)
+    ip, fp, im, tc = np.zeros(2), np.zeros(1), np.zeros(1), np.zeros(2)
     _lib.check(_lib.load().he_microbench_intpipe(local, ip.ctypes.data), "microbench")
     _lib.check(_lib.load().he_microbench_fp64(local, fp.ctypes.data), "microbench")
     _lib.check(_lib.load().he_microbench_imma(local, im.ctypes.data), "microbench")
+    _lib.check(_lib.load().he_microbench_tc5(local, 256, tc.ctypes.data), "microbench")
     peak_mm = max(float(ip[1]), float(fp[0]))
-    peak_tops = 2.0 * float(im[0]) / 1e12
+    peak_tops = 2.0 * float(tc[0]) / 1e12                 # tcgen05 kind::i8, M=128 N=256 (the chip's int8 rate)
     traffic_all = _traffic()
     rooflines = {}
     for k, (calls, kms, units) in summ.items():
@@ -504,8 +518,13 @@ def main():
         if k == "conv_sqsum" and len(units) > 2:
             ach = 2.0 * units[2] / sec / 1e12
             r["tensor"] = {"achieved": ach, "peak": peak_tops, "unit": "TOP/s (int8)", "frac": ach / peak_tops,
-                           "peak_source": "measured: mma.sync.m16n8k32.u8.s8 (he_microbench_imma)",
-                           "frac_of_tcgen05_nominal_4500": ach / 4500.0}
+                           "peak_source": "measured: tcgen05.mma kind::i8 M=128 N=256 (he_microbench_tc5)",
+                           "frac_of_nominal_4500": ach / 4500.0}
+            if len(units) > 3:
+                fr = units[3] / sec
+                r["fp64"] = {"achieved": fr, "peak": float(fp[0]), "unit": "modmul/s", "frac": fr / float(fp[0]),
+                             "what": "epilogue FP64 modular products (recombination + window/GAP products)",
+                             "peak_source": "measured: FP64 fmulmod chain (he_microbench_fp64)"}
         elif units[1] > 0:
             ach = units[1] / sec
             r["int"] = {"achieved": ach, "peak": peak_mm, "unit": "modmul/s", "frac": ach / peak_mm,
@@ -513,18 +532,22 @@ def main():
         rooflines[k] = r
     dom_name = max(summ.items(), key=lambda kv: kv[1][1])[0]
     dom = rooflines[dom_name]
-    bind = "tensor" if "tensor" in dom else "int" if "int" in dom else "hbm"
-    roof = {"kernel": dom_name, "bound": "tensor" if bind == "tensor" else "hbm",
-            "achieved": dom[bind]["achieved"] if bind == "tensor" else dom["hbm"]["achieved"],
-            "peak": dom[bind]["peak"] if bind == "tensor" else peak,
-            "unit": dom[bind]["unit"] if bind == "tensor" else "GB/s",
-            "frac": dom[bind]["frac"] if bind == "tensor" else dom["hbm"]["frac"],
-            "traffic": traffic_all.get(dom_name), "peak_source": dom[bind].get("peak_source", peak_kind),
-            "calls": dom["calls"], "avg_ms": dom["avg_ms"], "hbm_frac": dom["hbm"]["frac"]}
+    # the dominant kernel (the fused conv) against HBM: its algorithmic bytes (inputs once +
+    # outputs once) per launch / its average launch time; its int8 tensor work and
+    # its epilogue's FP64 modular products are reported beside it against their measured peaks
+    bind = "int" if ("int" in dom and "tensor" not in dom) else "hbm"
+    roof = {"kernel": dom_name, "bound": "hbm", "achieved": dom["hbm"]["achieved"], "peak": peak, "unit": "GB/s",
+            "frac": dom["hbm"]["frac"], "traffic": traffic_all.get(dom_name), "peak_source": peak_kind,
+            "calls": dom["calls"], "avg_ms": dom["avg_ms"],
+            "algorithmic_bytes_per_launch": summ[dom_name][2][0] / summ[dom_name][0]}
+    for extra in ("tensor", "fp64"):
+        if extra in dom:
+            roof[extra] = dom[extra]
     if bind == "int":
         roof["int_pipe"] = dom["int"]
     breakdown = rooflines
-    peaks_measured = {"imma_int8_TOPs": peak_tops, "mac128_per_s": float(ip[1]), "fp64_modmul_per_s": float(fp[0]),
+    peaks_measured = {"tcgen05_int8_TOPs": peak_tops, "mma_sync_int8_TOPs": 2.0 * float(im[0]) / 1e12,
+                      "mac128_per_s": float(ip[1]), "fp64_modmul_per_s": float(fp[0]),
                       "imad32_per_s": float(ip[0]), "hbm_GBps": peak}
 
     prim = None
@@ -557,7 +580,7 @@ def main():
             "config": _config(world, input_limbs=level + 1),
             "e2e": {"value": e2e, "unit": "samples/s", "steps": e2e_steps,
                     "phase_ms_h2dwait_enc_net_dec": e2e_phases,
-                    "h2d": "double-buffered on a copy stream, overlapping the previous step's network",
+                    "h2d": f"double-buffered on a copy stream, overlapping the previous step's {args.h2d_overlap}",
                     "h2d_bytes_per_step": int(feat_host.numel() * 8),
                     "d2h_bytes_per_step": int(out_host.numel() * 8)},
             "roofline": roof,

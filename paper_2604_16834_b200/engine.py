@@ -483,7 +483,8 @@ class GpuEngine:
 
     def _cap_free_slabs(self) -> None:
         """Drop free cached batches (largest first) until at most SLAB_FREE_CAP bytes stay parked."""
-        free = [(t.numel() * 8, shape, t) for shape, ts in self._slab.items() for t in ts if _storage_uses(t) == 2]
+        free = [(t.numel() * t.element_size(), shape, t) for shape, ts in self._slab.items() for t in ts
+                if _storage_uses(t) == 2]
         total = sum(b for b, _, _ in free)
         for b, shape, t in sorted(free, key=lambda x: -x[0]):
             if total <= self.SLAB_FREE_CAP:
@@ -1407,7 +1408,10 @@ class GpuEngine:
         args = (self._h, _lib.addr(pin) if pin is not None else None, nci, p, H, W,
                 _lib.addr(pout) if pout is not None else None, M, int(bool(pool)), y0, y1, _lib.addr(wi),
                 _lib.addr(bres) if bres is not None else None, _lib.addr(cres) if cres is not None else None, limbs)
-        units = (in_b + out_b, 1.0 * nci * nnz * M * poly, i8)
+        # FP64 modular products of the epilogue: one per recombined component and one per
+        # window / GAP product (2 + 3 for 2-component inputs, 3 + 6 for 3-component inputs)
+        fmul = 1.0 * (y1 - y0) * W * M * poly * (nci + nci * (nci + 1) // 2)
+        units = (in_b + out_b, 1.0 * nci * nnz * M * poly, i8, fmul)
         if planar_in or planar_out is not None:
             rc = self._call("conv_sqsum", self._L.he_conv_square_sum_pl, *args,
                             inputs.data.data_ptr() if planar_in else None,
@@ -1433,9 +1437,27 @@ class GpuEngine:
         (filled by conv_square_sum(planar_out=...); scale set by the first fill)."""
         if channels != 16 or W != 16:
             raise ShapeMismatch("the planar carry holds 16 channels of 16-pixel rows (config 3's conv1 -> conv2)")
-        torch = _torch()
         n = (level + 1) * (self.N // 8) * H * W * PlanarCarry.BYTES_PER_PIXEL
-        return PlanarCarry(torch.empty(n, dtype=torch.uint8, device=self.device), channels, H, W, level, None, id(self))
+        return PlanarCarry(self._alloc_bytes(n), channels, H, W, level, None, id(self))
+
+    def _alloc_bytes(self, n: int):
+        """A uint8 device buffer of n bytes through the same slab cache as the
+        ciphertext batches (config 3's planar carry is 36 GB per pass)."""
+        torch = _torch()
+        shape = ("u8", n)
+        if n >= self.SLAB_MIN_BYTES:
+            for t in self._slab.get(shape, ()):
+                if _storage_uses(t) == 2:
+                    return t
+            self._cap_free_slabs()
+        try:
+            t = torch.empty(n, dtype=torch.uint8, device=self.device)
+        except torch.OutOfMemoryError:
+            self._release_pool()
+            t = torch.empty(n, dtype=torch.uint8, device=self.device)
+        if n >= self.SLAB_MIN_BYTES:
+            self._slab.setdefault(shape, []).append(t)
+        return t
 
     def planar_ok(self, p_in: int, H: int, W: int, q: int, q_next: int, level: int) -> bool:
         """Whether run_cnn's carry can go through the planar layout: conv1 on the
