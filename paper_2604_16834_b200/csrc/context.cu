@@ -1,3 +1,4 @@
+#include <algorithm>
 // context.cu -- parameter generation, device tables, keys, scratch memory.
 //
 // Replaces the reference's EngineContext + SimulatorEngine construction
@@ -98,6 +99,20 @@ struct Staging {
     std::vector<cudaEvent_t> spare;
 };
 Staging g_stage;
+
+// The ring is mapped into the device address space and the upload is a small
+// kernel reading it over PCIe (zero-copy), NOT a copy-engine DMA: a large
+// host->device DMA on another stream (bench.py's e2e images, 805 MB) would
+// otherwise hold the H2D copy engine for ~15 ms and every small upload queued
+// behind it -- and the kernels that wait for those uploads -- would stall.
+__global__ void k_stage_copy(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src, size_t bytes) {
+    const size_t n16 = ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) ? bytes / 16 : 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+        ((uint4 *)dst)[i] = ((const uint4 *)src)[i];
+    for (size_t i = n16 * 16 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < bytes;
+         i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
 }  // namespace
 
 cudaError_t he_h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
@@ -105,7 +120,7 @@ cudaError_t he_h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(g_stage.mu);
     if (!g_stage.tried) {
         g_stage.tried = true;
-        if (cudaHostAlloc((void **)&g_stage.buf, (size_t)256 << 20, cudaHostAllocDefault) == cudaSuccess)
+        if (cudaHostAlloc((void **)&g_stage.buf, (size_t)256 << 20, cudaHostAllocMapped) == cudaSuccess)
             g_stage.cap = (size_t)256 << 20;
         else
             g_stage.buf = nullptr;
@@ -123,7 +138,12 @@ cudaError_t he_h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
         g_stage.fifo.pop_front();
     }
     memcpy(g_stage.buf + lo, src, bytes);
-    cudaError_t e = cudaMemcpyAsync(dst, g_stage.buf + lo, bytes, cudaMemcpyHostToDevice, s);
+    void *dsrc = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dsrc, g_stage.buf + lo, 0);
+    if (e != cudaSuccess) return e;
+    const unsigned blocks = (unsigned)std::min<size_t>((bytes + 4095) / 4096, 64);
+    k_stage_copy<<<blocks, 256, 0, s>>>((uint8_t *)dst, (const uint8_t *)dsrc, bytes);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     cudaEvent_t ev;
     if (g_stage.spare.empty()) {
