@@ -389,6 +389,7 @@ class GpuEngine:
         self._dnum = -(-context.n_q // context.alpha)  # key-switch digits (key layout [dnum][2][L+K][N])
         self._timing = None  # {category: [(start_event, end_event, units)]} when enabled
         self._slab: dict = {}  # shape -> cached ciphertext batches (see _alloc)
+        self.pool_releases = 0  # out-of-memory retries (_release_pool)
         # exact int8-digit tensor-core convolutions (he_conv_mma); False = CUDA-core kernel
         self.use_tensor_cores = True
         self.joint_moddown = True  # relin + rescales as one ModDown (N = 2^16)
@@ -498,6 +499,7 @@ class GpuEngine:
         """Drop the cached batches and hand the pool's unused pages back to the
         device, so a large request is not refused for want of one free range."""
         torch = _torch()
+        self.pool_releases += 1
         self.trim()
         torch.cuda.synchronize(self.device)
         torch.cuda.empty_cache()
@@ -1325,6 +1327,71 @@ class GpuEngine:
         self._acct.bump("plain_mults", nnz * M)
         self._acct.bump("adds", nnz * M)
         return self._wrap_batch(out, level, [s_out] * n_out)
+
+    @staticmethod
+    def split_scale_weights(w, mult: float, bits: int = 23):
+        """Integer weights of conv_exact_partial: round(w * mult / F) with F = 2^k the
+        smallest power of two that brings every |weight| within the 3-signed-digit
+        range of the tensor-core kernel (<= 127 (256^3 - 1) / 255 < 2^23).  The
+        effective integer weight is W * F (relative precision 2^-23 of the largest)."""
+        w = np.asarray(w, np.float64)
+        cap = 127 * (256 ** 3 - 1) // 255
+        top = float(np.abs(w).max(initial=0.0)) * float(mult)
+        k = 0
+        while top / (1 << k) > cap - 1:
+            k += 1
+        wi = np.rint(w * float(mult) / float(1 << k)).astype(np.int64)
+        while np.abs(wi).max(initial=0) > cap:
+            k += 1
+            wi = np.rint(w * float(mult) / float(1 << k)).astype(np.int64)
+        return np.ascontiguousarray(wi), 1 << k
+
+    def conv_exact_partial(self, inputs: Sequence[CipherVec], gcol, weights, n_out: int, out_scale: float):
+        """Tensor-core form of lincomb_grouped(skip_rescale=True) for config 4's
+        standard (rescaled) weight encoding: the exact sums
+            out[g + m * G] = sum_t (W[m, t] * F) * in[gcol[g, t]]   mod q
+        with (W, F) = split_scale_weights(w, q_l * out_scale / s_in): the int8-digit
+        GEMM (he_conv_mma) computes sum W x exactly and one he_mul_const multiplies
+        by F.  Declared scale q_l * out_scale, level unchanged (rescale once after
+        the partial sums are added).  None when the tensor-core bounds do not hold."""
+        for c in inputs:
+            self._check(c)
+        s_in = inputs[0].scale
+        if any(c.scale != s_in for c in inputs):
+            raise ScaleMismatch("conv_exact_partial needs inputs at one scale")
+        level = min(c.level for c in inputs)
+        if level < self.context.mult_level_cost:
+            raise LevelExhausted(f"level {level} < multiplication cost {self.context.mult_level_cost}")
+        limbs = level + 1
+        w = np.asarray(weights, np.float64)
+        M, T = w.shape
+        if M > 32 or self.N % 128:
+            return None
+        ql = self.moduli[limbs - 1]
+        wi, F = self.split_scale_weights(w, ql * float(out_scale) / s_in)
+        gc = np.ascontiguousarray(gcol, np.int32)
+        G = gc.shape[0]
+        ob = np.ascontiguousarray(np.arange(G), np.int32)
+        tins = self._at_level(inputs, level)
+        pin = _lib.ptr_array([t.data_ptr() for t in tins])
+        out = self._alloc(n_out, 2, limbs)
+        pout = self._tptrs(out)
+        poly = 2 * limbs * self.N
+        nnz = int((gc >= 0).sum())
+        rc = self._call("lincomb", self._L.he_conv_mma, self._h, _lib.addr(pin), len(inputs), _lib.addr(pout), n_out,
+                        G, _lib.addr(gc), _lib.addr(ob), G, M, T, _lib.addr(wi), None, limbs, 2, self.stream,
+                        units=((len(np.unique(gc[gc >= 0])) + n_out) * poly * 8.0, float(nnz) * M * poly))
+        if rc == _lib.HE_EINVAL:
+            return None
+        _lib.check(rc, "conv_exact_partial")
+        if F != 1:
+            res = np.array([self._res(F, limbs)] * n_out, np.uint64)
+            _lib.check(self._call("lincomb", self._L.he_mul_const, self._h, _lib.addr(pout), _lib.addr(pout), n_out,
+                                  limbs, 2, _lib.addr(res), self.stream, units=(n_out * 2.0 * poly * 8, 0.0)),
+                       "conv_exact_partial (x F)")
+        self._acct.bump("plain_mults", nnz * M)
+        self._acct.bump("adds", nnz * M)
+        return self._wrap_batch(out, level, [ql * float(out_scale)] * n_out)
 
     def conv_square_sum(self, inputs: Sequence[CipherVec], p: int, H: int, W: int, weights, weight_scale: float,
                         bias, const: float, pool: bool, rows=None, scale_mult: float | None = None,

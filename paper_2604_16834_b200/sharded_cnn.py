@@ -113,20 +113,45 @@ def conv3x3_window_groups(p: int, H: int, W: int, r0: int, r1: int, ya: int, yb:
     return term_ptr.astype(np.int32), col.astype(np.int32), tap.astype(np.int32), len(counts)
 
 
-def conv3x3_partial(engine, window, weights, H, W, r0, r1, ya, yb, out_scale):
+def conv3x3_window_fulltaps(p: int, H: int, W: int, r0: int, r1: int, ya: int, yb: int) -> np.ndarray:
+    """[pixels][9p] window index of every tap slot of output rows [r0, r1) (-1 outside
+    the image), tap order i*9 + (dy+1)*3 + (dx+1): the gather table of he_conv_mma."""
+    nw = yb - ya
+    y = np.arange(r0, r1)[:, None, None, None]
+    x = np.arange(W)[None, :, None, None]
+    k = np.arange(9)[None, None, None, :]
+    yy, xx = y + k // 3 - 1, x + k % 3 - 1
+    i = np.arange(p)[None, None, :, None]
+    valid = (yy >= 0) & (yy < H) & (xx >= 0) & (xx < W)
+    col = np.where(valid, i * nw * W + (yy - ya) * W + xx, -1)
+    return np.ascontiguousarray(col.reshape((r1 - r0) * W, p * 9).astype(np.int32))
+
+
+def conv3x3_partial(engine, window, weights, H, W, r0, r1, ya, yb, out_scale, tensor_cores: bool = True):
     """Exact (un-rescaled) contribution of one input-channel block (its rows
     [ya, yb) in ``window``) to output rows [r0, r1) of every output channel of
-    ``weights`` [q_local][p_block*9]: he_lincomb_grouped with skip_rescale,
-    outputs indexed (o, y, x), declared scale q_l * out_scale."""
+    ``weights`` [q_local][p_block*9], outputs indexed (o, y, x), declared scale
+    q_l * out_scale.  With ``tensor_cores`` (GpuEngine.conv_exact_partial) the
+    sums run as exact int8-digit GEMMs with split-scale integer weights W * 2^k;
+    otherwise (or when the tensor-core bounds fail) he_lincomb_grouped with the
+    weights round(w q_l out_scale / s_in)."""
     w = np.asarray(weights, np.float64)
     q = w.shape[0]
     p = w.shape[1] // 9
-    tp, col, tap, npix = conv3x3_window_groups(p, H, W, r0, r1, ya, yb)
+    tc = getattr(engine, "conv_exact_partial", None) if tensor_cores else None
+    gcol = conv3x3_window_fulltaps(p, H, W, r0, r1, ya, yb) if tc is not None else None
+    tp = col = tap = None
+    npix = (r1 - r0) * W
     out = []
-    for c0 in range(0, q, 32):  # he_lincomb_grouped takes <= 32 outputs per pixel group
+    for c0 in range(0, q, 32):  # <= 32 outputs per pixel group and launch
         m = min(32, q - c0)
-        out.extend(engine.lincomb_grouped(window, tp, col, tap, np.arange(npix), npix, w[c0:c0 + m], m * npix,
-                                          out_scale=out_scale, skip_rescale=True))
+        part = tc(window, gcol, w[c0:c0 + m], m * npix, out_scale) if tc is not None else None
+        if part is None:
+            if tp is None:
+                tp, col, tap, npix = conv3x3_window_groups(p, H, W, r0, r1, ya, yb)
+            part = engine.lincomb_grouped(window, tp, col, tap, np.arange(npix), npix, w[c0:c0 + m], m * npix,
+                                          out_scale=out_scale, skip_rescale=True)
+        out.extend(part)
     return out
 
 
@@ -185,7 +210,7 @@ class _BlockStage:
     replicated = False
 
     def __init__(self, engine, up, w, bias, act, fold, pool, H, W, rank, world, ring, tile_rows, trace, blk,
-                 max_outputs=512):
+                 max_outputs=512, tensor_cores=True):
         self.engine, self.up = engine, up
         self.q, self.p = w.shape[:2]
         self.mine = list(channel_shards(self.q, world)[rank])
@@ -201,6 +226,7 @@ class _BlockStage:
         self.R = R + (R % 2) if pool else R
         self.trace, self.blk = trace, blk
         self.max_outputs = max_outputs
+        self.tensor_cores = tensor_cores
         self.rows = {}
         self.done = 0          # conv rows produced so far
         self.released = 0      # output rows below this index are freed
@@ -236,7 +262,7 @@ class _BlockStage:
         acc = None
         local = self.up.window(ya, yb)         # this rank's input channels of rows [ya, yb)
         if self.up.replicated or self.world == 1:   # every input channel is resident: one local round
-            acc = conv3x3_partial(eng, local, self.wm, H, W, r0, r1, ya, yb, s_out)
+            acc = conv3x3_partial(eng, local, self.wm, H, W, r0, r1, ya, yb, s_out, self.tensor_cores)
         else:
             t, level, scale = eng.pack_batch(local)
             pad = max(len(sh) for sh in self.in_shards) * (yb - ya) * W
@@ -252,7 +278,7 @@ class _BlockStage:
                 n = len(chans) * (yb - ya) * W
                 blk_cts = eng.unpack_batch(t[:n], level, scale)
                 cols = (np.asarray(chans)[:, None] * 9 + np.arange(9)[None, :]).reshape(-1)
-                part = conv3x3_partial(eng, blk_cts, self.wm[:, cols], H, W, r0, r1, ya, yb, s_out)
+                part = conv3x3_partial(eng, blk_cts, self.wm[:, cols], H, W, r0, r1, ya, yb, s_out, self.tensor_cores)
                 eng.release(*blk_cts)
                 acc = _accumulate(eng, acc, part)
                 if h is not None:
@@ -295,13 +321,16 @@ class _BlockStage:
 
 
 def run_cnn_sharded(engine, x_cts, spec, wts, rank: int, world: int, ring=None, release_inputs: bool = True,
-                    tile_rows: int = 2, trace=None, max_outputs: int = 512):
+                    tile_rows: int = 2, trace=None, max_outputs: int = 512, tensor_cores: bool = True):
     """Encrypted forward pass of ``spec`` with output channels sharded over
     ``world`` ranks, streamed over image rows (module docstring).
 
     x_cts: the C0*H*W input ciphertexts (channel-major), replicated on every rank.
     ``tile_rows``: conv rows per tile (even for pooled blocks); ``max_outputs``:
-    ciphertexts per batch of a tile's rescale / activation / pool.  ``trace``
+    ciphertexts per batch of a tile's rescale / activation / pool.  ``tensor_cores``:
+    the conv sums as exact int8-digit GEMMs (split-scale weights, conv3x3_partial);
+    False keeps featuremajor.run_cnn's CUDA-core weight encoding (bit-identical
+    to run_cnn(lazy_relin=False)).  ``trace``
     (tests): trace(stage, cts, info) with stage "acc" (a tile's exact conv sums
     before the rescale), "act" (the activation outputs, info["pre"] its inputs),
     "gap" and "dense".  Returns the n_classes output ciphertexts on every rank."""
@@ -316,7 +345,7 @@ def run_cnn_sharded(engine, x_cts, spec, wts, rank: int, world: int, ring=None, 
         # sums is the same sum over every pixel)
         pool = blk in spec.pool_after and blk != nblk - 1
         st = _BlockStage(engine, src, w, bias, spec.act, fold, pool, H, W, rank, world, ring, tile_rows, trace, blk,
-                         max_outputs)
+                         max_outputs, tensor_cores)
         stages.append(st)
         src = st
         if pool:

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--tile-rows", type=int, default=2)
     ap.add_argument("--mem-trace", action="store_true", help="print HBM use at every tile")
+    ap.add_argument("--max-outputs", type=int, default=512)
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -68,7 +69,7 @@ def main():
               f"slab {sum(t.numel() * 8 for v in eng._slab.values() for t in v) / 1e9:.1f} GB", flush=True)
 
     out = run_cnn_sharded(eng, x, spec, wts, rank, world, ring=TorchRing(rank, world), tile_rows=args.tile_rows,
-                          trace=mem_trace if args.mem_trace else None)
+                          trace=mem_trace if args.mem_trace else None, max_outputs=args.max_outputs)
     e1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world, device="cuda")
@@ -79,7 +80,8 @@ def main():
                           "samples": n, "ms": ms, "samples_per_s": n / (ms / 1e3),
                           "max_abs_err_64": float(np.max(np.abs(got - ref))), "input_limbs": level + 1,
                           "peak_hbm_gb_rank0": torch.cuda.max_memory_allocated() / 1e9,
-                          "tile_rows": args.tile_rows, "ms_by_category": {k: [v[0], round(v[1], 1)] for k, v in eng.timing_summary().items()},
+                          "tile_rows": args.tile_rows, "pool_releases": eng.pool_releases,
+                          "max_outputs": args.max_outputs, "ms_by_category": {k: [v[0], round(v[1], 1)] for k, v in eng.timing_summary().items()},
                           "parallelism": f"output-channel shards x{world}, ring exchange"}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -7,9 +7,10 @@ Reference counterpart: the conv / activation / pool chain of
 /root/reference/pkg/src/hebatch/conv.py:109-173 on the feature-major layout.
 
 Parity, layer by layer, on the GPU's own layer inputs:
-  * every block's first tile: the exact conv sums (before the rescale) at 24
-    sampled evaluation points of EVERY output of the tile, replayed by the
-    oracle's lincomb on the sampled inputs (Oracle.coeff_view);
+  * every block's first tile: the exact conv sums (before the rescale; the
+    tensor-core path with split-scale integer weights W 2^k) at 24 sampled
+    evaluation points of EVERY output of the tile, replayed by the oracle's
+    lincomb with the same integer weights on the sampled inputs (Oracle.coeff_view);
   * one output per block: rescale + degree-3 activation (two ct x ct products
     with relinearisation and rescale, constant adds) on full polynomials;
   * pooled rows: the next block's window inputs == the sums of the 4 activation
@@ -101,7 +102,13 @@ def test_cfg4_full_shape_streamed_layerwise_bit_exact_vs_oracle():
         tp, col, tap, npix = conv3x3_window_groups(p, Hb, Wb, r0, r1, ya, yb)
         limbs = A["in_level"] + 1
         ql = orc.moduli[limbs - 1]
-        wi = np.rint(A["w"] * (ql * eng.context.scale) / A["in_scale"]).astype(np.int64)
+        # the tensor-core path's split-scale integer weights W * 2^k, per launch of <= 32 channels
+        mult = ql * eng.context.scale / A["in_scale"]
+        wi = np.zeros(A["w"].shape, np.int64)
+        for c0 in range(0, q, 32):
+            W_, F_ = GpuEngine.split_scale_weights(A["w"][c0:c0 + 32], mult)
+            wi[c0:c0 + 32] = W_ * F_
+            assert np.abs(W_).max() < 2 ** 23 and np.max(np.abs(W_ * F_ - A["w"][c0:c0 + 32] * mult)) <= F_ / 2
         rows, cols, ws = [0], [], []
         for m in range(q):
             for g in range(npix):

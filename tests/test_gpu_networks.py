@@ -184,13 +184,18 @@ def test_cfg4_layout_sharded_runner_world1_bit_exact_vs_run_cnn():
     images = rng.uniform(0.0, 1.0, size=(n, 3 * 64))
     x = pack_features(eng, images)
     ref_out = run_cnn(eng, x, spec, wts, release_inputs=False, lazy_relin=False)
-    sh_out = run_cnn_sharded(eng, x, spec, wts, 0, 1, release_inputs=False)
+    sh_out = run_cnn_sharded(eng, x, spec, wts, 0, 1, release_inputs=False, tensor_cores=False)
     for o in range(10):
         assert np.array_equal(to_np(sh_out[o].data), to_np(ref_out[o].data)), o
         assert sh_out[o].scale == ref_out[o].scale and sh_out[o].level == ref_out[o].level
     got = eng.decrypt_batch(sh_out).T
     ref = spec.forward_plain(wts, images.reshape(n, 3, 8, 8))
     assert np.max(np.abs(got - ref)) < TOL
+    # the tensor-core form (split-scale weights): same levels and scales, decrypts alike
+    tc_out = run_cnn_sharded(eng, x, spec, wts, 0, 1, release_inputs=False, tensor_cores=True)
+    for o in range(10):
+        assert tc_out[o].scale == ref_out[o].scale and tc_out[o].level == ref_out[o].level
+    assert np.max(np.abs(eng.decrypt_batch(tc_out).T - ref)) < TOL
 
 
 @pytest.mark.gpu
