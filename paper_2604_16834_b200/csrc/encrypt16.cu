@@ -150,10 +150,13 @@ __global__ void __launch_bounds__(NTT_TPB) k_enc16_rows(uint64_t *const *out, in
         const uint32_t k = r * 256 + cc;
         const uint64_t a = sample_uniform(seed, DOM_ENC_A, obj, (uint32_t)l, k, c.q);
         const uint64_t sv = skl[cc];
-        // the secret is ternary (residues 0, 1, q - 1): a s is 0, a or -a -- no product
-        const uint64_t x0 = s[pad16(cc)];
+        uint64_t as;
+        if (c.q < FP_QMAX)
+            as = fcanon(fmulmod(u2d(a), u2d(sv), c.qd, c.qid), c.qd, c.qid);
+        else
+            as = mul_mod(a, sv, c);
         c1[k] = a;
-        row[cc] = sv == 0 ? x0 : sv == 1 ? sub_mod(x0, a, c.q) : add_mod(x0, a, c.q);
+        row[cc] = sub_mod(s[pad16(cc)], as, c.q);
     }
 }
 
