@@ -727,6 +727,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
         // ======================= epilogue
         const int qd = warp & 3, cg = warp >> 2;
         const int row = qd * 32 + lane, j = row & 7;
+        const bool exp1 = a.exp == 1, hasb = a.biasd != nullptr;  // no bias: no per-row loads
         const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(cg * CPT);
         int k = 0, S = 0;
         for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
@@ -763,13 +764,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
 #pragma unroll
                     for (int m = 0; m < CPT; m++) yv[cc][m] = recombine<NSH>(C[m], yc, c);
                 }
-                if (a.exp == 1) {
+                if (exp1) {
 #pragma unroll
                     for (int m = 0; m < CPT; m++) gs[m][0] += yv[0][m] + yv[1][m] + yv[2][m];
                 } else
 #pragma unroll
                 for (int m = 0; m < CPT; m++) {
-                    const double d0 = yv[0][m] + a.biasd[(size_t)(m0 + m) * a.ell + l], d1 = yv[1][m], d2 = yv[2][m];
+                    const double d0 = hasb ? yv[0][m] + a.biasd[(size_t)(m0 + m) * a.ell + l] : yv[0][m];
+                    const double d1 = yv[1][m], d2 = yv[2][m];
                     gs[m][0] += fmulmod(d0, d0, c.qd, c.qid);
                     gs[m][1] += fmulmod(d0, d1, c.qd, c.qid);
                     gs[m][2] += fmulmod(d0 + d0, d2, c.qd, c.qid) + fmulmod(d1, d1, c.qd, c.qid);
@@ -812,7 +814,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                             else
                                 gs[m][s2] = v;
                         }
-                asm volatile("bar.sync 2, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+                // only the four warps of this channel group (one per lane quarter) meet here
+                switch (cg) {
+                    case 0: asm volatile("bar.sync 2, 128;" ::: "memory"); break;
+                    case 1: asm volatile("bar.sync 3, 128;" ::: "memory"); break;
+                    case 2: asm volatile("bar.sync 4, 128;" ::: "memory"); break;
+                    default: asm volatile("bar.sync 5, 128;" ::: "memory"); break;
+                }
             }
             if (qd == 3 && lane < 8) {
                 const size_t lo = (size_t)l * N + coff + j;
@@ -1067,7 +1075,8 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
         }
     }
     a.btiles = dbt;
-    a.biasd = dbias;
+    // P16 reads the bias per row only when there is one (config 3's biases are zero)
+    a.biasd = (p16 && std::all_of(biasd.begin(), biasd.end(), [](double v) { return v == 0.0; })) ? nullptr : dbias;
     a.cst = dc;
     a.yc = dyc;
     a.mc = c->d_mc;
