@@ -141,3 +141,30 @@ def test_streamed_rows_bound_resident_ciphertexts():
         assert eng.live == 0
         inputs, full_map = 2 * 24 * 4, 4 * 24 * 4   # block 1's whole output map: 384 ciphertexts
         assert peak[0] - inputs < full_map, (tile, peak[0])   # windows + one tile's temporaries only
+
+
+def test_window_fulltaps_equal_full_map_fulltaps():
+    """The tensor-core gather table of a row window == featuremajor.conv3x3_fulltaps
+    on the full map with indices translated into the window; and the split-scale
+    weights reproduce round(w * mult) within F / 2 with |W| < 2^23."""
+    from paper_2604_16834_b200.engine import GpuEngine
+    from paper_2604_16834_b200.featuremajor import conv3x3_fulltaps
+    from paper_2604_16834_b200.sharded_cnn import conv3x3_window_fulltaps
+
+    p, H, W = 3, 8, 6
+    for r0, r1 in [(0, 2), (2, 4), (6, 8), (3, 4), (0, 8)]:
+        ya, yb = max(0, r0 - 1), min(H, r1 + 1)
+        full = conv3x3_fulltaps(p, H, W, range(r0, r1))
+        win = conv3x3_window_fulltaps(p, H, W, r0, r1, ya, yb)
+        i, rest = full // (H * W), full % (H * W)
+        y, x = rest // W, rest % W
+        want = np.where(full >= 0, i * (yb - ya) * W + (y - ya) * W + x, -1)
+        assert np.array_equal(win, want)
+    rng = np.random.default_rng(8)
+    w = rng.normal(0, 0.3, (32, 144))
+    for mult in (2.0 ** 50, 2.0 ** 30, 1000.0):
+        wi, F = GpuEngine.split_scale_weights(w, mult)
+        assert np.abs(wi).max() < 2 ** 23 and F & (F - 1) == 0
+        assert np.max(np.abs(wi * float(F) - w * mult)) <= F / 2 + 1e-6 * F
+        if mult < 2 ** 22:
+            assert F == 1 and np.array_equal(wi, np.rint(w * mult).astype(np.int64))
