@@ -34,6 +34,20 @@ __device__ __forceinline__ void fft_bfly(double &ur, double &ui, double &vr0, do
     vi0 = __dsub_rn(b, vi);
 }
 
+// fft_bfly with the twiddle (sign already applied) passed in: identical operations
+__device__ __forceinline__ void fft_bfly_w(double &ur, double &ui, double &vr0, double &vi0, const double wr,
+                                           const double wi) {
+    const double t1 = __dmul_rn(vr0, wr), t2 = __dmul_rn(vi0, wi);
+    const double vr = __dsub_rn(t1, t2);
+    const double t3 = __dmul_rn(vr0, wi), t4 = __dmul_rn(vi0, wr);
+    const double vi = __dadd_rn(t3, t4);
+    const double a = ur, b = ui;
+    ur = __dadd_rn(a, vr);
+    ui = __dadd_rn(b, vi);
+    vr0 = __dsub_rn(a, vr);
+    vi0 = __dsub_rn(b, vi);
+}
+
 __global__ void k_fft_stage(double *re, double *im, size_t count, int logn, int len, int sign, const double *w) {
     size_t n = (size_t)1 << logn, halfn = n >> 1, tot = count * halfn;
     int half = len >> 1;
@@ -52,8 +66,16 @@ constexpr int FFT_B = 11, FFT_TPB = 256;
 __global__ void __launch_bounds__(FFT_TPB) k_fft_chunk(double *re, double *im, int logn, int B, int sign,
                                                        const double *w) {
     __shared__ double sr[1 << FFT_B], si[1 << FFT_B];
+    // the chunk stages only use twiddles w[k (n >> lg)], lg <= B: the 2^(B-1) entries of stride
+    // n >> B, staged once per CTA (sign applied) instead of two global loads per butterfly
+    __shared__ double swr[1 << (FFT_B - 1)], swi[1 << (FFT_B - 1)];
     const size_t n = (size_t)1 << logn, csz = (size_t)1 << B;
     const size_t base = (size_t)blockIdx.x * csz;  // chunks of consecutive polynomials tile the batch
+    const size_t wst = n >> B;
+    for (int i = threadIdx.x; i < (int)(csz >> 1); i += FFT_TPB) {
+        swr[i] = w[2 * (i * wst)];
+        swi[i] = sign < 0 ? -w[2 * (i * wst) + 1] : w[2 * (i * wst) + 1];
+    }
     for (int i = threadIdx.x; i < (int)csz; i += FFT_TPB) {
         sr[i] = re[base + i];
         si[i] = im[base + i];
@@ -82,7 +104,8 @@ __global__ void __launch_bounds__(FFT_TPB) k_fft_chunk(double *re, double *im, i
                 for (int j = 0; j < 8; j++) {
                     if (j >= m || (j >> st) & 1) continue;
                     const int k = (gbase & (h - 1)) + (j & ((1 << st) - 1)) * h;  // index inside the half
-                    fft_bfly(xr[j], xi[j], xr[j + (1 << st)], xi[j + (1 << st)], w, (size_t)k * step, sign);
+                    const int ti = (int)(((size_t)k * step) / wst);           // = k 2^(B - lg)
+                    fft_bfly_w(xr[j], xi[j], xr[j + (1 << st)], xi[j + (1 << st)], swr[ti], swi[ti]);
                 }
             }
 #pragma unroll
