@@ -63,6 +63,7 @@ struct he_ctx {
     double *d_fftw = nullptr;        // [nslots][2]  omega^k
     double *d_twist = nullptr;       // [nslots][2]  zeta^j
     int32_t *d_slot_brv = nullptr;   // [nslots]     brv(pos[i]): slot i <-> FFT input index
+    int32_t *d_slot_inv = nullptr;   // [nslots]     the inverse permutation: FFT input index -> slot
     uint8_t *d_ident = nullptr;      // [HE_MAXM]    identity modulus map
     std::map<uint32_t, uint64_t *> keys;            // [dnum][2][L+K][N] Montgomery form (HE_HOIST_CODE | g: hoisting keys)
     std::map<uint64_t, BconvTable> modup_tab;       // key = ell*64 + digit

@@ -388,6 +388,10 @@ static int build_tables(he_ctx *c) {
     HE_CHECK_CUDA(cudaMemcpy(c->d_twist, z.data(), z.size() * 8, cudaMemcpyHostToDevice));
     HE_CHECK_CUDA(cudaMalloc(&c->d_slot_brv, sb.size() * 4));
     HE_CHECK_CUDA(cudaMemcpy(c->d_slot_brv, sb.data(), sb.size() * 4, cudaMemcpyHostToDevice));
+    std::vector<int32_t> inv(n);
+    for (int i = 0; i < n; i++) inv[sb[i]] = i;
+    HE_CHECK_CUDA(cudaMalloc(&c->d_slot_inv, inv.size() * 4));
+    HE_CHECK_CUDA(cudaMemcpy(c->d_slot_inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
     uint8_t ident[HE_MAXM];
     for (int i = 0; i < HE_MAXM; i++) ident[i] = (uint8_t)i;
     HE_CHECK_CUDA(cudaMalloc(&c->d_ident, HE_MAXM));
@@ -475,6 +479,7 @@ extern "C" int he_ctx_destroy(he_ctx *c) {
     cudaFree(c->d_fftw);
     cudaFree(c->d_twist);
     cudaFree(c->d_slot_brv);
+    cudaFree(c->d_slot_inv);
     cudaFree(c->d_ident);
     cudaFree(c->d_pinv);
     cudaFree(c->d_qlinv);

@@ -63,8 +63,12 @@ __global__ void k_fft_stage(double *re, double *im, size_t count, int logn, int 
 // Stages len = 2 .. 2^B of every aligned 2^B-element chunk in shared memory
 // (one CTA per chunk): the same butterflies as k_fft_stage, one HBM pass.
 constexpr int FFT_B = 11, FFT_TPB = 256;
+// gvals != nullptr: the chunk's inputs are GATHERED from the slot values (the encoder's
+// scatter V[brv(pos[i])] = vals[i] read backwards through the inverse permutation; zero
+// imaginary parts and zero padding beyond nvals) instead of read from re / im
 __global__ void __launch_bounds__(FFT_TPB) k_fft_chunk(double *re, double *im, int logn, int B, int sign,
-                                                       const double *w) {
+                                                       const double *w, const double *gvals = nullptr,
+                                                       int nvals = 0, const int32_t *ginv = nullptr) {
     __shared__ double sr[1 << FFT_B], si[1 << FFT_B];
     // the chunk stages only use twiddles w[k (n >> lg)], lg <= B: the 2^(B-1) entries of stride
     // n >> B, staged once per CTA (sign applied) instead of two global loads per butterfly
@@ -76,9 +80,18 @@ __global__ void __launch_bounds__(FFT_TPB) k_fft_chunk(double *re, double *im, i
         swr[i] = w[2 * (i * wst)];
         swi[i] = sign < 0 ? -w[2 * (i * wst) + 1] : w[2 * (i * wst) + 1];
     }
-    for (int i = threadIdx.x; i < (int)csz; i += FFT_TPB) {
-        sr[i] = re[base + i];
-        si[i] = im[base + i];
+    if (gvals) {
+        const size_t v = base >> logn, t0 = base & (n - 1);
+        for (int i = threadIdx.x; i < (int)csz; i += FFT_TPB) {
+            const int sl = __ldg(ginv + t0 + i);
+            sr[i] = sl < nvals ? __ldg(gvals + v * (size_t)nvals + sl) : 0.0;
+            si[i] = 0.0;
+        }
+    } else {
+        for (int i = threadIdx.x; i < (int)csz; i += FFT_TPB) {
+            sr[i] = re[base + i];
+            si[i] = im[base + i];
+        }
     }
     __syncthreads();
     // stages in register groups of up to three (radix-8 passes): a thread owns the
@@ -157,6 +170,23 @@ __global__ void k_fft_high(double *re, double *im, size_t count, int logn, int B
                 Ip[(size_t)j << B] = xi[j];
             }
     }
+}
+
+// encoder FFT of `count` slot vectors vals [count][nvals] gathered straight into the first
+// pass (no zero fill, no scatter pass); N = 2^16 layout only (chunk + high stages)
+static int run_fft_gather(he_ctx *c, const double *vals, int nvals, double *re, double *im, size_t count,
+                          cudaStream_t s) {
+    const int logn = c->logN - 1;
+    const size_t n = (size_t)1 << logn;
+    const int B = FFT_B;
+    k_fft_chunk<<<(unsigned)(count * (n >> B)), FFT_TPB, 0, s>>>(re, im, logn, B, -1, c->d_fftw, vals, nvals,
+                                                                c->d_slot_inv);
+    HE_CHECK_LAUNCH();
+    const size_t tot = count << B;
+    unsigned grid = (unsigned)std::min<size_t>((tot + EW - 1) / EW, (size_t)148 * 32);
+    k_fft_high<<<grid, EW, 0, s>>>(re, im, count, logn, B, -1, c->d_fftw);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
 }
 
 int run_fft(he_ctx *c, double *re, double *im, size_t count, int sign, cudaStream_t s) {
@@ -398,13 +428,12 @@ extern "C" int he_encrypt_level(he_ctx *c, const double *vals, int count, int nv
         Buf f(s);
         HE_TRY(he_scratch_alloc(&f.p, (size_t)count * n * 16, s));
         double *re = (double *)f.p, *im = re + (size_t)count * n;
-        HE_CHECK_CUDA(cudaMemsetAsync(re, 0, (size_t)count * n * 16, s));
         if (nvals > 0) {
-            k_scatter_slots2<<<gridn((size_t)count * nvals), EW, 0, s>>>(re, vals, count, nvals, (int)n,
-                                                                         c->d_slot_brv);
-            HE_CHECK_LAUNCH();
+            HE_TRY(run_fft_gather(c, vals, nvals, re, im, count, s));  // scatter folded into the first pass
+        } else {
+            HE_CHECK_CUDA(cudaMemsetAsync(re, 0, (size_t)count * n * 16, s));
+            HE_TRY(run_fft(c, re, im, count, -1, s));
         }
-        HE_TRY(run_fft(c, re, im, count, -1, s));
         return he_encrypt16(c, re, im, count, scale, ct_index0, ell, op, s);
     }
     HE_TRY(encode_into(c, vals, count, nvals, scale, op, ell, 1, ct_index0, s));
