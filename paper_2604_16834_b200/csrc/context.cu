@@ -404,8 +404,8 @@ extern "C" int he_ctx_create(const he_params *p, int device, he_ctx **out) {
         he_set_error("he_ctx_create: null argument");
         return HE_EINVAL;
     }
-    if (p->log_n < 3 || (p->log_n > 14 && p->log_n != 16)) {
-        he_set_error("log_n=%d unsupported (N = 2^3 .. 2^14 and 2^16)", p->log_n);
+    if (p->log_n < 3 || p->log_n > 16) {
+        he_set_error("log_n=%d unsupported (N = 2^3 .. 2^16)", p->log_n);
         return HE_EINVAL;
     }
     if (p->n_q < 1 || p->n_q > 48 || p->n_p < 1 || p->n_p > 16 || p->n_q + p->n_p > HE_MAXM || p->alpha < 1 ||

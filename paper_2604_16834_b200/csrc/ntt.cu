@@ -384,7 +384,118 @@ __global__ void k_ntt_generic(PolySrc data, const uint8_t *mod_map, int per, con
     for (int i = threadIdx.x; i < N; i += blockDim.x) pi.p[i] = sg[i];
 }
 
+// ---------------------------------------------------------------- N = 2^15 (and any N > 2^14)
+// The transform splits into 2^(logN-14) independent sub-blocks of 2^14 after the first
+// logN - 14 forward stages (before the last ones inverse): those stages run over global
+// memory (k_ntt_gstage), the other 14 per sub-block in shared memory (k_ntt_sub, the
+// k_ntt_generic butterflies with the sub-block's twiddle-block offset).  Same butterflies in
+// the same order as the one-CTA kernel, canonical output.
+constexpr int SUBLOG = 14;
+
+__global__ void k_ntt_gstage(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw, const ModConst *mc,
+                             int logN, size_t n_polys, int stage, int inverse, int scale) {
+    const size_t N = (size_t)1 << logN, half = N >> 1;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < n_polys * half;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t poly = idx / half, b = idx % half;
+        PolyInfo pi;
+        if (!poly_info(pi, data, poly, mod_map, per, tw, mc, logN, inverse)) continue;
+        const uint64_t q = pi.q;
+        if (!inverse) {
+            const size_t t = half >> stage, i = b / t, j = 2 * i * t + (b % t);
+            const ulonglong2 w = pi.W2[((size_t)1 << stage) + i];
+            const uint64_t u = pi.p[j], v = shoup(pi.p[j + t], w.x, w.y, q);
+            pi.p[j] = add_mod(u, v, q);
+            pi.p[j + t] = sub_mod(u, v, q);
+        } else {
+            const size_t t = (size_t)1 << stage, i = b / t, j = 2 * i * t + (b % t);
+            const size_t wi = (N >> (stage + 1)) + i;
+            const uint64_t u = pi.p[j], v = pi.p[j + t];
+            uint64_t x0 = add_mod(u, v, q), x1 = shoup(sub_mod(u, v, q), pi.W2[wi].x, pi.W2[wi].y, q);
+            if (scale) {
+                x0 = shoup(x0, pi.mc->ninv, pi.mc->ninv_sh, q);
+                x1 = shoup(x1, pi.mc->ninv, pi.mc->ninv_sh, q);
+            }
+            pi.p[j] = x0;
+            pi.p[j + t] = x1;
+        }
+    }
+}
+
+// stages lm = logN-14 .. logN-1 (forward) or lt = 0 .. 13 (inverse, no scaling) of sub-block
+// blockIdx.x % nsub of polynomial blockIdx.x / nsub
+__global__ void k_ntt_sub(PolySrc data, const uint8_t *mod_map, int per, const uint64_t *tw, const ModConst *mc,
+                          int logN, int inverse) {
+    extern __shared__ uint64_t sg[];
+    const int nsub = 1 << (logN - SUBLOG);
+    const size_t sb = blockIdx.x % nsub;
+    PolyInfo pi;
+    if (!poly_info(pi, data, blockIdx.x / nsub, mod_map, per, tw, mc, logN, inverse)) return;
+    const int S = 1 << SUBLOG, half = S >> 1, lm0 = logN - SUBLOG;
+    uint64_t *p = pi.p + sb * S;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) sg[i] = p[i];
+    __syncthreads();
+    const uint64_t q = pi.q;
+    if (!inverse) {
+        for (int ls = 0; ls < SUBLOG; ls++) {
+            const int lm = lm0 + ls, t = half >> ls;
+            for (int b = threadIdx.x; b < half; b += blockDim.x) {
+                const int i = b / t, j = 2 * i * t + (b % t);
+                const ulonglong2 w = pi.W2[((size_t)1 << lm) + (sb << ls) + i];
+                const uint64_t u = sg[j], v = shoup(sg[j + t], w.x, w.y, q);
+                sg[j] = add_mod(u, v, q);
+                sg[j + t] = sub_mod(u, v, q);
+            }
+            __syncthreads();
+        }
+    } else {
+        const size_t N = (size_t)1 << logN;
+        for (int lt = 0; lt < SUBLOG; lt++) {
+            const int t = 1 << lt;
+            for (int b = threadIdx.x; b < half; b += blockDim.x) {
+                const int i = b / t, j = 2 * i * t + (b % t);
+                const size_t wi = (N >> (lt + 1)) + (sb << (SUBLOG - 1 - lt)) + i;
+                const uint64_t u = sg[j], v = sg[j + t];
+                sg[j] = add_mod(u, v, q);
+                sg[j + t] = shoup(sub_mod(u, v, q), pi.W2[wi].x, pi.W2[wi].y, q);
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < S; i += blockDim.x) p[i] = sg[i];
+}
+
 }  // namespace
+
+static int ntt_big(he_ctx *c, PolySrc src, int n_polys, const uint8_t *mod_map, int per, bool inv, cudaStream_t s) {
+    const int logN = c->logN, G = logN - SUBLOG;
+    const size_t smem = ((size_t)1 << SUBLOG) * 8;
+    static bool attr = false;
+    if (!attr) {
+        HE_CHECK_CUDA(cudaFuncSetAttribute(k_ntt_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const size_t tot = (size_t)n_polys * ((size_t)c->N >> 1);
+    const unsigned gg = (unsigned)std::min<size_t>((tot + 255) / 256, (size_t)148 * 32);
+    const unsigned gs = (unsigned)n_polys << G;
+    if (!inv) {
+        for (int st = 0; st < G; st++) {
+            k_ntt_gstage<<<gg, 256, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc, logN, (size_t)n_polys, st, 0, 0);
+            HE_CHECK_LAUNCH();
+        }
+        k_ntt_sub<<<gs, 1024, smem, s>>>(src, mod_map, per, c->d_tw, c->d_mc, logN, 0);
+        HE_CHECK_LAUNCH();
+    } else {
+        k_ntt_sub<<<gs, 1024, smem, s>>>(src, mod_map, per, c->d_tw, c->d_mc, logN, 1);
+        HE_CHECK_LAUNCH();
+        for (int st = SUBLOG; st < logN; st++) {
+            k_ntt_gstage<<<gg, 256, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc, logN, (size_t)n_polys, st, 1,
+                                           st == logN - 1);
+            HE_CHECK_LAUNCH();
+        }
+    }
+    return HE_OK;
+}
 
 static int ntt_launch(he_ctx *c, PolySrc src, int n_polys, const uint8_t *mod_map, int per, bool inv, cudaStream_t s) {
     if (n_polys <= 0) return HE_OK;
@@ -409,6 +520,8 @@ static int ntt_launch(he_ctx *c, PolySrc src, int n_polys, const uint8_t *mod_ma
             k_inv16_cols<<<g, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);
             he_count_launch(1);
         }
+    } else if (c->logN > SUBLOG) {
+        return ntt_big(c, src, n_polys, mod_map, per, inv, s);
     } else if (c->logN == 12) {
         if (!inv)
             k_fwd12<<<(unsigned)n_polys, TPB, 0, s>>>(src, mod_map, per, c->d_tw, c->d_mc);

@@ -15,6 +15,9 @@ PARAMS = {
     "cfg4s": (12, (50,) * 10, (50,) * 2, 2, 50),
     # config 3's prime sizes on a small ring (tcgen05 conv kernels vs the oracle)
     "cfg3s": (12, (40,) * 6, (42,) * 2, 3, 40),
+    # the paper's pipeline-1 ring degree (N = 2^15, 46-bit rescale primes): the split
+    # global-stage + shared-memory NTT (ntt.cu ntt_big) and the generic key switch
+    "p15": (15, (60, 46, 46, 46, 46, 46), (60, 60), 2, 46),
     # config 3's 9-limb carry plan (inputs at 9 of 14 limbs) on a 64-point ring (CPU tests)
     "carry9": (6, (40,) * 9, (42,) * 3, 3, 40),
 }

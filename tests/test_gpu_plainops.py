@@ -19,7 +19,7 @@ from helpers import engine_context, from_np, oracle_for, rand_residues, to_np
 
 pytestmark = pytest.mark.gpu
 
-NAMES = ["tiny", "cfg1", "cfg3", "cfg2"]
+NAMES = ["tiny", "cfg1", "cfg3", "cfg2", "p15"]
 
 
 @pytest.fixture(scope="module", params=NAMES)
