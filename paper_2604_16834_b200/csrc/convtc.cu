@@ -691,21 +691,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                     const uint32_t lv = r1 > r0 ? tc5::sdesc_lbo((r1 - r0) << 4) : tc5::sdesc_lbo((r0 - r1) << 4);
                     const uint32_t a3 = (r1 > r0 ? r0 : r1) + 2 * (PS >> 4) + lv;
                     const uint64_t b3 = r1 > r0 ? bd[3] : bd[5];
-                    // all three components' slots first: the MMAs interleave the components so
-                    // that consecutive groups never accumulate into partially overlapping TMEM
-                    // columns (plane d+1 overlaps plane d's upper shift block)
-                    uint32_t dsl[NCI];
+                    // one component at a time, each committed as soon as its 25 MMAs are issued,
+                    // so the epilogue starts on component 0 while components 1 and 2 multiply
+                    // (dependent accumulations cost no MMA throughput: tests/test_gpu_tc5.py)
+#pragma unroll
                     for (int c = 0; c < NCI; c++) {
                         const int Sc = S + c, ds = Sc % NSL;
                         if (Sc >= NSL) PWAIT(3, tc5::mbar_wait(&bar_dempty[ds], ((Sc / NSL) - 1) & 1));
-                        dsl[c] = tmem + (uint32_t)ds * SLC;
-                    }
-                    tc5::tc_fence_after();
+                        tc5::tc_fence_after();
+                        const uint32_t dslc = tmem + (uint32_t)ds * SLC;
 #pragma unroll
-                    for (int d = 0; d < 5; d++)
-#pragma unroll
-                        for (int c = 0; c < NCI; c++) {
-                            const uint32_t dcol = dsl[c] + d * 16;
+                        for (int d = 0; d < 5; d++) {
+                            const uint32_t dcol = dslc + d * 16;
                             const uint32_t co = (uint32_t)(c * 5 + d) * (128 >> 4);
                             if (d == 0)
                                 tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r0 + co + lps), bd[6], idesc96, false);
@@ -716,7 +713,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                             tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, a3 + co), b3, idesc32, true);
                             tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r2 + co + 2 * (PS >> 4) + lps), bd[4], idesc32, true);
                         }
-                    for (int c = 0; c < NCI; c++, S++) tc5::tc_commit_w(&bar_dfull[S % NSL]);
+                        tc5::tc_commit_w(&bar_dfull[Sc % NSL]);
+                    }
+                    S += NCI;
                     tc5::tc_commit_w(&bar_empty[slot_of(y - 1)]);  // row y-1 is not read again
                 }
                 tc5::tc_commit_w(&bar_empty[slot_of(a.y1 - 1)]);
