@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-CONVTC_EXP=1 timeout 300 python scripts/role_convtc.py > gpurun_out/role_exp1.log 2>&1
-cat gpurun_out/role_exp1.log | grep planar
+for e in 0 1 2; do CONVTC_EXP=$e timeout 300 python scripts/role_convtc.py > gpurun_out/role_exp$e.log 2>&1; echo "exp $e"; grep planar gpurun_out/role_exp$e.log; done
