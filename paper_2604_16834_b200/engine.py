@@ -1468,9 +1468,10 @@ class GpuEngine:
         E = 1 if wmax < 128 else 2 if wmax < 32768 else 3
         nbs = sum(5 if q < (1 << 40) else 8 for q in self.moduli[:limbs])
         i8 = 1.0 * nci * nnz * M * self.N * nbs * E
-        # algorithmic bytes: inputs once (+ the 2-row halo), outputs once; a planar carry
+        # algorithmic bytes: inputs once (+ the halo rows that exist), outputs once; a planar carry
         # moves 5 bytes per residue instead of 8
-        in_b = p * (y1 - y0 + 2) * W * nci * poly * (5.0 if planar_in else 8.0)
+        rows_read = min(H, y1 + 1) - max(0, y0 - 1)   # the tile's rows plus the halo inside the image
+        in_b = p * rows_read * W * nci * poly * (5.0 if planar_in else 8.0)
         out_b = n_out * nco * poly * (5.0 if planar_out is not None else 8.0)
         args = (self._h, _lib.addr(pin) if pin is not None else None, nci, p, H, W,
                 _lib.addr(pout) if pout is not None else None, M, int(bool(pool)), y0, y1, _lib.addr(wi),
