@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--tile-rows", type=int, default=2)
     ap.add_argument("--mem-trace", action="store_true", help="print HBM use at every tile")
     ap.add_argument("--max-outputs", type=int, default=512)
+    ap.add_argument("--slab-cap-gb", type=float, default=None, help="GpuEngine.SLAB_FREE_CAP override")
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -49,6 +50,8 @@ def main():
     spec = CnnSpec(channels=base.channels, H=args.hw, W=args.hw, act=base.act, pool_after=base.pool_after)
     wts = spec.make_weights(1234)
     eng = GpuEngine(configs.context(4, seed=42, device=local))
+    if args.slab_cap_gb is not None:
+        eng.SLAB_FREE_CAP = int(args.slab_cap_gb * (1 << 30))
     n = eng.context.n
     rng = np.random.default_rng(args.seed)
     images = rng.uniform(0.0, 1.0, size=(n, 3 * args.hw * args.hw))
@@ -81,7 +84,7 @@ def main():
                           "max_abs_err_64": float(np.max(np.abs(got - ref))), "input_limbs": level + 1,
                           "peak_hbm_gb_rank0": torch.cuda.max_memory_allocated() / 1e9,
                           "tile_rows": args.tile_rows, "pool_releases": eng.pool_releases,
-                          "max_outputs": args.max_outputs, "ms_by_category": {k: [v[0], round(v[1], 1)] for k, v in eng.timing_summary().items()},
+                          "max_outputs": args.max_outputs, "slab_cap_gb": args.slab_cap_gb, "ms_by_category": {k: [v[0], round(v[1], 1)] for k, v in eng.timing_summary().items()},
                           "parallelism": f"output-channel shards x{world}, ring exchange"}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
