@@ -122,6 +122,18 @@ int he_encode_plain_batch(he_ctx *ctx, const double *vals, int count, int nvals,
  * constant over the occupied span (engine.py:291-295, conv.py:160-166);
  * residues host [count][ell].  mul_const: scalar plaintext product
  * (mult_plain before its rescale, engine.py:297-304); residues [count][ell]. */
+/* he_encode_plain_batch for complex slot vectors: slot i = re[i] + j im[i]
+ * (device arrays [count][nvals]).  Used for the CoeffToSlot / SlotToCoeff
+ * diagonals of bootstrapping (engine.bootstrap; the reference's bootstrap,
+ * /root/reference/pkg/src/hebatch/engine.py:315-327, is level accounting only). */
+int he_encode_plain_batch_c(he_ctx *ctx, const double *re, const double *im, int count, int nvals, double scale,
+                            int ell, uint64_t *pt_out, void *stream);
+/* ModRaise: read each 2-component ciphertext of `in` (ell_in limbs) at level 0
+ * (limb q_0) and lift it centred to ell_out limbs (INTT, lift, NTT): the result
+ * decrypts to m + q_0 I(X).  First step of engine.bootstrap. */
+int he_mod_raise(he_ctx *ctx, const uint64_t *const *in, int ell_in, uint64_t *const *out, int count, int ell_out,
+                 void *stream);
+
 int he_add(he_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out,
            int count, int ell, int n_comp, void *stream);
 int he_sub(he_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out,

@@ -378,10 +378,20 @@ static void fft(const oc_ctx *c, double *re, double *im, int sign) {
 }
 
 void oc_encode(const oc_ctx *c, const double *vals, int nvals, double scale, int64_t *m_out) {
+    oc_encode_c(c, vals, NULL, nvals, scale, m_out);
+}
+
+/* complex slots z_i = vals[i] + j vals_im[i] (vals_im may be NULL): the same
+ * inverse canonical embedding; used by the bootstrap circuit's DFT diagonals */
+void oc_encode_c(const oc_ctx *c, const double *vals, const double *vals_im, int nvals, double scale,
+                 int64_t *m_out) {
     int n = c->nslots;
     double *re = (double *)calloc(n, sizeof(double));
     double *im = (double *)calloc(n, sizeof(double));
-    for (int i = 0; i < nvals && i < n; i++) re[c->pos[i]] = vals[i];
+    for (int i = 0; i < nvals && i < n; i++) {
+        re[c->pos[i]] = vals[i];
+        if (vals_im) im[c->pos[i]] = vals_im[i];
+    }
     fft(c, re, im, -1);
     double inv_n = 1.0 / (double)n; /* exact: n is a power of two */
     for (int j = 0; j < n; j++) {

@@ -59,6 +59,7 @@ def lib():
         L.oc_ntt.argtypes = [vp, u64p, C.c_int]
         L.oc_intt.argtypes = [vp, u64p, C.c_int]
         L.oc_encode.argtypes = [vp, dp, C.c_int, C.c_double, i64p]
+        L.oc_encode_c.argtypes = [vp, dp, dp, C.c_int, C.c_double, i64p]
         L.oc_decode.argtypes = [vp, dp, C.c_double, dp]
         L.oc_secret_key.argtypes = [vp, u64p]
         L.oc_gen_switch_key.argtypes = [vp, C.c_uint32, u64p]
@@ -172,6 +173,28 @@ class Oracle:
         m = np.zeros(self.N, np.int64)
         lib().oc_encode(self._h, _p(v, C.c_double), v.size, scale or self.scale, _p(m, C.c_int64))
         return m
+
+    def encode_complex(self, vals, scale=None):
+        """Complex slot vector -> plaintext coefficients (oc_encode_c)."""
+        v = np.asarray(vals, dtype=np.complex128)
+        re, im = np.ascontiguousarray(v.real), np.ascontiguousarray(v.imag)
+        m = np.zeros(self.N, np.int64)
+        lib().oc_encode_c(self._h, _p(re, C.c_double), _p(im, C.c_double), v.size, scale or self.scale,
+                          _p(m, C.c_int64))
+        return m
+
+    def mod_raise(self, ct, ell_out):
+        """ModRaise (bootstrapping's first step): limb 0 of each component, INTT,
+        centred lift mod q_0, then every limb of the chain q_0..q_{ell_out-1}, NTT."""
+        ct = np.ascontiguousarray(ct, dtype=np.uint64)
+        q0 = self.moduli[0]
+        out = np.zeros((ct.shape[0], ell_out, self.N), np.uint64)
+        for comp in range(ct.shape[0]):
+            v = self.intt(ct[comp, 0], 0)
+            cv = np.where(v > np.uint64(q0 // 2), v.astype(np.int64) - np.int64(q0), v.astype(np.int64))
+            for l in range(ell_out):
+                out[comp, l] = self.ntt(np.mod(cv, np.int64(self.moduli[l])).astype(np.uint64), l)
+        return out
 
     def decode(self, coeffs, scale):
         c = np.ascontiguousarray(coeffs, dtype=np.float64)

@@ -29,7 +29,7 @@ HE_OK, HE_EINVAL, HE_ECUDA, HE_ENOKEY, HE_ELEVEL, HE_ENOMEM, HE_ECONTEXT, HE_ELE
 EXPORTS = [
     "he_last_error", "he_abi_version", "he_ctx_create", "he_ctx_destroy", "he_ctx_moduli",
     "he_gen_switch_key", "he_drop_switch_key", "he_has_switch_key", "he_export_secret_key",
-    "he_export_switch_key", "he_import_switch_key", "he_lincomb_plain", "he_encode_plain_batch", "he_ntt", "he_encrypt", "he_encrypt_level", "he_decrypt", "he_decrypt_coeffs",
+    "he_export_switch_key", "he_import_switch_key", "he_lincomb_plain", "he_encode_plain_batch", "he_encode_plain_batch_c", "he_mod_raise", "he_ntt", "he_encrypt", "he_encrypt_level", "he_decrypt", "he_decrypt_coeffs",
     "he_encode_plain", "he_add", "he_sub", "he_add_const", "he_mul_const", "he_mul_plain",
     "he_drop_limbs", "he_tensor", "he_relin", "he_keyswitch", "he_rescale", "he_mult_ct",
     "he_automorphism", "he_rotate", "he_lincomb", "he_sync", "he_launch_count", "he_lincomb_grouped",
@@ -99,6 +99,8 @@ def load():
         "he_import_switch_key": (i, [vp, u32, vp, vp]),
         "he_lincomb_plain": (i, [vp, vp, i, vp, vp, i, i, vp]),
         "he_encode_plain_batch": (i, [vp, vp, i, i, dbl, i, vp, vp]),
+        "he_encode_plain_batch_c": (i, [vp, vp, vp, i, i, dbl, i, vp, vp]),
+        "he_mod_raise": (i, [vp, pp, i, pp, i, i, vp]),
         "he_ntt": (i, [vp, vp, i, i, i, vp]),
         "he_encrypt": (i, [vp, vp, i, i, dbl, u32, pp, vp]),
         "he_encrypt_level": (i, [vp, vp, i, i, dbl, u32, i, pp, vp]),

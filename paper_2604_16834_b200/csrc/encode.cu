@@ -347,7 +347,7 @@ struct Buf {
 
 // encode `count` vectors into c0-limb residues of `out` cts (L limbs each)
 int encode_into(he_ctx *c, const double *vals, int count, int nvals, double scale, uint64_t *const *out_dev, int L,
-                int add_error, uint32_t ct_index0, cudaStream_t s) {
+                int add_error, uint32_t ct_index0, cudaStream_t s, const double *vals_im = nullptr) {
     size_t n = c->nslots;
     Buf b(s);
     HE_TRY(he_scratch_alloc(&b.p, (size_t)count * n * 16, s));
@@ -356,6 +356,11 @@ int encode_into(he_ctx *c, const double *vals, int count, int nvals, double scal
     if (nvals > 0) {
         k_scatter_slots2<<<gridn((size_t)count * nvals), EW, 0, s>>>(re, vals, count, nvals, (int)n, c->d_slot_brv);
         HE_CHECK_LAUNCH();
+        if (vals_im) {  // complex slots: the imaginary parts go through the same scatter
+            k_scatter_slots2<<<gridn((size_t)count * nvals), EW, 0, s>>>(im, vals_im, count, nvals, (int)n,
+                                                                         c->d_slot_brv);
+            HE_CHECK_LAUNCH();
+        }
     }
     HE_TRY(run_fft(c, re, im, count, -1, s));
     k_encode_finish<<<gridn((size_t)count * n), EW, 0, s>>>(out_dev, re, im, count, c->logN, L, scale, c->d_twist,
@@ -484,6 +489,29 @@ extern "C" int he_encode_plain_batch(he_ctx *c, const double *vals, int count, i
     Buf ptrs(s);
     HE_TRY(he_upload_ptrs((const void *const *)h.data(), count, (void ***)&ptrs.p, s));
     HE_TRY(encode_into(c, vals, count, nvals, scale, (uint64_t *const *)ptrs.p, ell, 0, 0, s));
+    HE_TRY(he_ntt_fwd(c, pt_out, count * ell, c->d_ident, ell, s));
+    return HE_OK;
+}
+
+// complex slot vectors (bootstrapping's CoeffToSlot / SlotToCoeff diagonals):
+// slot i = re[i] + j im[i]; otherwise identical to he_encode_plain_batch
+extern "C" int he_encode_plain_batch_c(he_ctx *c, const double *re, const double *im, int count, int nvals,
+                                       double scale, int ell, uint64_t *pt_out, void *stream) {
+    if (!c || count < 0 || nvals < 0 || ell < 1 || ell > c->L || !pt_out || !(scale > 0) || (nvals && (!re || !im))) {
+        he_set_error("he_encode_plain_batch_c: bad arguments");
+        return HE_EINVAL;
+    }
+    if (nvals > c->nslots) {
+        he_set_error("%d values > %d slots", nvals, c->nslots);
+        return HE_ELENGTH;
+    }
+    if (!count) return HE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<const uint64_t *> h(count);
+    for (int i = 0; i < count; i++) h[i] = pt_out + (size_t)i * ell * c->N;
+    Buf ptrs(s);
+    HE_TRY(he_upload_ptrs((const void *const *)h.data(), count, (void ***)&ptrs.p, s));
+    HE_TRY(encode_into(c, re, count, nvals, scale, (uint64_t *const *)ptrs.p, ell, 0, 0, s, im));
     HE_TRY(he_ntt_fwd(c, pt_out, count * ell, c->d_ident, ell, s));
     return HE_OK;
 }

@@ -10,6 +10,7 @@
 //   conv_forward k=1 fold loop conv.py:137-156     -> k_lincomb (one launch)
 // Arithmetic contract: DESIGN.md section 2; oracle/ckks_oracle.c restates it.
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 
@@ -563,6 +564,68 @@ extern "C" int he_drop_limbs(he_ctx *c, const uint64_t *const *in, uint64_t *con
     k_drop<<<grid_ew((size_t)nc * ell_out * c->N, count), EW, 0, s>>>(O.as<uint64_t>(), I.as<const uint64_t>(), count,
                                                                        ell_in, ell_out, nc, c->logN);
     HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+// ---------------------------------------------------------------- bootstrapping: ModRaise
+// limb 0 (q_0) of both components -> t[2 ct + comp] (coefficient domain after the INTT)
+__global__ void k_take_limb0(uint64_t *t, const uint64_t *const *in, int count, int ell_in, int logN) {
+    const size_t N = (size_t)1 << logN;
+    for (int ct = blockIdx.y; ct < count; ct += gridDim.y)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 2 * N; i += (size_t)gridDim.x * blockDim.x) {
+            const size_t comp = i >> logN, k = i & (N - 1);
+            t[((size_t)ct * 2 + comp) * N + k] = in[ct][comp * ((size_t)ell_in << logN) + k];
+        }
+}
+
+// centred lift of a residue mod q_0 to every limb of the output chain:
+// v in [0, q_0) -> v - q_0 [v > q_0 / 2] -> mod q_l  (coefficient domain)
+__global__ void k_mod_raise_lift(uint64_t *const *out, const uint64_t *t, int count, int ell_out, int logN,
+                                 const ModConst *mc) {
+    const size_t N = (size_t)1 << logN;
+    const uint64_t q0 = mc[0].q;
+    for (int ct = blockIdx.y; ct < count; ct += gridDim.y)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 2 * N; i += (size_t)gridDim.x * blockDim.x) {
+            const size_t comp = i >> logN, k = i & (N - 1);
+            const uint64_t v = t[((size_t)ct * 2 + comp) * N + k];
+            const int64_t cv = v > (q0 >> 1) ? (int64_t)v - (int64_t)q0 : (int64_t)v;
+            uint64_t *O = out[ct] + comp * ((size_t)ell_out << logN) + k;
+            for (int l = 0; l < ell_out; l++) O[(size_t)l << logN] = smod64(cv, mc[l].q);
+        }
+}
+
+// ModRaise (the first step of CKKS bootstrapping): a ciphertext read at level 0
+// (limb q_0 of `in`, which may hold more limbs) is reinterpreted over the full
+// chain q_0 .. q_{ell_out-1}: INTT of limb 0, centred lift of each coefficient
+// into every limb, NTT.  Decrypts to m + q_0 I(X) with a small integer
+// polynomial I; the EvalMod step of the bootstrap circuit removes q_0 I.
+extern "C" int he_mod_raise(he_ctx *c, const uint64_t *const *in, int ell_in, uint64_t *const *out, int count,
+                            int ell_out, void *stream) {
+    HE_TRY(check_basic(c, count, ell_out, 2, "he_mod_raise"));
+    if (ell_in < 1 || ell_in > c->L) {
+        he_set_error("he_mod_raise: ell_in=%d not in [1, %d]", ell_in, c->L);
+        return HE_EINVAL;
+    }
+    if (!count) return HE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    DevPtrs I(s), O(s), O2(s);
+    HE_TRY(I.up((const void *const *)in, count));
+    HE_TRY(O.up((const void *const *)out, count));
+    std::vector<const uint64_t *> halves(2 * (size_t)count);
+    for (int i = 0; i < count; i++) {
+        halves[2 * i] = out[i];
+        halves[2 * i + 1] = out[i] + (size_t)ell_out * c->N;
+    }
+    HE_TRY(O2.up((const void *const *)halves.data(), 2 * count));
+    Scratch t(s);
+    HE_TRY(t.alloc((size_t)count * 2 * c->N * 8));
+    k_take_limb0<<<grid_ew(2 * (size_t)c->N, count), EW, 0, s>>>(t.u(), I.as<const uint64_t>(), count, ell_in, c->logN);
+    HE_CHECK_LAUNCH();
+    HE_TRY(he_ntt_inv(c, t.u(), 2 * count, c->d_ident, 1, s));
+    k_mod_raise_lift<<<grid_ew(2 * (size_t)c->N, count), EW, 0, s>>>(O.as<uint64_t>(), t.u(), count, ell_out, c->logN,
+                                                                      c->d_mc);
+    HE_CHECK_LAUNCH();
+    HE_TRY(he_ntt_fwd_ptrs(c, O2.as<uint64_t>(), 2 * count, ell_out, c->d_ident, s));
     return HE_OK;
 }
 

@@ -674,6 +674,18 @@ class GpuEngine:
                 raise MissingRotationKey(k)
             if k % self.context.n and k % self.context.n not in live:
                 live.append(k % self.context.n)
+        outs = self._rotate_hoisted_internal(cts, ks)
+        for k in ks:
+            if k % self.context.n:
+                self._acct.bump("rotations", len(cts))
+        return outs
+
+    def _rotate_hoisted_internal(self, cts: Sequence[CipherVec], ks: Sequence[int]) -> list[list[CipherVec]]:
+        """rotate_hoisted without key-set checks or counters (the keys must exist in the library)."""
+        live = []
+        for k in ks:
+            if k % self.context.n and k % self.context.n not in live:
+                live.append(k % self.context.n)
         res = {}
         if live:
             level = cts[0].level
@@ -686,19 +698,14 @@ class GpuEngine:
             wrapped = self._wrap_batch(out, level, [c.scale for c in cts] * len(live))
             for j, k in enumerate(live):
                 res[k] = wrapped[j * len(cts):(j + 1) * len(cts)]
-        outs = []
-        for k in ks:
-            kk = k % self.context.n
-            if kk == 0:
-                outs.append(list(cts))
-            else:
-                outs.append(res[kk])
-                self._acct.bump("rotations", len(cts))
-        return outs
+        return [list(cts) if k % self.context.n == 0 else res[k % self.context.n] for k in ks]
 
     def _rotate_batch(self, cts: Sequence[CipherVec], k: int) -> list[CipherVec]:
+        return self._automorph_batch(cts, pow(5, k % self.context.n, 2 * self.N))
+
+    def _automorph_batch(self, cts: Sequence[CipherVec], g: int) -> list[CipherVec]:
+        """X -> X^g plus key switch with the Galois key of g (5^k: rotation by k; 2N - 1: conjugation)."""
         level = cts[0].level
-        g = pow(5, k % self.context.n, 2 * self.N)
         out = self._alloc(len(cts), 2, level + 1)
         src = self._ptrs(cts)
         dst = self._tptrs(out)
@@ -988,6 +995,41 @@ class GpuEngine:
                                         self.stream), "mul_const")
         return self._rescale_tensor(tmp, limbs, outs)
 
+    def _mul_monomial_batch(self, cts: Sequence[CipherVec], power: int) -> list[CipherVec]:
+        """ct_i * X^power (exact, no rescale, no level): an element-wise product
+        with the NTT of the monomial (X^n multiplies every slot by i)."""
+        torch = _torch()
+        level = cts[0].level
+        limbs = level + 1
+        key = (power % (2 * self.N), limbs)
+        cache = self.__dict__.setdefault("_mono", {})
+        if key not in cache:
+            e = torch.zeros((limbs, self.N), dtype=torch.int64, device=self.device)
+            p = power % (2 * self.N)
+            for l in range(limbs):
+                e[l, p % self.N] = 1 if p < self.N else self.moduli[l] - 1  # X^N = -1
+            _lib.check(self._L.he_ntt(self._h, e.data_ptr(), 1, limbs, 0, self.stream), "monomial ntt")
+            cache[key] = e
+        pt = cache[key]
+        nc = self._ncomp(cts)
+        out = self._alloc(len(cts), nc, limbs)
+        pi, po = self._ptrs(cts), self._tptrs(out)
+        _lib.check(self._L.he_mul_plain(self._h, _lib.addr(pi), pt.data_ptr(), _lib.addr(po), len(cts), limbs, nc,
+                                        self.stream), "mul_monomial")
+        return self._wrap_batch(out, level, [c.scale for c in cts])
+
+    def _mul_int_batch(self, cts: Sequence[CipherVec], ks: Sequence[int], out_scales: Sequence[float]) -> list[CipherVec]:
+        """ct_i * ks[i] (an exact integer constant) then rescale; declared scales out_scales (no counters)."""
+        level = cts[0].level
+        limbs = level + 1
+        res = np.array([self._res(int(k), limbs) for k in ks], np.uint64)
+        nc = self._ncomp(cts)
+        tmp = self._alloc(len(cts), nc, limbs)
+        pi, pm = self._ptrs(cts), self._tptrs(tmp)
+        _lib.check(self._L.he_mul_const(self._h, _lib.addr(pi), _lib.addr(pm), len(cts), limbs, nc, _lib.addr(res),
+                                        self.stream), "mul_const")
+        return self._rescale_tensor(tmp, limbs, list(out_scales))
+
     def rescale_batch(self, cts: Sequence[CipherVec], out_scale: float | None = None) -> list[CipherVec]:
         """Divide-and-round by the last prime (one level); the declared output
         scale is ``out_scale`` when given (callers that encoded weights for an
@@ -1081,9 +1123,55 @@ class GpuEngine:
             out[i].copy_(c.data[:, : level + 1])
         return self._wrap_batch(out, level, [c.scale for c in cts])
 
+    def boot_plan(self):
+        """The bootstrap circuit's parameters for this ring (bootstrap.BootPlan)."""
+        from .bootstrap import BootPlan
+
+        if getattr(self, "_bplan", None) is None:
+            self._bplan = BootPlan(N=self.N, q0=self.moduli[0])
+        return self._bplan
+
+    def _ensure_boot_keys(self, plan) -> None:
+        self._ensure_relin()
+        gs = [pow(5, k, 2 * self.N) for k in plan.rotation_offsets()] + [2 * self.N - 1]
+        for g in gs:
+            if not self._L.he_has_switch_key(self._h, g):
+                _lib.check(self._L.he_gen_switch_key(self._h, g, self.stream), "bootstrap keygen")
+
     def bootstrap(self, ct: CipherVec) -> CipherVec:
+        """Real CKKS bootstrapping (bootstrap.py: ModRaise, CoeffToSlot, EvalMod,
+        SlotToCoeff) with the reference's contract (engine.py:315-319): the
+        result holds the same slots (up to the circuit's approximation error,
+        ~1e-5 with q_0 / scale = 2^10 and a 2^50 scale) at level
+        max_level - bootstrap_reserve, and only the ``bootstraps`` counter
+        moves.  The circuit needs bootstrap_reserve >= its depth
+        (BootPlan.depth, 17 at N = 2^12); its Galois keys (BSGS steps and
+        conjugation) are generated on first use."""
+        from .bootstrap import Bootstrapper, GpuBootOps
+
         self._check(ct)
-        raise HebatchError("bootstrapping is not part of the B200 engine (no BASELINE configuration bootstraps)")
+        self._need_two([ct], "bootstrap")
+        plan = self.boot_plan()
+        target = self.context.max_level - self.context.bootstrap_reserve
+        if self.context.max_level - plan.depth < target:
+            raise HebatchError(f"bootstrap_reserve {self.context.bootstrap_reserve} is below the bootstrap circuit's "
+                               f"depth {plan.depth}")
+        self._ensure_boot_keys(plan)
+        if getattr(self, "_booter", None) is None:
+            self._booter = Bootstrapper(GpuBootOps(self), plan)
+        with self._acct.lock:
+            saved = (dict(self._acct.counts), self._acct.peak, self._acct.window_peak, set(self._acct.live))
+        out = self._booter.run(ct, self.context.n_q)
+        if out.level > target:
+            out = self.drop_level_batch([out], target)[0]
+        with self._acct.lock:  # circuit temporaries are not user-visible ciphertexts
+            counts, peak, wpeak, live = saved
+            self._acct.counts = counts
+            self._acct.live = live | {out.id}
+            self._acct.peak = max(peak, len(self._acct.live))
+            self._acct.window_peak = max(wpeak, len(self._acct.live))
+        self._acct.bump("bootstraps")
+        return out
 
     def ensure_level(self, ct: CipherVec, needed: int) -> CipherVec:
         if ct.level >= needed:
@@ -1240,7 +1328,7 @@ class GpuEngine:
     # plaintext bytes one he_lincomb_plain launch may hold (larger folds are split over outputs)
     PLAIN_CHUNK_BYTES = 4 << 30
 
-    def lincomb_plain(self, inputs: Sequence[CipherVec], plains, n_out: int) -> list[CipherVec]:
+    def lincomb_plain(self, inputs: Sequence[CipherVec], plains, n_out: int, pt_scale: float = 1.0) -> list[CipherVec]:
         """The batched channel-by-channel fold (conv.py:137-156 as one kernel):
         out[o] = rescale(sum_j inputs[j] (.) encode(plains[o, j], q_last)) for
         full-width float64 plaintext slot vectors plains [n_out][n_in][<= n].
@@ -1248,7 +1336,10 @@ class GpuEngine:
         (he_encode_plain_batch), the products are summed exactly
         (he_lincomb_plain) and each output is rescaled ONCE, so the output
         scale is the input scale and the level drops by one, as for the
-        reference's per-term mult_plain + add fold.  Counters are the caller's."""
+        reference's per-term mult_plain + add fold.  Counters are the caller's.
+        ``pt_scale`` != 1 encodes the plaintexts at q_last * pt_scale (more
+        precision for small plaintext values) and declares the outputs at
+        scale(input) * pt_scale."""
         torch = _torch()
         for c in inputs:
             self._check(c)
@@ -1259,12 +1350,14 @@ class GpuEngine:
             raise HebatchError("lincomb_plain needs inputs at one level and scale")
         if level < self.context.mult_level_cost:
             raise LevelExhausted(f"level {level} < multiplication cost {self.context.mult_level_cost}")
-        P = torch.as_tensor(np.asarray(plains, np.float64) if not isinstance(plains, torch.Tensor) else plains,
-                            dtype=torch.float64, device=self.device)
+        if not isinstance(plains, torch.Tensor):
+            plains = np.asarray(plains)
+        cplx = plains.is_complex() if isinstance(plains, torch.Tensor) else np.iscomplexobj(plains)
+        P = torch.as_tensor(plains, dtype=torch.complex128 if cplx else torch.float64, device=self.device)
         if P.dim() != 3 or P.shape[0] != n_out or P.shape[1] != n_in or P.shape[2] > self.context.n:
             raise ShapeMismatch(f"plains {tuple(P.shape)} for {n_out} outputs x {n_in} inputs x <= {self.context.n}")
         limbs = level + 1
-        ql = float(self.moduli[limbs - 1])
+        ql = float(self.moduli[limbs - 1]) * pt_scale
         pin = self._ptrs(inputs)
         acc = self._alloc(n_out, 2, limbs)
         per_out = n_in * limbs * self.N * 8
@@ -1273,9 +1366,17 @@ class GpuEngine:
             o1 = min(n_out, o0 + step)
             vals = P[o0:o1].reshape((o1 - o0) * n_in, P.shape[2]).contiguous()
             pt = torch.empty(((o1 - o0) * n_in, limbs, self.N), dtype=torch.int64, device=self.device)
-            _lib.check(self._call("encode_plain", self._L.he_encode_plain_batch, self._h, vals.data_ptr(),
-                                  vals.shape[0], vals.shape[1], ql, limbs, pt.data_ptr(), self.stream,
-                                  units=(vals.numel() * 8.0 + pt.numel() * 8.0, 0.0)), "encode_plain_batch")
+            if cplx:  # complex slot vectors (bootstrap DFT diagonals)
+                vr, vi = vals.real.contiguous(), vals.imag.contiguous()
+                _lib.check(self._call("encode_plain", self._L.he_encode_plain_batch_c, self._h, vr.data_ptr(),
+                                      vi.data_ptr(), vals.shape[0], vals.shape[1], ql, limbs, pt.data_ptr(),
+                                      self.stream, units=(vals.numel() * 16.0 + pt.numel() * 8.0, 0.0)),
+                           "encode_plain_batch_c")
+                del vr, vi
+            else:
+                _lib.check(self._call("encode_plain", self._L.he_encode_plain_batch, self._h, vals.data_ptr(),
+                                      vals.shape[0], vals.shape[1], ql, limbs, pt.data_ptr(), self.stream,
+                                      units=(vals.numel() * 8.0 + pt.numel() * 8.0, 0.0)), "encode_plain_batch")
             ppt = self._tptrs(pt)
             pout = _lib.ptr_array([acc.data_ptr() + o * acc.stride(0) * 8 for o in range(o0, o1)])
             poly = 2 * limbs * self.N
@@ -1284,7 +1385,7 @@ class GpuEngine:
                                   units=(((o1 - o0) * n_in * limbs * self.N + (n_in + o1 - o0) * poly) * 8.0,
                                          float((o1 - o0) * n_in) * poly)), "lincomb_plain")
             del pt
-        return self._rescale_tensor(acc, limbs, [s_in] * n_out)
+        return self._rescale_tensor(acc, limbs, [s_in * pt_scale] * n_out)
 
     def conv_mma(self, inputs: Sequence[CipherVec], gcol, out_base, out_stride: int, weights, n_out: int,
                  weight_scale: float, bias=None) -> list[CipherVec] | None:

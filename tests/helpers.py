@@ -20,15 +20,21 @@ PARAMS = {
     "p15": (15, (60, 46, 46, 46, 46, 46), (60, 60), 2, 46),
     # config 3's 9-limb carry plan (inputs at 9 of 14 limbs) on a 64-point ring (CPU tests)
     "carry9": (6, (40,) * 9, (42,) * 3, 3, 40),
+    # bootstrapping rings (bootstrap.py): q_0 of 60 bits over 50-bit rescale primes at
+    # scale 2^50 (q_0 / scale = 2^10); depth 15 at N = 64, 18 at N = 2^11 / 2^12
+    "boot6": (6, (60,) + (50,) * 16, (60,) * 3, 3, 50),
+    "boot11": (11, (60,) + (50,) * 22, (60,) * 3, 3, 50),
+    "boot12": (12, (60,) + (50,) * 22, (60,) * 3, 3, 50),
 }
 
 
-def engine_context(name, seed=1):
+def engine_context(name, seed=1, bootstrap_reserve=1):
     from paper_2604_16834_b200.engine import EngineContext
 
     log_n, qb, pb, alpha, sb = PARAMS[name]
     L = len(qb)
-    return EngineContext(n=1 << (log_n - 1), max_level=L - 1, bootstrap_reserve=1, first_modulus_bits=qb[0],
+    return EngineContext(n=1 << (log_n - 1), max_level=L - 1, bootstrap_reserve=bootstrap_reserve,
+                         first_modulus_bits=qb[0],
                          rescale_bits=qb[-1] if L > 1 else qb[0], key_switch_digits=-(-L // alpha),
                          noise_seed=seed, special_prime_bits=tuple(pb), scale_bits=sb, q_bits=tuple(qb))
 
