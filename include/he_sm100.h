@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define HE_ABI_VERSION 1
+#define HE_ABI_VERSION 2
 
 enum {
     HE_OK = 0,
@@ -57,6 +57,9 @@ typedef struct {
     int32_t p_bits[16];
     uint64_t seed;        /* Philox4x32-10 key for every random stream     */
     double scale;         /* default encoding scale Delta                  */
+    int32_t sk_hamming;   /* 0: dense ternary secret; h > 0: sparse secret  */
+                          /* with expected Hamming weight h (bootstrapping) */
+    int32_t reserved;
 } he_params;
 
 typedef struct he_ctx he_ctx;

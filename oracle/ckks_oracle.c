@@ -156,10 +156,19 @@ static uint64_t sample_uniform(const oc_ctx *c, uint32_t dom, uint32_t obj, uint
     u128 mid = (u128)(uint64_t)ph + (pl >> 64);
     return (uint64_t)(ph >> 64) + (uint64_t)(mid >> 64);
 }
+/* secret coefficient j: dense ternary (r mod 3) - 1, or, for sk_hamming = h > 0,
+ * nonzero with probability h / N (a second Philox draw below floor(h 2^32 / N))
+ * and sign from the low bit of the first draw */
 static int64_t sample_ternary(const oc_ctx *c, uint32_t j) {
     uint32_t r[4];
     rnd4(c, DOM_SK, 0, 0, j >> 2, r);
-    return (int64_t)(r[j & 3] % 3u) - 1;
+    if (c->prm.sk_hamming <= 0) return (int64_t)(r[j & 3] % 3u) - 1;
+    uint32_t r2[4];
+    rnd4(c, DOM_SK, 1, 0, j >> 2, r2);
+    uint64_t t = ((uint64_t)c->prm.sk_hamming << 32) / (uint64_t)c->N;
+    uint32_t thr = t > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t;
+    if (r2[j & 3] >= thr) return 0;
+    return (r[j & 3] & 1u) ? 1 : -1;
 }
 
 /* ---------------------------------------------------------------- setup */

@@ -30,6 +30,8 @@ class OcParams(C.Structure):
         ("p_bits", C.c_int32 * 16),
         ("seed", C.c_uint64),
         ("scale", C.c_double),
+        ("sk_hamming", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -107,8 +109,9 @@ def philox(ctr, key):
     return list(o)
 
 
-def make_params(log_n, q_bits, p_bits, alpha, seed, scale):
+def make_params(log_n, q_bits, p_bits, alpha, seed, scale, sk_hamming=0):
     p = OcParams()
+    p.sk_hamming = sk_hamming
     p.log_n = log_n
     p.n_q = len(q_bits)
     p.n_p = len(p_bits)
@@ -125,8 +128,9 @@ def make_params(log_n, q_bits, p_bits, alpha, seed, scale):
 class Oracle:
     """One oracle context: moduli, twiddles, secret key (from params.seed)."""
 
-    def __init__(self, log_n, q_bits, p_bits, alpha, seed=0, scale=2.0 ** 40):
-        self.params = make_params(log_n, q_bits, p_bits, alpha, seed, scale)
+    def __init__(self, log_n, q_bits, p_bits, alpha, seed=0, scale=2.0 ** 40, sk_hamming=0):
+        self.params = make_params(log_n, q_bits, p_bits, alpha, seed, scale, sk_hamming)
+        self.sk_hamming = sk_hamming
         self.N = 1 << log_n
         self.n = self.N // 2
         self.L = len(q_bits)

@@ -62,6 +62,8 @@ class HeParams(C.Structure):
         ("p_bits", C.c_int32 * 16),
         ("seed", C.c_uint64),
         ("scale", C.c_double),
+        ("sk_hamming", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -151,7 +153,7 @@ def load():
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args
-    if L.he_abi_version() != 1:
+    if L.he_abi_version() != 2:  # 2: he_params.sk_hamming
         raise HebatchError("libhe_sm100.so ABI version mismatch")
     _lib = L
     return L

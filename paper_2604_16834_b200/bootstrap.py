@@ -53,16 +53,148 @@ import numpy as np
 
 from .errors import HebatchError
 
-THETA_MAX = 1.25     # |theta| bound for the degree-14 Taylor cosine
-CTS_PT_BITS = 20     # CoeffToSlot diagonals (|d| = 1/n) are encoded at q_l 2^20: their
-                     # plaintext coefficients (~ q_l / n^1.5) keep ~55 bits
+THETA_MAX = 1.25     # |theta| bound for the degree-14 / -15 Taylor cosine / sine
+PT_BITS = 60         # encoded DFT diagonals: |coefficient| < 2^60 (int64 encode), see _pt_scale
+CTS_GROWTH_BITS = 20  # total scale growth allowed to CoeffToSlot's plaintext encodings
 TAYLOR_TERMS = 8     # cos / sin(theta): 8 Taylor terms each (degrees 14 / 15)
 
 
-def secret_bound(N: int, sigma_mult: float = 6.0) -> float:
-    """Bound K on |I_j| after ModRaise for the dense ternary secret (each
-    coefficient of c1 s is a sum of ~2N/3 terms uniform in (-q_0/2, q_0/2])."""
-    return sigma_mult * math.sqrt((2.0 * N / 3.0) / 12.0) + 1.0
+def secret_bound(N: int, hamming: int = 0, sigma_mult: float = 6.0) -> float:
+    """Bound K on |I_j| after ModRaise: each coefficient of c1 s is a sum of
+    h terms uniform in (-q_0/2, q_0/2] (h ~ 2N/3 for the dense ternary secret,
+    the expected weight plus 4 standard deviations for a sparse one)."""
+    h = 2.0 * N / 3.0 if hamming <= 0 else hamming + 4.0 * math.sqrt(hamming)
+    return sigma_mult * math.sqrt(h / 12.0) + 1.0
+
+
+# ------------------------------------------------------------------ the factored DFT
+# Slots z = V u with u_j = t_j + i t_{j+n} and V[i][j] = zeta^{5^i j}.  Splitting
+# u into even / odd j halves the problem: the roots zeta^{5^i} square to the
+# half-size roots and zeta^{5^{i + n/2}} = -zeta^{5^i}, so
+#     V = B_m ... B_1 R        (m = log2 n, R = bit reversal of j)
+# where stage B_k (block size 2^k, h = 2^(k-1)) is the butterfly
+#     y_i = x_i + w_i x_{i+h},  y_{i+h} = x_i - w_i x_{i+h}   (i mod 2^k < h)
+# with w_i = zeta^{5^i n / 2^k}: a map with three diagonals (rotations 0, +h, -h).
+# SlotToCoeff applies B_1 .. B_m to bit-reversed coefficients and CoeffToSlot
+# applies B_m^-1 .. B_1^-1 (leaving the coefficients bit-reversed, which the
+# slot-wise EvalMod does not mind); consecutive stages are merged into a few
+# levels of 2^(t+1) - 1 diagonals each.
+
+
+def _pow5(n: int, N: int) -> np.ndarray:
+    out = np.empty(n, np.int64)
+    g = 1
+    for i in range(n):
+        out[i] = g
+        g = (g * 5) % (2 * N)
+    return out
+
+
+def _rot(x: np.ndarray, k: int) -> np.ndarray:
+    return np.roll(x, -k)
+
+
+def compose(A: dict, B: dict, n: int) -> dict:
+    """Diagonal form of A after B: (A B) x = sum_{r,s} (A_r (.) rot_r(B_s)) (.) rot_{r+s}(x)."""
+    out: dict = {}
+    for r, a in A.items():
+        for s_, b in B.items():
+            o = (r + s_) % n
+            out[o] = out.get(o, 0) + a * _rot(b, r)
+    return out
+
+
+def apply_map(D: dict, x: np.ndarray) -> np.ndarray:
+    return sum(d * _rot(x, o) for o, d in D.items())
+
+
+def butterfly_stages(N: int, inverse: bool = False) -> list[dict]:
+    """[B_1 .. B_m] (inverse: [B_1^-1 .. B_m^-1]) as {offset: diagonal} maps."""
+    n = N // 2
+    m = n.bit_length() - 1
+    p5 = _pow5(n, N)
+    i = np.arange(n)
+    out = []
+    for k in range(1, m + 1):
+        blk, h = 1 << k, 1 << (k - 1)
+        w = np.exp(1j * np.pi * ((p5 * (n // blk)) % (2 * N)) / N)
+        lo = (i % blk) < h
+        wl = np.roll(w, h)                           # w_{i-h} at the upper rows
+        if not inverse:
+            d0 = np.where(lo, 1.0 + 0j, -wl)
+            dp = np.where(lo, w, 0j)
+            dm = np.where(lo, 0j, 1.0 + 0j)
+        else:                                        # x_i = (y_i + y_{i+h}) / 2, x_{i+h} = (y_i - y_{i+h}) / (2 w_i)
+            d0 = np.where(lo, 0.5 + 0j, -0.5 / wl)
+            dp = np.where(lo, 0.5 + 0j, 0j)
+            dm = np.where(lo, 0j, 0.5 / wl)
+        if h == n - h:
+            out.append({0: d0, h: dp + dm})
+        else:
+            out.append({0: d0, h: dp, n - h: dm})
+    return out
+
+
+def dft_groups(N: int, levels: int, inverse: bool) -> list[tuple[int, dict]]:
+    """Merged stage groups in application order, each as (h0, map): SlotToCoeff
+    applies B_1 .. B_m, CoeffToSlot B_m^-1 .. B_1^-1; h0 is the group's
+    smallest butterfly distance (every offset is a multiple of it)."""
+    n = N // 2
+    st = butterfly_stages(N, inverse)
+    m = len(st)
+    order = list(range(m)) if not inverse else list(range(m - 1, -1, -1))
+    levels = max(1, min(levels, m))
+    bounds = [round(g * m / levels) for g in range(levels + 1)]
+    out = []
+    for g in range(levels):
+        idx = order[bounds[g]:bounds[g + 1]]
+        M = st[idx[0]]
+        for k in idx[1:]:
+            M = compose(st[k], M, n)
+        out.append((1 << min(idx), {o: d for o, d in M.items() if np.any(d != 0)}))
+    return out
+
+
+@dataclass
+class BsgsStage:
+    """One merged DFT level as a baby-step / giant-step plan: offsets
+    o = (base + g b + j) h0 (j < b baby steps, g < G giant steps) and the
+    plaintexts p[g][j] = roll(D[o], (base + g b) h0)."""
+
+    h0: int
+    base: int
+    baby: int
+    giant: int
+    rows: list             # giant steps with a nonzero plaintext
+    plains: np.ndarray     # [len(rows)][b][n] complex
+    dmax: float            # max |plaintext slot value|
+    tag: str = ""
+
+    @staticmethod
+    def build(h0: int, D: dict, n: int, scale: complex = 1.0) -> "BsgsStage":
+        span_n = n // h0
+        cs = []
+        for o in D:
+            c = o // h0
+            cs.append(c - span_n if c > span_n // 2 else c)
+        lo, hi = min(cs), max(cs)
+        span = hi - lo + 1
+        b = 1 << max(0, math.ceil(math.log2(span) / 2))
+        G = -(-span // b)
+        P = np.zeros((G, b, n), np.complex128)
+        for g in range(G):
+            for j in range(b):
+                o = ((lo + g * b + j) * h0) % n
+                if o in D:
+                    P[g, j] = np.roll(D[o] * scale, ((lo + g * b) * h0) % n)
+        rows = [g for g in range(G) if np.any(P[g] != 0)]
+        P = np.ascontiguousarray(P[rows])
+        return BsgsStage(h0=h0, base=lo, baby=b, giant=G, rows=rows, plains=P, dmax=float(np.max(np.abs(P))))
+
+    def rotations(self, n: int) -> list[int]:
+        r = [(j * self.h0) % n for j in range(1, self.baby)]
+        r += [((self.base + g * self.baby) * self.h0) % n for g in range(self.giant)]
+        return [x for x in r if x]
 
 
 @dataclass
@@ -71,23 +203,20 @@ class BootPlan:
 
     N: int
     q0: int
+    hamming: int = 0
     K: float = 0.0
     r: int = 0
-    baby: int = 0
-    giant: int = 0
-    taylor: list = field(default_factory=list)
+    dft_levels: int = 0
 
     def __post_init__(self) -> None:
-        n = self.N // 2
+        m = (self.N // 2).bit_length() - 1
         if not self.K:
-            self.K = secret_bound(self.N)
+            self.K = secret_bound(self.N, self.hamming)
         if not self.r:
             self.r = max(0, math.ceil(math.log2(2 * math.pi * (self.K + 0.25) / THETA_MAX)))
-        if not self.baby:
-            self.baby = 1 << ((n.bit_length() - 1 + 1) // 2)  # ~ sqrt(n), power of two
-        self.baby = min(self.baby, n)
-        self.giant = n // self.baby
-        self.taylor = [(-1.0) ** k / math.factorial(2 * k) for k in range(TAYLOR_TERMS)]
+        if not self.dft_levels:
+            self.dft_levels = max(1, -(-m // 6))
+        self.dft_levels = min(self.dft_levels, m)
 
     @property
     def n(self) -> int:
@@ -99,77 +228,42 @@ class BootPlan:
 
     @property
     def depth(self) -> int:
-        return 2 + 6 + self.r + 1
+        return self.dft_levels + 1 + 6 + self.r + self.dft_levels
+
+    def _groups(self, inverse: bool) -> list:
+        cache = self.__dict__.setdefault("_group_cache", {})
+        if inverse not in cache:
+            cache[inverse] = dft_groups(self.N, self.dft_levels, inverse)
+        return cache[inverse]
+
+    def stages(self, c2: float = 1.0) -> tuple[list[BsgsStage], list[BsgsStage]]:
+        """(CoeffToSlot stages, SlotToCoeff stages); c2 scales the first SlotToCoeff level."""
+        n = self.n
+        cts = [BsgsStage.build(h0, D, n) for h0, D in self._groups(True)]
+        stc = [BsgsStage.build(h0, D, n, c2 if g == 0 else 1.0) for g, (h0, D) in enumerate(self._groups(False))]
+        for i, st in enumerate(cts):
+            st.tag = f"cts{i}"
+        for i, st in enumerate(stc):
+            st.tag = f"stc{i}"
+        return cts, stc
 
     def rotation_offsets(self) -> list[int]:
-        """Baby steps 1..b-1 and giant steps b g (g = 1..G-1)."""
-        return list(range(1, self.baby)) + [self.baby * g for g in range(1, self.giant)]
-
-
-# ------------------------------------------------------------------ DFT diagonals
-def _pow5(n: int, N: int) -> np.ndarray:
-    out = np.empty(n, np.int64)
-    g = 1
-    for i in range(n):
-        out[i] = g
-        g = (g * 5) % (2 * N)
-    return out
-
-
-def _zeta(exps: np.ndarray, N: int) -> np.ndarray:
-    e = np.mod(exps, 2 * N).astype(np.float64)
-    return np.exp(1j * np.pi * e / N)
-
-
-def cts_diagonals(N: int) -> np.ndarray:
-    """Diagonals of V^-1 = V^H / n: d[k][i] = conj(V[(i+k) % n][i]) / n."""
-    n = N // 2
-    p5 = _pow5(n, N)
-    i = np.arange(n, dtype=np.int64)
-    out = np.empty((n, n), np.complex128)
-    for k in range(n):
-        j = (i + k) % n
-        out[k] = _zeta(-(p5[j] * i), N) / n
-    return out
-
-
-def stc_diagonals(N: int) -> np.ndarray:
-    """Diagonals of V: d[k][i] = V[i][(i+k) % n] = zeta^(5^i ((i+k) % n))."""
-    n = N // 2
-    p5 = _pow5(n, N)
-    i = np.arange(n, dtype=np.int64)
-    out = np.empty((n, n), np.complex128)
-    for k in range(n):
-        j = (i + k) % n
-        out[k] = _zeta(p5 * j, N)
-    return out
-
-
-def bsgs_plains(diags: np.ndarray, baby: int, giant: int) -> np.ndarray:
-    """BSGS plaintexts p[g][j] = roll(diag[b g + j], b g) so that
-    M z = sum_g rot_{b g}( sum_j p[g][j] (.) rot_j(z) )."""
-    n = diags.shape[1]
-    out = np.empty((giant, baby, n), np.complex128)
-    for g in range(giant):
-        for j in range(baby):
-            out[g, j] = np.roll(diags[baby * g + j], baby * g)
-    return out
+        if "_offsets" not in self.__dict__:
+            cts, stc = self.stages()
+            self._offsets = sorted({r for st in cts + stc for r in st.rotations(self.n)})
+        return self._offsets
 
 
 # ------------------------------------------------------------------ the circuit
 class Bootstrapper:
     """Runs the bootstrap circuit on a backend ``ops`` (GpuBootOps or the
-    tests' oracle backend).  Diagonal plaintext values are built once per
-    instance; encodings happen inside ``ops.lincomb_plain`` at each level."""
+    tests' oracle backend).  The DFT plans are built once per instance;
+    encodings happen inside ``ops.lincomb_plain`` at each level."""
 
-    def __init__(self, ops, plan: BootPlan):
-        self.ops, self.plan = ops, plan
-        b, G = plan.baby, plan.giant
-        inv = bsgs_plains(cts_diagonals(plan.N), b, G)                       # [G][b][n]
-        # CoeffToSlot: outputs (t, g), t = 0: V^-1, t = 1: -i V^-1 (Re -> Im(u))
-        self._cts = np.concatenate([inv, -1j * inv], axis=0)                 # [2G][b][n]
-        fwd = bsgs_plains(stc_diagonals(plan.N), b, G)                       # [G][b][n]
-        self._stc_fwd = fwd
+    def __init__(self, ops, plan: BootPlan, s_in: float):
+        self.ops, self.plan, self.s_in = ops, plan, s_in
+        # SlotToCoeff's input holds 2 sin(2 pi t / q_0) ~ 4 pi m / q_0: c2 = q_0 / (4 pi s_in)
+        self.cts, self.stc = plan.stages(plan.q0 / (4.0 * math.pi * s_in))
 
     # -- helpers
     def _exact_const(self, ct, v: float, target_scale: float):
@@ -182,35 +276,43 @@ class Bootstrapper:
             raise HebatchError("bootstrap constant underflows its encoding")
         return self.ops.mul_int(ct, k, ct.scale * k / (ql * v))
 
-    def _bsgs(self, cts, plains, pt_scale: float = 1.0):
-        """sum_g rot_{b g}(lincomb_plain(babies, plains[o])) for every output
-        row o of plains [n_out][n_in = b * len(cts)][n]; giant index g = o % G."""
-        ops, b, G = self.ops, self.plan.baby, self.plan.giant
-        babies = ops.rotate_hoisted(cts, list(range(b)))                     # [b][len(cts)]
-        ins = [babies[j][c] for j in range(b) for c in range(len(cts))]
-        partial = ops.lincomb_plain(ins, plains, pt_scale)
-        outs = []
-        for t in range(len(partial) // G):
-            acc = None
-            for g in range(G):
-                p = partial[t * G + g]
-                p = ops.rotate(p, b * g) if g else p
-                acc = p if acc is None else ops.add(acc, p)
-            outs.append(acc)
-        return outs
+    def _pt_scale(self, st: BsgsStage, level: int, grow: bool) -> float:
+        """2^k with max|d| q_l 2^k < 2^PT_BITS.  CoeffToSlot (grow) raises k so
+        its 2^-t-sized diagonals keep their bits (the exact constant product
+        that follows restores the scale); SlotToCoeff only lowers it when a
+        diagonal would overflow, so its output keeps the input's scale."""
+        dmax = st.dmax
+        ql = float(self.ops.moduli[level])
+        k = math.floor(PT_BITS - math.log2(ql) - math.log2(dmax))
+        if grow:  # at most CTS_GROWTH_BITS over all CoeffToSlot levels (the constant product stays >= 2^12)
+            return 2.0 ** min(k, CTS_GROWTH_BITS // self.plan.dft_levels)
+        return 2.0 ** min(k, 0)
+
+    def _bsgs(self, ct, st: BsgsStage, grow: bool = False):
+        """sum_g rot_{(base + g b) h0}( lincomb_plain(rot_{j h0}(ct), p[g]) )."""
+        ops, n = self.ops, self.plan.n
+        babies = ops.rotate_hoisted([ct], [j * st.h0 for j in range(st.baby)])
+        ins = [babies[j][0] for j in range(st.baby)]
+        partial = ops.lincomb_plain(ins, st.plains, self._pt_scale(st, ct.level, grow), key=st.tag)
+        acc = None
+        for g, p in zip(st.rows, partial):
+            k = ((st.base + g * st.baby) * st.h0) % n
+            p = ops.rotate(p, k) if k else p
+            acc = p if acc is None else ops.add(acc, p)
+        return acc
 
     def coeff_to_slot(self, raised):
         """-> [theta_lo, theta_hi]: theta = a (t / q_0 - 1/4) for the coefficient
-        halves t_j, t_{j+n} (j < n) of the raised plaintext."""
+        halves t_j, t_{j+n} (j < n, bit-reversed order) of the raised plaintext."""
         plan, ops = self.plan, self.ops
-        n_out = self._cts.shape[0]
-        # |d| = 1/n: plaintext coefficients stay below q_l 2^k / n < 2^60 (int64 encode)
-        ql_bits = self.ops.moduli[raised.level].bit_length()
-        k = max(0, min(CTS_PT_BITS, 60 - ql_bits + plan.n.bit_length() - 1))
-        w = self._bsgs([raised], self._cts.reshape(n_out, plan.baby, plan.n), float(1 << k))
-        re2 = [ops.add(x, ops.conj(x)) for x in w]                          # 2 t / s
+        w = raised
+        for st in self.cts:
+            w = self._bsgs(w, st, grow=True)                             # R u / s (complex)
+        wc = ops.conj(w)
+        lo = ops.add(w, wc)                                              # 2 Re: t_j
+        hi = ops.mul_monomial(ops.sub(w, wc), 3 * plan.n)                # -i (w - conj w) = 2 Im: t_{j+n}
         c = plan.a * raised.scale / (2.0 * plan.q0)
-        th = [self._exact_const(x, c, raised.scale) for x in re2]           # a t / q_0
+        th = [self._exact_const(x, c, raised.scale) for x in (lo, hi)]   # a t / q_0
         return [ops.add_const(x, -plan.a / 4.0) for x in th]
 
     def eval_mod(self, theta):
@@ -244,21 +346,23 @@ class Bootstrapper:
             zs = ops.mult_ct(zs, zs)
         return [ops.add(z, ops.conj(z)) for z in zs]
 
-    def slot_to_coeff(self, sines, s_in: float):
-        plan = self.plan
-        c2 = plan.q0 / (4.0 * math.pi * s_in)      # the EvalMod outputs hold 2 sin(2 pi t / q_0)
-        fwd = self._stc_fwd
-        # inputs ordered (j, t): babies[j][0] = rot_j(sin_lo), babies[j][1] = rot_j(sin_hi)
-        pl = np.stack([c2 * fwd, (1j * c2) * fwd], axis=2).reshape(plan.giant, 2 * plan.baby, plan.n)
-        return self._bsgs(sines, pl)[0]
+    def slot_to_coeff(self, sines):
+        """[2 sin lo, 2 sin hi] (bit-reversed coefficient order) -> the message slots."""
+        ops, plan = self.ops, self.plan
+        x = ops.add(sines[0], ops.mul_monomial(sines[1], plan.n))          # lo + i hi
+        for st in self.stc:
+            x = self._bsgs(x, st)
+        return x
 
     def run(self, ct, ell_top: int):
-        """Bootstrap ``ct`` (any level): ModRaise to ell_top limbs, CtS, EvalMod, StC."""
-        s_in = ct.scale
+        """Bootstrap ``ct`` (any level; its scale must be this instance's s_in):
+        ModRaise to ell_top limbs, CoeffToSlot, EvalMod, SlotToCoeff."""
+        if ct.scale != self.s_in:
+            raise HebatchError("Bootstrapper built for another input scale")
         raised = self.ops.mod_raise(ct, ell_top)
         theta = self.coeff_to_slot(raised)
         sines = self.eval_mod(theta)
-        return self.slot_to_coeff(sines, s_in)
+        return self.slot_to_coeff(sines)
 
 
 class GpuBootOps:
@@ -268,6 +372,7 @@ class GpuBootOps:
     def __init__(self, eng):
         self.e = eng
         self.moduli = eng.moduli
+        self._pts = {}  # (stage tag, limbs, pt_scale) -> encoded diagonals [rows * b][limbs][N]
 
     def mod_raise(self, ct, ell_out):
         e = self.e
@@ -294,6 +399,9 @@ class GpuBootOps:
     def add(self, a, b):
         return self.e._add_batch([a], [b])[0]
 
+    def sub(self, a, b):
+        return self.e._add_batch([a], [b], sub=True)[0]
+
     def add_const(self, ct, v):
         return self.e.add_const_batch([ct], [v], count=False)[0]
 
@@ -308,5 +416,13 @@ class GpuBootOps:
         return self.e.lincomb(ins, [0, n], list(range(n)), list(weights), bias=[bias], out_scale=out_scale,
                               count_as_conv=False)[0]
 
-    def lincomb_plain(self, ins, plains, pt_scale=1.0):
-        return self.e.lincomb_plain(ins, plains, len(plains), pt_scale)
+    def lincomb_plain(self, ins, plains, pt_scale=1.0, key=None):
+        """DFT levels: the encoded diagonals are cached on the device per (stage, level, scale)."""
+        e = self.e
+        if key is None:
+            return e.lincomb_plain(ins, plains, len(plains), pt_scale)
+        limbs = ins[0].level + 1
+        ck = (key, limbs, pt_scale)
+        if ck not in self._pts:
+            self._pts[ck] = e.encode_plains(plains.reshape(-1, plains.shape[-1]), limbs, pt_scale)
+        return e.lincomb_plain_encoded(ins, self._pts[ck], len(plains), pt_scale)

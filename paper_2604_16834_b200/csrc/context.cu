@@ -181,13 +181,22 @@ int he_upload_ptrs(const void *const *host_ptrs, int count, void ***dev_out, cud
 }
 
 // ---------------------------------------------------------------- key kernels
-__global__ void k_sk_fill(uint64_t *sk, const ModConst *mc, int N, int M, uint64_t seed) {
+// secret coefficient j (oracle sample_ternary): dense ternary, or for h > 0 nonzero
+// with probability h / N (second draw below thr = floor(h 2^32 / N)), sign = low bit
+__global__ void k_sk_fill(uint64_t *sk, const ModConst *mc, int N, int M, uint64_t seed, int h, uint32_t thr) {
     size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (idx >= (size_t)M * N) return;
     int m = (int)(idx / N), j = (int)(idx % N);
     uint32_t r[4];
     rnd4(seed, DOM_SK, 0, 0, (uint32_t)j >> 2, r);
-    int64_t s = (int64_t)(r[j & 3] % 3u) - 1;
+    int64_t s;
+    if (h <= 0) {
+        s = (int64_t)(r[j & 3] % 3u) - 1;
+    } else {
+        uint32_t r2[4];
+        rnd4(seed, DOM_SK, 1, 0, (uint32_t)j >> 2, r2);
+        s = r2[j & 3] >= thr ? 0 : ((r[j & 3] & 1u) ? 1 : -1);
+    }
     sk[idx] = smod64(s, mc[m].q);
 }
 
@@ -444,7 +453,11 @@ extern "C" int he_ctx_create(const he_params *p, int device, he_ctx **out) {
         he_ctx_destroy(c);
         return HE_ENOMEM;
     }
-    k_sk_fill<<<ceil_div(tot, 256), 256>>>(c->d_sk, c->d_mc, c->N, M, p->seed);
+    {
+        const uint64_t t = p->sk_hamming > 0 ? ((uint64_t)p->sk_hamming << 32) / (uint64_t)c->N : 0;
+        const uint32_t thr = t > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t;
+        k_sk_fill<<<ceil_div(tot, 256), 256>>>(c->d_sk, c->d_mc, c->N, M, p->seed, p->sk_hamming, thr);
+    }
     r = he_ntt_fwd(c, c->d_sk, M, c->d_ident, M, 0);
     if (r == HE_OK && cudaDeviceSynchronize() != cudaSuccess) {
         he_set_error("secret key generation failed: %s", cudaGetErrorString(cudaGetLastError()));

@@ -57,7 +57,9 @@ class EngineContext:
     (alpha = ceil((max_level+1)/digits) limbs each).  Additions:
     ``special_prime_bits`` (default: alpha primes of first_modulus_bits bits),
     ``scale_bits`` (encoding scale, default rescale_bits), ``q_bits`` (explicit
-    Q chain override) and ``device``.  ``noise_sigma`` is the simulator's
+    Q chain override), ``device`` and ``secret_hamming`` (0: dense ternary
+    secret; h > 0: sparse secret of expected Hamming weight h, which keeps the
+    bootstrap's ModRaise overflow small).  ``noise_sigma`` is the simulator's
     slot perturbation and has no meaning for real encryption (ignored).
     """
 
@@ -74,6 +76,7 @@ class EngineContext:
     scale_bits: int | None = None
     q_bits: tuple | None = None
     device: int = 0
+    secret_hamming: int = 0
 
     def __post_init__(self) -> None:
         if self.n < 1 or (self.n & (self.n - 1)) != 0:
@@ -133,6 +136,7 @@ class EngineContext:
             p.p_bits[i] = b
         p.seed = self.noise_seed & 0xFFFFFFFFFFFFFFFF
         p.scale = self.scale
+        p.sk_hamming = int(self.secret_hamming)
         return p
 
 
@@ -1128,7 +1132,7 @@ class GpuEngine:
         from .bootstrap import BootPlan
 
         if getattr(self, "_bplan", None) is None:
-            self._bplan = BootPlan(N=self.N, q0=self.moduli[0])
+            self._bplan = BootPlan(N=self.N, q0=self.moduli[0], hamming=self.context.secret_hamming)
         return self._bplan
 
     def _ensure_boot_keys(self, plan) -> None:
@@ -1145,8 +1149,9 @@ class GpuEngine:
         ~1e-5 with q_0 / scale = 2^10 and a 2^50 scale) at level
         max_level - bootstrap_reserve, and only the ``bootstraps`` counter
         moves.  The circuit needs bootstrap_reserve >= its depth
-        (BootPlan.depth, 17 at N = 2^12); its Galois keys (BSGS steps and
-        conjugation) are generated on first use."""
+        (BootPlan.depth: 20 at N = 2^12 with the dense secret); its Galois keys
+        (BSGS steps of the factored DFT and conjugation) are generated on
+        first use."""
         from .bootstrap import Bootstrapper, GpuBootOps
 
         self._check(ct)
@@ -1157,11 +1162,14 @@ class GpuEngine:
             raise HebatchError(f"bootstrap_reserve {self.context.bootstrap_reserve} is below the bootstrap circuit's "
                                f"depth {plan.depth}")
         self._ensure_boot_keys(plan)
-        if getattr(self, "_booter", None) is None:
-            self._booter = Bootstrapper(GpuBootOps(self), plan)
+        booters = self.__dict__.setdefault("_booters", {})  # per input scale (SlotToCoeff folds 1 / scale)
+        if ct.scale not in booters:
+            if len(booters) >= 4:
+                booters.pop(next(iter(booters)))
+            booters[ct.scale] = Bootstrapper(GpuBootOps(self), plan, ct.scale)
         with self._acct.lock:
             saved = (dict(self._acct.counts), self._acct.peak, self._acct.window_peak, set(self._acct.live))
-        out = self._booter.run(ct, self.context.n_q)
+        out = booters[ct.scale].run(ct, self.context.n_q)
         if out.level > target:
             out = self.drop_level_batch([out], target)[0]
         with self._acct.lock:  # circuit temporaries are not user-visible ciphertexts
@@ -1385,6 +1393,48 @@ class GpuEngine:
                                   units=(((o1 - o0) * n_in * limbs * self.N + (n_in + o1 - o0) * poly) * 8.0,
                                          float((o1 - o0) * n_in) * poly)), "lincomb_plain")
             del pt
+        return self._rescale_tensor(acc, limbs, [s_in * pt_scale] * n_out)
+
+    def encode_plains(self, plains, limbs: int, pt_scale: float = 1.0):
+        """Slot vectors [count][<= n] (real or complex) -> NTT-domain plaintexts
+        [count][limbs][N] at q_last * pt_scale (the encoding lincomb_plain uses)."""
+        torch = _torch()
+        cplx = np.iscomplexobj(plains)
+        P = torch.as_tensor(np.asarray(plains), dtype=torch.complex128 if cplx else torch.float64, device=self.device)
+        ql = float(self.moduli[limbs - 1]) * pt_scale
+        pt = torch.empty((P.shape[0], limbs, self.N), dtype=torch.int64, device=self.device)
+        if cplx:
+            vr, vi = P.real.contiguous(), P.imag.contiguous()
+            _lib.check(self._call("encode_plain", self._L.he_encode_plain_batch_c, self._h, vr.data_ptr(),
+                                  vi.data_ptr(), P.shape[0], P.shape[1], ql, limbs, pt.data_ptr(), self.stream),
+                       "encode_plain_batch_c")
+        else:
+            P = P.contiguous()
+            _lib.check(self._call("encode_plain", self._L.he_encode_plain_batch, self._h, P.data_ptr(), P.shape[0],
+                                  P.shape[1], ql, limbs, pt.data_ptr(), self.stream), "encode_plain_batch")
+        return pt
+
+    def lincomb_plain_encoded(self, inputs: Sequence[CipherVec], pt, n_out: int, pt_scale: float = 1.0):
+        """lincomb_plain over plaintexts already encoded by encode_plains (pt
+        [n_out * n_in][limbs >= level + 1][N], read at the inputs' level)."""
+        for c in inputs:
+            self._check(c)
+        n_in = len(inputs)
+        level, s_in = inputs[0].level, inputs[0].scale
+        if any(c.level != level or c.scale != s_in for c in inputs):
+            raise HebatchError("lincomb_plain needs inputs at one level and scale")
+        limbs = level + 1
+        if pt.shape[0] != n_out * n_in or pt.shape[1] != limbs:
+            raise ShapeMismatch(f"encoded plaintexts {tuple(pt.shape)} for {n_out} x {n_in} at {limbs} limbs")
+        pin = self._ptrs(inputs)
+        acc = self._alloc(n_out, 2, limbs)
+        ppt = self._tptrs(pt)
+        pout = self._tptrs(acc)
+        poly = 2 * limbs * self.N
+        _lib.check(self._call("lincomb_plain", self._L.he_lincomb_plain, self._h, _lib.addr(pin), n_in,
+                              _lib.addr(ppt), _lib.addr(pout), n_out, limbs, self.stream,
+                              units=((n_out * n_in * limbs * self.N + (n_in + n_out) * poly) * 8.0,
+                                     float(n_out * n_in) * poly)), "lincomb_plain")
         return self._rescale_tensor(acc, limbs, [s_in * pt_scale] * n_out)
 
     def conv_mma(self, inputs: Sequence[CipherVec], gcol, out_base, out_stride: int, weights, n_out: int,

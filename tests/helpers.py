@@ -25,15 +25,19 @@ PARAMS = {
     "boot6": (6, (60,) + (50,) * 16, (60,) * 3, 3, 50),
     "boot11": (11, (60,) + (50,) * 22, (60,) * 3, 3, 50),
     "boot12": (12, (60,) + (50,) * 22, (60,) * 3, 3, 50),
+    # sparse secret (expected Hamming weight 64, 6th field): K ~ 18, r = 7
+    "boot11s": (11, (60,) + (50,) * 22, (60,) * 3, 3, 50, 64),
+    # the config-2/4 ring degree with a sparse secret (h = 128): depth 20 of 25 levels
+    "boot16s": (16, (60,) + (50,) * 25, (60,) * 4, 4, 50, 128),
 }
 
 
 def engine_context(name, seed=1, bootstrap_reserve=1):
     from paper_2604_16834_b200.engine import EngineContext
 
-    log_n, qb, pb, alpha, sb = PARAMS[name]
+    log_n, qb, pb, alpha, sb, *rest = PARAMS[name]
     L = len(qb)
-    return EngineContext(n=1 << (log_n - 1), max_level=L - 1, bootstrap_reserve=bootstrap_reserve,
+    return EngineContext(secret_hamming=rest[0] if rest else 0, n=1 << (log_n - 1), max_level=L - 1, bootstrap_reserve=bootstrap_reserve,
                          first_modulus_bits=qb[0],
                          rescale_bits=qb[-1] if L > 1 else qb[0], key_switch_digits=-(-L // alpha),
                          noise_seed=seed, special_prime_bits=tuple(pb), scale_bits=sb, q_bits=tuple(qb))
@@ -42,8 +46,8 @@ def engine_context(name, seed=1, bootstrap_reserve=1):
 def oracle_for(name, seed=1):
     import oracle as O
 
-    log_n, qb, pb, alpha, sb = PARAMS[name]
-    return O.Oracle(log_n, list(qb), list(pb), alpha, seed=seed, scale=2.0 ** sb)
+    log_n, qb, pb, alpha, sb, *rest = PARAMS[name]
+    return O.Oracle(log_n, list(qb), list(pb), alpha, seed=seed, scale=2.0 ** sb, sk_hamming=rest[0] if rest else 0)
 
 
 def to_np(t):

@@ -84,6 +84,10 @@ class OracleBootOps:
         ell = min(a.ell, b.ell)
         return OCt(self.orc.add(np.ascontiguousarray(a.data[:, :ell]), np.ascontiguousarray(b.data[:, :ell])), a.scale)
 
+    def sub(self, a, b):
+        ell = min(a.ell, b.ell)
+        return OCt(self.orc.sub(np.ascontiguousarray(a.data[:, :ell]), np.ascontiguousarray(b.data[:, :ell])), a.scale)
+
     def add_const(self, ct, v):
         return OCt(self.orc.add_const(ct.data, self._res(np.rint(v * ct.scale))(ct.ell)), ct.scale)
 
@@ -104,7 +108,7 @@ class OracleBootOps:
                        list(weights), [bias], out_scale)[0]
         return OCt(r.data, r.scale)
 
-    def lincomb_plain(self, ins, plains, pt_scale=1.0):
+    def lincomb_plain(self, ins, plains, pt_scale=1.0, key=None):
         orc = self.orc
         ell = ins[0].ell
         ql = float(self.moduli[ell - 1]) * pt_scale

@@ -31,7 +31,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = _lib.load()
     for name in _lib.EXPORTS:
         assert hasattr(lib, name), name
-    assert lib.he_abi_version() == 1
+    assert lib.he_abi_version() == 2
     assert lib.he_launch_count() >= 0
 
 
