@@ -44,9 +44,11 @@ def _args():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=None, help="(ncu) run exactly this many network passes")
-    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg2"],
-                    help="cfg3: the CNN (default line); cfg2: only the config-2 primitive microbenchmark")
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg2", "boot"],
+                    help="cfg3: the CNN (default line); cfg2: only the config-2 primitive microbenchmark; "
+                         "boot: only the N = 2^16 bootstrap")
     ap.add_argument("--no-primitives", action="store_true", help="skip the config-2 primitives in the cfg3 line")
+    ap.add_argument("--no-bootstrap", action="store_true", help="skip the bootstrap timing in the cfg3 line")
     ap.add_argument("--h2d-overlap", default="network", choices=["encrypt", "network", "serial"],
                     help="e2e: which phase of step i the H2D copy of step i+1's images overlaps "
                          "(serial: each step's own copy, not overlapped)")
@@ -326,6 +328,49 @@ def primitives_cfg2(device: int = 0, cts: int = 256, reps: int = 5) -> dict:
                       "rescale, mult_ct, rotate, rotate_hoisted)"}
 
 
+def bootstrap_n16(device: int = 0, reps: int = 5) -> dict:
+    """CKKS bootstrapping (the reference's bootstrap is level
+    accounting only, /root/reference/pkg/src/hebatch/engine.py:315-319) on the
+    configs.boot_context ring: one ciphertext of 32768 seeded U[-1, 1] slots read at
+    level 0, ModRaise -> CoeffToSlot -> EvalMod -> SlotToCoeff, timed with CUDA
+    events on the engine's stream after one warm-up call (key generation and
+    diagonal encoding happen there).  Limb parity vs the CPU oracle:
+    tests/test_gpu_bootstrap.py (the same circuit on the oracle at N = 2^11)."""
+    import numpy as np
+    import torch
+
+    from paper_2604_16834_b200 import configs
+    from paper_2604_16834_b200.engine import GpuEngine
+
+    eng = GpuEngine(configs.boot_context(seed=11, device=device))
+    x = np.random.default_rng(3).uniform(-1, 1, eng.context.n)
+    low = eng.drop_level_batch([eng.encrypt_batch(x[None])[0]], 0)[0]
+    t0 = time.perf_counter()
+    out = eng.bootstrap(low)
+    eng.synchronize()
+    first = time.perf_counter() - t0
+    st = torch.cuda.current_stream(eng.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = eng._L.he_launch_count()
+    e0.record(st)
+    for _ in range(reps):
+        eng.release(out)
+        out = eng.bootstrap(low)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    plan = eng.boot_plan()
+    res = {"workload": "bootstrap: N=2^16, 32768 slots, q0 60 + 25x50-bit primes, scale 2^50, 4x60-bit P, "
+                       "sparse secret h=128, one ciphertext",
+           "ms": round(ms, 2), "reps": reps, "launches_per_bootstrap": (eng._L.he_launch_count() - n0) // reps,
+           "max_abs_err": float(np.max(np.abs(eng.decrypt(out) - x))), "depth": plan.depth, "r": plan.r,
+           "dft_levels": plan.dft_levels, "level_out": out.level, "rotation_keys": len(plan.rotation_offsets()) + 1,
+           "first_call_s_incl_keygen": round(first, 3),
+           "parity": "limb-exact vs the same circuit on the CPU oracle: tests/test_gpu_bootstrap.py"}
+    del eng
+    return res
+
+
 def main():
     args = _args()
     _self_launch(args)
@@ -337,6 +382,10 @@ def main():
     import torch
 
     torch.cuda.set_device(local)
+    if args.workload == "boot":
+        if rank == 0:
+            print(json.dumps(bootstrap_n16(local)), flush=True)
+        return
     if args.workload == "cfg2":
         if rank == 0:
             print(json.dumps(primitives_cfg2(local)), flush=True)
@@ -554,6 +603,10 @@ def main():
     if rank == 0 and not args.no_primitives:            # after every timed region: config-2 primitives
         eng.trim()
         prim = primitives_cfg2(local)
+    boot = None
+    if rank == 0 and not args.no_bootstrap:
+        eng.trim()
+        boot = bootstrap_n16(local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -588,6 +641,7 @@ def main():
             "peaks_measured": peaks_measured,
             "cpu_baseline": cpu,
             "primitives_cfg2": prim,
+            "bootstrap": boot,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

@@ -32,6 +32,16 @@ def context(cfg: int, seed: int = 0, device: int = 0) -> EngineContext:
     raise ValueError(f"unknown config {cfg}")
 
 
+def boot_context(seed: int = 0, device: int = 0) -> EngineContext:
+    """The bootstrapping ring (no BASELINE config bootstraps; engine.bootstrap,
+    bootstrap.py): N = 2^16, q_0 of 60 bits + 25 x 50-bit rescale primes at scale
+    2^50, 4 x 60-bit special primes (dnum 7), sparse secret of expected Hamming
+    weight 128.  The circuit takes 20 levels (bootstrap_reserve), leaving 5."""
+    return EngineContext(n=32768, max_level=25, bootstrap_reserve=20, first_modulus_bits=60, rescale_bits=50,
+                         key_switch_digits=7, noise_seed=seed, special_prime_bits=(60,) * 4, scale_bits=50,
+                         secret_hamming=128, device=device)
+
+
 MLP1 = MlpSpec(sizes=(64, 32, 10), act=Activation((0.0, 0.0, 1.0)))
 CNN3 = CnnSpec(channels=(3, 16, 32), H=32, W=32, act=Activation((0.25, 0.5, 0.125)), pool_after=(0,))
 CNN4 = CnnSpec(channels=(3, 16, 32, 64, 64), H=32, W=32, act=Activation((0.5, 0.5, 0.0, 0.0625)),
