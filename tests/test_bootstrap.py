@@ -112,3 +112,20 @@ def test_bootstrap_circuit_on_the_oracle():
     assert out.level == orc.L - 1 - plan.depth
     err = np.max(np.abs(orc.decrypt(out.data, out.scale) - x))
     assert err < 1e-4, err
+
+
+def test_sparse_secret_on_the_oracle():
+    """sk_hamming = h: ternary coefficients, about h of them nonzero (bootstrapping's K bound)."""
+    import oracle as O
+
+    o = O.Oracle(11, [60, 50, 50], [60], 1, seed=9, scale=2.0 ** 50, sk_hamming=64)
+    q = o.moduli[0]
+    c = o.intt(o.secret_key()[0], 0)
+    v = np.where(c > q // 2, c.astype(np.int64) - np.int64(q), c.astype(np.int64))
+    assert set(np.unique(v)) <= {-1, 0, 1}
+    assert 64 - 4 * 8 <= np.count_nonzero(v) <= 64 + 4 * 8
+    # every limb holds the same small polynomial
+    c1 = o.intt(o.secret_key()[1], 1)
+    q1 = o.moduli[1]
+    v1 = np.where(c1 > q1 // 2, c1.astype(np.int64) - np.int64(q1), c1.astype(np.int64))
+    assert np.array_equal(v, v1)
