@@ -359,11 +359,28 @@ def bootstrap_n16(device: int = 0, reps: int = 5) -> dict:
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    launches = (eng._L.he_launch_count() - n0) // reps
+    err = float(np.max(np.abs(eng.decrypt(out) - x)))
+    # throughput: one batched circuit for `batch` ciphertexts (bootstrap_batch)
+    batch = 8
+    xb = np.random.default_rng(4).uniform(-1, 1, (batch, eng.context.n))
+    lows = eng.drop_level_batch(eng.encrypt_batch(xb), 0)
+    outs = eng.bootstrap_batch(lows)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(2):
+        eng.release(*outs)
+        outs = eng.bootstrap_batch(lows)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_b = e0.elapsed_time(e1) / 2
+    err_b = max(float(np.max(np.abs(eng.decrypt(o) - xb[i]))) for i, o in enumerate(outs))
     plan = eng.boot_plan()
     res = {"workload": "bootstrap: N=2^16, 32768 slots, q0 60 + 25x50-bit primes, scale 2^50, 4x60-bit P, "
                        "sparse secret h=128, one ciphertext",
-           "ms": round(ms, 2), "reps": reps, "launches_per_bootstrap": (eng._L.he_launch_count() - n0) // reps,
-           "max_abs_err": float(np.max(np.abs(eng.decrypt(out) - x))), "depth": plan.depth, "r": plan.r,
+           "ms": round(ms, 2), "reps": reps, "launches_per_bootstrap": launches,
+           "max_abs_err": err, "depth": plan.depth, "r": plan.r,
+           "batch": {"cts": batch, "ms": round(ms_b, 2), "ms_per_ct": round(ms_b / batch, 2), "max_abs_err": err_b},
            "dft_levels": plan.dft_levels, "level_out": out.level, "rotation_keys": len(plan.rotation_offsets()) + 1,
            "first_call_s_incl_keygen": round(first, 3),
            "parity": "limb-exact vs the same circuit on the CPU oracle: tests/test_gpu_bootstrap.py"}

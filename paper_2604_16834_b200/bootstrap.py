@@ -257,7 +257,9 @@ class BootPlan:
 # ------------------------------------------------------------------ the circuit
 class Bootstrapper:
     """Runs the bootstrap circuit on a backend ``ops`` (GpuBootOps or the
-    tests' oracle backend).  The DFT plans are built once per instance;
+    tests' oracle backend) over a batch of ciphertexts of one level and scale.
+    Every backend op takes and returns lists, so each step is one batched
+    call for the whole batch.  The DFT plans are built once per instance;
     encodings happen inside ``ops.lincomb_plain`` at each level."""
 
     def __init__(self, ops, plan: BootPlan, s_in: float):
@@ -266,44 +268,46 @@ class Bootstrapper:
         self.cts, self.stc = plan.stages(plan.q0 / (4.0 * math.pi * s_in))
 
     # -- helpers
-    def _exact_const(self, ct, v: float, target_scale: float):
-        """ct * v landing near ``target_scale``: the constant's integer is
+    def _exact_const(self, cts, v: float, target_scale: float):
+        """cts * v landing near ``target_scale``: the constant's integer is
         k = rint(v q_l target / s) and the declared output scale is the exact
         s k / (q_l v), so the rounding of k costs no precision."""
-        ql = self.ops.moduli[ct.level]
-        k = int(np.rint(v * ql * target_scale / ct.scale))
+        ql = self.ops.moduli[cts[0].level]
+        s_ = cts[0].scale
+        k = int(np.rint(v * ql * target_scale / s_))
         if abs(k) < (1 << 8):
             raise HebatchError("bootstrap constant underflows its encoding")
-        return self.ops.mul_int(ct, k, ct.scale * k / (ql * v))
+        return self.ops.mul_int(cts, k, s_ * k / (ql * v))
 
     def _pt_scale(self, st: BsgsStage, level: int, grow: bool) -> float:
         """2^k with max|d| q_l 2^k < 2^PT_BITS.  CoeffToSlot (grow) raises k so
         its 2^-t-sized diagonals keep their bits (the exact constant product
         that follows restores the scale); SlotToCoeff only lowers it when a
         diagonal would overflow, so its output keeps the input's scale."""
-        dmax = st.dmax
         ql = float(self.ops.moduli[level])
-        k = math.floor(PT_BITS - math.log2(ql) - math.log2(dmax))
+        k = math.floor(PT_BITS - math.log2(ql) - math.log2(st.dmax))
         if grow:  # at most CTS_GROWTH_BITS over all CoeffToSlot levels (the constant product stays >= 2^12)
             return 2.0 ** min(k, CTS_GROWTH_BITS // self.plan.dft_levels)
         return 2.0 ** min(k, 0)
 
-    def _bsgs(self, ct, st: BsgsStage, grow: bool = False):
-        """sum_g rot_{(base + g b) h0}( lincomb_plain(rot_{j h0}(ct), p[g]) )."""
+    def _bsgs(self, cts, st: BsgsStage, grow: bool = False):
+        """sum_g rot_{(base + g b) h0}( lincomb_plain(rot_{j h0}(ct), p[g]) ) per ct."""
         ops, n = self.ops, self.plan.n
-        babies = ops.rotate_hoisted([ct], [j * st.h0 for j in range(st.baby)])
-        ins = [babies[j][0] for j in range(st.baby)]
-        partial = ops.lincomb_plain(ins, st.plains, self._pt_scale(st, ct.level, grow), key=st.tag)
+        babies = ops.rotate_hoisted(cts, [j * st.h0 for j in range(st.baby)])     # [b][B]
+        pts = self._pt_scale(st, cts[0].level, grow)
+        partial = [ops.lincomb_plain([babies[j][c] for j in range(st.baby)], st.plains, pts, key=st.tag)
+                   for c in range(len(cts))]                                       # [B][rows]
         acc = None
-        for g, p in zip(st.rows, partial):
+        for gi, g in enumerate(st.rows):
+            col = [p[gi] for p in partial]
             k = ((st.base + g * st.baby) * st.h0) % n
-            p = ops.rotate(p, k) if k else p
-            acc = p if acc is None else ops.add(acc, p)
+            col = ops.rotate(col, k) if k else col
+            acc = col if acc is None else ops.add(acc, col)
         return acc
 
     def coeff_to_slot(self, raised):
-        """-> [theta_lo, theta_hi]: theta = a (t / q_0 - 1/4) for the coefficient
-        halves t_j, t_{j+n} (j < n, bit-reversed order) of the raised plaintext."""
+        """-> theta (2B cts: the B low halves, then the B high halves): theta =
+        a (t / q_0 - 1/4) for the coefficients t_j, t_{j+n} (j < n, bit-reversed)."""
         plan, ops = self.plan, self.ops
         w = raised
         for st in self.cts:
@@ -311,110 +315,111 @@ class Bootstrapper:
         wc = ops.conj(w)
         lo = ops.add(w, wc)                                              # 2 Re: t_j
         hi = ops.mul_monomial(ops.sub(w, wc), 3 * plan.n)                # -i (w - conj w) = 2 Im: t_{j+n}
-        c = plan.a * raised.scale / (2.0 * plan.q0)
-        th = [self._exact_const(x, c, raised.scale) for x in (lo, hi)]   # a t / q_0
-        return [ops.add_const(x, -plan.a / 4.0) for x in th]
+        c = plan.a * raised[0].scale / (2.0 * plan.q0)
+        th = self._exact_const(lo + hi, c, raised[0].scale)              # a t / q_0
+        return ops.add_const(th, -plan.a / 4.0)
 
     def eval_mod(self, theta):
-        """[theta_i] -> [2 sin(2 pi t / q_0)]: z = e^{i theta} = C + i S from the
+        """theta -> 2 sin(2 pi t / q_0): z = e^{i theta} = C + i S from the
         Taylor cosine and sine (i S as the monomial X^n S: free and exact),
         r squarings z <- z^2 (error growth 2 per step, against 4 for the
         cosine double angle), then z + conj(z) = 2 Re(e^{i (2 pi x - pi/2)})."""
-        ops = self.ops
+        ops, m = self.ops, len(theta)
         cc = [(-1.0) ** k / math.factorial(2 * k) for k in range(TAYLOR_TERMS)]
         sc = [(-1.0) ** k / math.factorial(2 * k + 1) for k in range(TAYLOR_TERMS)]
         y = ops.mult_ct(theta, theta)                                   # theta^2
-        y2 = ops.mult_ct(y, y)
-        t1 = ops.mult_ct(theta, y)                                      # theta^3
-        y3 = ops.mult_ct(y, y2)
-        y4 = ops.mult_ct(y2, y2)
-        t2 = ops.mult_ct(theta, y2)                                     # theta^5
+        r1 = ops.mult_ct(y + theta, y + y)
+        y2, t1 = r1[:m], r1[m:]                                         # theta^4, theta^3
+        r2 = ops.mult_ct(y + y2 + theta, y2 + y2 + y2)
+        y3, y4, t2 = r2[:m], r2[m:2 * m], r2[2 * m:]                    # theta^6, theta^8, theta^5
         t3 = ops.mult_ct(theta, y3)                                     # theta^7
-        zs = []
-        for i in range(len(theta)):
-            target = y3[i].scale
-            mc, ms = y3[i].level - 1, t3[i].level - 1                  # levels of the y^4 products
-            q0c = ops.lincomb([y[i], y2[i], y3[i]], cc[1:4], cc[0], target)
-            q1c = ops.lincomb([y[i], y2[i], y3[i]], cc[5:8], cc[4], target * ops.moduli[mc] / y4[i].scale)
-            cos_t = ops.add(q0c, ops.mult_ct([y4[i]], [q1c])[0])
-            odd = [theta[i], t1[i], t2[i], t3[i]]
-            q0s = ops.lincomb(odd, sc[0:4], 0.0, target)
-            q1s = ops.lincomb(odd, sc[4:8], 0.0, target * ops.moduli[ms] / y4[i].scale)
-            sin_t = ops.add(q0s, ops.mult_ct([y4[i]], [q1s])[0])
-            zs.append(ops.add(cos_t, ops.mul_monomial(sin_t, self.plan.n)))  # cos + i sin
+        target = y3[0].scale
+        mc, ms = y3[0].level - 1, t3[0].level - 1                      # levels of the y^4 products
+        even = [[y[i], y2[i], y3[i]] for i in range(m)]
+        odd = [[theta[i], t1[i], t2[i], t3[i]] for i in range(m)]
+        q0c = ops.lincomb(even, cc[1:4], cc[0], target)
+        q1c = ops.lincomb(even, cc[5:8], cc[4], target * ops.moduli[mc] / y4[0].scale)
+        q0s = ops.lincomb(odd, sc[0:4], 0.0, target)
+        q1s = ops.lincomb(odd, sc[4:8], 0.0, target * ops.moduli[ms] / y4[0].scale)
+        cos_t = ops.add(q0c, ops.mult_ct(y4, q1c))
+        sin_t = ops.add(q0s, ops.mult_ct(y4, q1s))
+        z = ops.add(cos_t, ops.mul_monomial(sin_t, self.plan.n))       # cos + i sin
         for _ in range(self.plan.r):
-            zs = ops.mult_ct(zs, zs)
-        return [ops.add(z, ops.conj(z)) for z in zs]
+            z = ops.mult_ct(z, z)
+        return ops.add(z, ops.conj(z))
 
     def slot_to_coeff(self, sines):
-        """[2 sin lo, 2 sin hi] (bit-reversed coefficient order) -> the message slots."""
+        """2 sin for the B low halves then the B high halves (bit-reversed
+        coefficient order) -> the B message ciphertexts."""
         ops, plan = self.ops, self.plan
-        x = ops.add(sines[0], ops.mul_monomial(sines[1], plan.n))          # lo + i hi
+        B = len(sines) // 2
+        x = ops.add(sines[:B], ops.mul_monomial(sines[B:], plan.n))      # lo + i hi
         for st in self.stc:
             x = self._bsgs(x, st)
         return x
 
-    def run(self, ct, ell_top: int):
-        """Bootstrap ``ct`` (any level; its scale must be this instance's s_in):
-        ModRaise to ell_top limbs, CoeffToSlot, EvalMod, SlotToCoeff."""
-        if ct.scale != self.s_in:
-            raise HebatchError("Bootstrapper built for another input scale")
-        raised = self.ops.mod_raise(ct, ell_top)
-        theta = self.coeff_to_slot(raised)
-        sines = self.eval_mod(theta)
-        return self.slot_to_coeff(sines)
+    def run(self, cts, ell_top: int):
+        """Bootstrap ``cts`` (one level; scale this instance's s_in): ModRaise
+        to ell_top limbs, CoeffToSlot, EvalMod, SlotToCoeff.  Returns a list."""
+        if any(c.scale != self.s_in for c in cts) or len({c.level for c in cts}) != 1:
+            raise HebatchError("Bootstrapper: a batch needs one level and this instance's input scale")
+        raised = self.ops.mod_raise(cts, ell_top)
+        return self.slot_to_coeff(self.eval_mod(self.coeff_to_slot(raised)))
 
 
 class GpuBootOps:
-    """The circuit's backend on GpuEngine: every call is one of the engine's
-    batched C-ABI paths; no counters move (the caller accounts one bootstrap)."""
+    """The circuit's backend on GpuEngine: every call is one batched C-ABI
+    path over a list of ciphertexts; no counters move (the caller accounts
+    the bootstraps)."""
 
     def __init__(self, eng):
         self.e = eng
         self.moduli = eng.moduli
         self._pts = {}  # (stage tag, limbs, pt_scale) -> encoded diagonals [rows * b][limbs][N]
 
-    def mod_raise(self, ct, ell_out):
-        e = self.e
-        out = e._alloc(1, 2, ell_out)
+    def mod_raise(self, cts, ell_out):
         from . import _lib
 
-        src, dst = e._ptrs([ct]), e._tptrs(out)
-        _lib.check(e._call("mod_raise", e._L.he_mod_raise, e._h, _lib.addr(src), ct.level + 1, _lib.addr(dst), 1,
-                           ell_out, e.stream), "mod_raise")
-        return e._wrap_batch(out, ell_out - 1, [ct.scale])[0]
+        e = self.e
+        out = e._alloc(len(cts), 2, ell_out)
+        src, dst = e._ptrs(cts), e._tptrs(out)
+        _lib.check(e._call("mod_raise", e._L.he_mod_raise, e._h, _lib.addr(src), cts[0].level + 1, _lib.addr(dst),
+                           len(cts), ell_out, e.stream), "mod_raise")
+        return e._wrap_batch(out, ell_out - 1, [c.scale for c in cts])
 
     def rotate_hoisted(self, cts, ks):
         return self.e._rotate_hoisted_internal(cts, ks)
 
-    def rotate(self, ct, k):
-        return self.e._rotate_batch([ct], k)[0] if k % self.e.context.n else ct
+    def rotate(self, cts, k):
+        return self.e._rotate_batch(cts, k) if k % self.e.context.n else list(cts)
 
-    def conj(self, ct):
-        return self.e._automorph_batch([ct], 2 * self.e.N - 1)[0]
+    def conj(self, cts):
+        return self.e._automorph_batch(cts, 2 * self.e.N - 1)
 
-    def mul_monomial(self, ct, power):
-        return self.e._mul_monomial_batch([ct], power)[0]
+    def mul_monomial(self, cts, power):
+        return self.e._mul_monomial_batch(cts, power)
 
-    def add(self, a, b):
-        return self.e._add_batch([a], [b])[0]
+    def add(self, A, B):
+        return self.e._add_batch(A, B)
 
-    def sub(self, a, b):
-        return self.e._add_batch([a], [b], sub=True)[0]
+    def sub(self, A, B):
+        return self.e._add_batch(A, B, sub=True)
 
-    def add_const(self, ct, v):
-        return self.e.add_const_batch([ct], [v], count=False)[0]
+    def add_const(self, cts, v):
+        return self.e.add_const_batch(cts, [v] * len(cts), count=False)
 
-    def mul_int(self, ct, k, out_scale):
-        return self.e._mul_int_batch([ct], [k], [out_scale])[0]
+    def mul_int(self, cts, k, out_scale):
+        return self.e._mul_int_batch(cts, [k] * len(cts), [out_scale] * len(cts))
 
     def mult_ct(self, A, B):
         return self.e._mult_ct_batch(A, B)
 
-    def lincomb(self, ins, weights, bias, out_scale):
-        n = len(ins)
-        return self.e.lincomb(ins, [0, n], list(range(n)), list(weights), bias=[bias], out_scale=out_scale,
-                              count_as_conv=False)[0]
+    def lincomb(self, groups, weights, bias, out_scale):
+        """out[i] = sum_t weights[t] groups[i][t] + bias, one launch for all groups."""
+        k = len(groups[0])
+        ins = [c for g in groups for c in g]
+        return self.e.lincomb(ins, list(range(0, len(ins) + 1, k)), list(range(len(ins))), list(weights) * len(groups),
+                              bias=[bias] * len(groups), out_scale=out_scale, count_as_conv=False)
 
     def lincomb_plain(self, ins, plains, pt_scale=1.0, key=None):
         """DFT levels: the encoded diagonals are cached on the device per (stage, level, scale)."""

@@ -1146,39 +1146,52 @@ class GpuEngine:
         """Real CKKS bootstrapping (bootstrap.py: ModRaise, CoeffToSlot, EvalMod,
         SlotToCoeff) with the reference's contract (engine.py:315-319): the
         result holds the same slots (up to the circuit's approximation error,
-        ~1e-5 with q_0 / scale = 2^10 and a 2^50 scale) at level
+        ~2e-5 with q_0 / scale = 2^10 and a 2^50 scale) at level
         max_level - bootstrap_reserve, and only the ``bootstraps`` counter
         moves.  The circuit needs bootstrap_reserve >= its depth
         (BootPlan.depth: 20 at N = 2^12 with the dense secret); its Galois keys
         (BSGS steps of the factored DFT and conjugation) are generated on
         first use."""
+        return self.bootstrap_batch([ct])[0]
+
+    def bootstrap_batch(self, cts: Sequence[CipherVec]) -> list[CipherVec]:
+        """bootstrap() for several ciphertexts at once: every step of the circuit
+        is one batched launch sequence for the whole batch (inputs of one level
+        and scale).  Counts one bootstrap per ciphertext."""
         from .bootstrap import Bootstrapper, GpuBootOps
 
-        self._check(ct)
-        self._need_two([ct], "bootstrap")
+        cts = list(cts)
+        if not cts:
+            return []
+        for c in cts:
+            self._check(c)
+        self._need_two(cts, "bootstrap")
+        if len({(c.level, c.scale) for c in cts}) != 1:
+            raise HebatchError("bootstrap_batch needs ciphertexts of one level and scale")
         plan = self.boot_plan()
         target = self.context.max_level - self.context.bootstrap_reserve
         if self.context.max_level - plan.depth < target:
             raise HebatchError(f"bootstrap_reserve {self.context.bootstrap_reserve} is below the bootstrap circuit's "
                                f"depth {plan.depth}")
         self._ensure_boot_keys(plan)
+        s_in = cts[0].scale
         booters = self.__dict__.setdefault("_booters", {})  # per input scale (SlotToCoeff folds 1 / scale)
-        if ct.scale not in booters:
+        if s_in not in booters:
             if len(booters) >= 4:
                 booters.pop(next(iter(booters)))
-            booters[ct.scale] = Bootstrapper(GpuBootOps(self), plan, ct.scale)
+            booters[s_in] = Bootstrapper(GpuBootOps(self), plan, s_in)
         with self._acct.lock:
             saved = (dict(self._acct.counts), self._acct.peak, self._acct.window_peak, set(self._acct.live))
-        out = booters[ct.scale].run(ct, self.context.n_q)
-        if out.level > target:
-            out = self.drop_level_batch([out], target)[0]
+        out = booters[s_in].run(cts, self.context.n_q)
+        if out[0].level > target:
+            out = self.drop_level_batch(out, target)
         with self._acct.lock:  # circuit temporaries are not user-visible ciphertexts
             counts, peak, wpeak, live = saved
             self._acct.counts = counts
-            self._acct.live = live | {out.id}
+            self._acct.live = live | {o.id for o in out}
             self._acct.peak = max(peak, len(self._acct.live))
             self._acct.window_peak = max(wpeak, len(self._acct.live))
-        self._acct.bump("bootstraps")
+        self._acct.bump("bootstraps", len(out))
         return out
 
     def ensure_level(self, ct: CipherVec, needed: int) -> CipherVec:

@@ -31,6 +31,8 @@ class OCt:
 
 
 class OracleBootOps:
+    """List-in, list-out backend (the circuit batches every step)."""
+
     def __init__(self, orc):
         self.orc = orc
         self.moduli = orc.moduli
@@ -42,11 +44,11 @@ class OracleBootOps:
             self._keys[g] = self.orc.switch_key(g)
         return self._keys[g]
 
-    def _res(self, v):
-        return lambda ell: np.array([int(v) % q for q in self.moduli[:ell]], np.uint64)
+    def _res(self, v, ell):
+        return np.array([int(v) % q for q in self.moduli[:ell]], np.uint64)
 
-    def mod_raise(self, ct, ell_out):
-        return OCt(self.orc.mod_raise(ct.data[:, :1], ell_out), ct.scale)
+    def mod_raise(self, cts, ell_out):
+        return [OCt(self.orc.mod_raise(c.data[:, :1], ell_out), c.scale) for c in cts]
 
     def rotate_hoisted(self, cts, ks):
         orc, n = self.orc, self.orc.n
@@ -61,52 +63,62 @@ class OracleBootOps:
             outs.append([OCt(orc.rotate_hoisted(c.data, g, self._hkeys[g]), c.scale) for c in cts])
         return outs
 
-    def rotate(self, ct, k):
+    def rotate(self, cts, k):
         n = self.orc.n
         if k % n == 0:
-            return ct
+            return list(cts)
         g = pow(5, k % n, 2 * self.orc.N)
-        return OCt(self.orc.rotate(ct.data, g, self.key(g)), ct.scale)
+        return [OCt(self.orc.rotate(c.data, g, self.key(g)), c.scale) for c in cts]
 
-    def conj(self, ct):
+    def conj(self, cts):
         g = 2 * self.orc.N - 1
-        return OCt(self.orc.rotate(ct.data, g, self.key(g)), ct.scale)
+        return [OCt(self.orc.rotate(c.data, g, self.key(g)), c.scale) for c in cts]
 
-    def mul_monomial(self, ct, power):
-        orc = self.orc
-        e = np.zeros(orc.N, np.uint64)
-        e[power % orc.N] = 1
-        pt = np.stack([orc.ntt(e if (power // orc.N) % 2 == 0 else np.where(e == 1, np.uint64(q - 1), e), l)
-                       for l, q in enumerate(self.moduli[:ct.ell])])
-        return OCt(orc.mul_plain(ct.data, pt), ct.scale)
+    def mul_monomial(self, cts, power):
+        orc, out = self.orc, []
+        for ct in cts:
+            e = np.zeros(orc.N, np.uint64)
+            e[power % orc.N] = 1
+            pt = np.stack([orc.ntt(e if (power // orc.N) % 2 == 0 else np.where(e == 1, np.uint64(q - 1), e), l)
+                           for l, q in enumerate(self.moduli[:ct.ell])])
+            out.append(OCt(orc.mul_plain(ct.data, pt), ct.scale))
+        return out
 
-    def add(self, a, b):
+    def _add(self, a, b, sub):
         ell = min(a.ell, b.ell)
-        return OCt(self.orc.add(np.ascontiguousarray(a.data[:, :ell]), np.ascontiguousarray(b.data[:, :ell])), a.scale)
+        f = self.orc.sub if sub else self.orc.add
+        return OCt(f(np.ascontiguousarray(a.data[:, :ell]), np.ascontiguousarray(b.data[:, :ell])), a.scale)
 
-    def sub(self, a, b):
-        ell = min(a.ell, b.ell)
-        return OCt(self.orc.sub(np.ascontiguousarray(a.data[:, :ell]), np.ascontiguousarray(b.data[:, :ell])), a.scale)
+    def add(self, A, B):
+        return [self._add(a, b, False) for a, b in zip(A, B)]
 
-    def add_const(self, ct, v):
-        return OCt(self.orc.add_const(ct.data, self._res(np.rint(v * ct.scale))(ct.ell)), ct.scale)
+    def sub(self, A, B):
+        return [self._add(a, b, True) for a, b in zip(A, B)]
 
-    def mul_int(self, ct, k, out_scale):
-        return OCt(self.orc.rescale(self.orc.mul_const(ct.data, self._res(k)(ct.ell))), out_scale)
+    def add_const(self, cts, v):
+        return [OCt(self.orc.add_const(c.data, self._res(np.rint(v * c.scale), c.ell)), c.scale) for c in cts]
+
+    def mul_int(self, cts, k, out_scale):
+        return [OCt(self.orc.rescale(self.orc.mul_const(c.data, self._res(k, c.ell))), out_scale) for c in cts]
 
     def mult_ct(self, A, B):
         rk = self.key(0)
+        ell = min(min(c.ell for c in A), min(c.ell for c in B))  # GpuEngine: one level per batch
         out = []
         for a, b in zip(A, B):
-            r = ON.mult_ct(self.orc, rk, ON.OracleCts(a.data, a.scale), ON.OracleCts(b.data, b.scale))
+            r = ON.mult_ct(self.orc, rk, ON.OracleCts(a.data[:, :ell], a.scale), ON.OracleCts(b.data[:, :ell], b.scale))
             out.append(OCt(r.data, r.scale))
         return out
 
-    def lincomb(self, ins, weights, bias, out_scale):
-        n = len(ins)
-        r = ON.lincomb(self.orc, [ON.OracleCts(c.data, c.scale) for c in ins], [0, n], list(range(n)),
-                       list(weights), [bias], out_scale)[0]
-        return OCt(r.data, r.scale)
+    def lincomb(self, groups, weights, bias, out_scale):
+        out = []
+        ell = min(c.ell for g in groups for c in g)  # GpuEngine.lincomb: inputs read at the minimum level
+        for g in groups:
+            n = len(g)
+            r = ON.lincomb(self.orc, [ON.OracleCts(c.data[:, :ell], c.scale) for c in g], [0, n], list(range(n)),
+                           list(weights), [bias], out_scale)[0]
+            out.append(OCt(r.data, r.scale))
+        return out
 
     def lincomb_plain(self, ins, plains, pt_scale=1.0, key=None):
         orc = self.orc

@@ -108,7 +108,7 @@ def test_bootstrap_circuit_on_the_oracle():
     assert np.max(np.abs(orc.decrypt(low.data, low.scale) - x)) < 1e-9
     ops = OracleBootOps(orc)
     plan = BootPlan(N=orc.N, q0=orc.moduli[0])
-    out = Bootstrapper(ops, plan, low.scale).run(low, orc.L)
+    out = Bootstrapper(ops, plan, low.scale).run([low], orc.L)[0]
     assert out.level == orc.L - 1 - plan.depth
     err = np.max(np.abs(orc.decrypt(out.data, out.scale) - x))
     assert err < 1e-4, err

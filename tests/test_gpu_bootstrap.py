@@ -106,7 +106,7 @@ def test_bootstrap_bit_exact_vs_oracle_circuit_and_contract(name):
     # limb for limb against the same circuit on the oracle
     plan = eng.boot_plan()
     src = to_np(ct.data)
-    ref = Bootstrapper(OracleBootOps(orc), plan, ct.scale).run(OCt(src[:, :1], ct.scale), eng.context.n_q)
+    ref = Bootstrapper(OracleBootOps(orc), plan, ct.scale).run([OCt(src[:, :1], ct.scale)], eng.context.n_q)[0]
     assert ref.level == out.level and ref.scale == out.scale
     assert np.array_equal(to_np(out.data), ref.data)
 
@@ -146,3 +146,20 @@ def test_bootstrap_precision_ensure_level_and_products(name):
     assert fresh.level == eng.context.max_level - reserve
     assert eng.snapshot_counters().bootstraps == n0 + 1
     assert np.max(np.abs(eng.decrypt(fresh) - x)) < 1e-4
+
+
+def test_bootstrap_batch_equals_single_bootstraps():
+    """bootstrap_batch: one launch sequence for several ciphertexts, each result
+    bit-identical to its own bootstrap (N = 2^11, sparse secret)."""
+    name = "boot11s"
+    eng = _boot_engine(name)
+    rng = np.random.default_rng(75)
+    xs = rng.uniform(-1, 1, (3, eng.context.n))
+    cts = eng.encrypt_batch(xs)
+    n0 = eng.snapshot_counters().bootstraps
+    outs = eng.bootstrap_batch(cts)
+    assert eng.snapshot_counters().bootstraps == n0 + 3
+    for i, c in enumerate(cts):
+        single = eng.bootstrap(c)
+        assert np.array_equal(to_np(outs[i].data), to_np(single.data)) and outs[i].scale == single.scale
+        assert np.max(np.abs(eng.decrypt(outs[i]) - xs[i])) < 1e-4
