@@ -34,6 +34,7 @@
 //     the epilogue does its FP64 work.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "ntt_core.cuh"  // u2d / d2u / fmulmod / fcanon
@@ -48,6 +49,26 @@ constexpr int CPT = 4;           // output channels per epilogue thread
 constexpr int PROD_WARPS = 3;    // warps 16-18
 constexpr int MMA_WARP = 19;
 constexpr int THREADS = 32 * 20;  // 5 warps per SM sub-partition: 96 registers per thread
+// setmaxnreg: the four epilogue warpgroups grow to EPI registers per thread, the producer / MMA
+// warpgroup shrinks to AUX; 512 * EPI + 128 * AUX <= 640 * 96 (the launch allocation), or the
+// epilogue's request never completes
+template <int EPI, int AUX>
+struct RegSplit {
+    static_assert(512 * EPI + 128 * AUX <= 640 * 96 && EPI % 8 == 0 && AUX % 8 == 0 && AUX >= 24, "register pool");
+    static __device__ __forceinline__ void epilogue() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI)); }
+    static __device__ __forceinline__ void aux() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(AUX)); }
+};
+#ifndef P1_EPI_REGS
+#define P1_EPI_REGS 104
+#define P1_AUX_REGS 64
+#endif
+#ifndef P16_EPI_REGS
+#define P16_EPI_REGS 112  // planar carry: the producers only issue bulk copies
+#define P16_AUX_REGS 32
+#endif
+using P1Regs = RegSplit<P1_EPI_REGS, P1_AUX_REGS>;
+using P16Regs = RegSplit<104, 64>;  // pointer-list inputs: the producers transpose in registers
+using P16RegsPlanar = RegSplit<P16_EPI_REGS, P16_AUX_REGS>;
 constexpr int NSLOT = 4;         // TMEM accumulator slots (128 columns each)
 constexpr int MC = 16;           // output channels per CTA
 
@@ -102,16 +123,24 @@ __device__ __forceinline__ int64_t madw(int64_t acc, int a, int b) {
 // shift sums C[0..NSH) -> y = sum_s C[s] 2^(8s) mod q as an unreduced integer-valued
 // double (|y| < 2^48.2): P0 = sum_{s<4}, P1 = sum_{s>=4} (x 2^32, one FP64 modular product)
 template <int NSH>
-__device__ __forceinline__ double recombine(const int (&C)[NSH], double yc, const ModConst &c) {
+__device__ __forceinline__ void recombine_int(const int (&C)[NSH], int64_t &p0, int64_t &p1) {
     static_assert(NSH >= 5 && NSH <= 7, "40-bit limbs: 5 byte planes, 1-3 weight digits");
     // |C[s]| < 2^22, so pairs of shifts combine in 32 bits (|C0 + 2^8 C1| < 2^30.1)
     const int q0 = C[0] + C[1] * 256, q1 = C[2] + C[3] * 256;
     const int q2 = NSH > 5 ? C[4] + C[NSH > 5 ? 5 : 4] * 256 : C[4];
-    const int64_t p0 = madw((int64_t)q0, q1, 1 << 16);
-    const int64_t p1 = NSH > 6 ? madw((int64_t)q2, C[NSH > 6 ? 6 : 4], 1 << 16) : (int64_t)q2;
+    p0 = madw((int64_t)q0, q1, 1 << 16);
+    p1 = NSH > 6 ? madw((int64_t)q2, C[NSH > 6 ? 6 : 4], 1 << 16) : (int64_t)q2;
+}
+__device__ __forceinline__ double recombine_fp(int64_t p0, int64_t p1, double yc, const ModConst &c) {
     const double d0 = __longlong_as_double(0x4338000000000000ll + p0) - 6755399441055744.0;
     const double d1 = __longlong_as_double(0x4338000000000000ll + p1) - 6755399441055744.0;
     return d0 + fmulmod(d1, yc, c.qd, c.qid);
+}
+template <int NSH>
+__device__ __forceinline__ double recombine(const int (&C)[NSH], double yc, const ModConst &c) {
+    int64_t p0, p1;
+    recombine_int<NSH>(C, p0, p1);
+    return recombine_fp(p0, p1, yc, c);
 }
 
 // exact integer-valued double |x| < 2^50 -> canonical residue (magic-constant
@@ -202,6 +231,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
 
     if (warp >= EPI_WARPS && warp < EPI_WARPS + PROD_WARPS) {
         // ======================= producers: input rows -> packed ring rows
+        P1Regs::aux();
         const int pt = threadIdx.x - EPI_WARPS * 32;  // 0..95
         constexpr int PT = PROD_WARPS * 32;
         const uint32_t ring_s = tc5::smem_u32(ring);
@@ -255,6 +285,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
             }
         }
     } else if (warp == MMA_WARP) {
+        P1Regs::aux();
         // ======================= MMA issuer
         if (lane == 0) {
             tc5::mbar_wait(&bar_b, 0);
@@ -313,6 +344,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
         __syncwarp();
     } else if (warp < EPI_WARPS) {
         // ======================= epilogue
+        P1Regs::epilogue();
         const int qd = warp & 3, cg = warp >> 2;  // TMEM lane quarter, channel group (CPT channels)
         const int row = qd * 32 + lane, xl = row >> 3, j = row & 7;
         const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(cg * 32);
@@ -471,7 +503,9 @@ __device__ __forceinline__ void tr4b(uint32_t w0, uint32_t w1, uint32_t w2, uint
     o[3] = __byte_perm(t2, t3, 0x7632);
 }
 
+template <bool PLANAR>
 __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
+    using Regs = std::conditional_t<PLANAR, P16RegsPlanar, P16Regs>;
     using LY = P16Layout;
     constexpr int NCI = 3, PS = LY::PS, RR = LY::RR, NSH = 6;
     constexpr int NSL = 5, SLC = 96;  // TMEM slots: 5 x 96 columns (one per (row step, component))
@@ -487,7 +521,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
     double *red = (double *)(bsm + LY::BBYTES);        // [4 cg][4 m][5 s][8 j] cross-quarter GAP sums
     uint32_t *ptab = (uint32_t *)(red + 4 * CPT * 5 * 8);  // input offsets (256-byte units)
     uint8_t *stg = (uint8_t *)(((uintptr_t)(ptab + a.p * a.H * a.W) + 127) & ~(uintptr_t)127);  // 2 x 24 KB staging
-    if (!a.pl_in)
+    if (!PLANAR)
         for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.ioff[i];
     const size_t N = (size_t)1 << a.logN;
     const int nchunk = (int)(N / 8);
@@ -497,7 +531,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < RR; i++) {
-            tc5::mbar_init(&bar_full[i], a.pl_in ? 1 : PROD_WARPS * 32);
+            tc5::mbar_init(&bar_full[i], PLANAR ? 1 : PROD_WARPS * 32);
             tc5::mbar_init(&bar_empty[i], 1);
         }
         for (int i = 0; i < NSL; i++) {
@@ -527,6 +561,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
 
     if (warp >= EPI_WARPS && warp < EPI_WARPS + PROD_WARPS) {
         // ======================= producers: input rows -> plane-separated ring rows
+        Regs::aux();
         // Half rows (8 pixels x 3 components x 16 channels x 8 coefficients = 24 KB) are
         // copied raw into two shared staging buffers with cp.async (no registers held, a half
         // row in flight while the other is transposed), then byte-transposed into the ring.
@@ -562,7 +597,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
             issued++;
             (void)kk;
         };
-        if (a.pl_in) {
+        if constexpr (PLANAR) {
             // planar carry: one bulk copy (TMA engine) per input row into pixel slots 1..W
             const uint32_t rowb = (uint32_t)W * PS;
             for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
@@ -666,6 +701,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
     } else if (warp == MMA_WARP) {
+        Regs::aux();
         // ======================= MMA issuer (warp-uniform loop, one elected lane issues)
         {
             tc5::mbar_wait(&bar_b, 0);
@@ -724,6 +760,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
         }
     } else if (warp < EPI_WARPS) {
         // ======================= epilogue
+        Regs::epilogue();
         const int qd = warp & 3, cg = warp >> 2;
         const int row = qd * 32 + lane, j = row & 7;
         const bool exp1 = a.exp == 1, hasb = a.biasd != nullptr;  // no bias: no per-row loads
@@ -1105,7 +1142,8 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
         HE_CHECK_LAUNCH();
         return HE_OK;
     };
-    if (p16) rc = launch(k_convtc_p16_gap);
+    if (p16 && pl_in) rc = launch(k_convtc_p16_gap<true>);
+    else if (p16) rc = launch(k_convtc_p16_gap<false>);
     else if (NSH == 5) rc = launch(k_convtc_p1_pool<5>);
     else if (NSH == 6) rc = launch(k_convtc_p1_pool<6>);
     else rc = launch(k_convtc_p1_pool<7>);
