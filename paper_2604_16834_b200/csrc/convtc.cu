@@ -82,7 +82,6 @@ struct TcArgs {
     const uint8_t *btiles;       // B tiles (global), copied to shared memory once per CTA
     const double *biasd;         // [MC][ell] plain-domain bias (component 0), canonical
     const uint64_t *cst;         // [ell] constant added to component 0 of every output (or nullptr)
-    const double *yc;            // [ell] 2^32 mod q
     const ModConst *mc;
     const int32_t *limbs;        // [nlimbs] limb of limb-index
     int nlimbs, ell, logN, p, H, W, M, y0, y1, nwin, nitems;
@@ -106,6 +105,26 @@ struct TcArgs {
         if (prof_on) pc[slot] += clock64() - _t0;               \
     } while (0)
 
+// diagnostic build (-DCONVTC_PHASES, scripts/gpu): only the sampled epilogue thread reports, and
+// counters [0], [2], [3] hold its TMEM-load, recombination and window-product cycles
+#ifdef CONVTC_PHASES
+#define PH_ONLY_EPI (threadIdx.x == 0)
+#define PH_START() long long tph = clock64()
+#define PH(i)                                  \
+    if (prof_on) {                             \
+        const long long _n = clock64();        \
+        pc[i] += _n - tph;                     \
+        tph = _n;                              \
+    }
+#define PH_RESET() \
+    if (prof_on) tph = clock64()
+#else
+#define PH_ONLY_EPI true
+#define PH_START()
+#define PH(i)
+#define PH_RESET()
+#endif
+
 // ---------------------------------------------------------------- shared layout
 // ring row: (W + 3) pixel slots (halo, W pixels, halo, pad) x NCI components x
 // 128 bytes (8 coefficients x 16-byte chunk); RR rows
@@ -120,27 +139,51 @@ __device__ __forceinline__ int64_t madw(int64_t acc, int a, int b) {
     return acc;
 }
 
-// shift sums C[0..NSH) -> y = sum_s C[s] 2^(8s) mod q as an unreduced integer-valued
-// double (|y| < 2^48.2): P0 = sum_{s<4}, P1 = sum_{s>=4} (x 2^32, one FP64 modular product)
+// K independent FP64 modular products issued stage by stage (the K dependency chains
+// interleave in program order instead of running one after the other); each lane of the
+// batch computes exactly fmulmod(a, b)
+template <int K>
+__device__ __forceinline__ void fmulmod_v(const double (&a)[K], const double (&b)[K], double (&r)[K], double q,
+                                          double qi) {
+    double h[K], e[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) h[k] = a[k] * b[k];
+#pragma unroll
+    for (int k = 0; k < K; k++) e[k] = rint(h[k] * qi);
+#pragma unroll
+    for (int k = 0; k < K; k++) r[k] = fma(a[k], b[k], -h[k]);
+#pragma unroll
+    for (int k = 0; k < K; k++) h[k] = fma(-e[k], q, h[k]);
+#pragma unroll
+    for (int k = 0; k < K; k++) r[k] = h[k] + r[k];
+}
+// Recombination on the INTEGER pipe.  On B200 the FP64 pipe and the tensor core share one
+// issue resource (scripts/mb/mb_fp64_vs_mma.cu: a running tcgen05.mma stream cuts FP64
+// throughput 3x and is itself slowed), so every FP64 instruction the epilogue does not issue is
+// tensor time.  With kq = 2^40 - q < 2^25 (the 40-bit NTT primes are 2^40 - j 2N + 1, j small):
+//   S = sum_{s<6} C[s] 2^(8s) (int64, |S| < 2^62.2) = S_hi 2^40 + S_lo, 0 <= S_lo < 2^40
+//   y = S_lo + (S_hi + 2^8 C[6]) kq  == S + C[6] 2^48 (mod q)
+// and, with a seventh shift sum, one more fold; the result is an exact integer |y| < 2^47,
+// congruent to recombine<NSH>() (which differs from it by a multiple of q).
 template <int NSH>
-__device__ __forceinline__ void recombine_int(const int (&C)[NSH], int64_t &p0, int64_t &p1) {
+__device__ __forceinline__ double recombine_fold(const int (&C)[NSH], int kq) {
     static_assert(NSH >= 5 && NSH <= 7, "40-bit limbs: 5 byte planes, 1-3 weight digits");
-    // |C[s]| < 2^22, so pairs of shifts combine in 32 bits (|C0 + 2^8 C1| < 2^30.1)
+    constexpr int64_t M40 = (1ll << 40) - 1;
     const int q0 = C[0] + C[1] * 256, q1 = C[2] + C[3] * 256;
     const int q2 = NSH > 5 ? C[4] + C[NSH > 5 ? 5 : 4] * 256 : C[4];
-    p0 = madw((int64_t)q0, q1, 1 << 16);
-    p1 = NSH > 6 ? madw((int64_t)q2, C[NSH > 6 ? 6 : 4], 1 << 16) : (int64_t)q2;
+    int64_t S = madw((int64_t)q0, q1, 1 << 16);
+    S += (int64_t)q2 << 32;
+    int hi = (int)(S >> 40);  // |hi| < 2^22.2
+    if (NSH > 6) hi += C[NSH > 6 ? 6 : 4] * 256;  // |hi| < 2^30.2
+    int64_t y = madw(S & M40, hi, kq);
+    if (NSH > 6) y = madw(y & M40, (int)(y >> 40), kq);  // |y >> 40| < 2^15
+    return __longlong_as_double(0x4338000000000000ll + y) - 6755399441055744.0;
 }
-__device__ __forceinline__ double recombine_fp(int64_t p0, int64_t p1, double yc, const ModConst &c) {
-    const double d0 = __longlong_as_double(0x4338000000000000ll + p0) - 6755399441055744.0;
-    const double d1 = __longlong_as_double(0x4338000000000000ll + p1) - 6755399441055744.0;
-    return d0 + fmulmod(d1, yc, c.qd, c.qid);
-}
-template <int NSH>
-__device__ __forceinline__ double recombine(const int (&C)[NSH], double yc, const ModConst &c) {
-    int64_t p0, p1;
-    recombine_int<NSH>(C, p0, p1);
-    return recombine_fp(p0, p1, yc, c);
+// recombination of K channels at once
+template <int NSH, int K>
+__device__ __forceinline__ void recombine_v(const int (&C)[K][NSH], int kq, double (&y)[K]) {
+#pragma unroll
+    for (int k = 0; k < K; k++) y[k] = recombine_fold<NSH>(C[k], kq);
 }
 
 // exact integer-valued double |x| < 2^50 -> canonical residue (magic-constant
@@ -354,7 +397,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
             const int li = item / nchunk, l = a.limbs[li];
             const size_t coff = (size_t)(item % nchunk) * 8;
             const ModConst c = a.mc[l];
-            const double yc = a.yc[l];
+            const int kq = (int)(1099511627776.0 - c.qd);  // 2^40 - q < 2^25 (checked by the launcher)
             const double cstd = a.cst ? (double)a.cst[l] : 0.0;  // canonical, < 2^40
             double biasd[CPT];
 #pragma unroll
@@ -394,15 +437,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                                                      : s2 < 6 ? r1[(s2 - 4) * 4 + m] : r2[m]);
                             tc5::tc_fence_before();
                             tc5::mbar_arrive(&bar_dempty[ds]);
-#pragma unroll
-                            for (int m = 0; m < CPT; m++) yv[cc][m] = recombine<NSH>(C[m], yc, c);
+                            recombine_v<NSH, CPT>(C, kq, yv[cc]);
                         }
+                        {
+                            double d0[CPT], t[CPT];
 #pragma unroll
-                        for (int m = 0; m < CPT; m++) {
-                            const double d0 = yv[0][m] + biasd[m], d1 = yv[1][m];
-                            acc[m][0] += fmulmod(d0, d0, c.qd, c.qid);
-                            acc[m][1] += fmulmod(d0, d1, c.qd, c.qid);
-                            acc[m][2] += fmulmod(d1, d1, c.qd, c.qid);
+                            for (int m = 0; m < CPT; m++) d0[m] = yv[0][m] + biasd[m];
+                            fmulmod_v<CPT>(d0, d0, t, c.qd, c.qid);
+#pragma unroll
+                            for (int m = 0; m < CPT; m++) acc[m][0] += t[m];
+                            fmulmod_v<CPT>(d0, yv[1], t, c.qd, c.qid);
+#pragma unroll
+                            for (int m = 0; m < CPT; m++) acc[m][1] += t[m];
+                            fmulmod_v<CPT>(yv[1], yv[1], t, c.qd, c.qid);
+#pragma unroll
+                            for (int m = 0; m < CPT; m++) acc[m][2] += t[m];
                         }
                     }
                     // window = this pixel + its x-neighbour (lane ^ 8), rows yp, yp+1.  Reduce-scatter
@@ -555,7 +604,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
     __syncthreads();
     tc5::tc_fence_after();
     const uint32_t tmem = taddr_s;
-    const bool prof_on = a.prof && (threadIdx.x == 0 || threadIdx.x == EPI_WARPS * 32 || threadIdx.x == MMA_WARP * 32);
+    const bool prof_on = a.prof && PH_ONLY_EPI && (threadIdx.x == 0 || threadIdx.x == EPI_WARPS * 32 || threadIdx.x == MMA_WARP * 32);
     long long pc[7] = {0, 0, 0, 0, 0, 0, 0};
     const long long t_start = clock64();
 
@@ -771,19 +820,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
             const int l = a.limbs[it / nchunk];
             const size_t coff = (size_t)(it % nchunk) * 8;
             const ModConst c = a.mc[l];
-            const double yc = a.yc[l];
+            const int kq = (int)(1099511627776.0 - c.qd);  // 2^40 - q < 2^25 (checked by the launcher)
             const int m0 = half * MC + cg * CPT;  // this thread's first output channel
             double gs[CPT][5];  // (y0 y0, y0 y1, 2 y0 y2 + y1 y1, y1 y2, y2 y2) over the thread's pixel column
 #pragma unroll
             for (int m = 0; m < CPT; m++)
 #pragma unroll
                 for (int s2 = 0; s2 < 5; s2++) gs[m][s2] = 0.0;
+            PH_START();
             for (int yr = 0; yr < nrows; yr++) {
                 double yv[NCI][CPT];
 #pragma unroll
                 for (int cc = 0; cc < NCI; cc++, S++) {
                     const int ds = S % NSL;
                     PWAIT(5, tc5::mbar_wait(&bar_dfull[ds], (S / NSL) & 1));
+                    PH_RESET();
                     tc5::tc_fence_after();
                     int C[CPT][NSH];
                     const uint32_t ta = tq + (uint32_t)ds * SLC;
@@ -797,23 +848,38 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                     tc5::tld_wait();
                     tc5::tc_fence_before();
                     tc5::mbar_arrive(&bar_dempty[ds]);
-#pragma unroll
-                    for (int m = 0; m < CPT; m++) yv[cc][m] = recombine<NSH>(C[m], yc, c);
+                    PH(0);
+                    recombine_v<NSH, CPT>(C, kq, yv[cc]);
+                    PH(2);
                 }
                 if (exp1) {
 #pragma unroll
                     for (int m = 0; m < CPT; m++) gs[m][0] += yv[0][m] + yv[1][m] + yv[2][m];
-                } else
+                } else {
+                    double t[CPT], d00[CPT];
+                    if (hasb)
 #pragma unroll
-                for (int m = 0; m < CPT; m++) {
-                    const double d0 = hasb ? yv[0][m] + a.biasd[(size_t)(m0 + m) * a.ell + l] : yv[0][m];
-                    const double d1 = yv[1][m], d2 = yv[2][m];
-                    gs[m][0] += fmulmod(d0, d0, c.qd, c.qid);
-                    gs[m][1] += fmulmod(d0, d1, c.qd, c.qid);
-                    gs[m][2] += fmulmod(d0 + d0, d2, c.qd, c.qid) + fmulmod(d1, d1, c.qd, c.qid);
-                    gs[m][3] += fmulmod(d1, d2, c.qd, c.qid);
-                    gs[m][4] += fmulmod(d2, d2, c.qd, c.qid);
+                        for (int m = 0; m < CPT; m++) yv[0][m] += a.biasd[(size_t)(m0 + m) * a.ell + l];
+                    fmulmod_v<CPT>(yv[0], yv[0], t, c.qd, c.qid);
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) gs[m][0] += t[m];
+                    fmulmod_v<CPT>(yv[0], yv[1], t, c.qd, c.qid);
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) gs[m][1] += t[m];
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) d00[m] = yv[0][m] + yv[0][m];
+                    fmulmod_v<CPT>(d00, yv[2], t, c.qd, c.qid);
+                    fmulmod_v<CPT>(yv[1], yv[1], d00, c.qd, c.qid);
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) gs[m][2] += t[m] + d00[m];
+                    fmulmod_v<CPT>(yv[1], yv[2], t, c.qd, c.qid);
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) gs[m][3] += t[m];
+                    fmulmod_v<CPT>(yv[2], yv[2], t, c.qd, c.qid);
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) gs[m][4] += t[m];
                 }
+                PH(3);
                 if ((yr & 15) == 15)  // keep the exact sums below 2^53: centre every 16 rows
 #pragma unroll
                     for (int m = 0; m < CPT; m++)
@@ -1002,8 +1068,8 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
         return HE_EINVAL;
     }
     for (int l = 0; l < ell; l++)
-        if (c->mod[l] < (1ull << 36) || c->mod[l] >= (1ull << 40)) {
-            he_set_error("he_conv_square_sum_tc: prime %d outside [2^36, 2^40)", l);
+        if (c->mod[l] <= (1ull << 40) - (1ull << 25) || c->mod[l] >= (1ull << 40)) {  // recombine_fold: 2^40 - q < 2^25
+            he_set_error("he_conv_square_sum_tc: prime %d outside (2^40 - 2^25, 2^40)", l);
             return HE_EINVAL;
         }
     int64_t wmax = 0;
@@ -1025,10 +1091,9 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
     else
         build_btiles_p1(weights, M, p, E, NSH, bt);
     const int TB = p16 ? P16Layout::TB : P1_NCOL * 32;
-    std::vector<double> biasd((size_t)2 * MC * ell, 0.0), yc(ell);
+    std::vector<double> biasd((size_t)2 * MC * ell, 0.0);
     for (int l = 0; l < ell; l++) {
         const uint64_t q = c->mod[l];
-        yc[l] = (double)(((uint64_t)1 << 32) % q);
         if (cst && cst[l] >= q) {
             he_set_error("he_conv_square_sum_tc: residue not canonical");
             return HE_EINVAL;
@@ -1070,10 +1135,10 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
     if (out) HE_TRY(he_upload_ptrs((const void *const *)out, n_out, &dout, s));
     std::vector<int32_t> lorder(ell);
     for (int l = 0; l < ell; l++) lorder[l] = l;
-    const size_t b_bt = bt.size(), b_bias = biasd.size() * 8, b_yc = (size_t)ell * 8, b_lo = (size_t)ell * 4,
+    const size_t b_bt = bt.size(), b_bias = biasd.size() * 8, b_lo = (size_t)ell * 4,
                  b_c = cst ? (size_t)ell * 8 : 0, b_io = in ? (size_t)n_in * 4 : 16;
     char *meta = nullptr;
-    HE_TRY(he_scratch_alloc((void **)&meta, b_bt + b_bias + b_yc + b_lo + b_c + b_io + 1024, s));
+    HE_TRY(he_scratch_alloc((void **)&meta, b_bt + b_bias + b_lo + b_c + b_io + 1024, s));
     size_t off = 0;
     auto carve = [&](size_t bytes) {
         char *q = meta + off;
@@ -1082,14 +1147,12 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
     };
     uint8_t *dbt = (uint8_t *)carve(b_bt);
     double *dbias = (double *)carve(b_bias);
-    double *dyc = (double *)carve(b_yc);
     int32_t *dlo = (int32_t *)carve(b_lo);
     uint64_t *dc = cst ? (uint64_t *)carve(b_c) : nullptr;
     uint32_t *dio = (uint32_t *)carve(b_io);
     if (in) HE_CHECK_CUDA(he_h2d(dio, ioff.data(), b_io, s));
     HE_CHECK_CUDA(he_h2d(dbt, bt.data(), b_bt, s));
     HE_CHECK_CUDA(he_h2d(dbias, biasd.data(), b_bias, s));
-    HE_CHECK_CUDA(he_h2d(dyc, yc.data(), b_yc, s));
     HE_CHECK_CUDA(he_h2d(dlo, lorder.data(), b_lo, s));
     if (dc) HE_CHECK_CUDA(he_h2d(dc, cst, b_c, s));
     TcArgs a;
@@ -1114,7 +1177,6 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
     // P16 reads the bias per row only when there is one (config 3's biases are zero)
     a.biasd = (p16 && std::all_of(biasd.begin(), biasd.end(), [](double v) { return v == 0.0; })) ? nullptr : dbias;
     a.cst = dc;
-    a.yc = dyc;
     a.mc = c->d_mc;
     a.limbs = dlo;
     a.nlimbs = ell;
