@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
     __syncthreads();
     tc5::tc_fence_after();
     const uint32_t tmem = taddr_s;
-    const bool prof_on = a.prof && (threadIdx.x == 0 || threadIdx.x == EPI_WARPS * 32 || threadIdx.x == MMA_WARP * 32);
+    const bool prof_on = a.prof && PH_ONLY_EPI && (threadIdx.x == 0 || threadIdx.x == EPI_WARPS * 32 || threadIdx.x == MMA_WARP * 32);
     long long pc[7] = {0, 0, 0, 0, 0, 0, 0};
     const long long t_start = clock64();
 
@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
 #pragma unroll
             for (int m = 0; m < CPT; m++)
                 obm[m] = a.obase ? a.obase + (size_t)(cg * CPT + m) * a.nwin * a.ostride + lo : nullptr;
+            PH_START();
             for (int pr = 0; pr < npairs; pr++) {
                 for (int xb = 0; xb < XB; xb++) {
                     double acc[CPT][3];
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                         for (int cc = 0; cc < NCI; cc++, S++) {
                             const int ds = S % NSLOT;
                             PWAIT(5, tc5::mbar_wait(&bar_dfull[ds], (S / NSLOT) & 1));
+                            PH_RESET();
                             tc5::tc_fence_after();
                             int C[CPT][NSH];
                             const uint32_t ta = tq + (uint32_t)ds * 128;
@@ -437,7 +439,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                                                      : s2 < 6 ? r1[(s2 - 4) * 4 + m] : r2[m]);
                             tc5::tc_fence_before();
                             tc5::mbar_arrive(&bar_dempty[ds]);
+                            PH(0);
                             recombine_v<NSH, CPT>(C, kq, yv[cc]);
+                            PH(2);
                         }
                         {
                             double d0[CPT], t[CPT];
@@ -453,6 +457,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
 #pragma unroll
                             for (int m = 0; m < CPT; m++) acc[m][2] += t[m];
                         }
+                        PH(3);
                     }
                     // window = this pixel + its x-neighbour (lane ^ 8), rows yp, yp+1.  Reduce-scatter
                     // over the pair: lane par keeps channels 2 par, 2 par + 1 of its window (no
@@ -561,6 +566,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar_full[RR], bar_empty[RR], bar_dfull[NSL], bar_dempty[NSL], bar_b;
     __shared__ uint32_t taddr_s;
+    __shared__ unsigned int fin_cnt[4];  // planar: arrivals of a channel group's four lane quarters
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int W = a.W, H = a.H;
@@ -568,7 +574,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
     uint8_t *ring = smem;
     uint8_t *bsm = smem + (size_t)RR * RS;
     double *red = (double *)(bsm + LY::BBYTES);        // [4 cg][4 m][5 s][8 j] cross-quarter GAP sums
-    uint32_t *ptab = (uint32_t *)(red + 4 * CPT * 5 * 8);  // input offsets (256-byte units)
+    uint32_t *ptab = (uint32_t *)(red + (PLANAR ? 16 : 4) * CPT * 5 * 8);  // input offsets (256-byte units)
     uint8_t *stg = (uint8_t *)(((uintptr_t)(ptab + a.p * a.H * a.W) + 127) & ~(uintptr_t)127);  // 2 x 24 KB staging
     if (!PLANAR)
         for (int i = threadIdx.x; i < a.p * a.H * a.W; i += THREADS) ptab[i] = a.ioff[i];
@@ -589,6 +595,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
         }
         tc5::mbar_init(&bar_b, 1);
         tc5::mbar_fence_init();
+        fin_cnt[0] = fin_cnt[1] = fin_cnt[2] = fin_cnt[3] = 0;
     }
     for (int i = threadIdx.x * 16; i < RR * RS; i += THREADS * 16) *(uint4 *)(ring + i) = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
@@ -815,12 +822,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
         const bool exp1 = a.exp == 1, hasb = a.biasd != nullptr;  // no bias: no per-row loads
         const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(cg * CPT);
         int k = 0, S = 0;
+        int li_cur = -1, l = 0, kq = 0;
+        ModConst c;
         for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
             const int it = item >> 1;
-            const int l = a.limbs[it / nchunk];
             const size_t coff = (size_t)(it % nchunk) * 8;
-            const ModConst c = a.mc[l];
-            const int kq = (int)(1099511627776.0 - c.qd);  // 2^40 - q < 2^25 (checked by the launcher)
+            if (it / nchunk != li_cur) {  // a CTA's consecutive items mostly share the limb: reload on change only
+                li_cur = it / nchunk;
+                l = a.limbs[li_cur];
+                c = a.mc[l];
+                kq = (int)(1099511627776.0 - c.qd);  // 2^40 - q < 2^25 (checked by the launcher)
+            }
             const int m0 = half * MC + cg * CPT;  // this thread's first output channel
             double gs[CPT][5];  // (y0 y0, y0 y1, 2 y0 y2 + y1 y1, y1 y2, y2 y2) over the thread's pixel column
 #pragma unroll
@@ -880,7 +892,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                     for (int m = 0; m < CPT; m++) gs[m][4] += t[m];
                 }
                 PH(3);
-                if ((yr & 15) == 15)  // keep the exact sums below 2^53: centre every 16 rows
+                if ((yr & 15) == 15 && yr + 1 < nrows)  // keep the exact sums below 2^53: centre every 16 rows
 #pragma unroll
                     for (int m = 0; m < CPT; m++)
 #pragma unroll
@@ -901,6 +913,47 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                     v += __shfl_xor_sync(0xffffffffu, v, 16);
                     gs[m][s2] = v;
                 }
+            PH(1);
+            if constexpr (PLANAR) {
+                // no warp waits for another: each quarter leaves its partial sums in its own
+                // shared-memory block and counts in; the LAST of the channel group's four warps
+                // to arrive adds the four blocks and writes the outputs.  (A warp cannot reach the
+                // end of the next item before every warp has finished this one: the TMEM slots
+                // of the next item's rows are released by all sixteen warps.)
+                double *blk = red + (size_t)(cg * 4 + qd) * (CPT * 5 * 8);
+                if (lane < 8)
+#pragma unroll
+                    for (int m = 0; m < CPT; m++)
+#pragma unroll
+                        for (int s2 = 0; s2 < 5; s2++) blk[(m * 5 + s2) * 8 + lane] = gs[m][s2];
+                __syncwarp();
+                unsigned int old = 0;
+                if (lane == 0) {
+                    __threadfence_block();
+                    old = atomicAdd(&fin_cnt[cg], 1u);
+                }
+                old = __shfl_sync(0xffffffffu, old, 0);
+                PH(4);
+                if ((old & 3u) == 3u) {
+                    __threadfence_block();
+                    const double *b0 = red + (size_t)(cg * 4) * (CPT * 5 * 8);
+                    const size_t cs = (size_t)a.ell * N;
+                    const double cstd = a.cst ? (double)a.cst[l] : 0.0;
+#pragma unroll
+                    for (int i = 0; i < CPT * 5 * 8 / 32; i++) {
+                        const int idx = lane + 32 * i, jj = idx & 7, s2 = (idx >> 3) % 5, m = idx / 40;
+                        const volatile double *p = b0 + idx;
+                        double v = p[0] + p[CPT * 5 * 8] + p[2 * CPT * 5 * 8] + p[3 * CPT * 5 * 8];
+                        v = s2 == 0 ? v + cstd : (s2 & 1) ? 2.0 * v : v;
+                        const int mo = m0 + m;
+                        if (mo < a.M) {
+                            uint64_t *o = (a.obase ? a.obase + (size_t)mo * a.ostride : a.out[mo]) + (size_t)l * N + coff;
+                            o[(size_t)s2 * cs + jj] = canon_fast(v, c.qd, c.qid);
+                        }
+                    }
+                }
+                __syncwarp();
+            } else {
             // quarters 0..3 add into red[cg] in turn (named barrier over the epilogue warps)
             double *rr2 = red + (size_t)cg * (CPT * 5 * 8);
             for (int q2 = 0; q2 < 4; q2++) {
@@ -924,6 +977,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                     default: asm volatile("bar.sync 5, 128;" ::: "memory"); break;
                 }
             }
+            PH(4);
             if (qd == 3 && lane < 8) {
                 const size_t lo = (size_t)l * N + coff + j;
                 const size_t cs = (size_t)a.ell * N;
@@ -939,6 +993,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                     o[3 * cs] = canon_fast(2.0 * gs[m][3], c.qd, c.qid);
                     o[4 * cs] = canon_fast(gs[m][4], c.qd, c.qid);
                 }
+            }
             }
         }
     }
@@ -1111,7 +1166,7 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
     const int nwin = pool ? ((y1 - y0) / 2) * (W / 2) : 1;
     const int n_in = p * H * W, n_out = M * nwin;
     const size_t smem = p16 ? (size_t)P16Layout::RR * (W + 3) * P16Layout::PS + P16Layout::BBYTES +
-                                  (pl_in ? 0 : (size_t)n_in * 4 + 128 + P16Layout::STG) + (size_t)4 * CPT * 5 * 8 * 8
+                                  (pl_in ? 0 : (size_t)n_in * 4 + 128 + P16Layout::STG) + (size_t)(pl_in ? 16 : 4) * CPT * 5 * 8 * 8
                             : (size_t)P1Layout<2>::RR * (W + 3) * P1Layout<2>::PS + 6 * (size_t)TB + (size_t)n_in * 4;
     // inputs as 32-bit offsets from the lowest address in 256-byte units (every ciphertext of a
     // batch allocation is 256-byte aligned); anything else takes the mma.sync kernels
