@@ -589,8 +589,19 @@ def main():
             if len(units) > 3:
                 fr = units[3] / sec
                 r["fp64"] = {"achieved": fr, "peak": float(fp[0]), "unit": "modmul/s", "frac": fr / float(fp[0]),
-                             "what": "epilogue FP64 modular products (recombination + window/GAP products)",
+                             "what": "epilogue FP64 modular products (window/GAP products; recombination is integer)",
                              "peak_source": "measured: FP64 fmulmod chain (he_microbench_fp64)"}
+            if len(units) > 4:
+                # B200: tcgen05.mma and the FP64 pipe share one issue resource (scripts/mb/mb_fp64_vs_mma.cu,
+                # profiles/r2_mb_fp64_vs_mma.txt): what binds the kernel is MMA time + FP64 time
+                sm_mhz = 1965.0
+                mma_s = units[4] / 148.0 / (sm_mhz * 1e6)
+                fp64_s = units[3] / float(fp[0])
+                r["shared_pipe"] = {"what": "tensor + FP64 pipe (one shared issue resource on B200): the launch's "
+                                            "tcgen05 MMAs at their standalone cost plus its FP64 modular products at "
+                                            "the standalone fmulmod rate, over the measured kernel time",
+                                    "mma_ms": mma_s * 1e3 / calls, "fp64_ms": fp64_s * 1e3 / calls,
+                                    "frac": (mma_s + fp64_s) / sec, "sm_mhz_assumed": sm_mhz}
         elif units[1] > 0:
             ach = units[1] / sec
             r["int"] = {"achieved": ach, "peak": peak_mm, "unit": "modmul/s", "frac": ach / peak_mm,
@@ -606,7 +617,7 @@ def main():
             "frac": dom["hbm"]["frac"], "traffic": traffic_all.get(dom_name), "peak_source": peak_kind,
             "calls": dom["calls"], "avg_ms": dom["avg_ms"],
             "algorithmic_bytes_per_launch": summ[dom_name][2][0] / summ[dom_name][0]}
-    for extra in ("tensor", "fp64"):
+    for extra in ("tensor", "fp64", "shared_pipe"):
         if extra in dom:
             roof[extra] = dom[extra]
     if bind == "int":

@@ -1643,10 +1643,19 @@ class GpuEngine:
         args = (self._h, _lib.addr(pin) if pin is not None else None, nci, p, H, W,
                 _lib.addr(pout) if pout is not None else None, M, int(bool(pool)), y0, y1, _lib.addr(wi),
                 _lib.addr(bres) if bres is not None else None, _lib.addr(cres) if cres is not None else None, limbs)
-        # FP64 modular products of the epilogue: one per recombined component and one per
-        # window / GAP product (2 + 3 for 2-component inputs, 3 + 6 for 3-component inputs)
-        fmul = 1.0 * (y1 - y0) * W * M * poly * (nci + nci * (nci + 1) // 2)
-        units = (in_b + out_b, 1.0 * nci * nnz * M * poly, i8, fmul)
+        # FP64 modular products of the epilogue: one per window / GAP product (3 for 2-component
+        # inputs, 6 for 3-component inputs; the recombination runs on the integer pipe)
+        fmul = 1.0 * (y1 - y0) * W * M * poly * (nci * (nci + 1) // 2)
+        # tensor-pipe cycles of the tcgen05 kernels at the measured standalone cost of their MMAs
+        # (tests/test_gpu_tc5.py: 47 cycles for N <= 32, 50 for N = 96, 64 for N = 128); the FP64
+        # pipe shares this resource (bench.py roofline.shared_pipe).  One work item = (limb,
+        # 8-coefficient chunk[, channel half]); 5 K steps per (16-pixel row step, component)
+        items = limbs * (self.N // 8)
+        if nci == 2:    # P1: N = 128
+            mma_cyc = 1.0 * items * (y1 - y0) * (W // 16) * nci * 5 * 64
+        else:           # P16: 5 byte planes x 5 K steps, the first of each plane zero-extended to N = 96
+            mma_cyc = 1.0 * items * ((M + 15) // 16) * (y1 - y0) * (W // 16) * nci * (5 * 50 + 20 * 47)
+        units = (in_b + out_b, 1.0 * nci * nnz * M * poly, i8, fmul, mma_cyc)
         if planar_in or planar_out is not None:
             rc = self._call("conv_sqsum", self._L.he_conv_square_sum_pl, *args,
                             inputs.data.data_ptr() if planar_in else None,
@@ -1697,9 +1706,9 @@ class GpuEngine:
     def planar_ok(self, p_in: int, H: int, W: int, q: int, q_next: int, level: int) -> bool:
         """Whether run_cnn's carry can go through the planar layout: conv1 on the
         tcgen05 P1 kernel (p_in <= 3, 16 output channels, W % 16 == 0, pooled) feeding
-        conv2 on the P16 kernel (16 input channels, 16-pixel rows), primes in [2^36, 2^40)."""
+        conv2 on the P16 kernel (16 input channels, 16-pixel rows), primes in (2^40 - 2^25, 2^40)."""
         return (self.use_tensor_cores and self.N == 1 << 16 and p_in <= 3 and q == 16 and W == 32 and H % 2 == 0
-                and q_next <= 32 and all((1 << 36) <= m < (1 << 40) for m in self.moduli[:level + 1]))
+                and q_next <= 32 and all((1 << 40) - (1 << 25) < m < (1 << 40) for m in self.moduli[:level + 1]))
 
     def unpack_planar(self, pc: PlanarCarry) -> list[CipherVec]:
         """The planar carry as channel-major 3-component ciphertexts (tests, tracing)."""
