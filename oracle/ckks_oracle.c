@@ -144,17 +144,21 @@ static int64_t sample_cbd(const oc_ctx *c, uint32_t dom, uint32_t obj, uint32_t 
     rnd4(c, dom, obj, 0, j, r);
     return (int64_t)__builtin_popcount(r[0] & 0x1FFFFFu) - (int64_t)__builtin_popcount(r[1] & 0x1FFFFFu);
 }
-static uint64_t sample_uniform(const oc_ctx *c, uint32_t dom, uint32_t obj, uint32_t limb, uint32_t j,
+/* Uniform residue k of (dom, obj, limb).  One Philox block serves the pair of indices that
+ * differ in bit 4: block index = k with bit 4 removed, words (r0, r1) for bit 4 clear, (r2, r3)
+ * for bit 4 set.  A 64-bit draw x is accepted when x < q floor(2^64 / q) and reduced mod q; a
+ * rejected draw is replaced by words (r0, r1) of block (k, limb, obj, dom + 16 t), t = 1, 2, ... */
+static uint64_t sample_uniform(const oc_ctx *c, uint32_t dom, uint32_t obj, uint32_t limb, uint32_t k,
                                uint64_t q) {
     uint32_t r[4];
-    rnd4(c, dom, obj, limb, j, r);
-    uint64_t lo = (uint64_t)r[0] | ((uint64_t)r[1] << 32);
-    uint64_t hi = (uint64_t)r[2] | ((uint64_t)r[3] << 32);
-    /* floor((hi*2^64 + lo) * q / 2^128) */
-    u128 ph = (u128)hi * q;
-    u128 pl = (u128)lo * q;
-    u128 mid = (u128)(uint64_t)ph + (pl >> 64);
-    return (uint64_t)(ph >> 64) + (uint64_t)(mid >> 64);
+    rnd4(c, dom, obj, limb, ((k >> 5) << 4) | (k & 15u), r);
+    uint64_t x = (k & 16u) ? ((uint64_t)r[2] | ((uint64_t)r[3] << 32)) : ((uint64_t)r[0] | ((uint64_t)r[1] << 32));
+    const uint64_t T = (uint64_t)((((u128)1 << 64) / q) * q);
+    for (uint32_t t = 1; x >= T; t++) {
+        rnd4(c, dom + 16u * t, obj, limb, k, r);
+        x = (uint64_t)r[0] | ((uint64_t)r[1] << 32);
+    }
+    return x % q;
 }
 /* secret coefficient j: dense ternary (r mod 3) - 1, or, for sk_hamming = h > 0,
  * nonzero with probability h / N (a second Philox draw below floor(h 2^32 / N))

@@ -122,11 +122,19 @@ class PyRef:
         return out
 
     def uniform(self, dom, obj, limb, q):
+        # one Philox block per pair of indices differing in bit 4; accept x < q*floor(2^64/q), else
+        # redraw from block (k, limb, obj, dom + 16 t); the value is x mod q (exactly uniform)
+        T = ((1 << 64) // q) * q
         out = []
-        for j in range(self.N):
-            r = self._rnd(dom, obj, limb, j)
-            R = r[0] | r[1] << 32 | r[2] << 64 | r[3] << 96
-            out.append(R * q >> 128)
+        for k in range(self.N):
+            r = self._rnd(dom, obj, limb, ((k >> 5) << 4) | (k & 15))
+            x = (r[2] | r[3] << 32) if k & 16 else (r[0] | r[1] << 32)
+            t = 0
+            while x >= T:
+                t += 1
+                r = self._rnd(dom + 16 * t, obj, limb, k)
+                x = r[0] | r[1] << 32
+            out.append(x % q)
         return out
 
     # -- transforms by definition

@@ -236,16 +236,35 @@ __device__ __forceinline__ int64_t sample_cbd(uint64_t seed, uint32_t dom, uint3
     rnd4(seed, dom, obj, 0, j, r);
     return (int64_t)__popc(r[0] & 0x1FFFFFu) - (int64_t)__popc(r[1] & 0x1FFFFFu);
 }
-__device__ __forceinline__ uint64_t sample_uniform(uint64_t seed, uint32_t dom, uint32_t obj, uint32_t limb,
-                                                   uint32_t j, uint64_t q) {
+// Uniform residues mod q.  One Philox block serves the PAIR of indices k0
+// (bit 4 clear) and k0 | 16: its counter index is k with bit 4 removed, words (r0, r1) are the
+// 64-bit draw of k0 and (r2, r3) that of k0 | 16.  A draw x is accepted when x < q floor(2^64 / q)
+// and reduced mod q (exactly uniform); a rejected draw (probability < q / 2^64) is replaced by
+// words (r0, r1) of block (k, limb, obj, dom + 16 t), t = 1, 2, ...
+__device__ __forceinline__ uint64_t uniform_accept(uint64_t x, uint64_t seed, uint32_t dom, uint32_t obj, uint32_t limb,
+                                                   uint32_t k, const ModConst &mc) {
+    const uint64_t T = mc.ratio * mc.q;  // ratio = floor((2^64 - 1) / q) = floor(2^64 / q) for odd q
+    uint32_t t = 0;
+    while (x >= T) {
+        uint32_t r[4];
+        rnd4(seed, dom + 16u * ++t, obj, limb, k, r);
+        x = (uint64_t)r[0] | ((uint64_t)r[1] << 32);
+    }
+    return reduce64(x, mc);
+}
+__device__ __forceinline__ void sample_uniform_pair(uint64_t seed, uint32_t dom, uint32_t obj, uint32_t limb, uint32_t k0,
+                                                    const ModConst &mc, uint64_t &a0, uint64_t &a1) {
     uint32_t r[4];
-    rnd4(seed, dom, obj, limb, j, r);
-    uint64_t lo = (uint64_t)r[0] | ((uint64_t)r[1] << 32);
-    uint64_t hi = (uint64_t)r[2] | ((uint64_t)r[3] << 32);
-    uint64_t ph_lo = hi * q, ph_hi = mulhi(hi, q);
-    uint64_t pl_hi = mulhi(lo, q);
-    uint64_t mid = ph_lo + pl_hi;
-    return ph_hi + (mid < ph_lo ? 1 : 0);
+    rnd4(seed, dom, obj, limb, ((k0 >> 5) << 4) | (k0 & 15u), r);
+    a0 = uniform_accept((uint64_t)r[0] | ((uint64_t)r[1] << 32), seed, dom, obj, limb, k0, mc);
+    a1 = uniform_accept((uint64_t)r[2] | ((uint64_t)r[3] << 32), seed, dom, obj, limb, k0 | 16u, mc);
+}
+__device__ __forceinline__ uint64_t sample_uniform(uint64_t seed, uint32_t dom, uint32_t obj, uint32_t limb,
+                                                   uint32_t k, const ModConst &mc) {
+    uint32_t r[4];
+    rnd4(seed, dom, obj, limb, ((k >> 5) << 4) | (k & 15u), r);
+    const uint64_t x = (k & 16u) ? (uint64_t)r[2] | ((uint64_t)r[3] << 32) : (uint64_t)r[0] | ((uint64_t)r[1] << 32);
+    return uniform_accept(x, seed, dom, obj, limb, k, mc);
 }
 
 // ---------------------------------------------------------------- host helpers (defined in context.cu)

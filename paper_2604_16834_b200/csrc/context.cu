@@ -219,7 +219,7 @@ __global__ void k_ksk_final(uint64_t *key, const uint64_t *err, const uint64_t *
     int j = (int)(idx / ((size_t)M * N));
     int m = (int)((idx / N) % M), k = (int)(idx % N);
     const ModConst c = mc[m];
-    uint64_t a = sample_uniform(seed, DOM_KSK_A, g * 64u + (uint32_t)j, (uint32_t)m, (uint32_t)k, c.q);
+    uint64_t a = sample_uniform(seed, DOM_KSK_A, g * 64u + (uint32_t)j, (uint32_t)m, (uint32_t)k, c);
     uint64_t s = sk[(size_t)m * N + k];
     uint64_t b = sub_mod(err[idx], mul_mod(a, s, c), c.q);
     bool in_digit = m < L && m >= j * alpha && m < (j + 1) * alpha;

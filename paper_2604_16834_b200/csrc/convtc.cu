@@ -545,7 +545,8 @@ struct P16Layout {
     static constexpr int STG = 2 * 8 * NCI * 16 * 64;  // cp.async staging: 2 half rows
     static constexpr int TB = 32 * 32;             // B tile (N = 32 rows x 32 bytes)
     static constexpr int TB0 = 96 * 32;            // zero-extended K step 0 (N = 96)
-    static constexpr int BBYTES = 6 * TB + TB0;
+    static constexpr int TBP = 48 * 32;            // tap 8 of planes d and d + 1 in one K step (N = 48)
+    static constexpr int BBYTES = 6 * TB + TB0 + TBP;
 };
 
 __device__ __forceinline__ void tr4b(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&o)[4]) {
@@ -762,12 +763,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
         {
             tc5::mbar_wait(&bar_b, 0);
             const uint32_t ring_s = tc5::smem_u32(ring), b_s = tc5::smem_u32(bsm);
-            const uint32_t idesc32 = tc5::idesc_u8s8(128, 32), idesc96 = tc5::idesc_u8s8(128, 96);
+            const uint32_t idesc32 = tc5::idesc_u8s8(128, 32), idesc96 = tc5::idesc_u8s8(128, 96),
+                           idesc48 = tc5::idesc_u8s8(128, 48);
             const uint32_t blbo = 32 * 16, blbo0 = 96 * 16;
-            const uint32_t ahi = tc5::sdesc_hi(PS), lps = tc5::sdesc_lbo(PS);
+            const uint32_t ahi = tc5::sdesc_hi(PS), lps = tc5::sdesc_lbo(PS), lpl = tc5::sdesc_lbo(128);
             uint64_t bd[7];
             for (int t = 0; t < 6; t++) bd[t] = tc5::sdesc(b_s + t * LY::TB, blbo, 128);
             bd[6] = tc5::sdesc(b_s + 6 * LY::TB, blbo0, 128);
+            const uint64_t bdp = tc5::sdesc(b_s + 6 * LY::TB + LY::TB0, 48 * 16, 128);
             int k = 0, S = 0;
             for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, k++) {
                 const int Gb = k * rows_in;
@@ -803,7 +806,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p16_gap(const TcArgs a) {
                             tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r1 + co + lps), bd[1], idesc32, true);
                             tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r2 + co + lps), bd[2], idesc32, true);
                             tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, a3 + co), b3, idesc32, true);
-                            tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r2 + co + 2 * (PS >> 4) + lps), bd[4], idesc32, true);
+                            // tap 8: planes (0, 1) and (2, 3) share one K step (the two K chunks are
+                            // the two planes, 128 bytes apart; N = 48 covers shift blocks d .. d + 2)
+                            if (d == 0 || d == 2)
+                                tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r2 + co + 2 * (PS >> 4) + lpl), bdp, idesc48, true);
+                            else if (d == 4)
+                                tc5::mma_i8_w(dcol, tc5::sdesc_hl(ahi, r2 + co + 2 * (PS >> 4) + lps), bd[4], idesc32, true);
                         }
                         tc5::tc_commit_w(&bar_dfull[Sc % NSL]);
                     }
@@ -1073,6 +1081,19 @@ static void build_btiles_p16(const int64_t *weights, int M, int p, std::vector<u
                 }
             }
         }
+    // pair tile: K chunk k = tap 8 of byte plane d + k; row n = b * 16 + m is shift block d + b,
+    // so chunk k holds digit b - k of the weight (zero outside 0..1)
+    for (int h = 0; h < 2; h++) {
+        uint8_t *tile = bt.data() + (size_t)h * BB + (size_t)6 * P16Layout::TB + P16Layout::TB0;
+        for (int k = 0; k < 2; k++)
+            for (int n = 0; n < 48; n++) {
+                const int e = n / 16 - k, m = h * 16 + n % 16;
+                if (m >= M || e < 0 || e > 1) continue;
+                for (int i = 0; i < p && i < 16; i++)
+                    tile[(size_t)k * 48 * 16 + (size_t)(n / 8) * 128 + (n % 8) * 16 + i] =
+                        (uint8_t)(int8_t)digit_s8(weights[(size_t)m * p * 9 + i * 9 + 8], e);
+            }
+    }
 }
 
 static int g_conv_tc = 1;  // he_set_conv_tc: 0 forces the mma.sync kernels (A/B tests)
@@ -1138,6 +1159,18 @@ static int convtc_launch(he_ctx *c, const uint64_t *const *in, int nci, int p, i
     if (wmax > cap || (p16 && E > 2)) {
         he_set_error("he_conv_square_sum_tc: weights need more than %d signed byte digits", p16 ? 2 : 3);
         return HE_EINVAL;
+    }
+    // worst-case shift sums: |C[s]| <= 255 * sum over the digits and the K = 9 p weights of one
+    // output channel of |digit|.  The epilogue combines C[s] + 2^8 C[s+1] in 32 bits and
+    // (C[4] + 2^8 C[5]) 2^32 in 64 (recombine_fold), which is exact below 2^22.5.
+    for (int m = 0; m < M; m++) {
+        int64_t dsum = 0;
+        for (int i = 0; i < p * 9; i++)
+            for (int e = 0; e < E; e++) dsum += std::abs(digit_s8(weights[(size_t)m * p * 9 + i], e));
+        if (255 * dsum >= 5931641) {  // 2^22.5
+            he_set_error("he_conv_square_sum_tc: weights of channel %d too heavy for the 32-bit shift sums", m);
+            return HE_EINVAL;
+        }
     }
     const int NSH = p16 ? 6 : NB + E - 1;
     std::vector<uint8_t> bt;

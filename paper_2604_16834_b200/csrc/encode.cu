@@ -261,7 +261,7 @@ __global__ void k_encrypt_finish(uint64_t *const *out, size_t count, int logN, i
         int l = (int)(r >> logN);
         uint32_t k = (uint32_t)(r & (N - 1));
         const ModConst m = mc[l];
-        uint64_t a = sample_uniform(seed, DOM_ENC_A, ct_index0 + (uint32_t)v, (uint32_t)l, k, m.q);
+        uint64_t a = sample_uniform(seed, DOM_ENC_A, ct_index0 + (uint32_t)v, (uint32_t)l, k, m);
         uint64_t *O = out[v];
         O[per + r] = a;
         O[r] = sub_mod(O[r], mul_mod(a, sk[r], m), m.q);

@@ -144,19 +144,24 @@ __global__ void __launch_bounds__(NTT_TPB) k_enc16_rows(uint64_t *const *out, in
     __syncwarp();
     const uint64_t *skl = sk + (size_t)l * NN + r * 256;
     const uint32_t obj = ct_index0 + (uint32_t)v;
-#pragma unroll 4
-    for (int j = 0; j < 16; j++) {
+#pragma unroll 2
+    for (int j = 0; j < 16; j += 2) {  // coefficients k and k + 16 share one Philox block
         const int cc = g + 16 * j;
         const uint32_t k = r * 256 + cc;
-        const uint64_t a = sample_uniform(seed, DOM_ENC_A, obj, (uint32_t)l, k, c.q);
-        const uint64_t sv = skl[cc];
-        uint64_t as;
-        if (c.q < FP_QMAX)
-            as = fcanon(fmulmod(u2d(a), u2d(sv), c.qd, c.qid), c.qd, c.qid);
-        else
-            as = mul_mod(a, sv, c);
-        c1[k] = a;
-        row[cc] = sub_mod(s[pad16(cc)], as, c.q);
+        uint64_t av[2];
+        sample_uniform_pair(seed, DOM_ENC_A, obj, (uint32_t)l, k, c, av[0], av[1]);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const uint64_t a = av[h];
+            const uint64_t sv = skl[cc + 16 * h];
+            uint64_t as;
+            if (c.q < FP_QMAX)
+                as = fcanon(fmulmod(u2d(a), u2d(sv), c.qd, c.qid), c.qd, c.qid);
+            else
+                as = mul_mod(a, sv, c);
+            c1[k + 16 * h] = a;
+            row[cc + 16 * h] = sub_mod(s[pad16(cc + 16 * h)], as, c.q);
+        }
     }
 }
 

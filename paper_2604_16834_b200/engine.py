@@ -1653,8 +1653,9 @@ class GpuEngine:
         items = limbs * (self.N // 8)
         if nci == 2:    # P1: N = 128
             mma_cyc = 1.0 * items * (y1 - y0) * (W // 16) * nci * 5 * 64
-        else:           # P16: 5 byte planes x 5 K steps, the first of each plane zero-extended to N = 96
-            mma_cyc = 1.0 * items * ((M + 15) // 16) * (y1 - y0) * (W // 16) * nci * (5 * 50 + 20 * 47)
+        else:           # P16: 5 byte planes x 4 K steps (the very first zero-extended to N = 96) + tap 8 of the
+            # plane pairs (0, 1), (2, 3) at N = 48 and of plane 4 at N = 32: 23 MMAs per (row step, component)
+            mma_cyc = 1.0 * items * ((M + 15) // 16) * (y1 - y0) * (W // 16) * nci * (50 + 20 * 47 + 2 * 48)
         units = (in_b + out_b, 1.0 * nci * nnz * M * poly, i8, fmul, mma_cyc)
         if planar_in or planar_out is not None:
             rc = self._call("conv_sqsum", self._L.he_conv_square_sum_pl, *args,
