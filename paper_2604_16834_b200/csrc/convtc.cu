@@ -171,8 +171,7 @@ __device__ __forceinline__ double recombine_fold(const int (&C)[NSH], int kq) {
     constexpr int64_t M40 = (1ll << 40) - 1;
     const int q0 = C[0] + C[1] * 256, q1 = C[2] + C[3] * 256;
     const int q2 = NSH > 5 ? C[4] + C[NSH > 5 ? 5 : 4] * 256 : C[4];
-    int64_t S = madw((int64_t)q0, q1, 1 << 16);
-    S += (int64_t)q2 << 32;
+    const int64_t S = (int64_t)q0 + ((int64_t)q1 << 16) + ((int64_t)q2 << 32);
     int hi = (int)(S >> 40);  // |hi| < 2^22.2
     if (NSH > 6) hi += C[NSH > 6 ? 6 : 4] * 256;  // |hi| < 2^30.2
     int64_t y = madw(S & M40, hi, kq);
@@ -476,6 +475,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                                 const double keep = mine + __shfl_xor_sync(0xffffffffu, give, 8);
                                 v[h][s2] = canon_fast(s2 == 0 ? keep + cstd : s2 == 1 ? 2.0 * keep : keep, c.qd, c.qid);
                             }
+                        PH(1);
                         const int H2 = a.H >> 1, W2 = W >> 1, y2 = (a.y0 >> 1) + pr, x2 = x >> 1;
                         uint8_t *pb = a.pl_out +
                                       ((((size_t)l * nchunk + (size_t)(item % nchunk)) * H2 + y2) * W2 + x2) * (3 * 5 * 128) +
@@ -492,6 +492,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_convtc_p1_pool(const TcArgs a) {
                                 *(unsigned short *)(pb + (s2 * 5 + d) * 128) = (unsigned short)u;
                             }
                         }
+                        PH(4);
                     } else
 #pragma unroll
                     for (int h = 0; h < 2; h++) {

@@ -36,6 +36,13 @@ if which.endswith("pl"):
     for _ in range(launches):
         _lib.check(f())
     torch.cuda.synchronize()
+    if os.environ.get("CONVTC_ROLES"):  # per-role / per-phase cycle counters of one more launch
+        _lib.check(L.he_convtc_profile(1, None))
+        _lib.check(f())
+        torch.cuda.synchronize()
+        r = np.zeros(7)
+        _lib.check(L.he_convtc_profile(0, r.ctypes.data))
+        print(which, "counters (M cycles per CTA):", [round(v / 148 / 1e6, 2) for v in r])
     print("ok", which)
     sys.exit(0)
 if which == "conv1":
