@@ -92,6 +92,49 @@ def test_convtc_gap_vs_oracle(small, H, rows, wbits, M):
         assert np.array_equal(to_np(o), r), k
 
 
+@pytest.mark.parametrize("shape", ["conv1", "conv2"])
+def test_convtc_extreme_values_vs_oracle(small, shape):
+    """The 32-/64-bit shift-sum bounds of the integer recombination: inputs whose residues are all
+    q - 1 or 2^40 - 2^32 - 1 patterns (every byte plane at or near 255) with the heaviest weights
+    the launcher accepts (same sign, every digit large), against the oracle chain; heavier weights
+    are refused (HE_EINVAL, nothing enqueued) so the caller falls back to the mma.sync kernels."""
+    eng, orc = small
+    ell = 3
+    mods = eng.moduli[:ell]
+    if shape == "conv1":
+        nci, p, H, W, M, pool, rows = 2, 3, 2, 16, 16, 1, (0, 2)
+        heavy = (127 << 16) + (127 << 8) + 127       # three digits of 127: 255 * 27 * 381 < 2^22.5
+        too_heavy = None                              # 27 taps cannot exceed the bound with three digits
+    else:
+        nci, p, H, W, M, pool, rows = 3, 16, 2, 16, 32, 0, (0, 2)
+        heavy = (30 << 8) + 127                       # 255 * 144 * 157 = 5.77e6 < 2^22.5 = 5.93e6
+        too_heavy = (127 << 8) + 127
+    n_in = p * H * W
+    x = np.empty((n_in, nci, ell, eng.N), np.uint64)
+    for l, q in enumerate(mods):
+        x[:, :, l, 0::2] = q - 1
+        x[:, :, l, 1::2] = (1 << 40) - (1 << 32) - 1 if (1 << 40) - (1 << 32) - 1 < q else q - 2
+    ins = [from_np(x[i], eng.device) for i in range(n_in)]
+    wi = np.full((M, 9 * p), heavy, np.int64)
+    wi[1::2] *= -1
+    bres = np.array([[q - 1 for q in mods] for _ in range(M)], np.uint64)
+    cst = np.array([q - 1 for q in mods], np.uint64)
+    y0, y1 = rows
+    got = _run(eng, eng._L.he_conv_square_sum_tc, ins, nci, p, H, W, M, pool, y0, y1, wi, bres, cst, ell)
+    ref = _oracle_conv_square_sum(orc, [x[i] for i in range(n_in)], p, H, W, wi, bres, cst, pool, y0, y1)
+    for k, (o, r) in enumerate(zip(got, ref)):
+        assert np.array_equal(to_np(o), r), k
+    if too_heavy is not None:
+        import torch
+
+        w2 = np.full((M, 9 * p), too_heavy, np.int64)
+        outs = [torch.zeros((2 * nci - 1, ell, eng.N), dtype=torch.int64, device=eng.device) for _ in range(M)]
+        pi, po = _ptrs(ins), _ptrs(outs)
+        rc = eng._L.he_conv_square_sum_tc(eng._h, pi.ctypes.data, nci, p, H, W, po.ctypes.data, M, pool, y0, y1,
+                                          w2.ctypes.data, None, None, ell, None)
+        assert rc != 0 and b"too heavy" in eng._L.he_last_error()
+
+
 def _rand_dev(eng, count, nci, ell, seed):
     import torch
 
