@@ -23,10 +23,15 @@
 //     goes into N: B[(i,d)][(s,m)] = digit_{s-d}(w[m][i][tap]), so one MMA
 //     (N = NSH x 16) produces every shift sum C[s] of all 16 output channels.
 //   * Warp roles: warps 0-15 epilogue (four per TMEM lane quarter, 4 channels
-//     each: tcgen05.ld -> exact recombination -> FP64 products -> window sums
-//     -> stores; the FP64 work is latency-bound, so it gets the warps), warps
-//     16-18 producers (128-bit global loads -> PRMT byte packing -> shared
-//     ring), warp 19 TMEM allocator + MMA issuer.  mbarriers
+//     each: tcgen05.ld -> exact recombination on the integer pipe -> FP64
+//     window products -> window sums -> stores), warps 16-18 producers (128-bit
+//     global loads -> PRMT byte packing -> shared ring), warp 19 TMEM allocator
+//     + MMA issuer.  After the role split the epilogue warpgroups raise their
+//     register limit and the producer / MMA warpgroup lowers its own
+//     (setmaxnreg, RegSplit).  On B200 the FP64 pipe and the tensor core share
+//     one issue resource (scripts/mb/mb_fp64_vs_mma.cu), so what bounds these
+//     kernels is MMA cycles + FP64 cycles: FP64 work is kept to the window
+//     products (recombine_fold does the rest in integers).  mbarriers
 //     connect them: ring row full (producers -> MMA), ring row empty
 //     (tcgen05.commit -> producers), TMEM slot full (commit -> epilogue), TMEM
 //     slot empty (epilogue -> MMA).  Four TMEM slots of 128 columns (one per
